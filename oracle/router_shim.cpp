@@ -1,0 +1,107 @@
+// TEST INFRASTRUCTURE ONLY — extern "C" shim over the UNMODIFIED reference
+// router (P/src/wiring.cpp) and rebalancer (P/src/rebalancer.cpp), so tests can
+// check that the B200 build's host router makes pick-for-pick identical
+// decisions on the same call sequence.
+#include <cstdint>
+#include <set>
+
+#include "swarmsim/errors.hpp"
+#include "swarmsim/rebalancer.hpp"
+#include "swarmsim/wiring.hpp"
+
+using namespace swarmsim;
+
+extern "C" {
+
+void* ref_router_new(size_t n_stages, double gamma, double epsilon) {
+    try {
+        return new wiring::RoutingState(n_stages, gamma, epsilon);
+    } catch (...) {
+        return nullptr;
+    }
+}
+
+void ref_router_free(void* r) { delete static_cast<wiring::RoutingState*>(r); }
+
+int ref_router_add_server(void* r, uint64_t peer, const size_t* stages, size_t n, double phase) {
+    try {
+        std::set<size_t> s(stages, stages + n);
+        static_cast<wiring::RoutingState*>(r)->add_server(PeerId{peer}, s, phase);
+        return 0;
+    } catch (const ConfigError&) {
+        return 1;
+    } catch (...) {
+        return 3;
+    }
+}
+
+int ref_router_ban_server(void* r, uint64_t peer) {
+    try {
+        static_cast<wiring::RoutingState*>(r)->ban_server(PeerId{peer});
+        return 0;
+    } catch (const ConfigError&) {
+        return 1;
+    }
+}
+
+void ref_router_remove_server(void* r, uint64_t peer) {
+    static_cast<wiring::RoutingState*>(r)->remove_server(PeerId{peer});
+}
+
+// 0 ok (peer in *out), 1 ConfigError, 2 NoPeerAvailable
+int ref_router_choose_server(void* r, size_t stage, uint64_t* out) {
+    try {
+        *out = static_cast<wiring::RoutingState*>(r)->choose_server(stage).value;
+        return 0;
+    } catch (const ConfigError&) {
+        return 1;
+    } catch (const NoPeerAvailable&) {
+        return 2;
+    }
+}
+
+int ref_router_record_response(void* r, uint64_t peer, double elapsed) {
+    try {
+        static_cast<wiring::RoutingState*>(r)->record_response(PeerId{peer}, elapsed);
+        return 0;
+    } catch (const ConfigError&) {
+        return 1;
+    }
+}
+
+double ref_router_ema_of(void* r, uint64_t peer) {
+    return static_cast<wiring::RoutingState*>(r)->ema_of(PeerId{peer});
+}
+
+double ref_router_priority_of(void* r, uint64_t peer) {
+    return static_cast<wiring::RoutingState*>(r)->priority_of(PeerId{peer});
+}
+
+// Table in CSR form: stage s owns members [offsets[s], offsets[s+1]).
+// Returns 0 and fills mover (or -1 as UINT64_MAX), from, to.
+int ref_rebalance_decide(size_t n_stages, const size_t* offsets, const uint64_t* peers,
+                         const double* queues, uint64_t* mover, size_t* from_stage,
+                         size_t* to_stage, size_t* ops) {
+    try {
+        rebalancer::StageLoadTable t;
+        t.loads.assign(n_stages, 0.0);
+        t.members.resize(n_stages);
+        for (size_t s = 0; s < n_stages; ++s) {
+            for (size_t i = offsets[s]; i < offsets[s + 1]; ++i) {
+                t.members[s][PeerId{peers[i]}] = queues[i];
+                t.loads[s] += queues[i];
+            }
+        }
+        size_t n_ops = 0;
+        const auto d = rebalancer::decide(t, &n_ops);
+        *mover = d.mover ? d.mover->value : UINT64_MAX;
+        *from_stage = d.from_stage;
+        *to_stage = d.to_stage;
+        if (ops) *ops = n_ops;
+        return 0;
+    } catch (const ConfigError&) {
+        return 1;
+    }
+}
+
+}  // extern "C"

@@ -1,0 +1,79 @@
+"""ctypes binding of include/swarm_b200.h (libswarm_b200.so).
+
+This is the reference-side binding a Python maintainer would add for the
+C-ABI.  Loading fails loudly when the library was not
+built: there is no CPU fallback anywhere in this package.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libswarm_b200.so")
+
+SWARM_OK, SWARM_E_INVALID, SWARM_E_NONFINITE, SWARM_E_CUDA, SWARM_E_UNSUPPORTED = 0, 1, 2, 3, 4
+DT_F32, DT_BF16, DT_F64 = 0, 1, 2
+FLAG_NONFINITE = 1
+EPI_STORE_BF16, EPI_STORE_F32, EPI_ACCUM_F32, EPI_RESIDUAL, EPI_GELU, EPI_DGELU = range(6)
+
+
+class GemmArgs(C.Structure):
+    _fields_ = [(n, C.c_int) for n in ("m", "n", "k", "batch", "bh")] + [
+        ("a", C.c_void_p), ("lda", C.c_int), ("a_mn_major", C.c_int), ("a_rows", C.c_int), ("a_cols", C.c_int),
+        ("ra0", C.c_int), ("ra1", C.c_int), ("ca0", C.c_int), ("ca1", C.c_int),
+        ("b", C.c_void_p), ("ldb", C.c_int), ("b_mn_major", C.c_int), ("b_rows", C.c_int), ("b_cols", C.c_int),
+        ("rb0", C.c_int), ("rb1", C.c_int), ("cb0", C.c_int), ("cb1", C.c_int),
+        ("d", C.c_void_p), ("ldd", C.c_int), ("rd0", C.c_int), ("rd1", C.c_int), ("cd0", C.c_int), ("cd1", C.c_int),
+        ("aux", C.c_void_p), ("alpha", C.c_float), ("epilogue", C.c_int)]
+
+
+# (name, restype, argtypes) for every symbol include/swarm_b200.h declares
+P, SZ, I, U32P, U8P, F, D = C.c_void_p, C.c_size_t, C.c_int, C.c_void_p, C.c_void_p, C.c_float, C.c_double
+SIGNATURES = {
+    "swarm_last_error": (C.c_char_p, []),
+    "swarm_version": (I, []),
+    "swarm_launch_count": (C.c_uint64, []),
+    "swarm_quantize_blockwise": (I, [P, I, SZ, SZ, P, P, U32P, P]),
+    "swarm_dequantize_blockwise": (I, [P, P, I, SZ, SZ, P, I, P]),
+    "swarm_quantize_blockwise_host": (I, [P, I, SZ, SZ, P, P]),
+    "swarm_dequantize_blockwise_host": (I, [P, P, I, SZ, SZ, P, I]),
+    "swarm_maxout_forward": (I, [P, I, SZ, SZ, P, U8P, P]),
+    "swarm_maxout_backward": (I, [P, I, U8P, SZ, SZ, P, P]),
+    "swarm_layer_norm_forward": (I, [P, I, SZ, SZ, P, P, D, P, P, P, P]),
+    "swarm_layer_norm_backward_workspace": (SZ, [SZ, SZ]),
+    "swarm_layer_norm_backward": (I, [P, P, I, SZ, SZ, P, P, P, P, P, P, P, P]),
+    "swarm_matvec_f64": (I, [P, SZ, P, SZ, P, P]),
+    "swarm_gemm_bf16": (I, [C.POINTER(GemmArgs), P]),
+}
+
+_lib = None
+
+
+def lib() -> C.CDLL:
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} is not built; run `python -c 'import __graft_entry__ as g; g.build()'` "
+                              "(there is no CPU fallback)")
+        L = C.CDLL(LIB_PATH)
+        for name, (res, args) in SIGNATURES.items():
+            fn = getattr(L, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = L
+    return _lib
+
+
+def last_error() -> str:
+    return lib().swarm_last_error().decode(errors="replace")
+
+
+def check(rc: int, what: str) -> None:
+    if rc == SWARM_OK:
+        return
+    from ._swarmsim_b200 import ConfigError  # noqa: WPS433 — the reference's exception type
+    msg = f"{what}: {last_error()}"
+    if rc in (SWARM_E_INVALID, SWARM_E_NONFINITE):
+        raise ConfigError(msg)
+    raise RuntimeError(msg)

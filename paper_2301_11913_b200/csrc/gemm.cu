@@ -1,0 +1,477 @@
+// K5: persistent, warp-specialised tcgen05 bf16 GEMM for sm_100a.
+//
+// Every dense contraction of the transformer block (QKV, O, FFN1, FFN2 and
+// their dgrad/wgrad; attention S = QK^T, O = PV and their backward) goes
+// through this kernel.  The reference only counts these FLOPs
+// (/root/reference/proj/src/cost_model.cpp:31-42); it never executes them.
+//
+// Structure (one CTA per SM, 256 threads):
+//   warp 0  TMA producer: 128x64 A tile + BNx64 B tile per stage, SWIZZLE_128B,
+//           STAGES-deep smem ring guarded by full/empty mbarriers;
+//   warp 1  MMA issuer: one elected thread issues tcgen05.mma (M=128, N=BN, K=16)
+//           into a double-buffered fp32 accumulator in TMEM (2 x BN columns),
+//           tcgen05.commit frees smem slots and signals the epilogue;
+//   warp 2  TMEM allocator;
+//   warps 4-7 epilogue: tcgen05.ld (32 lanes x 32 columns) -> fused op (scale,
+//           residual add, GeLU / GeLU', fp32 accumulate) -> global stores, then
+//           release the TMEM buffer so the next tile's MMAs overlap this drain.
+// Operands may be K-major or MN-major (transposed) on either side, so dgrad and
+// wgrad read activations/weights in place with no transpose pass.
+#include <cudaTypedefs.h>
+
+#include <algorithm>
+#include <mutex>
+
+#include "common.cuh"
+#include "sm100.cuh"
+
+namespace swarm {
+namespace gemm {
+
+using namespace swarm::sm100;
+
+constexpr int BM = 128;
+constexpr int BK = 64;
+constexpr int kThreads = 256;
+
+struct Params {
+    int m, n, k, bh;
+    int tiles_m, tiles_n, tiles_per_batch, total_tiles, k_blocks;
+    int ra0, ra1, ca0, ca1, rb0, rb1, cb0, cb1;
+    void* d;
+    long long ldd;
+    int rd0, rd1, cd0, cd1;
+    const void* aux;
+    float alpha;
+    int epi;
+    int vec_ok;
+};
+
+template <int BN>
+struct Cfg {
+    static constexpr int A_BYTES = BM * BK * 2;
+    static constexpr int B_BYTES = BN * BK * 2;
+    static constexpr int STAGES = BN == 256 ? 4 : 6;
+    static constexpr int TMEM_COLS = 2 * BN;
+    static constexpr int SMEM = STAGES * (A_BYTES + B_BYTES) + 1024 + 256;
+};
+
+__device__ __forceinline__ float gelu_f(float x) {
+    const float k0 = 0.7978845608028654f, k1 = 0.044715f;
+    return 0.5f * x * (1.f + tanhf(k0 * (x + k1 * x * x * x)));
+}
+__device__ __forceinline__ float dgelu_f(float x) {
+    const float k0 = 0.7978845608028654f, k1 = 0.044715f;
+    const float t = tanhf(k0 * (x + k1 * x * x * x));
+    return 0.5f * (1.f + t) + 0.5f * x * (1.f - t * t) * k0 * (1.f + 3.f * k1 * x * x);
+}
+
+__device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
+    const __nv_bfloat162 p = __floats2bfloat162_rn(a, b);
+    return *reinterpret_cast<const uint32_t*>(&p);
+}
+__device__ __forceinline__ float bf_lo(uint32_t w) { return __uint_as_float(w << 16); }
+__device__ __forceinline__ float bf_hi(uint32_t w) { return __uint_as_float(w & 0xffff0000u); }
+
+// Apply the fused epilogue to 32 consecutive columns [col0, col0+32) of one row.
+__device__ __forceinline__ void epilogue_chunk(const Params& p, float (&v)[32], long long off, int ncols_valid) {
+    const bool full = p.vec_ok && ncols_valid >= 32;
+    switch (p.epi) {
+        case SWARM_EPI_STORE_BF16:
+        case SWARM_EPI_RESIDUAL: {
+            __nv_bfloat16* dst = static_cast<__nv_bfloat16*>(p.d) + off;
+            if (p.epi == SWARM_EPI_RESIDUAL) {
+                const __nv_bfloat16* r = static_cast<const __nv_bfloat16*>(p.aux) + off;
+                if (full) {
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        const uint4 w = reinterpret_cast<const uint4*>(r)[q];
+                        const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+                        for (int j = 0; j < 4; ++j) {
+                            v[q * 8 + 2 * j] += bf_lo(ws[j]);
+                            v[q * 8 + 2 * j + 1] += bf_hi(ws[j]);
+                        }
+                    }
+                } else {
+                    for (int j = 0; j < ncols_valid; ++j) v[j] += __bfloat162float(r[j]);
+                }
+            }
+            if (full) {
+#pragma unroll
+                for (int q = 0; q < 4; ++q)
+                    reinterpret_cast<uint4*>(dst)[q] =
+                        make_uint4(pack_bf16(v[q * 8 + 0], v[q * 8 + 1]), pack_bf16(v[q * 8 + 2], v[q * 8 + 3]),
+                                   pack_bf16(v[q * 8 + 4], v[q * 8 + 5]), pack_bf16(v[q * 8 + 6], v[q * 8 + 7]));
+            } else {
+                for (int j = 0; j < ncols_valid; ++j) dst[j] = __float2bfloat16_rn(v[j]);
+            }
+            break;
+        }
+        case SWARM_EPI_STORE_F32:
+        case SWARM_EPI_ACCUM_F32: {
+            float* dst = static_cast<float*>(p.d) + off;
+            if (full) {
+#pragma unroll
+                for (int q = 0; q < 8; ++q) {
+                    float4 o = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+                    if (p.epi == SWARM_EPI_ACCUM_F32) {
+                        const float4 c = reinterpret_cast<const float4*>(dst)[q];
+                        o.x += c.x;
+                        o.y += c.y;
+                        o.z += c.z;
+                        o.w += c.w;
+                    }
+                    reinterpret_cast<float4*>(dst)[q] = o;
+                }
+            } else {
+                for (int j = 0; j < ncols_valid; ++j)
+                    dst[j] = (p.epi == SWARM_EPI_ACCUM_F32) ? dst[j] + v[j] : v[j];
+            }
+            break;
+        }
+        case SWARM_EPI_GELU: {
+            __nv_bfloat16* dst = static_cast<__nv_bfloat16*>(p.d) + off;
+            __nv_bfloat16* u = const_cast<__nv_bfloat16*>(static_cast<const __nv_bfloat16*>(p.aux)) + off;
+            if (full) {
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    reinterpret_cast<uint4*>(u)[q] =
+                        make_uint4(pack_bf16(v[q * 8 + 0], v[q * 8 + 1]), pack_bf16(v[q * 8 + 2], v[q * 8 + 3]),
+                                   pack_bf16(v[q * 8 + 4], v[q * 8 + 5]), pack_bf16(v[q * 8 + 6], v[q * 8 + 7]));
+                }
+#pragma unroll
+                for (int j = 0; j < 32; ++j) v[j] = gelu_f(v[j]);
+#pragma unroll
+                for (int q = 0; q < 4; ++q)
+                    reinterpret_cast<uint4*>(dst)[q] =
+                        make_uint4(pack_bf16(v[q * 8 + 0], v[q * 8 + 1]), pack_bf16(v[q * 8 + 2], v[q * 8 + 3]),
+                                   pack_bf16(v[q * 8 + 4], v[q * 8 + 5]), pack_bf16(v[q * 8 + 6], v[q * 8 + 7]));
+            } else {
+                for (int j = 0; j < ncols_valid; ++j) {
+                    u[j] = __float2bfloat16_rn(v[j]);
+                    dst[j] = __float2bfloat16_rn(gelu_f(v[j]));
+                }
+            }
+            break;
+        }
+        case SWARM_EPI_DGELU: {
+            __nv_bfloat16* dst = static_cast<__nv_bfloat16*>(p.d) + off;
+            const __nv_bfloat16* u = static_cast<const __nv_bfloat16*>(p.aux) + off;
+            if (full) {
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    const uint4 w = reinterpret_cast<const uint4*>(u)[q];
+                    const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) {
+                        v[q * 8 + 2 * j] *= dgelu_f(bf_lo(ws[j]));
+                        v[q * 8 + 2 * j + 1] *= dgelu_f(bf_hi(ws[j]));
+                    }
+                }
+#pragma unroll
+                for (int q = 0; q < 4; ++q)
+                    reinterpret_cast<uint4*>(dst)[q] =
+                        make_uint4(pack_bf16(v[q * 8 + 0], v[q * 8 + 1]), pack_bf16(v[q * 8 + 2], v[q * 8 + 3]),
+                                   pack_bf16(v[q * 8 + 4], v[q * 8 + 5]), pack_bf16(v[q * 8 + 6], v[q * 8 + 7]));
+            } else {
+                for (int j = 0; j < ncols_valid; ++j)
+                    dst[j] = __float2bfloat16_rn(v[j] * dgelu_f(__bfloat162float(u[j])));
+            }
+            break;
+        }
+        default: break;
+    }
+}
+
+template <int BN, bool A_MN, bool B_MN>
+__global__ void __launch_bounds__(kThreads, 1)
+    k_gemm(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUtensorMap tma_b, const Params p) {
+    using C = Cfg<BN>;
+    extern __shared__ uint8_t smem_raw[];
+    const uint32_t raw = smem_u32(smem_raw);
+    uint8_t* smem = smem_raw + ((1024 - (raw & 1023)) & 1023);
+    uint8_t* sa = smem;
+    uint8_t* sb = smem + C::STAGES * C::A_BYTES;
+    uint64_t* full = reinterpret_cast<uint64_t*>(sb + C::STAGES * C::B_BYTES);
+    uint64_t* empty = full + C::STAGES;
+    uint64_t* tfull = empty + C::STAGES;
+    uint64_t* tempty = tfull + 2;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+    const int warp = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
+
+    if (warp == 0 && lane == 0) {
+        tma_prefetch(&tma_a);
+        tma_prefetch(&tma_b);
+        for (int s = 0; s < C::STAGES; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], 1);
+        }
+        for (int s = 0; s < 2; ++s) {
+            mbar_init(&tfull[s], 1);
+            mbar_init(&tempty[s], 4);
+        }
+        fence_barrier_init();
+    }
+    if (warp == 2) {
+        tmem_alloc(tmem_slot, C::TMEM_COLS);
+        tmem_relinquish();
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+
+    if (warp == 0) {
+        if (lane == 0) {
+            // ------------------------------------------------ TMA producer
+            int stage = 0;
+            uint32_t phase = 0;
+            for (int t = blockIdx.x; t < p.total_tiles; t += gridDim.x) {
+                const int z = t / p.tiles_per_batch;
+                const int r = t - z * p.tiles_per_batch;
+                const int mt = r % p.tiles_m, nt = r / p.tiles_m;
+                const int zb = z / p.bh, zh = z - zb * p.bh;
+                const int ra = p.ra0 * zb + p.ra1 * zh, ca = p.ca0 * zb + p.ca1 * zh;
+                const int rb = p.rb0 * zb + p.rb1 * zh, cb = p.cb0 * zb + p.cb1 * zh;
+                for (int kb = 0; kb < p.k_blocks; ++kb) {
+                    mbar_wait(&empty[stage], phase ^ 1);
+                    mbar_arrive_expect_tx(&full[stage], C::A_BYTES + C::B_BYTES);
+                    uint8_t* a_dst = sa + stage * C::A_BYTES;
+                    uint8_t* b_dst = sb + stage * C::B_BYTES;
+                    if constexpr (!A_MN) {
+                        tma_load_2d(a_dst, &tma_a, &full[stage], ca + kb * BK, ra + mt * BM);
+                    } else {
+#pragma unroll
+                        for (int j = 0; j < BM / 64; ++j)
+                            tma_load_2d(a_dst + j * (64 * BK * 2), &tma_a, &full[stage], ca + mt * BM + j * 64,
+                                        ra + kb * BK);
+                    }
+                    if constexpr (!B_MN) {
+                        tma_load_2d(b_dst, &tma_b, &full[stage], cb + kb * BK, rb + nt * BN);
+                    } else {
+#pragma unroll
+                        for (int j = 0; j < BN / 64; ++j)
+                            tma_load_2d(b_dst + j * (64 * BK * 2), &tma_b, &full[stage], cb + nt * BN + j * 64,
+                                        rb + kb * BK);
+                    }
+                    if (++stage == C::STAGES) {
+                        stage = 0;
+                        phase ^= 1;
+                    }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {
+            // ------------------------------------------------ MMA issuer
+            constexpr uint32_t idesc = make_idesc_bf16(BM, BN, A_MN, B_MN);
+            int stage = 0;
+            uint32_t phase = 0;
+            int acc = 0;
+            uint32_t acc_phase = 0;
+            for (int t = blockIdx.x; t < p.total_tiles; t += gridDim.x) {
+                mbar_wait(&tempty[acc], acc_phase ^ 1);
+                tc_fence_after();
+                const uint32_t d_tmem = tmem_base + static_cast<uint32_t>(acc * BN);
+                for (int kb = 0; kb < p.k_blocks; ++kb) {
+                    mbar_wait(&full[stage], phase);
+                    tc_fence_after();
+                    const uint32_t a_base = smem_u32(sa + stage * C::A_BYTES);
+                    const uint32_t b_base = smem_u32(sb + stage * C::B_BYTES);
+#pragma unroll
+                    for (int k = 0; k < BK / 16; ++k) {
+                        const uint64_t ad = A_MN ? make_sdesc(a_base + k * 2048, 64 * BK * 2, 1024)
+                                                 : make_sdesc(a_base + k * 32, 16, 1024);
+                        const uint64_t bd = B_MN ? make_sdesc(b_base + k * 2048, 64 * BK * 2, 1024)
+                                                 : make_sdesc(b_base + k * 32, 16, 1024);
+                        mma_bf16(d_tmem, ad, bd, idesc, (kb | k) != 0 ? 1u : 0u);
+                    }
+                    mma_commit(&empty[stage]);
+                    if (++stage == C::STAGES) {
+                        stage = 0;
+                        phase ^= 1;
+                    }
+                }
+                mma_commit(&tfull[acc]);
+                acc ^= 1;
+                if (acc == 0) acc_phase ^= 1;
+            }
+        }
+    } else if (warp >= 4) {
+        // ------------------------------------------------ epilogue (TMEM -> HBM)
+        const int q = warp - 4;  // TMEM lane quarter owned by this warp (warp % 4)
+        int acc = 0;
+        uint32_t acc_phase = 0;
+        for (int t = blockIdx.x; t < p.total_tiles; t += gridDim.x) {
+            const int z = t / p.tiles_per_batch;
+            const int r = t - z * p.tiles_per_batch;
+            const int mt = r % p.tiles_m, nt = r / p.tiles_m;
+            const int zb = z / p.bh, zh = z - zb * p.bh;
+            const long long rd = p.rd0 * zb + p.rd1 * zh, cd = p.cd0 * zb + p.cd1 * zh;
+            const int row = mt * BM + q * 32 + lane;
+            mbar_wait(&tfull[acc], acc_phase);
+            tc_fence_after();
+#pragma unroll 1
+            for (int c = 0; c < BN / 32; ++c) {
+                uint32_t rr[32];
+                tmem_ld_32x32b_x32(tmem_base + (static_cast<uint32_t>(q * 32) << 16) +
+                                       static_cast<uint32_t>(acc * BN + c * 32),
+                                   rr);
+                tmem_ld_wait();
+                const int col0 = nt * BN + c * 32;
+                if (row < p.m && col0 < p.n) {
+                    float v[32];
+#pragma unroll
+                    for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(rr[j]) * p.alpha;
+                    const long long off = (rd + row) * p.ldd + cd + col0;
+                    epilogue_chunk(p, v, off, min(32, p.n - col0));
+                }
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&tempty[acc]);
+            acc ^= 1;
+            if (acc == 0) acc_phase ^= 1;
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 2) {
+        tc_fence_after();
+        tmem_dealloc(tmem_base, C::TMEM_COLS);
+    }
+}
+
+// ---------------------------------------------------------------- host side
+using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                              const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                              CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeFn get_encode() {
+    static EncodeFn fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void* ptr = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<EncodeFn>(ptr);
+    });
+    return fn;
+}
+
+int encode_2d(CUtensorMap* m, const void* ptr, long long rows, long long cols, long long ld, int box_inner,
+              int box_outer) {
+    EncodeFn enc = get_encode();
+    if (!enc) {
+        set_error("gemm: cuTensorMapEncodeTiled unavailable");
+        return SWARM_E_CUDA;
+    }
+    const cuuint64_t dims[2] = {static_cast<cuuint64_t>(cols), static_cast<cuuint64_t>(rows)};
+    const cuuint64_t strides[1] = {static_cast<cuuint64_t>(ld) * 2};
+    const cuuint32_t box[2] = {static_cast<cuuint32_t>(box_inner), static_cast<cuuint32_t>(box_outer)};
+    const cuuint32_t estr[2] = {1, 1};
+    const CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims, strides, box, estr,
+                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) {
+        set_error("gemm: cuTensorMapEncodeTiled failed (" + std::to_string(static_cast<int>(r)) + ")");
+        return SWARM_E_INVALID;
+    }
+    return SWARM_OK;
+}
+
+int num_sms() {
+    static int n = 0;
+    if (n == 0) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+        if (n <= 0) n = kNumSMs;
+    }
+    return n;
+}
+
+template <int BN, bool A_MN, bool B_MN>
+int launch(const CUtensorMap& ta, const CUtensorMap& tb, const Params& p, cudaStream_t st) {
+    auto kern = k_gemm<BN, A_MN, B_MN>;
+    static bool attr = false;
+    if (!attr) {
+        SWARM_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg<BN>::SMEM));
+        attr = true;
+    }
+    const int grid = std::min(p.total_tiles, num_sms());
+    kern<<<grid, kThreads, Cfg<BN>::SMEM, st>>>(ta, tb, p);
+    SWARM_LAUNCH_CHECK("k_gemm");
+    return SWARM_OK;
+}
+
+template <int BN>
+int dispatch(bool amn, bool bmn, const CUtensorMap& ta, const CUtensorMap& tb, const Params& p, cudaStream_t st) {
+    if (!amn && !bmn) return launch<BN, false, false>(ta, tb, p, st);
+    if (!amn && bmn) return launch<BN, false, true>(ta, tb, p, st);
+    if (amn && !bmn) return launch<BN, true, false>(ta, tb, p, st);
+    return launch<BN, true, true>(ta, tb, p, st);
+}
+
+}  // namespace gemm
+}  // namespace swarm
+
+extern "C" int swarm_gemm_bf16(const swarm_gemm_args* a, swarm_stream_t stream) {
+    using namespace swarm;
+    using namespace swarm::gemm;
+    if (!a) return invalid("gemm: null args");
+    if (a->m <= 0 || a->n <= 0 || a->k <= 0 || a->batch <= 0 || a->bh <= 0) return invalid("gemm: bad shape");
+    if (!a->a || !a->b || !a->d) return invalid("gemm: null operand");
+    if ((a->epilogue == SWARM_EPI_RESIDUAL || a->epilogue == SWARM_EPI_GELU || a->epilogue == SWARM_EPI_DGELU) &&
+        !a->aux)
+        return invalid("gemm: epilogue needs aux");
+    if (a->epilogue < 0 || a->epilogue > SWARM_EPI_DGELU) return invalid("gemm: bad epilogue");
+    if (a->lda % 8 || a->ldb % 8 || (reinterpret_cast<uintptr_t>(a->a) & 15) || (reinterpret_cast<uintptr_t>(a->b) & 15))
+        return invalid("gemm: A/B rows must be 16-byte aligned");
+    // storage extents
+    long long ar = a->a_rows, ac = a->a_cols, br = a->b_rows, bc = a->b_cols;
+    if (ar == 0 || ac == 0) {
+        ar = a->a_mn_major ? a->k : a->m;
+        ac = a->a_mn_major ? a->m : a->k;
+    }
+    if (br == 0 || bc == 0) {
+        br = a->b_mn_major ? a->k : a->n;
+        bc = a->b_mn_major ? a->n : a->k;
+    }
+    const int BN = a->n <= 128 ? 128 : 256;
+    CUtensorMap ta, tb;
+    int rc = encode_2d(&ta, a->a, ar, ac, a->lda, 64, a->a_mn_major ? BK : BM);
+    if (rc) return rc;
+    rc = encode_2d(&tb, a->b, br, bc, a->ldb, 64, a->b_mn_major ? BK : BN);
+    if (rc) return rc;
+    Params p{};
+    p.m = a->m;
+    p.n = a->n;
+    p.k = a->k;
+    p.bh = a->bh;
+    p.tiles_m = (a->m + BM - 1) / BM;
+    p.tiles_n = (a->n + BN - 1) / BN;
+    p.tiles_per_batch = p.tiles_m * p.tiles_n;
+    p.total_tiles = p.tiles_per_batch * a->batch;
+    p.k_blocks = (a->k + BK - 1) / BK;
+    p.ra0 = a->ra0; p.ra1 = a->ra1; p.ca0 = a->ca0; p.ca1 = a->ca1;
+    p.rb0 = a->rb0; p.rb1 = a->rb1; p.cb0 = a->cb0; p.cb1 = a->cb1;
+    p.d = a->d;
+    p.ldd = a->ldd;
+    p.rd0 = a->rd0; p.rd1 = a->rd1; p.cd0 = a->cd0; p.cd1 = a->cd1;
+    p.aux = a->aux;
+    p.alpha = a->alpha;
+    p.epi = a->epilogue;
+    const int esz = (a->epilogue == SWARM_EPI_STORE_F32 || a->epilogue == SWARM_EPI_ACCUM_F32) ? 4 : 2;
+    const int vec_elems = 16 / esz;
+    const bool cd_ok = (a->cd0 % vec_elems == 0) && (a->cd1 % vec_elems == 0);
+    p.vec_ok = (a->ldd % vec_elems == 0) && cd_ok && ((reinterpret_cast<uintptr_t>(a->d) & 15) == 0) &&
+               (!a->aux || (reinterpret_cast<uintptr_t>(a->aux) & 15) == 0);
+    cudaStream_t st = as_stream(stream);
+    if (BN == 128) return dispatch<128>(a->a_mn_major, a->b_mn_major, ta, tb, p, st);
+    return dispatch<256>(a->a_mn_major, a->b_mn_major, ta, tb, p, st);
+}

@@ -1,0 +1,468 @@
+// K3 maxout and K4 LayerNorm (sm_100a).
+//
+// maxout_k  — replaces compress::maxout_k (/root/reference/proj/src/compression.cpp:39-50);
+//             adds the argmax the training backward needs (no reference).
+// layer_norm — replaces compress::layer_norm (compression.cpp:52-74), row-wise over a
+//             [rows, cols] activation: the row lives in registers, two-pass mean /
+//             biased variance like the reference, fp32 statistics for f32/bf16 I/O
+//             (fp64 for the f64 API path).  Backward is the standard LN gradient with
+//             deterministic two-stage column reductions for dgain/dbias.
+#include <algorithm>
+
+#include "common.cuh"
+
+namespace swarm {
+namespace {
+
+template <typename T>
+__device__ __forceinline__ float ld_f(const T* p);
+template <>
+__device__ __forceinline__ float ld_f<float>(const float* p) { return *p; }
+template <>
+__device__ __forceinline__ float ld_f<__nv_bfloat16>(const __nv_bfloat16* p) { return __bfloat162float(*p); }
+
+template <typename T>
+__device__ __forceinline__ T st_t(float v);
+template <>
+__device__ __forceinline__ float st_t<float>(float v) { return v; }
+template <>
+__device__ __forceinline__ __nv_bfloat16 st_t<__nv_bfloat16>(float v) { return __float2bfloat16_rn(v); }
+
+// ---------------------------------------------------------------- maxout ----
+template <typename T>
+__device__ __forceinline__ bool less(T a, T b) {
+    return a < b;
+}
+template <>
+__device__ __forceinline__ bool less<__nv_bfloat16>(__nv_bfloat16 a, __nv_bfloat16 b) {
+    return __bfloat162float(a) < __bfloat162float(b);
+}
+
+template <typename T>
+__global__ void k_maxout_fwd(const T* __restrict__ x, size_t nout, int k, T* __restrict__ out,
+                             uint8_t* __restrict__ argmax) {
+    for (size_t j = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; j < nout;
+         j += static_cast<size_t>(gridDim.x) * blockDim.x) {
+        const T* w = x + j * k;
+        T m = w[0];
+        int am = 0;
+        for (int i = 1; i < k; ++i) {
+            const T v = w[i];
+            if (less(m, v)) {  // std::max(m, v) keeps m unless m < v
+                m = v;
+                am = i;
+            }
+        }
+        out[j] = m;
+        if (argmax) argmax[j] = static_cast<uint8_t>(am);
+    }
+}
+
+template <typename T>
+__global__ void k_maxout_bwd(const T* __restrict__ gout, const uint8_t* __restrict__ argmax, size_t nin, int k,
+                             T* __restrict__ gin) {
+    for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < nin;
+         i += static_cast<size_t>(gridDim.x) * blockDim.x) {
+        const size_t j = i / k;
+        const int r = static_cast<int>(i - j * k);
+        gin[i] = (r == argmax[j]) ? gout[j] : T(0);
+    }
+}
+
+unsigned grid_1d(size_t n, unsigned threads) {
+    const size_t g = (n + threads - 1) / threads;
+    return static_cast<unsigned>(std::max<size_t>(1, std::min<size_t>(g, 148u * 32u)));
+}
+
+// ------------------------------------------------------------- layernorm ----
+constexpr int kLnThreads = 256;
+constexpr int kLnMaxPerThread = 32;  // cols <= 8192
+
+template <int THREADS>
+__device__ __forceinline__ float block_sum(float v, float* red) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    __syncthreads();  // protect red from a previous use
+    if (lane == 0) red[warp] = v;
+    __syncthreads();
+    float r = 0.f;
+#pragma unroll
+    for (int w = 0; w < THREADS / 32; ++w) r += red[w];
+    return r;
+}
+
+// column owned by (thread, slot): col = slot*THREADS*VEC + threadIdx.x*VEC + v
+template <typename T, int VEC>
+__device__ __forceinline__ void load_row(const T* __restrict__ row, int cols, float (&v)[kLnMaxPerThread]) {
+#pragma unroll
+    for (int s = 0; s < kLnMaxPerThread / VEC; ++s) {
+        const int c0 = s * kLnThreads * VEC + threadIdx.x * VEC;
+        if (c0 < cols) {
+            if constexpr (VEC == 8) {  // bf16 x8
+                const uint4 q = *reinterpret_cast<const uint4*>(row + c0);
+                const uint32_t w[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    v[s * 8 + 2 * j] = __uint_as_float(w[j] << 16);
+                    v[s * 8 + 2 * j + 1] = __uint_as_float(w[j] & 0xffff0000u);
+                }
+            } else if constexpr (VEC == 4) {  // f32 x4
+                const float4 q = *reinterpret_cast<const float4*>(row + c0);
+                v[s * 4 + 0] = q.x;
+                v[s * 4 + 1] = q.y;
+                v[s * 4 + 2] = q.z;
+                v[s * 4 + 3] = q.w;
+            } else {
+                v[s] = ld_f<T>(row + c0);
+            }
+        }
+    }
+}
+
+template <typename T, int VEC>
+__device__ __forceinline__ void store_row(T* __restrict__ row, int cols, const float (&v)[kLnMaxPerThread]) {
+#pragma unroll
+    for (int s = 0; s < kLnMaxPerThread / VEC; ++s) {
+        const int c0 = s * kLnThreads * VEC + threadIdx.x * VEC;
+        if (c0 < cols) {
+            if constexpr (VEC == 8) {
+                uint32_t w[4];
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    const __nv_bfloat162 p = __floats2bfloat162_rn(v[s * 8 + 2 * j], v[s * 8 + 2 * j + 1]);
+                    w[j] = *reinterpret_cast<const uint32_t*>(&p);
+                }
+                *reinterpret_cast<uint4*>(row + c0) = make_uint4(w[0], w[1], w[2], w[3]);
+            } else if constexpr (VEC == 4) {
+                *reinterpret_cast<float4*>(row + c0) = make_float4(v[s * 4], v[s * 4 + 1], v[s * 4 + 2], v[s * 4 + 3]);
+            } else {
+                row[c0] = st_t<T>(v[s]);
+            }
+        }
+    }
+}
+
+template <int VEC>
+__device__ __forceinline__ int col_of(int s, int j) {
+    return s * kLnThreads * VEC + threadIdx.x * VEC + j;
+}
+
+template <typename T, int VEC>
+__global__ void __launch_bounds__(kLnThreads) k_ln_fwd(const T* __restrict__ x, int rows, int cols,
+                                                       const float* __restrict__ gain, const float* __restrict__ bias,
+                                                       float eps, T* __restrict__ out, float* __restrict__ mean_out,
+                                                       float* __restrict__ rstd_out) {
+    __shared__ float red[kLnThreads / 32];
+    for (int r = blockIdx.x; r < rows; r += gridDim.x) {
+        float v[kLnMaxPerThread];
+        load_row<T, VEC>(x + static_cast<size_t>(r) * cols, cols, v);
+        float s = 0.f;
+#pragma unroll
+        for (int q = 0; q < kLnMaxPerThread / VEC; ++q)
+#pragma unroll
+            for (int j = 0; j < VEC; ++j)
+                if (col_of<VEC>(q, j) < cols) s += v[q * VEC + j];
+        const float mean = block_sum<kLnThreads>(s, red) / static_cast<float>(cols);
+        float s2 = 0.f;
+#pragma unroll
+        for (int q = 0; q < kLnMaxPerThread / VEC; ++q)
+#pragma unroll
+            for (int j = 0; j < VEC; ++j)
+                if (col_of<VEC>(q, j) < cols) {
+                    const float d = v[q * VEC + j] - mean;
+                    s2 += d * d;
+                }
+        const float var = block_sum<kLnThreads>(s2, red) / static_cast<float>(cols);
+        const float rstd = 1.0f / sqrtf(var + eps);
+#pragma unroll
+        for (int q = 0; q < kLnMaxPerThread / VEC; ++q)
+#pragma unroll
+            for (int j = 0; j < VEC; ++j) {
+                const int c = col_of<VEC>(q, j);
+                if (c < cols) {
+                    float o = (v[q * VEC + j] - mean) * rstd;
+                    if (gain) o *= gain[c];
+                    if (bias) o += bias[c];
+                    v[q * VEC + j] = o;
+                }
+            }
+        store_row<T, VEC>(out + static_cast<size_t>(r) * cols, cols, v);
+        if (threadIdx.x == 0) {
+            if (mean_out) mean_out[r] = mean;
+            if (rstd_out) rstd_out[r] = rstd;
+        }
+    }
+}
+
+// rows handled per CTA in the backward: partial dgain/dbias rows = gridDim.x
+template <typename T, int VEC>
+__global__ void __launch_bounds__(kLnThreads) k_ln_bwd(const T* __restrict__ dy, const T* __restrict__ x, int rows,
+                                                       int cols, const float* __restrict__ gain,
+                                                       const float* __restrict__ mean, const float* __restrict__ rstd,
+                                                       T* __restrict__ dx, float* __restrict__ part_g,
+                                                       float* __restrict__ part_b, int rows_per_cta) {
+    __shared__ float red[kLnThreads / 32];
+    float acc_g[kLnMaxPerThread], acc_b[kLnMaxPerThread];
+#pragma unroll
+    for (int i = 0; i < kLnMaxPerThread; ++i) acc_g[i] = acc_b[i] = 0.f;
+    const int r0 = blockIdx.x * rows_per_cta;
+    const int r1 = min(rows, r0 + rows_per_cta);
+    for (int r = r0; r < r1; ++r) {
+        float xv[kLnMaxPerThread], gv[kLnMaxPerThread];
+        load_row<T, VEC>(x + static_cast<size_t>(r) * cols, cols, xv);
+        load_row<T, VEC>(dy + static_cast<size_t>(r) * cols, cols, gv);
+        const float mu = mean[r], rs = rstd[r];
+        float s1 = 0.f, s2 = 0.f;
+#pragma unroll
+        for (int q = 0; q < kLnMaxPerThread / VEC; ++q)
+#pragma unroll
+            for (int j = 0; j < VEC; ++j) {
+                const int c = col_of<VEC>(q, j);
+                const int i = q * VEC + j;
+                if (c < cols) {
+                    const float xh = (xv[i] - mu) * rs;
+                    const float d = gv[i];
+                    acc_g[i] += d * xh;
+                    acc_b[i] += d;
+                    const float gy = gain ? d * gain[c] : d;
+                    xv[i] = xh;
+                    gv[i] = gy;
+                    s1 += gy * xh;
+                    s2 += gy;
+                }
+            }
+        const float c1 = block_sum<kLnThreads>(s1, red) / static_cast<float>(cols);
+        const float c2 = block_sum<kLnThreads>(s2, red) / static_cast<float>(cols);
+#pragma unroll
+        for (int i = 0; i < kLnMaxPerThread; ++i) xv[i] = rs * (gv[i] - c2 - xv[i] * c1);
+        store_row<T, VEC>(dx + static_cast<size_t>(r) * cols, cols, xv);
+    }
+    float* pg = part_g + static_cast<size_t>(blockIdx.x) * cols;
+    float* pb = part_b + static_cast<size_t>(blockIdx.x) * cols;
+#pragma unroll
+    for (int q = 0; q < kLnMaxPerThread / VEC; ++q)
+#pragma unroll
+        for (int j = 0; j < VEC; ++j) {
+            const int c = col_of<VEC>(q, j);
+            if (c < cols) {
+                pg[c] = acc_g[q * VEC + j];
+                pb[c] = acc_b[q * VEC + j];
+            }
+        }
+}
+
+__global__ void k_col_reduce(const float* __restrict__ part, int nparts, int cols, float* __restrict__ out) {
+    const int c = blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= cols) return;
+    float s = 0.f;
+    for (int p = 0; p < nparts; ++p) s += part[static_cast<size_t>(p) * cols + c];
+    out[c] = s;
+}
+
+// fp64 API path: one CTA per row, three passes over global, verbatim formula.
+__global__ void k_ln_fwd_f64(const double* __restrict__ x, int rows, int cols, const double* __restrict__ gain,
+                             const double* __restrict__ bias, double eps, double* __restrict__ out) {
+    __shared__ double red[32];
+    for (int r = blockIdx.x; r < rows; r += gridDim.x) {
+        const double* xr = x + static_cast<size_t>(r) * cols;
+        double s = 0.0;
+        for (int c = threadIdx.x; c < cols; c += blockDim.x) s += xr[c];
+        for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+        __syncthreads();
+        if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+        __syncthreads();
+        s = 0.0;
+        for (int w = 0; w < static_cast<int>(blockDim.x >> 5); ++w) s += red[w];
+        const double mean = s / static_cast<double>(cols);
+        double v = 0.0;
+        for (int c = threadIdx.x; c < cols; c += blockDim.x) v += (xr[c] - mean) * (xr[c] - mean);
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        __syncthreads();
+        if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+        __syncthreads();
+        v = 0.0;
+        for (int w = 0; w < static_cast<int>(blockDim.x >> 5); ++w) v += red[w];
+        const double var = v / static_cast<double>(cols);
+        const double inv = 1.0 / sqrt(var + eps);
+        for (int c = threadIdx.x; c < cols; c += blockDim.x) {
+            double o = (xr[c] - mean) * inv;
+            if (gain) o *= gain[c];
+            if (bias) o += bias[c];
+            out[static_cast<size_t>(r) * cols + c] = o;
+        }
+    }
+}
+
+__global__ void k_matvec_f64(const double* __restrict__ x, int rows, const double* __restrict__ w, int cols,
+                             double* __restrict__ out) {
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= cols) return;
+    double s = 0.0;
+    for (int i = 0; i < rows; ++i) s = __dadd_rn(s, __dmul_rn(x[i], w[static_cast<size_t>(i) * cols + j]));
+    out[j] = s;
+}
+
+bool al(const void* p, size_t a) { return (reinterpret_cast<uintptr_t>(p) % a) == 0; }
+
+template <typename T>
+int ln_fwd_launch(const T* x, int rows, int cols, const float* g, const float* b, float eps, T* out, float* mean,
+                  float* rstd, cudaStream_t st) {
+    const unsigned grid = static_cast<unsigned>(std::min(rows, 148 * 8));
+    constexpr int V = sizeof(T) == 2 ? 8 : 4;
+    if (cols % V == 0 && al(x, 16) && al(out, 16))
+        k_ln_fwd<T, V><<<grid, kLnThreads, 0, st>>>(x, rows, cols, g, b, eps, out, mean, rstd);
+    else
+        k_ln_fwd<T, 1><<<grid, kLnThreads, 0, st>>>(x, rows, cols, g, b, eps, out, mean, rstd);
+    SWARM_LAUNCH_CHECK("k_ln_fwd");
+    return SWARM_OK;
+}
+
+int ln_bwd_parts(size_t rows) { return static_cast<int>(std::min<size_t>(rows, 2 * 148)); }
+
+template <typename T>
+int ln_bwd_launch(const T* dy, const T* x, int rows, int cols, const float* g, const float* mean, const float* rstd,
+                  T* dx, float* dg, float* db, float* ws, cudaStream_t st) {
+    const int parts = ln_bwd_parts(rows);
+    const int rpc = (rows + parts - 1) / parts;
+    const int grid = (rows + rpc - 1) / rpc;
+    float* pg = ws;
+    float* pb = ws + static_cast<size_t>(parts) * cols;
+    constexpr int V = sizeof(T) == 2 ? 8 : 4;
+    if (cols % V == 0 && al(x, 16) && al(dy, 16) && al(dx, 16))
+        k_ln_bwd<T, V><<<grid, kLnThreads, 0, st>>>(dy, x, rows, cols, g, mean, rstd, dx, pg, pb, rpc);
+    else
+        k_ln_bwd<T, 1><<<grid, kLnThreads, 0, st>>>(dy, x, rows, cols, g, mean, rstd, dx, pg, pb, rpc);
+    SWARM_LAUNCH_CHECK("k_ln_bwd");
+    const unsigned cg = static_cast<unsigned>((cols + 255) / 256);
+    if (dg) {
+        k_col_reduce<<<cg, 256, 0, st>>>(pg, grid, cols, dg);
+        SWARM_LAUNCH_CHECK("k_col_reduce");
+    }
+    if (db) {
+        k_col_reduce<<<cg, 256, 0, st>>>(pb, grid, cols, db);
+        SWARM_LAUNCH_CHECK("k_col_reduce");
+    }
+    return SWARM_OK;
+}
+
+}  // namespace
+}  // namespace swarm
+
+using namespace swarm;
+
+extern "C" {
+
+int swarm_maxout_forward(const void* x, int dtype, size_t n, size_t k, void* out, uint8_t* argmax,
+                         swarm_stream_t stream) {
+    if (k == 0 || n % k != 0) return invalid("maxout_k: k must divide the input length");
+    if (k > 255) return invalid("maxout_k: k must be <= 255 on the device path");
+    if (n == 0) return SWARM_OK;
+    const size_t nout = n / k;
+    cudaStream_t st = as_stream(stream);
+    const unsigned g = grid_1d(nout, 256);
+    switch (dtype) {
+        case SWARM_DTYPE_F32:
+            k_maxout_fwd<float><<<g, 256, 0, st>>>(static_cast<const float*>(x), nout, static_cast<int>(k),
+                                                   static_cast<float*>(out), argmax);
+            break;
+        case SWARM_DTYPE_BF16:
+            k_maxout_fwd<__nv_bfloat16><<<g, 256, 0, st>>>(static_cast<const __nv_bfloat16*>(x), nout,
+                                                           static_cast<int>(k), static_cast<__nv_bfloat16*>(out),
+                                                           argmax);
+            break;
+        case SWARM_DTYPE_F64:
+            k_maxout_fwd<double><<<g, 256, 0, st>>>(static_cast<const double*>(x), nout, static_cast<int>(k),
+                                                    static_cast<double*>(out), argmax);
+            break;
+        default: set_error("maxout_k: unsupported dtype"); return SWARM_E_UNSUPPORTED;
+    }
+    SWARM_LAUNCH_CHECK("k_maxout_fwd");
+    return SWARM_OK;
+}
+
+int swarm_maxout_backward(const void* grad_out, int dtype, const uint8_t* argmax, size_t n_out, size_t k,
+                          void* grad_in, swarm_stream_t stream) {
+    if (k == 0 || k > 255) return invalid("maxout backward: bad k");
+    if (n_out == 0) return SWARM_OK;
+    const size_t nin = n_out * k;
+    cudaStream_t st = as_stream(stream);
+    const unsigned g = grid_1d(nin, 256);
+    switch (dtype) {
+        case SWARM_DTYPE_F32:
+            k_maxout_bwd<float><<<g, 256, 0, st>>>(static_cast<const float*>(grad_out), argmax, nin,
+                                                   static_cast<int>(k), static_cast<float*>(grad_in));
+            break;
+        case SWARM_DTYPE_BF16:
+            k_maxout_bwd<__nv_bfloat16><<<g, 256, 0, st>>>(static_cast<const __nv_bfloat16*>(grad_out), argmax, nin,
+                                                           static_cast<int>(k), static_cast<__nv_bfloat16*>(grad_in));
+            break;
+        case SWARM_DTYPE_F64:
+            k_maxout_bwd<double><<<g, 256, 0, st>>>(static_cast<const double*>(grad_out), argmax, nin,
+                                                    static_cast<int>(k), static_cast<double*>(grad_in));
+            break;
+        default: set_error("maxout backward: unsupported dtype"); return SWARM_E_UNSUPPORTED;
+    }
+    SWARM_LAUNCH_CHECK("k_maxout_bwd");
+    return SWARM_OK;
+}
+
+int swarm_layer_norm_forward(const void* x, int dtype, size_t rows, size_t cols, const void* gain, const void* bias,
+                             double eps, void* out, float* mean, float* rstd, swarm_stream_t stream) {
+    if (cols == 0) return invalid("layer_norm: empty input");
+    if (rows == 0) return SWARM_OK;
+    cudaStream_t st = as_stream(stream);
+    if (dtype == SWARM_DTYPE_F64) {
+        k_ln_fwd_f64<<<static_cast<unsigned>(std::min<size_t>(rows, 148 * 8)), 256, 0, st>>>(
+            static_cast<const double*>(x), static_cast<int>(rows), static_cast<int>(cols),
+            static_cast<const double*>(gain), static_cast<const double*>(bias), eps, static_cast<double*>(out));
+        SWARM_LAUNCH_CHECK("k_ln_fwd_f64");
+        return SWARM_OK;
+    }
+    if (cols > static_cast<size_t>(kLnThreads * kLnMaxPerThread)) return invalid("layer_norm: cols > 8192 unsupported");
+    const float* g = static_cast<const float*>(gain);
+    const float* b = static_cast<const float*>(bias);
+    if (dtype == SWARM_DTYPE_F32)
+        return ln_fwd_launch<float>(static_cast<const float*>(x), static_cast<int>(rows), static_cast<int>(cols), g,
+                                    b, static_cast<float>(eps), static_cast<float*>(out), mean, rstd, st);
+    if (dtype == SWARM_DTYPE_BF16)
+        return ln_fwd_launch<__nv_bfloat16>(static_cast<const __nv_bfloat16*>(x), static_cast<int>(rows),
+                                            static_cast<int>(cols), g, b, static_cast<float>(eps),
+                                            static_cast<__nv_bfloat16*>(out), mean, rstd, st);
+    set_error("layer_norm: unsupported dtype");
+    return SWARM_E_UNSUPPORTED;
+}
+
+int swarm_matvec_f64(const double* x, size_t rows, const double* w, size_t cols, double* out, swarm_stream_t stream) {
+    if (cols == 0) return SWARM_OK;
+    k_matvec_f64<<<static_cast<unsigned>((cols + 127) / 128), 128, 0, as_stream(stream)>>>(
+        x, static_cast<int>(rows), w, static_cast<int>(cols), out);
+    SWARM_LAUNCH_CHECK("k_matvec_f64");
+    return SWARM_OK;
+}
+
+size_t swarm_layer_norm_backward_workspace(size_t rows, size_t cols) {
+    return 2 * static_cast<size_t>(ln_bwd_parts(rows)) * cols * sizeof(float);
+}
+
+int swarm_layer_norm_backward(const void* dy, const void* x, int dtype, size_t rows, size_t cols, const float* gain,
+                              const float* mean, const float* rstd, void* dx, float* dgain, float* dbias,
+                              void* workspace, swarm_stream_t stream) {
+    if (cols == 0 || cols > static_cast<size_t>(kLnThreads * kLnMaxPerThread))
+        return invalid("layer_norm backward: bad cols");
+    if (rows == 0) return SWARM_OK;
+    cudaStream_t st = as_stream(stream);
+    float* ws = static_cast<float*>(workspace);
+    if (dtype == SWARM_DTYPE_F32)
+        return ln_bwd_launch<float>(static_cast<const float*>(dy), static_cast<const float*>(x), static_cast<int>(rows),
+                                    static_cast<int>(cols), gain, mean, rstd, static_cast<float*>(dx), dgain, dbias,
+                                    ws, st);
+    if (dtype == SWARM_DTYPE_BF16)
+        return ln_bwd_launch<__nv_bfloat16>(static_cast<const __nv_bfloat16*>(dy), static_cast<const __nv_bfloat16*>(x),
+                                            static_cast<int>(rows), static_cast<int>(cols), gain, mean, rstd,
+                                            static_cast<__nv_bfloat16*>(dx), dgain, dbias, ws, st);
+    set_error("layer_norm backward: unsupported dtype");
+    return SWARM_E_UNSUPPORTED;
+}
+
+}  // extern "C"

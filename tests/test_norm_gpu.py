@@ -1,0 +1,90 @@
+"""GPU parity: K3 maxout (bit-exact vs the oracle) and K4 LayerNorm
+(fp32/bf16 vs a torch fp64 reference of compression.cpp:52-74; tolerance
+stated per dtype below)."""
+import numpy as np
+import pytest
+
+import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+# LayerNorm tolerances: fp32 I/O with fp32 statistics; bf16 I/O (output rounding 2^-8 relative)
+LN_TOL = {"float32": dict(rtol=1e-5, atol=2e-5), "bfloat16": dict(rtol=1e-2, atol=1.6e-2)}
+
+
+@pytest.mark.parametrize("k", [1, 2, 3, 4, 8])
+@pytest.mark.parametrize("dtype", ["float32", "bfloat16", "float64"])
+def test_maxout_bitexact(cuda, k, dtype):
+    import torch
+    from paper_2301_11913_b200 import ops
+    n = 4096 * 3 * k
+    rng = np.random.default_rng(k)
+    x = np.round(rng.standard_normal(n) * 4) / 4  # many ties
+    t = torch.from_numpy(x).to(getattr(torch, dtype)).cuda()
+    out, am = ops.maxout(t, k)
+    xr = t.double().cpu().numpy()
+    st, exp, exp_am = O.maxout(xr, k)
+    assert np.array_equal(out.double().cpu().numpy(), exp)
+    assert np.array_equal(am.cpu().numpy(), exp_am)
+    # backward scatters to the winning element only
+    g = torch.randn(n // k, device="cuda").to(t.dtype)
+    gin = ops.maxout_backward(g, am, k).view(-1, k).double().cpu().numpy()
+    want = np.zeros((n // k, k))
+    want[np.arange(n // k), exp_am] = g.double().cpu().numpy()
+    assert np.array_equal(gin, want)
+
+
+def test_maxout_bad_k(cuda):
+    import torch
+    from paper_2301_11913_b200 import ConfigError, ops
+    with pytest.raises(ConfigError):
+        ops.maxout(torch.ones(3, device="cuda"), 2)
+
+
+@pytest.mark.parametrize("cols", [256, 2048, 4096, 1000, 7])
+@pytest.mark.parametrize("dtype", ["float32", "bfloat16"])
+def test_layer_norm_forward(cuda, cols, dtype):
+    import torch
+    from paper_2301_11913_b200 import ops
+    torch.manual_seed(cols)
+    rows = 129
+    x = (torch.randn(rows, cols, device="cuda") * 3 + 1).to(getattr(torch, dtype))
+    g = torch.rand(cols, device="cuda") + 0.5
+    b = torch.randn(cols, device="cuda")
+    y, mean, rstd = ops.layer_norm(x, g, b)
+    xd = x.double()
+    ref = torch.nn.functional.layer_norm(xd, (cols,), g.double(), b.double(), 1e-5)
+    torch.testing.assert_close(y.double(), ref, **LN_TOL[dtype])
+    torch.testing.assert_close(mean.double(), xd.mean(1), rtol=1e-5, atol=1e-5)
+
+
+def test_layer_norm_f64_matches_oracle(cuda):
+    import torch
+    from paper_2301_11913_b200 import ops
+    x = np.random.default_rng(11).standard_normal(2048) * 3 + 0.5
+    y, _, _ = ops.layer_norm(torch.from_numpy(x).cuda().view(1, -1))
+    st, exp = O.layer_norm(x)
+    np.testing.assert_allclose(y.cpu().numpy().ravel(), exp, rtol=1e-13, atol=1e-13)
+
+
+@pytest.mark.parametrize("cols", [256, 2048, 4096])
+@pytest.mark.parametrize("dtype", ["float32", "bfloat16"])
+def test_layer_norm_backward(cuda, cols, dtype):
+    import torch
+    from paper_2301_11913_b200 import ops
+    torch.manual_seed(1)
+    rows = 300
+    x = torch.randn(rows, cols, device="cuda").to(getattr(torch, dtype))
+    g = torch.rand(cols, device="cuda") + 0.5
+    b = torch.randn(cols, device="cuda")
+    dy = torch.randn(rows, cols, device="cuda").to(x.dtype)
+    y, mean, rstd = ops.layer_norm(x, g, b)
+    dx, dg, db = ops.layer_norm_backward(dy, x, g, mean, rstd)
+    xd = x.double().requires_grad_()
+    gd = g.double().requires_grad_()
+    bd = b.double().requires_grad_()
+    torch.nn.functional.layer_norm(xd, (cols,), gd, bd, 1e-5).backward(dy.double())
+    tol = dict(rtol=1e-4, atol=1e-4) if dtype == "float32" else dict(rtol=2e-2, atol=3e-2)
+    torch.testing.assert_close(dx.double(), xd.grad, **tol)
+    torch.testing.assert_close(dg.double(), gd.grad, rtol=1e-4, atol=1e-3 * rows ** 0.5)
+    torch.testing.assert_close(db.double(), bd.grad, rtol=1e-4, atol=1e-3 * rows ** 0.5)
