@@ -97,13 +97,15 @@ int swarm_maxout_backward(const void* grad_out, int dtype, const uint8_t* argmax
 int swarm_layer_norm_forward(const void* x, int dtype, size_t rows, size_t cols, const void* gain,
                              const void* bias, double eps, void* out, float* mean, float* rstd,
                              swarm_stream_t stream);
-/* dx (dtype), dgain/dbias (float, cols; written, not accumulated) from dy,
- * x and the saved statistics.  `workspace` >= swarm_layer_norm_backward_workspace()
+/* dx = LN'(dy) (+ dres when non-NULL: the residual branch's gradient, fused),
+ * dgain/dbias (float, cols) written, or added when `accumulate` != 0 (gradient
+ * accumulation over microbatches).  `workspace` >= swarm_layer_norm_backward_workspace()
  * bytes of device memory. */
 size_t swarm_layer_norm_backward_workspace(size_t rows, size_t cols);
 int swarm_layer_norm_backward(const void* dy, const void* x, int dtype, size_t rows, size_t cols,
-                              const float* gain, const float* mean, const float* rstd, void* dx,
-                              float* dgain, float* dbias, void* workspace, swarm_stream_t stream);
+                              const float* gain, const float* mean, const float* rstd, const void* dres,
+                              void* dx, float* dgain, float* dbias, int accumulate, void* workspace,
+                              swarm_stream_t stream);
 
 /* ---- bottleneck projection (fp64 API path) -------------------------------
  * Replaces the private matvec behind compress::bottleneck_forward /
@@ -140,6 +142,93 @@ typedef struct {
     int epilogue;
 } swarm_gemm_args;
 int swarm_gemm_bf16(const swarm_gemm_args* args, swarm_stream_t stream);
+
+/* ---- training building blocks (stage executor internals, exported for tests)
+ * None of these has a reference counterpart: the reference only models the
+ * block's cost (cost_model.cpp:31-42, sim.cpp:361-364).  bf16 tensors are
+ * passed as void*. */
+/* out[t,:] = table[tokens[t],:]  (bf16 [vocab,d] -> bf16 [n,d]); out-of-range ids give 0 */
+int swarm_embedding_forward(const int32_t* tokens, size_t n_tokens, const void* table, size_t vocab, size_t d,
+                            void* out, swarm_stream_t stream);
+/* dtable[tokens[t],:] += dout[t,:]  (fp32 accumulate) */
+int swarm_embedding_backward(const int32_t* tokens, size_t n_tokens, const void* dout, size_t vocab, size_t d,
+                             float* dtable, swarm_stream_t stream);
+/* P = softmax(S) row-wise over L columns (rows = batch*heads*L); causal masks
+ * column j > (row % L).  S fp32 (already scaled), P bf16. */
+int swarm_attn_softmax_forward(const float* s, size_t rows, size_t L, int causal, void* p, swarm_stream_t stream);
+/* dS = scale * P * (dP - rowsum(P*dP)), bf16 */
+int swarm_attn_softmax_backward(const void* p, const float* dp, size_t rows, size_t L, float scale, void* ds,
+                                swarm_stream_t stream);
+/* token cross-entropy on fp32 logits [rows, vocab]: loss_sum += sum_t (lse_t - logit_t[target_t]);
+ * dlogits (bf16, optional) = grad_scale * (softmax - onehot) */
+int swarm_cross_entropy(const float* logits, const int32_t* targets, size_t rows, size_t vocab, float grad_scale,
+                        float* loss_sum, void* dlogits, swarm_stream_t stream);
+/* fused AdamW over a flat fp32 arena; refreshes the bf16 shadow (p16, optional)
+ * and zeroes the gradient when zero_grad != 0.  step >= 1 (bias correction). */
+int swarm_adamw_step(float* p32, void* p16, float* grad, float* m, float* v, size_t n, float lr, float beta1,
+                     float beta2, float eps, float weight_decay, int step, float grad_scale, int zero_grad,
+                     swarm_stream_t stream);
+/* p[i] = mean + std * N(0,1) from a counter-based hash of (seed, i) */
+int swarm_fill_normal(float* p, size_t n, float mean, float std, uint64_t seed, swarm_stream_t stream);
+int swarm_cast_f32_bf16(const float* in, void* out, size_t n, swarm_stream_t stream);
+
+/* ---- stage executor -------------------------------------------------------
+ * One SWARM pipeline stage on one GPU: a contiguous range of pre-LN
+ * transformer blocks (Wqkv d x 3d, Wo d x d, W1 d x d_ffn, W2 d_ffn x d, no
+ * biases: P/src/cost_model.cpp:31-35; GeLU MLP with residual: PAPER:787), the
+ * embedding on the first stage and final LN + LM head + cross-entropy on the
+ * last.  It is the real work behind the reference's simulated stage visit
+ * (Engine::visit_seconds / start_service, P/src/sim.cpp:361-364, 395-403):
+ * forward = one forward visit, backward = one backward visit.  Boundary
+ * tensors cross stages as a "wire message": bf16 activations, or int8 codes
+ * followed by fp32 per-block scales (the codec above; payload as
+ * QuantizedTensor::payload_bits, compression.hpp:20).  Weights, fp32 master
+ * copy, fp32 gradients and AdamW moments live in flat device arenas owned by
+ * the stage; activations for up to max_slots in-flight microbatches too.  */
+#define SWARM_WIRE_BF16 0
+#define SWARM_WIRE_INT8 1
+typedef struct swarm_stage* swarm_stage_t;
+typedef struct {
+    int d_model, n_heads, d_ffn, seq_len, micro_batch;
+    int n_layers;      /* block applications in this stage */
+    int shared_layers; /* 1: one weight set applied n_layers times (layer sharing) */
+    int vocab;
+    int is_first, is_last;
+    int causal;
+    int max_slots;     /* microbatches in flight (activation slots) */
+    int wire;          /* SWARM_WIRE_BF16 | SWARM_WIRE_INT8 */
+    int block_size;    /* int8 codec block */
+    float lr, beta1, beta2, eps, weight_decay, init_std;
+    uint64_t seed;
+} swarm_stage_config;
+
+int swarm_stage_create(const swarm_stage_config* cfg, swarm_stage_t* out);
+void swarm_stage_destroy(swarm_stage_t st);
+size_t swarm_stage_wire_bytes(swarm_stage_t st);
+size_t swarm_stage_num_params(swarm_stage_t st);
+/* forward visit of microbatch `slot`.  in: int32 tokens [B*L] on the first
+ * stage, else a wire message.  out: wire message for the next stage (unused on
+ * the last).  Last stage: targets int32 [B*L]; loss_sum (device float) += the
+ * token losses; the LM-head backward runs here too (dlogits scaled by
+ * loss_scale, so backward needs no second pass over the vocabulary). */
+int swarm_stage_forward(swarm_stage_t st, int slot, const void* in, const int32_t* targets, void* out,
+                        float* loss_sum, float loss_scale, swarm_stream_t stream);
+/* backward visit: grad_in = wire message from the next stage (unused on the
+ * last), grad_out = wire message for the previous stage (unused on the first).
+ * Parameter gradients accumulate into the fp32 gradient arena. */
+int swarm_stage_backward(swarm_stage_t st, int slot, const void* grad_in, void* grad_out, swarm_stream_t stream);
+/* AdamW over the whole stage; grads are multiplied by grad_scale first, then zeroed. */
+int swarm_stage_optimizer_step(swarm_stage_t st, float grad_scale, swarm_stream_t stream);
+float* swarm_stage_grads(swarm_stage_t st);  /* fp32 [num_params]: intra-stage all-reduce buffer */
+float* swarm_stage_params(swarm_stage_t st); /* fp32 master [num_params] */
+void* swarm_stage_params_bf16(swarm_stage_t st);
+/* re-derive the bf16 shadow from the fp32 master (after loading / receiving weights) */
+int swarm_stage_sync_shadow(swarm_stage_t st, swarm_stream_t stream);
+/* enumerate parameter tensors: index -> name, offset (elements), rows, cols */
+int swarm_stage_param_info(swarm_stage_t st, int index, const char** name, size_t* offset, size_t* rows,
+                           size_t* cols);
+/* saved activation of (slot, layer) by name ("x","a","qkv","P","o","h","c","u","g","xf","dxf"), for tests */
+int swarm_stage_activation(swarm_stage_t st, int slot, int layer, const char* name, void** ptr, size_t* numel);
 
 #ifdef __cplusplus
 }

@@ -28,6 +28,14 @@ class GemmArgs(C.Structure):
         ("aux", C.c_void_p), ("alpha", C.c_float), ("epilogue", C.c_int)]
 
 
+class StageConfigC(C.Structure):
+    _fields_ = [(n, C.c_int) for n in ("d_model", "n_heads", "d_ffn", "seq_len", "micro_batch", "n_layers",
+                                       "shared_layers", "vocab", "is_first", "is_last", "causal", "max_slots", "wire",
+                                       "block_size")] + \
+               [(n, C.c_float) for n in ("lr", "beta1", "beta2", "eps", "weight_decay", "init_std")] + \
+               [("seed", C.c_uint64)]
+
+
 # (name, restype, argtypes) for every symbol include/swarm_b200.h declares
 P, SZ, I, U32P, U8P, F, D = C.c_void_p, C.c_size_t, C.c_int, C.c_void_p, C.c_void_p, C.c_float, C.c_double
 SIGNATURES = {
@@ -42,9 +50,30 @@ SIGNATURES = {
     "swarm_maxout_backward": (I, [P, I, U8P, SZ, SZ, P, P]),
     "swarm_layer_norm_forward": (I, [P, I, SZ, SZ, P, P, D, P, P, P, P]),
     "swarm_layer_norm_backward_workspace": (SZ, [SZ, SZ]),
-    "swarm_layer_norm_backward": (I, [P, P, I, SZ, SZ, P, P, P, P, P, P, P, P]),
+    "swarm_layer_norm_backward": (I, [P, P, I, SZ, SZ, P, P, P, P, P, P, P, I, P, P]),
     "swarm_matvec_f64": (I, [P, SZ, P, SZ, P, P]),
     "swarm_gemm_bf16": (I, [C.POINTER(GemmArgs), P]),
+    "swarm_embedding_forward": (I, [P, SZ, P, SZ, SZ, P, P]),
+    "swarm_embedding_backward": (I, [P, SZ, P, SZ, SZ, P, P]),
+    "swarm_attn_softmax_forward": (I, [P, SZ, SZ, I, P, P]),
+    "swarm_attn_softmax_backward": (I, [P, P, SZ, SZ, F, P, P]),
+    "swarm_cross_entropy": (I, [P, P, SZ, SZ, F, P, P, P]),
+    "swarm_adamw_step": (I, [P, P, P, P, P, SZ, F, F, F, F, F, I, F, I, P]),
+    "swarm_fill_normal": (I, [P, SZ, F, F, C.c_uint64, P]),
+    "swarm_cast_f32_bf16": (I, [P, P, SZ, P]),
+    "swarm_stage_create": (I, [C.POINTER(StageConfigC), C.POINTER(C.c_void_p)]),
+    "swarm_stage_destroy": (None, [P]),
+    "swarm_stage_wire_bytes": (SZ, [P]),
+    "swarm_stage_num_params": (SZ, [P]),
+    "swarm_stage_forward": (I, [P, I, P, P, P, P, F, P]),
+    "swarm_stage_backward": (I, [P, I, P, P, P]),
+    "swarm_stage_optimizer_step": (I, [P, F, P]),
+    "swarm_stage_grads": (P, [P]),
+    "swarm_stage_params": (P, [P]),
+    "swarm_stage_params_bf16": (P, [P]),
+    "swarm_stage_sync_shadow": (I, [P, P]),
+    "swarm_stage_param_info": (I, [P, I, C.POINTER(C.c_char_p), C.POINTER(SZ), C.POINTER(SZ), C.POINTER(SZ)]),
+    "swarm_stage_activation": (I, [P, I, I, C.c_char_p, C.POINTER(P), C.POINTER(SZ)]),
 }
 
 _lib = None

@@ -200,7 +200,8 @@ template <typename T, int VEC>
 __global__ void __launch_bounds__(kLnThreads) k_ln_bwd(const T* __restrict__ dy, const T* __restrict__ x, int rows,
                                                        int cols, const float* __restrict__ gain,
                                                        const float* __restrict__ mean, const float* __restrict__ rstd,
-                                                       T* __restrict__ dx, float* __restrict__ part_g,
+                                                       const T* __restrict__ dres, T* __restrict__ dx,
+                                                       float* __restrict__ part_g,
                                                        float* __restrict__ part_b, int rows_per_cta) {
     __shared__ float red[kLnThreads / 32];
     float acc_g[kLnMaxPerThread], acc_b[kLnMaxPerThread];
@@ -236,6 +237,11 @@ __global__ void __launch_bounds__(kLnThreads) k_ln_bwd(const T* __restrict__ dy,
         const float c2 = block_sum<kLnThreads>(s2, red) / static_cast<float>(cols);
 #pragma unroll
         for (int i = 0; i < kLnMaxPerThread; ++i) xv[i] = rs * (gv[i] - c2 - xv[i] * c1);
+        if (dres) {
+            load_row<T, VEC>(dres + static_cast<size_t>(r) * cols, cols, gv);
+#pragma unroll
+            for (int i = 0; i < kLnMaxPerThread; ++i) xv[i] += gv[i];
+        }
         store_row<T, VEC>(dx + static_cast<size_t>(r) * cols, cols, xv);
     }
     float* pg = part_g + static_cast<size_t>(blockIdx.x) * cols;
@@ -252,12 +258,13 @@ __global__ void __launch_bounds__(kLnThreads) k_ln_bwd(const T* __restrict__ dy,
         }
 }
 
-__global__ void k_col_reduce(const float* __restrict__ part, int nparts, int cols, float* __restrict__ out) {
+__global__ void k_col_reduce(const float* __restrict__ part, int nparts, int cols, float* __restrict__ out,
+                             int accumulate) {
     const int c = blockIdx.x * blockDim.x + threadIdx.x;
     if (c >= cols) return;
     float s = 0.f;
     for (int p = 0; p < nparts; ++p) s += part[static_cast<size_t>(p) * cols + c];
-    out[c] = s;
+    out[c] = accumulate ? out[c] + s : s;
 }
 
 // fp64 API path: one CTA per row, three passes over global, verbatim formula.
@@ -322,25 +329,25 @@ int ln_bwd_parts(size_t rows) { return static_cast<int>(std::min<size_t>(rows, 2
 
 template <typename T>
 int ln_bwd_launch(const T* dy, const T* x, int rows, int cols, const float* g, const float* mean, const float* rstd,
-                  T* dx, float* dg, float* db, float* ws, cudaStream_t st) {
+                  const T* dres, T* dx, float* dg, float* db, int accumulate, float* ws, cudaStream_t st) {
     const int parts = ln_bwd_parts(rows);
     const int rpc = (rows + parts - 1) / parts;
     const int grid = (rows + rpc - 1) / rpc;
     float* pg = ws;
     float* pb = ws + static_cast<size_t>(parts) * cols;
     constexpr int V = sizeof(T) == 2 ? 8 : 4;
-    if (cols % V == 0 && al(x, 16) && al(dy, 16) && al(dx, 16))
-        k_ln_bwd<T, V><<<grid, kLnThreads, 0, st>>>(dy, x, rows, cols, g, mean, rstd, dx, pg, pb, rpc);
+    if (cols % V == 0 && al(x, 16) && al(dy, 16) && al(dx, 16) && (!dres || al(dres, 16)))
+        k_ln_bwd<T, V><<<grid, kLnThreads, 0, st>>>(dy, x, rows, cols, g, mean, rstd, dres, dx, pg, pb, rpc);
     else
-        k_ln_bwd<T, 1><<<grid, kLnThreads, 0, st>>>(dy, x, rows, cols, g, mean, rstd, dx, pg, pb, rpc);
+        k_ln_bwd<T, 1><<<grid, kLnThreads, 0, st>>>(dy, x, rows, cols, g, mean, rstd, dres, dx, pg, pb, rpc);
     SWARM_LAUNCH_CHECK("k_ln_bwd");
     const unsigned cg = static_cast<unsigned>((cols + 255) / 256);
     if (dg) {
-        k_col_reduce<<<cg, 256, 0, st>>>(pg, grid, cols, dg);
+        k_col_reduce<<<cg, 256, 0, st>>>(pg, grid, cols, dg, accumulate);
         SWARM_LAUNCH_CHECK("k_col_reduce");
     }
     if (db) {
-        k_col_reduce<<<cg, 256, 0, st>>>(pb, grid, cols, db);
+        k_col_reduce<<<cg, 256, 0, st>>>(pb, grid, cols, db, accumulate);
         SWARM_LAUNCH_CHECK("k_col_reduce");
     }
     return SWARM_OK;
@@ -446,8 +453,8 @@ size_t swarm_layer_norm_backward_workspace(size_t rows, size_t cols) {
 }
 
 int swarm_layer_norm_backward(const void* dy, const void* x, int dtype, size_t rows, size_t cols, const float* gain,
-                              const float* mean, const float* rstd, void* dx, float* dgain, float* dbias,
-                              void* workspace, swarm_stream_t stream) {
+                              const float* mean, const float* rstd, const void* dres, void* dx, float* dgain,
+                              float* dbias, int accumulate, void* workspace, swarm_stream_t stream) {
     if (cols == 0 || cols > static_cast<size_t>(kLnThreads * kLnMaxPerThread))
         return invalid("layer_norm backward: bad cols");
     if (rows == 0) return SWARM_OK;
@@ -455,12 +462,13 @@ int swarm_layer_norm_backward(const void* dy, const void* x, int dtype, size_t r
     float* ws = static_cast<float*>(workspace);
     if (dtype == SWARM_DTYPE_F32)
         return ln_bwd_launch<float>(static_cast<const float*>(dy), static_cast<const float*>(x), static_cast<int>(rows),
-                                    static_cast<int>(cols), gain, mean, rstd, static_cast<float*>(dx), dgain, dbias,
-                                    ws, st);
+                                    static_cast<int>(cols), gain, mean, rstd, static_cast<const float*>(dres),
+                                    static_cast<float*>(dx), dgain, dbias, accumulate, ws, st);
     if (dtype == SWARM_DTYPE_BF16)
-        return ln_bwd_launch<__nv_bfloat16>(static_cast<const __nv_bfloat16*>(dy), static_cast<const __nv_bfloat16*>(x),
-                                            static_cast<int>(rows), static_cast<int>(cols), gain, mean, rstd,
-                                            static_cast<__nv_bfloat16*>(dx), dgain, dbias, ws, st);
+        return ln_bwd_launch<__nv_bfloat16>(
+            static_cast<const __nv_bfloat16*>(dy), static_cast<const __nv_bfloat16*>(x), static_cast<int>(rows),
+            static_cast<int>(cols), gain, mean, rstd, static_cast<const __nv_bfloat16*>(dres),
+            static_cast<__nv_bfloat16*>(dx), dgain, dbias, accumulate, ws, st);
     set_error("layer_norm backward: unsupported dtype");
     return SWARM_E_UNSUPPORTED;
 }

@@ -1,0 +1,535 @@
+// Stage executor: the real forward / backward visit of one SWARM pipeline
+// stage on one B200 (the reference simulates it as a constant service time,
+// /root/reference/proj/src/sim.cpp:361-364 and :395-403).
+//
+// Host C++ that only enqueues sm_100a kernels through the C-ABI on the
+// caller's stream; every buffer is allocated once at creation, so a visit
+// performs no allocation and no host synchronisation.
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstring>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "swarm_b200.h"
+
+namespace {
+
+using bf16 = uint16_t;  // storage only; kernels interpret it
+
+struct TensorInfo {
+    std::string name;
+    size_t off, rows, cols;
+};
+
+struct LayerW {
+    size_t wqkv, wo, w1, w2, ln1g, ln1b, ln2g, ln2b;
+};
+
+struct Act {
+    bf16 *x, *a, *qkv, *P, *o, *h, *c, *u, *g;
+    float *mu1, *rs1, *mu2, *rs2;
+};
+
+struct Slot {
+    std::vector<Act> layer;  // n_layers entries; layer[l].x is the input of application l
+    bf16* out;               // output of the last application (input of the next stage / final LN)
+    bf16* xf;                // final LN output (last stage)
+    float *muf, *rsf;
+    bf16* dxf;               // d loss / d xf, produced by the fused LM-head backward
+    int32_t* tokens;         // first stage: the microbatch's token ids (embedding backward)
+};
+
+}  // namespace
+
+struct swarm_stage {
+    swarm_stage_config cfg{};
+    int T = 0, d = 0, H = 0, dh = 0, F = 0, V = 0, L = 0, B = 0;
+    size_t nparams = 0;
+    std::vector<TensorInfo> tensors;
+    std::vector<LayerW> layers;
+    size_t emb = 0, lnfg = 0, lnfb = 0, head = 0;
+    float *p32 = nullptr, *grad = nullptr, *m = nullptr, *v = nullptr;
+    bf16* p16 = nullptr;
+    std::vector<Slot> slots;
+    // workspaces (one visit at a time per stage)
+    float *S = nullptr, *dP = nullptr, *logits = nullptr;
+    bf16 *dS = nullptr, *gy[2] = {nullptr, nullptr}, *dhid = nullptr, *dc = nullptr, *du = nullptr, *dqkv = nullptr,
+         *dO = nullptr, *da = nullptr, *dlogits = nullptr;
+    void* lnws = nullptr;
+    std::vector<void*> allocations;
+    int step = 0;
+};
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(const std::string& m) {
+    g_err = m;
+    return SWARM_E_INVALID;
+}
+
+#define TRY(expr)                   \
+    do {                            \
+        int _rc = (expr);           \
+        if (_rc != SWARM_OK) return _rc; \
+    } while (0)
+
+int dmalloc(swarm_stage* s, void** p, size_t bytes) {
+    if (bytes == 0) bytes = 16;
+    bytes = (bytes + 255) & ~size_t(255);
+    cudaError_t e = cudaMalloc(p, bytes);
+    if (e != cudaSuccess) {
+        g_err = std::string("stage: cudaMalloc failed: ") + cudaGetErrorString(e);
+        return SWARM_E_CUDA;
+    }
+    s->allocations.push_back(*p);
+    return SWARM_OK;
+}
+
+template <typename T>
+int alloc(swarm_stage* s, T** p, size_t count) {
+    void* q = nullptr;
+    TRY(dmalloc(s, &q, count * sizeof(T)));
+    *p = static_cast<T*>(q);
+    return SWARM_OK;
+}
+
+size_t add_tensor(swarm_stage* s, const std::string& name, size_t rows, size_t cols) {
+    const size_t off = s->nparams;
+    s->tensors.push_back({name, off, rows, cols});
+    s->nparams += (rows * cols + 63) & ~size_t(63);  // 256-byte aligned fp32 / 128-byte bf16 slices
+    return off;
+}
+
+// ------------------------------------------------------------------ GEMMs --
+struct Op {  // one operand in its 2-D storage
+    const void* p;
+    int ld, rows, cols;
+    bool mn;  // MN-major (the operand is stored transposed)
+};
+
+int mm(int M, int N, int K, Op a, Op b, void* d, int ldd, int epi, const void* aux, float alpha, cudaStream_t st) {
+    swarm_gemm_args g{};
+    g.m = M;
+    g.n = N;
+    g.k = K;
+    g.batch = 1;
+    g.bh = 1;
+    g.a = a.p;
+    g.lda = a.ld;
+    g.a_mn_major = a.mn;
+    g.a_rows = a.rows;
+    g.a_cols = a.cols;
+    g.b = b.p;
+    g.ldb = b.ld;
+    g.b_mn_major = b.mn;
+    g.b_rows = b.rows;
+    g.b_cols = b.cols;
+    g.d = d;
+    g.ldd = ldd;
+    g.aux = aux;
+    g.alpha = alpha;
+    g.epilogue = epi;
+    return swarm_gemm_bf16(&g, st);
+}
+
+// Attention GEMM batched over z = b*H + h.  Offsets in storage coordinates:
+// token-major operands move by L rows per batch and dh columns per head;
+// [B*H*L, L] score-like operands move by H*L rows per batch and L per head.
+struct BOp {
+    Op op;
+    int r0, r1, c0, c1;
+};
+
+int bmm(swarm_stage* s, int M, int N, int K, BOp a, BOp b, void* d, int ldd, int rd0, int rd1, int cd0, int cd1,
+        int epi, float alpha, cudaStream_t st) {
+    swarm_gemm_args g{};
+    g.m = M;
+    g.n = N;
+    g.k = K;
+    g.batch = s->B * s->H;
+    g.bh = s->H;
+    g.a = a.op.p;
+    g.lda = a.op.ld;
+    g.a_mn_major = a.op.mn;
+    g.a_rows = a.op.rows;
+    g.a_cols = a.op.cols;
+    g.ra0 = a.r0;
+    g.ra1 = a.r1;
+    g.ca0 = a.c0;
+    g.ca1 = a.c1;
+    g.b = b.op.p;
+    g.ldb = b.op.ld;
+    g.b_mn_major = b.op.mn;
+    g.b_rows = b.op.rows;
+    g.b_cols = b.op.cols;
+    g.rb0 = b.r0;
+    g.rb1 = b.r1;
+    g.cb0 = b.c0;
+    g.cb1 = b.c1;
+    g.d = d;
+    g.ldd = ldd;
+    g.rd0 = rd0;
+    g.rd1 = rd1;
+    g.cd0 = cd0;
+    g.cd1 = cd1;
+    g.alpha = alpha;
+    g.epilogue = epi;
+    return swarm_gemm_bf16(&g, st);
+}
+
+const LayerW& weights(const swarm_stage* s, int l) { return s->layers[s->cfg.shared_layers ? 0 : l]; }
+
+// ---------------------------------------------------------- block forward --
+int block_forward(swarm_stage* s, Act& A, bf16* y, const LayerW& W, cudaStream_t st) {
+    const int T = s->T, d = s->d, H = s->H, dh = s->dh, F = s->F, L = s->L;
+    const bf16* p16 = s->p16;
+    const float* p32 = s->p32;
+    TRY(swarm_layer_norm_forward(A.x, SWARM_DTYPE_BF16, T, d, p32 + W.ln1g, p32 + W.ln1b, 1e-5, A.a, A.mu1, A.rs1, st));
+    TRY(mm(T, 3 * d, d, {A.a, d, T, d, false}, {p16 + W.wqkv, d, 3 * d, d, false}, A.qkv, 3 * d,
+           SWARM_EPI_STORE_BF16, nullptr, 1.f, st));
+    const float scale = 1.f / std::sqrt(static_cast<float>(dh));
+    // S = scale * Q K^T per (b, h)
+    TRY(bmm(s, L, L, dh, {{A.qkv, 3 * d, T, d, false}, L, 0, 0, dh}, {{A.qkv + d, 3 * d, T, d, false}, L, 0, 0, dh},
+            s->S, L, H * L, L, 0, 0, SWARM_EPI_STORE_F32, scale, st));
+    TRY(swarm_attn_softmax_forward(s->S, static_cast<size_t>(s->B) * H * L, L, s->cfg.causal, A.P, st));
+    // O = P V  (V read MN-major straight from the qkv buffer)
+    TRY(bmm(s, L, dh, L, {{A.P, L, s->B * H * L, L, false}, H * L, L, 0, 0},
+            {{A.qkv + 2 * d, 3 * d, T, d, true}, L, 0, 0, dh}, A.o, d, L, 0, 0, dh, SWARM_EPI_STORE_BF16, 1.f, st));
+    // h = x + O Wo^T
+    TRY(mm(T, d, d, {A.o, d, T, d, false}, {p16 + W.wo, d, d, d, false}, A.h, d, SWARM_EPI_RESIDUAL, A.x, 1.f, st));
+    TRY(swarm_layer_norm_forward(A.h, SWARM_DTYPE_BF16, T, d, p32 + W.ln2g, p32 + W.ln2b, 1e-5, A.c, A.mu2, A.rs2, st));
+    // u = c W1^T, g = gelu(u)
+    TRY(mm(T, F, d, {A.c, d, T, d, false}, {p16 + W.w1, d, F, d, false}, A.g, F, SWARM_EPI_GELU, A.u, 1.f, st));
+    // y = h + g W2^T
+    TRY(mm(T, d, F, {A.g, F, T, F, false}, {p16 + W.w2, F, d, F, false}, y, d, SWARM_EPI_RESIDUAL, A.h, 1.f, st));
+    return SWARM_OK;
+}
+
+// --------------------------------------------------------- block backward --
+// dy: gradient w.r.t. the block output; dx: gradient w.r.t. the block input.
+int block_backward(swarm_stage* s, const Act& A, const bf16* dy, bf16* dx, const LayerW& W, cudaStream_t st) {
+    const int T = s->T, d = s->d, H = s->H, dh = s->dh, F = s->F, L = s->L, BHL = s->B * s->H * s->L;
+    const bf16* p16 = s->p16;
+    const float* p32 = s->p32;
+    float* G = s->grad;
+    // MLP: du = (dy W2) * gelu'(u); dW2 += dy^T g; dc = du W1; dW1 += du^T c
+    TRY(mm(T, F, d, {dy, d, T, d, false}, {p16 + W.w2, F, d, F, true}, s->du, F, SWARM_EPI_DGELU, A.u, 1.f, st));
+    TRY(mm(d, F, T, {dy, d, T, d, true}, {A.g, F, T, F, true}, G + W.w2, F, SWARM_EPI_ACCUM_F32, nullptr, 1.f, st));
+    TRY(mm(T, d, F, {s->du, F, T, F, false}, {p16 + W.w1, d, F, d, true}, s->dc, d, SWARM_EPI_STORE_BF16, nullptr, 1.f,
+           st));
+    TRY(mm(F, d, T, {s->du, F, T, F, true}, {A.c, d, T, d, true}, G + W.w1, d, SWARM_EPI_ACCUM_F32, nullptr, 1.f, st));
+    // dh = LN2'(dc) + dy
+    TRY(swarm_layer_norm_backward(s->dc, A.h, SWARM_DTYPE_BF16, T, d, p32 + W.ln2g, A.mu2, A.rs2, dy, s->dhid,
+                                  G + W.ln2g, G + W.ln2b, 1, s->lnws, st));
+    // attention output projection
+    TRY(mm(T, d, d, {s->dhid, d, T, d, false}, {p16 + W.wo, d, d, d, true}, s->dO, d, SWARM_EPI_STORE_BF16, nullptr, 1.f,
+           st));
+    TRY(mm(d, d, T, {s->dhid, d, T, d, true}, {A.o, d, T, d, true}, G + W.wo, d, SWARM_EPI_ACCUM_F32, nullptr, 1.f, st));
+    // dP = dO V^T ; dS = scale * P (dP - rowsum(P dP))
+    TRY(bmm(s, L, L, dh, {{s->dO, d, T, d, false}, L, 0, 0, dh}, {{A.qkv + 2 * d, 3 * d, T, d, false}, L, 0, 0, dh},
+            s->dP, L, H * L, L, 0, 0, SWARM_EPI_STORE_F32, 1.f, st));
+    const float scale = 1.f / std::sqrt(static_cast<float>(dh));
+    TRY(swarm_attn_softmax_backward(A.P, s->dP, BHL, L, scale, s->dS, st));
+    // dQ = dS K ; dK = dS^T Q ; dV = P^T dO   (all read in place, written into dqkv)
+    TRY(bmm(s, L, dh, L, {{s->dS, L, BHL, L, false}, H * L, L, 0, 0}, {{A.qkv + d, 3 * d, T, d, true}, L, 0, 0, dh},
+            s->dqkv, 3 * d, L, 0, 0, dh, SWARM_EPI_STORE_BF16, 1.f, st));
+    TRY(bmm(s, L, dh, L, {{s->dS, L, BHL, L, true}, H * L, L, 0, 0}, {{A.qkv, 3 * d, T, d, true}, L, 0, 0, dh},
+            s->dqkv + d, 3 * d, L, 0, 0, dh, SWARM_EPI_STORE_BF16, 1.f, st));
+    TRY(bmm(s, L, dh, L, {{A.P, L, BHL, L, true}, H * L, L, 0, 0}, {{s->dO, d, T, d, true}, L, 0, 0, dh},
+            s->dqkv + 2 * d, 3 * d, L, 0, 0, dh, SWARM_EPI_STORE_BF16, 1.f, st));
+    // da = dqkv Wqkv ; dWqkv += dqkv^T a
+    TRY(mm(T, d, 3 * d, {s->dqkv, 3 * d, T, 3 * d, false}, {p16 + W.wqkv, d, 3 * d, d, true}, s->da, d,
+           SWARM_EPI_STORE_BF16, nullptr, 1.f, st));
+    TRY(mm(3 * d, d, T, {s->dqkv, 3 * d, T, 3 * d, true}, {A.a, d, T, d, true}, G + W.wqkv, d, SWARM_EPI_ACCUM_F32,
+           nullptr, 1.f, st));
+    // dx = LN1'(da) + dh
+    TRY(swarm_layer_norm_backward(s->da, A.x, SWARM_DTYPE_BF16, T, d, p32 + W.ln1g, A.mu1, A.rs1, s->dhid, dx,
+                                  G + W.ln1g, G + W.ln1b, 1, s->lnws, st));
+    return SWARM_OK;
+}
+
+size_t wire_bytes(const swarm_stage* s) {
+    const size_t n = static_cast<size_t>(s->T) * s->d;
+    if (s->cfg.wire == SWARM_WIRE_INT8) {
+        const size_t bs = static_cast<size_t>(s->cfg.block_size);
+        return ((n + 15) & ~size_t(15)) + ((n + bs - 1) / bs) * sizeof(float);
+    }
+    return n * 2;
+}
+
+int wire_decode(swarm_stage* s, const void* msg, bf16* out, cudaStream_t st) {
+    const size_t n = static_cast<size_t>(s->T) * s->d;
+    if (s->cfg.wire == SWARM_WIRE_INT8) {
+        const int8_t* codes = static_cast<const int8_t*>(msg);
+        const void* scales = static_cast<const char*>(msg) + ((n + 15) & ~size_t(15));
+        return swarm_dequantize_blockwise(codes, scales, SWARM_DTYPE_F32, n, s->cfg.block_size, out, SWARM_DTYPE_BF16,
+                                          st);
+    }
+    const cudaError_t e = cudaMemcpyAsync(out, msg, n * 2, cudaMemcpyDeviceToDevice, st);
+    return e == cudaSuccess ? SWARM_OK : SWARM_E_CUDA;
+}
+
+int wire_encode(swarm_stage* s, const bf16* x, void* msg, cudaStream_t st) {
+    const size_t n = static_cast<size_t>(s->T) * s->d;
+    if (s->cfg.wire == SWARM_WIRE_INT8) {
+        int8_t* codes = static_cast<int8_t*>(msg);
+        void* scales = static_cast<char*>(msg) + ((n + 15) & ~size_t(15));
+        return swarm_quantize_blockwise(x, SWARM_DTYPE_BF16, n, s->cfg.block_size, codes, scales, nullptr, st);
+    }
+    const cudaError_t e = cudaMemcpyAsync(msg, x, n * 2, cudaMemcpyDeviceToDevice, st);
+    return e == cudaSuccess ? SWARM_OK : SWARM_E_CUDA;
+}
+
+int init_params(swarm_stage* s, cudaStream_t st) {
+    const uint64_t base = s->cfg.seed * 1000003ull;
+    if (cudaMemsetAsync(s->p32, 0, s->nparams * 4, st) != cudaSuccess) return SWARM_E_CUDA;  // alignment padding
+    for (size_t i = 0; i < s->tensors.size(); ++i) {
+        const auto& t = s->tensors[i];
+        const size_t n = t.rows * t.cols;
+        const bool is_gain = t.name.find("_g") != std::string::npos && t.rows == 1;
+        const bool is_bias = t.name.find("_b") != std::string::npos && t.rows == 1;
+        const float mean = is_gain ? 1.f : 0.f;
+        const float stdv = (is_gain || is_bias) ? 0.f : s->cfg.init_std;
+        TRY(swarm_fill_normal(s->p32 + t.off, n, mean, stdv, base + i, st));
+    }
+    TRY(swarm_cast_f32_bf16(s->p32, s->p16, s->nparams, st));
+    if (cudaMemsetAsync(s->grad, 0, s->nparams * 4, st) != cudaSuccess ||
+        cudaMemsetAsync(s->m, 0, s->nparams * 4, st) != cudaSuccess ||
+        cudaMemsetAsync(s->v, 0, s->nparams * 4, st) != cudaSuccess)
+        return SWARM_E_CUDA;
+    return SWARM_OK;
+}
+
+int create(const swarm_stage_config* c, swarm_stage* s) {
+    s->cfg = *c;
+    s->d = c->d_model;
+    s->H = c->n_heads;
+    s->F = c->d_ffn;
+    s->L = c->seq_len;
+    s->B = c->micro_batch;
+    s->V = c->vocab;
+    s->T = s->B * s->L;
+    if (s->d <= 0 || s->H <= 0 || s->d % s->H || s->F <= 0 || s->L <= 0 || s->B <= 0 || c->n_layers <= 0 ||
+        c->max_slots <= 0)
+        return fail("stage: bad shape");
+    s->dh = s->d / s->H;
+    if (s->d % 64 || s->F % 64 || s->dh % 64 || s->L % 64) return fail("stage: d, d_ffn, d_head, seq_len must be multiples of 64");
+    if (s->L > 1024) return fail("stage: seq_len > 1024 unsupported");
+    if ((c->is_first || c->is_last) && (s->V <= 0 || s->V % 8)) return fail("stage: vocab must be a positive multiple of 8");
+    if (c->wire == SWARM_WIRE_INT8 && c->block_size <= 0) return fail("stage: block_size must be positive");
+    const int d = s->d, F = s->F;
+    // parameter layout
+    if (c->is_first) s->emb = add_tensor(s, "embedding", s->V, d);
+    const int nw = c->shared_layers ? 1 : c->n_layers;
+    for (int l = 0; l < nw; ++l) {
+        const std::string p = "layer" + std::to_string(l) + ".";
+        LayerW w{};
+        w.wqkv = add_tensor(s, p + "wqkv", 3 * d, d);
+        w.wo = add_tensor(s, p + "wo", d, d);
+        w.w1 = add_tensor(s, p + "w1", F, d);
+        w.w2 = add_tensor(s, p + "w2", d, F);
+        w.ln1g = add_tensor(s, p + "ln1_g", 1, d);
+        w.ln1b = add_tensor(s, p + "ln1_b", 1, d);
+        w.ln2g = add_tensor(s, p + "ln2_g", 1, d);
+        w.ln2b = add_tensor(s, p + "ln2_b", 1, d);
+        s->layers.push_back(w);
+    }
+    if (c->is_last) {
+        s->lnfg = add_tensor(s, "lnf_g", 1, d);
+        s->lnfb = add_tensor(s, "lnf_b", 1, d);
+        s->head = add_tensor(s, "head", s->V, d);
+    }
+    TRY(alloc(s, &s->p32, s->nparams));
+    TRY(alloc(s, &s->grad, s->nparams));
+    TRY(alloc(s, &s->m, s->nparams));
+    TRY(alloc(s, &s->v, s->nparams));
+    TRY(alloc(s, &s->p16, s->nparams));
+    // activation slots
+    const size_t T = s->T, Td = T * d, TF = T * F, BHLL = static_cast<size_t>(s->B) * s->H * s->L * s->L;
+    s->slots.resize(c->max_slots);
+    for (auto& sl : s->slots) {
+        sl.layer.resize(c->n_layers);
+        for (auto& A : sl.layer) {
+            TRY(alloc(s, &A.x, Td));
+            TRY(alloc(s, &A.a, Td));
+            TRY(alloc(s, &A.qkv, 3 * Td));
+            TRY(alloc(s, &A.P, BHLL));
+            TRY(alloc(s, &A.o, Td));
+            TRY(alloc(s, &A.h, Td));
+            TRY(alloc(s, &A.c, Td));
+            TRY(alloc(s, &A.u, TF));
+            TRY(alloc(s, &A.g, TF));
+            TRY(alloc(s, &A.mu1, T));
+            TRY(alloc(s, &A.rs1, T));
+            TRY(alloc(s, &A.mu2, T));
+            TRY(alloc(s, &A.rs2, T));
+        }
+        TRY(alloc(s, &sl.out, Td));
+        if (c->is_last) {
+            TRY(alloc(s, &sl.xf, Td));
+            TRY(alloc(s, &sl.muf, T));
+            TRY(alloc(s, &sl.rsf, T));
+            TRY(alloc(s, &sl.dxf, Td));
+        }
+        if (c->is_first) TRY(alloc(s, &sl.tokens, T));
+    }
+    // workspaces
+    TRY(alloc(s, &s->S, BHLL));
+    TRY(alloc(s, &s->dP, BHLL));
+    TRY(alloc(s, &s->dS, BHLL));
+    TRY(alloc(s, &s->gy[0], Td));
+    TRY(alloc(s, &s->gy[1], Td));
+    TRY(alloc(s, &s->dhid, Td));
+    TRY(alloc(s, &s->dc, Td));
+    TRY(alloc(s, &s->du, TF));
+    TRY(alloc(s, &s->dqkv, 3 * Td));
+    TRY(alloc(s, &s->dO, Td));
+    TRY(alloc(s, &s->da, Td));
+    TRY(dmalloc(s, &s->lnws, swarm_layer_norm_backward_workspace(T, d)));
+    if (c->is_last) {
+        TRY(alloc(s, &s->logits, T * s->V));
+        TRY(alloc(s, &s->dlogits, T * s->V));
+    }
+    TRY(init_params(s, nullptr));
+    if (cudaStreamSynchronize(nullptr) != cudaSuccess) return SWARM_E_CUDA;
+    return SWARM_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int swarm_stage_create(const swarm_stage_config* cfg, swarm_stage_t* out) {
+    if (!cfg || !out) return fail("stage: null argument");
+    auto* s = new (std::nothrow) swarm_stage;
+    if (!s) return fail("stage: out of host memory");
+    const int rc = create(cfg, s);
+    if (rc != SWARM_OK) {
+        swarm_stage_destroy(s);
+        return rc;
+    }
+    *out = s;
+    return SWARM_OK;
+}
+
+void swarm_stage_destroy(swarm_stage_t s) {
+    if (!s) return;
+    cudaDeviceSynchronize();
+    for (void* p : s->allocations) cudaFree(p);
+    delete s;
+}
+
+size_t swarm_stage_wire_bytes(swarm_stage_t s) { return wire_bytes(s); }
+size_t swarm_stage_num_params(swarm_stage_t s) { return s->nparams; }
+float* swarm_stage_grads(swarm_stage_t s) { return s->grad; }
+float* swarm_stage_params(swarm_stage_t s) { return s->p32; }
+void* swarm_stage_params_bf16(swarm_stage_t s) { return s->p16; }
+
+int swarm_stage_sync_shadow(swarm_stage_t s, swarm_stream_t stream) {
+    return swarm_cast_f32_bf16(s->p32, s->p16, s->nparams, stream);
+}
+
+int swarm_stage_param_info(swarm_stage_t s, int index, const char** name, size_t* offset, size_t* rows, size_t* cols) {
+    if (index < 0 || index >= static_cast<int>(s->tensors.size())) return SWARM_E_INVALID;
+    const auto& t = s->tensors[index];
+    if (name) *name = t.name.c_str();
+    if (offset) *offset = t.off;
+    if (rows) *rows = t.rows;
+    if (cols) *cols = t.cols;
+    return SWARM_OK;
+}
+
+int swarm_stage_activation(swarm_stage_t s, int slot, int layer, const char* name, void** ptr, size_t* numel) {
+    if (slot < 0 || slot >= static_cast<int>(s->slots.size())) return fail("activation: bad slot");
+    Slot& sl = s->slots[slot];
+    const size_t Td = static_cast<size_t>(s->T) * s->d;
+    const std::string n = name ? name : "";
+    if (n == "out") return *ptr = sl.out, *numel = Td, SWARM_OK;
+    if (n == "xf") return *ptr = sl.xf, *numel = sl.xf ? Td : 0, SWARM_OK;
+    if (n == "dxf") return *ptr = sl.dxf, *numel = sl.dxf ? Td : 0, SWARM_OK;
+    if (layer < 0 || layer >= static_cast<int>(sl.layer.size())) return fail("activation: bad layer");
+    Act& A = sl.layer[layer];
+    const size_t TF = static_cast<size_t>(s->T) * s->F;
+    struct {
+        const char* k;
+        void* p;
+        size_t n;
+    } table[] = {{"x", A.x, Td}, {"a", A.a, Td}, {"qkv", A.qkv, 3 * Td},
+                 {"P", A.P, static_cast<size_t>(s->B) * s->H * s->L * s->L},
+                 {"o", A.o, Td}, {"h", A.h, Td}, {"c", A.c, Td}, {"u", A.u, TF}, {"g", A.g, TF}};
+    for (auto& e : table)
+        if (n == e.k) return *ptr = e.p, *numel = e.n, SWARM_OK;
+    return fail("activation: unknown name " + n);
+}
+
+int swarm_stage_forward(swarm_stage_t s, int slot, const void* in, const int32_t* targets, void* out, float* loss_sum,
+                        float loss_scale, swarm_stream_t stream) {
+    if (slot < 0 || slot >= static_cast<int>(s->slots.size())) return fail("forward: bad slot");
+    if (!in) return fail("forward: null input");
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    Slot& sl = s->slots[slot];
+    const int T = s->T, d = s->d, n = s->cfg.n_layers;
+    if (s->cfg.is_first) {
+        if (cudaMemcpyAsync(sl.tokens, in, T * sizeof(int32_t), cudaMemcpyDeviceToDevice, st) != cudaSuccess)
+            return SWARM_E_CUDA;
+        TRY(swarm_embedding_forward(sl.tokens, T, s->p16 + s->emb, s->V, d, sl.layer[0].x, st));
+    } else {
+        TRY(wire_decode(s, in, sl.layer[0].x, st));
+    }
+    for (int l = 0; l < n; ++l) {
+        bf16* y = (l + 1 < n) ? sl.layer[l + 1].x : sl.out;
+        TRY(block_forward(s, sl.layer[l], y, weights(s, l), st));
+    }
+    if (!s->cfg.is_last) {
+        if (!out) return fail("forward: null output message");
+        return wire_encode(s, sl.out, out, st);
+    }
+    if (!targets) return fail("forward: last stage needs targets");
+    // final LN + LM head + cross-entropy, with the head's backward fused in
+    TRY(swarm_layer_norm_forward(sl.out, SWARM_DTYPE_BF16, T, d, s->p32 + s->lnfg, s->p32 + s->lnfb, 1e-5, sl.xf,
+                                 sl.muf, sl.rsf, st));
+    TRY(mm(T, s->V, d, {sl.xf, d, T, d, false}, {s->p16 + s->head, d, s->V, d, false}, s->logits, s->V,
+           SWARM_EPI_STORE_F32, nullptr, 1.f, st));
+    TRY(swarm_cross_entropy(s->logits, targets, T, s->V, loss_scale, loss_sum, s->dlogits, st));
+    TRY(mm(s->V, d, T, {s->dlogits, s->V, T, s->V, true}, {sl.xf, d, T, d, true}, s->grad + s->head, d,
+           SWARM_EPI_ACCUM_F32, nullptr, 1.f, st));
+    TRY(mm(T, d, s->V, {s->dlogits, s->V, T, s->V, false}, {s->p16 + s->head, d, s->V, d, true}, sl.dxf, d,
+           SWARM_EPI_STORE_BF16, nullptr, 1.f, st));
+    return SWARM_OK;
+}
+
+int swarm_stage_backward(swarm_stage_t s, int slot, const void* grad_in, void* grad_out, swarm_stream_t stream) {
+    if (slot < 0 || slot >= static_cast<int>(s->slots.size())) return fail("backward: bad slot");
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    Slot& sl = s->slots[slot];
+    const int T = s->T, d = s->d, n = s->cfg.n_layers;
+    int cur = 0;
+    if (s->cfg.is_last) {
+        TRY(swarm_layer_norm_backward(sl.dxf, sl.out, SWARM_DTYPE_BF16, T, d, s->p32 + s->lnfg, sl.muf, sl.rsf, nullptr,
+                                      s->gy[0], s->grad + s->lnfg, s->grad + s->lnfb, 1, s->lnws, st));
+    } else {
+        if (!grad_in) return fail("backward: null gradient message");
+        TRY(wire_decode(s, grad_in, s->gy[0], st));
+    }
+    for (int l = n - 1; l >= 0; --l) {
+        TRY(block_backward(s, sl.layer[l], s->gy[cur], s->gy[cur ^ 1], weights(s, l), st));
+        cur ^= 1;
+    }
+    if (s->cfg.is_first) return swarm_embedding_backward(sl.tokens, T, s->gy[cur], s->V, d, s->grad + s->emb, st);
+    if (!grad_out) return fail("backward: null output gradient message");
+    return wire_encode(s, s->gy[cur], grad_out, st);
+}
+
+int swarm_stage_optimizer_step(swarm_stage_t s, float grad_scale, swarm_stream_t stream) {
+    s->step += 1;
+    const auto& c = s->cfg;
+    return swarm_adamw_step(s->p32, s->p16, s->grad, s->m, s->v, s->nparams, c.lr, c.beta1, c.beta2, c.eps,
+                            c.weight_decay, s->step, grad_scale, 1, stream);
+}
+
+}  // extern "C"

@@ -1,0 +1,300 @@
+// Training building blocks around the GEMMs of the stage executor (sm_100a):
+// token embedding, attention softmax forward/backward, fused LM-head
+// cross-entropy, fused AdamW over the flat parameter arena, and init.
+// All are bandwidth-bound; each touches its operands once with coalesced,
+// vectorised accesses where the layout allows.
+#include <algorithm>
+#include <cmath>
+
+#include "common.cuh"
+
+namespace swarm {
+namespace {
+
+unsigned grid_for(size_t work, unsigned per_block, unsigned cap = 148u * 32u) {
+    const size_t g = (work + per_block - 1) / per_block;
+    return static_cast<unsigned>(std::max<size_t>(1, std::min<size_t>(g, cap)));
+}
+
+__device__ __forceinline__ float warp_max(float v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+    return v;
+}
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+// ------------------------------------------------------------- embedding --
+__global__ void k_embed_fwd(const int32_t* __restrict__ tok, int n, const uint4* __restrict__ table, int vocab,
+                            int d8, uint4* __restrict__ out) {
+    const int warps = (gridDim.x * blockDim.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    for (int t = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; t < n; t += warps) {
+        const int id = tok[t];
+        const bool ok = id >= 0 && id < vocab;
+        for (int c = lane; c < d8; c += 32)
+            out[static_cast<size_t>(t) * d8 + c] = ok ? table[static_cast<size_t>(id) * d8 + c] : make_uint4(0, 0, 0, 0);
+    }
+}
+
+__global__ void k_embed_bwd(const int32_t* __restrict__ tok, int n, const __nv_bfloat16* __restrict__ dout,
+                            int vocab, int d, float* __restrict__ dtable) {
+    const int warps = (gridDim.x * blockDim.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    for (int t = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; t < n; t += warps) {
+        const int id = tok[t];
+        if (id < 0 || id >= vocab) continue;
+        for (int c = lane; c < d; c += 32)
+            atomicAdd(dtable + static_cast<size_t>(id) * d + c, __bfloat162float(dout[static_cast<size_t>(t) * d + c]));
+    }
+}
+
+// --------------------------------------------------------------- softmax --
+constexpr int kMaxLPerLane = 32;  // L <= 1024
+
+__global__ void k_softmax_fwd(const float* __restrict__ S, int rows, int L, int causal,
+                              __nv_bfloat16* __restrict__ P) {
+    const int warps = (gridDim.x * blockDim.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    const float log2e = 1.4426950408889634f;
+    for (int row = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; row < rows; row += warps) {
+        const float* s = S + static_cast<size_t>(row) * L;
+        const int qi = row % L;
+        float v[kMaxLPerLane];
+        float m = -INFINITY;
+#pragma unroll
+        for (int k = 0; k < kMaxLPerLane; ++k) {
+            const int j = k * 32 + lane;
+            float x = -INFINITY;
+            if (j < L) {
+                x = s[j];
+                if (causal && j > qi) x = -INFINITY;
+            }
+            v[k] = x;
+            m = fmaxf(m, x);
+        }
+        m = warp_max(m);
+        float sum = 0.f;
+#pragma unroll
+        for (int k = 0; k < kMaxLPerLane; ++k) {
+            const float e = (v[k] == -INFINITY) ? 0.f : exp2f((v[k] - m) * log2e);
+            v[k] = e;
+            sum += e;
+        }
+        const float inv = 1.f / warp_sum(sum);
+        __nv_bfloat16* p = P + static_cast<size_t>(row) * L;
+#pragma unroll
+        for (int k = 0; k < kMaxLPerLane; ++k) {
+            const int j = k * 32 + lane;
+            if (j < L) p[j] = __float2bfloat16_rn(v[k] * inv);
+        }
+    }
+}
+
+__global__ void k_softmax_bwd(const __nv_bfloat16* __restrict__ P, const float* __restrict__ dP, int rows, int L,
+                              float scale, __nv_bfloat16* __restrict__ dS) {
+    const int warps = (gridDim.x * blockDim.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    for (int row = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; row < rows; row += warps) {
+        const size_t base = static_cast<size_t>(row) * L;
+        float p[kMaxLPerLane], g[kMaxLPerLane];
+        float acc = 0.f;
+#pragma unroll
+        for (int k = 0; k < kMaxLPerLane; ++k) {
+            const int j = k * 32 + lane;
+            p[k] = j < L ? __bfloat162float(P[base + j]) : 0.f;
+            g[k] = j < L ? dP[base + j] : 0.f;
+            acc += p[k] * g[k];
+        }
+        acc = warp_sum(acc);
+#pragma unroll
+        for (int k = 0; k < kMaxLPerLane; ++k) {
+            const int j = k * 32 + lane;
+            if (j < L) dS[base + j] = __float2bfloat16_rn(scale * p[k] * (g[k] - acc));
+        }
+    }
+}
+
+// ---------------------------------------------------------- cross-entropy --
+constexpr int kCeThreads = 512;
+
+__global__ void __launch_bounds__(kCeThreads) k_cross_entropy(const float* __restrict__ logits,
+                                                              const int32_t* __restrict__ targets, int vocab,
+                                                              float grad_scale, float* __restrict__ loss_sum,
+                                                              __nv_bfloat16* __restrict__ dlogits) {
+    __shared__ float sm[kCeThreads / 32], ss[kCeThreads / 32];
+    const int row = blockIdx.x;
+    const float* x = logits + static_cast<size_t>(row) * vocab;
+    float m = -INFINITY, s = 0.f;
+    for (int j = threadIdx.x; j < vocab; j += kCeThreads) {
+        const float v = x[j];
+        if (v > m) {
+            s = s * __expf(m - v) + 1.f;
+            m = v;
+        } else {
+            s += __expf(v - m);
+        }
+    }
+    // combine (m, s) pairs: warp then block
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        const float m2 = __shfl_xor_sync(0xffffffffu, m, o), s2 = __shfl_xor_sync(0xffffffffu, s, o);
+        const float mm = fmaxf(m, m2);
+        s = (mm == -INFINITY) ? 0.f : s * __expf(m - mm) + s2 * __expf(m2 - mm);
+        m = mm;
+    }
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (lane == 0) {
+        sm[warp] = m;
+        ss[warp] = s;
+    }
+    __syncthreads();
+    float M = -INFINITY;
+    for (int w = 0; w < kCeThreads / 32; ++w) M = fmaxf(M, sm[w]);
+    float Ssum = 0.f;
+    for (int w = 0; w < kCeThreads / 32; ++w) Ssum += ss[w] * __expf(sm[w] - M);
+    const float lse = M + logf(Ssum);
+    const int tgt = targets[row];
+    if (threadIdx.x == 0 && loss_sum) atomicAdd(loss_sum, lse - x[tgt]);
+    if (dlogits) {
+        __nv_bfloat16* d = dlogits + static_cast<size_t>(row) * vocab;
+        for (int j = threadIdx.x; j < vocab; j += kCeThreads) {
+            const float p = __expf(x[j] - lse);
+            d[j] = __float2bfloat16_rn(grad_scale * (p - (j == tgt ? 1.f : 0.f)));
+        }
+    }
+}
+
+// ------------------------------------------------------------------ AdamW --
+__global__ void k_adamw(float* __restrict__ p32, __nv_bfloat16* __restrict__ p16, float* __restrict__ grad,
+                        float* __restrict__ m, float* __restrict__ v, size_t n, float lr, float b1, float b2,
+                        float eps, float wd, float bc1, float bc2, float gscale, int zero_grad) {
+    for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<size_t>(gridDim.x) * blockDim.x) {
+        const float g = grad[i] * gscale;
+        const float mi = b1 * m[i] + (1.f - b1) * g;
+        const float vi = b2 * v[i] + (1.f - b2) * g * g;
+        m[i] = mi;
+        v[i] = vi;
+        float p = p32[i];
+        p -= lr * ((mi / bc1) / (sqrtf(vi / bc2) + eps) + wd * p);
+        p32[i] = p;
+        if (p16) p16[i] = __float2bfloat16_rn(p);
+        if (zero_grad) grad[i] = 0.f;
+    }
+}
+
+// ------------------------------------------------------------------- init --
+__device__ __forceinline__ uint64_t splitmix64(uint64_t x) {
+    x += 0x9E3779B97F4A7C15ull;
+    x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
+    x = (x ^ (x >> 27)) * 0x94D049BB133111EBull;
+    return x ^ (x >> 31);
+}
+
+__global__ void k_fill_normal(float* __restrict__ p, size_t n, float mean, float stdv, uint64_t seed) {
+    for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<size_t>(gridDim.x) * blockDim.x) {
+        const uint64_t r = splitmix64(seed * 0xD1B54A32D192ED03ull + i);
+        const float u1 = (static_cast<float>(r >> 40) + 1.f) * (1.f / 16777217.f);  // (0,1]
+        const float u2 = static_cast<float>((r >> 16) & 0xffffffull) * (1.f / 16777216.f);
+        p[i] = mean + stdv * sqrtf(-2.f * logf(u1)) * cospif(2.f * u2);
+    }
+}
+
+__global__ void k_cast(const float* __restrict__ in, __nv_bfloat16* __restrict__ out, size_t n) {
+    for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<size_t>(gridDim.x) * blockDim.x)
+        out[i] = __float2bfloat16_rn(in[i]);
+}
+
+}  // namespace
+}  // namespace swarm
+
+using namespace swarm;
+
+extern "C" {
+
+int swarm_embedding_forward(const int32_t* tokens, size_t n, const void* table, size_t vocab, size_t d, void* out,
+                            swarm_stream_t stream) {
+    if (d % 8) return invalid("embedding: d must be a multiple of 8");
+    if (n == 0) return SWARM_OK;
+    k_embed_fwd<<<grid_for(n * 32, 256), 256, 0, as_stream(stream)>>>(
+        tokens, static_cast<int>(n), static_cast<const uint4*>(table), static_cast<int>(vocab),
+        static_cast<int>(d / 8), static_cast<uint4*>(out));
+    SWARM_LAUNCH_CHECK("k_embed_fwd");
+    return SWARM_OK;
+}
+
+int swarm_embedding_backward(const int32_t* tokens, size_t n, const void* dout, size_t vocab, size_t d, float* dtable,
+                             swarm_stream_t stream) {
+    if (n == 0) return SWARM_OK;
+    k_embed_bwd<<<grid_for(n * 32, 256), 256, 0, as_stream(stream)>>>(
+        tokens, static_cast<int>(n), static_cast<const __nv_bfloat16*>(dout), static_cast<int>(vocab),
+        static_cast<int>(d), dtable);
+    SWARM_LAUNCH_CHECK("k_embed_bwd");
+    return SWARM_OK;
+}
+
+int swarm_attn_softmax_forward(const float* s, size_t rows, size_t L, int causal, void* p, swarm_stream_t stream) {
+    if (L == 0 || L > 32 * kMaxLPerLane) return invalid("attn softmax: L must be in [1, 1024]");
+    if (rows == 0) return SWARM_OK;
+    k_softmax_fwd<<<grid_for(rows * 32, 256), 256, 0, as_stream(stream)>>>(
+        s, static_cast<int>(rows), static_cast<int>(L), causal, static_cast<__nv_bfloat16*>(p));
+    SWARM_LAUNCH_CHECK("k_softmax_fwd");
+    return SWARM_OK;
+}
+
+int swarm_attn_softmax_backward(const void* p, const float* dp, size_t rows, size_t L, float scale, void* ds,
+                                swarm_stream_t stream) {
+    if (L == 0 || L > 32 * kMaxLPerLane) return invalid("attn softmax bwd: L must be in [1, 1024]");
+    if (rows == 0) return SWARM_OK;
+    k_softmax_bwd<<<grid_for(rows * 32, 256), 256, 0, as_stream(stream)>>>(
+        static_cast<const __nv_bfloat16*>(p), dp, static_cast<int>(rows), static_cast<int>(L), scale,
+        static_cast<__nv_bfloat16*>(ds));
+    SWARM_LAUNCH_CHECK("k_softmax_bwd");
+    return SWARM_OK;
+}
+
+int swarm_cross_entropy(const float* logits, const int32_t* targets, size_t rows, size_t vocab, float grad_scale,
+                        float* loss_sum, void* dlogits, swarm_stream_t stream) {
+    if (vocab == 0) return invalid("cross_entropy: empty vocab");
+    if (rows == 0) return SWARM_OK;
+    k_cross_entropy<<<static_cast<unsigned>(rows), kCeThreads, 0, as_stream(stream)>>>(
+        logits, targets, static_cast<int>(vocab), grad_scale, loss_sum, static_cast<__nv_bfloat16*>(dlogits));
+    SWARM_LAUNCH_CHECK("k_cross_entropy");
+    return SWARM_OK;
+}
+
+int swarm_adamw_step(float* p32, void* p16, float* grad, float* m, float* v, size_t n, float lr, float beta1,
+                     float beta2, float eps, float weight_decay, int step, float grad_scale, int zero_grad,
+                     swarm_stream_t stream) {
+    if (step < 1) return invalid("adamw: step must be >= 1");
+    if (n == 0) return SWARM_OK;
+    const float bc1 = 1.f - std::pow(beta1, static_cast<float>(step));
+    const float bc2 = 1.f - std::pow(beta2, static_cast<float>(step));
+    k_adamw<<<grid_for(n, 256, 148u * 16u), 256, 0, as_stream(stream)>>>(
+        p32, static_cast<__nv_bfloat16*>(p16), grad, m, v, n, lr, beta1, beta2, eps, weight_decay, bc1, bc2,
+        grad_scale, zero_grad);
+    SWARM_LAUNCH_CHECK("k_adamw");
+    return SWARM_OK;
+}
+
+int swarm_fill_normal(float* p, size_t n, float mean, float stdv, uint64_t seed, swarm_stream_t stream) {
+    if (n == 0) return SWARM_OK;
+    k_fill_normal<<<grid_for(n, 256), 256, 0, as_stream(stream)>>>(p, n, mean, stdv, seed);
+    SWARM_LAUNCH_CHECK("k_fill_normal");
+    return SWARM_OK;
+}
+
+int swarm_cast_f32_bf16(const float* in, void* out, size_t n, swarm_stream_t stream) {
+    if (n == 0) return SWARM_OK;
+    k_cast<<<grid_for(n, 256), 256, 0, as_stream(stream)>>>(in, static_cast<__nv_bfloat16*>(out), n);
+    SWARM_LAUNCH_CHECK("k_cast");
+    return SWARM_OK;
+}
+
+}  // extern "C"

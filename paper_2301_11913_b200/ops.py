@@ -109,7 +109,7 @@ def layer_norm(x: torch.Tensor, gain: torch.Tensor | None = None, bias: torch.Te
 
 
 def layer_norm_backward(dy: torch.Tensor, x: torch.Tensor, gain: torch.Tensor | None, mean: torch.Tensor,
-                        rstd: torch.Tensor, dx: torch.Tensor | None = None):
+                        rstd: torch.Tensor, dx: torch.Tensor | None = None, dres: torch.Tensor | None = None):
     _dev(dy, "dy")
     _dev(x, "x")
     cols = x.shape[-1]
@@ -120,7 +120,8 @@ def layer_norm_backward(dy: torch.Tensor, x: torch.Tensor, gain: torch.Tensor | 
     db = torch.empty(cols, dtype=torch.float32, device=x.device)
     ws = torch.empty(L.lib().swarm_layer_norm_backward_workspace(rows, cols), dtype=torch.uint8, device=x.device)
     rc = L.lib().swarm_layer_norm_backward(_ptr(dy), _ptr(x), _DT[x.dtype], rows, cols, _ptr(gain), _ptr(mean),
-                                           _ptr(rstd), _ptr(dx), _ptr(dg), _ptr(db), _ptr(ws), _stream())
+                                           _ptr(rstd), _ptr(dres), _ptr(dx), _ptr(dg), _ptr(db), 0, _ptr(ws),
+                                           _stream())
     L.check(rc, "layer_norm_backward")
     return dx, dg, db
 

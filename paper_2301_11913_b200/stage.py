@@ -1,0 +1,153 @@
+"""Python handle of the C++ stage executor (include/swarm_b200.h, csrc/stage.cpp).
+
+A Stage is one SWARM pipeline stage resident on the current CUDA device.  The
+executor owns its weights / optimizer state / activation slots; callers own
+the wire messages that cross stage boundaries (torch uint8 tensors here) and
+drive visits on a CUDA stream.  torch only supplies memory for the messages,
+streams and NCCL; all math runs in libswarm_b200.so.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, fields
+
+import torch
+
+from . import _lib as L
+
+WIRE_BF16, WIRE_INT8 = 0, 1
+
+
+@dataclass
+class StageConfig:
+    d_model: int = 256
+    n_heads: int = 4
+    d_ffn: int = 1024
+    seq_len: int = 128
+    micro_batch: int = 8
+    n_layers: int = 2
+    shared_layers: int = 0
+    vocab: int = 512
+    is_first: int = 1
+    is_last: int = 1
+    causal: int = 1
+    max_slots: int = 1
+    wire: int = WIRE_INT8
+    block_size: int = 4096
+    lr: float = 1e-4
+    beta1: float = 0.9
+    beta2: float = 0.95
+    eps: float = 1e-8
+    weight_decay: float = 0.0
+    init_std: float = 0.02
+    seed: int = 0
+
+    def to_c(self) -> L.StageConfigC:
+        c = L.StageConfigC()
+        for f in fields(self):
+            setattr(c, f.name, getattr(self, f.name))
+        return c
+
+    @property
+    def tokens(self) -> int:
+        return self.micro_batch * self.seq_len
+
+
+class _CAI:
+    """__cuda_array_interface__ view of executor-owned device memory (zero-copy)."""
+
+    def __init__(self, ptr: int, n: int, typestr: str):
+        self.__cuda_array_interface__ = {"shape": (n,), "typestr": typestr, "data": (ptr, False), "version": 3,
+                                         "strides": None}
+
+
+def device_view(ptr: int, n: int, dtype: torch.dtype, device: torch.device) -> torch.Tensor:
+    if dtype == torch.bfloat16:
+        return torch.as_tensor(_CAI(ptr, n, "<i2"), device=device).view(torch.bfloat16)
+    ts = {torch.float32: "<f4", torch.int32: "<i4", torch.uint8: "|u1"}[dtype]
+    return torch.as_tensor(_CAI(ptr, n, ts), device=device)
+
+
+def _stream(stream: torch.cuda.Stream | None):
+    return (stream or torch.cuda.current_stream()).cuda_stream
+
+
+class Stage:
+    def __init__(self, cfg: StageConfig, device: torch.device | None = None):
+        self.cfg = cfg
+        self.device = device or torch.device("cuda", torch.cuda.current_device())
+        self.lib = L.lib()
+        h = C.c_void_p()
+        with torch.cuda.device(self.device):
+            L.check(self.lib.swarm_stage_create(C.byref(cfg.to_c()), C.byref(h)), "stage_create")
+        self.h = h
+        self.n_params = int(self.lib.swarm_stage_num_params(h))
+        self.wire_bytes = int(self.lib.swarm_stage_wire_bytes(h))
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.lib.swarm_stage_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # -- messages ------------------------------------------------------------
+    def new_wire(self) -> torch.Tensor:
+        return torch.empty(self.wire_bytes, dtype=torch.uint8, device=self.device)
+
+    # -- visits ---------------------------------------------------------------
+    def forward(self, slot: int, inp: torch.Tensor, out: torch.Tensor | None = None, targets: torch.Tensor | None = None,
+                loss_sum: torch.Tensor | None = None, loss_scale: float = 1.0, stream=None) -> None:
+        rc = self.lib.swarm_stage_forward(self.h, slot, inp.data_ptr(), None if targets is None else targets.data_ptr(),
+                                          None if out is None else out.data_ptr(),
+                                          None if loss_sum is None else loss_sum.data_ptr(), loss_scale,
+                                          _stream(stream))
+        L.check(rc, "stage_forward")
+
+    def backward(self, slot: int, grad_in: torch.Tensor | None = None, grad_out: torch.Tensor | None = None,
+                 stream=None) -> None:
+        rc = self.lib.swarm_stage_backward(self.h, slot, None if grad_in is None else grad_in.data_ptr(),
+                                           None if grad_out is None else grad_out.data_ptr(), _stream(stream))
+        L.check(rc, "stage_backward")
+
+    def optimizer_step(self, grad_scale: float = 1.0, stream=None) -> None:
+        L.check(self.lib.swarm_stage_optimizer_step(self.h, grad_scale, _stream(stream)), "stage_optimizer_step")
+
+    def sync_shadow(self, stream=None) -> None:
+        L.check(self.lib.swarm_stage_sync_shadow(self.h, _stream(stream)), "stage_sync_shadow")
+
+    # -- state ---------------------------------------------------------------
+    def grads(self) -> torch.Tensor:
+        return device_view(self.lib.swarm_stage_grads(self.h), self.n_params, torch.float32, self.device)
+
+    def params(self) -> torch.Tensor:
+        return device_view(self.lib.swarm_stage_params(self.h), self.n_params, torch.float32, self.device)
+
+    def params_bf16(self) -> torch.Tensor:
+        return device_view(self.lib.swarm_stage_params_bf16(self.h), self.n_params, torch.bfloat16, self.device)
+
+    def param_info(self):
+        out, i = [], 0
+        name, off, r, c = C.c_char_p(), C.c_size_t(), C.c_size_t(), C.c_size_t()
+        while self.lib.swarm_stage_param_info(self.h, i, C.byref(name), C.byref(off), C.byref(r), C.byref(c)) == 0:
+            out.append((name.value.decode(), off.value, r.value, c.value))
+            i += 1
+        return out
+
+    def tensor(self, name: str, which: str = "param") -> torch.Tensor:
+        """A parameter (fp32 master), its bf16 shadow or its gradient, shaped [rows, cols]."""
+        for n, off, r, c in self.param_info():
+            if n == name:
+                src = {"param": self.params(), "bf16": self.params_bf16(), "grad": self.grads()}[which]
+                return src[off:off + r * c].view(r, c)
+        raise KeyError(name)
+
+    def activation(self, slot: int, layer: int, name: str) -> torch.Tensor:
+        ptr, n = C.c_void_p(), C.c_size_t()
+        L.check(self.lib.swarm_stage_activation(self.h, slot, layer, name.encode(), C.byref(ptr), C.byref(n)),
+                "stage_activation")
+        return device_view(ptr.value, n.value, torch.bfloat16, self.device)

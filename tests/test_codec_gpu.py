@@ -125,16 +125,20 @@ def test_all_128_negative_code_and_zero_block(cuda):
     assert not c.any() and not s.any()
 
 
-@pytest.mark.parametrize("bad", [np.nan, np.inf, -np.inf])
+BAD = {"nan": (np.nan, 0x7FC0), "inf": (np.inf, 0x7F80), "-inf": (-np.inf, 0xFF80)}
+
+
+@pytest.mark.parametrize("bad", list(BAD))
 @pytest.mark.parametrize("dtype", ["f32", "bf16", "f64"])
 def test_nonfinite_sets_flag(cuda, bad, dtype):
+    val, bits = BAD[bad]
     x = np.linspace(-1, 1, 3 * 4096).astype(np.float64)
-    x[5000] = bad
+    x[5000] = val
     if dtype == "f32":
         x = x.astype(np.float32)
     elif dtype == "bf16":
-        x = O.f32_to_bf16_bits(x.astype(np.float32))
-        x[5000] = {np.nan: 0x7FC0, np.inf: 0x7F80, -np.inf: 0xFF80}[bad] if not np.isnan(bad) else 0x7FC0
+        x = O.f32_to_bf16_bits(np.nan_to_num(x).astype(np.float32))
+        x[5000] = bits
     _, _, fl = gpu_quant(x, 4096, dtype)
     assert fl & 1
 
@@ -158,14 +162,15 @@ def test_full_size_roundtrip_properties(cuda):
     c, s = ops.quantize(x, bs)
     y = ops.dequantize(c, s, bs, torch.float32)
     err = (y.double() - x.double()).abs().view(-1, bs).amax(1)
-    bound = 0.5 * s.double() / 127.0 * (1 + 1e-6) + 1e-30
+    # exact bound of acceptance #8 plus the one fp32 rounding of the dequantized value
+    ymax = y.abs().view(-1, bs).amax(1).double()
+    bound = 0.5 * s.double() / 127.0 + ymax * 2.0 ** -24
     assert bool((err <= bound).all())
-    # spot-check 64 blocks spread over the tensor bit-exactly against the oracle
-    idx = torch.linspace(0, n // bs - 1, 64).long()
-    xb = x.view(-1, bs)[idx].cpu().numpy().ravel()
-    st, c0, s0 = O.quantize(xb, bs)
-    assert np.array_equal(c.view(-1, bs)[idx].cpu().numpy().ravel(), c0)
-    assert np.array_equal(s[idx].cpu().numpy(), s0)
+    # the whole 1 GiB tensor bit-exactly against the oracle
+    st, c0, s0 = O.quantize(x.cpu().numpy(), bs)
+    assert st == 0
+    assert np.array_equal(c.cpu().numpy(), c0)
+    assert np.array_equal(s.cpu().numpy(), s0)
 
 
 def test_host_entry_points_match_device(cuda):

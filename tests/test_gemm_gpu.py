@@ -85,8 +85,9 @@ def test_gemm_batched_heads(cuda):
     args.m, args.n, args.k, args.batch, args.bh = Lq, Lq, dh, B * H, H
     args.a, args.lda, args.a_mn_major, args.a_rows, args.a_cols = qkv.data_ptr(), 3 * d, 0, B * Lq, 3 * d
     args.ra0, args.ra1, args.ca0, args.ca1 = Lq, 0, 0, dh
-    args.b, args.ldb, args.b_mn_major, args.b_rows, args.b_cols = qkv.data_ptr(), 3 * d, 0, B * Lq, 3 * d
-    args.rb0, args.rb1, args.cb0, args.cb1 = Lq, 0, d, dh  # K block starts at column d
+    kv = qkv[:, d:]  # the K block starts at column d: offset the base pointer
+    args.b, args.ldb, args.b_mn_major, args.b_rows, args.b_cols = kv.data_ptr(), 3 * d, 0, B * Lq, 2 * d
+    args.rb0, args.rb1, args.cb0, args.cb1 = Lq, 0, 0, dh
     args.d, args.ldd = S.data_ptr(), Lq
     args.rd0, args.rd1, args.cd0, args.cd1 = H * Lq, Lq, 0, 0
     args.alpha, args.epilogue = 1.0, L.EPI_STORE_F32
