@@ -35,6 +35,7 @@ extern "C" {
 #define SWARM_E_NONFINITE 2
 #define SWARM_E_CUDA 3
 #define SWARM_E_UNSUPPORTED 4
+#define SWARM_E_NO_PEER 5 /* maps to swarmsim::NoPeerAvailable */
 
 #define SWARM_DTYPE_F32 0
 #define SWARM_DTYPE_BF16 1
@@ -229,6 +230,25 @@ int swarm_stage_param_info(swarm_stage_t st, int index, const char** name, size_
                            size_t* cols);
 /* saved activation of (slot, layer) by name ("x","a","qkv","P","o","h","c","u","g","xf","dxf"), for tests */
 int swarm_stage_activation(swarm_stage_t st, int slot, int layer, const char* name, void** ptr, size_t* numel);
+
+/* ---- host control plane: stochastic wiring + rebalancing ------------------
+ * Replace wiring::RoutingState (P/include/swarmsim/wiring.hpp:19-90,
+ * P/src/wiring.cpp:33-120) and rebalancer::decide (P/src/rebalancer.cpp:25-69)
+ * with decision-identical host C++ (no GPU).  Peers are the reference's PeerId
+ * values (uint64).  Errors: SWARM_E_INVALID (ConfigError), SWARM_E_NO_PEER. */
+typedef struct swarm_router* swarm_router_t;
+const char* swarm_router_last_error(void);
+int swarm_router_create(size_t n_stages, double gamma, double epsilon, swarm_router_t* out);
+void swarm_router_destroy(swarm_router_t r);
+int swarm_router_add_server(swarm_router_t r, uint64_t peer, const size_t* stages, size_t n_stages, double phase);
+int swarm_router_ban_server(swarm_router_t r, uint64_t peer);
+void swarm_router_remove_server(swarm_router_t r, uint64_t peer);
+int swarm_router_is_banned(swarm_router_t r, uint64_t peer);
+int swarm_router_choose_server(swarm_router_t r, size_t stage, uint64_t* peer);
+int swarm_router_record_response(swarm_router_t r, uint64_t peer, double elapsed_seconds);
+int swarm_router_peer_state(swarm_router_t r, uint64_t peer, double* ema, double* priority);
+int swarm_rebalance_decide(size_t n_stages, const size_t* offsets, const uint64_t* peers, const double* queues,
+                           uint64_t* mover, size_t* from_stage, size_t* to_stage, size_t* op_count);
 
 #ifdef __cplusplus
 }

@@ -12,7 +12,7 @@ import os
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "libswarm_b200.so")
 
-SWARM_OK, SWARM_E_INVALID, SWARM_E_NONFINITE, SWARM_E_CUDA, SWARM_E_UNSUPPORTED = 0, 1, 2, 3, 4
+SWARM_OK, SWARM_E_INVALID, SWARM_E_NONFINITE, SWARM_E_CUDA, SWARM_E_UNSUPPORTED, SWARM_E_NO_PEER = 0, 1, 2, 3, 4, 5
 DT_F32, DT_BF16, DT_F64 = 0, 1, 2
 FLAG_NONFINITE = 1
 EPI_STORE_BF16, EPI_STORE_F32, EPI_ACCUM_F32, EPI_RESIDUAL, EPI_GELU, EPI_DGELU = range(6)
@@ -74,6 +74,17 @@ SIGNATURES = {
     "swarm_stage_sync_shadow": (I, [P, P]),
     "swarm_stage_param_info": (I, [P, I, C.POINTER(C.c_char_p), C.POINTER(SZ), C.POINTER(SZ), C.POINTER(SZ)]),
     "swarm_stage_activation": (I, [P, I, I, C.c_char_p, C.POINTER(P), C.POINTER(SZ)]),
+    "swarm_router_last_error": (C.c_char_p, []),
+    "swarm_router_create": (I, [SZ, D, D, C.POINTER(P)]),
+    "swarm_router_destroy": (None, [P]),
+    "swarm_router_add_server": (I, [P, C.c_uint64, P, SZ, D]),
+    "swarm_router_ban_server": (I, [P, C.c_uint64]),
+    "swarm_router_remove_server": (None, [P, C.c_uint64]),
+    "swarm_router_is_banned": (I, [P, C.c_uint64]),
+    "swarm_router_choose_server": (I, [P, SZ, C.POINTER(C.c_uint64)]),
+    "swarm_router_record_response": (I, [P, C.c_uint64, D]),
+    "swarm_router_peer_state": (I, [P, C.c_uint64, C.POINTER(D), C.POINTER(D)]),
+    "swarm_rebalance_decide": (I, [SZ, P, P, P, C.POINTER(C.c_uint64), C.POINTER(SZ), C.POINTER(SZ), C.POINTER(SZ)]),
 }
 
 _lib = None
@@ -105,4 +116,7 @@ def check(rc: int, what: str) -> None:
     msg = f"{what}: {last_error()}"
     if rc in (SWARM_E_INVALID, SWARM_E_NONFINITE):
         raise ConfigError(msg)
+    if rc == SWARM_E_NO_PEER:
+        from ._swarmsim_b200 import NoPeerAvailable
+        raise NoPeerAvailable(msg)
     raise RuntimeError(msg)

@@ -30,20 +30,31 @@ namespace {
 constexpr uint32_t kF32AbsMask = 0x7fffffffu;
 constexpr uint32_t kF32Inf = 0x7f800000u;
 
-__device__ __forceinline__ int code_from_f32(float x, float a, float inv) {
+// Slow, exact path (taken with probability ~2e-4): 127|x| vs (fl+0.5)*a,
+// both products exact in fp64 for fp32/bf16 x and fp32 a.
+__device__ __noinline__ int code_exact(float x, float a, float inv) {
     const float ax = fabsf(x);
-    const float ar = __fmul_rn(ax, inv);
-    const float fl = floorf(ar);
-    const float frac = __fsub_rn(ar, fl);
-    int m = static_cast<int>(fl) + (frac >= 0.5f ? 1 : 0);
-    if (fabsf(frac - 0.5f) < 1e-4f) {
-        // exact tie-break: 127|x| vs (fl+0.5)*a, both exact products in fp64
-        const double t = __dmul_rn(127.0, static_cast<double>(ax));
-        const double bnd = __dmul_rn(static_cast<double>(fl) + 0.5, static_cast<double>(a));
-        m = static_cast<int>(fl) + (t >= bnd ? 1 : 0);
-    }
+    const float fl = floorf(__fmul_rn(ax, inv));
+    const double t = __dmul_rn(127.0, static_cast<double>(ax));
+    const double bnd = __dmul_rn(static_cast<double>(fl) + 0.5, static_cast<double>(a));
+    int m = static_cast<int>(fl) + (t >= bnd ? 1 : 0);
     m = m > 127 ? 127 : m;
     return x < 0.f ? -m : m;
+}
+
+// Fast path without F2I/FRND (those issue on the narrow XU pipe and made this
+// kernel issue-bound): y = x*(127/a) is within 1.5e-5 of the exact quotient;
+// adding 1.5*2^23 rounds it to the nearest integer inside the mantissa, which
+// equals round-half-away-from-zero unless y is within 1e-4 of a half-integer.
+__device__ __forceinline__ int code_from_f32(float x, float a, float inv) {
+    constexpr float kMagic = 12582912.0f;  // 1.5 * 2^23
+    const float y = __fmul_rn(x, inv);
+    const float t = __fadd_rn(y, kMagic);
+    const float r = __fsub_rn(t, kMagic);
+    const float d = __fsub_rn(y, r);
+    if (fabsf(fabsf(d) - 0.5f) < 1e-4f) return code_exact(x, a, inv);
+    const int m = __float_as_int(t) - 0x4B400000;
+    return max(-127, min(127, m));
 }
 
 __device__ __forceinline__ uint32_t pack4(int c0, int c1, int c2, int c3) {
@@ -237,14 +248,17 @@ __global__ void __launch_bounds__(THREADS) k_dequant_table(const uint4* __restri
                                                            OutT* __restrict__ out) {
     __shared__ OutT table[256];
     const size_t b = blockIdx.x;
-    const double a = static_cast<double>(scales[b]);
-    if (threadIdx.x < 256) table[threadIdx.x] = from_f64<OutT>(deq(static_cast<int>(threadIdx.x) - 128, a));
-    __syncthreads();
     const size_t n16 = bs / 16;
     const uint4* cb = codes + b * n16;
     OutT* ob = out + b * bs;
+    // issue this thread's first code load before the codebook build so the
+    // HBM latency overlaps the 256 fp64 divides
+    const uint4 first = threadIdx.x < n16 ? __ldcs(cb + threadIdx.x) : make_uint4(0, 0, 0, 0);
+    const double a = static_cast<double>(scales[b]);
+    if (threadIdx.x < 256) table[threadIdx.x] = from_f64<OutT>(deq(static_cast<int>(threadIdx.x) - 128, a));
+    __syncthreads();
     for (size_t j = threadIdx.x; j < n16; j += THREADS) {
-        const uint4 c = __ldcs(cb + j);
+        const uint4 c = j == threadIdx.x ? first : __ldcs(cb + j);
         const uint32_t w[4] = {c.x, c.y, c.z, c.w};
         OutT vals[16];
 #pragma unroll
