@@ -61,6 +61,11 @@ struct swarm_stage {
     void* lnws = nullptr;
     std::vector<void*> allocations;
     int step = 0;
+    // GEMM profiling (bench.py's live roofline): event pairs around each GEMM
+    bool prof_on = false;
+    std::vector<cudaEvent_t> prof_events;
+    std::vector<double> prof_flops;
+    size_t prof_used = 0;
 };
 
 namespace {
@@ -112,6 +117,29 @@ struct Op {  // one operand in its 2-D storage
     bool mn;  // MN-major (the operand is stored transposed)
 };
 
+thread_local swarm_stage* t_prof = nullptr;  // stage whose visit is being profiled, if any
+
+struct ProfScope {
+    explicit ProfScope(swarm_stage* s) { t_prof = s->prof_on ? s : nullptr; }
+    ~ProfScope() { t_prof = nullptr; }
+};
+
+int run_gemm(const swarm_gemm_args& g, cudaStream_t st) {
+    swarm_stage* s = t_prof;
+    if (!s) return swarm_gemm_bf16(&g, st);
+    while (s->prof_events.size() < 2 * (s->prof_used + 1)) {
+        cudaEvent_t e;
+        if (cudaEventCreate(&e) != cudaSuccess) return SWARM_E_CUDA;
+        s->prof_events.push_back(e);
+    }
+    cudaEventRecord(s->prof_events[2 * s->prof_used], st);
+    const int rc = swarm_gemm_bf16(&g, st);
+    cudaEventRecord(s->prof_events[2 * s->prof_used + 1], st);
+    s->prof_flops.push_back(2.0 * g.m * g.n * static_cast<double>(g.k) * g.batch);
+    s->prof_used += 1;
+    return rc;
+}
+
 int mm(int M, int N, int K, Op a, Op b, void* d, int ldd, int epi, const void* aux, float alpha, cudaStream_t st) {
     swarm_gemm_args g{};
     g.m = M;
@@ -134,7 +162,7 @@ int mm(int M, int N, int K, Op a, Op b, void* d, int ldd, int epi, const void* a
     g.aux = aux;
     g.alpha = alpha;
     g.epilogue = epi;
-    return swarm_gemm_bf16(&g, st);
+    return run_gemm(g, st);
 }
 
 // Attention GEMM batched over z = b*H + h.  Offsets in storage coordinates:
@@ -179,7 +207,7 @@ int bmm(swarm_stage* s, int M, int N, int K, BOp a, BOp b, void* d, int ldd, int
     g.cd1 = cd1;
     g.alpha = alpha;
     g.epilogue = epi;
-    return swarm_gemm_bf16(&g, st);
+    return run_gemm(g, st);
 }
 
 const LayerW& weights(const swarm_stage* s, int l) { return s->layers[s->cfg.shared_layers ? 0 : l]; }
@@ -420,11 +448,35 @@ int swarm_stage_create(const swarm_stage_config* cfg, swarm_stage_t* out) {
 void swarm_stage_destroy(swarm_stage_t s) {
     if (!s) return;
     cudaDeviceSynchronize();
+    for (cudaEvent_t e : s->prof_events) cudaEventDestroy(e);
     for (void* p : s->allocations) cudaFree(p);
     delete s;
 }
 
 size_t swarm_stage_wire_bytes(swarm_stage_t s) { return wire_bytes(s); }
+
+void swarm_stage_profile(swarm_stage_t s, int enable) {
+    s->prof_on = enable != 0;
+    s->prof_used = 0;
+    s->prof_flops.clear();
+}
+
+int swarm_stage_profile_read(swarm_stage_t s, double* gemm_ms, double* gemm_flops, uint64_t* gemm_launches) {
+    double ms = 0.0, fl = 0.0;
+    for (size_t i = 0; i < s->prof_used; ++i) {
+        if (cudaEventSynchronize(s->prof_events[2 * i + 1]) != cudaSuccess) return SWARM_E_CUDA;
+        float e = 0.f;
+        cudaEventElapsedTime(&e, s->prof_events[2 * i], s->prof_events[2 * i + 1]);
+        ms += e;
+        fl += s->prof_flops[i];
+    }
+    if (gemm_ms) *gemm_ms = ms;
+    if (gemm_flops) *gemm_flops = fl;
+    if (gemm_launches) *gemm_launches = s->prof_used;
+    s->prof_used = 0;
+    s->prof_flops.clear();
+    return SWARM_OK;
+}
 size_t swarm_stage_num_params(swarm_stage_t s) { return s->nparams; }
 float* swarm_stage_grads(swarm_stage_t s) { return s->grad; }
 float* swarm_stage_params(swarm_stage_t s) { return s->p32; }
@@ -472,6 +524,7 @@ int swarm_stage_forward(swarm_stage_t s, int slot, const void* in, const int32_t
     if (slot < 0 || slot >= static_cast<int>(s->slots.size())) return fail("forward: bad slot");
     if (!in) return fail("forward: null input");
     cudaStream_t st = static_cast<cudaStream_t>(stream);
+    ProfScope prof(s);
     Slot& sl = s->slots[slot];
     const int T = s->T, d = s->d, n = s->cfg.n_layers;
     if (s->cfg.is_first) {
@@ -506,6 +559,7 @@ int swarm_stage_forward(swarm_stage_t s, int slot, const void* in, const int32_t
 int swarm_stage_backward(swarm_stage_t s, int slot, const void* grad_in, void* grad_out, swarm_stream_t stream) {
     if (slot < 0 || slot >= static_cast<int>(s->slots.size())) return fail("backward: bad slot");
     cudaStream_t st = static_cast<cudaStream_t>(stream);
+    ProfScope prof(s);
     Slot& sl = s->slots[slot];
     const int T = s->T, d = s->d, n = s->cfg.n_layers;
     int cur = 0;

@@ -146,6 +146,15 @@ class Stage:
                 return src[off:off + r * c].view(r, c)
         raise KeyError(name)
 
+    def profile(self, enable: bool = True) -> None:
+        self.lib.swarm_stage_profile(self.h, int(enable))
+
+    def profile_read(self):
+        """(gemm_ms, gemm_flops, gemm_launches) since the last read (synchronises)."""
+        ms, fl, n = C.c_double(), C.c_double(), C.c_uint64()
+        L.check(self.lib.swarm_stage_profile_read(self.h, C.byref(ms), C.byref(fl), C.byref(n)), "profile_read")
+        return ms.value, fl.value, n.value
+
     def activation(self, slot: int, layer: int, name: str) -> torch.Tensor:
         ptr, n = C.c_void_p(), C.c_size_t()
         L.check(self.lib.swarm_stage_activation(self.h, slot, layer, name.encode(), C.byref(ptr), C.byref(n)),

@@ -149,7 +149,8 @@ def test_optimizer_step_is_adamw(cuda):
     want = p0 - 1e-3 * ((m / 0.1) / (torch.sqrt(v / 0.05) + cfg.eps) + 0.1 * p0)
     torch.testing.assert_close(st.params(), want, rtol=1e-5, atol=1e-6)
     assert float(st.grads().abs().max()) == 0.0
-    torch.testing.assert_close(st.params_bf16().float(), want.bfloat16().float())
+    # the bf16 shadow is exactly the round-to-nearest of the updated fp32 master
+    assert torch.equal(st.params_bf16(), st.params().bfloat16())
 
 
 def test_training_reduces_loss(cuda):
