@@ -228,10 +228,10 @@ int swarm_stage_sync_shadow(swarm_stage_t st, swarm_stream_t stream);
 /* enumerate parameter tensors: index -> name, offset (elements), rows, cols */
 int swarm_stage_param_info(swarm_stage_t st, int index, const char** name, size_t* offset, size_t* rows,
                            size_t* cols);
-/* GEMM profiling for the live roofline: when enabled, every GEMM of this
+/* GEMM profiling for the live roofline: while enabled, every GEMM of this
  * stage's visits is bracketed by CUDA events on the visit's stream;
  * profile_read synchronises, returns the summed GEMM time (ms), algorithmic
- * FLOPs (2*M*N*K*batch) and launch count since the last read, and resets. */
+ * FLOPs (2*M*N*K*batch) and launch count recorded since the last read, and resets. */
 void swarm_stage_profile(swarm_stage_t st, int enable);
 int swarm_stage_profile_read(swarm_stage_t st, double* gemm_ms, double* gemm_flops, uint64_t* gemm_launches);
 /* saved activation of (slot, layer) by name ("x","a","qkv","P","o","h","c","u","g","xf","dxf"), for tests */

@@ -21,6 +21,7 @@
 
 #include <algorithm>
 #include <mutex>
+#include <unordered_map>
 
 #include "common.cuh"
 #include "sm100.cuh"
@@ -363,8 +364,47 @@ EncodeFn get_encode() {
     return fn;
 }
 
+// Descriptor cache: a training step re-issues the same few hundred
+// (pointer, shape, box) operands every microbatch, so encode each once.
+struct MapKey {
+    const void* ptr;
+    long long rows, cols, ld;
+    int bi, bo;
+    bool operator==(const MapKey& o) const {
+        return ptr == o.ptr && rows == o.rows && cols == o.cols && ld == o.ld && bi == o.bi && bo == o.bo;
+    }
+};
+struct MapKeyHash {
+    size_t operator()(const MapKey& k) const {
+        size_t h = reinterpret_cast<uintptr_t>(k.ptr);
+        for (long long v : {k.rows, k.cols, k.ld, static_cast<long long>(k.bi) << 16 | k.bo})
+            h = h * 0x9E3779B97F4A7C15ull + static_cast<size_t>(v);
+        return h;
+    }
+};
+
+int encode_2d_uncached(CUtensorMap* m, const void* ptr, long long rows, long long cols, long long ld, int box_inner,
+                       int box_outer);
+
 int encode_2d(CUtensorMap* m, const void* ptr, long long rows, long long cols, long long ld, int box_inner,
               int box_outer) {
+    thread_local std::unordered_map<MapKey, CUtensorMap, MapKeyHash> cache;
+    const MapKey key{ptr, rows, cols, ld, box_inner, box_outer};
+    auto it = cache.find(key);
+    if (it != cache.end()) {
+        *m = it->second;
+        return SWARM_OK;
+    }
+    const int rc = encode_2d_uncached(m, ptr, rows, cols, ld, box_inner, box_outer);
+    if (rc == SWARM_OK) {
+        if (cache.size() > 16384) cache.clear();  // bounded: pointers of freed buffers age out
+        cache.emplace(key, *m);
+    }
+    return rc;
+}
+
+int encode_2d_uncached(CUtensorMap* m, const void* ptr, long long rows, long long cols, long long ld, int box_inner,
+                       int box_outer) {
     EncodeFn enc = get_encode();
     if (!enc) {
         set_error("gemm: cuTensorMapEncodeTiled unavailable");

@@ -455,11 +455,7 @@ void swarm_stage_destroy(swarm_stage_t s) {
 
 size_t swarm_stage_wire_bytes(swarm_stage_t s) { return wire_bytes(s); }
 
-void swarm_stage_profile(swarm_stage_t s, int enable) {
-    s->prof_on = enable != 0;
-    s->prof_used = 0;
-    s->prof_flops.clear();
-}
+void swarm_stage_profile(swarm_stage_t s, int enable) { s->prof_on = enable != 0; }
 
 int swarm_stage_profile_read(swarm_stage_t s, double* gemm_ms, double* gemm_flops, uint64_t* gemm_launches) {
     double ms = 0.0, fl = 0.0;

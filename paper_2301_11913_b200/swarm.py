@@ -167,7 +167,7 @@ def message_log(pl: Placement, routes: list[list[int]], rank: int):
 class SwarmPipeline:
     def __init__(self, mcfg: ModelConfig, n_stages: int = 4, *, n_microbatches: int = 16, n_trainers: int | None = None,
                  seed: int = 0, lr: float = 1e-4, weight_decay: float = 0.0, gamma: float = 0.1, epsilon: float = 1.0,
-                 modeled_flops: float = 1.0e15, profile: bool = False):
+                 modeled_flops: float = 1.0e15, profile: bool = False, use_graphs: bool = True):
         self.m = mcfg
         self.S = n_stages
         self.M = n_microbatches
@@ -193,8 +193,14 @@ class SwarmPipeline:
                               block_size=mcfg.block_size, lr=lr, weight_decay=weight_decay,
                               seed=seed * 1000 + s)  # every replica of a stage starts identical
             self.stages[s] = Stage(cfg, self.device)
-            if profile:
-                self.stages[s].profile(True)
+        # CUDA graphs: a visit enqueues ~200 kernels; replaying a captured graph
+        # removes the per-launch host cost.  With `profile`, the first visit of
+        # each stage per step runs eagerly with GEMM events (live roofline).
+        self.profile = profile
+        self.use_graphs = use_graphs
+        self.graphs: dict = {}
+        self._warm: set = set()
+        self._profiled: set = set()
         self.wire_bytes = next(iter(self.stages.values())).wire_bytes
         tokens = mcfg.tokens
         self.fwd_seconds = 2.0 * mcfg.params_per_layer() * tokens * mcfg.layers_per_stage / modeled_flops
@@ -225,6 +231,7 @@ class SwarmPipeline:
         """One optimizer step over M microbatches.  tokens/targets: int32
         [M, B*L] on this device (only read by the first / last stage)."""
         routes = self.plan()
+        self._profiled.clear()
         scale = loss_scale if loss_scale is not None else 1.0 / (self.M * self.m.tokens)
         if self.all_local:
             self._step_local(routes, tokens, targets, scale)
@@ -235,20 +242,53 @@ class SwarmPipeline:
                 dist.all_reduce(st.grads(), op=dist.ReduceOp.SUM, group=self.stage_group[s])
             st.optimizer_step(grad_scale=1.0 / self.P)
 
+    # ---------------------------------------------------------------- visits
+    def _run(self, key, fn) -> None:
+        s, kind = key[0], key[1]
+        eager_prof = self.profile and (s, kind) not in self._profiled
+        if eager_prof or not self.use_graphs or (s, kind) not in self._warm:
+            st = self.stages[s]
+            if eager_prof:
+                st.profile(True)
+                self._profiled.add((s, kind))
+            fn()
+            if eager_prof:
+                st.profile(False)  # keep the events recorded so far; stop adding
+            self._warm.add((s, kind))
+            return
+        g = self.graphs.get(key)
+        if g is None:
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                fn()
+            self.graphs[key] = g
+        g.replay()
+
+    def _fwd(self, s, slot, inp, out=None, targets=None, scale=1.0) -> None:
+        st = self.stages[s]
+        key = (s, "f", slot, inp.data_ptr(), None if out is None else out.data_ptr(),
+               None if targets is None else targets.data_ptr())
+        self._run(key, lambda: st.forward(slot, inp, out=out, targets=targets, loss_sum=self.loss_sum,
+                                          loss_scale=scale))
+
+    def _bwd(self, s, slot, gin=None, gout=None) -> None:
+        st = self.stages[s]
+        key = (s, "b", slot, None if gin is None else gin.data_ptr(), None if gout is None else gout.data_ptr())
+        self._run(key, lambda: st.backward(slot, grad_in=gin, grad_out=gout))
+
     def _step_local(self, routes, tokens, targets, scale) -> None:
         # every stage lives here: run each microbatch depth-first (fwd 0..S-1,
         # bwd S-1..0) so one activation slot per stage suffices
         a, g = self.act[0], self.grd[0]
         for mb in range(self.M):
             for s in range(self.S):
-                st = self.stages[s]
                 inp = tokens[mb] if s == 0 else a
                 if s == self.S - 1:
-                    st.forward(0, inp, targets=targets[mb], loss_sum=self.loss_sum, loss_scale=scale)
+                    self._fwd(s, 0, inp, targets=targets[mb], scale=scale)
                 else:
-                    st.forward(0, inp, out=a)
+                    self._fwd(s, 0, inp, out=a)
             for s in reversed(range(self.S)):
-                self.stages[s].backward(0, grad_in=None if s == self.S - 1 else g, grad_out=None if s == 0 else g)
+                self._bwd(s, 0, None if s == self.S - 1 else g, None if s == 0 else g)
 
     def _step_pipelined(self, routes, tokens, targets, scale) -> None:
         """GPipe order over this rank's visits: all forwards by ascending
@@ -274,10 +314,10 @@ class SwarmPipeline:
                 if src != self.rank:
                     dist.recv(inp, src)
             if s == self.S - 1:
-                st.forward(slot[(mb, s)], inp, targets=targets[mb], loss_sum=self.loss_sum, loss_scale=scale)
+                self._fwd(s, slot[(mb, s)], inp, targets=targets[mb], scale=scale)
             else:
                 out = self.act[mb]
-                st.forward(slot[(mb, s)], inp, out=out)
+                self._fwd(s, slot[(mb, s)], inp, out=out)
                 dst = self.rank_of_peer(routes[mb][s + 1])
                 if dst != self.rank:
                     pending.append(dist.isend(out, dst))
@@ -293,7 +333,7 @@ class SwarmPipeline:
                 if src != self.rank:
                     dist.recv(gin, src)
             gout = None if s == 0 else self.grd[mb]
-            st.backward(slot[(mb, s)], grad_in=gin, grad_out=gout)
+            self._bwd(s, slot[(mb, s)], gin, gout)
             if s > 0:
                 dst = self.rank_of_peer(routes[mb][s - 1])
                 if dst != self.rank:
