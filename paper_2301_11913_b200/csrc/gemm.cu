@@ -20,6 +20,7 @@
 #include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <mutex>
 #include <unordered_map>
 
@@ -346,6 +347,190 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
 }
 
+// ------------------------------------------------- 2-CTA pair variant (M=256)
+// A cluster of two CTAs on one TPC computes a 256 x 256 tile with
+// tcgen05.mma.cta_group::2: each CTA stages its own 128 rows of A and its own
+// 128 rows (N) of B, so per-SM operand traffic (TMA ingest and smem reads) is
+// half of the single-CTA 128 x 256 tile for the same MMA rate.  The leader
+// (rank 0) issues the MMAs; both CTAs' TMA loads complete on the leader's full
+// barrier; commits multicast to both CTAs' empty / tmem-full barriers; both
+// CTAs' epilogue warps release the accumulator on the leader's tmem-empty.
+constexpr int PAIR_BN = 256;
+struct Cfg2 {
+    static constexpr int A_BYTES = 128 * BK * 2;  // this CTA's half of A
+    static constexpr int B_BYTES = 128 * BK * 2;  // this CTA's half of B
+    static constexpr int STAGES = 6;
+    static constexpr int TMEM_COLS = 2 * PAIR_BN;
+    static constexpr int SMEM = STAGES * (A_BYTES + B_BYTES) + 1024 + 256;
+};
+
+template <bool A_MN, bool B_MN>
+__global__ void __launch_bounds__(kThreads, 1)
+    k_gemm2(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUtensorMap tma_b, const Params p) {
+    using C = Cfg2;
+    extern __shared__ uint8_t smem_raw[];
+    const uint32_t raw = smem_u32(smem_raw);
+    uint8_t* smem = smem_raw + ((1024 - (raw & 1023)) & 1023);
+    uint8_t* sa = smem;
+    uint8_t* sb = smem + C::STAGES * C::A_BYTES;
+    uint64_t* full = reinterpret_cast<uint64_t*>(sb + C::STAGES * C::B_BYTES);
+    uint64_t* empty = full + C::STAGES;
+    uint64_t* tfull = empty + C::STAGES;
+    uint64_t* tempty = tfull + 2;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+    const int warp = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
+    const uint32_t rank = cluster_ctarank();
+    const bool leader = rank == 0;
+    const int cluster = blockIdx.x >> 1;
+    const int n_clusters = gridDim.x >> 1;
+
+    if (warp == 0 && lane == 0) {
+        tma_prefetch(&tma_a);
+        tma_prefetch(&tma_b);
+        for (int s = 0; s < C::STAGES; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], 1);
+        }
+        for (int s = 0; s < 2; ++s) {
+            mbar_init(&tfull[s], 1);
+            mbar_init(&tempty[s], 8);  // 4 epilogue warps x 2 CTAs (only the leader's is used)
+        }
+        fence_barrier_init();
+    }
+    if (warp == 2) {
+        tmem_alloc_pair(tmem_slot, C::TMEM_COLS);
+        tmem_relinquish_pair();
+    }
+    tc_fence_before();
+    cluster_sync();  // barriers of both CTAs initialised before any remote arrive / TMA
+    tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+
+    if (warp == 0) {
+        if (lane == 0) {
+            // ------------------------------------------------ TMA producer (both CTAs)
+            int stage = 0;
+            uint32_t phase = 0;
+            for (int t = cluster; t < p.total_tiles; t += n_clusters) {
+                const int z = t / p.tiles_per_batch;
+                const int r = t - z * p.tiles_per_batch;
+                const int mt = r % p.tiles_m, nt = r / p.tiles_m;
+                const int zb = z / p.bh, zh = z - zb * p.bh;
+                const int ra = p.ra0 * zb + p.ra1 * zh, ca = p.ca0 * zb + p.ca1 * zh;
+                const int rb = p.rb0 * zb + p.rb1 * zh, cb = p.cb0 * zb + p.cb1 * zh;
+                const int m0 = mt * 256 + static_cast<int>(rank) * 128;
+                const int n0 = nt * PAIR_BN + static_cast<int>(rank) * 128;
+                for (int kb = 0; kb < p.k_blocks; ++kb) {
+                    mbar_wait(&empty[stage], phase ^ 1);
+                    if (leader) mbar_arrive_expect_tx(&full[stage], 2 * (C::A_BYTES + C::B_BYTES));
+                    const uint32_t bar = map_to_cta(&full[stage], 0);
+                    uint8_t* a_dst = sa + stage * C::A_BYTES;
+                    uint8_t* b_dst = sb + stage * C::B_BYTES;
+                    if constexpr (!A_MN) {
+                        tma_load_2d_pair(a_dst, &tma_a, bar, ca + kb * BK, ra + m0);
+                    } else {
+#pragma unroll
+                        for (int j = 0; j < 2; ++j)
+                            tma_load_2d_pair(a_dst + j * (64 * BK * 2), &tma_a, bar, ca + m0 + j * 64, ra + kb * BK);
+                    }
+                    if constexpr (!B_MN) {
+                        tma_load_2d_pair(b_dst, &tma_b, bar, cb + kb * BK, rb + n0);
+                    } else {
+#pragma unroll
+                        for (int j = 0; j < 2; ++j)
+                            tma_load_2d_pair(b_dst + j * (64 * BK * 2), &tma_b, bar, cb + n0 + j * 64, rb + kb * BK);
+                    }
+                    if (++stage == C::STAGES) {
+                        stage = 0;
+                        phase ^= 1;
+                    }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0 && leader) {
+            // ------------------------------------------------ MMA issuer (leader only)
+            constexpr uint32_t idesc = make_idesc_bf16(256, PAIR_BN, A_MN, B_MN);
+            int stage = 0;
+            uint32_t phase = 0;
+            int acc = 0;
+            uint32_t acc_phase = 0;
+            for (int t = cluster; t < p.total_tiles; t += n_clusters) {
+                mbar_wait(&tempty[acc], acc_phase ^ 1);
+                tc_fence_after();
+                const uint32_t d_tmem = tmem_base + static_cast<uint32_t>(acc * PAIR_BN);
+                for (int kb = 0; kb < p.k_blocks; ++kb) {
+                    mbar_wait(&full[stage], phase);
+                    tc_fence_after();
+                    const uint32_t a_base = smem_u32(sa + stage * C::A_BYTES);
+                    const uint32_t b_base = smem_u32(sb + stage * C::B_BYTES);
+#pragma unroll
+                    for (int k = 0; k < BK / 16; ++k) {
+                        const uint64_t ad = A_MN ? make_sdesc(a_base + k * 2048, 64 * BK * 2, 1024)
+                                                 : make_sdesc(a_base + k * 32, 16, 1024);
+                        const uint64_t bd = B_MN ? make_sdesc(b_base + k * 2048, 64 * BK * 2, 1024)
+                                                 : make_sdesc(b_base + k * 32, 16, 1024);
+                        mma_bf16_pair(d_tmem, ad, bd, idesc, (kb | k) != 0 ? 1u : 0u);
+                    }
+                    mma_commit_pair(&empty[stage], 0x3);
+                    if (++stage == C::STAGES) {
+                        stage = 0;
+                        phase ^= 1;
+                    }
+                }
+                mma_commit_pair(&tfull[acc], 0x3);
+                acc ^= 1;
+                if (acc == 0) acc_phase ^= 1;
+            }
+        }
+    } else if (warp >= 4) {
+        // ------------------------------------------------ epilogue (both CTAs, own 128 rows)
+        const int q = warp - 4;
+        const uint32_t tempty_leader[2] = {map_to_cta(&tempty[0], 0), map_to_cta(&tempty[1], 0)};
+        int acc = 0;
+        uint32_t acc_phase = 0;
+        for (int t = cluster; t < p.total_tiles; t += n_clusters) {
+            const int z = t / p.tiles_per_batch;
+            const int r = t - z * p.tiles_per_batch;
+            const int mt = r % p.tiles_m, nt = r / p.tiles_m;
+            const int zb = z / p.bh, zh = z - zb * p.bh;
+            const long long rd = p.rd0 * zb + p.rd1 * zh, cd = p.cd0 * zb + p.cd1 * zh;
+            const int row = mt * 256 + static_cast<int>(rank) * 128 + q * 32 + lane;
+            mbar_wait(&tfull[acc], acc_phase);
+            tc_fence_after();
+#pragma unroll 1
+            for (int c = 0; c < PAIR_BN / 32; ++c) {
+                uint32_t rr[32];
+                tmem_ld_32x32b_x32(tmem_base + (static_cast<uint32_t>(q * 32) << 16) +
+                                       static_cast<uint32_t>(acc * PAIR_BN + c * 32),
+                                   rr);
+                tmem_ld_wait();
+                const int col0 = nt * PAIR_BN + c * 32;
+                if (row < p.m && col0 < p.n) {
+                    float v[32];
+#pragma unroll
+                    for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(rr[j]) * p.alpha;
+                    const long long off = (rd + row) * p.ldd + cd + col0;
+                    epilogue_chunk(p, v, off, min(32, p.n - col0));
+                }
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive_cluster(tempty_leader[acc]);
+            acc ^= 1;
+            if (acc == 0) acc_phase ^= 1;
+        }
+    }
+    tc_fence_before();
+    cluster_sync();  // both CTAs finished every MMA / TMEM read before the pair frees TMEM
+    if (warp == 2) {
+        tc_fence_after();
+        tmem_dealloc_pair(tmem_base, C::TMEM_COLS);
+    }
+}
+
 // ---------------------------------------------------------------- host side
 using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                               const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
@@ -449,6 +634,47 @@ int launch(const CUtensorMap& ta, const CUtensorMap& tb, const Params& p, cudaSt
     return SWARM_OK;
 }
 
+template <bool A_MN, bool B_MN>
+int launch_pair(const CUtensorMap& ta, const CUtensorMap& tb, const Params& p, cudaStream_t st) {
+    auto kern = k_gemm2<A_MN, B_MN>;
+    static bool attr = false;
+    if (!attr) {
+        SWARM_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg2::SMEM));
+        attr = true;
+    }
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(2 * std::min(p.total_tiles, num_sms() / 2));
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = Cfg2::SMEM;
+    cfg.stream = st;
+    cudaLaunchAttribute attrs[1];
+    attrs[0].id = cudaLaunchAttributeClusterDimension;
+    attrs[0].val.clusterDim.x = 2;
+    attrs[0].val.clusterDim.y = 1;
+    attrs[0].val.clusterDim.z = 1;
+    cfg.attrs = attrs;
+    cfg.numAttrs = 1;
+    SWARM_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, ta, tb, p));
+    SWARM_LAUNCH_CHECK("k_gemm2");
+    return SWARM_OK;
+}
+
+int dispatch_pair(bool amn, bool bmn, const CUtensorMap& ta, const CUtensorMap& tb, const Params& p,
+                  cudaStream_t st) {
+    if (!amn && !bmn) return launch_pair<false, false>(ta, tb, p, st);
+    if (!amn && bmn) return launch_pair<false, true>(ta, tb, p, st);
+    if (amn && !bmn) return launch_pair<true, false>(ta, tb, p, st);
+    return launch_pair<true, true>(ta, tb, p, st);
+}
+
+bool pair_enabled() {
+    static const bool on = [] {
+        const char* e = getenv("SWARM_GEMM_PAIR");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
+
 template <int BN>
 int dispatch(bool amn, bool bmn, const CUtensorMap& ta, const CUtensorMap& tb, const Params& p, cudaStream_t st) {
     if (!amn && !bmn) return launch<BN, false, false>(ta, tb, p, st);
@@ -482,18 +708,21 @@ extern "C" int swarm_gemm_bf16(const swarm_gemm_args* a, swarm_stream_t stream) 
         br = a->b_mn_major ? a->k : a->n;
         bc = a->b_mn_major ? a->n : a->k;
     }
-    const int BN = a->n <= 128 ? 128 : 256;
+    // 2-CTA pair tiles (256 x 256) when both M and N fill them; else one CTA, 128 x BN
+    const bool pair = pair_enabled() && a->m > 128 && a->n > 128;
+    const int BN = pair ? PAIR_BN : (a->n <= 128 ? 128 : 256);
+    const int TM = pair ? 256 : BM;
     CUtensorMap ta, tb;
     int rc = encode_2d(&ta, a->a, ar, ac, a->lda, 64, a->a_mn_major ? BK : BM);
     if (rc) return rc;
-    rc = encode_2d(&tb, a->b, br, bc, a->ldb, 64, a->b_mn_major ? BK : BN);
+    rc = encode_2d(&tb, a->b, br, bc, a->ldb, 64, a->b_mn_major ? BK : (pair ? 128 : BN));
     if (rc) return rc;
     Params p{};
     p.m = a->m;
     p.n = a->n;
     p.k = a->k;
     p.bh = a->bh;
-    p.tiles_m = (a->m + BM - 1) / BM;
+    p.tiles_m = (a->m + TM - 1) / TM;
     p.tiles_n = (a->n + BN - 1) / BN;
     p.tiles_per_batch = p.tiles_m * p.tiles_n;
     p.total_tiles = p.tiles_per_batch * a->batch;
@@ -512,6 +741,7 @@ extern "C" int swarm_gemm_bf16(const swarm_gemm_args* a, swarm_stream_t stream) 
     p.vec_ok = (a->ldd % vec_elems == 0) && cd_ok && ((reinterpret_cast<uintptr_t>(a->d) & 15) == 0) &&
                (!a->aux || (reinterpret_cast<uintptr_t>(a->aux) & 15) == 0);
     cudaStream_t st = as_stream(stream);
+    if (pair) return dispatch_pair(a->a_mn_major, a->b_mn_major, ta, tb, p, st);
     if (BN == 128) return dispatch<128>(a->a_mn_major, a->b_mn_major, ta, tb, p, st);
     return dispatch<256>(a->a_mn_major, a->b_mn_major, ta, tb, p, st);
 }
