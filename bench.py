@@ -362,7 +362,7 @@ def bench_train(args, world, rank, local):
     time.sleep(0.3)  # let nvidia-smi produce its first sample before the timed region
     barrier(world)
     torch.cuda.synchronize()
-    n0 = L.swarm_launch_count()
+    n0 = pipe.kernels_launched()
     t0 = torch.cuda.Event(enable_timing=True)
     t1 = torch.cuda.Event(enable_timing=True)
     t0.record(stream)
@@ -371,7 +371,7 @@ def bench_train(args, world, rank, local):
     t1.record(stream)
     torch.cuda.synchronize()
     barrier(world)
-    launches = L.swarm_launch_count() - n0
+    launches = pipe.kernels_launched() - n0
     clocks = clk.stop()
     ms = max_over_ranks(t0.elapsed_time(t1), world)
     gemm_ms, gemm_flops, gemm_n = pipe.profile_read()

@@ -35,6 +35,8 @@ using namespace swarm::sm100;
 constexpr int BM = 128;
 constexpr int BK = 64;
 constexpr int kThreads = 256;
+constexpr int kEpiSlot = 4096;                   // one 32x32 fp32 (or 2 x 32x32 bf16) chunk
+constexpr int kEpiSmem = 4 * 2 * kEpiSlot;       // 4 epilogue warps x double buffer
 
 struct Params {
     int m, n, k, bh;
@@ -47,6 +49,7 @@ struct Params {
     float alpha;
     int epi;
     int vec_ok;
+    int tma_epi;  // stage output chunks in smem and write them with TMA (store / reduce-add)
 };
 
 template <int BN>
@@ -55,7 +58,7 @@ struct Cfg {
     static constexpr int B_BYTES = BN * BK * 2;
     static constexpr int STAGES = BN == 256 ? 4 : 6;
     static constexpr int TMEM_COLS = 2 * BN;
-    static constexpr int SMEM = STAGES * (A_BYTES + B_BYTES) + 1024 + 256;
+    static constexpr int SMEM = STAGES * (A_BYTES + B_BYTES) + kEpiSmem + 1024 + 256;
 };
 
 __device__ __forceinline__ float gelu_f(float x) {
@@ -186,16 +189,123 @@ __device__ __forceinline__ void epilogue_chunk(const Params& p, float (&v)[32], 
     }
 }
 
+
+// Swizzled staging of one 32 x 32 chunk (this warp's 32 rows; thread = row):
+// fp32 rows are 128 B (TMA SWIZZLE_128B: 16-B chunk j at j ^ (row & 7)), bf16
+// rows 64 B (SWIZZLE_64B: j ^ ((row >> 1) & 3)); both bank-conflict free.
+__device__ __forceinline__ void stage_f32(uint8_t* slot, int row, const float (&v)[32]) {
+    const uint32_t base = smem_u32(slot) + row * 128;
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+        st_shared_v4(base + ((j ^ (row & 7)) << 4), __float_as_uint(v[4 * j]), __float_as_uint(v[4 * j + 1]),
+                     __float_as_uint(v[4 * j + 2]), __float_as_uint(v[4 * j + 3]));
+}
+__device__ __forceinline__ void stage_bf16(uint8_t* slot, int row, const float (&v)[32]) {
+    const uint32_t base = smem_u32(slot) + row * 64;
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+        st_shared_v4(base + ((j ^ ((row >> 1) & 3)) << 4), pack_bf16(v[8 * j], v[8 * j + 1]),
+                     pack_bf16(v[8 * j + 2], v[8 * j + 3]), pack_bf16(v[8 * j + 4], v[8 * j + 5]),
+                     pack_bf16(v[8 * j + 6], v[8 * j + 7]));
+}
+
+// Drain this warp's 32 rows x BN_TILE columns of one accumulator tile.
+template <int BN_TILE>
+__device__ __forceinline__ void drain_tile(const Params& p, const CUtensorMap* md, const CUtensorMap* mu,
+                                           uint8_t* stg, int& slot_idx, uint32_t taddr, int row_base, long long rd,
+                                           long long cd, int col_tile0, int lane) {
+    const int row = row_base + lane;
+#pragma unroll 1
+    for (int c = 0; c < BN_TILE / 32; ++c) {
+        uint32_t rr[32];
+        tmem_ld_32x32b_x32(taddr + static_cast<uint32_t>(c * 32), rr);
+        tmem_ld_wait();
+        const int col0 = col_tile0 + c * 32;
+        if (col0 >= p.n) continue;  // warp-uniform
+        float v[32];
+#pragma unroll
+        for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(rr[j]) * p.alpha;
+        const long long off = (rd + row) * p.ldd + cd + col0;
+        if (!p.tma_epi) {
+            if (row < p.m) epilogue_chunk(p, v, off, min(32, p.n - col0));
+            continue;
+        }
+        uint8_t* slot = stg + slot_idx * kEpiSlot;
+        slot_idx ^= 1;
+        if (lane == 0) bulk_wait_read<1>();  // the store issued from this slot two chunks ago has read it
+        __syncwarp();
+        const bool row_ok = row < p.m;
+        const int gc = static_cast<int>(cd) + col0, gr = static_cast<int>(rd) + row_base;
+        switch (p.epi) {
+            case SWARM_EPI_STORE_F32:
+            case SWARM_EPI_ACCUM_F32:
+                stage_f32(slot, lane, v);
+                break;
+            case SWARM_EPI_RESIDUAL:
+                if (row_ok) {
+                    const uint4* r4 = reinterpret_cast<const uint4*>(static_cast<const __nv_bfloat16*>(p.aux) + off);
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        const uint4 w = r4[q];
+                        const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+                        for (int j = 0; j < 4; ++j) {
+                            v[q * 8 + 2 * j] += bf_lo(ws[j]);
+                            v[q * 8 + 2 * j + 1] += bf_hi(ws[j]);
+                        }
+                    }
+                }
+                stage_bf16(slot, lane, v);
+                break;
+            case SWARM_EPI_GELU:
+                stage_bf16(slot + 2048, lane, v);  // U = pre-activation
+#pragma unroll
+                for (int j = 0; j < 32; ++j) v[j] = gelu_f(v[j]);
+                stage_bf16(slot, lane, v);
+                break;
+            case SWARM_EPI_DGELU:
+                if (row_ok) {
+                    const uint4* u4 = reinterpret_cast<const uint4*>(static_cast<const __nv_bfloat16*>(p.aux) + off);
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        const uint4 w = u4[q];
+                        const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+                        for (int j = 0; j < 4; ++j) {
+                            v[q * 8 + 2 * j] *= dgelu_f(bf_lo(ws[j]));
+                            v[q * 8 + 2 * j + 1] *= dgelu_f(bf_hi(ws[j]));
+                        }
+                    }
+                }
+                stage_bf16(slot, lane, v);
+                break;
+            default:
+                stage_bf16(slot, lane, v);
+                break;
+        }
+        fence_async_smem();
+        __syncwarp();
+        if (lane == 0 && row_base < p.m) {
+            if (p.epi == SWARM_EPI_ACCUM_F32) tma_reduce_add_2d(md, slot, gc, gr);
+            else tma_store_2d(md, slot, gc, gr);
+            if (p.epi == SWARM_EPI_GELU) tma_store_2d(mu, slot + 2048, gc, gr);
+            bulk_commit();
+        }
+    }
+}
+
 template <int BN, bool A_MN, bool B_MN>
 __global__ void __launch_bounds__(kThreads, 1)
-    k_gemm(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUtensorMap tma_b, const Params p) {
+    k_gemm(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUtensorMap tma_b,
+           const __grid_constant__ CUtensorMap tma_d, const __grid_constant__ CUtensorMap tma_u, const Params p) {
     using C = Cfg<BN>;
     extern __shared__ uint8_t smem_raw[];
     const uint32_t raw = smem_u32(smem_raw);
     uint8_t* smem = smem_raw + ((1024 - (raw & 1023)) & 1023);
     uint8_t* sa = smem;
     uint8_t* sb = smem + C::STAGES * C::A_BYTES;
-    uint64_t* full = reinterpret_cast<uint64_t*>(sb + C::STAGES * C::B_BYTES);
+    uint8_t* stg_all = sb + C::STAGES * C::B_BYTES;  // epilogue staging, 1024-aligned
+    uint64_t* full = reinterpret_cast<uint64_t*>(stg_all + kEpiSmem);
     uint64_t* empty = full + C::STAGES;
     uint64_t* tfull = empty + C::STAGES;
     uint64_t* tempty = tfull + 2;
@@ -305,6 +415,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     } else if (warp >= 4) {
         // ------------------------------------------------ epilogue (TMEM -> HBM)
         const int q = warp - 4;  // TMEM lane quarter owned by this warp (warp % 4)
+        uint8_t* stg = stg_all + q * 2 * kEpiSlot;
+        int slot_idx = 0;
         int acc = 0;
         uint32_t acc_phase = 0;
         for (int t = blockIdx.x; t < p.total_tiles; t += gridDim.x) {
@@ -313,31 +425,18 @@ __global__ void __launch_bounds__(kThreads, 1)
             const int mt = r % p.tiles_m, nt = r / p.tiles_m;
             const int zb = z / p.bh, zh = z - zb * p.bh;
             const long long rd = p.rd0 * zb + p.rd1 * zh, cd = p.cd0 * zb + p.cd1 * zh;
-            const int row = mt * BM + q * 32 + lane;
             mbar_wait(&tfull[acc], acc_phase);
             tc_fence_after();
-#pragma unroll 1
-            for (int c = 0; c < BN / 32; ++c) {
-                uint32_t rr[32];
-                tmem_ld_32x32b_x32(tmem_base + (static_cast<uint32_t>(q * 32) << 16) +
-                                       static_cast<uint32_t>(acc * BN + c * 32),
-                                   rr);
-                tmem_ld_wait();
-                const int col0 = nt * BN + c * 32;
-                if (row < p.m && col0 < p.n) {
-                    float v[32];
-#pragma unroll
-                    for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(rr[j]) * p.alpha;
-                    const long long off = (rd + row) * p.ldd + cd + col0;
-                    epilogue_chunk(p, v, off, min(32, p.n - col0));
-                }
-            }
+            drain_tile<BN>(p, &tma_d, &tma_u, stg, slot_idx,
+                           tmem_base + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(acc * BN),
+                           mt * BM + q * 32, rd, cd, nt * BN, lane);
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(&tempty[acc]);
             acc ^= 1;
             if (acc == 0) acc_phase ^= 1;
         }
+        if (lane == 0) bulk_wait_all();  // TMA stores drained before the CTA exits
     }
     tc_fence_before();
     __syncthreads();
@@ -366,14 +465,16 @@ struct Cfg2 {
 
 template <bool A_MN, bool B_MN>
 __global__ void __launch_bounds__(kThreads, 1)
-    k_gemm2(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUtensorMap tma_b, const Params p) {
+    k_gemm2(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUtensorMap tma_b,
+            const __grid_constant__ CUtensorMap tma_d, const __grid_constant__ CUtensorMap tma_u, const Params p) {
     using C = Cfg2;
     extern __shared__ uint8_t smem_raw[];
     const uint32_t raw = smem_u32(smem_raw);
     uint8_t* smem = smem_raw + ((1024 - (raw & 1023)) & 1023);
     uint8_t* sa = smem;
     uint8_t* sb = smem + C::STAGES * C::A_BYTES;
-    uint64_t* full = reinterpret_cast<uint64_t*>(sb + C::STAGES * C::B_BYTES);
+    uint8_t* stg_all = sb + C::STAGES * C::B_BYTES;  // epilogue staging, 1024-aligned
+    uint64_t* full = reinterpret_cast<uint64_t*>(stg_all + kEpiSmem);
     uint64_t* empty = full + C::STAGES;
     uint64_t* tfull = empty + C::STAGES;
     uint64_t* tempty = tfull + 2;
@@ -489,6 +590,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         // ------------------------------------------------ epilogue (both CTAs, own 128 rows)
         const int q = warp - 4;
         const uint32_t tempty_leader[2] = {map_to_cta(&tempty[0], 0), map_to_cta(&tempty[1], 0)};
+        uint8_t* stg = stg_all + q * 2 * kEpiSlot;
+        int slot_idx = 0;
         int acc = 0;
         uint32_t acc_phase = 0;
         for (int t = cluster; t < p.total_tiles; t += n_clusters) {
@@ -497,31 +600,19 @@ __global__ void __launch_bounds__(kThreads, 1)
             const int mt = r % p.tiles_m, nt = r / p.tiles_m;
             const int zb = z / p.bh, zh = z - zb * p.bh;
             const long long rd = p.rd0 * zb + p.rd1 * zh, cd = p.cd0 * zb + p.cd1 * zh;
-            const int row = mt * 256 + static_cast<int>(rank) * 128 + q * 32 + lane;
             mbar_wait(&tfull[acc], acc_phase);
             tc_fence_after();
-#pragma unroll 1
-            for (int c = 0; c < PAIR_BN / 32; ++c) {
-                uint32_t rr[32];
-                tmem_ld_32x32b_x32(tmem_base + (static_cast<uint32_t>(q * 32) << 16) +
-                                       static_cast<uint32_t>(acc * PAIR_BN + c * 32),
-                                   rr);
-                tmem_ld_wait();
-                const int col0 = nt * PAIR_BN + c * 32;
-                if (row < p.m && col0 < p.n) {
-                    float v[32];
-#pragma unroll
-                    for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(rr[j]) * p.alpha;
-                    const long long off = (rd + row) * p.ldd + cd + col0;
-                    epilogue_chunk(p, v, off, min(32, p.n - col0));
-                }
-            }
+            drain_tile<PAIR_BN>(p, &tma_d, &tma_u, stg, slot_idx,
+                                tmem_base + (static_cast<uint32_t>(q * 32) << 16) +
+                                    static_cast<uint32_t>(acc * PAIR_BN),
+                                mt * 256 + static_cast<int>(rank) * 128 + q * 32, rd, cd, nt * PAIR_BN, lane);
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive_cluster(tempty_leader[acc]);
             acc ^= 1;
             if (acc == 0) acc_phase ^= 1;
         }
+        if (lane == 0) bulk_wait_all();
     }
     tc_fence_before();
     cluster_sync();  // both CTAs finished every MMA / TMEM read before the pair frees TMEM
@@ -609,6 +700,30 @@ int encode_2d_uncached(CUtensorMap* m, const void* ptr, long long rows, long lon
     return SWARM_OK;
 }
 
+// Output map for the TMA epilogue: 32 x 32 boxes, fp32 (128-B rows, SWIZZLE_128B)
+// or bf16 (64-B rows, SWIZZLE_64B), matching stage_f32 / stage_bf16.
+int encode_2d_out(CUtensorMap* m, const void* ptr, long long rows, long long cols, long long ld, bool f32) {
+    EncodeFn enc = get_encode();
+    if (!enc) return SWARM_E_CUDA;
+    const cuuint64_t dims[2] = {static_cast<cuuint64_t>(cols), static_cast<cuuint64_t>(rows)};
+    const cuuint64_t strides[1] = {static_cast<cuuint64_t>(ld) * (f32 ? 4 : 2)};
+    const cuuint32_t box[2] = {32, 32};
+    const cuuint32_t estr[2] = {1, 1};
+    const CUresult r = enc(m, f32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2,
+                           const_cast<void*>(ptr), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                           f32 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B,
+                           CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS ? SWARM_OK : SWARM_E_INVALID;
+}
+
+bool tma_epi_enabled() {
+    static const bool on = [] {
+        const char* e = getenv("SWARM_GEMM_TMA_EPI");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
+
 int num_sms() {
     static int n = 0;
     if (n == 0) {
@@ -621,7 +736,8 @@ int num_sms() {
 }
 
 template <int BN, bool A_MN, bool B_MN>
-int launch(const CUtensorMap& ta, const CUtensorMap& tb, const Params& p, cudaStream_t st) {
+int launch(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& td, const CUtensorMap& tu, const Params& p,
+           cudaStream_t st) {
     auto kern = k_gemm<BN, A_MN, B_MN>;
     static bool attr = false;
     if (!attr) {
@@ -629,13 +745,14 @@ int launch(const CUtensorMap& ta, const CUtensorMap& tb, const Params& p, cudaSt
         attr = true;
     }
     const int grid = std::min(p.total_tiles, num_sms());
-    kern<<<grid, kThreads, Cfg<BN>::SMEM, st>>>(ta, tb, p);
+    kern<<<grid, kThreads, Cfg<BN>::SMEM, st>>>(ta, tb, td, tu, p);
     SWARM_LAUNCH_CHECK("k_gemm");
     return SWARM_OK;
 }
 
 template <bool A_MN, bool B_MN>
-int launch_pair(const CUtensorMap& ta, const CUtensorMap& tb, const Params& p, cudaStream_t st) {
+int launch_pair(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& td, const CUtensorMap& tu,
+                const Params& p, cudaStream_t st) {
     auto kern = k_gemm2<A_MN, B_MN>;
     static bool attr = false;
     if (!attr) {
@@ -654,17 +771,17 @@ int launch_pair(const CUtensorMap& ta, const CUtensorMap& tb, const Params& p, c
     attrs[0].val.clusterDim.z = 1;
     cfg.attrs = attrs;
     cfg.numAttrs = 1;
-    SWARM_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, ta, tb, p));
+    SWARM_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, ta, tb, td, tu, p));
     SWARM_LAUNCH_CHECK("k_gemm2");
     return SWARM_OK;
 }
 
-int dispatch_pair(bool amn, bool bmn, const CUtensorMap& ta, const CUtensorMap& tb, const Params& p,
-                  cudaStream_t st) {
-    if (!amn && !bmn) return launch_pair<false, false>(ta, tb, p, st);
-    if (!amn && bmn) return launch_pair<false, true>(ta, tb, p, st);
-    if (amn && !bmn) return launch_pair<true, false>(ta, tb, p, st);
-    return launch_pair<true, true>(ta, tb, p, st);
+int dispatch_pair(bool amn, bool bmn, const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& td,
+                  const CUtensorMap& tu, const Params& p, cudaStream_t st) {
+    if (!amn && !bmn) return launch_pair<false, false>(ta, tb, td, tu, p, st);
+    if (!amn && bmn) return launch_pair<false, true>(ta, tb, td, tu, p, st);
+    if (amn && !bmn) return launch_pair<true, false>(ta, tb, td, tu, p, st);
+    return launch_pair<true, true>(ta, tb, td, tu, p, st);
 }
 
 bool pair_enabled() {
@@ -676,11 +793,12 @@ bool pair_enabled() {
 }
 
 template <int BN>
-int dispatch(bool amn, bool bmn, const CUtensorMap& ta, const CUtensorMap& tb, const Params& p, cudaStream_t st) {
-    if (!amn && !bmn) return launch<BN, false, false>(ta, tb, p, st);
-    if (!amn && bmn) return launch<BN, false, true>(ta, tb, p, st);
-    if (amn && !bmn) return launch<BN, true, false>(ta, tb, p, st);
-    return launch<BN, true, true>(ta, tb, p, st);
+int dispatch(bool amn, bool bmn, const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& td,
+             const CUtensorMap& tu, const Params& p, cudaStream_t st) {
+    if (!amn && !bmn) return launch<BN, false, false>(ta, tb, td, tu, p, st);
+    if (!amn && bmn) return launch<BN, false, true>(ta, tb, td, tu, p, st);
+    if (amn && !bmn) return launch<BN, true, false>(ta, tb, td, tu, p, st);
+    return launch<BN, true, true>(ta, tb, td, tu, p, st);
 }
 
 }  // namespace gemm
@@ -740,8 +858,24 @@ extern "C" int swarm_gemm_bf16(const swarm_gemm_args* a, swarm_stream_t stream) 
     const bool cd_ok = (a->cd0 % vec_elems == 0) && (a->cd1 % vec_elems == 0);
     p.vec_ok = (a->ldd % vec_elems == 0) && cd_ok && ((reinterpret_cast<uintptr_t>(a->d) & 15) == 0) &&
                (!a->aux || (reinterpret_cast<uintptr_t>(a->aux) & 15) == 0);
+    // TMA-store epilogue: output extents from the batch offsets; exact tiles or
+    // a single batch (so TMA's bounds clipping never writes another batch's rows)
+    const int nb = (a->batch + a->bh - 1) / a->bh;
+    const long long d_rows = static_cast<long long>(a->rd0) * (nb - 1) + static_cast<long long>(a->rd1) * (a->bh - 1) + a->m;
+    const long long d_cols = static_cast<long long>(a->cd0) * (nb - 1) + static_cast<long long>(a->cd1) * (a->bh - 1) + a->n;
+    const bool exact = (a->m % TM == 0) && (a->n % 32 == 0);
+    p.tma_epi = tma_epi_enabled() && (a->batch == 1 || exact) && d_cols <= a->ldd &&
+                ((reinterpret_cast<uintptr_t>(a->d) & 15) == 0) && ((a->ldd * esz) % 16 == 0) &&
+                (!a->aux || (reinterpret_cast<uintptr_t>(a->aux) & 15) == 0);
+    CUtensorMap td{}, tu{};
+    if (p.tma_epi) {
+        const bool f32 = esz == 4;
+        rc = encode_2d_out(&td, a->d, d_rows, d_cols, a->ldd, f32);
+        if (rc == SWARM_OK && a->epilogue == SWARM_EPI_GELU) rc = encode_2d_out(&tu, a->aux, d_rows, d_cols, a->ldd, false);
+        if (rc != SWARM_OK) p.tma_epi = 0;  // fall back to direct stores
+    }
     cudaStream_t st = as_stream(stream);
-    if (pair) return dispatch_pair(a->a_mn_major, a->b_mn_major, ta, tb, p, st);
-    if (BN == 128) return dispatch<128>(a->a_mn_major, a->b_mn_major, ta, tb, p, st);
-    return dispatch<256>(a->a_mn_major, a->b_mn_major, ta, tb, p, st);
+    if (pair) return dispatch_pair(a->a_mn_major, a->b_mn_major, ta, tb, td, tu, p, st);
+    if (BN == 128) return dispatch<128>(a->a_mn_major, a->b_mn_major, ta, tb, td, tu, p, st);
+    return dispatch<256>(a->a_mn_major, a->b_mn_major, ta, tb, td, tu, p, st);
 }

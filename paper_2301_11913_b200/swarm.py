@@ -199,6 +199,9 @@ class SwarmPipeline:
         self.profile = profile
         self.use_graphs = use_graphs
         self.graphs: dict = {}
+        self.graph_kernels: dict = {}  # kernels captured per graph (for gpu_launches)
+        self.captured_kernels = 0      # launches counted while capturing (they did not run then)
+        self.replayed_kernels = 0
         self._warm: set = set()
         self._profiled: set = set()
         self.wire_bytes = next(iter(self.stages.values())).wire_bytes
@@ -258,11 +261,16 @@ class SwarmPipeline:
             return
         g = self.graphs.get(key)
         if g is None:
+            n0 = L.lib().swarm_launch_count()
             g = torch.cuda.CUDAGraph()
             with torch.cuda.graph(g):
                 fn()
+            n = L.lib().swarm_launch_count() - n0
+            self.graph_kernels[key] = n
+            self.captured_kernels += n
             self.graphs[key] = g
         g.replay()
+        self.replayed_kernels += self.graph_kernels[key]
 
     def _fwd(self, s, slot, inp, out=None, targets=None, scale=1.0) -> None:
         st = self.stages[s]
@@ -349,6 +357,11 @@ class SwarmPipeline:
             a, b, c = st.profile_read()
             ms, fl, n = ms + a, fl + b, n + c
         return ms, fl, n
+
+    def kernels_launched(self) -> int:
+        """Kernels of libswarm_b200.so that actually ran: eager launches plus
+        the kernel nodes of every replayed visit graph."""
+        return L.lib().swarm_launch_count() - self.captured_kernels + self.replayed_kernels
 
     def tokens_per_step(self) -> int:
         return self.M * self.m.tokens
