@@ -59,6 +59,8 @@ struct Cfg {
     static constexpr int STAGES = BN == 256 ? 4 : 6;
     static constexpr int TMEM_COLS = 2 * BN;
     static constexpr int SMEM = STAGES * (A_BYTES + B_BYTES) + kEpiSmem + 1024 + 256;
+    static_assert(SMEM <= 232448, "GEMM exceeds the 227 KB dynamic smem limit");
+    static_assert(2 * STAGES * 8 + 4 * 8 + 4 <= 256, "barrier area overflow");
 };
 
 __device__ __forceinline__ float gelu_f(float x) {
@@ -460,7 +462,9 @@ struct Cfg2 {
     static constexpr int B_BYTES = 128 * BK * 2;  // this CTA's half of B
     static constexpr int STAGES = 6;
     static constexpr int TMEM_COLS = 2 * PAIR_BN;
-    static constexpr int SMEM = STAGES * (A_BYTES + B_BYTES) + 1024 + 256;
+    static constexpr int SMEM = STAGES * (A_BYTES + B_BYTES) + kEpiSmem + 1024 + 256;
+    static_assert(SMEM <= 232448, "pair GEMM exceeds the 227 KB dynamic smem limit");
+    static_assert(2 * STAGES * 8 + 4 * 8 + 4 <= 256, "barrier area overflow");
 };
 
 template <bool A_MN, bool B_MN>
