@@ -8,6 +8,7 @@
 #include <cuda_runtime.h>
 
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <new>
 #include <string>
@@ -61,6 +62,7 @@ struct swarm_stage {
     void* lnws = nullptr;
     std::vector<void*> allocations;
     int step = 0;
+    bool fused_attn = false;  // scores+softmax in one tcgen05 kernel (csrc/attention.cu)
     // GEMM profiling (bench.py's live roofline): event pairs around each GEMM
     bool prof_on = false;
     std::vector<cudaEvent_t> prof_events;
@@ -221,10 +223,16 @@ int block_forward(swarm_stage* s, Act& A, bf16* y, const LayerW& W, cudaStream_t
     TRY(mm(T, 3 * d, d, {A.a, d, T, d, false}, {p16 + W.wqkv, d, 3 * d, d, false}, A.qkv, 3 * d,
            SWARM_EPI_STORE_BF16, nullptr, 1.f, st));
     const float scale = 1.f / std::sqrt(static_cast<float>(dh));
-    // S = scale * Q K^T per (b, h)
-    TRY(bmm(s, L, L, dh, {{A.qkv, 3 * d, T, d, false}, L, 0, 0, dh}, {{A.qkv + d, 3 * d, T, d, false}, L, 0, 0, dh},
-            s->S, L, H * L, L, 0, 0, SWARM_EPI_STORE_F32, scale, st));
-    TRY(swarm_attn_softmax_forward(s->S, static_cast<size_t>(s->B) * H * L, L, s->cfg.causal, A.P, st));
+    if (s->fused_attn) {
+        // P = softmax(scale * Q K^T) per (b, h), scores kept in TMEM
+        TRY(swarm_attn_scores_softmax(A.qkv, A.qkv + d, 3 * d, d, s->B, H, L, dh, scale, s->cfg.causal, A.P, st));
+    } else {
+        // S = scale * Q K^T per (b, h), then a row softmax
+        TRY(bmm(s, L, L, dh, {{A.qkv, 3 * d, T, d, false}, L, 0, 0, dh},
+                {{A.qkv + d, 3 * d, T, d, false}, L, 0, 0, dh}, s->S, L, H * L, L, 0, 0, SWARM_EPI_STORE_F32, scale,
+                st));
+        TRY(swarm_attn_softmax_forward(s->S, static_cast<size_t>(s->B) * H * L, L, s->cfg.causal, A.P, st));
+    }
     // O = P V  (V read MN-major straight from the qkv buffer)
     TRY(bmm(s, L, dh, L, {{A.P, L, s->B * H * L, L, false}, H * L, L, 0, 0},
             {{A.qkv + 2 * d, 3 * d, T, d, true}, L, 0, 0, dh}, A.o, d, L, 0, 0, dh, SWARM_EPI_STORE_BF16, 1.f, st));
@@ -259,10 +267,16 @@ int block_backward(swarm_stage* s, const Act& A, const bf16* dy, bf16* dx, const
            st));
     TRY(mm(d, d, T, {s->dhid, d, T, d, true}, {A.o, d, T, d, true}, G + W.wo, d, SWARM_EPI_ACCUM_F32, nullptr, 1.f, st));
     // dP = dO V^T ; dS = scale * P (dP - rowsum(P dP))
-    TRY(bmm(s, L, L, dh, {{s->dO, d, T, d, false}, L, 0, 0, dh}, {{A.qkv + 2 * d, 3 * d, T, d, false}, L, 0, 0, dh},
-            s->dP, L, H * L, L, 0, 0, SWARM_EPI_STORE_F32, 1.f, st));
     const float scale = 1.f / std::sqrt(static_cast<float>(dh));
-    TRY(swarm_attn_softmax_backward(A.P, s->dP, BHL, L, scale, s->dS, st));
+    if (s->fused_attn) {
+        TRY(swarm_attn_scores_softmax_backward(s->dO, d, A.qkv + 2 * d, 3 * d, d, A.P, s->B, H, L, dh, scale,
+                                               s->cfg.causal, s->dS, st));
+    } else {
+        TRY(bmm(s, L, L, dh, {{s->dO, d, T, d, false}, L, 0, 0, dh},
+                {{A.qkv + 2 * d, 3 * d, T, d, false}, L, 0, 0, dh}, s->dP, L, H * L, L, 0, 0, SWARM_EPI_STORE_F32,
+                1.f, st));
+        TRY(swarm_attn_softmax_backward(A.P, s->dP, BHL, L, scale, s->dS, st));
+    }
     // dQ = dS K ; dK = dS^T Q ; dV = P^T dO   (all read in place, written into dqkv)
     TRY(bmm(s, L, dh, L, {{s->dS, L, BHL, L, false}, H * L, L, 0, 0}, {{A.qkv + d, 3 * d, T, d, true}, L, 0, 0, dh},
             s->dqkv, 3 * d, L, 0, 0, dh, SWARM_EPI_STORE_BF16, 1.f, st));
@@ -406,9 +420,15 @@ int create(const swarm_stage_config* c, swarm_stage* s) {
         }
         if (c->is_first) TRY(alloc(s, &sl.tokens, T));
     }
-    // workspaces
-    TRY(alloc(s, &s->S, BHLL));
-    TRY(alloc(s, &s->dP, BHLL));
+    // workspaces (fp32 scores only for the unfused attention path)
+    {
+        const char* e = getenv("SWARM_ATTN_FUSED");
+        s->fused_attn = !(e && e[0] == '0') && s->L % 128 == 0 && s->L <= 512 && s->dh % 64 == 0 && s->dh <= 128;
+    }
+    if (!s->fused_attn) {
+        TRY(alloc(s, &s->S, BHLL));
+        TRY(alloc(s, &s->dP, BHLL));
+    }
     TRY(alloc(s, &s->dS, BHLL));
     TRY(alloc(s, &s->gy[0], Td));
     TRY(alloc(s, &s->gy[1], Td));

@@ -1,0 +1,77 @@
+"""GPU numerics: fused attention-score kernels vs a torch fp32 reference of the
+same op on the same bf16 inputs.  Tolerances: P and dS are bf16 outputs
+(rounding 2^-8 relative) of fp32 math: atol 4e-3 on P (entries <= 1), rtol 2e-2 /
+atol 2e-3*max|dS| on dS."""
+import ctypes as C
+import math
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def ref_P(qkv, B, H, L, dh, causal):
+    import torch
+    d = H * dh
+    q = qkv[:, :d].float().view(B, L, H, dh).transpose(1, 2)
+    k = qkv[:, d:2 * d].float().view(B, L, H, dh).transpose(1, 2)
+    s = (q @ k.transpose(-1, -2)) / math.sqrt(dh)
+    if causal:
+        s = s.masked_fill(torch.triu(torch.ones(L, L, dtype=torch.bool, device=s.device), 1), float("-inf"))
+    return torch.softmax(s, -1).reshape(B * H * L, L)
+
+
+@pytest.mark.parametrize("B,H,L,dh,causal", [(2, 4, 512, 128, 1), (2, 4, 512, 128, 0), (2, 2, 128, 64, 1),
+                                             (1, 3, 256, 128, 1), (1, 2, 384, 64, 0)])
+def test_fused_scores_softmax(cuda, B, H, L, dh, causal):
+    import torch
+    from paper_2301_11913_b200 import _lib
+    torch.manual_seed(L + dh + causal)
+    d = H * dh
+    qkv = (torch.randn(B * L, 3 * d, device="cuda") * 2).bfloat16()
+    P = torch.empty(B * H * L, L, device="cuda", dtype=torch.bfloat16)
+    scale = 1 / math.sqrt(dh)
+    st = torch.cuda.current_stream().cuda_stream
+    rc = _lib.lib().swarm_attn_scores_softmax(C.c_void_p(qkv.data_ptr()), C.c_void_p(qkv[:, d:].data_ptr()), 3 * d, d,
+                                              B, H, L, dh, scale, causal, C.c_void_p(P.data_ptr()), st)
+    assert rc == 0, _lib.last_error()
+    ref = ref_P(qkv, B, H, L, dh, causal)
+    torch.testing.assert_close(P.float(), ref, rtol=0, atol=4e-3)
+    # backward: dS = scale * P * (dP - rowsum(P dP)), dP = dO V^T (with the kernel's own bf16 P)
+    dO = torch.randn(B * L, d, device="cuda").bfloat16()
+    dS = torch.empty_like(P)
+    rc = _lib.lib().swarm_attn_scores_softmax_backward(C.c_void_p(dO.data_ptr()), d, C.c_void_p(qkv[:, 2 * d:].data_ptr()),
+                                                       3 * d, d, C.c_void_p(P.data_ptr()), B, H, L, dh, scale, causal,
+                                                       C.c_void_p(dS.data_ptr()), st)
+    assert rc == 0, _lib.last_error()
+    v = qkv[:, 2 * d:].float().view(B, L, H, dh).transpose(1, 2)
+    do = dO.float().view(B, L, H, dh).transpose(1, 2)
+    dP = (do @ v.transpose(-1, -2)).reshape(B * H * L, L)
+    Pf = P.float()
+    want = scale * Pf * (dP - (Pf * dP).sum(-1, keepdim=True))
+    torch.testing.assert_close(dS.float(), want, rtol=2e-2, atol=2e-3 * float(want.abs().max()))
+
+
+def test_fused_matches_unfused_path(cuda):
+    """The fused kernel reproduces the executor's previous GEMM + softmax kernels."""
+    import torch
+    from paper_2301_11913_b200 import _lib, ops
+    B, H, L, dh = 2, 4, 512, 128
+    d = H * dh
+    torch.manual_seed(3)
+    qkv = torch.randn(B * L, 3 * d, device="cuda").bfloat16()
+    st = torch.cuda.current_stream().cuda_stream
+    P1 = torch.empty(B * H * L, L, device="cuda", dtype=torch.bfloat16)
+    _lib.lib().swarm_attn_scores_softmax(C.c_void_p(qkv.data_ptr()), C.c_void_p(qkv[:, d:].data_ptr()), 3 * d, d, B, H,
+                                         L, dh, 1 / math.sqrt(dh), 1, C.c_void_p(P1.data_ptr()), st)
+    S = torch.empty(B * H * L, L, device="cuda")
+    g = _lib.GemmArgs()
+    g.m, g.n, g.k, g.batch, g.bh = L, L, dh, B * H, H
+    g.a, g.lda, g.a_rows, g.a_cols, g.ra0, g.ca1 = qkv.data_ptr(), 3 * d, B * L, d, L, dh
+    g.b, g.ldb, g.b_rows, g.b_cols, g.rb0, g.cb1 = qkv[:, d:].data_ptr(), 3 * d, B * L, d, L, dh
+    g.d, g.ldd, g.rd0, g.rd1 = S.data_ptr(), L, H * L, L
+    g.alpha, g.epilogue = 1 / math.sqrt(dh), _lib.EPI_STORE_F32
+    ops.gemm_raw(g)
+    P2 = torch.empty_like(P1)
+    _lib.lib().swarm_attn_softmax_forward(C.c_void_p(S.data_ptr()), B * H * L, L, 1, C.c_void_p(P2.data_ptr()), st)
+    torch.testing.assert_close(P1.float(), P2.float(), rtol=0, atol=4e-3)
