@@ -209,6 +209,8 @@ typedef struct {
     int max_slots;     /* microbatches in flight (activation slots) */
     int wire;          /* SWARM_WIRE_BF16 | SWARM_WIRE_INT8 */
     int block_size;    /* int8 codec block */
+    int maxout_k;      /* > 1: maxout bottleneck at the boundaries: the sender sends
+                          maxout_k(LN(y)) (d/k wide), the receiver applies LN then W_d (d/k -> d) */
     float lr, beta1, beta2, eps, weight_decay, init_std;
     uint64_t seed;
 } swarm_stage_config;

@@ -12,7 +12,9 @@ stated tolerance:
   * MLP(x) = sigma(x w1) w2 + x with sigma = GeLU (tanh form), PAPER:787;
   * causal multi-head attention with 1/sqrt(d_head) scaling;
   * first stage: token embedding; last stage: final LN, LM head, token
-    cross-entropy summed over tokens and scaled by `loss_scale`.
+    cross-entropy summed over tokens and scaled by `loss_scale` (PAPER:362);
+  * optional maxout bottleneck at the boundaries: the sender
+    emits maxout_k(LN(x)), the receiver applies LN then W_d (d/k -> d).
 It runs in float64 on the CPU with torch autograd for the backward.
 """
 from __future__ import annotations
@@ -56,13 +58,22 @@ def stage(params: dict, cfg, inp, targets=None, loss_scale=1.0):
     caller wants).  inp: int64 tokens [T] on the first stage, else float64 [T, d].
     Returns (output [T, d], loss or None)."""
     B, L, H = cfg.micro_batch, cfg.seq_len, cfg.n_heads
-    x = params["embedding"][inp] if cfg.is_first else inp
+    mk = getattr(cfg, "maxout_k", 0)
+    if cfg.is_first:
+        x = params["embedding"][inp]
+    elif mk > 1:  # receiving side of the maxout bottleneck: LN then W_d (PAPER:803-806)
+        x = layer_norm(inp, params["bneck_in_ln_g"], params["bneck_in_ln_b"]) @ params["bneck_wd"].T
+    else:
+        x = inp
     nw = 1 if cfg.shared_layers else cfg.n_layers
     for l in range(cfg.n_layers):
         i = 0 if nw == 1 else l
         W = {k: params[f"layer{i}.{k}"] for k in ("wqkv", "wo", "w1", "w2", "ln1_g", "ln1_b", "ln2_g", "ln2_b")}
         x = block(x, W, B, L, H, bool(cfg.causal))
     if not cfg.is_last:
+        if mk > 1:  # sending side: maxout_k(LN(x)) over windows of k consecutive features
+            z = layer_norm(x, params["bneck_out_ln_g"], params["bneck_out_ln_b"])
+            return z.reshape(z.shape[0], -1, mk).max(-1).values, None
         return x, None
     xf = layer_norm(x, params["lnf_g"], params["lnf_b"])
     logits = xf @ params["head"].T

@@ -31,7 +31,7 @@ class GemmArgs(C.Structure):
 class StageConfigC(C.Structure):
     _fields_ = [(n, C.c_int) for n in ("d_model", "n_heads", "d_ffn", "seq_len", "micro_batch", "n_layers",
                                        "shared_layers", "vocab", "is_first", "is_last", "causal", "max_slots", "wire",
-                                       "block_size")] + \
+                                       "block_size", "maxout_k")] + \
                [(n, C.c_float) for n in ("lr", "beta1", "beta2", "eps", "weight_decay", "init_std")] + \
                [("seed", C.c_uint64)]
 

@@ -41,6 +41,14 @@ struct Slot {
     float *muf, *rsf;
     bf16* dxf;               // d loss / d xf, produced by the fused LM-head backward
     int32_t* tokens;         // first stage: the microbatch's token ids (embedding backward)
+    // maxout bottleneck: sender keeps LN_c(out), its stats and the argmax;
+    // receiver keeps the dequantized wire tensor, LN_d of it and its stats
+    bf16* z;
+    float *muc, *rsc;
+    bf16* mo;
+    uint8_t* am;
+    bf16 *mi, *ni;
+    float *mud, *rsd;
 };
 
 }  // namespace
@@ -52,13 +60,16 @@ struct swarm_stage {
     std::vector<TensorInfo> tensors;
     std::vector<LayerW> layers;
     size_t emb = 0, lnfg = 0, lnfb = 0, head = 0;
+    bool bneck = false;  // maxout bottleneck at the boundaries
+    int wire_w = 0;      // features per token on the wire (d, or d / maxout_k)
+    size_t bn_in_g = 0, bn_in_b = 0, bn_wd = 0, bn_out_g = 0, bn_out_b = 0;
     float *p32 = nullptr, *grad = nullptr, *m = nullptr, *v = nullptr;
     bf16* p16 = nullptr;
     std::vector<Slot> slots;
     // workspaces (one visit at a time per stage)
     float *S = nullptr, *dP = nullptr, *logits = nullptr;
     bf16 *dS = nullptr, *gy[2] = {nullptr, nullptr}, *dhid = nullptr, *dc = nullptr, *du = nullptr, *dqkv = nullptr,
-         *dO = nullptr, *da = nullptr, *dlogits = nullptr;
+         *dO = nullptr, *da = nullptr, *dlogits = nullptr, *wtmp = nullptr;
     void* lnws = nullptr;
     std::vector<void*> allocations;
     int step = 0;
@@ -296,7 +307,7 @@ int block_backward(swarm_stage* s, const Act& A, const bf16* dy, bf16* dx, const
 }
 
 size_t wire_bytes(const swarm_stage* s) {
-    const size_t n = static_cast<size_t>(s->T) * s->d;
+    const size_t n = static_cast<size_t>(s->T) * s->wire_w;
     if (s->cfg.wire == SWARM_WIRE_INT8) {
         const size_t bs = static_cast<size_t>(s->cfg.block_size);
         return ((n + 15) & ~size_t(15)) + ((n + bs - 1) / bs) * sizeof(float);
@@ -305,7 +316,7 @@ size_t wire_bytes(const swarm_stage* s) {
 }
 
 int wire_decode(swarm_stage* s, const void* msg, bf16* out, cudaStream_t st) {
-    const size_t n = static_cast<size_t>(s->T) * s->d;
+    const size_t n = static_cast<size_t>(s->T) * s->wire_w;
     if (s->cfg.wire == SWARM_WIRE_INT8) {
         const int8_t* codes = static_cast<const int8_t*>(msg);
         const void* scales = static_cast<const char*>(msg) + ((n + 15) & ~size_t(15));
@@ -317,7 +328,7 @@ int wire_decode(swarm_stage* s, const void* msg, bf16* out, cudaStream_t st) {
 }
 
 int wire_encode(swarm_stage* s, const bf16* x, void* msg, cudaStream_t st) {
-    const size_t n = static_cast<size_t>(s->T) * s->d;
+    const size_t n = static_cast<size_t>(s->T) * s->wire_w;
     if (s->cfg.wire == SWARM_WIRE_INT8) {
         int8_t* codes = static_cast<int8_t*>(msg);
         void* scales = static_cast<char*>(msg) + ((n + 15) & ~size_t(15));
@@ -366,7 +377,16 @@ int create(const swarm_stage_config* c, swarm_stage* s) {
     if (c->wire == SWARM_WIRE_INT8 && c->block_size <= 0) return fail("stage: block_size must be positive");
     const int d = s->d, F = s->F;
     // parameter layout
+    s->bneck = c->maxout_k > 1;
+    if (s->bneck && (d % c->maxout_k || (d / c->maxout_k) % 64 || c->maxout_k > 255))
+        return fail("stage: maxout_k must divide d_model into a multiple of 64");
+    s->wire_w = s->bneck ? d / c->maxout_k : d;
     if (c->is_first) s->emb = add_tensor(s, "embedding", s->V, d);
+    if (s->bneck && !c->is_first) {  // receiving side of the bottleneck
+        s->bn_in_g = add_tensor(s, "bneck_in_ln_g", 1, s->wire_w);
+        s->bn_in_b = add_tensor(s, "bneck_in_ln_b", 1, s->wire_w);
+        s->bn_wd = add_tensor(s, "bneck_wd", d, s->wire_w);
+    }
     const int nw = c->shared_layers ? 1 : c->n_layers;
     for (int l = 0; l < nw; ++l) {
         const std::string p = "layer" + std::to_string(l) + ".";
@@ -380,6 +400,10 @@ int create(const swarm_stage_config* c, swarm_stage* s) {
         w.ln2g = add_tensor(s, p + "ln2_g", 1, d);
         w.ln2b = add_tensor(s, p + "ln2_b", 1, d);
         s->layers.push_back(w);
+    }
+    if (s->bneck && !c->is_last) {  // sending side
+        s->bn_out_g = add_tensor(s, "bneck_out_ln_g", 1, d);
+        s->bn_out_b = add_tensor(s, "bneck_out_ln_b", 1, d);
     }
     if (c->is_last) {
         s->lnfg = add_tensor(s, "lnf_g", 1, d);
@@ -419,6 +443,19 @@ int create(const swarm_stage_config* c, swarm_stage* s) {
             TRY(alloc(s, &sl.dxf, Td));
         }
         if (c->is_first) TRY(alloc(s, &sl.tokens, T));
+        if (s->bneck && !c->is_last) {
+            TRY(alloc(s, &sl.z, Td));
+            TRY(alloc(s, &sl.muc, T));
+            TRY(alloc(s, &sl.rsc, T));
+            TRY(alloc(s, &sl.mo, T * s->wire_w));
+            TRY(alloc(s, &sl.am, T * s->wire_w));
+        }
+        if (s->bneck && !c->is_first) {
+            TRY(alloc(s, &sl.mi, T * s->wire_w));
+            TRY(alloc(s, &sl.ni, T * s->wire_w));
+            TRY(alloc(s, &sl.mud, T));
+            TRY(alloc(s, &sl.rsd, T));
+        }
     }
     // workspaces (fp32 scores only for the unfused attention path)
     {
@@ -438,6 +475,7 @@ int create(const swarm_stage_config* c, swarm_stage* s) {
     TRY(alloc(s, &s->dqkv, 3 * Td));
     TRY(alloc(s, &s->dO, Td));
     TRY(alloc(s, &s->da, Td));
+    TRY(alloc(s, &s->wtmp, T * s->wire_w));
     TRY(dmalloc(s, &s->lnws, swarm_layer_norm_backward_workspace(T, d)));
     if (c->is_last) {
         TRY(alloc(s, &s->logits, T * s->V));
@@ -547,6 +585,14 @@ int swarm_stage_forward(swarm_stage_t s, int slot, const void* in, const int32_t
         if (cudaMemcpyAsync(sl.tokens, in, T * sizeof(int32_t), cudaMemcpyDeviceToDevice, st) != cudaSuccess)
             return SWARM_E_CUDA;
         TRY(swarm_embedding_forward(sl.tokens, T, s->p16 + s->emb, s->V, d, sl.layer[0].x, st));
+    } else if (s->bneck) {
+        // receiver: x0 = LN_d(dequant(wire)) W_d^T   (d/k -> d)
+        const int w = s->wire_w;
+        TRY(wire_decode(s, in, sl.mi, st));
+        TRY(swarm_layer_norm_forward(sl.mi, SWARM_DTYPE_BF16, T, w, s->p32 + s->bn_in_g, s->p32 + s->bn_in_b, 1e-5,
+                                     sl.ni, sl.mud, sl.rsd, st));
+        TRY(mm(T, d, w, {sl.ni, w, T, w, false}, {s->p16 + s->bn_wd, w, d, w, false}, sl.layer[0].x, d,
+               SWARM_EPI_STORE_BF16, nullptr, 1.f, st));
     } else {
         TRY(wire_decode(s, in, sl.layer[0].x, st));
     }
@@ -556,7 +602,13 @@ int swarm_stage_forward(swarm_stage_t s, int slot, const void* in, const int32_t
     }
     if (!s->cfg.is_last) {
         if (!out) return fail("forward: null output message");
-        return wire_encode(s, sl.out, out, st);
+        if (!s->bneck) return wire_encode(s, sl.out, out, st);
+        // sender: wire = int8(maxout_k(LN_c(out)))
+        TRY(swarm_layer_norm_forward(sl.out, SWARM_DTYPE_BF16, T, d, s->p32 + s->bn_out_g, s->p32 + s->bn_out_b, 1e-5,
+                                     sl.z, sl.muc, sl.rsc, st));
+        TRY(swarm_maxout_forward(sl.z, SWARM_DTYPE_BF16, static_cast<size_t>(T) * d, s->cfg.maxout_k, sl.mo, sl.am,
+                                 st));
+        return wire_encode(s, sl.mo, out, st);
     }
     if (!targets) return fail("forward: last stage needs targets");
     // final LN + LM head + cross-entropy, with the head's backward fused in
@@ -584,7 +636,17 @@ int swarm_stage_backward(swarm_stage_t s, int slot, const void* grad_in, void* g
                                       s->gy[0], s->grad + s->lnfg, s->grad + s->lnfb, 1, s->lnws, st));
     } else {
         if (!grad_in) return fail("backward: null gradient message");
-        TRY(wire_decode(s, grad_in, s->gy[0], st));
+        if (s->bneck) {
+            // d out = LN_c'(maxout'(dequant(grad)))
+            TRY(wire_decode(s, grad_in, s->wtmp, st));
+            TRY(swarm_maxout_backward(s->wtmp, SWARM_DTYPE_BF16, sl.am, static_cast<size_t>(T) * s->wire_w,
+                                      s->cfg.maxout_k, s->dc, st));
+            TRY(swarm_layer_norm_backward(s->dc, sl.out, SWARM_DTYPE_BF16, T, d, s->p32 + s->bn_out_g, sl.muc, sl.rsc,
+                                          nullptr, s->gy[0], s->grad + s->bn_out_g, s->grad + s->bn_out_b, 1, s->lnws,
+                                          st));
+        } else {
+            TRY(wire_decode(s, grad_in, s->gy[0], st));
+        }
     }
     for (int l = n - 1; l >= 0; --l) {
         TRY(block_backward(s, sl.layer[l], s->gy[cur], s->gy[cur ^ 1], weights(s, l), st));
@@ -592,7 +654,17 @@ int swarm_stage_backward(swarm_stage_t s, int slot, const void* grad_in, void* g
     }
     if (s->cfg.is_first) return swarm_embedding_backward(sl.tokens, T, s->gy[cur], s->V, d, s->grad + s->emb, st);
     if (!grad_out) return fail("backward: null output gradient message");
-    return wire_encode(s, s->gy[cur], grad_out, st);
+    if (!s->bneck) return wire_encode(s, s->gy[cur], grad_out, st);
+    // receiver side of the bottleneck: dW_d += dx0^T ni ; dni = dx0 W_d ; dmi = LN_d'(dni)
+    const int w = s->wire_w;
+    bf16* dx0 = s->gy[cur];
+    TRY(mm(d, w, T, {dx0, d, T, d, true}, {sl.ni, w, T, w, true}, s->grad + s->bn_wd, w, SWARM_EPI_ACCUM_F32, nullptr,
+           1.f, st));
+    TRY(mm(T, w, d, {dx0, d, T, d, false}, {s->p16 + s->bn_wd, w, d, w, true}, s->wtmp, w, SWARM_EPI_STORE_BF16,
+           nullptr, 1.f, st));
+    TRY(swarm_layer_norm_backward(s->wtmp, sl.mi, SWARM_DTYPE_BF16, T, w, s->p32 + s->bn_in_g, sl.mud, sl.rsd, nullptr,
+                                  s->dqkv, s->grad + s->bn_in_g, s->grad + s->bn_in_b, 1, s->lnws, st));
+    return wire_encode(s, s->dqkv, grad_out, st);
 }
 
 int swarm_stage_optimizer_step(swarm_stage_t s, float grad_scale, swarm_stream_t stream) {

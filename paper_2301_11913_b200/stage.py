@@ -34,6 +34,7 @@ class StageConfig:
     max_slots: int = 1
     wire: int = WIRE_INT8
     block_size: int = 4096
+    maxout_k: int = 0
     lr: float = 1e-4
     beta1: float = 0.9
     beta2: float = 0.95

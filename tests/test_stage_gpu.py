@@ -170,3 +170,49 @@ def test_training_reduces_loss(cuda):
         st.optimizer_step()
         losses.append(loss.item() / cfg.tokens)
     assert losses[-1] < losses[0] - 0.5, losses
+
+
+def test_two_stage_maxout_bottleneck(cuda):
+    """configs[3]'s boundary: sender maxout_2(LN(y)) -> int8 wire -> receiver LN then W_d.
+    Both stages vs the oracle fed the exact bits crossing the boundary."""
+    import torch
+    from oracle import block_oracle as BO
+    from paper_2301_11913_b200.stage import Stage
+    c0 = tiny_cfg(is_last=0, seed=4, maxout_k=2)
+    c1 = tiny_cfg(is_first=0, seed=5, maxout_k=2)
+    s0, s1 = Stage(c0), Stage(c1)
+    w = c0.d_model // 2
+    assert s0.wire_bytes == (c0.tokens * w + 15) // 16 * 16 + c0.tokens * w // c0.block_size * 4
+    g = torch.Generator().manual_seed(8)
+    tok = torch.randint(0, c0.vocab, (c0.tokens,), generator=g)
+    tgt = torch.randint(0, c0.vocab, (c0.tokens,), generator=g)
+    act, grad = s0.new_wire(), s1.new_wire()
+    loss = torch.zeros(1, device="cuda")
+    scale = 1.0 / c0.tokens
+    s0.forward(0, tok.int().cuda(), out=act)
+    s1.forward(0, act, targets=tgt.int().cuda(), loss_sum=loss, loss_scale=scale)
+    s1.backward(0, grad_out=grad)
+    s0.backward(0, grad_in=grad)
+    torch.cuda.synchronize()
+
+    def dec(st, wire):
+        from paper_2301_11913_b200 import ops
+        n = st.cfg.tokens * w
+        off = (n + 15) // 16 * 16
+        return ops.dequantize(wire[:n].view(torch.int8), wire[off:off + n // st.cfg.block_size * 4].view(torch.float32),
+                              st.cfg.block_size, torch.bfloat16).view(st.cfg.tokens, w)
+
+    x1 = dec(s1, act).double().cpu().requires_grad_()
+    P1 = oracle_params(s1)
+    _, l1 = BO.stage(P1, c1, x1, tgt, loss_scale=scale)
+    l1.backward()
+    assert abs(loss.item() * scale - l1.item()) <= LOSS_TOL * abs(l1.item())
+    for name, off, r, c in s1.param_info():
+        assert rel(grad_of(s1, name, r), P1[name].grad) <= GRAD_TOL, name
+    assert rel(dec(s0, grad), x1.grad) <= GRAD_TOL
+    P0 = oracle_params(s0)
+    m_ref, _ = BO.stage(P0, c0, tok)
+    assert rel(dec(s0, act), m_ref.detach()) <= FWD_TOL
+    m_ref.backward(dec(s0, grad).double().cpu())
+    for name, off, r, c in s0.param_info():
+        assert rel(grad_of(s0, name, r), P0[name].grad) <= GRAD_TOL, name
