@@ -312,9 +312,222 @@ __global__ void k_matvec_f64(const double* __restrict__ x, int rows, const doubl
 
 bool al(const void* p, size_t a) { return (reinterpret_cast<uintptr_t>(p) % a) == 0; }
 
+// ---------------------------------------------- warp-per-row bf16 LayerNorm --
+// cols = 256*NV: each lane holds NV 16-byte vectors (8 bf16) of the row, so a
+// row needs no block barrier and each warp keeps 2*NV loads in flight.  This is
+// the training path (d_model 256..4096); the block-per-row kernels above remain
+// for fp32 / odd widths.
+__device__ __forceinline__ void unpack8(const uint4& q, float* v) {
+    const uint32_t w[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        v[2 * j] = __uint_as_float(w[j] << 16);
+        v[2 * j + 1] = __uint_as_float(w[j] & 0xffff0000u);
+    }
+}
+__device__ __forceinline__ uint4 pack8(const float* v) {
+    uint32_t w[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        const __nv_bfloat162 p = __floats2bfloat162_rn(v[2 * j], v[2 * j + 1]);
+        w[j] = *reinterpret_cast<const uint32_t*>(&p);
+    }
+    return make_uint4(w[0], w[1], w[2], w[3]);
+}
+__device__ __forceinline__ float wsum(float v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+template <int NV>
+__global__ void __launch_bounds__(256) k_ln_fwd_w(const uint4* __restrict__ x, int rows, const float* __restrict__ g,
+                                                  const float* __restrict__ b, float eps, uint4* __restrict__ out,
+                                                  float* __restrict__ mean_out, float* __restrict__ rstd_out) {
+    constexpr int C8 = 32 * NV;
+    const int lane = threadIdx.x & 31;
+    const int warps = (gridDim.x * blockDim.x) >> 5;
+    const float inv_n = 1.f / (256.f * NV);
+    for (int r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < rows; r += warps) {
+        const uint4* xr = x + static_cast<size_t>(r) * C8;
+        float v[NV * 8];
+#pragma unroll
+        for (int i = 0; i < NV; ++i) unpack8(xr[lane + 32 * i], v + 8 * i);
+        float s = 0.f;
+#pragma unroll
+        for (int i = 0; i < NV * 8; ++i) s += v[i];
+        const float mean = wsum(s) * inv_n;
+        float s2 = 0.f;
+#pragma unroll
+        for (int i = 0; i < NV * 8; ++i) s2 += (v[i] - mean) * (v[i] - mean);
+        const float rstd = 1.0f / sqrtf(wsum(s2) * inv_n + eps);
+        uint4* orow = out + static_cast<size_t>(r) * C8;
+#pragma unroll
+        for (int i = 0; i < NV; ++i) {
+            const int c0 = (lane + 32 * i) * 8;
+            float o[8];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                o[j] = (v[8 * i + j] - mean) * rstd;
+                if (g) o[j] *= g[c0 + j];
+                if (b) o[j] += b[c0 + j];
+            }
+            orow[lane + 32 * i] = pack8(o);
+        }
+        if (lane == 0) {
+            if (mean_out) mean_out[r] = mean;
+            if (rstd_out) rstd_out[r] = rstd;
+        }
+    }
+}
+
+// dx = rstd * (g*dy - mean(g*dy) - xhat * mean(g*dy*xhat)) (+ dres)
+template <int NV>
+__global__ void __launch_bounds__(256) k_ln_bwd_dx_w(const uint4* __restrict__ dy, const uint4* __restrict__ x, int rows,
+                                                     const float* __restrict__ g, const float* __restrict__ mean,
+                                                     const float* __restrict__ rstd, const uint4* __restrict__ dres,
+                                                     uint4* __restrict__ dx) {
+    constexpr int C8 = 32 * NV;
+    constexpr bool KEEP = NV <= 8;  // keep the row in registers, else re-read it (L1/L2 hits)
+    const int lane = threadIdx.x & 31;
+    const int warps = (gridDim.x * blockDim.x) >> 5;
+    const float inv_n = 1.f / (256.f * NV);
+    for (int r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < rows; r += warps) {
+        const size_t base = static_cast<size_t>(r) * C8;
+        const float mu = mean[r], rs = rstd[r];
+        float xh[KEEP ? NV * 8 : 8], gy[KEEP ? NV * 8 : 8];
+        float s1 = 0.f, s2 = 0.f;
+#pragma unroll
+        for (int i = 0; i < NV; ++i) {
+            float xv[8], dv[8];
+            unpack8(x[base + lane + 32 * i], xv);
+            unpack8(dy[base + lane + 32 * i], dv);
+            const int c0 = (lane + 32 * i) * 8;
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                const float h = (xv[j] - mu) * rs;
+                const float q = g ? dv[j] * g[c0 + j] : dv[j];
+                s1 += q * h;
+                s2 += q;
+                if constexpr (KEEP) {
+                    xh[8 * i + j] = h;
+                    gy[8 * i + j] = q;
+                }
+            }
+        }
+        const float c1 = wsum(s1) * inv_n, c2 = wsum(s2) * inv_n;
+#pragma unroll
+        for (int i = 0; i < NV; ++i) {
+            const int c0 = (lane + 32 * i) * 8;
+            float o[8];
+            if constexpr (KEEP) {
+#pragma unroll
+                for (int j = 0; j < 8; ++j) o[j] = rs * (gy[8 * i + j] - c2 - xh[8 * i + j] * c1);
+            } else {
+                float xv[8], dv[8];
+                unpack8(x[base + lane + 32 * i], xv);
+                unpack8(dy[base + lane + 32 * i], dv);
+#pragma unroll
+                for (int j = 0; j < 8; ++j) {
+                    const float h = (xv[j] - mu) * rs;
+                    const float q = g ? dv[j] * g[c0 + j] : dv[j];
+                    o[j] = rs * (q - c2 - h * c1);
+                }
+            }
+            if (dres) {
+                float rv[8];
+                unpack8(dres[base + lane + 32 * i], rv);
+#pragma unroll
+                for (int j = 0; j < 8; ++j) o[j] += rv[j];
+            }
+            dx[base + lane + 32 * i] = pack8(o);
+        }
+    }
+}
+
+// dgain/dbias partials: CTA (column strip of 64, row split) with 8 column
+// vectors x 32 row lanes; deterministic (fixed reduction order).
+__global__ void __launch_bounds__(256) k_ln_bwd_dgb(const uint4* __restrict__ dy, const uint4* __restrict__ x, int rows,
+                                                    int cols, const float* __restrict__ mean,
+                                                    const float* __restrict__ rstd, int rows_per_split,
+                                                    float* __restrict__ part_g, float* __restrict__ part_b) {
+    __shared__ float sg[32][65], sb[32][65];
+    const int cv = threadIdx.x & 7, rl = threadIdx.x >> 3;
+    const int c8 = blockIdx.x * 8 + cv;  // column vector
+    const int cols8 = cols / 8;
+    const int r0 = blockIdx.y * rows_per_split, r1 = min(rows, r0 + rows_per_split);
+    float ag[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f}, ab[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+    if (c8 < cols8) {
+        for (int r = r0 + rl; r < r1; r += 32) {
+            float xv[8], dv[8];
+            unpack8(x[static_cast<size_t>(r) * cols8 + c8], xv);
+            unpack8(dy[static_cast<size_t>(r) * cols8 + c8], dv);
+            const float mu = mean[r], rs = rstd[r];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                ag[j] += dv[j] * (xv[j] - mu) * rs;
+                ab[j] += dv[j];
+            }
+        }
+    }
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+        sg[rl][cv * 8 + j] = ag[j];
+        sb[rl][cv * 8 + j] = ab[j];
+    }
+    __syncthreads();
+    if (threadIdx.x < 128) {
+        const int col = threadIdx.x & 63;
+        const bool isg = threadIdx.x < 64;
+        float acc = 0.f;
+        for (int k = 0; k < 32; ++k) acc += isg ? sg[k][col] : sb[k][col];
+        const int gcol = blockIdx.x * 64 + col;
+        if (gcol < cols) (isg ? part_g : part_b)[static_cast<size_t>(blockIdx.y) * cols + gcol] = acc;
+    }
+}
+
+template <int NV>
+void ln_fwd_w(const __nv_bfloat16* x, int rows, const float* g, const float* b, float eps, __nv_bfloat16* out,
+              float* mean, float* rstd, cudaStream_t st) {
+    const unsigned grid = static_cast<unsigned>(std::min((rows + 7) / 8, 148 * 8));
+    k_ln_fwd_w<NV><<<grid, 256, 0, st>>>(reinterpret_cast<const uint4*>(x), rows, g, b, eps,
+                                         reinterpret_cast<uint4*>(out), mean, rstd);
+}
+
+template <int NV>
+void ln_bwd_dx_w(const __nv_bfloat16* dy, const __nv_bfloat16* x, int rows, const float* g, const float* mean,
+                 const float* rstd, const __nv_bfloat16* dres, __nv_bfloat16* dx, cudaStream_t st) {
+    const unsigned grid = static_cast<unsigned>(std::min((rows + 7) / 8, 148 * 8));
+    k_ln_bwd_dx_w<NV><<<grid, 256, 0, st>>>(reinterpret_cast<const uint4*>(dy), reinterpret_cast<const uint4*>(x), rows,
+                                            g, mean, rstd, reinterpret_cast<const uint4*>(dres),
+                                            reinterpret_cast<uint4*>(dx));
+}
+
+bool warp_ln_ok(int cols) { return cols % 256 == 0 && cols <= 4096 && (cols / 256) <= 16; }
+
+template <typename F>
+bool dispatch_nv(int nv, F&& f) {
+    switch (nv) {
+        case 1: f(std::integral_constant<int, 1>{}); return true;
+        case 2: f(std::integral_constant<int, 2>{}); return true;
+        case 4: f(std::integral_constant<int, 4>{}); return true;
+        case 8: f(std::integral_constant<int, 8>{}); return true;
+        case 12: f(std::integral_constant<int, 12>{}); return true;
+        case 16: f(std::integral_constant<int, 16>{}); return true;
+        default: return false;
+    }
+}
+
 template <typename T>
 int ln_fwd_launch(const T* x, int rows, int cols, const float* g, const float* b, float eps, T* out, float* mean,
                   float* rstd, cudaStream_t st) {
+    if constexpr (sizeof(T) == 2) {
+        if (warp_ln_ok(cols) && al(x, 16) && al(out, 16) &&
+            dispatch_nv(cols / 256, [&](auto nv) { ln_fwd_w<decltype(nv)::value>(x, rows, g, b, eps, out, mean, rstd, st); })) {
+            SWARM_LAUNCH_CHECK("k_ln_fwd_w");
+            return SWARM_OK;
+        }
+    }
     const unsigned grid = static_cast<unsigned>(std::min(rows, 148 * 8));
     constexpr int V = sizeof(T) == 2 ? 8 : 4;
     if (cols % V == 0 && al(x, 16) && al(out, 16))
@@ -330,6 +543,34 @@ int ln_bwd_parts(size_t rows) { return static_cast<int>(std::min<size_t>(rows, 2
 template <typename T>
 int ln_bwd_launch(const T* dy, const T* x, int rows, int cols, const float* g, const float* mean, const float* rstd,
                   const T* dres, T* dx, float* dg, float* db, int accumulate, float* ws, cudaStream_t st) {
+    if constexpr (sizeof(T) == 2) {
+        if (warp_ln_ok(cols) && al(x, 16) && al(dy, 16) && al(dx, 16) && (!dres || al(dres, 16)) &&
+            dispatch_nv(cols / 256, [&](auto nv) {
+                ln_bwd_dx_w<decltype(nv)::value>(dy, x, rows, g, mean, rstd, dres, dx, st);
+            })) {
+            SWARM_LAUNCH_CHECK("k_ln_bwd_dx_w");
+            if (dg || db) {
+                const int splits = std::max(1, std::min(ln_bwd_parts(rows), (rows + 63) / 64));
+                const int rps = (rows + splits - 1) / splits;
+                float* pg = ws;
+                float* pb = ws + static_cast<size_t>(splits) * cols;
+                k_ln_bwd_dgb<<<dim3((cols + 63) / 64, splits), 256, 0, st>>>(
+                    reinterpret_cast<const uint4*>(dy), reinterpret_cast<const uint4*>(x), rows, cols, mean, rstd, rps,
+                    pg, pb);
+                SWARM_LAUNCH_CHECK("k_ln_bwd_dgb");
+                const unsigned cg = static_cast<unsigned>((cols + 255) / 256);
+                if (dg) {
+                    k_col_reduce<<<cg, 256, 0, st>>>(pg, splits, cols, dg, accumulate);
+                    SWARM_LAUNCH_CHECK("k_col_reduce");
+                }
+                if (db) {
+                    k_col_reduce<<<cg, 256, 0, st>>>(pb, splits, cols, db, accumulate);
+                    SWARM_LAUNCH_CHECK("k_col_reduce");
+                }
+            }
+            return SWARM_OK;
+        }
+    }
     const int parts = ln_bwd_parts(rows);
     const int rpc = (rows + parts - 1) / parts;
     const int grid = (rows + rpc - 1) / rpc;

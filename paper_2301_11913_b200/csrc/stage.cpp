@@ -74,6 +74,11 @@ struct swarm_stage {
     std::vector<void*> allocations;
     int step = 0;
     bool fused_attn = false;  // scores+softmax in one tcgen05 kernel (csrc/attention.cu)
+    // weight-gradient GEMMs run on a side stream forked/joined per layer, so they
+    // fill the SMs the data-gradient chain leaves idle (GEMM wave tails)
+    cudaStream_t side = nullptr;
+    cudaEvent_t ev_fork[4] = {nullptr, nullptr, nullptr, nullptr};
+    cudaEvent_t ev_join = nullptr;
     // GEMM profiling (bench.py's live roofline): event pairs around each GEMM
     bool prof_on = false;
     std::vector<cudaEvent_t> prof_events;
@@ -225,6 +230,23 @@ int bmm(swarm_stage* s, int M, int N, int K, BOp a, BOp b, void* d, int ldd, int
 
 const LayerW& weights(const swarm_stage* s, int l) { return s->layers[s->cfg.shared_layers ? 0 : l]; }
 
+// Profiled (eager) visits keep every GEMM on the visit stream so the events
+// around each GEMM time that kernel alone; other visits overlap the two streams.
+cudaStream_t side_of(swarm_stage* s, cudaStream_t main) { return t_prof ? main : s->side; }
+
+// side stream waits for everything enqueued on `main` so far
+int fork_side(swarm_stage* s, cudaStream_t main, int i) {
+    if (t_prof) return SWARM_OK;
+    if (cudaEventRecord(s->ev_fork[i], main) != cudaSuccess) return SWARM_E_CUDA;
+    return cudaStreamWaitEvent(s->side, s->ev_fork[i], 0) == cudaSuccess ? SWARM_OK : SWARM_E_CUDA;
+}
+// main waits for everything enqueued on the side stream so far
+int join_side(swarm_stage* s, cudaStream_t main) {
+    if (t_prof) return SWARM_OK;
+    if (cudaEventRecord(s->ev_join, s->side) != cudaSuccess) return SWARM_E_CUDA;
+    return cudaStreamWaitEvent(main, s->ev_join, 0) == cudaSuccess ? SWARM_OK : SWARM_E_CUDA;
+}
+
 // ---------------------------------------------------------- block forward --
 int block_forward(swarm_stage* s, Act& A, bf16* y, const LayerW& W, cudaStream_t st) {
     const int T = s->T, d = s->d, H = s->H, dh = s->dh, F = s->F, L = s->L;
@@ -264,19 +286,23 @@ int block_backward(swarm_stage* s, const Act& A, const bf16* dy, bf16* dx, const
     const bf16* p16 = s->p16;
     const float* p32 = s->p32;
     float* G = s->grad;
+    cudaStream_t sd = side_of(s, st);  // weight gradients
     // MLP: du = (dy W2) * gelu'(u); dW2 += dy^T g; dc = du W1; dW1 += du^T c
+    TRY(fork_side(s, st, 0));
+    TRY(mm(d, F, T, {dy, d, T, d, true}, {A.g, F, T, F, true}, G + W.w2, F, SWARM_EPI_ACCUM_F32, nullptr, 1.f, sd));
     TRY(mm(T, F, d, {dy, d, T, d, false}, {p16 + W.w2, F, d, F, true}, s->du, F, SWARM_EPI_DGELU, A.u, 1.f, st));
-    TRY(mm(d, F, T, {dy, d, T, d, true}, {A.g, F, T, F, true}, G + W.w2, F, SWARM_EPI_ACCUM_F32, nullptr, 1.f, st));
+    TRY(fork_side(s, st, 1));
+    TRY(mm(F, d, T, {s->du, F, T, F, true}, {A.c, d, T, d, true}, G + W.w1, d, SWARM_EPI_ACCUM_F32, nullptr, 1.f, sd));
     TRY(mm(T, d, F, {s->du, F, T, F, false}, {p16 + W.w1, d, F, d, true}, s->dc, d, SWARM_EPI_STORE_BF16, nullptr, 1.f,
            st));
-    TRY(mm(F, d, T, {s->du, F, T, F, true}, {A.c, d, T, d, true}, G + W.w1, d, SWARM_EPI_ACCUM_F32, nullptr, 1.f, st));
     // dh = LN2'(dc) + dy
     TRY(swarm_layer_norm_backward(s->dc, A.h, SWARM_DTYPE_BF16, T, d, p32 + W.ln2g, A.mu2, A.rs2, dy, s->dhid,
                                   G + W.ln2g, G + W.ln2b, 1, s->lnws, st));
     // attention output projection
+    TRY(fork_side(s, st, 2));
+    TRY(mm(d, d, T, {s->dhid, d, T, d, true}, {A.o, d, T, d, true}, G + W.wo, d, SWARM_EPI_ACCUM_F32, nullptr, 1.f, sd));
     TRY(mm(T, d, d, {s->dhid, d, T, d, false}, {p16 + W.wo, d, d, d, true}, s->dO, d, SWARM_EPI_STORE_BF16, nullptr, 1.f,
            st));
-    TRY(mm(d, d, T, {s->dhid, d, T, d, true}, {A.o, d, T, d, true}, G + W.wo, d, SWARM_EPI_ACCUM_F32, nullptr, 1.f, st));
     // dP = dO V^T ; dS = scale * P (dP - rowsum(P dP))
     const float scale = 1.f / std::sqrt(static_cast<float>(dh));
     if (s->fused_attn) {
@@ -296,14 +322,16 @@ int block_backward(swarm_stage* s, const Act& A, const bf16* dy, bf16* dx, const
     TRY(bmm(s, L, dh, L, {{A.P, L, BHL, L, true}, H * L, L, 0, 0}, {{s->dO, d, T, d, true}, L, 0, 0, dh},
             s->dqkv + 2 * d, 3 * d, L, 0, 0, dh, SWARM_EPI_STORE_BF16, 1.f, st));
     // da = dqkv Wqkv ; dWqkv += dqkv^T a
+    TRY(fork_side(s, st, 3));
+    TRY(mm(3 * d, d, T, {s->dqkv, 3 * d, T, 3 * d, true}, {A.a, d, T, d, true}, G + W.wqkv, d, SWARM_EPI_ACCUM_F32,
+           nullptr, 1.f, sd));
     TRY(mm(T, d, 3 * d, {s->dqkv, 3 * d, T, 3 * d, false}, {p16 + W.wqkv, d, 3 * d, d, true}, s->da, d,
            SWARM_EPI_STORE_BF16, nullptr, 1.f, st));
-    TRY(mm(3 * d, d, T, {s->dqkv, 3 * d, T, 3 * d, true}, {A.a, d, T, d, true}, G + W.wqkv, d, SWARM_EPI_ACCUM_F32,
-           nullptr, 1.f, st));
     // dx = LN1'(da) + dh
     TRY(swarm_layer_norm_backward(s->da, A.x, SWARM_DTYPE_BF16, T, d, p32 + W.ln1g, A.mu1, A.rs1, s->dhid, dx,
                                   G + W.ln1g, G + W.ln1b, 1, s->lnws, st));
-    return SWARM_OK;
+    // the next layer overwrites the workspaces the weight gradients read
+    return join_side(s, st);
 }
 
 size_t wire_bytes(const swarm_stage* s) {
@@ -481,6 +509,10 @@ int create(const swarm_stage_config* c, swarm_stage* s) {
         TRY(alloc(s, &s->logits, T * s->V));
         TRY(alloc(s, &s->dlogits, T * s->V));
     }
+    if (cudaStreamCreateWithFlags(&s->side, cudaStreamNonBlocking) != cudaSuccess) return SWARM_E_CUDA;
+    for (auto& e : s->ev_fork)
+        if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) return SWARM_E_CUDA;
+    if (cudaEventCreateWithFlags(&s->ev_join, cudaEventDisableTiming) != cudaSuccess) return SWARM_E_CUDA;
     TRY(init_params(s, nullptr));
     if (cudaStreamSynchronize(nullptr) != cudaSuccess) return SWARM_E_CUDA;
     return SWARM_OK;
@@ -507,6 +539,10 @@ void swarm_stage_destroy(swarm_stage_t s) {
     if (!s) return;
     cudaDeviceSynchronize();
     for (cudaEvent_t e : s->prof_events) cudaEventDestroy(e);
+    for (cudaEvent_t e : s->ev_fork)
+        if (e) cudaEventDestroy(e);
+    if (s->ev_join) cudaEventDestroy(s->ev_join);
+    if (s->side) cudaStreamDestroy(s->side);
     for (void* p : s->allocations) cudaFree(p);
     delete s;
 }
@@ -617,11 +653,12 @@ int swarm_stage_forward(swarm_stage_t s, int slot, const void* in, const int32_t
     TRY(mm(T, s->V, d, {sl.xf, d, T, d, false}, {s->p16 + s->head, d, s->V, d, false}, s->logits, s->V,
            SWARM_EPI_STORE_F32, nullptr, 1.f, st));
     TRY(swarm_cross_entropy(s->logits, targets, T, s->V, loss_scale, loss_sum, s->dlogits, st));
+    TRY(fork_side(s, st, 0));
     TRY(mm(s->V, d, T, {s->dlogits, s->V, T, s->V, true}, {sl.xf, d, T, d, true}, s->grad + s->head, d,
-           SWARM_EPI_ACCUM_F32, nullptr, 1.f, st));
+           SWARM_EPI_ACCUM_F32, nullptr, 1.f, side_of(s, st)));
     TRY(mm(T, d, s->V, {s->dlogits, s->V, T, s->V, false}, {s->p16 + s->head, d, s->V, d, true}, sl.dxf, d,
            SWARM_EPI_STORE_BF16, nullptr, 1.f, st));
-    return SWARM_OK;
+    return join_side(s, st);
 }
 
 int swarm_stage_backward(swarm_stage_t s, int slot, const void* grad_in, void* grad_out, swarm_stream_t stream) {

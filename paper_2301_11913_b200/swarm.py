@@ -47,6 +47,7 @@ class ModelConfig:
     causal: int = 1
     wire: int = WIRE_INT8
     block_size: int = 4096
+    maxout_k: int = 0  # > 1: maxout bottleneck at the stage boundaries
 
     @property
     def tokens(self) -> int:
@@ -68,7 +69,7 @@ PRESETS = {
     # configs[2]: 8 layers/stage, d 2048, 16 heads, L 512; microbatch 4 (PAPER:292 xxlarge)
     "C": ModelConfig(2048, 16, 8192, 512, 4, 8, 50304),
     # configs[3]: d 4096, 32 heads, 16 shared layers per stage, L 512, microbatch 1
-    "D": ModelConfig(4096, 32, 16384, 512, 1, 16, 50304, shared_layers=1),
+    "D": ModelConfig(4096, 32, 16384, 512, 1, 16, 50304, shared_layers=1, maxout_k=2),
 }
 
 
@@ -190,7 +191,8 @@ class SwarmPipeline:
                               micro_batch=mcfg.micro_batch, n_layers=mcfg.layers_per_stage,
                               shared_layers=mcfg.shared_layers, vocab=mcfg.vocab, is_first=int(s == 0),
                               is_last=int(s == S - 1), causal=mcfg.causal, max_slots=slots, wire=mcfg.wire,
-                              block_size=mcfg.block_size, lr=lr, weight_decay=weight_decay,
+                              block_size=mcfg.block_size, maxout_k=mcfg.maxout_k, lr=lr,
+                              weight_decay=weight_decay,
                               seed=seed * 1000 + s)  # every replica of a stage starts identical
             self.stages[s] = Stage(cfg, self.device)
         # CUDA graphs: a visit enqueues ~200 kernels; replaying a captured graph
