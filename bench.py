@@ -349,7 +349,8 @@ def bench_train(args, world, rank, local):
     L = _lib.lib()
     mcfg = PRESETS[args.model]
     M = args.microbatches
-    pipe = SwarmPipeline(mcfg, TRAIN_STAGES, n_microbatches=M, seed=1, lr=1e-4, profile=True)
+    S = args.stages
+    pipe = SwarmPipeline(mcfg, S, n_microbatches=M, seed=1, lr=1e-4, profile=True)
     tok, tgt = synthetic_batch(mcfg, M, seed=7, device=dev)
     stream = torch.cuda.current_stream()
     for _ in range(args.warmup):
@@ -410,15 +411,15 @@ def bench_train(args, world, rank, local):
     visits_per_stage = (M // pipe.P) if not pipe.all_local else M
     gemm_share = (gemm_ms / args.steps) * visits_per_stage / (t0.elapsed_time(t1) / args.steps) \
         if gemm_ms > 0 else None
-    model_tflops = value * mcfg.flops_per_token(TRAIN_STAGES) / 1e12
-    placement = {1: "1 GPU hosts all 4 stages", 2: "2 GPUs x 2 stages", 4: "4 stages x 1 peer",
-                 8: "4 stages x 2 peers"}.get(world, f"{world} ranks")
+    model_tflops = value * mcfg.flops_per_token(S) / 1e12
+    placement = (f"{S} stages x {pipe.P} peer(s) per stage" if world >= S else
+                 f"{world} GPU(s) x {S // world} stage(s) each")
     line = {
         "metric": "training tokens/s (SWARM pipeline)", "value": value, "unit": "tokens/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
         "data": "synthetic tokens uniform over the vocab, random-init weights",
-        "config": {"workload": f"BASELINE configs[2]: {TRAIN_STAGES} stages, {mcfg.layers_per_stage} layers/stage, "
+        "config": {"workload": f"BASELINE configs[2]: {S} stages, {mcfg.layers_per_stage} layers/stage, "
                                f"d_model {mcfg.d_model}, {mcfg.n_heads} heads, seq {mcfg.seq_len}, int8 boundary codec, "
                                "stochastic wiring + intra-stage all-reduce",
                    "model": args.model, "global_batch": M * mcfg.micro_batch, "micro_batch": mcfg.micro_batch,
@@ -426,7 +427,7 @@ def bench_train(args, world, rank, local):
                    "vocab": mcfg.vocab, "parallelism": placement, "optimizer": "AdamW (fused, fp32 master)",
                    "l2": "per-step working set (weights + activations, GBs) far exceeds L2; no flush needed",
                    "mean_loss": mean_loss, "model_tflops_per_s": model_tflops,
-                   "model_flops_per_token": mcfg.flops_per_token(TRAIN_STAGES)},
+                   "model_flops_per_token": mcfg.flops_per_token(S)},
         "roofline": {"bound": "tensor", "kernel": "k_gemm (tcgen05 bf16, every block/attention/head GEMM)",
                      "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
                      "traffic": None, "peak_source": pk["source"] + " bf16 sustained",
@@ -485,6 +486,7 @@ def main():
     ap.add_argument("--workload", default="train", choices=["train", "codec"])
     ap.add_argument("--model", default="C", choices=["C", "D", "tiny"])
     ap.add_argument("--microbatches", type=int, default=TRAIN_MICROBATCHES)
+    ap.add_argument("--stages", type=int, default=TRAIN_STAGES, help="pipeline stages (default 4, SURVEY §8(d))")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-codec", action="store_true", help="train: skip the codec sub-measurement")
     args = ap.parse_args()
