@@ -50,6 +50,7 @@ struct Params {
     int epi;
     int vec_ok;
     int tma_epi;  // stage output chunks in smem and write them with TMA (store / reduce-add)
+    int dbg;      // SWARM_GEMM_DBG (experiments only): 1 skip output stores, 2 skip MMAs, 4 skip TMA loads
 };
 
 template <int BN>
@@ -287,7 +288,7 @@ __device__ __forceinline__ void drain_tile(const Params& p, const CUtensorMap* m
         }
         fence_async_smem();
         __syncwarp();
-        if (lane == 0 && row_base < p.m) {
+        if (lane == 0 && row_base < p.m && !(p.dbg & 1)) {
             if (p.epi == SWARM_EPI_ACCUM_F32) tma_reduce_add_2d(md, slot, gc, gr);
             else tma_store_2d(md, slot, gc, gr);
             if (p.epi == SWARM_EPI_GELU) tma_store_2d(mu, slot + 2048, gc, gr);
@@ -529,6 +530,14 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const int n0 = nt * PAIR_BN + static_cast<int>(rank) * 128;
                 for (int kb = 0; kb < p.k_blocks; ++kb) {
                     mbar_wait(&empty[stage], phase ^ 1);
+                    if (p.dbg & 4) {  // experiment: no operand traffic
+                        if (leader) mbar_arrive(&full[stage]);
+                        if (++stage == C::STAGES) {
+                            stage = 0;
+                            phase ^= 1;
+                        }
+                        continue;
+                    }
                     if (leader) mbar_arrive_expect_tx(&full[stage], 2 * (C::A_BYTES + C::B_BYTES));
                     const uint32_t bar = map_to_cta(&full[stage], 0);
                     uint8_t* a_dst = sa + stage * C::A_BYTES;
@@ -577,7 +586,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                                                  : make_sdesc(a_base + k * 32, 16, 1024);
                         const uint64_t bd = B_MN ? make_sdesc(b_base + k * 2048, 64 * BK * 2, 1024)
                                                  : make_sdesc(b_base + k * 32, 16, 1024);
-                        mma_bf16_pair(d_tmem, ad, bd, idesc, (kb | k) != 0 ? 1u : 0u);
+                        if (!(p.dbg & 2)) mma_bf16_pair(d_tmem, ad, bd, idesc, (kb | k) != 0 ? 1u : 0u);
                     }
                     mma_commit_pair(&empty[stage], 0x3);
                     if (++stage == C::STAGES) {
@@ -868,6 +877,13 @@ extern "C" int swarm_gemm_bf16(const swarm_gemm_args* a, swarm_stream_t stream) 
     const long long d_rows = static_cast<long long>(a->rd0) * (nb - 1) + static_cast<long long>(a->rd1) * (a->bh - 1) + a->m;
     const long long d_cols = static_cast<long long>(a->cd0) * (nb - 1) + static_cast<long long>(a->cd1) * (a->bh - 1) + a->n;
     const bool exact = (a->m % TM == 0) && (a->n % 32 == 0);
+    {
+        static const int dbg = [] {
+            const char* e = getenv("SWARM_GEMM_DBG");
+            return e ? atoi(e) : 0;
+        }();
+        p.dbg = dbg;
+    }
     p.tma_epi = tma_epi_enabled() && (a->batch == 1 || exact) && d_cols <= a->ldd &&
                 ((reinterpret_cast<uintptr_t>(a->d) & 15) == 0) && ((a->ldd * esz) % 16 == 0) &&
                 (!a->aux || (reinterpret_cast<uintptr_t>(a->aux) & 15) == 0);

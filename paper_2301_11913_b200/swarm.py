@@ -180,7 +180,7 @@ class SwarmPipeline:
         self.P = self.pl.P
         self.per_rank = self.pl.per_rank
         self.local_stages = self.pl.local_stages(self.rank)
-        self.all_local = len(self.local_stages) == S
+        self.all_local = len(self.local_stages) == S and self.P == 1  # sole peer of every stage
         self.n_trainers = n_trainers or self.P
         # stage executors for the stages this rank serves
         slots = 1 if self.all_local else (self.M if self.P == 1 else math.ceil(self.M / self.P) + 2)
