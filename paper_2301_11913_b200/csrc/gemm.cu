@@ -468,7 +468,7 @@ struct Cfg2 {
     static_assert(2 * STAGES * 8 + 4 * 8 + 4 <= 256, "barrier area overflow");
 };
 
-template <bool A_MN, bool B_MN>
+template <bool A_MN, bool B_MN, int NPAIR>
 __global__ void __launch_bounds__(kThreads, 1)
     k_gemm2(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUtensorMap tma_b,
             const __grid_constant__ CUtensorMap tma_d, const __grid_constant__ CUtensorMap tma_u, const Params p) {
@@ -487,17 +487,22 @@ __global__ void __launch_bounds__(kThreads, 1)
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
+    // cluster = NPAIR CTA pairs side by side in N; CTA rank = 2*pair + half
     const uint32_t rank = cluster_ctarank();
-    const bool leader = rank == 0;
-    const int cluster = blockIdx.x >> 1;
-    const int n_clusters = gridDim.x >> 1;
+    const int pair = static_cast<int>(rank >> 1);
+    const int half = static_cast<int>(rank & 1);
+    const bool leader = half == 0;
+    const int cluster = blockIdx.x / (2 * NPAIR);
+    const int n_clusters = gridDim.x / (2 * NPAIR);
+    const uint16_t pair_mask = static_cast<uint16_t>(0x3u << (2 * pair));
+    const uint16_t all_mask = static_cast<uint16_t>((1u << (2 * NPAIR)) - 1);
 
     if (warp == 0 && lane == 0) {
         tma_prefetch(&tma_a);
         tma_prefetch(&tma_b);
         for (int s = 0; s < C::STAGES; ++s) {
             mbar_init(&full[s], 1);
-            mbar_init(&empty[s], 1);
+            mbar_init(&empty[s], NPAIR);  // every pair's MMA frees a stage its A multicast wrote
         }
         for (int s = 0; s < 2; ++s) {
             mbar_init(&tfull[s], 1);
@@ -526,8 +531,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const int zb = z / p.bh, zh = z - zb * p.bh;
                 const int ra = p.ra0 * zb + p.ra1 * zh, ca = p.ca0 * zb + p.ca1 * zh;
                 const int rb = p.rb0 * zb + p.rb1 * zh, cb = p.cb0 * zb + p.cb1 * zh;
-                const int m0 = mt * 256 + static_cast<int>(rank) * 128;
-                const int n0 = nt * PAIR_BN + static_cast<int>(rank) * 128;
+                const int m0 = mt * 256 + half * 128;
+                const int n0 = (nt * NPAIR + pair) * PAIR_BN + half * 128;
                 for (int kb = 0; kb < p.k_blocks; ++kb) {
                     mbar_wait(&empty[stage], phase ^ 1);
                     if (p.dbg & 4) {  // experiment: no operand traffic
@@ -539,15 +544,28 @@ __global__ void __launch_bounds__(kThreads, 1)
                         continue;
                     }
                     if (leader) mbar_arrive_expect_tx(&full[stage], 2 * (C::A_BYTES + C::B_BYTES));
-                    const uint32_t bar = map_to_cta(&full[stage], 0);
+                    const uint32_t bar = pair_leader_addr(&full[stage]);
                     uint8_t* a_dst = sa + stage * C::A_BYTES;
                     uint8_t* b_dst = sb + stage * C::B_BYTES;
-                    if constexpr (!A_MN) {
-                        tma_load_2d_pair(a_dst, &tma_a, bar, ca + kb * BK, ra + m0);
-                    } else {
+                    if constexpr (NPAIR == 1) {
+                        if constexpr (!A_MN) {
+                            tma_load_2d_pair(a_dst, &tma_a, bar, ca + kb * BK, ra + m0);
+                        } else {
 #pragma unroll
-                        for (int j = 0; j < 2; ++j)
-                            tma_load_2d_pair(a_dst + j * (64 * BK * 2), &tma_a, bar, ca + m0 + j * 64, ra + kb * BK);
+                            for (int j = 0; j < 2; ++j)
+                                tma_load_2d_pair(a_dst + j * (64 * BK * 2), &tma_a, bar, ca + m0 + j * 64,
+                                                 ra + kb * BK);
+                        }
+                    } else {
+                        // both pairs need this A half: each pair loads one 64-row (K-major) or
+                        // 64-column (MN-major) piece and multicasts it to the same half of every pair
+                        const uint16_t mc = static_cast<uint16_t>(0x5u << half);
+                        if constexpr (!A_MN)
+                            tma_load_2d_pair_mc(a_dst + pair * (64 * 128), &tma_a, bar, ca + kb * BK, ra + m0 + pair * 64,
+                                                mc);
+                        else
+                            tma_load_2d_pair_mc(a_dst + pair * (64 * BK * 2), &tma_a, bar, ca + m0 + pair * 64,
+                                                ra + kb * BK, mc);
                     }
                     if constexpr (!B_MN) {
                         tma_load_2d_pair(b_dst, &tma_b, bar, cb + kb * BK, rb + n0);
@@ -588,13 +606,13 @@ __global__ void __launch_bounds__(kThreads, 1)
                                                  : make_sdesc(b_base + k * 32, 16, 1024);
                         if (!(p.dbg & 2)) mma_bf16_pair(d_tmem, ad, bd, idesc, (kb | k) != 0 ? 1u : 0u);
                     }
-                    mma_commit_pair(&empty[stage], 0x3);
+                    mma_commit_pair(&empty[stage], all_mask);
                     if (++stage == C::STAGES) {
                         stage = 0;
                         phase ^= 1;
                     }
                 }
-                mma_commit_pair(&tfull[acc], 0x3);
+                mma_commit_pair(&tfull[acc], pair_mask);
                 acc ^= 1;
                 if (acc == 0) acc_phase ^= 1;
             }
@@ -602,7 +620,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     } else if (warp >= 4) {
         // ------------------------------------------------ epilogue (both CTAs, own 128 rows)
         const int q = warp - 4;
-        const uint32_t tempty_leader[2] = {map_to_cta(&tempty[0], 0), map_to_cta(&tempty[1], 0)};
+        const uint32_t tempty_leader[2] = {map_to_cta(&tempty[0], rank & ~1u), map_to_cta(&tempty[1], rank & ~1u)};
         uint8_t* stg = stg_all + q * 2 * kEpiSlot;
         int slot_idx = 0;
         int acc = 0;
@@ -618,7 +636,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             drain_tile<PAIR_BN>(p, &tma_d, &tma_u, stg, slot_idx,
                                 tmem_base + (static_cast<uint32_t>(q * 32) << 16) +
                                     static_cast<uint32_t>(acc * PAIR_BN),
-                                mt * 256 + static_cast<int>(rank) * 128 + q * 32, rd, cd, nt * PAIR_BN, lane);
+                                mt * 256 + half * 128 + q * 32, rd, cd, (nt * NPAIR + pair) * PAIR_BN, lane);
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive_cluster(tempty_leader[acc]);
@@ -763,23 +781,23 @@ int launch(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& td, 
     return SWARM_OK;
 }
 
-template <bool A_MN, bool B_MN>
+template <bool A_MN, bool B_MN, int NPAIR>
 int launch_pair(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& td, const CUtensorMap& tu,
                 const Params& p, cudaStream_t st) {
-    auto kern = k_gemm2<A_MN, B_MN>;
+    auto kern = k_gemm2<A_MN, B_MN, NPAIR>;
     static bool attr = false;
     if (!attr) {
         SWARM_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg2::SMEM));
         attr = true;
     }
     cudaLaunchConfig_t cfg{};
-    cfg.gridDim = dim3(2 * std::min(p.total_tiles, num_sms() / 2));
+    cfg.gridDim = dim3(2 * NPAIR * std::min(p.total_tiles, num_sms() / (2 * NPAIR)));
     cfg.blockDim = dim3(kThreads);
     cfg.dynamicSmemBytes = Cfg2::SMEM;
     cfg.stream = st;
     cudaLaunchAttribute attrs[1];
     attrs[0].id = cudaLaunchAttributeClusterDimension;
-    attrs[0].val.clusterDim.x = 2;
+    attrs[0].val.clusterDim.x = 2 * NPAIR;
     attrs[0].val.clusterDim.y = 1;
     attrs[0].val.clusterDim.z = 1;
     cfg.attrs = attrs;
@@ -789,12 +807,21 @@ int launch_pair(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap&
     return SWARM_OK;
 }
 
+template <int NPAIR>
 int dispatch_pair(bool amn, bool bmn, const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& td,
                   const CUtensorMap& tu, const Params& p, cudaStream_t st) {
-    if (!amn && !bmn) return launch_pair<false, false>(ta, tb, td, tu, p, st);
-    if (!amn && bmn) return launch_pair<false, true>(ta, tb, td, tu, p, st);
-    if (amn && !bmn) return launch_pair<true, false>(ta, tb, td, tu, p, st);
-    return launch_pair<true, true>(ta, tb, td, tu, p, st);
+    if (!amn && !bmn) return launch_pair<false, false, NPAIR>(ta, tb, td, tu, p, st);
+    if (!amn && bmn) return launch_pair<false, true, NPAIR>(ta, tb, td, tu, p, st);
+    if (amn && !bmn) return launch_pair<true, false, NPAIR>(ta, tb, td, tu, p, st);
+    return launch_pair<true, true, NPAIR>(ta, tb, td, tu, p, st);
+}
+
+int multicast_mode() {  // SWARM_GEMM_MCAST=0 disables the 4-CTA multicast clusters
+    static const int on = [] {
+        const char* e = getenv("SWARM_GEMM_MCAST");
+        return !(e && e[0] == '0');
+    }();
+    return on;
 }
 
 bool pair_enabled() {
@@ -843,8 +870,12 @@ extern "C" int swarm_gemm_bf16(const swarm_gemm_args* a, swarm_stream_t stream) 
     const bool pair = pair_enabled() && a->m > 128 && a->n > 128;
     const int BN = pair ? PAIR_BN : (a->n <= 128 ? 128 : 256);
     const int TM = pair ? 256 : BM;
+    // two pairs per cluster sharing A by TMA multicast when N splits into an even
+    // number of 256-wide tiles (halves the A traffic from L2 per SM)
+    const int pair_tiles_n = (a->n + PAIR_BN - 1) / PAIR_BN;
+    const int npair = (pair && multicast_mode() && pair_tiles_n % 2 == 0) ? 2 : 1;
     CUtensorMap ta, tb;
-    int rc = encode_2d(&ta, a->a, ar, ac, a->lda, 64, a->a_mn_major ? BK : BM);
+    int rc = encode_2d(&ta, a->a, ar, ac, a->lda, 64, a->a_mn_major ? BK : (npair == 2 ? 64 : BM));
     if (rc) return rc;
     rc = encode_2d(&tb, a->b, br, bc, a->ldb, 64, a->b_mn_major ? BK : (pair ? 128 : BN));
     if (rc) return rc;
@@ -854,7 +885,7 @@ extern "C" int swarm_gemm_bf16(const swarm_gemm_args* a, swarm_stream_t stream) 
     p.k = a->k;
     p.bh = a->bh;
     p.tiles_m = (a->m + TM - 1) / TM;
-    p.tiles_n = (a->n + BN - 1) / BN;
+    p.tiles_n = (a->n + BN - 1) / BN / (pair ? npair : 1);  // cluster tiles along N
     p.tiles_per_batch = p.tiles_m * p.tiles_n;
     p.total_tiles = p.tiles_per_batch * a->batch;
     p.k_blocks = (a->k + BK - 1) / BK;
@@ -895,7 +926,8 @@ extern "C" int swarm_gemm_bf16(const swarm_gemm_args* a, swarm_stream_t stream) 
         if (rc != SWARM_OK) p.tma_epi = 0;  // fall back to direct stores
     }
     cudaStream_t st = as_stream(stream);
-    if (pair) return dispatch_pair(a->a_mn_major, a->b_mn_major, ta, tb, td, tu, p, st);
+    if (pair && npair == 2) return dispatch_pair<2>(a->a_mn_major, a->b_mn_major, ta, tb, td, tu, p, st);
+    if (pair) return dispatch_pair<1>(a->a_mn_major, a->b_mn_major, ta, tb, td, tu, p, st);
     if (BN == 128) return dispatch<128>(a->a_mn_major, a->b_mn_major, ta, tb, td, tu, p, st);
     return dispatch<256>(a->a_mn_major, a->b_mn_major, ta, tb, td, tu, p, st);
 }
