@@ -816,10 +816,13 @@ int dispatch_pair(bool amn, bool bmn, const CUtensorMap& ta, const CUtensorMap& 
     return launch_pair<true, true, NPAIR>(ta, tb, td, tu, p, st);
 }
 
-int multicast_mode() {  // SWARM_GEMM_MCAST=0 disables the 4-CTA multicast clusters
+// 4-CTA multicast clusters are opt-in (SWARM_GEMM_MCAST=1): measured slower on
+// B200 — cluster-4 placement strands SMs and couples the two pairs' pipelines
+// (profiles/r01_gemm_experiments.md).
+int multicast_mode() {
     static const int on = [] {
         const char* e = getenv("SWARM_GEMM_MCAST");
-        return !(e && e[0] == '0');
+        return e && e[0] == '1';
     }();
     return on;
 }
