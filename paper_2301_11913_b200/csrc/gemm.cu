@@ -50,6 +50,7 @@ struct Params {
     int epi;
     int vec_ok;
     int tma_epi;  // stage output chunks in smem and write them with TMA (store / reduce-add)
+    int ksplit, kb_per_split;  // split-K units per tile (pair kernel, fp32 reduce-add epilogue only)
     int dbg;      // SWARM_GEMM_DBG (experiments only): 1 skip output stores, 2 skip MMAs, 4 skip TMA loads
 };
 
@@ -525,15 +526,17 @@ __global__ void __launch_bounds__(kThreads, 1)
             int stage = 0;
             uint32_t phase = 0;
             for (int t = cluster; t < p.total_tiles; t += n_clusters) {
-                const int z = t / p.tiles_per_batch;
-                const int r = t - z * p.tiles_per_batch;
+                const int tt = t / p.ksplit, split = t - tt * p.ksplit;  // split-K unit
+                const int z = tt / p.tiles_per_batch;
+                const int r = tt - z * p.tiles_per_batch;
                 const int mt = r % p.tiles_m, nt = r / p.tiles_m;
                 const int zb = z / p.bh, zh = z - zb * p.bh;
                 const int ra = p.ra0 * zb + p.ra1 * zh, ca = p.ca0 * zb + p.ca1 * zh;
                 const int rb = p.rb0 * zb + p.rb1 * zh, cb = p.cb0 * zb + p.cb1 * zh;
                 const int m0 = mt * 256 + half * 128;
                 const int n0 = (nt * NPAIR + pair) * PAIR_BN + half * 128;
-                for (int kb = 0; kb < p.k_blocks; ++kb) {
+                const int kb0 = split * p.kb_per_split, kb1 = min(p.k_blocks, kb0 + p.kb_per_split);
+                for (int kb = kb0; kb < kb1; ++kb) {
                     mbar_wait(&empty[stage], phase ^ 1);
                     if (p.dbg & 4) {  // experiment: no operand traffic
                         if (leader) mbar_arrive(&full[stage]);
@@ -590,10 +593,12 @@ __global__ void __launch_bounds__(kThreads, 1)
             int acc = 0;
             uint32_t acc_phase = 0;
             for (int t = cluster; t < p.total_tiles; t += n_clusters) {
+                const int split = t % p.ksplit;
+                const int kb0 = split * p.kb_per_split, kb1 = min(p.k_blocks, kb0 + p.kb_per_split);
                 mbar_wait(&tempty[acc], acc_phase ^ 1);
                 tc_fence_after();
                 const uint32_t d_tmem = tmem_base + static_cast<uint32_t>(acc * PAIR_BN);
-                for (int kb = 0; kb < p.k_blocks; ++kb) {
+                for (int kb = kb0; kb < kb1; ++kb) {
                     mbar_wait(&full[stage], phase);
                     tc_fence_after();
                     const uint32_t a_base = smem_u32(sa + stage * C::A_BYTES);
@@ -604,7 +609,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                                                  : make_sdesc(a_base + k * 32, 16, 1024);
                         const uint64_t bd = B_MN ? make_sdesc(b_base + k * 2048, 64 * BK * 2, 1024)
                                                  : make_sdesc(b_base + k * 32, 16, 1024);
-                        if (!(p.dbg & 2)) mma_bf16_pair(d_tmem, ad, bd, idesc, (kb | k) != 0 ? 1u : 0u);
+                        if (!(p.dbg & 2)) mma_bf16_pair(d_tmem, ad, bd, idesc, (kb != kb0 || k != 0) ? 1u : 0u);
                     }
                     mma_commit_pair(&empty[stage], all_mask);
                     if (++stage == C::STAGES) {
@@ -626,8 +631,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         int acc = 0;
         uint32_t acc_phase = 0;
         for (int t = cluster; t < p.total_tiles; t += n_clusters) {
-            const int z = t / p.tiles_per_batch;
-            const int r = t - z * p.tiles_per_batch;
+            const int tt = t / p.ksplit;
+            const int z = tt / p.tiles_per_batch;
+            const int r = tt - z * p.tiles_per_batch;
             const int mt = r % p.tiles_m, nt = r / p.tiles_m;
             const int zb = z / p.bh, zh = z - zb * p.bh;
             const long long rd = p.rd0 * zb + p.rd1 * zh, cd = p.cd0 * zb + p.cd1 * zh;
@@ -745,6 +751,14 @@ int encode_2d_out(CUtensorMap* m, const void* ptr, long long rows, long long col
                            f32 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B,
                            CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     return r == CUDA_SUCCESS ? SWARM_OK : SWARM_E_INVALID;
+}
+
+bool ksplit_enabled() {
+    static const bool on = [] {
+        const char* e = getenv("SWARM_GEMM_KSPLIT");
+        return !(e && e[0] == '0');
+    }();
+    return on;
 }
 
 bool tma_epi_enabled() {
@@ -892,6 +906,8 @@ extern "C" int swarm_gemm_bf16(const swarm_gemm_args* a, swarm_stream_t stream) 
     p.tiles_per_batch = p.tiles_m * p.tiles_n;
     p.total_tiles = p.tiles_per_batch * a->batch;
     p.k_blocks = (a->k + BK - 1) / BK;
+    p.ksplit = 1;
+    p.kb_per_split = p.k_blocks;
     p.ra0 = a->ra0; p.ra1 = a->ra1; p.ca0 = a->ca0; p.ca1 = a->ca1;
     p.rb0 = a->rb0; p.rb1 = a->rb1; p.cb0 = a->cb0; p.cb1 = a->cb1;
     p.d = a->d;
@@ -927,6 +943,26 @@ extern "C" int swarm_gemm_bf16(const swarm_gemm_args* a, swarm_stream_t stream) 
         rc = encode_2d_out(&td, a->d, d_rows, d_cols, a->ldd, f32);
         if (rc == SWARM_OK && a->epilogue == SWARM_EPI_GELU) rc = encode_2d_out(&tu, a->aux, d_rows, d_cols, a->ldd, false);
         if (rc != SWARM_OK) p.tma_epi = 0;  // fall back to direct stores
+    }
+    // Split-K for fp32 reduce-add outputs: partial tiles simply reduce-add, so
+    // pick the split (<= 4, >= 8 k-blocks each) that best fills whole waves of
+    // clusters — the GEMM wave tail (e.g. 256 tiles on 74 clusters) disappears.
+    if (pair && p.tma_epi && a->epilogue == SWARM_EPI_ACCUM_F32 && ksplit_enabled()) {
+        const int clusters = num_sms() / (2 * npair);
+        double best = 0.0;
+        for (int sp = 1; sp <= 4; ++sp) {
+            const int kps = (p.k_blocks + sp - 1) / sp;
+            if (sp > 1 && kps < 8) break;
+            const int units = p.tiles_per_batch * a->batch * sp;
+            const double eff = static_cast<double>(units) / (static_cast<double>((units + clusters - 1) / clusters) * clusters);
+            if (eff > best + 0.02) {
+                best = eff;
+                p.ksplit = sp;
+                p.kb_per_split = kps;
+            }
+        }
+        p.ksplit = (p.k_blocks + p.kb_per_split - 1) / p.kb_per_split;
+        p.total_tiles = p.tiles_per_batch * a->batch * p.ksplit;
     }
     cudaStream_t st = as_stream(stream);
     if (pair && npair == 2) return dispatch_pair<2>(a->a_mn_major, a->b_mn_major, ta, tb, td, tu, p, st);
