@@ -198,6 +198,22 @@ int swarm_cast_f32_bf16(const float* in, void* out, size_t n, swarm_stream_t str
  * the stage; activations for up to max_slots in-flight microbatches too.  */
 #define SWARM_WIRE_BF16 0
 #define SWARM_WIRE_INT8 1
+/* Wire message = payload ‖ header.  INT8 payload: codes[n] (padded to 16 B) then
+ * fp32 scales[ceil(n/block)] (padded to 16 B); BF16 payload: bf16[n] (padded).
+ * The last 16 bytes are this header (one self-describing message
+ * per hop, one NCCL call). */
+#define SWARM_WIRE_MAGIC 0x314D5753u /* "SWM1" */
+typedef struct {
+    uint32_t magic;
+    uint32_t n_elems;
+    uint32_t block_size;
+    uint8_t kind; /* SWARM_WIRE_* */
+    uint8_t maxout_k;
+    uint8_t version;
+    uint8_t reserved;
+} swarm_wire_header;
+/* parse a header copied to host memory (last sizeof(swarm_wire_header) bytes of a message) */
+int swarm_wire_parse_header(const void* header, uint32_t* n_elems, uint32_t* block_size, int* kind, int* maxout_k);
 typedef struct swarm_stage* swarm_stage_t;
 typedef struct {
     int d_model, n_heads, d_ffn, seq_len, micro_batch;

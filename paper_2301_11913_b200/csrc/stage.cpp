@@ -68,6 +68,7 @@ struct swarm_stage {
     std::vector<Slot> slots;
     // workspaces (one visit at a time per stage)
     float *S = nullptr, *dP = nullptr, *logits = nullptr;
+    void* wire_hdr = nullptr;  // device copy of this stage's swarm_wire_header
     bf16 *dS = nullptr, *gy[2] = {nullptr, nullptr}, *dhid = nullptr, *dc = nullptr, *du = nullptr, *dqkv = nullptr,
          *dO = nullptr, *da = nullptr, *dlogits = nullptr, *wtmp = nullptr;
     void* lnws = nullptr;
@@ -334,14 +335,18 @@ int block_backward(swarm_stage* s, const Act& A, const bf16* dy, bf16* dx, const
     return join_side(s, st);
 }
 
-size_t wire_bytes(const swarm_stage* s) {
+// Wire message: payload (int8 codes, 16-B padded, then fp32 per-block scales;
+// or raw bf16) followed by a 16-byte swarm_wire_header.
+size_t wire_payload_bytes(const swarm_stage* s) {
     const size_t n = static_cast<size_t>(s->T) * s->wire_w;
     if (s->cfg.wire == SWARM_WIRE_INT8) {
         const size_t bs = static_cast<size_t>(s->cfg.block_size);
-        return ((n + 15) & ~size_t(15)) + ((n + bs - 1) / bs) * sizeof(float);
+        return ((n + 15) & ~size_t(15)) + (((n + bs - 1) / bs) * sizeof(float) + 15) / 16 * 16;
     }
-    return n * 2;
+    return (n * 2 + 15) / 16 * 16;
 }
+
+size_t wire_bytes(const swarm_stage* s) { return wire_payload_bytes(s) + sizeof(swarm_wire_header); }
 
 int wire_decode(swarm_stage* s, const void* msg, bf16* out, cudaStream_t st) {
     const size_t n = static_cast<size_t>(s->T) * s->wire_w;
@@ -357,6 +362,10 @@ int wire_decode(swarm_stage* s, const void* msg, bf16* out, cudaStream_t st) {
 
 int wire_encode(swarm_stage* s, const bf16* x, void* msg, cudaStream_t st) {
     const size_t n = static_cast<size_t>(s->T) * s->wire_w;
+    // header first (a 16-byte device-to-device copy of the stage's prebuilt header)
+    if (cudaMemcpyAsync(static_cast<char*>(msg) + wire_payload_bytes(s), s->wire_hdr, sizeof(swarm_wire_header),
+                        cudaMemcpyDeviceToDevice, st) != cudaSuccess)
+        return SWARM_E_CUDA;
     if (s->cfg.wire == SWARM_WIRE_INT8) {
         int8_t* codes = static_cast<int8_t*>(msg);
         void* scales = static_cast<char*>(msg) + ((n + 15) & ~size_t(15));
@@ -504,6 +513,17 @@ int create(const swarm_stage_config* c, swarm_stage* s) {
     TRY(alloc(s, &s->dO, Td));
     TRY(alloc(s, &s->da, Td));
     TRY(alloc(s, &s->wtmp, T * s->wire_w));
+    {
+        swarm_wire_header h{};
+        h.magic = SWARM_WIRE_MAGIC;
+        h.n_elems = static_cast<uint32_t>(T * s->wire_w);
+        h.block_size = static_cast<uint32_t>(c->block_size);
+        h.kind = static_cast<uint8_t>(c->wire);
+        h.maxout_k = static_cast<uint8_t>(s->bneck ? c->maxout_k : 1);
+        h.version = 1;
+        TRY(dmalloc(s, &s->wire_hdr, sizeof(h)));
+        if (cudaMemcpy(s->wire_hdr, &h, sizeof(h), cudaMemcpyHostToDevice) != cudaSuccess) return SWARM_E_CUDA;
+    }
     TRY(dmalloc(s, &s->lnws, swarm_layer_norm_backward_workspace(T, d)));
     if (c->is_last) {
         TRY(alloc(s, &s->logits, T * s->V));
@@ -548,6 +568,16 @@ void swarm_stage_destroy(swarm_stage_t s) {
 }
 
 size_t swarm_stage_wire_bytes(swarm_stage_t s) { return wire_bytes(s); }
+
+int swarm_wire_parse_header(const void* header, uint32_t* n_elems, uint32_t* block_size, int* kind, int* maxout_k) {
+    const auto* h = static_cast<const swarm_wire_header*>(header);
+    if (!h || h->magic != SWARM_WIRE_MAGIC || h->version != 1) return fail("wire: bad header");
+    if (n_elems) *n_elems = h->n_elems;
+    if (block_size) *block_size = h->block_size;
+    if (kind) *kind = h->kind;
+    if (maxout_k) *maxout_k = h->maxout_k;
+    return SWARM_OK;
+}
 
 void swarm_stage_profile(swarm_stage_t s, int enable) { s->prof_on = enable != 0; }
 

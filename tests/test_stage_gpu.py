@@ -118,7 +118,16 @@ def test_two_stage_int8_boundary(cuda):
     y0 = s0.activation(0, 0, "out")
     st, codes, scales = O.quantize(y0.view(torch.int16).cpu().numpy().view(np.uint16), c0.block_size)
     assert np.array_equal(act[:n].cpu().numpy().view(np.int8), codes)
-    assert np.array_equal(act[(n + 15) // 16 * 16:].view(torch.float32).cpu().numpy(), scales)
+    off = (n + 15) // 16 * 16
+    assert np.array_equal(act[off:off + scales.size * 4].view(torch.float32).cpu().numpy(), scales)
+    # the message ends with a self-describing header
+    import ctypes as C
+    from paper_2301_11913_b200 import _lib
+    hdr = act[-16:].cpu().numpy().copy()
+    ne, bsz, kind, mk = C.c_uint32(), C.c_uint32(), C.c_int(), C.c_int()
+    assert _lib.lib().swarm_wire_parse_header(hdr.ctypes.data_as(C.c_void_p), C.byref(ne), C.byref(bsz), C.byref(kind),
+                                              C.byref(mk)) == 0
+    assert (ne.value, bsz.value, kind.value, mk.value) == (n, c0.block_size, 1, 1)
     # stage 1 vs oracle on the exact dequantized input
     x1 = decode_wire(s1, act).double().cpu().requires_grad_()
     P1 = oracle_params(s1)
@@ -186,7 +195,7 @@ def test_two_stage_maxout_bottleneck(cuda):
     c1 = tiny_cfg(is_first=0, seed=5, maxout_k=2)
     s0, s1 = Stage(c0), Stage(c1)
     w = c0.d_model // 2
-    assert s0.wire_bytes == (c0.tokens * w + 15) // 16 * 16 + c0.tokens * w // c0.block_size * 4
+    assert s0.wire_bytes == (c0.tokens * w + 15) // 16 * 16 + (c0.tokens * w // c0.block_size * 4 + 15) // 16 * 16 + 16
     g = torch.Generator().manual_seed(8)
     tok = torch.randint(0, c0.vocab, (c0.tokens,), generator=g)
     tgt = torch.randint(0, c0.vocab, (c0.tokens,), generator=g)
