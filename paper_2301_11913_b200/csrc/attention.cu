@@ -11,9 +11,10 @@
 // (SPEC:90 folds it into 6*P*T); parity is against the fp64 block oracle.
 //
 // Warp roles: warp 0 TMA (Q/dO block, K/V rows, and in the backward the P block
-// after the MMAs), warp 1 MMA issuer, warp 2 TMEM allocator, warps 4-7 one
-// row per thread for the softmax epilogue, staged through swizzled smem and
-// written with TMA stores.
+// after the MMAs), warp 1 MMA issuer, warp 2 TMEM allocator; then all 8 warps
+// run the softmax epilogue (one row per thread, key columns split between warps
+// 4-7 and 0-3, row statistics combined through smem), staged through swizzled
+// smem and written with TMA stores.
 #include <cudaTypedefs.h>
 
 #include <algorithm>
@@ -39,10 +40,10 @@ struct Params {
 };
 
 // smem: A [dh/64][128 x 64] bf16 | B [dh/64][L x 64] bf16 (reused for the P tile
-// in the backward) | staging 4 warps x 2 x 4 KB | barriers
+// in the backward) | staging 8 warps x 4 KB | barriers
 constexpr int kABytes = (kMaxDh / 64) * BQ * 64 * 2;       // 32 KB
 constexpr int kBBytes = (kMaxDh / 64) * kMaxL * 64 * 2;    // 128 KB (>= the 128 x 512 P tile)
-constexpr int kStgBytes = 4 * 2 * kSlot;                   // 32 KB
+constexpr int kStgBytes = 8 * kSlot;                       // 32 KB
 constexpr int kSmem = kABytes + kBBytes + kStgBytes + 1024 + 128;
 static_assert(kSmem <= 232448, "attention kernel exceeds 227 KB smem");
 
@@ -158,46 +159,67 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
         }
         mma_commit(bar_mma);
-    } else if (warp >= 4) {
+    }
+    __syncwarp();  // lanes of warps 0/1 re-converge after their single-thread roles
+    {
         // ------------------------------------------------------------ softmax epilogue
-        const int q = warp - 4;
+        // All 8 warps: warp w owns TMEM lane quarter w % 4 (32 rows, one per
+        // thread); warps 4-7 take the first half of the key chunks, warps 0-3 the
+        // second half (and the all-masked tail); row statistics meet in smem.
+        __shared__ float st_a[2][BQ], st_b[2][BQ];
+        const int q = warp & 3;
+        const int grp = warp >= 4 ? 0 : 1;
         const int r = q * 32 + lane;            // row inside the block
         const int qi = mt * BQ + r;             // query position in the sequence
         const int valid = p.causal ? qi + 1 : p.L;
         const uint32_t trow = tmem + (static_cast<uint32_t>(q * 32) << 16);
-        uint8_t* stg = stg_all + q * 2 * kSlot;
-        int slot_idx = 0;
+        uint8_t* stg = stg_all + (warp & 7) * kSlot;  // one 4 KB slot per warp (8 warps)
         const int out_row = z * p.L + mt * BQ + q * 32;
+        const int n32 = kv_len / 32;
+        const int split = (n32 / 2) * 32;
+        const int c_lo = grp == 0 ? 0 : split, c_hi = grp == 0 ? split : kv_len;
         mbar_wait(bar_mma, 0);
         tc_fence_after();
         const float l2e = 1.4426950408889634f;
-        float stat_a = 0.f, stat_b = 0.f;  // fwd: running max / sum; bwd: rowsum(P*dP)
+        float stat_a = 0.f, stat_b = 0.f;  // fwd: row max / 1/sum; bwd: rowsum(P*dP)
         if constexpr (!BWD) {
             float m = -INFINITY, s = 0.f;
-            for (int c0 = 0; c0 < kv_len; c0 += 32) {
-                uint32_t rr[32];
-                tmem_ld_32x32b_x32(trow + c0, rr);
+            for (int c0 = c_lo; c0 < c_hi; c0 += 64) {
+                uint32_t ra[32], rb[32];
+                tmem_ld_32x32b_x32(trow + c0, ra);
+                tmem_ld_32x32b_x32(trow + c0 + 32, rb);
                 tmem_ld_wait();
                 float cm = -INFINITY;
 #pragma unroll
-                for (int j = 0; j < 32; ++j)
-                    if (c0 + j < valid) cm = fmaxf(cm, __uint_as_float(rr[j]));
+                for (int j = 0; j < 32; ++j) {
+                    if (c0 + j < valid) cm = fmaxf(cm, __uint_as_float(ra[j]));
+                    if (c0 + 32 + j < valid) cm = fmaxf(cm, __uint_as_float(rb[j]));
+                }
                 const float nm = fmaxf(m, cm * p.scale);
                 if (nm != -INFINITY) {
                     float add = 0.f;
 #pragma unroll
-                    for (int j = 0; j < 32; ++j)
-                        if (c0 + j < valid) add += exp2f((__uint_as_float(rr[j]) * p.scale - nm) * l2e);
+                    for (int j = 0; j < 32; ++j) {
+                        if (c0 + j < valid) add += exp2f((__uint_as_float(ra[j]) * p.scale - nm) * l2e);
+                        if (c0 + 32 + j < valid) add += exp2f((__uint_as_float(rb[j]) * p.scale - nm) * l2e);
+                    }
                     s = (m == -INFINITY ? 0.f : s * exp2f((m - nm) * l2e)) + add;
                     m = nm;
                 }
             }
-            stat_a = m;
-            stat_b = 1.f / s;
+            st_a[grp][r] = m;
+            st_b[grp][r] = s;
+            asm volatile("bar.sync 1, 256;" ::: "memory");
+            const float m0 = st_a[0][r], m1 = st_a[1][r];
+            const float mm = fmaxf(m0, m1);
+            const float ss = (m0 == -INFINITY ? 0.f : st_b[0][r] * exp2f((m0 - mm) * l2e)) +
+                             (m1 == -INFINITY ? 0.f : st_b[1][r] * exp2f((m1 - mm) * l2e));
+            stat_a = mm;
+            stat_b = 1.f / ss;
         } else {
             mbar_wait(bar_p, 0);
             float acc = 0.f;
-            for (int c0 = 0; c0 < kv_len; c0 += 32) {
+            for (int c0 = c_lo; c0 < c_hi; c0 += 32) {
                 uint32_t rr[32];
                 tmem_ld_32x32b_x32(trow + c0, rr);
                 tmem_ld_wait();
@@ -206,10 +228,13 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
                 for (int j = 0; j < 32; ++j) acc += pv[j] * __uint_as_float(rr[j]);
             }
-            stat_a = acc;
+            st_a[grp][r] = acc;
+            asm volatile("bar.sync 1, 256;" ::: "memory");
+            stat_a = st_a[0][r] + st_a[1][r];
         }
         // second pass: normalise (fwd) / form dS (bwd); masked / skipped columns write 0
-        for (int c0 = 0; c0 < p.L; c0 += 32) {
+        const int w_hi = grp == 0 ? c_hi : p.L;
+        for (int c0 = c_lo; c0 < w_hi; c0 += 32) {
             float v[32];
             if (c0 < kv_len) {
                 uint32_t rr[32];
@@ -230,15 +255,13 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
                 for (int j = 0; j < 32; ++j) v[j] = 0.f;
             }
-            uint8_t* slot = stg + slot_idx * kSlot;
-            slot_idx ^= 1;
-            if (lane == 0) bulk_wait_read<1>();
+            if (lane == 0) bulk_wait_read<0>();  // this warp's single slot is free again
             __syncwarp();
-            stage_bf16(slot, lane, v);
+            stage_bf16(stg, lane, v);
             fence_async_smem();
             __syncwarp();
             if (lane == 0) {
-                tma_store_2d(&tma_out, slot, c0, out_row);
+                tma_store_2d(&tma_out, stg, c0, out_row);
                 bulk_commit();
             }
         }

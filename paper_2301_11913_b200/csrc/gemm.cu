@@ -753,10 +753,12 @@ int encode_2d_out(CUtensorMap* m, const void* ptr, long long rows, long long col
     return r == CUDA_SUCCESS ? SWARM_OK : SWARM_E_INVALID;
 }
 
+// Split-K for reduce-add GEMMs is opt-in (SWARM_GEMM_KSPLIT=1): measured slower —
+// the extra partial-tile reduce-add traffic costs more than the wave tail it removes.
 bool ksplit_enabled() {
     static const bool on = [] {
         const char* e = getenv("SWARM_GEMM_KSPLIT");
-        return !(e && e[0] == '0');
+        return e && e[0] == '1';
     }();
     return on;
 }

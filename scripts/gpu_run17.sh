@@ -1,0 +1,19 @@
+cd $GRAFT_REPO_ROOT
+timeout -k 5 300 python -m pytest tests/test_attention_gpu.py tests/test_stage_gpu.py tests/test_pipeline_gpu.py -q -p no:cacheprovider > gpurun_out/t17.log 2>&1; echo "rc=$?" >> gpurun_out/t17.log
+timeout -k 10 600 python bench.py --steps 3 --warmup 3 --no-cpu-baseline --no-codec > gpurun_out/b17_C.log 2>&1; echo "rc=$?" >> gpurun_out/b17_C.log
+cat > /tmp/attn_time.py <<'PY'
+import sys, math, ctypes as C; sys.path.insert(0, ".")
+import torch
+from paper_2301_11913_b200 import _lib
+B,H,L,dh=4,16,512,128; d=H*dh
+qkv=torch.randn(B*L,3*d,device="cuda").bfloat16(); P=torch.empty(B*H*L,L,device="cuda",dtype=torch.bfloat16)
+dO=torch.randn(B*L,d,device="cuda").bfloat16(); dS=torch.empty_like(P); st=torch.cuda.current_stream().cuda_stream
+f=lambda: _lib.lib().swarm_attn_scores_softmax(C.c_void_p(qkv.data_ptr()),C.c_void_p(qkv[:,d:].data_ptr()),3*d,d,B,H,L,dh,1/math.sqrt(dh),1,C.c_void_p(P.data_ptr()),st)
+g=lambda: _lib.lib().swarm_attn_scores_softmax_backward(C.c_void_p(dO.data_ptr()),d,C.c_void_p(qkv[:,2*d:].data_ptr()),3*d,d,C.c_void_p(P.data_ptr()),B,H,L,dh,1/math.sqrt(dh),1,C.c_void_p(dS.data_ptr()),st)
+for name,fn in (("fwd",f),("bwd",g)):
+    for _ in range(3): fn()
+    torch.cuda.synchronize(); e0,e1=torch.cuda.Event(True),torch.cuda.Event(True); e0.record()
+    for _ in range(20): fn()
+    e1.record(); torch.cuda.synchronize(); print(name, e0.elapsed_time(e1)/20*1e3, "us")
+PY
+timeout -k 5 120 python /tmp/attn_time.py > gpurun_out/attn17.log 2>&1
