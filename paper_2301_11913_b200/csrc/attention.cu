@@ -40,12 +40,19 @@ struct Params {
 };
 
 // smem: A [dh/64][128 x 64] bf16 | B [dh/64][L x 64] bf16 (reused for the P tile
-// in the backward) | staging 8 warps x 4 KB | barriers
+// in the backward) | staging 8 warps x 2 x 4 KB | barriers
 constexpr int kABytes = (kMaxDh / 64) * BQ * 64 * 2;       // 32 KB
 constexpr int kBBytes = (kMaxDh / 64) * kMaxL * 64 * 2;    // 128 KB (>= the 128 x 512 P tile)
-constexpr int kStgBytes = 8 * kSlot;                       // 32 KB
+constexpr int kStgBytes = 8 * 2 * kSlot;                   // 64 KB: 8 warps x double buffer
 constexpr int kSmem = kABytes + kBBytes + kStgBytes + 1024 + 128;
 static_assert(kSmem <= 232448, "attention kernel exceeds 227 KB smem");
+
+// 2^x on the SFU (ex2.approx.ftz: 2 ulp; the probabilities are rounded to bf16 anyway)
+__device__ __forceinline__ float fast_exp2(float x) {
+    float y;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
 
 __device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
     const __nv_bfloat162 p = __floats2bfloat162_rn(a, b);
@@ -173,7 +180,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int qi = mt * BQ + r;             // query position in the sequence
         const int valid = p.causal ? qi + 1 : p.L;
         const uint32_t trow = tmem + (static_cast<uint32_t>(q * 32) << 16);
-        uint8_t* stg = stg_all + (warp & 7) * kSlot;  // one 4 KB slot per warp (8 warps)
+        uint8_t* stg = stg_all + (warp & 7) * 2 * kSlot;  // two 4 KB slots per warp
+        int slot_idx = 0;
         const int out_row = z * p.L + mt * BQ + q * 32;
         const int n32 = kv_len / 32;
         const int split = (n32 / 2) * 32;
@@ -200,10 +208,10 @@ __global__ void __launch_bounds__(kThreads, 1)
                     float add = 0.f;
 #pragma unroll
                     for (int j = 0; j < 32; ++j) {
-                        if (c0 + j < valid) add += exp2f((__uint_as_float(ra[j]) * p.scale - nm) * l2e);
-                        if (c0 + 32 + j < valid) add += exp2f((__uint_as_float(rb[j]) * p.scale - nm) * l2e);
+                        if (c0 + j < valid) add += fast_exp2((__uint_as_float(ra[j]) * p.scale - nm) * l2e);
+                        if (c0 + 32 + j < valid) add += fast_exp2((__uint_as_float(rb[j]) * p.scale - nm) * l2e);
                     }
-                    s = (m == -INFINITY ? 0.f : s * exp2f((m - nm) * l2e)) + add;
+                    s = (m == -INFINITY ? 0.f : s * fast_exp2((m - nm) * l2e)) + add;
                     m = nm;
                 }
             }
@@ -212,8 +220,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             asm volatile("bar.sync 1, 256;" ::: "memory");
             const float m0 = st_a[0][r], m1 = st_a[1][r];
             const float mm = fmaxf(m0, m1);
-            const float ss = (m0 == -INFINITY ? 0.f : st_b[0][r] * exp2f((m0 - mm) * l2e)) +
-                             (m1 == -INFINITY ? 0.f : st_b[1][r] * exp2f((m1 - mm) * l2e));
+            const float ss = (m0 == -INFINITY ? 0.f : st_b[0][r] * fast_exp2((m0 - mm) * l2e)) +
+                             (m1 == -INFINITY ? 0.f : st_b[1][r] * fast_exp2((m1 - mm) * l2e));
             stat_a = mm;
             stat_b = 1.f / ss;
         } else {
@@ -243,7 +251,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 if constexpr (!BWD) {
 #pragma unroll
                     for (int j = 0; j < 32; ++j)
-                        v[j] = (c0 + j < valid) ? exp2f((__uint_as_float(rr[j]) * p.scale - stat_a) * l2e) * stat_b
+                        v[j] = (c0 + j < valid) ? fast_exp2((__uint_as_float(rr[j]) * p.scale - stat_a) * l2e) * stat_b
                                                 : 0.f;
                 } else {
                     float pv[32];
@@ -255,13 +263,15 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
                 for (int j = 0; j < 32; ++j) v[j] = 0.f;
             }
-            if (lane == 0) bulk_wait_read<0>();  // this warp's single slot is free again
+            uint8_t* slot = stg + slot_idx * kSlot;
+            slot_idx ^= 1;
+            if (lane == 0) bulk_wait_read<1>();  // the store issued from this slot two chunks ago has read it
             __syncwarp();
-            stage_bf16(stg, lane, v);
+            stage_bf16(slot, lane, v);
             fence_async_smem();
             __syncwarp();
             if (lane == 0) {
-                tma_store_2d(&tma_out, stg, c0, out_row);
+                tma_store_2d(&tma_out, slot, c0, out_row);
                 bulk_commit();
             }
         }
