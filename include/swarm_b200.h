@@ -251,6 +251,10 @@ int swarm_stage_optimizer_step(swarm_stage_t st, float grad_scale, swarm_stream_
 float* swarm_stage_grads(swarm_stage_t st);  /* fp32 [num_params]: intra-stage all-reduce buffer */
 float* swarm_stage_params(swarm_stage_t st); /* fp32 master [num_params] */
 void* swarm_stage_params_bf16(swarm_stage_t st);
+/* migration state (params() + AdamW m, v, step): what a peer moving to this stage
+ * downloads from a stage-mate (P/src/rebalancer.cpp:71-75 counts these bytes) */
+int swarm_stage_optimizer_state(swarm_stage_t st, float** m, float** v, int* step);
+int swarm_stage_set_step(swarm_stage_t st, int step);
 /* re-derive the bf16 shadow from the fp32 master (after loading / receiving weights) */
 int swarm_stage_sync_shadow(swarm_stage_t st, swarm_stream_t stream);
 /* enumerate parameter tensors: index -> name, offset (elements), rows, cols */

@@ -90,6 +90,8 @@ def _load_ref():
     lib.ref_router_priority_of.argtypes = [P, C.c_uint64]
     lib.ref_router_priority_of.restype = C.c_double
     lib.ref_rebalance_decide.argtypes = [sz, P, P, P, P, P, P, P]
+    lib.ref_oracle_throughput.argtypes = [P, sz, C.c_int64]
+    lib.ref_oracle_throughput.restype = C.c_double
     return lib
 
 

@@ -105,3 +105,14 @@ int ref_rebalance_decide(size_t n_stages, const size_t* offsets, const uint64_t*
 }
 
 }  // extern "C"
+
+// The reference's best-case pipeline rate for `total_peers` peers given per-peer
+// rates per stage (P/src/sim.cpp:88-116) — the CPU prediction for config E.
+#include "swarmsim/sim.hpp"
+extern "C" double ref_oracle_throughput(const double* rates, size_t n_stages, int64_t total_peers) {
+    try {
+        return swarmsim::sim::oracle_throughput(std::vector<double>(rates, rates + n_stages), total_peers);
+    } catch (...) {
+        return -1.0;
+    }
+}

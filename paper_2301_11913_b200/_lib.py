@@ -77,6 +77,8 @@ SIGNATURES = {
     "swarm_stage_param_info": (I, [P, I, C.POINTER(C.c_char_p), C.POINTER(SZ), C.POINTER(SZ), C.POINTER(SZ)]),
     "swarm_stage_activation": (I, [P, I, I, C.c_char_p, C.POINTER(P), C.POINTER(SZ)]),
     "swarm_stage_profile": (None, [P, I]),
+    "swarm_stage_optimizer_state": (I, [P, C.POINTER(P), C.POINTER(P), C.POINTER(I)]),
+    "swarm_stage_set_step": (I, [P, I]),
     "swarm_wire_parse_header": (I, [P, C.POINTER(C.c_uint32), C.POINTER(C.c_uint32), C.POINTER(I), C.POINTER(I)]),
     "swarm_stage_profile_read": (I, [P, C.POINTER(D), C.POINTER(D), C.POINTER(C.c_uint64)]),
     "swarm_router_last_error": (C.c_char_p, []),

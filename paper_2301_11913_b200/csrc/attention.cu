@@ -173,7 +173,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         // All 8 warps: warp w owns TMEM lane quarter w % 4 (32 rows, one per
         // thread); warps 4-7 take the first half of the key chunks, warps 0-3 the
         // second half (and the all-masked tail); row statistics meet in smem.
-        __shared__ float st_a[2][BQ], st_b[2][BQ];
+        // row statistics live in the A (Q / dO) tile, dead once the MMAs completed
+        float (*st_a)[BQ] = reinterpret_cast<float (*)[BQ]>(sa);
+        float (*st_b)[BQ] = reinterpret_cast<float (*)[BQ]>(sa + 2 * BQ * sizeof(float));
         const int q = warp & 3;
         const int grp = warp >= 4 ? 0 : 1;
         const int r = q * 32 + lane;            // row inside the block

@@ -734,6 +734,19 @@ int swarm_stage_backward(swarm_stage_t s, int slot, const void* grad_in, void* g
     return wire_encode(s, s->dqkv, grad_out, st);
 }
 
+int swarm_stage_optimizer_state(swarm_stage_t s, float** m, float** v, int* step) {
+    if (m) *m = s->m;
+    if (v) *v = s->v;
+    if (step) *step = s->step;
+    return SWARM_OK;
+}
+
+int swarm_stage_set_step(swarm_stage_t s, int step) {
+    if (step < 0) return fail("set_step: negative step");
+    s->step = step;
+    return SWARM_OK;
+}
+
 int swarm_stage_optimizer_step(swarm_stage_t s, float grad_scale, swarm_stream_t stream) {
     s->step += 1;
     const auto& c = s->cfg;

@@ -131,6 +131,16 @@ class Stage:
     def params_bf16(self) -> torch.Tensor:
         return device_view(self.lib.swarm_stage_params_bf16(self.h), self.n_params, torch.bfloat16, self.device)
 
+    def optimizer_state(self):
+        """(m, v, step): AdamW moments as fp32 device views and the step counter."""
+        m, v, step = C.c_void_p(), C.c_void_p(), C.c_int()
+        L.check(self.lib.swarm_stage_optimizer_state(self.h, C.byref(m), C.byref(v), C.byref(step)), "optimizer_state")
+        return (device_view(m.value, self.n_params, torch.float32, self.device),
+                device_view(v.value, self.n_params, torch.float32, self.device), step.value)
+
+    def set_step(self, step: int) -> None:
+        L.check(self.lib.swarm_stage_set_step(self.h, step), "set_step")
+
     def param_info(self):
         out, i = [], 0
         name, off, r, c = C.c_char_p(), C.c_size_t(), C.c_size_t(), C.c_size_t()

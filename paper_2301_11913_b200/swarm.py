@@ -75,31 +75,51 @@ PRESETS = {
 
 @dataclass
 class Placement:
-    """Which GPU serves which (stage, replica).  Peer id = stage * P + replica."""
+    """Which GPU serves which stage.  With world >= S every rank is one peer
+    (peer id == rank) and `layout` gives the peers per stage (default: even
+    split, P = world / S); membership changes with failures and migrations.
+    With world < S every rank hosts S / world consecutive stages (one peer
+    each, peer id == stage)."""
     world: int
     n_stages: int
+    layout: list | None = None
 
     def __post_init__(self):
         W, S = self.world, self.n_stages
         if W >= S:
-            if W % S:
-                raise ValueError(f"world {W} must be a multiple of the stage count {S}")
-            self.P, self.per_rank = W // S, 1
+            if self.layout is None:
+                if W % S:
+                    raise ValueError(f"world {W} must be a multiple of the stage count {S}")
+                self.layout = [W // S] * S
+            if len(self.layout) != S or sum(self.layout) != W or min(self.layout) < 1:
+                raise ValueError(f"layout {self.layout} must give >= 1 peer to each of {S} stages and sum to {W}")
+            self.per_rank = 1
+            self.stage_of = [s for s, n in enumerate(self.layout) for _ in range(n)]
         else:
             if S % W:
                 raise ValueError(f"stage count {S} must be a multiple of world {W}")
-            self.P, self.per_rank = 1, S // W
-        self.peers = [(s, p) for s in range(S) for p in range(self.P)]
+            self.per_rank = S // W
+            self.layout = [1] * S
+            self.stage_of = list(range(S))
+        self.P = max(self.layout)
+        self.alive = set(range(len(self.stage_of)))
+
+    @property
+    def peers(self) -> list[tuple[int, int]]:
+        return [(s, pid) for pid, s in enumerate(self.stage_of)]
 
     def stage_of_peer(self, pid: int) -> int:
-        return self.peers[pid][0]
+        return self.stage_of[pid]
 
     def rank_of_peer(self, pid: int) -> int:
-        return pid if self.world >= self.n_stages else self.peers[pid][0] // self.per_rank
+        return pid if self.world >= self.n_stages else self.stage_of[pid] // self.per_rank
+
+    def members(self, stage: int) -> list[int]:
+        return sorted(pid for pid in self.alive if self.stage_of[pid] == stage)
 
     def local_stages(self, rank: int) -> list[int]:
         if self.world >= self.n_stages:
-            return [rank // self.P]
+            return [self.stage_of[rank]] if rank in self.alive else []
         return list(range(rank * self.per_rank, (rank + 1) * self.per_rank))
 
 
@@ -110,18 +130,35 @@ class RoutePlanner:
     record_response after each modeled visit (forward 0..S-1, then backward
     S-1..0 on the same route), the per-trainer call order of the reference
     engine (sim.cpp:472-510).  Routes are therefore a pure function of the
-    configuration and the step index."""
+    configuration, the step index and the membership events (remove on failure,
+    ban + re-add on migration, as kill_worker / begin_migration /
+    on_migration_complete do, sim.cpp:583-719)."""
 
     def __init__(self, placement: Placement, n_trainers: int, fwd_seconds: float, gamma: float = 0.1,
-                 epsilon: float = 1.0, backward_multiplier: float = 2.0):
+                 epsilon: float = 1.0, backward_multiplier: float = 2.0, seed: int = 0):
+        import random
         self.pl = placement
         self.fwd, self.bwd = fwd_seconds, fwd_seconds * backward_multiplier
+        self.rng = random.Random(seed)  # newcomer phases (uniform01, one per router, like sim.cpp:716)
         self.routers = []
         for _ in range(n_trainers):
             r = RoutingState(placement.n_stages, gamma, epsilon)
             for pid, (s, _p) in enumerate(placement.peers):
-                r.add_server(pid, {s}, 1.0)
+                if pid in placement.alive:
+                    r.add_server(pid, {s}, 1.0)
             self.routers.append(r)
+
+    def remove(self, pid: int) -> None:
+        for r in self.routers:
+            r.remove_server(pid)
+
+    def ban(self, pid: int) -> None:
+        for r in self.routers:
+            r.ban_server(pid)
+
+    def add(self, pid: int, stage: int) -> None:
+        for r in self.routers:
+            r.add_server(pid, {stage}, self.rng.random())
 
     def plan(self, n_microbatches: int) -> list[list[int]]:
         routes = []
@@ -136,6 +173,18 @@ class RoutePlanner:
                 r.record_response(route[s], self.bwd)
             routes.append(route)
         return routes
+
+
+def queue_proxy_table(pl: Placement, visits: list):
+    """Load table for Alg. 2 (rebalancer.cpp:25-69).  The reference publishes
+    time-averaged queue lengths; in this synchronous pipeline a peer's queue
+    proxy is the forward work it was routed beyond the least-loaded live peer
+    since the last rebalance (bottleneck peers accumulate it, idle ones do not)."""
+    from .routing import StageLoadTable
+    live = sorted(pl.alive)
+    base = min(visits[p] for p in live)
+    members = [{p: float(visits[p] - base) for p in pl.members(s)} for s in range(pl.n_stages)]
+    return StageLoadTable([sum(m.values()) for m in members], members)
 
 
 def visit_schedule(pl: Placement, routes: list[list[int]], rank: int) -> list[tuple[int, int]]:
@@ -168,33 +217,29 @@ def message_log(pl: Placement, routes: list[list[int]], rank: int):
 class SwarmPipeline:
     def __init__(self, mcfg: ModelConfig, n_stages: int = 4, *, n_microbatches: int = 16, n_trainers: int | None = None,
                  seed: int = 0, lr: float = 1e-4, weight_decay: float = 0.0, gamma: float = 0.1, epsilon: float = 1.0,
-                 modeled_flops: float = 1.0e15, profile: bool = False, use_graphs: bool = True):
+                 modeled_flops: float = 1.0e15, profile: bool = False, use_graphs: bool = True,
+                 layout: list | None = None, max_slots: int | None = None):
         self.m = mcfg
         self.S = n_stages
         self.M = n_microbatches
+        self.seed = seed
+        self.lr, self.weight_decay = lr, weight_decay
         self.world = dist.get_world_size() if dist.is_initialized() else 1
         self.rank = dist.get_rank() if dist.is_initialized() else 0
         self.device = torch.device("cuda", torch.cuda.current_device())
         S = self.S
-        self.pl = Placement(self.world, S)
+        self.pl = Placement(self.world, S, layout)
         self.P = self.pl.P
         self.per_rank = self.pl.per_rank
         self.local_stages = self.pl.local_stages(self.rank)
         self.all_local = len(self.local_stages) == S and self.P == 1  # sole peer of every stage
         self.n_trainers = n_trainers or self.P
-        # stage executors for the stages this rank serves
-        slots = 1 if self.all_local else (self.M if self.P == 1 else math.ceil(self.M / self.P) + 2)
-        self.max_slots = slots
-        self.stages: dict[int, Stage] = {}
-        for s in self.local_stages:
-            cfg = StageConfig(d_model=mcfg.d_model, n_heads=mcfg.n_heads, d_ffn=mcfg.d_ffn, seq_len=mcfg.seq_len,
-                              micro_batch=mcfg.micro_batch, n_layers=mcfg.layers_per_stage,
-                              shared_layers=mcfg.shared_layers, vocab=mcfg.vocab, is_first=int(s == 0),
-                              is_last=int(s == S - 1), causal=mcfg.causal, max_slots=slots, wire=mcfg.wire,
-                              block_size=mcfg.block_size, maxout_k=mcfg.maxout_k, lr=lr,
-                              weight_decay=weight_decay,
-                              seed=seed * 1000 + s)  # every replica of a stage starts identical
-            self.stages[s] = Stage(cfg, self.device)
+        # activation slots: a peer holds every microbatch routed to it in a step
+        if max_slots is None:
+            max_slots = 1 if self.all_local else (self.M if self.P == 1 or layout is not None
+                                                  else math.ceil(self.M / self.P) + 2)
+        self.max_slots = max_slots
+        self.stages: dict[int, Stage] = {s: self._new_stage(s) for s in self.local_stages}
         # CUDA graphs: a visit enqueues ~200 kernels; replaying a captured graph
         # removes the per-launch host cost.  With `profile`, the first visit of
         # each stage per step runs eagerly with GEMM events (live roofline).
@@ -206,29 +251,117 @@ class SwarmPipeline:
         self.replayed_kernels = 0
         self._warm: set = set()
         self._profiled: set = set()
-        self.wire_bytes = next(iter(self.stages.values())).wire_bytes
+        probe = next(iter(self.stages.values()), None) or self._new_stage(0, slots=1)
+        self.wire_bytes = probe.wire_bytes
         tokens = mcfg.tokens
         self.fwd_seconds = 2.0 * mcfg.params_per_layer() * tokens * mcfg.layers_per_stage / modeled_flops
-        self.planner = RoutePlanner(self.pl, self.n_trainers, self.fwd_seconds, gamma, epsilon)
-        # per-stage gradient all-reduce groups (every rank creates every group, same order)
-        self.stage_group = {}
-        if self.P > 1:
-            for s in range(S):
-                g = dist.new_group([s * self.P + p for p in range(self.P)])
-                if s in self.local_stages:
-                    self.stage_group[s] = g
+        self.planner = RoutePlanner(self.pl, self.n_trainers, self.fwd_seconds, gamma, epsilon, seed=seed)
+        self.stage_group: dict = {}
+        self._build_groups()
         # wire message pools (per microbatch) and the loss accumulator
         n_buf = 1 if self.all_local else self.M
         self.act = [torch.empty(self.wire_bytes, dtype=torch.uint8, device=self.device) for _ in range(n_buf)]
         self.grd = [torch.empty(self.wire_bytes, dtype=torch.uint8, device=self.device) for _ in range(n_buf)]
         self.loss_sum = torch.zeros(1, dtype=torch.float32, device=self.device)
         self.last_routes: list[list[int]] = []
+        self.visits = [0] * len(self.pl.stage_of)  # forward visits per peer since the last rebalance
+        self.events: list[dict] = []               # membership log (failures, migrations)
+
+    def _new_stage(self, s: int, slots: int | None = None) -> Stage:
+        m = self.m
+        cfg = StageConfig(d_model=m.d_model, n_heads=m.n_heads, d_ffn=m.d_ffn, seq_len=m.seq_len,
+                          micro_batch=m.micro_batch, n_layers=m.layers_per_stage, shared_layers=m.shared_layers,
+                          vocab=m.vocab, is_first=int(s == 0), is_last=int(s == self.S - 1), causal=m.causal,
+                          max_slots=slots or self.max_slots, wire=m.wire, block_size=m.block_size,
+                          maxout_k=m.maxout_k, lr=self.lr, weight_decay=self.weight_decay,
+                          seed=self.seed * 1000 + s)  # every replica of a stage starts identical
+        return Stage(cfg, self.device)
+
+    def _build_groups(self) -> None:
+        """Per-stage gradient all-reduce groups over the live members (collective:
+        every rank creates every group, in stage order)."""
+        self.stage_group = {}
+        if self.world < self.S or not dist.is_initialized():
+            return
+        for s in range(self.S):
+            members = self.pl.members(s)
+            if len(members) > 1:
+                g = dist.new_group(members)
+                if self.rank in members:
+                    self.stage_group[s] = g
+
+    # ------------------------------------------------------- membership events
+    def fail_peer(self, pid: int) -> None:
+        """A peer leaves (sim.cpp:583-625 kill_worker): every router forgets it,
+        its stage's all-reduce group shrinks, and the rank stops serving."""
+        torch.cuda.synchronize()
+        self.planner.remove(pid)
+        self.pl.alive.discard(pid)
+        if pid == self.rank:
+            self.local_stages = []
+            self.stages = {}
+            self.graphs = {}
+        self._build_groups()
+        self.events.append({"event": "peer_leave", "peer": pid})
+
+    def stage_loads(self):
+        return queue_proxy_table(self.pl, self.visits)
+
+    def rebalance(self):
+        """One rebalancing round: decide (host C++, decision-identical to the
+        reference) and migrate the mover with its state (weights + AdamW)."""
+        from .routing import decide
+        d = decide(self.stage_loads())
+        self.visits = [0] * len(self.visits)
+        if d.mover is not None:
+            self.migrate(d.mover, d.to_stage)
+        self.events.append({"event": "rebalance", "mover": d.mover, "from": d.from_stage, "to": d.to_stage})
+        return d
+
+    def migrate(self, pid: int, to_stage: int) -> None:
+        """begin_migration / on_migration_complete (sim.cpp:673-719) for real:
+        routers ban the mover, it rebuilds its stage executor for `to_stage`
+        and downloads params + AdamW moments + step from the lowest-id live
+        stage-mate (NCCL point-to-point), groups are rebuilt, routers re-add it."""
+        torch.cuda.synchronize()
+        if self.world < self.S:
+            raise RuntimeError("migration needs one peer per rank (world >= stages)")
+        self.planner.ban(pid)
+        old = self.pl.stage_of[pid]
+        donor = self.pl.members(to_stage)[0]
+        if self.rank == pid:
+            self.stages = {}
+            self.graphs = {k: g for k, g in self.graphs.items() if k[0] != old}
+            self._warm = {w for w in self._warm if w[0] != old}
+            st = self._new_stage(to_stage)
+            m, v, _ = st.optimizer_state()
+            step = torch.zeros(1, dtype=torch.int64, device=self.device)
+            for t in (st.params(), m, v, step):
+                dist.recv(t, donor)
+            st.set_step(int(step.item()))
+            st.sync_shadow()
+            self.stages = {to_stage: st}
+            self.local_stages = [to_stage]
+        elif self.rank == donor:
+            st = self.stages[to_stage]
+            m, v, step = st.optimizer_state()
+            for t in (st.params(), m, v, torch.tensor([step], dtype=torch.int64, device=self.device)):
+                dist.send(t, pid)
+        torch.cuda.synchronize()
+        self.pl.stage_of[pid] = to_stage
+        self._build_groups()
+        self.planner.add(pid, to_stage)
+        self.events.append({"event": "migration", "peer": pid, "from": old, "to": to_stage,
+                            "state_bytes": 12 * (self.stages[to_stage].n_params if to_stage in self.stages else 0)})
 
     def rank_of_peer(self, pid: int) -> int:
         return self.pl.rank_of_peer(pid)
 
     def plan(self) -> list[list[int]]:
         self.last_routes = self.planner.plan(self.M)
+        for route in self.last_routes:
+            for pid in route:
+                self.visits[pid] += 1
         return self.last_routes
 
     # ------------------------------------------------------------ execution
@@ -243,9 +376,11 @@ class SwarmPipeline:
         else:
             self._step_pipelined(routes, tokens, targets, scale)
         for s, st in self.stages.items():
-            if self.P > 1:
+            if s in self.stage_group:
                 dist.all_reduce(st.grads(), op=dist.ReduceOp.SUM, group=self.stage_group[s])
-            st.optimizer_step(grad_scale=1.0 / self.P)
+            # every peer holds the sum over ITS microbatches of d(loss/(M*T)); the SUM over
+            # the stage peers is the full-batch gradient, so no further scaling
+            st.optimizer_step(grad_scale=1.0)
 
     # ---------------------------------------------------------------- visits
     def _run(self, key, fn) -> None:

@@ -93,3 +93,43 @@ def test_replicated_routing_gloo():
     # world 2: rank 0 runs stages 0-1, rank 1 stages 2-3 of every microbatch
     assert out[0][1] == [(mb, s) for mb in range(8) for s in (0, 1)]
     assert out[1][1] == [(mb, s) for mb in range(8) for s in (2, 3)]
+
+
+def test_rebalance_moves_from_overprovisioned_stage():
+    """Layout (3,1,2,2): the queue proxy makes stage 1 the max-load stage and
+    Alg. 2 moves the lowest-id idle peer of stage 0 there; after the move the
+    layout is (2,2,2,2) and the decision is a no-op."""
+    from paper_2301_11913_b200.routing import decide
+    from paper_2301_11913_b200.swarm import Placement, RoutePlanner, queue_proxy_table
+    pl = Placement(8, 4, [3, 1, 2, 2])
+    planner = RoutePlanner(pl, 2, 0.25)
+    visits = [0] * 8
+    for route in planner.plan(24):
+        for p in route:
+            visits[p] += 1
+    assert visits == [8, 8, 8, 24, 12, 12, 12, 12]
+    d = decide(queue_proxy_table(pl, visits))
+    assert (d.mover, d.from_stage, d.to_stage) == (0, 0, 1)
+    # migration: routers ban then re-add the mover on its new stage
+    planner.ban(0)
+    pl.stage_of[0] = 1
+    planner.add(0, 1)
+    visits = [0] * 8
+    for route in planner.plan(24):
+        for p in route:
+            visits[p] += 1
+    assert all(v == 12 for v in visits)
+    d = decide(queue_proxy_table(pl, visits))
+    assert d.mover is None
+
+
+def test_peer_failure_reroutes():
+    from paper_2301_11913_b200.swarm import Placement, RoutePlanner
+    pl = Placement(8, 4)
+    planner = RoutePlanner(pl, 2, 0.25)
+    planner.remove(5)
+    pl.alive.discard(5)
+    routes = planner.plan(16)
+    assert all(5 not in r for r in routes)
+    assert sum(r[2] == 4 for r in routes) == 16  # stage 2 is down to peer 4
+    assert pl.local_stages(5) == [] and pl.members(2) == [4]
