@@ -446,6 +446,87 @@ def bench_train(args, world, rank, local):
     return line
 
 
+# ----------------------------------------------------------------- failure
+def bench_failure(args, world, rank, local):
+    """BASELINE configs[4]: peer failure + adaptive
+    rebalancing on a real multi-GPU pipeline.  Start imbalanced (one stage short
+    a peer, e.g. 3,1,2,2 on 8 GPUs or 3,1 on 4), rebalance (Alg. 2 moves a peer,
+    which downloads weights + AdamW state from a stage-mate), then remove a peer
+    mid-training and rebalance again.  Each phase's tokens/s is measured; the
+    CPU reference is the reference's own oracle_throughput (P/src/sim.cpp:88-116,
+    compiled in oracle/_ref) fed the measured per-peer stage rate."""
+    import ctypes as C
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_2301_11913_b200.swarm import PRESETS, SwarmPipeline, synthetic_batch
+    dev = torch.device("cuda", local)
+    torch.cuda.set_device(dev)
+    S = args.stages if args.stages != TRAIN_STAGES or world >= 8 else max(2, world // 2)
+    if world < 2 * S:
+        raise SystemExit("failure workload needs >= 2 peers per stage on average (world >= 2*stages)")
+    per = world // S
+    layout = [per + 1, per - 1] + [per] * (S - 2)  # stage 1 short one peer
+    mcfg = PRESETS[args.model]
+    M = args.microbatches
+    pipe = SwarmPipeline(mcfg, S, n_microbatches=M, seed=1, lr=1e-4, layout=layout, max_slots=M)
+    tok, tgt = synthetic_batch(mcfg, M, seed=7, device=dev)
+
+    def phase(name, steps):
+        pipe.step(tok, tgt)  # untimed: capture graphs after a membership change
+        torch.cuda.synchronize()
+        barrier(world)
+        t0 = torch.cuda.Event(enable_timing=True)
+        t1 = torch.cuda.Event(enable_timing=True)
+        t0.record()
+        for _ in range(steps):
+            pipe.step(tok, tgt)
+        t1.record()
+        torch.cuda.synchronize()
+        barrier(world)
+        ms = max_over_ranks(t0.elapsed_time(t1), world)
+        counts = [len(pipe.pl.members(s)) for s in range(S)]
+        return {"phase": name, "layout": counts, "tokens_per_s": pipe.tokens_per_step() * steps / (ms / 1e3),
+                "ms_per_step": ms / steps}
+
+    for _ in range(max(args.warmup - 1, 1)):
+        pipe.step(tok, tgt)
+    phases = [phase("A: imbalanced start", args.steps)]
+    d1 = pipe.rebalance()
+    phases.append(phase("B: after rebalance", args.steps))
+    victim = pipe.pl.members(S - 2)[-1]  # a peer of the second-to-last stage leaves mid-training
+    pipe.fail_peer(victim)
+    phases.append(phase(f"C: after peer {victim} left", args.steps))
+    d2 = pipe.rebalance()
+    phases.append(phase("D: after second rebalance", args.steps))
+    # CPU reference prediction: oracle_throughput with the per-peer rate measured in B
+    ref_pred = None
+    if rank == 0:
+        try:
+            import oracle as O
+            if O.ref is not None:
+                b = phases[1]
+                rate = b["tokens_per_s"] / min(b["layout"])  # per-peer rate of the balanced bottleneck stage
+                r = (C.c_double * S)(*([rate] * S))
+                ref_pred = {"kind": "reference sim::oracle_throughput (oracle/_ref)",
+                            "per_peer_rate_tokens_per_s": rate,
+                            "predicted_tokens_per_s": {p["phase"][0]: O.ref.ref_oracle_throughput(r, S, sum(p["layout"]))
+                                                       for p in phases},
+                            "layout_bound_tokens_per_s": {p["phase"][0]: rate * min(p["layout"]) for p in phases}}
+        except Exception as e:  # the prediction is a report, not part of the measured path
+            ref_pred = {"unavailable": str(e)}
+    dec = lambda d: {"mover": d.mover, "from_stage": d.from_stage, "to_stage": d.to_stage}
+    return {"metric": "training tokens/s per phase (peer failure + adaptive rebalancing)",
+            "value": phases[-1]["tokens_per_s"], "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": phases[-1]["ms_per_step"], "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+            "config": {"workload": "BASELINE configs[4]: failure + rebalancing", "model": args.model, "stages": S,
+                       "initial_layout": layout, "microbatches_per_step": M},
+            "phases": phases, "decisions": [dec(d1), dec(d2)], "membership_log": pipe.events,
+            "reference": ref_pred}
+
+
 def run_reference(args, world, rank):
     """--impl reference: the reference's CPU implementation of the path on this
     box's host cores (rank 0 only).  train: the block oracle port (the reference
@@ -483,7 +564,7 @@ def main():
     ap.add_argument("--steps", type=int, default=None)
     ap.add_argument("--warmup", type=int, default=None)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="train", choices=["train", "codec"])
+    ap.add_argument("--workload", default="train", choices=["train", "codec", "failure"])
     ap.add_argument("--model", default="C", choices=["C", "D", "tiny"])
     ap.add_argument("--microbatches", type=int, default=TRAIN_MICROBATCHES)
     ap.add_argument("--stages", type=int, default=TRAIN_STAGES, help="pipeline stages (default 4, SURVEY §8(d))")
@@ -491,15 +572,17 @@ def main():
     ap.add_argument("--no-codec", action="store_true", help="train: skip the codec sub-measurement")
     args = ap.parse_args()
     if args.steps is None:
-        args.steps = 6 if args.workload == "train" else 1000
+        args.steps = {"train": 6, "failure": 3}.get(args.workload, 1000)
     if args.warmup is None:
-        args.warmup = 3 if args.workload == "train" else 10
+        args.warmup = {"train": 3, "failure": 3}.get(args.workload, 10)
     args.warmup = max(args.warmup, 3)
     world, rank, local = dist_setup(args)
     if args.impl == "reference":
         line = run_reference(args, world, rank)
     elif args.workload == "codec":
         line = bench_codec(args, world, rank, local)
+    elif args.workload == "failure":
+        line = bench_failure(args, world, rank, local)
     else:
         line = bench_train(args, world, rank, local)
         if not args.no_codec:
