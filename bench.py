@@ -411,6 +411,12 @@ def bench_train(args, world, rank, local):
     visits_per_stage = (M // pipe.P) if not pipe.all_local else M
     gemm_share = (gemm_ms / args.steps) * visits_per_stage / (t0.elapsed_time(t1) / args.steps) \
         if gemm_ms > 0 else None
+    # per-category kernel time of the profiled visits, scaled to every visit of a step
+    step_ms_rank = t0.elapsed_time(t1) / args.steps
+    breakdown = {cat: {"ms_per_step": cms / args.steps * visits_per_stage,
+                       "share_of_step": cms / args.steps * visits_per_stage / step_ms_rank,
+                       "calls_per_step": int(cn / args.steps * visits_per_stage)}
+                 for cat, (cms, cn) in getattr(pipe, "last_breakdown", {}).items()}
     model_tflops = value * mcfg.flops_per_token(S) / 1e12
     placement = (f"{S} stages x {pipe.P} peer(s) per stage" if world >= S else
                  f"{world} GPU(s) x {S // world} stage(s) each")
@@ -435,6 +441,10 @@ def bench_train(args, world, rank, local):
                      "note": "GEMM events bracket every GEMM of the first visit of each (stage, direction) per step "
                              "(run eagerly); the other visits replay CUDA graphs of the same kernels",
                      "gemm_launches": gemm_n, "gemm_flops": gemm_flops, "gemm_ms": gemm_ms},
+        "step_breakdown": {"note": "kernel time per category on this rank (profiled eager visits, side stream "
+                                   "folded onto the visit stream), scaled to all visits of a step; the remainder "
+                                   "of the step is optimizer, all-reduce, transport and idle time",
+                           **breakdown},
         "e2e": {"value": e2e_val, "unit": "tokens/s", "h2d_bytes_per_step": int(tok.numel() * 8),
                 "d2h_bytes_per_step": 4, "path": "SwarmPipeline.step with tokens/targets copied from pinned host "
                                                  "memory and the loss read back every step"},

@@ -141,8 +141,25 @@ typedef struct {
     const void* aux; /* R (RESIDUAL) or U (DGELU): bf16, same layout as D; U output for GELU */
     float alpha;
     int epilogue;
+    /* causal structure of A per batch entry (M == K): 0 dense; 1 A[i][j] == 0 for
+       j > i (P, dS: k-blocks past the tile's last row are skipped); 2 A[i][j] == 0
+       for j < i (P^T, dS^T: k-blocks before the tile's first row are skipped) */
+    int k_tri;
+    /* optional stream-K scratch (NULL = whole tiles only): at least
+       swarm_gemm_workspace_bytes(), zero-filled once before its first use (the
+       kernel leaves it zeroed again); never shared by GEMMs that can run
+       concurrently.  With it, the last partial wave of 256x256 tiles is split
+       along K across every SM pair (results identical up to fp32 summation
+       order).  Measured slower than whole tiles for the block shapes on B200,
+       so the stage executor passes one only under SWARM_GEMM_STREAMK=1. */
+    void* workspace;
+    size_t workspace_bytes;
 } swarm_gemm_args;
 int swarm_gemm_bf16(const swarm_gemm_args* args, swarm_stream_t stream);
+size_t swarm_gemm_workspace_bytes(void);
+/* resident 2-CTA clusters of the 256x256 pair kernel on the current device (its
+   persistent grid size; below SMs / 2 when GPCs strand SMs) */
+int swarm_gemm_pair_clusters(void);
 
 /* ---- training building blocks (stage executor internals, exported for tests)
  * None of these has a reference counterpart: the reference only models the
@@ -260,12 +277,22 @@ int swarm_stage_sync_shadow(swarm_stage_t st, swarm_stream_t stream);
 /* enumerate parameter tensors: index -> name, offset (elements), rows, cols */
 int swarm_stage_param_info(swarm_stage_t st, int index, const char** name, size_t* offset, size_t* rows,
                            size_t* cols);
-/* GEMM profiling for the live roofline: while enabled, every GEMM of this
- * stage's visits is bracketed by CUDA events on the visit's stream;
- * profile_read synchronises, returns the summed GEMM time (ms), algorithmic
- * FLOPs (2*M*N*K*batch) and launch count recorded since the last read, and resets. */
+/* Visit profiling for the live roofline: while enabled, every kernel call of
+ * this stage's visits is bracketed by CUDA events on the visit's stream (the
+ * weight-gradient side stream is folded onto it);
+ * profile_read synchronises, returns the summed GEMM time (ms), executed
+ * FLOPs (2*M*N*K*batch, less the k-blocks a causal k_tri skips) and launch
+ * count recorded since the last read, and resets.  profile_breakdown returns
+ * the per-category time / call counts of that last read. */
+#define SWARM_PROF_GEMM 0
+#define SWARM_PROF_ATTENTION 1  /* fused score/softmax kernels (their GEMMs count as GEMM) */
+#define SWARM_PROF_LAYERNORM 2
+#define SWARM_PROF_OTHER 3      /* embedding, codec / wire, maxout, cross-entropy */
+#define SWARM_PROF_CATEGORIES 4
 void swarm_stage_profile(swarm_stage_t st, int enable);
 int swarm_stage_profile_read(swarm_stage_t st, double* gemm_ms, double* gemm_flops, uint64_t* gemm_launches);
+void swarm_stage_profile_breakdown(swarm_stage_t st, double* ms /* [SWARM_PROF_CATEGORIES] */,
+                                   uint64_t* launches /* [SWARM_PROF_CATEGORIES] */);
 /* saved activation of (slot, layer) by name ("x","a","qkv","P","o","h","c","u","g","xf","dxf"), for tests */
 int swarm_stage_activation(swarm_stage_t st, int slot, int layer, const char* name, void** ptr, size_t* numel);
 

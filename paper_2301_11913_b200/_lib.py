@@ -25,7 +25,8 @@ class GemmArgs(C.Structure):
         ("b", C.c_void_p), ("ldb", C.c_int), ("b_mn_major", C.c_int), ("b_rows", C.c_int), ("b_cols", C.c_int),
         ("rb0", C.c_int), ("rb1", C.c_int), ("cb0", C.c_int), ("cb1", C.c_int),
         ("d", C.c_void_p), ("ldd", C.c_int), ("rd0", C.c_int), ("rd1", C.c_int), ("cd0", C.c_int), ("cd1", C.c_int),
-        ("aux", C.c_void_p), ("alpha", C.c_float), ("epilogue", C.c_int)]
+        ("aux", C.c_void_p), ("alpha", C.c_float), ("epilogue", C.c_int), ("k_tri", C.c_int),
+        ("workspace", C.c_void_p), ("workspace_bytes", C.c_size_t)]
 
 
 class StageConfigC(C.Structure):
@@ -53,6 +54,8 @@ SIGNATURES = {
     "swarm_layer_norm_backward": (I, [P, P, I, SZ, SZ, P, P, P, P, P, P, P, I, P, P]),
     "swarm_matvec_f64": (I, [P, SZ, P, SZ, P, P]),
     "swarm_gemm_bf16": (I, [C.POINTER(GemmArgs), P]),
+    "swarm_gemm_workspace_bytes": (SZ, []),
+    "swarm_gemm_pair_clusters": (I, []),
     "swarm_embedding_forward": (I, [P, SZ, P, SZ, SZ, P, P]),
     "swarm_embedding_backward": (I, [P, SZ, P, SZ, SZ, P, P]),
     "swarm_attn_softmax_forward": (I, [P, SZ, SZ, I, P, P]),
@@ -81,6 +84,7 @@ SIGNATURES = {
     "swarm_stage_set_step": (I, [P, I]),
     "swarm_wire_parse_header": (I, [P, C.POINTER(C.c_uint32), C.POINTER(C.c_uint32), C.POINTER(I), C.POINTER(I)]),
     "swarm_stage_profile_read": (I, [P, C.POINTER(D), C.POINTER(D), C.POINTER(C.c_uint64)]),
+    "swarm_stage_profile_breakdown": (None, [P, P, P]),
     "swarm_router_last_error": (C.c_char_p, []),
     "swarm_router_create": (I, [SZ, D, D, C.POINTER(P)]),
     "swarm_router_destroy": (None, [P]),

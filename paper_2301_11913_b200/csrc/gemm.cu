@@ -50,8 +50,16 @@ struct Params {
     int epi;
     int vec_ok;
     int tma_epi;  // stage output chunks in smem and write them with TMA (store / reduce-add)
-    int ksplit, kb_per_split;  // split-K units per tile (pair kernel, fp32 reduce-add epilogue only)
-    int dbg;      // SWARM_GEMM_DBG (experiments only): 1 skip output stores, 2 skip MMAs, 4 skip TMA loads
+    // stream-K (pair kernel): tiles [0, dp_tiles) are whole-tile units dealt
+    // round-robin to the clusters; the sk_tiles after them are cut into
+    // sk_tiles * k_blocks k-block iterations split evenly over the clusters
+    int dp_tiles, sk_tiles, sk_iters;
+    float* ws;      // per-cluster partial accumulators: [cluster][first|last][half][128][256] fp32
+    int* sk_cnt;    // [sk_tile][half][warp] arrival counters (self-resetting)
+    int* sk_ready;  // [cluster][first|last][half][warp] partial-ready flags (self-resetting)
+    int k_tri;    // swarm_gemm_args.k_tri (1-CTA kernel): skip all-zero k-blocks of a triangular A
+    int dbg;      // SWARM_GEMM_DBG (experiments only): 1 skip output stores, 2 skip MMAs, 4 skip TMA loads,
+                  // 8 stream-K units store directly (no fixup), 16 fixup without waiting for partials
 };
 
 template <int BN>
@@ -103,7 +111,9 @@ __device__ __forceinline__ void epilogue_chunk(const Params& p, float (&v)[32], 
                         }
                     }
                 } else {
-                    for (int j = 0; j < ncols_valid; ++j) v[j] += __bfloat162float(r[j]);
+#pragma unroll
+                    for (int j = 0; j < 32; ++j)
+                        if (j < ncols_valid) v[j] += __bfloat162float(r[j]);
                 }
             }
             if (full) {
@@ -113,7 +123,9 @@ __device__ __forceinline__ void epilogue_chunk(const Params& p, float (&v)[32], 
                         make_uint4(pack_bf16(v[q * 8 + 0], v[q * 8 + 1]), pack_bf16(v[q * 8 + 2], v[q * 8 + 3]),
                                    pack_bf16(v[q * 8 + 4], v[q * 8 + 5]), pack_bf16(v[q * 8 + 6], v[q * 8 + 7]));
             } else {
-                for (int j = 0; j < ncols_valid; ++j) dst[j] = __float2bfloat16_rn(v[j]);
+#pragma unroll
+                for (int j = 0; j < 32; ++j)
+                    if (j < ncols_valid) dst[j] = __float2bfloat16_rn(v[j]);
             }
             break;
         }
@@ -134,8 +146,9 @@ __device__ __forceinline__ void epilogue_chunk(const Params& p, float (&v)[32], 
                     reinterpret_cast<float4*>(dst)[q] = o;
                 }
             } else {
-                for (int j = 0; j < ncols_valid; ++j)
-                    dst[j] = (p.epi == SWARM_EPI_ACCUM_F32) ? dst[j] + v[j] : v[j];
+#pragma unroll
+                for (int j = 0; j < 32; ++j)
+                    if (j < ncols_valid) dst[j] = (p.epi == SWARM_EPI_ACCUM_F32) ? dst[j] + v[j] : v[j];
             }
             break;
         }
@@ -157,7 +170,9 @@ __device__ __forceinline__ void epilogue_chunk(const Params& p, float (&v)[32], 
                         make_uint4(pack_bf16(v[q * 8 + 0], v[q * 8 + 1]), pack_bf16(v[q * 8 + 2], v[q * 8 + 3]),
                                    pack_bf16(v[q * 8 + 4], v[q * 8 + 5]), pack_bf16(v[q * 8 + 6], v[q * 8 + 7]));
             } else {
-                for (int j = 0; j < ncols_valid; ++j) {
+#pragma unroll
+                for (int j = 0; j < 32; ++j) {
+                    if (j >= ncols_valid) continue;
                     u[j] = __float2bfloat16_rn(v[j]);
                     dst[j] = __float2bfloat16_rn(gelu_f(v[j]));
                 }
@@ -184,8 +199,9 @@ __device__ __forceinline__ void epilogue_chunk(const Params& p, float (&v)[32], 
                         make_uint4(pack_bf16(v[q * 8 + 0], v[q * 8 + 1]), pack_bf16(v[q * 8 + 2], v[q * 8 + 3]),
                                    pack_bf16(v[q * 8 + 4], v[q * 8 + 5]), pack_bf16(v[q * 8 + 6], v[q * 8 + 7]));
             } else {
-                for (int j = 0; j < ncols_valid; ++j)
-                    dst[j] = __float2bfloat16_rn(v[j] * dgelu_f(__bfloat162float(u[j])));
+#pragma unroll
+                for (int j = 0; j < 32; ++j)
+                    if (j < ncols_valid) dst[j] = __float2bfloat16_rn(v[j] * dgelu_f(__bfloat162float(u[j])));
             }
             break;
         }
@@ -214,10 +230,20 @@ __device__ __forceinline__ void stage_bf16(uint8_t* slot, int row, const float (
 }
 
 // Drain this warp's 32 rows x BN_TILE columns of one accumulator tile.
+// Stream-K fixup: `fix_slots` packs (8 bits each) the workspace slots holding
+// the other clusters' partial sums of this tile; `fix_row` is this warp's
+// 32-row block inside a slot.  A block is stored as [chunk c][float4 j][lane]
+// so that each warp access is 512 contiguous bytes (row-per-thread addressing
+// would scatter every store over 32 rows).
+__device__ __forceinline__ const float4* sk_part(const Params& p, uint64_t slots, int f, size_t row_off) {
+    const int sl = static_cast<int>((slots >> (8 * f)) & 0xff);
+    return reinterpret_cast<const float4*>(p.ws + static_cast<size_t>(sl) * 2 * 128 * 256 + row_off);
+}
 template <int BN_TILE>
 __device__ __forceinline__ void drain_tile(const Params& p, const CUtensorMap* md, const CUtensorMap* mu,
                                            uint8_t* stg, int& slot_idx, uint32_t taddr, int row_base, long long rd,
-                                           long long cd, int col_tile0, int lane) {
+                                           long long cd, int col_tile0, int lane, uint64_t fix_slots = 0,
+                                           int nfix = 0, size_t fix_row = 0) {
     const int row = row_base + lane;
 #pragma unroll 1
     for (int c = 0; c < BN_TILE / 32; ++c) {
@@ -228,7 +254,20 @@ __device__ __forceinline__ void drain_tile(const Params& p, const CUtensorMap* m
         if (col0 >= p.n) continue;  // warp-uniform
         float v[32];
 #pragma unroll
-        for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(rr[j]) * p.alpha;
+        for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(rr[j]);
+        for (int f = 0; f < nfix; ++f) {
+            const float4* src = sk_part(p, fix_slots, f, fix_row) + c * 256 + lane;
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                const float4 w = __ldcg(src + j * 32);
+                v[4 * j] += w.x;
+                v[4 * j + 1] += w.y;
+                v[4 * j + 2] += w.z;
+                v[4 * j + 3] += w.w;
+            }
+        }
+#pragma unroll
+        for (int j = 0; j < 32; ++j) v[j] *= p.alpha;
         const long long off = (rd + row) * p.ldd + cd + col0;
         if (!p.tma_epi) {
             if (row < p.m) epilogue_chunk(p, v, off, min(32, p.n - col0));
@@ -298,6 +337,14 @@ __device__ __forceinline__ void drain_tile(const Params& p, const CUtensorMap* m
     }
 }
 
+// k-block range of m-tile mt (all of K unless A is triangular, see k_tri)
+__device__ __forceinline__ void k_range(const Params& p, int mt, int& kb0, int& kb1) {
+    kb0 = 0;
+    kb1 = p.k_blocks;
+    if (p.k_tri == 1) kb1 = min(p.k_blocks, ((mt + 1) * BM + BK - 1) / BK);
+    else if (p.k_tri == 2) kb0 = (mt * BM) / BK;
+}
+
 template <int BN, bool A_MN, bool B_MN>
 __global__ void __launch_bounds__(kThreads, 1)
     k_gemm(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUtensorMap tma_b,
@@ -352,7 +399,9 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const int zb = z / p.bh, zh = z - zb * p.bh;
                 const int ra = p.ra0 * zb + p.ra1 * zh, ca = p.ca0 * zb + p.ca1 * zh;
                 const int rb = p.rb0 * zb + p.rb1 * zh, cb = p.cb0 * zb + p.cb1 * zh;
-                for (int kb = 0; kb < p.k_blocks; ++kb) {
+                int kb0, kb1;
+                k_range(p, mt, kb0, kb1);
+                for (int kb = kb0; kb < kb1; ++kb) {
                     mbar_wait(&empty[stage], phase ^ 1);
                     mbar_arrive_expect_tx(&full[stage], C::A_BYTES + C::B_BYTES);
                     uint8_t* a_dst = sa + stage * C::A_BYTES;
@@ -389,10 +438,13 @@ __global__ void __launch_bounds__(kThreads, 1)
             int acc = 0;
             uint32_t acc_phase = 0;
             for (int t = blockIdx.x; t < p.total_tiles; t += gridDim.x) {
+                const int r = t % p.tiles_per_batch;
+                int kb0, kb1;
+                k_range(p, r % p.tiles_m, kb0, kb1);
                 mbar_wait(&tempty[acc], acc_phase ^ 1);
                 tc_fence_after();
                 const uint32_t d_tmem = tmem_base + static_cast<uint32_t>(acc * BN);
-                for (int kb = 0; kb < p.k_blocks; ++kb) {
+                for (int kb = kb0; kb < kb1; ++kb) {
                     mbar_wait(&full[stage], phase);
                     tc_fence_after();
                     const uint32_t a_base = smem_u32(sa + stage * C::A_BYTES);
@@ -403,7 +455,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                                                  : make_sdesc(a_base + k * 32, 16, 1024);
                         const uint64_t bd = B_MN ? make_sdesc(b_base + k * 2048, 64 * BK * 2, 1024)
                                                  : make_sdesc(b_base + k * 32, 16, 1024);
-                        mma_bf16(d_tmem, ad, bd, idesc, (kb | k) != 0 ? 1u : 0u);
+                        mma_bf16(d_tmem, ad, bd, idesc, (kb != kb0 || k != 0) ? 1u : 0u);
                     }
                     mma_commit(&empty[stage]);
                     if (++stage == C::STAGES) {
@@ -459,6 +511,48 @@ __global__ void __launch_bounds__(kThreads, 1)
 // barrier; commits multicast to both CTAs' empty / tmem-full barriers; both
 // CTAs' epilogue warps release the accumulator on the leader's tmem-empty.
 constexpr int PAIR_BN = 256;
+constexpr int kMaxSkParts = 8;  // host keeps every stream-K tile within this many clusters
+
+// One work unit of a cluster: k-blocks [kb0, kb1) of `tile`.  Whole tiles come
+// first (data-parallel waves), then this cluster's contiguous stream-K range.
+struct Unit {
+    int tile, kb0, kb1;
+    int sk;     // stream-K tile index (tile - dp_tiles), -1 for a data-parallel tile
+    int first;  // 1 when the unit opens this cluster's stream-K range
+};
+__device__ __forceinline__ int sk_bound(const Params& p, int c, int n_clusters) {
+    return static_cast<int>(static_cast<long long>(c) * p.sk_iters / n_clusters);
+}
+struct UnitIter {
+    int c, nc, t, i, e, b;
+    __device__ UnitIter(const Params& p, int cluster, int n_clusters)
+        : c(cluster), nc(n_clusters), t(cluster), i(sk_bound(p, cluster, n_clusters)),
+          e(sk_bound(p, cluster + 1, n_clusters)), b(i) {}
+    __device__ bool next(const Params& p, Unit& u) {
+        if (t < p.dp_tiles) {
+            u = Unit{t, 0, p.k_blocks, -1, 0};
+            t += nc;
+            return true;
+        }
+        if (i >= e) return false;
+        const int st = i / p.k_blocks, k0 = i - st * p.k_blocks;
+        const int k1 = min(p.k_blocks, k0 + (e - i));
+        u = Unit{p.dp_tiles + st, k0, k1, st, i == b ? 1 : 0};
+        i += k1 - k0;
+        return true;
+    }
+};
+// Partial-sum slot of the segment of stream-K tile `st` computed by cluster cc:
+// a cluster owns at most one segment that opens its range (slot 0) and one that
+// closes it mid-tile (slot 1).  Returns -1 when cc has no segment of st.
+__device__ __forceinline__ int sk_slot(const Params& p, int st, int cc, int n_clusters) {
+    const int lo = st * p.k_blocks, hi = lo + p.k_blocks;
+    const int b0 = sk_bound(p, cc, n_clusters), b1 = sk_bound(p, cc + 1, n_clusters);
+    const int s0 = max(b0, lo), s1 = min(b1, hi);
+    if (s0 >= s1) return -1;
+    return cc * 2 + (s0 == b0 ? 0 : 1);
+}
+
 struct Cfg2 {
     static constexpr int A_BYTES = 128 * BK * 2;  // this CTA's half of A
     static constexpr int B_BYTES = 128 * BK * 2;  // this CTA's half of B
@@ -525,18 +619,18 @@ __global__ void __launch_bounds__(kThreads, 1)
             // ------------------------------------------------ TMA producer (both CTAs)
             int stage = 0;
             uint32_t phase = 0;
-            for (int t = cluster; t < p.total_tiles; t += n_clusters) {
-                const int tt = t / p.ksplit, split = t - tt * p.ksplit;  // split-K unit
-                const int z = tt / p.tiles_per_batch;
-                const int r = tt - z * p.tiles_per_batch;
+            UnitIter it(p, cluster, n_clusters);
+            Unit u;
+            while (it.next(p, u)) {
+                const int z = u.tile / p.tiles_per_batch;
+                const int r = u.tile - z * p.tiles_per_batch;
                 const int mt = r % p.tiles_m, nt = r / p.tiles_m;
                 const int zb = z / p.bh, zh = z - zb * p.bh;
                 const int ra = p.ra0 * zb + p.ra1 * zh, ca = p.ca0 * zb + p.ca1 * zh;
                 const int rb = p.rb0 * zb + p.rb1 * zh, cb = p.cb0 * zb + p.cb1 * zh;
                 const int m0 = mt * 256 + half * 128;
                 const int n0 = (nt * NPAIR + pair) * PAIR_BN + half * 128;
-                const int kb0 = split * p.kb_per_split, kb1 = min(p.k_blocks, kb0 + p.kb_per_split);
-                for (int kb = kb0; kb < kb1; ++kb) {
+                for (int kb = u.kb0; kb < u.kb1; ++kb) {
                     mbar_wait(&empty[stage], phase ^ 1);
                     if (p.dbg & 4) {  // experiment: no operand traffic
                         if (leader) mbar_arrive(&full[stage]);
@@ -592,9 +686,10 @@ __global__ void __launch_bounds__(kThreads, 1)
             uint32_t phase = 0;
             int acc = 0;
             uint32_t acc_phase = 0;
-            for (int t = cluster; t < p.total_tiles; t += n_clusters) {
-                const int split = t % p.ksplit;
-                const int kb0 = split * p.kb_per_split, kb1 = min(p.k_blocks, kb0 + p.kb_per_split);
+            UnitIter it(p, cluster, n_clusters);
+            Unit u;
+            while (it.next(p, u)) {
+                const int kb0 = u.kb0, kb1 = u.kb1;
                 mbar_wait(&tempty[acc], acc_phase ^ 1);
                 tc_fence_after();
                 const uint32_t d_tmem = tmem_base + static_cast<uint32_t>(acc * PAIR_BN);
@@ -630,19 +725,76 @@ __global__ void __launch_bounds__(kThreads, 1)
         int slot_idx = 0;
         int acc = 0;
         uint32_t acc_phase = 0;
-        for (int t = cluster; t < p.total_tiles; t += n_clusters) {
-            const int tt = t / p.ksplit;
-            const int z = tt / p.tiles_per_batch;
-            const int r = tt - z * p.tiles_per_batch;
+        UnitIter it(p, cluster, n_clusters);
+        Unit u;
+        while (it.next(p, u)) {
+            const int z = u.tile / p.tiles_per_batch;
+            const int r = u.tile - z * p.tiles_per_batch;
             const int mt = r % p.tiles_m, nt = r / p.tiles_m;
             const int zb = z / p.bh, zh = z - zb * p.bh;
             const long long rd = p.rd0 * zb + p.rd1 * zh, cd = p.cd0 * zb + p.cd1 * zh;
             mbar_wait(&tfull[acc], acc_phase);
             tc_fence_after();
-            drain_tile<PAIR_BN>(p, &tma_d, &tma_u, stg, slot_idx,
-                                tmem_base + (static_cast<uint32_t>(q * 32) << 16) +
-                                    static_cast<uint32_t>(acc * PAIR_BN),
-                                mt * 256 + half * 128 + q * 32, rd, cd, (nt * NPAIR + pair) * PAIR_BN, lane);
+            const uint32_t taddr =
+                tmem_base + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(acc * PAIR_BN);
+            uint64_t fix_slots = 0;  // other contributors' slots, 8 bits each
+            int nfix = 0;
+            const size_t fix_row = static_cast<size_t>(half * 128 + q * 32) * PAIR_BN;
+            bool drain = true;
+            if (u.sk >= 0 && (u.kb0 != 0 || u.kb1 != p.k_blocks) && !(p.dbg & 8)) {
+                // stream-K partial tile: the last of its clusters to arrive (per warp
+                // quarter) sums everyone's partials and runs the epilogue; the others
+                // park their fp32 partial in the workspace.  Nobody waits on a
+                // cluster that has not arrived, so co-residency is never assumed.
+                const int wq = half * 4 + q;
+                int* cnt = p.sk_cnt + u.sk * 8 + wq;
+                int order = 0;
+                if (lane == 0) order = atomicAdd(cnt, 1);
+                order = __shfl_sync(0xffffffffu, order, 0);
+                const int lo = u.sk * p.k_blocks;
+                int c_lo = static_cast<int>(static_cast<long long>(lo) * n_clusters / p.sk_iters);
+                while (c_lo > 0 && sk_bound(p, c_lo, n_clusters) > lo) --c_lo;
+                int parts = 0, my_slot = cluster * 2 + (u.first ? 0 : 1);
+                for (int cc = c_lo; cc < n_clusters && sk_bound(p, cc, n_clusters) < lo + p.k_blocks; ++cc) {
+                    const int sl = sk_slot(p, u.sk, cc, n_clusters);
+                    if (sl < 0) continue;
+                    ++parts;
+                    if (sl != my_slot && nfix < kMaxSkParts) fix_slots |= static_cast<uint64_t>(sl) << (8 * nfix++);
+                }
+                if (order < parts - 1) {
+                    float* dst = p.ws + static_cast<size_t>(my_slot) * 2 * 128 * PAIR_BN + fix_row;
+#pragma unroll 1
+                    for (int c = 0; c < PAIR_BN / 32; ++c) {
+                        uint32_t rr[32];
+                        tmem_ld_32x32b_x32(taddr + static_cast<uint32_t>(c * 32), rr);
+                        tmem_ld_wait();
+                        float4* d4 = reinterpret_cast<float4*>(dst) + c * 256 + lane;
+#pragma unroll
+                        for (int j = 0; j < 8; ++j)
+                            __stcg(d4 + j * 32, make_float4(__uint_as_float(rr[4 * j]), __uint_as_float(rr[4 * j + 1]),
+                                                       __uint_as_float(rr[4 * j + 2]), __uint_as_float(rr[4 * j + 3])));
+                    }
+                    __threadfence();
+                    __syncwarp();
+                    if (lane == 0) st_release_gpu(p.sk_ready + my_slot * 8 + wq, 1);
+                    drain = false;
+                    nfix = 0;
+                } else {
+                    if (lane == 0) *cnt = 0;  // every contributor has arrived: reset for the next launch
+                    for (int f = 0; f < nfix; ++f) {
+                        const int sl = static_cast<int>((fix_slots >> (8 * f)) & 0xff);
+                        while (!(p.dbg & 16) && ld_acquire_gpu(p.sk_ready + sl * 8 + wq) == 0) {
+                        }
+                    }
+                }
+            }
+            if (drain)
+                drain_tile<PAIR_BN>(p, &tma_d, &tma_u, stg, slot_idx, taddr, mt * 256 + half * 128 + q * 32, rd, cd,
+                                    (nt * NPAIR + pair) * PAIR_BN, lane, fix_slots, nfix, fix_row);
+            __syncwarp();
+            if (lane == 0)
+                for (int f = 0; f < nfix; ++f)
+                    p.sk_ready[static_cast<int>((fix_slots >> (8 * f)) & 0xff) * 8 + half * 4 + q] = 0;
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive_cluster(tempty_leader[acc]);
@@ -753,14 +905,18 @@ int encode_2d_out(CUtensorMap* m, const void* ptr, long long rows, long long col
     return r == CUDA_SUCCESS ? SWARM_OK : SWARM_E_INVALID;
 }
 
-// Split-K for reduce-add GEMMs is opt-in (SWARM_GEMM_KSPLIT=1): measured slower —
-// the extra partial-tile reduce-add traffic costs more than the wave tail it removes.
-bool ksplit_enabled() {
-    static const bool on = [] {
-        const char* e = getenv("SWARM_GEMM_KSPLIT");
-        return e && e[0] == '1';
-    }();
-    return on;
+// Stream-K runs only when the caller passes a workspace (the stage executor
+// does so under SWARM_GEMM_STREAMK=1).  Measured on B200 it does not pay for
+// the block shapes: the data-parallel tail wave runs faster than a full wave
+// (fewer clusters share L2 bandwidth), so there is little quantization loss to
+// recover, and the fixup adds traffic (profiles/r01_gemm_experiments.md).
+// Stream-K scratch layout (caller-owned, see swarm_gemm_args.workspace):
+// [arrival counters | ready flags | partial accumulators].
+constexpr int kMaxClusters = 128;
+constexpr size_t kSkFlagBytes = 65536;
+static_assert(kMaxClusters * 8 * 3 * sizeof(int) <= kSkFlagBytes, "flag area");
+size_t sk_bytes(int clusters) {
+    return kSkFlagBytes + static_cast<size_t>(clusters) * 2 * 2 * 128 * PAIR_BN * sizeof(float);
 }
 
 bool tma_epi_enabled() {
@@ -799,7 +955,7 @@ int launch(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& td, 
 
 template <bool A_MN, bool B_MN, int NPAIR>
 int launch_pair(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& td, const CUtensorMap& tu,
-                const Params& p, cudaStream_t st) {
+                const Params& p, int clusters, cudaStream_t st) {
     auto kern = k_gemm2<A_MN, B_MN, NPAIR>;
     static bool attr = false;
     if (!attr) {
@@ -807,7 +963,7 @@ int launch_pair(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap&
         attr = true;
     }
     cudaLaunchConfig_t cfg{};
-    cfg.gridDim = dim3(2 * NPAIR * std::min(p.total_tiles, num_sms() / (2 * NPAIR)));
+    cfg.gridDim = dim3(2 * NPAIR * clusters);
     cfg.blockDim = dim3(kThreads);
     cfg.dynamicSmemBytes = Cfg2::SMEM;
     cfg.stream = st;
@@ -823,13 +979,46 @@ int launch_pair(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap&
     return SWARM_OK;
 }
 
+// How many 2-CTA clusters of the pair kernel can be resident at once.  On B200
+// this is below num_sms / 2 (GPCs with an odd number of usable SMs strand one
+// SM each), and a persistent grid larger than it runs its extra clusters as a
+// second wave — doubling a stream-K launch, whose clusters all get equal work.
+int max_pair_clusters() {
+    static const int n = [] {
+        const int cap = num_sms() / 2;
+        auto kern = k_gemm2<false, false, 1>;
+        if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg2::SMEM) != cudaSuccess) {
+            cudaGetLastError();
+            return cap;
+        }
+        cudaLaunchConfig_t cfg{};
+        cfg.gridDim = dim3(2 * cap);
+        cfg.blockDim = dim3(kThreads);
+        cfg.dynamicSmemBytes = Cfg2::SMEM;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = 2;
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        int c = 0;
+        if (cudaOccupancyMaxActiveClusters(&c, kern, &cfg) != cudaSuccess || c <= 0) {
+            cudaGetLastError();
+            return cap;
+        }
+        return std::min(c, cap);
+    }();
+    return n;
+}
+
 template <int NPAIR>
 int dispatch_pair(bool amn, bool bmn, const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& td,
-                  const CUtensorMap& tu, const Params& p, cudaStream_t st) {
-    if (!amn && !bmn) return launch_pair<false, false, NPAIR>(ta, tb, td, tu, p, st);
-    if (!amn && bmn) return launch_pair<false, true, NPAIR>(ta, tb, td, tu, p, st);
-    if (amn && !bmn) return launch_pair<true, false, NPAIR>(ta, tb, td, tu, p, st);
-    return launch_pair<true, true, NPAIR>(ta, tb, td, tu, p, st);
+                  const CUtensorMap& tu, const Params& p, int clusters, cudaStream_t st) {
+    if (!amn && !bmn) return launch_pair<false, false, NPAIR>(ta, tb, td, tu, p, clusters, st);
+    if (!amn && bmn) return launch_pair<false, true, NPAIR>(ta, tb, td, tu, p, clusters, st);
+    if (amn && !bmn) return launch_pair<true, false, NPAIR>(ta, tb, td, tu, p, clusters, st);
+    return launch_pair<true, true, NPAIR>(ta, tb, td, tu, p, clusters, st);
 }
 
 // 4-CTA multicast clusters are opt-in (SWARM_GEMM_MCAST=1): measured slower on
@@ -863,6 +1052,13 @@ int dispatch(bool amn, bool bmn, const CUtensorMap& ta, const CUtensorMap& tb, c
 }  // namespace gemm
 }  // namespace swarm
 
+extern "C" int swarm_gemm_pair_clusters(void) { return swarm::gemm::max_pair_clusters(); }
+
+extern "C" size_t swarm_gemm_workspace_bytes(void) {
+    using namespace swarm::gemm;
+    return sk_bytes(std::min(num_sms() / 2, kMaxClusters));
+}
+
 extern "C" int swarm_gemm_bf16(const swarm_gemm_args* a, swarm_stream_t stream) {
     using namespace swarm;
     using namespace swarm::gemm;
@@ -873,6 +1069,7 @@ extern "C" int swarm_gemm_bf16(const swarm_gemm_args* a, swarm_stream_t stream) 
         !a->aux)
         return invalid("gemm: epilogue needs aux");
     if (a->epilogue < 0 || a->epilogue > SWARM_EPI_DGELU) return invalid("gemm: bad epilogue");
+    if (a->k_tri < 0 || a->k_tri > 2 || (a->k_tri && a->m != a->k)) return invalid("gemm: k_tri needs M == K");
     if (a->lda % 8 || a->ldb % 8 || (reinterpret_cast<uintptr_t>(a->a) & 15) || (reinterpret_cast<uintptr_t>(a->b) & 15))
         return invalid("gemm: A/B rows must be 16-byte aligned");
     // storage extents
@@ -908,14 +1105,13 @@ extern "C" int swarm_gemm_bf16(const swarm_gemm_args* a, swarm_stream_t stream) 
     p.tiles_per_batch = p.tiles_m * p.tiles_n;
     p.total_tiles = p.tiles_per_batch * a->batch;
     p.k_blocks = (a->k + BK - 1) / BK;
-    p.ksplit = 1;
-    p.kb_per_split = p.k_blocks;
     p.ra0 = a->ra0; p.ra1 = a->ra1; p.ca0 = a->ca0; p.ca1 = a->ca1;
     p.rb0 = a->rb0; p.rb1 = a->rb1; p.cb0 = a->cb0; p.cb1 = a->cb1;
     p.d = a->d;
     p.ldd = a->ldd;
     p.rd0 = a->rd0; p.rd1 = a->rd1; p.cd0 = a->cd0; p.cd1 = a->cd1;
     p.aux = a->aux;
+    p.k_tri = pair ? 0 : a->k_tri;  // the pair kernel computes the zero blocks (still exact)
     p.alpha = a->alpha;
     p.epi = a->epilogue;
     const int esz = (a->epilogue == SWARM_EPI_STORE_F32 || a->epilogue == SWARM_EPI_ACCUM_F32) ? 4 : 2;
@@ -946,29 +1142,38 @@ extern "C" int swarm_gemm_bf16(const swarm_gemm_args* a, swarm_stream_t stream) 
         if (rc == SWARM_OK && a->epilogue == SWARM_EPI_GELU) rc = encode_2d_out(&tu, a->aux, d_rows, d_cols, a->ldd, false);
         if (rc != SWARM_OK) p.tma_epi = 0;  // fall back to direct stores
     }
-    // Split-K for fp32 reduce-add outputs: partial tiles simply reduce-add, so
-    // pick the split (<= 4, >= 8 k-blocks each) that best fills whole waves of
-    // clusters — the GEMM wave tail (e.g. 256 tiles on 74 clusters) disappears.
-    if (pair && p.tma_epi && a->epilogue == SWARM_EPI_ACCUM_F32 && ksplit_enabled()) {
-        const int clusters = num_sms() / (2 * npair);
-        double best = 0.0;
-        for (int sp = 1; sp <= 4; ++sp) {
-            const int kps = (p.k_blocks + sp - 1) / sp;
-            if (sp > 1 && kps < 8) break;
-            const int units = p.tiles_per_batch * a->batch * sp;
-            const double eff = static_cast<double>(units) / (static_cast<double>((units + clusters - 1) / clusters) * clusters);
-            if (eff > best + 0.02) {
-                best = eff;
-                p.ksplit = sp;
-                p.kb_per_split = kps;
-            }
-        }
-        p.ksplit = (p.k_blocks + p.kb_per_split - 1) / p.kb_per_split;
-        p.total_tiles = p.tiles_per_batch * a->batch * p.ksplit;
-    }
+    // Stream-K tail: whole waves of 256x256 tiles stay data-parallel; the last,
+    // partial wave's tiles are cut into k-block ranges spread evenly over every
+    // cluster (e.g. 256 tiles on 74 clusters: 3 waves + 34 tiles x 32 k-blocks
+    // / 74 = 14.7 k-blocks each instead of a fourth, half-empty wave).
+    p.dp_tiles = p.total_tiles;
+    p.sk_tiles = 0;
+    p.sk_iters = 0;
     cudaStream_t st = as_stream(stream);
-    if (pair && npair == 2) return dispatch_pair<2>(a->a_mn_major, a->b_mn_major, ta, tb, td, tu, p, st);
-    if (pair) return dispatch_pair<1>(a->a_mn_major, a->b_mn_major, ta, tb, td, tu, p, st);
+    const int resident = npair == 1 ? max_pair_clusters() : num_sms() / (2 * npair);
+    int grid_clusters = std::min(p.total_tiles, resident);
+    if (pair && npair == 1 && a->workspace &&
+        a->workspace_bytes >= sk_bytes(std::min(num_sms() / 2, kMaxClusters)) &&
+        (reinterpret_cast<uintptr_t>(a->workspace) & 255) == 0) {
+        const int C = std::min(resident, kMaxClusters);
+        const int waves = p.total_tiles / C, rem = p.total_tiles % C;
+        const int kb = p.k_blocks;
+        const long long w = static_cast<long long>(rem) * kb;
+        const int per = static_cast<int>(w / C);
+        const long long t_dp = static_cast<long long>(waves + (rem ? 1 : 0)) * kb;
+        const long long t_sk = static_cast<long long>(waves) * kb + (w + C - 1) / C + 2;  // +2: fixup
+        if (rem && per >= 4 && per * (kMaxSkParts - 1) >= kb && t_sk < t_dp) {
+            p.dp_tiles = waves * C;
+            p.sk_tiles = rem;
+            p.sk_iters = static_cast<int>(w);
+            p.sk_cnt = static_cast<int*>(a->workspace);
+            p.sk_ready = p.sk_cnt + kMaxClusters * 8;
+            p.ws = reinterpret_cast<float*>(static_cast<uint8_t*>(a->workspace) + kSkFlagBytes);
+            grid_clusters = C;
+        }
+    }
+    if (pair && npair == 2) return dispatch_pair<2>(a->a_mn_major, a->b_mn_major, ta, tb, td, tu, p, grid_clusters, st);
+    if (pair) return dispatch_pair<1>(a->a_mn_major, a->b_mn_major, ta, tb, td, tu, p, grid_clusters, st);
     if (BN == 128) return dispatch<128>(a->a_mn_major, a->b_mn_major, ta, tb, td, tu, p, st);
     return dispatch<256>(a->a_mn_major, a->b_mn_major, ta, tb, td, tu, p, st);
 }

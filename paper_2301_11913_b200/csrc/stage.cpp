@@ -78,13 +78,18 @@ struct swarm_stage {
     // weight-gradient GEMMs run on a side stream forked/joined per layer, so they
     // fill the SMs the data-gradient chain leaves idle (GEMM wave tails)
     cudaStream_t side = nullptr;
+    void* skws[2] = {nullptr, nullptr};  // GEMM stream-K scratch: visit stream, side stream
     cudaEvent_t ev_fork[4] = {nullptr, nullptr, nullptr, nullptr};
     cudaEvent_t ev_join = nullptr;
-    // GEMM profiling (bench.py's live roofline): event pairs around each GEMM
+    // visit profiling (bench.py's live roofline and step breakdown): event pairs
+    // around each GEMM (category 0) and each other kernel call of a profiled visit
     bool prof_on = false;
     std::vector<cudaEvent_t> prof_events;
     std::vector<double> prof_flops;
+    std::vector<int> prof_cat;
     size_t prof_used = 0;
+    double prof_last_ms[SWARM_PROF_CATEGORIES] = {};
+    uint64_t prof_last_n[SWARM_PROF_CATEGORIES] = {};
 };
 
 namespace {
@@ -137,24 +142,76 @@ struct Op {  // one operand in its 2-D storage
 };
 
 thread_local swarm_stage* t_prof = nullptr;  // stage whose visit is being profiled, if any
+thread_local swarm_stage* t_cur = nullptr;   // stage whose visit is being issued
 
 struct ProfScope {
-    explicit ProfScope(swarm_stage* s) { t_prof = s->prof_on ? s : nullptr; }
-    ~ProfScope() { t_prof = nullptr; }
+    explicit ProfScope(swarm_stage* s) {
+        t_prof = s->prof_on ? s : nullptr;
+        t_cur = s;
+    }
+    ~ProfScope() { t_prof = t_cur = nullptr; }
 };
 
-int run_gemm(const swarm_gemm_args& g, cudaStream_t st) {
+// Begin / end one profiled kernel call (no-ops outside a profiled visit).
+int prof_begin(int cat, cudaStream_t st) {
     swarm_stage* s = t_prof;
-    if (!s) return swarm_gemm_bf16(&g, st);
+    if (!s) return SWARM_OK;
     while (s->prof_events.size() < 2 * (s->prof_used + 1)) {
         cudaEvent_t e;
         if (cudaEventCreate(&e) != cudaSuccess) return SWARM_E_CUDA;
         s->prof_events.push_back(e);
     }
     cudaEventRecord(s->prof_events[2 * s->prof_used], st);
-    const int rc = swarm_gemm_bf16(&g, st);
+    s->prof_cat.push_back(cat);
+    s->prof_flops.push_back(0.0);
+    return SWARM_OK;
+}
+void prof_end(cudaStream_t st) {
+    swarm_stage* s = t_prof;
+    if (!s) return;
     cudaEventRecord(s->prof_events[2 * s->prof_used + 1], st);
-    s->prof_flops.push_back(2.0 * g.m * g.n * static_cast<double>(g.k) * g.batch);
+    s->prof_used += 1;
+}
+struct ProfOp {
+    cudaStream_t st;
+    ProfOp(int cat, cudaStream_t st_) : st(st_) { prof_begin(cat, st); }
+    ~ProfOp() { prof_end(st); }
+};
+#define PTRY(cat, st, expr)        \
+    do {                           \
+        ProfOp _po((cat), (st));   \
+        TRY(expr);                 \
+    } while (0)
+
+bool streamk_requested() {
+    static const bool on = [] {
+        const char* e = getenv("SWARM_GEMM_STREAMK");
+        return e && e[0] == '1';
+    }();
+    return on;
+}
+
+int run_gemm(swarm_gemm_args g, cudaStream_t st) {
+    if (t_cur && streamk_requested()) {  // the visit stream and the side stream each own a stream-K scratch
+        g.workspace = t_cur->skws[st == t_cur->side ? 1 : 0];
+        g.workspace_bytes = swarm_gemm_workspace_bytes();
+    }
+    swarm_stage* s = t_prof;
+    if (!s) return swarm_gemm_bf16(&g, st);
+    TRY(prof_begin(SWARM_PROF_GEMM, st));
+    const int rc = swarm_gemm_bf16(&g, st);
+    prof_end(st);
+    s->prof_used -= 1;  // fill in the FLOPs of the pair just closed
+    double kfrac = 1.0;  // executed share of K when a causal A lets the kernel skip zero k-blocks
+    const bool pair_kernel = g.m > 128 && g.n > 128;  // csrc/gemm.cu ignores k_tri there
+    if (g.k_tri && !pair_kernel) {
+        const int tm = (g.m + 127) / 128, kb = (g.k + 63) / 64;
+        long long done = 0;
+        for (int mt = 0; mt < tm; ++mt)
+            done += g.k_tri == 1 ? std::min(kb, ((mt + 1) * 128 + 63) / 64) : kb - (mt * 128) / 64;
+        kfrac = static_cast<double>(done) / (static_cast<double>(tm) * kb);
+    }
+    s->prof_flops.back() = 2.0 * g.m * g.n * static_cast<double>(g.k) * g.batch * kfrac;
     s->prof_used += 1;
     return rc;
 }
@@ -193,8 +250,9 @@ struct BOp {
 };
 
 int bmm(swarm_stage* s, int M, int N, int K, BOp a, BOp b, void* d, int ldd, int rd0, int rd1, int cd0, int cd1,
-        int epi, float alpha, cudaStream_t st) {
+        int epi, float alpha, cudaStream_t st, int k_tri = 0) {
     swarm_gemm_args g{};
+    g.k_tri = s->cfg.causal ? k_tri : 0;  // causal P / dS: skip the all-zero key blocks
     g.m = M;
     g.n = N;
     g.k = K;
@@ -253,26 +311,26 @@ int block_forward(swarm_stage* s, Act& A, bf16* y, const LayerW& W, cudaStream_t
     const int T = s->T, d = s->d, H = s->H, dh = s->dh, F = s->F, L = s->L;
     const bf16* p16 = s->p16;
     const float* p32 = s->p32;
-    TRY(swarm_layer_norm_forward(A.x, SWARM_DTYPE_BF16, T, d, p32 + W.ln1g, p32 + W.ln1b, 1e-5, A.a, A.mu1, A.rs1, st));
+    PTRY(SWARM_PROF_LAYERNORM, st, swarm_layer_norm_forward(A.x, SWARM_DTYPE_BF16, T, d, p32 + W.ln1g, p32 + W.ln1b, 1e-5, A.a, A.mu1, A.rs1, st));
     TRY(mm(T, 3 * d, d, {A.a, d, T, d, false}, {p16 + W.wqkv, d, 3 * d, d, false}, A.qkv, 3 * d,
            SWARM_EPI_STORE_BF16, nullptr, 1.f, st));
     const float scale = 1.f / std::sqrt(static_cast<float>(dh));
     if (s->fused_attn) {
         // P = softmax(scale * Q K^T) per (b, h), scores kept in TMEM
-        TRY(swarm_attn_scores_softmax(A.qkv, A.qkv + d, 3 * d, d, s->B, H, L, dh, scale, s->cfg.causal, A.P, st));
+        PTRY(SWARM_PROF_ATTENTION, st, swarm_attn_scores_softmax(A.qkv, A.qkv + d, 3 * d, d, s->B, H, L, dh, scale, s->cfg.causal, A.P, st));
     } else {
         // S = scale * Q K^T per (b, h), then a row softmax
         TRY(bmm(s, L, L, dh, {{A.qkv, 3 * d, T, d, false}, L, 0, 0, dh},
                 {{A.qkv + d, 3 * d, T, d, false}, L, 0, 0, dh}, s->S, L, H * L, L, 0, 0, SWARM_EPI_STORE_F32, scale,
                 st));
-        TRY(swarm_attn_softmax_forward(s->S, static_cast<size_t>(s->B) * H * L, L, s->cfg.causal, A.P, st));
+        PTRY(SWARM_PROF_ATTENTION, st, swarm_attn_softmax_forward(s->S, static_cast<size_t>(s->B) * H * L, L, s->cfg.causal, A.P, st));
     }
     // O = P V  (V read MN-major straight from the qkv buffer)
     TRY(bmm(s, L, dh, L, {{A.P, L, s->B * H * L, L, false}, H * L, L, 0, 0},
-            {{A.qkv + 2 * d, 3 * d, T, d, true}, L, 0, 0, dh}, A.o, d, L, 0, 0, dh, SWARM_EPI_STORE_BF16, 1.f, st));
+            {{A.qkv + 2 * d, 3 * d, T, d, true}, L, 0, 0, dh}, A.o, d, L, 0, 0, dh, SWARM_EPI_STORE_BF16, 1.f, st, 1));
     // h = x + O Wo^T
     TRY(mm(T, d, d, {A.o, d, T, d, false}, {p16 + W.wo, d, d, d, false}, A.h, d, SWARM_EPI_RESIDUAL, A.x, 1.f, st));
-    TRY(swarm_layer_norm_forward(A.h, SWARM_DTYPE_BF16, T, d, p32 + W.ln2g, p32 + W.ln2b, 1e-5, A.c, A.mu2, A.rs2, st));
+    PTRY(SWARM_PROF_LAYERNORM, st, swarm_layer_norm_forward(A.h, SWARM_DTYPE_BF16, T, d, p32 + W.ln2g, p32 + W.ln2b, 1e-5, A.c, A.mu2, A.rs2, st));
     // u = c W1^T, g = gelu(u)
     TRY(mm(T, F, d, {A.c, d, T, d, false}, {p16 + W.w1, d, F, d, false}, A.g, F, SWARM_EPI_GELU, A.u, 1.f, st));
     // y = h + g W2^T
@@ -297,7 +355,7 @@ int block_backward(swarm_stage* s, const Act& A, const bf16* dy, bf16* dx, const
     TRY(mm(T, d, F, {s->du, F, T, F, false}, {p16 + W.w1, d, F, d, true}, s->dc, d, SWARM_EPI_STORE_BF16, nullptr, 1.f,
            st));
     // dh = LN2'(dc) + dy
-    TRY(swarm_layer_norm_backward(s->dc, A.h, SWARM_DTYPE_BF16, T, d, p32 + W.ln2g, A.mu2, A.rs2, dy, s->dhid,
+    PTRY(SWARM_PROF_LAYERNORM, st, swarm_layer_norm_backward(s->dc, A.h, SWARM_DTYPE_BF16, T, d, p32 + W.ln2g, A.mu2, A.rs2, dy, s->dhid,
                                   G + W.ln2g, G + W.ln2b, 1, s->lnws, st));
     // attention output projection
     TRY(fork_side(s, st, 2));
@@ -307,21 +365,21 @@ int block_backward(swarm_stage* s, const Act& A, const bf16* dy, bf16* dx, const
     // dP = dO V^T ; dS = scale * P (dP - rowsum(P dP))
     const float scale = 1.f / std::sqrt(static_cast<float>(dh));
     if (s->fused_attn) {
-        TRY(swarm_attn_scores_softmax_backward(s->dO, d, A.qkv + 2 * d, 3 * d, d, A.P, s->B, H, L, dh, scale,
+        PTRY(SWARM_PROF_ATTENTION, st, swarm_attn_scores_softmax_backward(s->dO, d, A.qkv + 2 * d, 3 * d, d, A.P, s->B, H, L, dh, scale,
                                                s->cfg.causal, s->dS, st));
     } else {
         TRY(bmm(s, L, L, dh, {{s->dO, d, T, d, false}, L, 0, 0, dh},
                 {{A.qkv + 2 * d, 3 * d, T, d, false}, L, 0, 0, dh}, s->dP, L, H * L, L, 0, 0, SWARM_EPI_STORE_F32,
                 1.f, st));
-        TRY(swarm_attn_softmax_backward(A.P, s->dP, BHL, L, scale, s->dS, st));
+        PTRY(SWARM_PROF_ATTENTION, st, swarm_attn_softmax_backward(A.P, s->dP, BHL, L, scale, s->dS, st));
     }
     // dQ = dS K ; dK = dS^T Q ; dV = P^T dO   (all read in place, written into dqkv)
     TRY(bmm(s, L, dh, L, {{s->dS, L, BHL, L, false}, H * L, L, 0, 0}, {{A.qkv + d, 3 * d, T, d, true}, L, 0, 0, dh},
-            s->dqkv, 3 * d, L, 0, 0, dh, SWARM_EPI_STORE_BF16, 1.f, st));
+            s->dqkv, 3 * d, L, 0, 0, dh, SWARM_EPI_STORE_BF16, 1.f, st, 1));
     TRY(bmm(s, L, dh, L, {{s->dS, L, BHL, L, true}, H * L, L, 0, 0}, {{A.qkv, 3 * d, T, d, true}, L, 0, 0, dh},
-            s->dqkv + d, 3 * d, L, 0, 0, dh, SWARM_EPI_STORE_BF16, 1.f, st));
+            s->dqkv + d, 3 * d, L, 0, 0, dh, SWARM_EPI_STORE_BF16, 1.f, st, 2));
     TRY(bmm(s, L, dh, L, {{A.P, L, BHL, L, true}, H * L, L, 0, 0}, {{s->dO, d, T, d, true}, L, 0, 0, dh},
-            s->dqkv + 2 * d, 3 * d, L, 0, 0, dh, SWARM_EPI_STORE_BF16, 1.f, st));
+            s->dqkv + 2 * d, 3 * d, L, 0, 0, dh, SWARM_EPI_STORE_BF16, 1.f, st, 2));
     // da = dqkv Wqkv ; dWqkv += dqkv^T a
     TRY(fork_side(s, st, 3));
     TRY(mm(3 * d, d, T, {s->dqkv, 3 * d, T, 3 * d, true}, {A.a, d, T, d, true}, G + W.wqkv, d, SWARM_EPI_ACCUM_F32,
@@ -329,7 +387,7 @@ int block_backward(swarm_stage* s, const Act& A, const bf16* dy, bf16* dx, const
     TRY(mm(T, d, 3 * d, {s->dqkv, 3 * d, T, 3 * d, false}, {p16 + W.wqkv, d, 3 * d, d, true}, s->da, d,
            SWARM_EPI_STORE_BF16, nullptr, 1.f, st));
     // dx = LN1'(da) + dh
-    TRY(swarm_layer_norm_backward(s->da, A.x, SWARM_DTYPE_BF16, T, d, p32 + W.ln1g, A.mu1, A.rs1, s->dhid, dx,
+    PTRY(SWARM_PROF_LAYERNORM, st, swarm_layer_norm_backward(s->da, A.x, SWARM_DTYPE_BF16, T, d, p32 + W.ln1g, A.mu1, A.rs1, s->dhid, dx,
                                   G + W.ln1g, G + W.ln1b, 1, s->lnws, st));
     // the next layer overwrites the workspaces the weight gradients read
     return join_side(s, st);
@@ -530,6 +588,11 @@ int create(const swarm_stage_config* c, swarm_stage* s) {
         TRY(alloc(s, &s->dlogits, T * s->V));
     }
     if (cudaStreamCreateWithFlags(&s->side, cudaStreamNonBlocking) != cudaSuccess) return SWARM_E_CUDA;
+    for (void*& w : s->skws) {
+        if (!streamk_requested()) break;
+        TRY(dmalloc(s, &w, swarm_gemm_workspace_bytes()));
+        if (cudaMemset(w, 0, swarm_gemm_workspace_bytes()) != cudaSuccess) return SWARM_E_CUDA;
+    }
     for (auto& e : s->ev_fork)
         if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) return SWARM_E_CUDA;
     if (cudaEventCreateWithFlags(&s->ev_join, cudaEventDisableTiming) != cudaSuccess) return SWARM_E_CUDA;
@@ -582,20 +645,35 @@ int swarm_wire_parse_header(const void* header, uint32_t* n_elems, uint32_t* blo
 void swarm_stage_profile(swarm_stage_t s, int enable) { s->prof_on = enable != 0; }
 
 int swarm_stage_profile_read(swarm_stage_t s, double* gemm_ms, double* gemm_flops, uint64_t* gemm_launches) {
-    double ms = 0.0, fl = 0.0;
+    double fl = 0.0;
+    double ms[SWARM_PROF_CATEGORIES] = {};
+    uint64_t n[SWARM_PROF_CATEGORIES] = {};
     for (size_t i = 0; i < s->prof_used; ++i) {
         if (cudaEventSynchronize(s->prof_events[2 * i + 1]) != cudaSuccess) return SWARM_E_CUDA;
         float e = 0.f;
         cudaEventElapsedTime(&e, s->prof_events[2 * i], s->prof_events[2 * i + 1]);
-        ms += e;
+        ms[s->prof_cat[i]] += e;
+        n[s->prof_cat[i]] += 1;
         fl += s->prof_flops[i];
     }
-    if (gemm_ms) *gemm_ms = ms;
+    if (gemm_ms) *gemm_ms = ms[SWARM_PROF_GEMM];
     if (gemm_flops) *gemm_flops = fl;
-    if (gemm_launches) *gemm_launches = s->prof_used;
+    if (gemm_launches) *gemm_launches = n[SWARM_PROF_GEMM];
+    for (int c = 0; c < SWARM_PROF_CATEGORIES; ++c) {
+        s->prof_last_ms[c] = ms[c];
+        s->prof_last_n[c] = n[c];
+    }
     s->prof_used = 0;
     s->prof_flops.clear();
+    s->prof_cat.clear();
     return SWARM_OK;
+}
+
+void swarm_stage_profile_breakdown(swarm_stage_t s, double* ms, uint64_t* launches) {
+    for (int c = 0; c < SWARM_PROF_CATEGORIES; ++c) {
+        if (ms) ms[c] = s->prof_last_ms[c];
+        if (launches) launches[c] = s->prof_last_n[c];
+    }
 }
 size_t swarm_stage_num_params(swarm_stage_t s) { return s->nparams; }
 float* swarm_stage_grads(swarm_stage_t s) { return s->grad; }
@@ -650,17 +728,17 @@ int swarm_stage_forward(swarm_stage_t s, int slot, const void* in, const int32_t
     if (s->cfg.is_first) {
         if (cudaMemcpyAsync(sl.tokens, in, T * sizeof(int32_t), cudaMemcpyDeviceToDevice, st) != cudaSuccess)
             return SWARM_E_CUDA;
-        TRY(swarm_embedding_forward(sl.tokens, T, s->p16 + s->emb, s->V, d, sl.layer[0].x, st));
+        PTRY(SWARM_PROF_OTHER, st, swarm_embedding_forward(sl.tokens, T, s->p16 + s->emb, s->V, d, sl.layer[0].x, st));
     } else if (s->bneck) {
         // receiver: x0 = LN_d(dequant(wire)) W_d^T   (d/k -> d)
         const int w = s->wire_w;
-        TRY(wire_decode(s, in, sl.mi, st));
-        TRY(swarm_layer_norm_forward(sl.mi, SWARM_DTYPE_BF16, T, w, s->p32 + s->bn_in_g, s->p32 + s->bn_in_b, 1e-5,
+        PTRY(SWARM_PROF_OTHER, st, wire_decode(s, in, sl.mi, st));
+        PTRY(SWARM_PROF_LAYERNORM, st, swarm_layer_norm_forward(sl.mi, SWARM_DTYPE_BF16, T, w, s->p32 + s->bn_in_g, s->p32 + s->bn_in_b, 1e-5,
                                      sl.ni, sl.mud, sl.rsd, st));
         TRY(mm(T, d, w, {sl.ni, w, T, w, false}, {s->p16 + s->bn_wd, w, d, w, false}, sl.layer[0].x, d,
                SWARM_EPI_STORE_BF16, nullptr, 1.f, st));
     } else {
-        TRY(wire_decode(s, in, sl.layer[0].x, st));
+        PTRY(SWARM_PROF_OTHER, st, wire_decode(s, in, sl.layer[0].x, st));
     }
     for (int l = 0; l < n; ++l) {
         bf16* y = (l + 1 < n) ? sl.layer[l + 1].x : sl.out;
@@ -668,21 +746,25 @@ int swarm_stage_forward(swarm_stage_t s, int slot, const void* in, const int32_t
     }
     if (!s->cfg.is_last) {
         if (!out) return fail("forward: null output message");
-        if (!s->bneck) return wire_encode(s, sl.out, out, st);
+        if (!s->bneck) {
+            ProfOp po(SWARM_PROF_OTHER, st);
+            return wire_encode(s, sl.out, out, st);
+        }
         // sender: wire = int8(maxout_k(LN_c(out)))
-        TRY(swarm_layer_norm_forward(sl.out, SWARM_DTYPE_BF16, T, d, s->p32 + s->bn_out_g, s->p32 + s->bn_out_b, 1e-5,
+        PTRY(SWARM_PROF_LAYERNORM, st, swarm_layer_norm_forward(sl.out, SWARM_DTYPE_BF16, T, d, s->p32 + s->bn_out_g, s->p32 + s->bn_out_b, 1e-5,
                                      sl.z, sl.muc, sl.rsc, st));
-        TRY(swarm_maxout_forward(sl.z, SWARM_DTYPE_BF16, static_cast<size_t>(T) * d, s->cfg.maxout_k, sl.mo, sl.am,
+        PTRY(SWARM_PROF_OTHER, st, swarm_maxout_forward(sl.z, SWARM_DTYPE_BF16, static_cast<size_t>(T) * d, s->cfg.maxout_k, sl.mo, sl.am,
                                  st));
+        ProfOp po(SWARM_PROF_OTHER, st);
         return wire_encode(s, sl.mo, out, st);
     }
     if (!targets) return fail("forward: last stage needs targets");
     // final LN + LM head + cross-entropy, with the head's backward fused in
-    TRY(swarm_layer_norm_forward(sl.out, SWARM_DTYPE_BF16, T, d, s->p32 + s->lnfg, s->p32 + s->lnfb, 1e-5, sl.xf,
+    PTRY(SWARM_PROF_LAYERNORM, st, swarm_layer_norm_forward(sl.out, SWARM_DTYPE_BF16, T, d, s->p32 + s->lnfg, s->p32 + s->lnfb, 1e-5, sl.xf,
                                  sl.muf, sl.rsf, st));
     TRY(mm(T, s->V, d, {sl.xf, d, T, d, false}, {s->p16 + s->head, d, s->V, d, false}, s->logits, s->V,
            SWARM_EPI_STORE_F32, nullptr, 1.f, st));
-    TRY(swarm_cross_entropy(s->logits, targets, T, s->V, loss_scale, loss_sum, s->dlogits, st));
+    PTRY(SWARM_PROF_OTHER, st, swarm_cross_entropy(s->logits, targets, T, s->V, loss_scale, loss_sum, s->dlogits, st));
     TRY(fork_side(s, st, 0));
     TRY(mm(s->V, d, T, {s->dlogits, s->V, T, s->V, true}, {sl.xf, d, T, d, true}, s->grad + s->head, d,
            SWARM_EPI_ACCUM_F32, nullptr, 1.f, side_of(s, st)));
@@ -699,29 +781,35 @@ int swarm_stage_backward(swarm_stage_t s, int slot, const void* grad_in, void* g
     const int T = s->T, d = s->d, n = s->cfg.n_layers;
     int cur = 0;
     if (s->cfg.is_last) {
-        TRY(swarm_layer_norm_backward(sl.dxf, sl.out, SWARM_DTYPE_BF16, T, d, s->p32 + s->lnfg, sl.muf, sl.rsf, nullptr,
+        PTRY(SWARM_PROF_LAYERNORM, st, swarm_layer_norm_backward(sl.dxf, sl.out, SWARM_DTYPE_BF16, T, d, s->p32 + s->lnfg, sl.muf, sl.rsf, nullptr,
                                       s->gy[0], s->grad + s->lnfg, s->grad + s->lnfb, 1, s->lnws, st));
     } else {
         if (!grad_in) return fail("backward: null gradient message");
         if (s->bneck) {
             // d out = LN_c'(maxout'(dequant(grad)))
-            TRY(wire_decode(s, grad_in, s->wtmp, st));
-            TRY(swarm_maxout_backward(s->wtmp, SWARM_DTYPE_BF16, sl.am, static_cast<size_t>(T) * s->wire_w,
+            PTRY(SWARM_PROF_OTHER, st, wire_decode(s, grad_in, s->wtmp, st));
+            PTRY(SWARM_PROF_OTHER, st, swarm_maxout_backward(s->wtmp, SWARM_DTYPE_BF16, sl.am, static_cast<size_t>(T) * s->wire_w,
                                       s->cfg.maxout_k, s->dc, st));
-            TRY(swarm_layer_norm_backward(s->dc, sl.out, SWARM_DTYPE_BF16, T, d, s->p32 + s->bn_out_g, sl.muc, sl.rsc,
+            PTRY(SWARM_PROF_LAYERNORM, st, swarm_layer_norm_backward(s->dc, sl.out, SWARM_DTYPE_BF16, T, d, s->p32 + s->bn_out_g, sl.muc, sl.rsc,
                                           nullptr, s->gy[0], s->grad + s->bn_out_g, s->grad + s->bn_out_b, 1, s->lnws,
                                           st));
         } else {
-            TRY(wire_decode(s, grad_in, s->gy[0], st));
+            PTRY(SWARM_PROF_OTHER, st, wire_decode(s, grad_in, s->gy[0], st));
         }
     }
     for (int l = n - 1; l >= 0; --l) {
         TRY(block_backward(s, sl.layer[l], s->gy[cur], s->gy[cur ^ 1], weights(s, l), st));
         cur ^= 1;
     }
-    if (s->cfg.is_first) return swarm_embedding_backward(sl.tokens, T, s->gy[cur], s->V, d, s->grad + s->emb, st);
+    if (s->cfg.is_first) {
+        ProfOp po(SWARM_PROF_OTHER, st);
+        return swarm_embedding_backward(sl.tokens, T, s->gy[cur], s->V, d, s->grad + s->emb, st);
+    }
     if (!grad_out) return fail("backward: null output gradient message");
-    if (!s->bneck) return wire_encode(s, s->gy[cur], grad_out, st);
+    if (!s->bneck) {
+        ProfOp po(SWARM_PROF_OTHER, st);
+        return wire_encode(s, s->gy[cur], grad_out, st);
+    }
     // receiver side of the bottleneck: dW_d += dx0^T ni ; dni = dx0 W_d ; dmi = LN_d'(dni)
     const int w = s->wire_w;
     bf16* dx0 = s->gy[cur];
@@ -729,8 +817,9 @@ int swarm_stage_backward(swarm_stage_t s, int slot, const void* grad_in, void* g
            1.f, st));
     TRY(mm(T, w, d, {dx0, d, T, d, false}, {s->p16 + s->bn_wd, w, d, w, true}, s->wtmp, w, SWARM_EPI_STORE_BF16,
            nullptr, 1.f, st));
-    TRY(swarm_layer_norm_backward(s->wtmp, sl.mi, SWARM_DTYPE_BF16, T, w, s->p32 + s->bn_in_g, sl.mud, sl.rsd, nullptr,
+    PTRY(SWARM_PROF_LAYERNORM, st, swarm_layer_norm_backward(s->wtmp, sl.mi, SWARM_DTYPE_BF16, T, w, s->p32 + s->bn_in_g, sl.mud, sl.rsd, nullptr,
                                   s->dqkv, s->grad + s->bn_in_g, s->grad + s->bn_in_b, 1, s->lnws, st));
+    ProfOp po(SWARM_PROF_OTHER, st);
     return wire_encode(s, s->dqkv, grad_out, st);
 }
 

@@ -127,13 +127,30 @@ def layer_norm_backward(dy: torch.Tensor, x: torch.Tensor, gain: torch.Tensor | 
 
 
 # -------------------------------------------------------------------- gemm
+_GEMM_WS: dict = {}
+
+
+def gemm_workspace(device=None) -> torch.Tensor:
+    """The stream-K scratch for GEMMs issued on the current stream of `device`
+    (zero-filled once; the kernel leaves it zeroed)."""
+    dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+    key = (dev.index, torch.cuda.current_stream(dev).cuda_stream)
+    ws = _GEMM_WS.get(key)
+    if ws is None:
+        ws = torch.zeros(int(L.lib().swarm_gemm_workspace_bytes()), dtype=torch.uint8, device=dev)
+        _GEMM_WS[key] = ws
+    return ws
+
+
 def gemm(a: torch.Tensor, b: torch.Tensor, *, a_t: bool = False, b_t: bool = False, out: torch.Tensor | None = None,
          epilogue: int = L.EPI_STORE_BF16, aux: torch.Tensor | None = None, alpha: float = 1.0,
-         out_dtype=torch.bfloat16) -> torch.Tensor:
+         out_dtype=torch.bfloat16, streamk: bool = False) -> torch.Tensor:
     """K5: D = alpha * op(A) @ op(B)^T on the tcgen05 kernel.
 
     a: [M, K] (or [K, M] with a_t=True, i.e. MN-major), b: [N, K] (or [K, N] with b_t=True).
-    So `gemm(x, w)` is x @ w.T for a row-major Linear weight w[out, in]."""
+    So `gemm(x, w)` is x @ w.T for a row-major Linear weight w[out, in].  With
+    `streamk` the last partial wave of tiles is split along K (per-stream scratch;
+    off by default: measured slower on B200, see profiles/r01_gemm_experiments.md)."""
     for t, nm in ((a, "a"), (b, "b")):
         _dev(t, nm)
         if t.dtype != torch.bfloat16 or t.dim() != 2:
@@ -155,6 +172,9 @@ def gemm(a: torch.Tensor, b: torch.Tensor, *, a_t: bool = False, b_t: bool = Fal
     args.aux = None if aux is None else aux.data_ptr()
     args.alpha = alpha
     args.epilogue = epilogue
+    if streamk:
+        ws = gemm_workspace(a.device)
+        args.workspace, args.workspace_bytes = ws.data_ptr(), ws.numel()
     L.check(L.lib().swarm_gemm_bf16(C.byref(args), _stream()), "gemm_bf16")
     return out
 

@@ -166,6 +166,15 @@ class Stage:
         L.check(self.lib.swarm_stage_profile_read(self.h, C.byref(ms), C.byref(fl), C.byref(n)), "profile_read")
         return ms.value, fl.value, n.value
 
+    PROF_CATEGORIES = ("gemm", "attention", "layernorm", "other")
+
+    def profile_breakdown(self) -> dict:
+        """{category: (ms, calls)} of the last profile_read."""
+        ms = (C.c_double * 4)()
+        n = (C.c_uint64 * 4)()
+        self.lib.swarm_stage_profile_breakdown(self.h, ms, n)
+        return {c: (ms[i], n[i]) for i, c in enumerate(self.PROF_CATEGORIES)}
+
     def activation(self, slot: int, layer: int, name: str) -> torch.Tensor:
         ptr, n = C.c_void_p(), C.c_size_t()
         L.check(self.lib.swarm_stage_activation(self.h, slot, layer, name.encode(), C.byref(ptr), C.byref(n)),

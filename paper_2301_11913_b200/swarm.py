@@ -490,9 +490,13 @@ class SwarmPipeline:
     def profile_read(self):
         ms = fl = 0.0
         n = 0
+        self.last_breakdown = {}
         for st in self.stages.values():
             a, b, c = st.profile_read()
             ms, fl, n = ms + a, fl + b, n + c
+            for cat, (cms, cn) in st.profile_breakdown().items():
+                pm, pn = self.last_breakdown.get(cat, (0.0, 0))
+                self.last_breakdown[cat] = (pm + cms, pn + cn)
         return ms, fl, n
 
     def kernels_launched(self) -> int:

@@ -96,3 +96,108 @@ def test_gemm_batched_heads(cuda):
     kk = qkv[:, d:2 * d].float().view(B, Lq, H, dh).transpose(1, 2)
     ref = (q @ kk.transpose(-1, -2)).reshape(B * H * Lq, Lq)
     torch.testing.assert_close(S, ref, rtol=1e-4, atol=1e-3)
+
+
+# Stream-K tail (csrc/gemm.cu): shapes whose 256x256 tile count leaves a partial
+# last wave on 74 SM pairs, so the tail tiles are split along K across clusters.
+SK_SHAPES = [(2048, 2048, 2048), (2048, 8192, 2048), (2048, 6144, 2048), (2048, 2048, 8192), (8192, 2048, 2048),
+             (4096, 2304, 1024), (768, 3328, 4096), (1000, 2000, 1000)]
+
+
+@pytest.mark.parametrize("m,n,k", SK_SHAPES)
+@pytest.mark.parametrize("a_t,b_t", [(False, False), (False, True), (True, True)])
+def test_gemm_streamk_matches_whole_tiles(cuda, m, n, k, a_t, b_t):
+    """Stream-K vs whole-tile launches: identical up to fp32 summation order
+    (rtol 1e-5, atol 5e-5 * sqrt(K) for O(sqrt(K)) outputs), against torch as
+    well, and repeated launches agree (the self-resetting flags are clean)."""
+    import torch
+    from paper_2301_11913_b200 import ops
+    torch.manual_seed(m + 3 * n + 7 * k)
+    a = torch.randn((k, m) if a_t else (m, k), device="cuda").bfloat16()
+    b = torch.randn((k, n) if b_t else (n, k), device="cuda").bfloat16()
+    ref = ref_mm(a, b, a_t, b_t)
+    whole = ops.gemm(a, b, a_t=a_t, b_t=b_t, epilogue=1, streamk=False)
+    for _ in range(3):
+        sk = ops.gemm(a, b, a_t=a_t, b_t=b_t, epilogue=1, streamk=True)
+        torch.testing.assert_close(sk, whole, rtol=1e-5, atol=5e-5 * math.sqrt(k))
+    torch.testing.assert_close(sk, ref, rtol=1e-4, atol=1e-4 * math.sqrt(k))
+    sk16 = ops.gemm(a, b, a_t=a_t, b_t=b_t, streamk=True)
+    torch.testing.assert_close(sk16.float(), ref, rtol=1e-2, atol=1e-2 * math.sqrt(k) / 8 + 1e-2)
+
+
+def test_gemm_streamk_epilogues_and_graph(cuda):
+    """Every fused epilogue on a stream-K shape, eager and replayed from a CUDA
+    graph several times (the partial/flag handshake must be replay-safe)."""
+    import torch
+    from paper_2301_11913_b200 import _lib as L, ops
+    torch.manual_seed(1)
+    m, n, k = 2048, 2048, 2048
+    a = torch.randn(m, k, device="cuda").bfloat16()
+    b = torch.randn(n, k, device="cuda").bfloat16()
+    r = torch.randn(m, n, device="cuda").bfloat16()
+    ref = a.float() @ b.float().t()
+    out = ops.gemm(a, b, epilogue=L.EPI_RESIDUAL, aux=r, streamk=True)
+    torch.testing.assert_close(out.float(), ref + r.float(), rtol=1e-2, atol=0.5)
+    u = torch.empty(m, n, device="cuda").bfloat16()
+    g = ops.gemm(a, b, epilogue=L.EPI_GELU, aux=u, streamk=True)
+    torch.testing.assert_close(u.float(), ref, rtol=1e-2, atol=0.5)
+    torch.testing.assert_close(g.float(), torch.nn.functional.gelu(u.float(), approximate="tanh"), rtol=2e-2, atol=2e-2)
+    acc = torch.zeros(m, n, device="cuda")
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        ops.gemm_workspace()  # allocate this stream's scratch before capture
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph, stream=s):
+            ops.gemm(a, b, epilogue=L.EPI_ACCUM_F32, out=acc, streamk=True)
+    torch.cuda.current_stream().wait_stream(s)
+    acc.zero_()
+    for _ in range(4):
+        graph.replay()
+    torch.cuda.synchronize()
+    torch.testing.assert_close(acc, 4 * ref, rtol=1e-4, atol=1e-2 * math.sqrt(k))
+
+
+@pytest.mark.parametrize("tri", [1, 2])
+def test_gemm_causal_k_skip(cuda, tri):
+    """k_tri: with a causal A (P / dS, tri=1; their transposes, tri=2) the kernel
+    skips the all-zero k-blocks; the result equals the dense product exactly
+    because the skipped blocks contribute nothing.  Poison the skipped region
+    with NaN to prove it is never read."""
+    import torch
+    from paper_2301_11913_b200 import _lib as L, ops
+    Bz, Lq, dh = 6, 512, 128
+    torch.manual_seed(tri)
+    A = torch.randn(Bz, Lq, Lq, device="cuda")
+    mask = torch.ones(Lq, Lq, device="cuda").tril().bool()  # A[i, j] != 0 only for j <= i
+    dense = A.masked_fill(~mask, 0.0)
+    if tri == 2:
+        dense = dense.transpose(1, 2).contiguous()  # A[i, j] != 0 only for j >= i
+        mask = mask.t()
+    Ab = dense.bfloat16()
+    # rows of a tile that still share a k-block with the nonzero region stay zero;
+    # everything outside whole skipped 64-wide k-blocks of each 128-row tile -> NaN
+    poisoned = Ab.clone()
+    for mt in range(Lq // 128):
+        r0, r1 = mt * 128, (mt + 1) * 128
+        if tri == 1:
+            k_end = -(-r1 // 64) * 64
+            poisoned[:, r0:r1, k_end:] = float("nan")
+        else:
+            k_beg = (r0 // 64) * 64
+            poisoned[:, r0:r1, :k_beg] = float("nan")
+    V = torch.randn(Bz * Lq, dh, device="cuda").bfloat16()
+    out = torch.empty(Bz * Lq, dh, device="cuda", dtype=torch.float32)
+    a2 = poisoned.reshape(Bz * Lq, Lq)
+    args = L.GemmArgs()
+    args.m, args.n, args.k, args.batch, args.bh = Lq, dh, Lq, Bz, 1
+    args.a, args.lda, args.a_mn_major, args.a_rows, args.a_cols = a2.data_ptr(), Lq, 0, Bz * Lq, Lq
+    args.ra0 = Lq
+    args.b, args.ldb, args.b_mn_major, args.b_rows, args.b_cols = V.data_ptr(), dh, 1, Bz * Lq, dh
+    args.rb0 = Lq
+    args.d, args.ldd, args.rd0 = out.data_ptr(), dh, Lq
+    args.alpha, args.epilogue, args.k_tri = 1.0, L.EPI_STORE_F32, tri
+    ops.gemm_raw(args)
+    ref = (Ab.float() @ V.float().view(Bz, Lq, dh)).reshape(Bz * Lq, dh)
+    assert torch.isfinite(out).all()
+    torch.testing.assert_close(out, ref, rtol=1e-4, atol=1e-3)
