@@ -291,6 +291,10 @@ int swarm_stage_param_info(swarm_stage_t st, int index, const char** name, size_
 #define SWARM_PROF_CATEGORIES 4
 void swarm_stage_profile(swarm_stage_t st, int enable);
 int swarm_stage_profile_read(swarm_stage_t st, double* gemm_ms, double* gemm_flops, uint64_t* gemm_launches);
+/* measurement utility: occupy `stream` for `ns` nanoseconds (one spinning
+   thread) so the kernels issued behind it run back to back, free of host
+   launch gaps, while an eagerly issued visit is being profiled */
+int swarm_gpu_spin(uint64_t ns, swarm_stream_t stream);
 void swarm_stage_profile_breakdown(swarm_stage_t st, double* ms /* [SWARM_PROF_CATEGORIES] */,
                                    uint64_t* launches /* [SWARM_PROF_CATEGORIES] */);
 /* saved activation of (slot, layer) by name ("x","a","qkv","P","o","h","c","u","g","xf","dxf"), for tests */

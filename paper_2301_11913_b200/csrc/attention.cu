@@ -18,6 +18,7 @@
 #include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <unordered_map>
 
 #include "common.cuh"
 #include "sm100.cuh"
@@ -94,6 +95,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     k_attn_rows(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUtensorMap tma_b,
                 const __grid_constant__ CUtensorMap tma_p_in, const __grid_constant__ CUtensorMap tma_out,
                 const Params p) {
+    pdl_trigger();
     extern __shared__ uint8_t smem_raw[];
     const uint32_t raw = smem_u32(smem_raw);
     uint8_t* smem = smem_raw + ((1024 - (raw & 1023)) & 1023);
@@ -129,6 +131,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
+    pdl_wait();
 
     if (warp == 0 && lane == 0) {
         // ------------------------------------------------------------ TMA
@@ -303,8 +306,48 @@ EncodeFn encoder() {
     return fn;
 }
 
+int map_bf16_uncached(CUtensorMap* m, const void* ptr, long long rows, long long cols, long long ld, int bi, int bo,
+                      CUtensorMapSwizzle sw);
+
+// Descriptor cache (the same few operands recur every layer and microbatch):
+// encoding costs microseconds of host time per map, which an eager visit would
+// otherwise spend with the GPU idle.
+struct MapKey {
+    const void* ptr;
+    long long rows, cols, ld;
+    int bi, bo, sw;
+    bool operator==(const MapKey& o) const {
+        return ptr == o.ptr && rows == o.rows && cols == o.cols && ld == o.ld && bi == o.bi && bo == o.bo && sw == o.sw;
+    }
+};
+struct MapKeyHash {
+    size_t operator()(const MapKey& k) const {
+        size_t h = reinterpret_cast<uintptr_t>(k.ptr);
+        for (long long v : {k.rows, k.cols, k.ld, static_cast<long long>(k.bi) << 32 | k.bo << 8 | k.sw})
+            h = h * 0x9E3779B97F4A7C15ull + static_cast<size_t>(v);
+        return h;
+    }
+};
+
 int map_bf16(CUtensorMap* m, const void* ptr, long long rows, long long cols, long long ld, int bi, int bo,
              CUtensorMapSwizzle sw) {
+    thread_local std::unordered_map<MapKey, CUtensorMap, MapKeyHash> cache;
+    const MapKey key{ptr, rows, cols, ld, bi, bo, static_cast<int>(sw)};
+    auto it = cache.find(key);
+    if (it != cache.end()) {
+        *m = it->second;
+        return SWARM_OK;
+    }
+    const int rc = map_bf16_uncached(m, ptr, rows, cols, ld, bi, bo, sw);
+    if (rc == SWARM_OK) {
+        if (cache.size() > 4096) cache.clear();
+        cache.emplace(key, *m);
+    }
+    return rc;
+}
+
+int map_bf16_uncached(CUtensorMap* m, const void* ptr, long long rows, long long cols, long long ld, int bi, int bo,
+                      CUtensorMapSwizzle sw) {
     EncodeFn enc = encoder();
     if (!enc) return SWARM_E_CUDA;
     const cuuint64_t dims[2] = {static_cast<cuuint64_t>(cols), static_cast<cuuint64_t>(rows)};
@@ -339,7 +382,7 @@ int launch(const void* a, int lda, int a_cols, int a_col0, const void* b, int ld
         attr = true;
     }
     Params p{B, H, L, dh, causal, a_col0, b_col0, scale};
-    kern<<<B * H * (L / BQ), kThreads, kSmem, st>>>(ta, tb, tp, to, p);
+    SWARM_CUDA_TRY(launch_pdl(kern, dim3(B * H * (L / BQ)), dim3(kThreads), kSmem, st, ta, tb, tp, to, p));
     SWARM_LAUNCH_CHECK("k_attn_rows");
     return SWARM_OK;
 }

@@ -46,4 +46,35 @@ inline cudaStream_t as_stream(swarm_stream_t s) { return static_cast<cudaStream_
 
 constexpr int kNumSMs = 148;
 
+// Programmatic dependent launch.  Kernels of the per-layer chain (GEMMs,
+// attention, LayerNorm) are launched with programmatic stream serialization, so
+// a kernel's CTAs can be scheduled — and run their prologue (barrier init, TMEM
+// allocation, descriptor prefetch) on SMs the previous kernel's tail leaves
+// idle — before that kernel finishes.  Every such kernel calls pdl_trigger()
+// first and pdl_wait() before its first global-memory access; both are no-ops
+// for a kernel launched without the attribute.  SWARM_PDL=0 disables it.
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+bool pdl_enabled();
+
+inline int pdl_attr(cudaLaunchAttribute* a) {
+    if (!pdl_enabled()) return 0;
+    a->id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    a->val.programmaticStreamSerializationAllowed = 1;
+    return 1;
+}
+
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args... args) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    cfg.numAttrs = static_cast<unsigned>(pdl_attr(&attr[0]));
+    cfg.attrs = attr;
+    return cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+}
+
 }  // namespace swarm

@@ -350,6 +350,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     k_gemm(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUtensorMap tma_b,
            const __grid_constant__ CUtensorMap tma_d, const __grid_constant__ CUtensorMap tma_u, const Params p) {
     using C = Cfg<BN>;
+    pdl_trigger();
     extern __shared__ uint8_t smem_raw[];
     const uint32_t raw = smem_u32(smem_raw);
     uint8_t* smem = smem_raw + ((1024 - (raw & 1023)) & 1023);
@@ -386,6 +387,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
+    pdl_wait();  // the previous kernel's outputs (our operands) are complete from here on
 
     if (warp == 0) {
         if (lane == 0) {
@@ -568,6 +570,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     k_gemm2(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUtensorMap tma_b,
             const __grid_constant__ CUtensorMap tma_d, const __grid_constant__ CUtensorMap tma_u, const Params p) {
     using C = Cfg2;
+    pdl_trigger();
     extern __shared__ uint8_t smem_raw[];
     const uint32_t raw = smem_u32(smem_raw);
     uint8_t* smem = smem_raw + ((1024 - (raw & 1023)) & 1023);
@@ -613,6 +616,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     cluster_sync();  // barriers of both CTAs initialised before any remote arrive / TMA
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
+    pdl_wait();  // the previous kernel's outputs (our operands) are complete from here on
 
     if (warp == 0) {
         if (lane == 0) {
@@ -891,7 +895,25 @@ int encode_2d_uncached(CUtensorMap* m, const void* ptr, long long rows, long lon
 
 // Output map for the TMA epilogue: 32 x 32 boxes, fp32 (128-B rows, SWIZZLE_128B)
 // or bf16 (64-B rows, SWIZZLE_64B), matching stage_f32 / stage_bf16.
+int encode_2d_out_uncached(CUtensorMap* m, const void* ptr, long long rows, long long cols, long long ld, bool f32);
+
 int encode_2d_out(CUtensorMap* m, const void* ptr, long long rows, long long cols, long long ld, bool f32) {
+    thread_local std::unordered_map<MapKey, CUtensorMap, MapKeyHash> cache;
+    const MapKey key{ptr, rows, cols, ld, f32 ? -32 : -16, 32};  // negative box tags: output maps
+    auto it = cache.find(key);
+    if (it != cache.end()) {
+        *m = it->second;
+        return SWARM_OK;
+    }
+    const int rc = encode_2d_out_uncached(m, ptr, rows, cols, ld, f32);
+    if (rc == SWARM_OK) {
+        if (cache.size() > 16384) cache.clear();
+        cache.emplace(key, *m);
+    }
+    return rc;
+}
+
+int encode_2d_out_uncached(CUtensorMap* m, const void* ptr, long long rows, long long cols, long long ld, bool f32) {
     EncodeFn enc = get_encode();
     if (!enc) return SWARM_E_CUDA;
     const cuuint64_t dims[2] = {static_cast<cuuint64_t>(cols), static_cast<cuuint64_t>(rows)};
@@ -948,7 +970,7 @@ int launch(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& td, 
         attr = true;
     }
     const int grid = std::min(p.total_tiles, num_sms());
-    kern<<<grid, kThreads, Cfg<BN>::SMEM, st>>>(ta, tb, td, tu, p);
+    SWARM_CUDA_TRY(launch_pdl(kern, dim3(grid), dim3(kThreads), Cfg<BN>::SMEM, st, ta, tb, td, tu, p));
     SWARM_LAUNCH_CHECK("k_gemm");
     return SWARM_OK;
 }
@@ -967,13 +989,13 @@ int launch_pair(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap&
     cfg.blockDim = dim3(kThreads);
     cfg.dynamicSmemBytes = Cfg2::SMEM;
     cfg.stream = st;
-    cudaLaunchAttribute attrs[1];
+    cudaLaunchAttribute attrs[2];
     attrs[0].id = cudaLaunchAttributeClusterDimension;
     attrs[0].val.clusterDim.x = 2 * NPAIR;
     attrs[0].val.clusterDim.y = 1;
     attrs[0].val.clusterDim.z = 1;
     cfg.attrs = attrs;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = 1 + pdl_attr(&attrs[1]);
     SWARM_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, ta, tb, td, tu, p));
     SWARM_LAUNCH_CHECK("k_gemm2");
     return SWARM_OK;

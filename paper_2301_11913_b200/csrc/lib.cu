@@ -1,5 +1,6 @@
 // Library-wide state of libswarm_b200.so: per-thread error text and the
 // launch counter bench.py reports as gpu_launches.
+#include <cstdlib>
 #include <string>
 
 #include "common.cuh"
@@ -12,6 +13,27 @@ std::atomic<uint64_t> g_launches{0};
 }  // namespace
 
 void set_error(const std::string& msg) { g_last_error = msg; }
+
+bool pdl_enabled() {
+    static const bool on = [] {
+        const char* e = getenv("SWARM_PDL");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
+
+namespace {
+// Busy-wait on the global timer (one thread): keeps a stream occupied so the
+// kernels a host thread issues behind it queue up back to back.
+__global__ void k_spin(uint64_t ns) {
+    uint64_t t0, t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+    do {
+        __nanosleep(1000);
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    } while (t - t0 < ns);
+}
+}  // namespace
 std::atomic<uint64_t>& launch_counter() { return g_launches; }
 
 }  // namespace swarm
@@ -21,5 +43,11 @@ extern "C" {
 const char* swarm_last_error(void) { return swarm::g_last_error.c_str(); }
 int swarm_version(void) { return 1; }
 uint64_t swarm_launch_count(void) { return swarm::launch_counter().load(); }
+
+int swarm_gpu_spin(uint64_t ns, swarm_stream_t stream) {
+    swarm::k_spin<<<1, 1, 0, swarm::as_stream(stream)>>>(ns);
+    SWARM_LAUNCH_CHECK("k_spin");
+    return SWARM_OK;
+}
 
 }  // extern "C"

@@ -260,11 +260,41 @@ __global__ void __launch_bounds__(kLnThreads) k_ln_bwd(const T* __restrict__ dy,
 
 __global__ void k_col_reduce(const float* __restrict__ part, int nparts, int cols, float* __restrict__ out,
                              int accumulate) {
+    pdl_trigger();
+    pdl_wait();
     const int c = blockIdx.x * blockDim.x + threadIdx.x;
     if (c >= cols) return;
     float s = 0.f;
     for (int p = 0; p < nparts; ++p) s += part[static_cast<size_t>(p) * cols + c];
     out[c] = accumulate ? out[c] + s : s;
+}
+
+// Sum of nparts rows of two [nparts, cols] partial arrays (gain and bias
+// gradients) in one launch: CTA = 32 columns x 8 warps, warp w sums parts
+// w, w+8, ... (coalesced 128-B rows), then the 8 warp sums meet in smem in a
+// fixed order (deterministic).  blockIdx.y selects the array.
+__global__ void __launch_bounds__(256) k_col_reduce2(const float* __restrict__ part_g, const float* __restrict__ part_b,
+                                                     int nparts, int cols, float* __restrict__ out_g,
+                                                     float* __restrict__ out_b, int accumulate) {
+    pdl_trigger();
+    pdl_wait();
+    __shared__ float red[8][33];
+    const float* part = blockIdx.y ? part_b : part_g;
+    float* out = blockIdx.y ? out_b : out_g;
+    if (!out) return;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int c = blockIdx.x * 32 + lane;
+    float s = 0.f;
+    if (c < cols)
+        for (int p = w; p < nparts; p += 8) s += part[static_cast<size_t>(p) * cols + c];
+    red[w][lane] = s;
+    __syncthreads();
+    if (w == 0 && c < cols) {
+        float t = 0.f;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) t += red[k][lane];
+        out[c] = accumulate ? out[c] + t : t;
+    }
 }
 
 // fp64 API path: one CTA per row, three passes over global, verbatim formula.
@@ -334,6 +364,19 @@ __device__ __forceinline__ uint4 pack8(const float* v) {
     }
     return make_uint4(w[0], w[1], w[2], w[3]);
 }
+
+// 8 consecutive fp32 (16-B aligned) or `dflt` when p is null
+__device__ __forceinline__ void load8f(const float* __restrict__ p, int c0, float dflt, float (&v)[8]) {
+    if (!p) {
+#pragma unroll
+        for (int j = 0; j < 8; ++j) v[j] = dflt;
+        return;
+    }
+    const float4 a = __ldg(reinterpret_cast<const float4*>(p + c0));
+    const float4 b = __ldg(reinterpret_cast<const float4*>(p + c0) + 1);
+    v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w;
+    v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
+}
 __device__ __forceinline__ float wsum(float v) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
@@ -344,6 +387,8 @@ template <int NV>
 __global__ void __launch_bounds__(256) k_ln_fwd_w(const uint4* __restrict__ x, int rows, const float* __restrict__ g,
                                                   const float* __restrict__ b, float eps, uint4* __restrict__ out,
                                                   float* __restrict__ mean_out, float* __restrict__ rstd_out) {
+    pdl_trigger();
+    pdl_wait();
     constexpr int C8 = 32 * NV;
     const int lane = threadIdx.x & 31;
     const int warps = (gridDim.x * blockDim.x) >> 5;
@@ -366,12 +411,11 @@ __global__ void __launch_bounds__(256) k_ln_fwd_w(const uint4* __restrict__ x, i
         for (int i = 0; i < NV; ++i) {
             const int c0 = (lane + 32 * i) * 8;
             float o[8];
+            float gv[8], bv[8];
+            load8f(g, c0, 1.f, gv);  // 2 x 16-B loads (scalar loads here were the kernel's bottleneck)
+            load8f(b, c0, 0.f, bv);
 #pragma unroll
-            for (int j = 0; j < 8; ++j) {
-                o[j] = (v[8 * i + j] - mean) * rstd;
-                if (g) o[j] *= g[c0 + j];
-                if (b) o[j] += b[c0 + j];
-            }
+            for (int j = 0; j < 8; ++j) o[j] = (v[8 * i + j] - mean) * rstd * gv[j] + bv[j];
             orow[lane + 32 * i] = pack8(o);
         }
         if (lane == 0) {
@@ -387,6 +431,8 @@ __global__ void __launch_bounds__(256) k_ln_bwd_dx_w(const uint4* __restrict__ d
                                                      const float* __restrict__ g, const float* __restrict__ mean,
                                                      const float* __restrict__ rstd, const uint4* __restrict__ dres,
                                                      uint4* __restrict__ dx) {
+    pdl_trigger();
+    pdl_wait();
     constexpr int C8 = 32 * NV;
     constexpr bool KEEP = NV <= 8;  // keep the row in registers, else re-read it (L1/L2 hits)
     const int lane = threadIdx.x & 31;
@@ -403,10 +449,12 @@ __global__ void __launch_bounds__(256) k_ln_bwd_dx_w(const uint4* __restrict__ d
             unpack8(x[base + lane + 32 * i], xv);
             unpack8(dy[base + lane + 32 * i], dv);
             const int c0 = (lane + 32 * i) * 8;
+            float gv[8];
+            load8f(g, c0, 1.f, gv);
 #pragma unroll
             for (int j = 0; j < 8; ++j) {
                 const float h = (xv[j] - mu) * rs;
-                const float q = g ? dv[j] * g[c0 + j] : dv[j];
+                const float q = dv[j] * gv[j];
                 s1 += q * h;
                 s2 += q;
                 if constexpr (KEEP) {
@@ -424,14 +472,14 @@ __global__ void __launch_bounds__(256) k_ln_bwd_dx_w(const uint4* __restrict__ d
 #pragma unroll
                 for (int j = 0; j < 8; ++j) o[j] = rs * (gy[8 * i + j] - c2 - xh[8 * i + j] * c1);
             } else {
-                float xv[8], dv[8];
+                float xv[8], dv[8], gv[8];
                 unpack8(x[base + lane + 32 * i], xv);
                 unpack8(dy[base + lane + 32 * i], dv);
+                load8f(g, c0, 1.f, gv);
 #pragma unroll
                 for (int j = 0; j < 8; ++j) {
                     const float h = (xv[j] - mu) * rs;
-                    const float q = g ? dv[j] * g[c0 + j] : dv[j];
-                    o[j] = rs * (q - c2 - h * c1);
+                    o[j] = rs * (dv[j] * gv[j] - c2 - h * c1);
                 }
             }
             if (dres) {
@@ -451,6 +499,8 @@ __global__ void __launch_bounds__(256) k_ln_bwd_dgb(const uint4* __restrict__ dy
                                                     int cols, const float* __restrict__ mean,
                                                     const float* __restrict__ rstd, int rows_per_split,
                                                     float* __restrict__ part_g, float* __restrict__ part_b) {
+    pdl_trigger();
+    pdl_wait();
     __shared__ float sg[32][65], sb[32][65];
     const int cv = threadIdx.x & 7, rl = threadIdx.x >> 3;
     const int c8 = blockIdx.x * 8 + cv;  // column vector
@@ -490,17 +540,17 @@ template <int NV>
 void ln_fwd_w(const __nv_bfloat16* x, int rows, const float* g, const float* b, float eps, __nv_bfloat16* out,
               float* mean, float* rstd, cudaStream_t st) {
     const unsigned grid = static_cast<unsigned>(std::min((rows + 7) / 8, 148 * 8));
-    k_ln_fwd_w<NV><<<grid, 256, 0, st>>>(reinterpret_cast<const uint4*>(x), rows, g, b, eps,
-                                         reinterpret_cast<uint4*>(out), mean, rstd);
+    launch_pdl(k_ln_fwd_w<NV>, dim3(grid), dim3(256), 0, st, reinterpret_cast<const uint4*>(x), rows, g, b, eps,
+               reinterpret_cast<uint4*>(out), mean, rstd);
 }
 
 template <int NV>
 void ln_bwd_dx_w(const __nv_bfloat16* dy, const __nv_bfloat16* x, int rows, const float* g, const float* mean,
                  const float* rstd, const __nv_bfloat16* dres, __nv_bfloat16* dx, cudaStream_t st) {
     const unsigned grid = static_cast<unsigned>(std::min((rows + 7) / 8, 148 * 8));
-    k_ln_bwd_dx_w<NV><<<grid, 256, 0, st>>>(reinterpret_cast<const uint4*>(dy), reinterpret_cast<const uint4*>(x), rows,
-                                            g, mean, rstd, reinterpret_cast<const uint4*>(dres),
-                                            reinterpret_cast<uint4*>(dx));
+    launch_pdl(k_ln_bwd_dx_w<NV>, dim3(grid), dim3(256), 0, st, reinterpret_cast<const uint4*>(dy),
+               reinterpret_cast<const uint4*>(x), rows, g, mean, rstd, reinterpret_cast<const uint4*>(dres),
+               reinterpret_cast<uint4*>(dx));
 }
 
 bool warp_ln_ok(int cols) { return cols % 256 == 0 && cols <= 4096 && (cols / 256) <= 16; }
@@ -522,7 +572,7 @@ template <typename T>
 int ln_fwd_launch(const T* x, int rows, int cols, const float* g, const float* b, float eps, T* out, float* mean,
                   float* rstd, cudaStream_t st) {
     if constexpr (sizeof(T) == 2) {
-        if (warp_ln_ok(cols) && al(x, 16) && al(out, 16) &&
+        if (warp_ln_ok(cols) && al(x, 16) && al(out, 16) && (!g || al(g, 16)) && (!b || al(b, 16)) &&
             dispatch_nv(cols / 256, [&](auto nv) { ln_fwd_w<decltype(nv)::value>(x, rows, g, b, eps, out, mean, rstd, st); })) {
             SWARM_LAUNCH_CHECK("k_ln_fwd_w");
             return SWARM_OK;
@@ -544,7 +594,7 @@ template <typename T>
 int ln_bwd_launch(const T* dy, const T* x, int rows, int cols, const float* g, const float* mean, const float* rstd,
                   const T* dres, T* dx, float* dg, float* db, int accumulate, float* ws, cudaStream_t st) {
     if constexpr (sizeof(T) == 2) {
-        if (warp_ln_ok(cols) && al(x, 16) && al(dy, 16) && al(dx, 16) && (!dres || al(dres, 16)) &&
+        if (warp_ln_ok(cols) && al(x, 16) && al(dy, 16) && al(dx, 16) && (!dres || al(dres, 16)) && (!g || al(g, 16)) &&
             dispatch_nv(cols / 256, [&](auto nv) {
                 ln_bwd_dx_w<decltype(nv)::value>(dy, x, rows, g, mean, rstd, dres, dx, st);
             })) {
@@ -554,19 +604,13 @@ int ln_bwd_launch(const T* dy, const T* x, int rows, int cols, const float* g, c
                 const int rps = (rows + splits - 1) / splits;
                 float* pg = ws;
                 float* pb = ws + static_cast<size_t>(splits) * cols;
-                k_ln_bwd_dgb<<<dim3((cols + 63) / 64, splits), 256, 0, st>>>(
-                    reinterpret_cast<const uint4*>(dy), reinterpret_cast<const uint4*>(x), rows, cols, mean, rstd, rps,
-                    pg, pb);
+                launch_pdl(k_ln_bwd_dgb, dim3((cols + 63) / 64, splits), dim3(256), 0, st,
+                           reinterpret_cast<const uint4*>(dy), reinterpret_cast<const uint4*>(x), rows, cols, mean,
+                           rstd, rps, pg, pb);
                 SWARM_LAUNCH_CHECK("k_ln_bwd_dgb");
-                const unsigned cg = static_cast<unsigned>((cols + 255) / 256);
-                if (dg) {
-                    k_col_reduce<<<cg, 256, 0, st>>>(pg, splits, cols, dg, accumulate);
-                    SWARM_LAUNCH_CHECK("k_col_reduce");
-                }
-                if (db) {
-                    k_col_reduce<<<cg, 256, 0, st>>>(pb, splits, cols, db, accumulate);
-                    SWARM_LAUNCH_CHECK("k_col_reduce");
-                }
+                launch_pdl(k_col_reduce2, dim3((cols + 31) / 32, 2), dim3(256), 0, st, pg, pb, splits, cols, dg, db,
+                           accumulate);
+                SWARM_LAUNCH_CHECK("k_col_reduce2");
             }
             return SWARM_OK;
         }

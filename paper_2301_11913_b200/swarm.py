@@ -251,6 +251,7 @@ class SwarmPipeline:
         self.replayed_kernels = 0
         self._warm: set = set()
         self._profiled: set = set()
+        self.prof_spin_ns = 0  # >0: profiled visits start behind a GPU spin of this length
         probe = next(iter(self.stages.values()), None) or self._new_stage(0, slots=1)
         self.wire_bytes = probe.wire_bytes
         tokens = mcfg.tokens
@@ -389,6 +390,9 @@ class SwarmPipeline:
         if eager_prof or not self.use_graphs or (s, kind) not in self._warm:
             st = self.stages[s]
             if eager_prof:
+                if self.prof_spin_ns:  # let the host run ahead: kernels queue back to back
+                    L.check(L.lib().swarm_gpu_spin(int(self.prof_spin_ns), torch.cuda.current_stream().cuda_stream),
+                            "gpu_spin")
                 st.profile(True)
                 self._profiled.add((s, kind))
             fn()
