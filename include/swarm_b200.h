@@ -158,7 +158,8 @@ typedef struct {
 int swarm_gemm_bf16(const swarm_gemm_args* args, swarm_stream_t stream);
 size_t swarm_gemm_workspace_bytes(void);
 /* resident 2-CTA clusters of the 256x256 pair kernel on the current device (its
-   persistent grid size; below SMs / 2 when GPCs strand SMs) */
+   persistent grid size; below SMs / 2 when GPCs strand SMs); 4-CTA clusters
+   for the multicast variant (the default; SWARM_GEMM_MCAST=0 selects pairs) */
 int swarm_gemm_pair_clusters(void);
 
 /* ---- training building blocks (stage executor internals, exported for tests)

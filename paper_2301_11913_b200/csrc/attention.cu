@@ -2,19 +2,23 @@
 //
 // Forward:  P[z, i, :] = softmax(scale * Q_z[i] K_z^T)        (causal optional)
 // Backward: dS[z, i, :] = scale * P (dP - rowsum(P * dP)),  dP = dO_z[i] V_z^T
-// for z = b*H + h.  One CTA owns 128 query rows of one (b, h): the full
-// 128 x L score block (L <= 512) is accumulated in TMEM (up to all 512
-// columns), so the softmax (or its gradient) is applied straight out of TMEM
-// and only the bf16 probabilities / score gradients reach HBM — no fp32 S or
-// dP round trip and no separate softmax kernel (csrc/train_ops.cu keeps the
-// unfused kernels for reference/tests).  The reference has no attention at all
-// (SPEC:90 folds it into 6*P*T); parity is against the fp64 block oracle.
+// for z = b*H + h.  One CTA owns 128 query rows of one (b, h) and streams the
+// keys in 64-wide chunks: a 3-stage TMA ring of K (or V) chunks feeds
+// tcgen05.mma (M=128, N=64) into two 64-column TMEM accumulators, so the MMA
+// of chunk j+1 overlaps the softmax of chunk j.  Two passes over the chunks:
+// pass 0 gathers the row statistics (online max / sum for the forward,
+// rowsum(P * dP) for the backward), pass 1 recomputes each chunk's scores and
+// writes the bf16 probabilities (score gradients) with TMA stores.  Recomputing
+// the 128 x 64 x d_head product is cheaper than keeping 128 x L scores resident,
+// and the small footprint (~99 KB smem, 128 TMEM columns) puts two CTAs on every
+// SM, so one CTA's softmax overlaps the other's loads and MMAs.  No fp32 score
+// matrix and no separate softmax kernel (csrc/train_ops.cu keeps the unfused
+// kernels for reference/tests).  The reference has no attention at all (SPEC:90
+// folds it into 6*P*T); parity is against the fp64 block oracle.
 //
-// Warp roles: warp 0 TMA (Q/dO block, K/V rows, and in the backward the P block
-// after the MMAs), warp 1 MMA issuer, warp 2 TMEM allocator; then all 8 warps
-// run the softmax epilogue (one row per thread, key columns split between warps
-// 4-7 and 0-3, row statistics combined through smem), staged through swizzled
-// smem and written with TMA stores.
+// Warp roles: warp 0 TMA, warp 1 MMA issuer, warp 2 TMEM allocator, warps 4-7
+// one query row per thread (TMEM lane quarter = warp % 4).  CTAs are ordered
+// heaviest first (causal: the last query blocks see the most keys).
 #include <cudaTypedefs.h>
 
 #include <algorithm>
@@ -29,24 +33,25 @@ namespace attn {
 using namespace swarm::sm100;
 
 constexpr int kThreads = 256;
-constexpr int BQ = 128;      // query rows per CTA
-constexpr int kMaxL = 512;   // TMEM columns
-constexpr int kMaxDh = 128;  // K extent of the score GEMM (2 x 64-wide k-blocks)
-constexpr int kSlot = 4096;
+constexpr int BQ = 128;        // query rows per CTA
+constexpr int BKV = 64;        // keys per chunk (MMA N)
+constexpr int kStages = 3;     // K / V chunk ring
+constexpr int kMaxL = 1024;
+constexpr int kMaxDh = 128;    // K extent of the score GEMM (<= 2 x 64-wide boxes)
+constexpr int kSlot = 2048;    // one 32 x 32 bf16 staging box
 
 struct Params {
     int B, H, L, dh, causal;
     int a_col0, b_col0;  // column of head 0 in the A / B storages
     float scale;
+    const __nv_bfloat16* p_in;  // backward: P [B*H*L, L]
 };
 
-// smem: A [dh/64][128 x 64] bf16 | B [dh/64][L x 64] bf16 (reused for the P tile
-// in the backward) | staging 8 warps x 2 x 4 KB | barriers
-constexpr int kABytes = (kMaxDh / 64) * BQ * 64 * 2;       // 32 KB
-constexpr int kBBytes = (kMaxDh / 64) * kMaxL * 64 * 2;    // 128 KB (>= the 128 x 512 P tile)
-constexpr int kStgBytes = 8 * 2 * kSlot;                   // 64 KB: 8 warps x double buffer
-constexpr int kSmem = kABytes + kBBytes + kStgBytes + 1024 + 128;
-static_assert(kSmem <= 232448, "attention kernel exceeds 227 KB smem");
+constexpr int kABytes = (kMaxDh / 64) * BQ * 128;       // 32 KB: Q / dO block
+constexpr int kChunkBytes = (kMaxDh / 64) * BKV * 128;  // 16 KB: K / V chunk
+constexpr int kStgBytes = 4 * 2 * kSlot + kSlot;        // 4 row warps x 2 slots + a zero box
+constexpr int kSmem = kABytes + kStages * kChunkBytes + kStgBytes + 1024 + 256;
+static_assert(2 * (kSmem + 1024) <= 233472, "two attention CTAs must fit one SM");
 
 // 2^x on the SFU (ex2.approx.ftz: 2 ulp; the probabilities are rounded to bf16 anyway)
 __device__ __forceinline__ float fast_exp2(float x) {
@@ -60,7 +65,8 @@ __device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
     return *reinterpret_cast<const uint32_t*>(&p);
 }
 
-__device__ __forceinline__ void stage_bf16(uint8_t* slot, int row, const float (&v)[32]) {
+// 32 x 32 bf16 box, SWIZZLE_64B (16-B chunk j of row r at j ^ ((r >> 1) & 3))
+__device__ __forceinline__ void stage_bf16(uint8_t* slot, int row, const float* v) {
     const uint32_t base = smem_u32(slot) + row * 64;
 #pragma unroll
     for (int j = 0; j < 4; ++j)
@@ -69,62 +75,64 @@ __device__ __forceinline__ void stage_bf16(uint8_t* slot, int row, const float (
                      pack_bf16(v[8 * j + 6], v[8 * j + 7]));
 }
 
-// P tile in smem: [L/64 boxes][128 rows x 128 B], SWIZZLE_128B: 16-B chunk j of
-// row r at j ^ (r & 7).  Returns 32 consecutive P values of row r from column c0.
-__device__ __forceinline__ void load_p32(const uint8_t* ptile, int r, int c0, float (&p)[32]) {
-    const uint8_t* box = ptile + (c0 >> 6) * (BQ * 128);
-    const uint32_t rowbase = smem_u32(box) + r * 128;
-    const int j0 = (c0 & 63) >> 3;  // first 16-B chunk inside the 128-B row
+// 64 consecutive bf16 of one P row (128 B, 16-B aligned) as floats
+__device__ __forceinline__ void load_p64(const __nv_bfloat16* src, float (&p)[64]) {
+    const uint4* s4 = reinterpret_cast<const uint4*>(src);
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
-        uint32_t w0, w1, w2, w3;
-        asm volatile("ld.shared.v4.b32 {%0,%1,%2,%3}, [%4];"
-                     : "=r"(w0), "=r"(w1), "=r"(w2), "=r"(w3)
-                     : "r"(rowbase + (((j0 + q) ^ (r & 7)) << 4)));
-        const uint32_t w[4] = {w0, w1, w2, w3};
+    for (int q = 0; q < 8; ++q) {
+        const uint4 w = __ldg(s4 + q);
+        const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
-            p[q * 8 + 2 * k] = __uint_as_float(w[k] << 16);
-            p[q * 8 + 2 * k + 1] = __uint_as_float(w[k] & 0xffff0000u);
+            p[q * 8 + 2 * k] = __uint_as_float(ws[k] << 16);
+            p[q * 8 + 2 * k + 1] = __uint_as_float(ws[k] & 0xffff0000u);
         }
     }
 }
 
 template <bool BWD>
-__global__ void __launch_bounds__(kThreads, 1)
-    k_attn_rows(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUtensorMap tma_b,
-                const __grid_constant__ CUtensorMap tma_p_in, const __grid_constant__ CUtensorMap tma_out,
-                const Params p) {
+__global__ void __launch_bounds__(kThreads, 2)
+    k_attn_chunks(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUtensorMap tma_b,
+                  const __grid_constant__ CUtensorMap tma_out, const Params p) {
     pdl_trigger();
     extern __shared__ uint8_t smem_raw[];
     const uint32_t raw = smem_u32(smem_raw);
     uint8_t* smem = smem_raw + ((1024 - (raw & 1023)) & 1023);
     uint8_t* sa = smem;
-    uint8_t* sb = smem + kABytes;
-    uint8_t* stg_all = sb + kBBytes;
-    uint64_t* bar_ab = reinterpret_cast<uint64_t*>(stg_all + kStgBytes);
-    uint64_t* bar_mma = bar_ab + 1;
-    uint64_t* bar_p = bar_ab + 2;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar_ab + 3);
+    uint8_t* sb = sa + kABytes;
+    uint8_t* stg_all = sb + kStages * kChunkBytes;
+    uint8_t* zero_box = stg_all + 4 * 2 * kSlot;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(stg_all + kStgBytes);
+    uint64_t* qfull = bars;
+    uint64_t* full = bars + 1;
+    uint64_t* empty = full + kStages;
+    uint64_t* sfull = empty + kStages;
+    uint64_t* sempty = sfull + 2;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sempty + 2);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int nqb = p.L / BQ;
-    const int z = blockIdx.x / nqb, mt = blockIdx.x - z * nqb;
+    const int nqb = p.L / BQ, nz = p.B * p.H;
+    const int mt = nqb - 1 - static_cast<int>(blockIdx.x) / nz;  // heaviest query blocks first
+    const int z = static_cast<int>(blockIdx.x) % nz;
     const int zb = z / p.H, zh = z - zb * p.H;
-    const int kblocks = p.dh / 64;
-    const int nmma = p.L < 256 ? p.L : 256;  // MMA N per instruction
-    // causal: keys beyond the last query row of this block are fully masked
-    const int kv_len = p.causal ? min(p.L, (mt + 1) * BQ) : p.L;
-    const int n_halves = (kv_len + nmma - 1) / nmma;
+    const int kboxes = p.dh / 64;
+    const int kv_len = p.causal ? (mt + 1) * BQ : p.L;  // keys past the block's last query are masked
+    const int nch = kv_len / BKV;
 
     if (warp == 0 && lane == 0) {
-        mbar_init(bar_ab, 1);
-        mbar_init(bar_mma, 1);
-        mbar_init(bar_p, 1);
+        mbar_init(qfull, 1);
+        for (int s = 0; s < kStages; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], 1);
+        }
+        for (int b = 0; b < 2; ++b) {
+            mbar_init(&sfull[b], 1);
+            mbar_init(&sempty[b], 4);
+        }
         fence_barrier_init();
     }
     if (warp == 2) {
-        tmem_alloc(tmem_slot, 512);
+        tmem_alloc(tmem_slot, 2 * BKV);
         tmem_relinquish();
     }
     tc_fence_before();
@@ -137,156 +145,183 @@ __global__ void __launch_bounds__(kThreads, 1)
         // ------------------------------------------------------------ TMA
         const int arow = zb * p.L + mt * BQ, acol = p.a_col0 + zh * p.dh;
         const int brow = zb * p.L, bcol = p.b_col0 + zh * p.dh;
-        const uint32_t bytes = kblocks * (BQ * 128 + n_halves * nmma * 128);
-        mbar_arrive_expect_tx(bar_ab, bytes);
-        for (int kb = 0; kb < kblocks; ++kb) {
-            tma_load_2d(sa + kb * BQ * 128, &tma_a, bar_ab, acol + kb * 64, arow);
-            for (int h = 0; h < n_halves; ++h)
-                tma_load_2d(sb + kb * (kMaxL * 128) + h * nmma * 128, &tma_b, bar_ab, bcol + kb * 64, brow + h * nmma);
-        }
-        if constexpr (BWD) {
-            // after the MMAs have consumed B, bring the P block into the same space
-            mbar_wait(bar_mma, 0);
-            mbar_arrive_expect_tx(bar_p, (kv_len / 64) * BQ * 128);
-            for (int c = 0; c < kv_len / 64; ++c)
-                tma_load_2d(sb + c * BQ * 128, &tma_p_in, bar_p, c * 64, z * p.L + mt * BQ);
-        }
+        mbar_arrive_expect_tx(qfull, kboxes * BQ * 128);
+        for (int kb = 0; kb < kboxes; ++kb) tma_load_2d(sa + kb * BQ * 128, &tma_a, qfull, acol + kb * 64, arow);
+        int stage = 0;
+        uint32_t phase = 0;
+        for (int pass = 0; pass < 2; ++pass)
+            for (int j = 0; j < nch; ++j) {
+                mbar_wait(&empty[stage], phase ^ 1);
+                mbar_arrive_expect_tx(&full[stage], kboxes * BKV * 128);
+                for (int kb = 0; kb < kboxes; ++kb)
+                    tma_load_2d(sb + stage * kChunkBytes + kb * BKV * 128, &tma_b, &full[stage], bcol + kb * 64,
+                                brow + j * BKV);
+                if (++stage == kStages) {
+                    stage = 0;
+                    phase ^= 1;
+                }
+            }
     } else if (warp == 1 && lane == 0) {
         // ------------------------------------------------------------ MMA
-        mbar_wait(bar_ab, 0);
-        tc_fence_after();
-        const uint32_t idesc = make_idesc_bf16(BQ, nmma, false, false);
-        for (int kb = 0; kb < kblocks; ++kb) {
-            const uint32_t a_base = smem_u32(sa + kb * BQ * 128);
-#pragma unroll
-            for (int k = 0; k < 4; ++k) {
-                const uint64_t ad = make_sdesc(a_base + k * 32, 16, 1024);
-                for (int h = 0; h < n_halves; ++h) {
-                    const uint32_t b_base = smem_u32(sb + kb * (kMaxL * 128) + h * nmma * 128);
-                    const uint64_t bd = make_sdesc(b_base + k * 32, 16, 1024);
-                    mma_bf16(tmem + h * nmma, ad, bd, idesc, (kb | k) != 0 ? 1u : 0u);
+        constexpr uint32_t idesc = make_idesc_bf16(BQ, BKV, false, false);
+        mbar_wait(qfull, 0);
+        int stage = 0, buf = 0;
+        uint32_t phase = 0, bphase = 0;
+        const int ksteps = p.dh / 16;
+        for (int pass = 0; pass < 2; ++pass)
+            for (int j = 0; j < nch; ++j) {
+                mbar_wait(&full[stage], phase);
+                mbar_wait(&sempty[buf], bphase ^ 1);
+                tc_fence_after();
+                const uint32_t a_base = smem_u32(sa), b_base = smem_u32(sb + stage * kChunkBytes);
+                for (int kk = 0; kk < ksteps; ++kk) {
+                    const uint64_t ad = make_sdesc(a_base + (kk >> 2) * (BQ * 128) + (kk & 3) * 32, 16, 1024);
+                    const uint64_t bd = make_sdesc(b_base + (kk >> 2) * (BKV * 128) + (kk & 3) * 32, 16, 1024);
+                    mma_bf16(tmem + buf * BKV, ad, bd, idesc, kk != 0 ? 1u : 0u);
+                }
+                mma_commit(&empty[stage]);
+                mma_commit(&sfull[buf]);
+                if (++stage == kStages) {
+                    stage = 0;
+                    phase ^= 1;
+                }
+                if (++buf == 2) {
+                    buf = 0;
+                    bphase ^= 1;
                 }
             }
-        }
-        mma_commit(bar_mma);
-    }
-    __syncwarp();  // lanes of warps 0/1 re-converge after their single-thread roles
-    {
-        // ------------------------------------------------------------ softmax epilogue
-        // All 8 warps: warp w owns TMEM lane quarter w % 4 (32 rows, one per
-        // thread); warps 4-7 take the first half of the key chunks, warps 0-3 the
-        // second half (and the all-masked tail); row statistics meet in smem.
-        // row statistics live in the A (Q / dO) tile, dead once the MMAs completed
-        float (*st_a)[BQ] = reinterpret_cast<float (*)[BQ]>(sa);
-        float (*st_b)[BQ] = reinterpret_cast<float (*)[BQ]>(sa + 2 * BQ * sizeof(float));
-        const int q = warp & 3;
-        const int grp = warp >= 4 ? 0 : 1;
-        const int r = q * 32 + lane;            // row inside the block
-        const int qi = mt * BQ + r;             // query position in the sequence
-        const int valid = p.causal ? qi + 1 : p.L;
+    } else if (warp >= 4) {
+        // ------------------------------------------------------------ one query row per thread
+        const int q = warp - 4;
+        const int r = q * 32 + lane;
+        const int qi = mt * BQ + r;
+        const int valid = p.causal ? qi + 1 : p.L;  // columns < valid are unmasked
         const uint32_t trow = tmem + (static_cast<uint32_t>(q * 32) << 16);
-        uint8_t* stg = stg_all + (warp & 7) * 2 * kSlot;  // two 4 KB slots per warp
+        uint8_t* stg = stg_all + q * 2 * kSlot;
         int slot_idx = 0;
         const int out_row = z * p.L + mt * BQ + q * 32;
-        const int n32 = kv_len / 32;
-        const int split = (n32 / 2) * 32;
-        const int c_lo = grp == 0 ? 0 : split, c_hi = grp == 0 ? split : kv_len;
-        mbar_wait(bar_mma, 0);
-        tc_fence_after();
-        const float l2e = 1.4426950408889634f;
-        float stat_a = 0.f, stat_b = 0.f;  // fwd: row max / 1/sum; bwd: rowsum(P*dP)
-        if constexpr (!BWD) {
-            float m = -INFINITY, s = 0.f;
-            for (int c0 = c_lo; c0 < c_hi; c0 += 64) {
-                uint32_t ra[32], rb[32];
-                tmem_ld_32x32b_x32(trow + c0, ra);
-                tmem_ld_32x32b_x32(trow + c0 + 32, rb);
-                tmem_ld_wait();
-                float cm = -INFINITY;
-#pragma unroll
-                for (int j = 0; j < 32; ++j) {
-                    if (c0 + j < valid) cm = fmaxf(cm, __uint_as_float(ra[j]));
-                    if (c0 + 32 + j < valid) cm = fmaxf(cm, __uint_as_float(rb[j]));
-                }
-                const float nm = fmaxf(m, cm * p.scale);
-                if (nm != -INFINITY) {
-                    float add = 0.f;
-#pragma unroll
-                    for (int j = 0; j < 32; ++j) {
-                        if (c0 + j < valid) add += fast_exp2((__uint_as_float(ra[j]) * p.scale - nm) * l2e);
-                        if (c0 + 32 + j < valid) add += fast_exp2((__uint_as_float(rb[j]) * p.scale - nm) * l2e);
-                    }
-                    s = (m == -INFINITY ? 0.f : s * fast_exp2((m - nm) * l2e)) + add;
-                    m = nm;
-                }
-            }
-            st_a[grp][r] = m;
-            st_b[grp][r] = s;
-            asm volatile("bar.sync 1, 256;" ::: "memory");
-            const float m0 = st_a[0][r], m1 = st_a[1][r];
-            const float mm = fmaxf(m0, m1);
-            const float ss = (m0 == -INFINITY ? 0.f : st_b[0][r] * fast_exp2((m0 - mm) * l2e)) +
-                             (m1 == -INFINITY ? 0.f : st_b[1][r] * fast_exp2((m1 - mm) * l2e));
-            stat_a = mm;
-            stat_b = 1.f / ss;
-        } else {
-            mbar_wait(bar_p, 0);
-            float acc = 0.f;
-            for (int c0 = c_lo; c0 < c_hi; c0 += 32) {
-                uint32_t rr[32];
-                tmem_ld_32x32b_x32(trow + c0, rr);
-                tmem_ld_wait();
-                float pv[32];
-                load_p32(sb, r, c0, pv);
-#pragma unroll
-                for (int j = 0; j < 32; ++j) acc += pv[j] * __uint_as_float(rr[j]);
-            }
-            st_a[grp][r] = acc;
-            asm volatile("bar.sync 1, 256;" ::: "memory");
-            stat_a = st_a[0][r] + st_a[1][r];
+        const __nv_bfloat16* prow = BWD ? p.p_in + (static_cast<size_t>(z) * p.L + mt * BQ + r) * p.L : nullptr;
+        if (q == 0) {  // the zero box written for fully masked key chunks
+            for (int i = lane; i < kSlot / 16; i += 32) st_shared_v4(smem_u32(zero_box) + i * 16, 0, 0, 0, 0);
+            fence_async_smem();
         }
-        // second pass: normalise (fwd) / form dS (bwd); masked / skipped columns write 0
-        const int w_hi = grp == 0 ? c_hi : p.L;
-        for (int c0 = c_lo; c0 < w_hi; c0 += 32) {
-            float v[32];
-            if (c0 < kv_len) {
-                uint32_t rr[32];
-                tmem_ld_32x32b_x32(trow + c0, rr);
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+        const float l2e = 1.4426950408889634f;
+        int buf = 0;
+        uint32_t bphase = 0;
+        float stat_a = 0.f, stat_b = 0.f;  // fwd: row max (scaled) / 1 / sum; bwd: rowsum(P * dP)
+        // ---------------- pass 0: row statistics
+        {
+            float m = -INFINITY, l = 0.f, acc = 0.f;
+            for (int j = 0; j < nch; ++j) {
+                uint32_t ra[32], rb[32];
+                mbar_wait(&sfull[buf], bphase);
+                tc_fence_after();
+                tmem_ld_32x32b_x32(trow + buf * BKV, ra);
+                tmem_ld_32x32b_x32(trow + buf * BKV + 32, rb);
                 tmem_ld_wait();
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&sempty[buf]);
+                if (++buf == 2) {
+                    buf = 0;
+                    bphase ^= 1;
+                }
+                const int c0 = j * BKV;
                 if constexpr (!BWD) {
+                    float cm = -INFINITY;
 #pragma unroll
-                    for (int j = 0; j < 32; ++j)
-                        v[j] = (c0 + j < valid) ? fast_exp2((__uint_as_float(rr[j]) * p.scale - stat_a) * l2e) * stat_b
-                                                : 0.f;
+                    for (int jj = 0; jj < 32; ++jj) {
+                        if (c0 + jj < valid) cm = fmaxf(cm, __uint_as_float(ra[jj]));
+                        if (c0 + 32 + jj < valid) cm = fmaxf(cm, __uint_as_float(rb[jj]));
+                    }
+                    if (cm != -INFINITY) {
+                        const float nm = fmaxf(m, cm * p.scale);
+                        float add = 0.f;
+#pragma unroll
+                        for (int jj = 0; jj < 32; ++jj) {
+                            if (c0 + jj < valid) add += fast_exp2((__uint_as_float(ra[jj]) * p.scale - nm) * l2e);
+                            if (c0 + 32 + jj < valid)
+                                add += fast_exp2((__uint_as_float(rb[jj]) * p.scale - nm) * l2e);
+                        }
+                        l = (m == -INFINITY ? 0.f : l * fast_exp2((m - nm) * l2e)) + add;
+                        m = nm;
+                    }
                 } else {
-                    float pv[32];
-                    load_p32(sb, r, c0, pv);
+                    float pv[64];
+                    load_p64(prow + c0, pv);
 #pragma unroll
-                    for (int j = 0; j < 32; ++j) v[j] = p.scale * pv[j] * (__uint_as_float(rr[j]) - stat_a);
+                    for (int jj = 0; jj < 32; ++jj)
+                        acc += pv[jj] * __uint_as_float(ra[jj]) + pv[32 + jj] * __uint_as_float(rb[jj]);
+                }
+            }
+            stat_a = BWD ? acc : m;
+            stat_b = BWD ? 0.f : 1.f / l;
+        }
+        // ---------------- pass 1: probabilities / score gradients
+        for (int j = 0; j < nch; ++j) {
+            uint32_t ra[32], rb[32];
+            mbar_wait(&sfull[buf], bphase);
+            tc_fence_after();
+            tmem_ld_32x32b_x32(trow + buf * BKV, ra);
+            tmem_ld_32x32b_x32(trow + buf * BKV + 32, rb);
+            tmem_ld_wait();
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&sempty[buf]);
+            if (++buf == 2) {
+                buf = 0;
+                bphase ^= 1;
+            }
+            const int c0 = j * BKV;
+            float v[64];
+            if constexpr (!BWD) {
+#pragma unroll
+                for (int jj = 0; jj < 32; ++jj) {
+                    v[jj] = (c0 + jj < valid) ? fast_exp2((__uint_as_float(ra[jj]) * p.scale - stat_a) * l2e) * stat_b
+                                              : 0.f;
+                    v[32 + jj] = (c0 + 32 + jj < valid)
+                                     ? fast_exp2((__uint_as_float(rb[jj]) * p.scale - stat_a) * l2e) * stat_b
+                                     : 0.f;
                 }
             } else {
+                load_p64(prow + c0, v);
 #pragma unroll
-                for (int j = 0; j < 32; ++j) v[j] = 0.f;
+                for (int jj = 0; jj < 32; ++jj) {
+                    v[jj] = p.scale * v[jj] * (__uint_as_float(ra[jj]) - stat_a);
+                    v[32 + jj] = p.scale * v[32 + jj] * (__uint_as_float(rb[jj]) - stat_a);
+                }
             }
-            uint8_t* slot = stg + slot_idx * kSlot;
-            slot_idx ^= 1;
-            if (lane == 0) bulk_wait_read<1>();  // the store issued from this slot two chunks ago has read it
-            __syncwarp();
-            stage_bf16(slot, lane, v);
-            fence_async_smem();
-            __syncwarp();
-            if (lane == 0) {
-                tma_store_2d(&tma_out, slot, c0, out_row);
-                bulk_commit();
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                uint8_t* slot = stg + slot_idx * kSlot;
+                slot_idx ^= 1;
+                if (lane == 0) bulk_wait_read<1>();  // the store issued from this slot two boxes ago has read it
+                __syncwarp();
+                stage_bf16(slot, lane, v + 32 * h);
+                fence_async_smem();
+                __syncwarp();
+                if (lane == 0) {
+                    tma_store_2d(&tma_out, slot, c0 + 32 * h, out_row);
+                    bulk_commit();
+                }
             }
         }
-        if (lane == 0) bulk_wait_all();
+        // keys past the causal block: zeros (read by nothing on the hot path, but P / dS stay well defined)
+        if (lane == 0) {
+            for (int c0 = kv_len; c0 < p.L; c0 += 32) {
+                tma_store_2d(&tma_out, zero_box, c0, out_row);
+                bulk_commit();
+            }
+            bulk_wait_all();
+        }
+        __syncwarp();
     }
     tc_fence_before();
     __syncthreads();
     if (warp == 2) {
         tc_fence_after();
-        tmem_dealloc(tmem, 512);
+        tmem_dealloc(tmem, 2 * BKV);
     }
 }
 
@@ -365,25 +400,24 @@ template <bool BWD>
 int launch(const void* a, int lda, int a_cols, int a_col0, const void* b, int ldb, int b_cols, int b_col0,
            const void* pin, void* out, int B, int H, int L, int dh, float scale, int causal, cudaStream_t st) {
     if (L % BQ || L > kMaxL || dh % 64 || dh > kMaxDh || B <= 0 || H <= 0)
-        return invalid("attention: need L % 128 == 0, L <= 512, dh % 64 == 0, dh <= 128");
+        return invalid("attention: need L % 128 == 0, L <= 1024, dh % 64 == 0, dh <= 128");
+    if (BWD && (!pin || (reinterpret_cast<uintptr_t>(pin) & 15)))
+        return invalid("attention: P must be a 16-byte aligned bf16 [B*H*L, L] array");
     const long long T = static_cast<long long>(B) * L, rows_out = static_cast<long long>(B) * H * L;
-    const int nmma = L < 256 ? L : 256;
-    CUtensorMap ta, tb, tp{}, to;
+    CUtensorMap ta, tb, to;
     if (map_bf16(&ta, a, T, a_cols, lda, 64, BQ, CU_TENSOR_MAP_SWIZZLE_128B) ||
-        map_bf16(&tb, b, T, b_cols, ldb, 64, nmma, CU_TENSOR_MAP_SWIZZLE_128B) ||
+        map_bf16(&tb, b, T, b_cols, ldb, 64, BKV, CU_TENSOR_MAP_SWIZZLE_128B) ||
         map_bf16(&to, out, rows_out, L, L, 32, 32, CU_TENSOR_MAP_SWIZZLE_64B))
         return invalid("attention: tensor map encoding failed");
-    if (BWD && map_bf16(&tp, pin, rows_out, L, L, 64, BQ, CU_TENSOR_MAP_SWIZZLE_128B))
-        return invalid("attention: tensor map encoding failed (P)");
-    auto kern = k_attn_rows<BWD>;
+    auto kern = k_attn_chunks<BWD>;
     static bool attr = false;
     if (!attr) {
         SWARM_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem));
         attr = true;
     }
-    Params p{B, H, L, dh, causal, a_col0, b_col0, scale};
-    SWARM_CUDA_TRY(launch_pdl(kern, dim3(B * H * (L / BQ)), dim3(kThreads), kSmem, st, ta, tb, tp, to, p));
-    SWARM_LAUNCH_CHECK("k_attn_rows");
+    Params p{B, H, L, dh, causal, a_col0, b_col0, scale, static_cast<const __nv_bfloat16*>(pin)};
+    SWARM_CUDA_TRY(launch_pdl(kern, dim3(B * H * (L / BQ)), dim3(kThreads), kSmem, st, ta, tb, to, p));
+    SWARM_LAUNCH_CHECK("k_attn_chunks");
     return SWARM_OK;
 }
 

@@ -1005,32 +1005,39 @@ int launch_pair(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap&
 // this is below num_sms / 2 (GPCs with an odd number of usable SMs strand one
 // SM each), and a persistent grid larger than it runs its extra clusters as a
 // second wave — doubling a stream-K launch, whose clusters all get equal work.
+template <int NPAIR>
+int query_clusters() {
+    const int cap = num_sms() / (2 * NPAIR);
+    auto kern = k_gemm2<false, false, NPAIR>;
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg2::SMEM) != cudaSuccess) {
+        cudaGetLastError();
+        return cap;
+    }
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(2 * NPAIR * cap);
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = Cfg2::SMEM;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2 * NPAIR;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    int c = 0;
+    if (cudaOccupancyMaxActiveClusters(&c, kern, &cfg) != cudaSuccess || c <= 0) {
+        cudaGetLastError();
+        return cap;
+    }
+    return std::min(c, cap);
+}
+
 int max_pair_clusters() {
-    static const int n = [] {
-        const int cap = num_sms() / 2;
-        auto kern = k_gemm2<false, false, 1>;
-        if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg2::SMEM) != cudaSuccess) {
-            cudaGetLastError();
-            return cap;
-        }
-        cudaLaunchConfig_t cfg{};
-        cfg.gridDim = dim3(2 * cap);
-        cfg.blockDim = dim3(kThreads);
-        cfg.dynamicSmemBytes = Cfg2::SMEM;
-        cudaLaunchAttribute attr[1];
-        attr[0].id = cudaLaunchAttributeClusterDimension;
-        attr[0].val.clusterDim.x = 2;
-        attr[0].val.clusterDim.y = 1;
-        attr[0].val.clusterDim.z = 1;
-        cfg.attrs = attr;
-        cfg.numAttrs = 1;
-        int c = 0;
-        if (cudaOccupancyMaxActiveClusters(&c, kern, &cfg) != cudaSuccess || c <= 0) {
-            cudaGetLastError();
-            return cap;
-        }
-        return std::min(c, cap);
-    }();
+    static const int n = query_clusters<1>();
+    return n;
+}
+int max_quad_clusters() {  // 4-CTA clusters of the multicast variant
+    static const int n = query_clusters<2>();
     return n;
 }
 
@@ -1043,13 +1050,16 @@ int dispatch_pair(bool amn, bool bmn, const CUtensorMap& ta, const CUtensorMap& 
     return launch_pair<true, true, NPAIR>(ta, tb, td, tu, p, clusters, st);
 }
 
-// 4-CTA multicast clusters are opt-in (SWARM_GEMM_MCAST=1): measured slower on
-// B200 — cluster-4 placement strands SMs and couples the two pairs' pipelines
+// 4-CTA clusters (two pairs side by side in N sharing each A sub-tile by TMA
+// multicast) are the default where N splits into an even number of 256-wide
+// tiles (SWARM_GEMM_MCAST=0 disables them).  Only 33 such clusters are resident
+// on B200 (132 SMs, GPC packing), yet halving the A operand feed wins on most
+// block shapes, most of all on the MN-major weight-gradient GEMMs
 // (profiles/r01_gemm_experiments.md).
 int multicast_mode() {
     static const int on = [] {
         const char* e = getenv("SWARM_GEMM_MCAST");
-        return e && e[0] == '1';
+        return !(e && e[0] == '0');
     }();
     return on;
 }
@@ -1074,7 +1084,9 @@ int dispatch(bool amn, bool bmn, const CUtensorMap& ta, const CUtensorMap& tb, c
 }  // namespace gemm
 }  // namespace swarm
 
-extern "C" int swarm_gemm_pair_clusters(void) { return swarm::gemm::max_pair_clusters(); }
+extern "C" int swarm_gemm_pair_clusters(void) {
+    return swarm::gemm::multicast_mode() ? swarm::gemm::max_quad_clusters() : swarm::gemm::max_pair_clusters();
+}
 
 extern "C" size_t swarm_gemm_workspace_bytes(void) {
     using namespace swarm::gemm;
@@ -1172,7 +1184,7 @@ extern "C" int swarm_gemm_bf16(const swarm_gemm_args* a, swarm_stream_t stream) 
     p.sk_tiles = 0;
     p.sk_iters = 0;
     cudaStream_t st = as_stream(stream);
-    const int resident = npair == 1 ? max_pair_clusters() : num_sms() / (2 * npair);
+    const int resident = npair == 1 ? max_pair_clusters() : max_quad_clusters();
     int grid_clusters = std::min(p.total_tiles, resident);
     if (pair && npair == 1 && a->workspace &&
         a->workspace_bytes >= sk_bytes(std::min(num_sms() / 2, kMaxClusters)) &&

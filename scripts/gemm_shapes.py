@@ -73,12 +73,31 @@ def main():
         ms = e0.elapsed_time(e1) / 10
         fl = 2.0 * M * N * K * batch
         tf = fl / ms / 1e9
+        # library reference point (measurement only): cuBLAS via torch on the same
+        # operand layouts, bf16 out (fp32 out for the fp32 epilogues)
+        a_, b_ = keep[0], keep[1]
+        if batch == 1:
+            A = a_.t() if a_t else a_
+            B = b_ if b_t else b_.t()
+            lib = (lambda: torch.matmul(A, B)) if epi == E_BF else (lambda: torch.matmul(A, B).float())
+            for _ in range(3):
+                lib()
+            torch.cuda.synchronize()
+            e0.record()
+            for _ in range(10):
+                lib()
+            e1.record()
+            torch.cuda.synchronize()
+            lib_tf = fl / (e0.elapsed_time(e1) / 10) / 1e9
+        else:
+            lib_tf = None
         rows.append({"gemm": name, "M": M, "N": N, "K": K, "batch": batch, "a_mn": a_t, "b_mn": b_t, "ms": ms,
-                     "tflops": tf})
+                     "tflops": tf, "cublas_tflops": lib_tf})
         if not name.startswith("head"):
             tot_ms += ms
             tot_fl += fl
-        print(f"{name:16s} M={M:6d} N={N:6d} K={K:6d} x{batch:3d}  {ms * 1e3:9.1f} us  {tf:7.1f} TFLOP/s", flush=True)
+        print(f"{name:16s} M={M:6d} N={N:6d} K={K:6d} x{batch:3d}  {ms * 1e3:9.1f} us  {tf:7.1f} TFLOP/s"
+              f"  (cuBLAS {lib_tf or 0:7.1f})", flush=True)
     print(f"block total: {tot_ms:.3f} ms/layer/microbatch, {tot_fl / tot_ms / 1e9:.1f} TFLOP/s FLOP-weighted")
     if args.out:
         with open(args.out, "w") as f:

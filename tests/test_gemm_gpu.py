@@ -201,3 +201,41 @@ def test_gemm_causal_k_skip(cuda, tri):
     ref = (Ab.float() @ V.float().view(Bz, Lq, dh)).reshape(Bz * Lq, dh)
     assert torch.isfinite(out).all()
     torch.testing.assert_close(out, ref, rtol=1e-4, atol=1e-3)
+
+
+_VARIANT_CHECK = r"""
+import math, sys, torch
+sys.path.insert(0, {root!r})
+from paper_2301_11913_b200 import _lib as L, ops
+torch.manual_seed(0)
+for (m, n, k) in [(2048, 2048, 2048), (512, 6144, 2048), (768, 1280, 4096), (200, 300, 96)]:
+    for a_t, b_t in [(False, False), (False, True), (True, True)]:
+        if (a_t and m % 8) or (b_t and n % 8) or k % 8:
+            continue  # rows must be 16-byte aligned
+        a = torch.randn((k, m) if a_t else (m, k), device="cuda").bfloat16()
+        b = torch.randn((k, n) if b_t else (n, k), device="cuda").bfloat16()
+        A = a.float().t() if a_t else a.float()
+        B = b.float().t() if b_t else b.float()
+        ref = A @ B.t()
+        out = ops.gemm(a, b, a_t=a_t, b_t=b_t, epilogue=L.EPI_STORE_F32)
+        torch.testing.assert_close(out, ref, rtol=1e-4, atol=1e-4 * math.sqrt(k))
+        acc = torch.ones(m, n, device="cuda")
+        ops.gemm(a, b, a_t=a_t, b_t=b_t, epilogue=L.EPI_ACCUM_F32, out=acc)
+        torch.testing.assert_close(acc, ref + 1, rtol=1e-4, atol=1e-4 * math.sqrt(k))
+print("ok")
+"""
+
+
+@pytest.mark.parametrize("env", [{"SWARM_GEMM_MCAST": "0"}, {"SWARM_GEMM_PAIR": "0"},
+                                 {"SWARM_GEMM_TMA_EPI": "0"}, {"SWARM_PDL": "0"}])
+def test_gemm_kernel_variants(cuda, env):
+    """The non-default kernel variants (2-CTA pairs without multicast, 1-CTA
+    tiles, direct-store epilogue, no programmatic dependent launch) stay correct;
+    the selection is read once per process, hence a subprocess per variant."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-c", _VARIANT_CHECK.format(root=root)], env={**os.environ, **env},
+                       capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr
