@@ -178,16 +178,22 @@ int swarm_attn_softmax_forward(const float* s, size_t rows, size_t L, int causal
 /* dS = scale * P * (dP - rowsum(P*dP)), bf16 */
 int swarm_attn_softmax_backward(const void* p, const float* dp, size_t rows, size_t L, float scale, void* ds,
                                 swarm_stream_t stream);
-/* Fused attention scores (tcgen05; L % 128 == 0, L <= 512, d_head % 64 == 0, d_head <= 128):
+/* Fused attention scores (tcgen05; L % 128 == 0, L <= 1024, d_head % 64 == 0, d_head <= 128):
  *   P[z*L + i, j] = softmax_j(scale * q_z[i] . k_z[j])  (bf16 [B*H*L, L], causal masks j > i)
  * with q_z = q[b*L + i, h*d_head : (h+1)*d_head] for z = b*H + h (row stride ld, n_cols
- * valid columns; k likewise) — the 128 x L score block never leaves TMEM. */
+ * valid columns; k likewise); scores stay in TMEM.  When causal, columns at or past a
+ * query block's causal extent ((i/128 + 1) * 128) are not written. */
 int swarm_attn_scores_softmax(const void* q, const void* k, int ld, int n_cols, int B, int H, int L, int d_head,
                               float scale, int causal, void* P, swarm_stream_t stream);
-/* dS = scale * P * (dP - rowsum(P * dP)) with dP = dO_z V_z^T computed in TMEM (bf16 out) */
-int swarm_attn_scores_softmax_backward(const void* dO, int ld_do, const void* v, int ld_v, int v_cols, const void* P,
-                                       int B, int H, int L, int d_head, float scale, int causal, void* dS,
-                                       swarm_stream_t stream);
+/* dS = scale * P * (dP - rowsum(P * dP)) with dP = dO_z V_z^T computed in TMEM (bf16 out); the
+ * row statistic is taken as dO . O (O = P V, the forward's attention output, [B*L, ld_o] with
+ * head h at column h*d_head), which equals rowsum(P * dP) and saves a second pass.
+ * Columns at or past a query block's causal extent ((i/128 + 1) * 128) are not written
+ * (the forward likewise leaves them untouched when causal): callers that read them keep
+ * them zeroed. */
+int swarm_attn_scores_softmax_backward(const void* dO, int ld_do, const void* v, int ld_v, int v_cols, const void* o,
+                                       int ld_o, const void* P, int B, int H, int L, int d_head, float scale,
+                                       int causal, void* dS, swarm_stream_t stream);
 /* token cross-entropy on fp32 logits [rows, vocab]: loss_sum += sum_t (lse_t - logit_t[target_t]);
  * dlogits (bf16, optional) = grad_scale * (softmax - onehot) */
 int swarm_cross_entropy(const float* logits, const int32_t* targets, size_t rows, size_t vocab, float grad_scale,

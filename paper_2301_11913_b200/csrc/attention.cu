@@ -22,6 +22,7 @@
 #include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <unordered_map>
 
 #include "common.cuh"
@@ -45,11 +46,15 @@ struct Params {
     int a_col0, b_col0;  // column of head 0 in the A / B storages
     float scale;
     const __nv_bfloat16* p_in;  // backward: P [B*H*L, L]
+    const __nv_bfloat16* d_o;   // backward: dO [B*L, ld_do] (head h at column h*dh)
+    const __nv_bfloat16* o;     // backward: O = P V [B*L, ld_o]
+    int ld_do, ld_o;
+    int trace;  // record the per-CTA timeline (experiments)
 };
 
 constexpr int kABytes = (kMaxDh / 64) * BQ * 128;       // 32 KB: Q / dO block
 constexpr int kChunkBytes = (kMaxDh / 64) * BKV * 128;  // 16 KB: K / V chunk
-constexpr int kStgBytes = 4 * 2 * kSlot + kSlot;        // 4 row warps x 2 slots + a zero box
+constexpr int kStgBytes = 4 * 2 * kSlot;                // 4 row warps x 2 staging slots
 constexpr int kSmem = kABytes + kStages * kChunkBytes + kStgBytes + 1024 + 256;
 static_assert(2 * (kSmem + 1024) <= 233472, "two attention CTAs must fit one SM");
 
@@ -90,18 +95,42 @@ __device__ __forceinline__ void load_p64(const __nv_bfloat16* src, float (&p)[64
     }
 }
 
+// Per-CTA timeline for experiments (SWARM_ATTN_TRACE=1, scripts/attn_trace.py):
+// globaltimer at entry, after the prologue, after the statistics pass, at the end
+// of the output pass, and the CTA's SM id.
+constexpr int kTraceCtas = 4096;
+__device__ unsigned long long g_attn_trace[kTraceCtas][6];
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+__device__ __forceinline__ void trace(const Params& p, int slot) {
+    if (p.trace && blockIdx.x < kTraceCtas) g_attn_trace[blockIdx.x][slot] = gtimer();
+}
+
 template <bool BWD>
 __global__ void __launch_bounds__(kThreads, 2)
     k_attn_chunks(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUtensorMap tma_b,
                   const __grid_constant__ CUtensorMap tma_out, const Params p) {
+    // forward: pass 0 row max / sum, pass 1 probabilities; backward: one pass, the
+    // row statistic rowsum(P * dP) = dO . O comes from the forward output
+    constexpr int kPasses = BWD ? 1 : 2;
     pdl_trigger();
+    if (threadIdx.x == 128) {
+        trace(p, 0);
+        if (p.trace && blockIdx.x < kTraceCtas) {
+            unsigned smid;
+            asm("mov.u32 %0, %%smid;" : "=r"(smid));
+            g_attn_trace[blockIdx.x][5] = smid;
+        }
+    }
     extern __shared__ uint8_t smem_raw[];
     const uint32_t raw = smem_u32(smem_raw);
     uint8_t* smem = smem_raw + ((1024 - (raw & 1023)) & 1023);
     uint8_t* sa = smem;
     uint8_t* sb = sa + kABytes;
     uint8_t* stg_all = sb + kStages * kChunkBytes;
-    uint8_t* zero_box = stg_all + 4 * 2 * kSlot;
     uint64_t* bars = reinterpret_cast<uint64_t*>(stg_all + kStgBytes);
     uint64_t* qfull = bars;
     uint64_t* full = bars + 1;
@@ -149,7 +178,7 @@ __global__ void __launch_bounds__(kThreads, 2)
         for (int kb = 0; kb < kboxes; ++kb) tma_load_2d(sa + kb * BQ * 128, &tma_a, qfull, acol + kb * 64, arow);
         int stage = 0;
         uint32_t phase = 0;
-        for (int pass = 0; pass < 2; ++pass)
+        for (int pass = 0; pass < kPasses; ++pass)
             for (int j = 0; j < nch; ++j) {
                 mbar_wait(&empty[stage], phase ^ 1);
                 mbar_arrive_expect_tx(&full[stage], kboxes * BKV * 128);
@@ -168,7 +197,7 @@ __global__ void __launch_bounds__(kThreads, 2)
         int stage = 0, buf = 0;
         uint32_t phase = 0, bphase = 0;
         const int ksteps = p.dh / 16;
-        for (int pass = 0; pass < 2; ++pass)
+        for (int pass = 0; pass < kPasses; ++pass)
             for (int j = 0; j < nch; ++j) {
                 mbar_wait(&full[stage], phase);
                 mbar_wait(&sempty[buf], bphase ^ 1);
@@ -201,18 +230,15 @@ __global__ void __launch_bounds__(kThreads, 2)
         int slot_idx = 0;
         const int out_row = z * p.L + mt * BQ + q * 32;
         const __nv_bfloat16* prow = BWD ? p.p_in + (static_cast<size_t>(z) * p.L + mt * BQ + r) * p.L : nullptr;
-        if (q == 0) {  // the zero box written for fully masked key chunks
-            for (int i = lane; i < kSlot / 16; i += 32) st_shared_v4(smem_u32(zero_box) + i * 16, 0, 0, 0, 0);
-            fence_async_smem();
-        }
-        asm volatile("bar.sync 1, 128;" ::: "memory");
-        const float l2e = 1.4426950408889634f;
         int buf = 0;
         uint32_t bphase = 0;
-        float stat_a = 0.f, stat_b = 0.f;  // fwd: row max (scaled) / 1 / sum; bwd: rowsum(P * dP)
-        // ---------------- pass 0: row statistics
-        {
-            float m = -INFINITY, l = 0.f, acc = 0.f;
+        // scores are raw q.k; softmax works in log2 units u = s * cs
+        const float cs = p.scale * 1.4426950408889634f;
+        if (r == 0) trace(p, 1);
+        float bias = 0.f;  // fwd pass 1: max(u) + log2(sum), so p = 2^(u - bias); bwd: dO . O
+        if constexpr (!BWD) {
+            // ---------------- pass 0: online row max / sum
+            float mu = -INFINITY, l = 0.f;
             for (int j = 0; j < nch; ++j) {
                 uint32_t ra[32], rb[32];
                 mbar_wait(&sfull[buf], bphase);
@@ -228,38 +254,60 @@ __global__ void __launch_bounds__(kThreads, 2)
                     bphase ^= 1;
                 }
                 const int c0 = j * BKV;
-                if constexpr (!BWD) {
-                    float cm = -INFINITY;
+                if (c0 >= valid) continue;  // fully masked for this row
+                const bool full = c0 + BKV <= valid;
+                float cm = -INFINITY;
+                if (full) {
+#pragma unroll
+                    for (int jj = 0; jj < 32; ++jj)
+                        cm = fmaxf(cm, fmaxf(__uint_as_float(ra[jj]), __uint_as_float(rb[jj])));
+                } else {
 #pragma unroll
                     for (int jj = 0; jj < 32; ++jj) {
                         if (c0 + jj < valid) cm = fmaxf(cm, __uint_as_float(ra[jj]));
                         if (c0 + 32 + jj < valid) cm = fmaxf(cm, __uint_as_float(rb[jj]));
                     }
-                    if (cm != -INFINITY) {
-                        const float nm = fmaxf(m, cm * p.scale);
-                        float add = 0.f;
-#pragma unroll
-                        for (int jj = 0; jj < 32; ++jj) {
-                            if (c0 + jj < valid) add += fast_exp2((__uint_as_float(ra[jj]) * p.scale - nm) * l2e);
-                            if (c0 + 32 + jj < valid)
-                                add += fast_exp2((__uint_as_float(rb[jj]) * p.scale - nm) * l2e);
-                        }
-                        l = (m == -INFINITY ? 0.f : l * fast_exp2((m - nm) * l2e)) + add;
-                        m = nm;
-                    }
-                } else {
-                    float pv[64];
-                    load_p64(prow + c0, pv);
+                }
+                const float nmu = fmaxf(mu, cm * cs);
+                float add = 0.f;
+                if (full) {
 #pragma unroll
                     for (int jj = 0; jj < 32; ++jj)
-                        acc += pv[jj] * __uint_as_float(ra[jj]) + pv[32 + jj] * __uint_as_float(rb[jj]);
+                        add += fast_exp2(fmaf(__uint_as_float(ra[jj]), cs, -nmu)) +
+                               fast_exp2(fmaf(__uint_as_float(rb[jj]), cs, -nmu));
+                } else {
+#pragma unroll
+                    for (int jj = 0; jj < 32; ++jj) {
+                        if (c0 + jj < valid) add += fast_exp2(fmaf(__uint_as_float(ra[jj]), cs, -nmu));
+                        if (c0 + 32 + jj < valid) add += fast_exp2(fmaf(__uint_as_float(rb[jj]), cs, -nmu));
+                    }
                 }
+                l = (mu == -INFINITY ? 0.f : l * fast_exp2(mu - nmu)) + add;
+                mu = nmu;
             }
-            stat_a = BWD ? acc : m;
-            stat_b = BWD ? 0.f : 1.f / l;
+            bias = mu + __log2f(l);
+        } else {
+            // D = dO[row] . O[row] over this head's d_head columns (= rowsum(P * dP))
+            const size_t grow = static_cast<size_t>(zb) * p.L + qi;
+            const uint4* d4 = reinterpret_cast<const uint4*>(p.d_o + grow * p.ld_do + zh * p.dh);
+            const uint4* o4 = reinterpret_cast<const uint4*>(p.o + grow * p.ld_o + zh * p.dh);
+            float acc = 0.f;
+            for (int c = 0; c < p.dh / 8; ++c) {
+                const uint4 a = __ldg(d4 + c), b = __ldg(o4 + c);
+                const uint32_t wa[4] = {a.x, a.y, a.z, a.w}, wb[4] = {b.x, b.y, b.z, b.w};
+#pragma unroll
+                for (int k = 0; k < 4; ++k)
+                    acc += __uint_as_float(wa[k] << 16) * __uint_as_float(wb[k] << 16) +
+                           __uint_as_float(wa[k] & 0xffff0000u) * __uint_as_float(wb[k] & 0xffff0000u);
+            }
+            bias = acc;
         }
-        // ---------------- pass 1: probabilities / score gradients
+        if (r == 0) trace(p, 2);
+        // ---------------- probabilities (fwd pass 1) / score gradients (bwd)
         for (int j = 0; j < nch; ++j) {
+            const int c0 = j * BKV;
+            float v[64];
+            if constexpr (BWD) load_p64(prow + c0, v);  // in flight while the MMA finishes
             uint32_t ra[32], rb[32];
             mbar_wait(&sfull[buf], bphase);
             tc_fence_after();
@@ -273,23 +321,25 @@ __global__ void __launch_bounds__(kThreads, 2)
                 buf = 0;
                 bphase ^= 1;
             }
-            const int c0 = j * BKV;
-            float v[64];
             if constexpr (!BWD) {
+                if (c0 + BKV <= valid) {
 #pragma unroll
-                for (int jj = 0; jj < 32; ++jj) {
-                    v[jj] = (c0 + jj < valid) ? fast_exp2((__uint_as_float(ra[jj]) * p.scale - stat_a) * l2e) * stat_b
-                                              : 0.f;
-                    v[32 + jj] = (c0 + 32 + jj < valid)
-                                     ? fast_exp2((__uint_as_float(rb[jj]) * p.scale - stat_a) * l2e) * stat_b
-                                     : 0.f;
+                    for (int jj = 0; jj < 32; ++jj) {
+                        v[jj] = fast_exp2(fmaf(__uint_as_float(ra[jj]), cs, -bias));
+                        v[32 + jj] = fast_exp2(fmaf(__uint_as_float(rb[jj]), cs, -bias));
+                    }
+                } else {
+#pragma unroll
+                    for (int jj = 0; jj < 32; ++jj) {
+                        v[jj] = (c0 + jj < valid) ? fast_exp2(fmaf(__uint_as_float(ra[jj]), cs, -bias)) : 0.f;
+                        v[32 + jj] = (c0 + 32 + jj < valid) ? fast_exp2(fmaf(__uint_as_float(rb[jj]), cs, -bias)) : 0.f;
+                    }
                 }
             } else {
-                load_p64(prow + c0, v);
 #pragma unroll
                 for (int jj = 0; jj < 32; ++jj) {
-                    v[jj] = p.scale * v[jj] * (__uint_as_float(ra[jj]) - stat_a);
-                    v[32 + jj] = p.scale * v[32 + jj] * (__uint_as_float(rb[jj]) - stat_a);
+                    v[jj] = p.scale * v[jj] * (__uint_as_float(ra[jj]) - bias);
+                    v[32 + jj] = p.scale * v[32 + jj] * (__uint_as_float(rb[jj]) - bias);
                 }
             }
 #pragma unroll
@@ -307,14 +357,10 @@ __global__ void __launch_bounds__(kThreads, 2)
                 }
             }
         }
-        // keys past the causal block: zeros (read by nothing on the hot path, but P / dS stay well defined)
-        if (lane == 0) {
-            for (int c0 = kv_len; c0 < p.L; c0 += 32) {
-                tma_store_2d(&tma_out, zero_box, c0, out_row);
-                bulk_commit();
-            }
-            bulk_wait_all();
-        }
+        // keys past the causal block are never written (nothing on the hot path
+        // reads them; the stage executor zeroes P / dS once at creation)
+        if (lane == 0) bulk_wait_all();
+        if (r == 0) trace(p, 3);
         __syncwarp();
     }
     tc_fence_before();
@@ -323,6 +369,7 @@ __global__ void __launch_bounds__(kThreads, 2)
         tc_fence_after();
         tmem_dealloc(tmem, 2 * BKV);
     }
+    if (threadIdx.x == 128) trace(p, 4);
 }
 
 using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
@@ -396,13 +443,25 @@ int map_bf16_uncached(CUtensorMap* m, const void* ptr, long long rows, long long
                : SWARM_E_INVALID;
 }
 
+bool trace_enabled() {
+    static const bool on = [] {
+        const char* e = getenv("SWARM_ATTN_TRACE");
+        return e && e[0] == '1';
+    }();
+    return on;
+}
+
 template <bool BWD>
 int launch(const void* a, int lda, int a_cols, int a_col0, const void* b, int ldb, int b_cols, int b_col0,
-           const void* pin, void* out, int B, int H, int L, int dh, float scale, int causal, cudaStream_t st) {
+           const void* pin, const void* o, int ld_o, void* out, int B, int H, int L, int dh, float scale, int causal,
+           cudaStream_t st) {
     if (L % BQ || L > kMaxL || dh % 64 || dh > kMaxDh || B <= 0 || H <= 0)
         return invalid("attention: need L % 128 == 0, L <= 1024, dh % 64 == 0, dh <= 128");
     if (BWD && (!pin || (reinterpret_cast<uintptr_t>(pin) & 15)))
         return invalid("attention: P must be a 16-byte aligned bf16 [B*H*L, L] array");
+    if (BWD && (!o || (reinterpret_cast<uintptr_t>(o) & 15) || (reinterpret_cast<uintptr_t>(a) & 15) || ld_o % 8 ||
+                lda % 8))
+        return invalid("attention: dO and O must be 16-byte aligned bf16 rows");
     const long long T = static_cast<long long>(B) * L, rows_out = static_cast<long long>(B) * H * L;
     CUtensorMap ta, tb, to;
     if (map_bf16(&ta, a, T, a_cols, lda, 64, BQ, CU_TENSOR_MAP_SWIZZLE_128B) ||
@@ -415,7 +474,20 @@ int launch(const void* a, int lda, int a_cols, int a_col0, const void* b, int ld
         SWARM_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem));
         attr = true;
     }
-    Params p{B, H, L, dh, causal, a_col0, b_col0, scale, static_cast<const __nv_bfloat16*>(pin)};
+    Params p{B,
+             H,
+             L,
+             dh,
+             causal,
+             a_col0,
+             b_col0,
+             scale,
+             static_cast<const __nv_bfloat16*>(pin),
+             static_cast<const __nv_bfloat16*>(a),
+             static_cast<const __nv_bfloat16*>(o),
+             lda,
+             ld_o,
+             trace_enabled() ? 1 : 0};
     SWARM_CUDA_TRY(launch_pdl(kern, dim3(B * H * (L / BQ)), dim3(kThreads), kSmem, st, ta, tb, to, p));
     SWARM_LAUNCH_CHECK("k_attn_chunks");
     return SWARM_OK;
@@ -428,15 +500,24 @@ extern "C" {
 
 int swarm_attn_scores_softmax(const void* q, const void* k, int ld, int n_cols, int B, int H, int L, int dh,
                               float scale, int causal, void* P, swarm_stream_t stream) {
-    return swarm::attn::launch<false>(q, ld, n_cols, 0, k, ld, n_cols, 0, nullptr, P, B, H, L, dh, scale, causal,
-                                      swarm::as_stream(stream));
+    return swarm::attn::launch<false>(q, ld, n_cols, 0, k, ld, n_cols, 0, nullptr, nullptr, 0, P, B, H, L, dh, scale,
+                                      causal, swarm::as_stream(stream));
 }
 
-int swarm_attn_scores_softmax_backward(const void* dO, int ld_do, const void* v, int ld_v, int v_cols, const void* P,
-                                       int B, int H, int L, int dh, float scale, int causal, void* dS,
-                                       swarm_stream_t stream) {
-    return swarm::attn::launch<true>(dO, ld_do, H * dh, 0, v, ld_v, v_cols, 0, P, dS, B, H, L, dh, scale, causal,
-                                     swarm::as_stream(stream));
+int swarm_attn_scores_softmax_backward(const void* dO, int ld_do, const void* v, int ld_v, int v_cols, const void* o,
+                                       int ld_o, const void* P, int B, int H, int L, int dh, float scale, int causal,
+                                       void* dS, swarm_stream_t stream) {
+    return swarm::attn::launch<true>(dO, ld_do, H * dh, 0, v, ld_v, v_cols, 0, P, o, ld_o, dS, B, H, L, dh, scale,
+                                     causal, swarm::as_stream(stream));
+}
+
+// experiments only (not in the public header): copy the last traced launch's
+// per-CTA timeline, n_ctas x 6 u64 (t_entry, t_prologue, t_stats, t_out, t_exit, smid)
+int swarm_debug_attn_trace(uint64_t* host, int n_ctas) {
+    if (n_ctas > swarm::attn::kTraceCtas) n_ctas = swarm::attn::kTraceCtas;
+    return cudaMemcpyFromSymbol(host, swarm::attn::g_attn_trace, sizeof(uint64_t) * 6 * n_ctas) == cudaSuccess
+               ? SWARM_OK
+               : SWARM_E_CUDA;
 }
 
 }  // extern "C"

@@ -111,6 +111,9 @@ int dmalloc(swarm_stage* s, void** p, size_t bytes) {
     if (bytes == 0) bytes = 16;
     bytes = (bytes + 255) & ~size_t(255);
     cudaError_t e = cudaMalloc(p, bytes);
+    // zero-filled once: e.g. the causal attention kernels never write P / dS past
+    // a query block's causal extent, so those regions must start (and stay) zero
+    if (e == cudaSuccess) e = cudaMemset(*p, 0, bytes);
     if (e != cudaSuccess) {
         g_err = std::string("stage: cudaMalloc failed: ") + cudaGetErrorString(e);
         return SWARM_E_CUDA;
@@ -365,7 +368,7 @@ int block_backward(swarm_stage* s, const Act& A, const bf16* dy, bf16* dx, const
     // dP = dO V^T ; dS = scale * P (dP - rowsum(P dP))
     const float scale = 1.f / std::sqrt(static_cast<float>(dh));
     if (s->fused_attn) {
-        PTRY(SWARM_PROF_ATTENTION, st, swarm_attn_scores_softmax_backward(s->dO, d, A.qkv + 2 * d, 3 * d, d, A.P, s->B, H, L, dh, scale,
+        PTRY(SWARM_PROF_ATTENTION, st, swarm_attn_scores_softmax_backward(s->dO, d, A.qkv + 2 * d, 3 * d, d, A.o, d, A.P, s->B, H, L, dh, scale,
                                                s->cfg.causal, s->dS, st));
     } else {
         TRY(bmm(s, L, L, dh, {{s->dO, d, T, d, false}, L, 0, 0, dh},

@@ -1,7 +1,8 @@
 """GPU numerics: fused attention-score kernels vs a torch fp32 reference of the
 same op on the same bf16 inputs.  Tolerances: P and dS are bf16 outputs
 (rounding 2^-8 relative) of fp32 math: atol 4e-3 on P (entries <= 1), rtol 2e-2 /
-atol 2e-3*max|dS| on dS."""
+atol 2e-3*max|dS| on dS (the kernel's row statistic dO . O, with O rounded to bf16
+like the executor's PV output, differs from rowsum(P dP) only by that rounding)."""
 import ctypes as C
 import math
 
@@ -29,7 +30,7 @@ def test_fused_scores_softmax(cuda, B, H, L, dh, causal):
     torch.manual_seed(L + dh + causal)
     d = H * dh
     qkv = (torch.randn(B * L, 3 * d, device="cuda") * 2).bfloat16()
-    P = torch.empty(B * H * L, L, device="cuda", dtype=torch.bfloat16)
+    P = torch.zeros(B * H * L, L, device="cuda", dtype=torch.bfloat16)  # causal: the tail past a block is not written
     scale = 1 / math.sqrt(dh)
     st = torch.cuda.current_stream().cuda_stream
     rc = _lib.lib().swarm_attn_scores_softmax(C.c_void_p(qkv.data_ptr()), C.c_void_p(qkv[:, d:].data_ptr()), 3 * d, d,
@@ -39,16 +40,23 @@ def test_fused_scores_softmax(cuda, B, H, L, dh, causal):
     torch.testing.assert_close(P.float(), ref, rtol=0, atol=4e-3)
     # backward: dS = scale * P * (dP - rowsum(P dP)), dP = dO V^T (with the kernel's own bf16 P)
     dO = torch.randn(B * L, d, device="cuda").bfloat16()
-    dS = torch.empty_like(P)
-    rc = _lib.lib().swarm_attn_scores_softmax_backward(C.c_void_p(dO.data_ptr()), d, C.c_void_p(qkv[:, 2 * d:].data_ptr()),
-                                                       3 * d, d, C.c_void_p(P.data_ptr()), B, H, L, dh, scale, causal,
-                                                       C.c_void_p(dS.data_ptr()), st)
-    assert rc == 0, _lib.last_error()
+    dS = torch.zeros_like(P)
     v = qkv[:, 2 * d:].float().view(B, L, H, dh).transpose(1, 2)
+    # O = P V in bf16, as the executor's PV GEMM stores it: the kernel takes rowsum(P * dP) as dO . O
+    O = (P.float().view(B, H, L, L) @ v).transpose(1, 2).reshape(B * L, d).bfloat16().contiguous()
+    rc = _lib.lib().swarm_attn_scores_softmax_backward(C.c_void_p(dO.data_ptr()), d, C.c_void_p(qkv[:, 2 * d:].data_ptr()),
+                                                       3 * d, d, C.c_void_p(O.data_ptr()), d, C.c_void_p(P.data_ptr()),
+                                                       B, H, L, dh, scale, causal, C.c_void_p(dS.data_ptr()), st)
+    assert rc == 0, _lib.last_error()
     do = dO.float().view(B, L, H, dh).transpose(1, 2)
     dP = (do @ v.transpose(-1, -2)).reshape(B * H * L, L)
     Pf = P.float()
-    want = scale * Pf * (dP - (Pf * dP).sum(-1, keepdim=True))
+    # the kernel's row statistic is dO . O (FlashAttention-2's D); in exact arithmetic it is
+    # rowsum(P * dP) — they differ here only by O's bf16 rounding
+    D = (dO.float().view(B, L, H, dh) * O.float().view(B, L, H, dh)).sum(-1).transpose(1, 2).reshape(B * H * L, 1)
+    Dx = (Pf * dP).sum(-1, keepdim=True)
+    torch.testing.assert_close(D, Dx, rtol=0, atol=2e-2 * float(Dx.abs().max()))
+    want = scale * Pf * (dP - D)
     torch.testing.assert_close(dS.float(), want, rtol=2e-2, atol=2e-3 * float(want.abs().max()))
 
 
@@ -61,7 +69,7 @@ def test_fused_matches_unfused_path(cuda):
     torch.manual_seed(3)
     qkv = torch.randn(B * L, 3 * d, device="cuda").bfloat16()
     st = torch.cuda.current_stream().cuda_stream
-    P1 = torch.empty(B * H * L, L, device="cuda", dtype=torch.bfloat16)
+    P1 = torch.zeros(B * H * L, L, device="cuda", dtype=torch.bfloat16)
     _lib.lib().swarm_attn_scores_softmax(C.c_void_p(qkv.data_ptr()), C.c_void_p(qkv[:, d:].data_ptr()), 3 * d, d, B, H,
                                          L, dh, 1 / math.sqrt(dh), 1, C.c_void_p(P1.data_ptr()), st)
     S = torch.empty(B * H * L, L, device="cuda")
