@@ -36,7 +36,6 @@ using namespace swarm::sm100;
 constexpr int kThreads = 256;
 constexpr int BQ = 128;        // query rows per CTA
 constexpr int BKV = 64;        // keys per chunk (MMA N)
-constexpr int kStages = 3;     // K / V chunk ring
 constexpr int kMaxL = 1024;
 constexpr int kMaxDh = 128;    // K extent of the score GEMM (<= 2 x 64-wide boxes)
 constexpr int kSlot = 2048;    // one 32 x 32 bf16 staging box
@@ -45,18 +44,24 @@ struct Params {
     int B, H, L, dh, causal;
     int a_col0, b_col0;  // column of head 0 in the A / B storages
     float scale;
-    const __nv_bfloat16* p_in;  // backward: P [B*H*L, L]
-    const __nv_bfloat16* d_o;   // backward: dO [B*L, ld_do] (head h at column h*dh)
-    const __nv_bfloat16* o;     // backward: O = P V [B*L, ld_o]
-    int ld_do, ld_o;
+    const __nv_bfloat16* o;  // backward: O = P V [B*L, ld_o] (head h at column h*dh)
+    int ld_o;
     int trace;  // record the per-CTA timeline (experiments)
 };
 
 constexpr int kABytes = (kMaxDh / 64) * BQ * 128;       // 32 KB: Q / dO block
 constexpr int kChunkBytes = (kMaxDh / 64) * BKV * 128;  // 16 KB: K / V chunk
-constexpr int kStgBytes = 4 * 2 * kSlot;                // 4 row warps x 2 staging slots
-constexpr int kSmem = kABytes + kStages * kChunkBytes + kStgBytes + 1024 + 256;
-static_assert(2 * (kSmem + 1024) <= 233472, "two attention CTAs must fit one SM");
+constexpr int kPChunkBytes = BQ * BKV * 2;              // 16 KB: P chunk (backward), dS written in place
+// forward: 3-stage K ring + 4 row warps x 2 staging slots; backward: 2-stage
+// (V chunk, P chunk) ring, dS staged in place of the P chunk it replaces
+template <bool BWD>
+struct Lay {
+    static constexpr int kStages = BWD ? 2 : 3;
+    static constexpr int kStageBytes = kChunkBytes + (BWD ? kPChunkBytes : 0);
+    static constexpr int kStgBytes = BWD ? 0 : 4 * 2 * kSlot;
+    static constexpr int kSmem = kABytes + kStages * kStageBytes + kStgBytes + 1024 + 256;
+    static_assert(2 * (kSmem + 1024) <= 233472, "two attention CTAs must fit one SM");
+};
 
 // 2^x on the SFU (ex2.approx.ftz: 2 ulp; the probabilities are rounded to bf16 anyway)
 __device__ __forceinline__ float fast_exp2(float x) {
@@ -80,21 +85,6 @@ __device__ __forceinline__ void stage_bf16(uint8_t* slot, int row, const float* 
                      pack_bf16(v[8 * j + 6], v[8 * j + 7]));
 }
 
-// 64 consecutive bf16 of one P row (128 B, 16-B aligned) as floats
-__device__ __forceinline__ void load_p64(const __nv_bfloat16* src, float (&p)[64]) {
-    const uint4* s4 = reinterpret_cast<const uint4*>(src);
-#pragma unroll
-    for (int q = 0; q < 8; ++q) {
-        const uint4 w = __ldg(s4 + q);
-        const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-            p[q * 8 + 2 * k] = __uint_as_float(ws[k] << 16);
-            p[q * 8 + 2 * k + 1] = __uint_as_float(ws[k] & 0xffff0000u);
-        }
-    }
-}
-
 // Per-CTA timeline for experiments (SWARM_ATTN_TRACE=1, scripts/attn_trace.py):
 // globaltimer at entry, after the prologue, after the statistics pass, at the end
 // of the output pass, and the CTA's SM id.
@@ -112,7 +102,8 @@ __device__ __forceinline__ void trace(const Params& p, int slot) {
 template <bool BWD>
 __global__ void __launch_bounds__(kThreads, 2)
     k_attn_chunks(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUtensorMap tma_b,
-                  const __grid_constant__ CUtensorMap tma_out, const Params p) {
+                  const __grid_constant__ CUtensorMap tma_p, const __grid_constant__ CUtensorMap tma_out,
+                  const Params p) {
     // forward: pass 0 row max / sum, pass 1 probabilities; backward: one pass, the
     // row statistic rowsum(P * dP) = dO . O comes from the forward output
     constexpr int kPasses = BWD ? 1 : 2;
@@ -128,10 +119,12 @@ __global__ void __launch_bounds__(kThreads, 2)
     extern __shared__ uint8_t smem_raw[];
     const uint32_t raw = smem_u32(smem_raw);
     uint8_t* smem = smem_raw + ((1024 - (raw & 1023)) & 1023);
+    using Y = Lay<BWD>;
+    constexpr int kStages = Y::kStages;
     uint8_t* sa = smem;
-    uint8_t* sb = sa + kABytes;
-    uint8_t* stg_all = sb + kStages * kChunkBytes;
-    uint64_t* bars = reinterpret_cast<uint64_t*>(stg_all + kStgBytes);
+    uint8_t* sb = sa + kABytes;  // stage s: K / V chunk, then (backward) the P chunk
+    uint8_t* stg_all = sb + kStages * Y::kStageBytes;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(stg_all + Y::kStgBytes);
     uint64_t* qfull = bars;
     uint64_t* full = bars + 1;
     uint64_t* empty = full + kStages;
@@ -152,7 +145,7 @@ __global__ void __launch_bounds__(kThreads, 2)
         mbar_init(qfull, 1);
         for (int s = 0; s < kStages; ++s) {
             mbar_init(&full[s], 1);
-            mbar_init(&empty[s], 1);
+            mbar_init(&empty[s], BWD ? 5 : 1);  // bwd: the MMA and the 4 row warps (P read, dS stored)
         }
         for (int b = 0; b < 2; ++b) {
             mbar_init(&sfull[b], 1);
@@ -181,10 +174,12 @@ __global__ void __launch_bounds__(kThreads, 2)
         for (int pass = 0; pass < kPasses; ++pass)
             for (int j = 0; j < nch; ++j) {
                 mbar_wait(&empty[stage], phase ^ 1);
-                mbar_arrive_expect_tx(&full[stage], kboxes * BKV * 128);
+                uint8_t* sst = sb + stage * Y::kStageBytes;
+                mbar_arrive_expect_tx(&full[stage], kboxes * BKV * 128 + (BWD ? kPChunkBytes : 0));
                 for (int kb = 0; kb < kboxes; ++kb)
-                    tma_load_2d(sb + stage * kChunkBytes + kb * BKV * 128, &tma_b, &full[stage], bcol + kb * 64,
-                                brow + j * BKV);
+                    tma_load_2d(sst + kb * BKV * 128, &tma_b, &full[stage], bcol + kb * 64, brow + j * BKV);
+                if constexpr (BWD)  // P[z, mt*128 .. +128, j*64 .. +64]
+                    tma_load_2d(sst + kChunkBytes, &tma_p, &full[stage], j * BKV, z * p.L + mt * BQ);
                 if (++stage == kStages) {
                     stage = 0;
                     phase ^= 1;
@@ -202,7 +197,7 @@ __global__ void __launch_bounds__(kThreads, 2)
                 mbar_wait(&full[stage], phase);
                 mbar_wait(&sempty[buf], bphase ^ 1);
                 tc_fence_after();
-                const uint32_t a_base = smem_u32(sa), b_base = smem_u32(sb + stage * kChunkBytes);
+                const uint32_t a_base = smem_u32(sa), b_base = smem_u32(sb + stage * Y::kStageBytes);
                 for (int kk = 0; kk < ksteps; ++kk) {
                     const uint64_t ad = make_sdesc(a_base + (kk >> 2) * (BQ * 128) + (kk & 3) * 32, 16, 1024);
                     const uint64_t bd = make_sdesc(b_base + (kk >> 2) * (BKV * 128) + (kk & 3) * 32, 16, 1024);
@@ -229,7 +224,6 @@ __global__ void __launch_bounds__(kThreads, 2)
         uint8_t* stg = stg_all + q * 2 * kSlot;
         int slot_idx = 0;
         const int out_row = z * p.L + mt * BQ + q * 32;
-        const __nv_bfloat16* prow = BWD ? p.p_in + (static_cast<size_t>(z) * p.L + mt * BQ + r) * p.L : nullptr;
         int buf = 0;
         uint32_t bphase = 0;
         // scores are raw q.k; softmax works in log2 units u = s * cs
@@ -289,25 +283,36 @@ __global__ void __launch_bounds__(kThreads, 2)
         } else {
             // D = dO[row] . O[row] over this head's d_head columns (= rowsum(P * dP))
             const size_t grow = static_cast<size_t>(zb) * p.L + qi;
-            const uint4* d4 = reinterpret_cast<const uint4*>(p.d_o + grow * p.ld_do + zh * p.dh);
+            // dO[row] from the A tile (2 x 128-B SWIZZLE_128B boxes), O[row] from global in 2 batches
             const uint4* o4 = reinterpret_cast<const uint4*>(p.o + grow * p.ld_o + zh * p.dh);
+            mbar_wait(qfull, 0);
             float acc = 0.f;
-            for (int c = 0; c < p.dh / 8; ++c) {
-                const uint4 a = __ldg(d4 + c), b = __ldg(o4 + c);
-                const uint32_t wa[4] = {a.x, a.y, a.z, a.w}, wb[4] = {b.x, b.y, b.z, b.w};
+            for (int half = 0; half < p.dh / 64; ++half) {
+                uint4 b[8];
 #pragma unroll
-                for (int k = 0; k < 4; ++k)
-                    acc += __uint_as_float(wa[k] << 16) * __uint_as_float(wb[k] << 16) +
-                           __uint_as_float(wa[k] & 0xffff0000u) * __uint_as_float(wb[k] & 0xffff0000u);
+                for (int c = 0; c < 8; ++c) b[c] = __ldg(o4 + half * 8 + c);
+                const uint32_t arow_s = smem_u32(sa + half * BQ * 128) + r * 128;
+#pragma unroll
+                for (int c = 0; c < 8; ++c) {
+                    uint32_t a0, a1, a2, a3;
+                    asm volatile("ld.shared.v4.b32 {%0,%1,%2,%3}, [%4];"
+                                 : "=r"(a0), "=r"(a1), "=r"(a2), "=r"(a3)
+                                 : "r"(arow_s + ((c ^ (r & 7)) << 4)));
+                    const uint32_t wa[4] = {a0, a1, a2, a3}, wb[4] = {b[c].x, b[c].y, b[c].z, b[c].w};
+#pragma unroll
+                    for (int k = 0; k < 4; ++k)
+                        acc += __uint_as_float(wa[k] << 16) * __uint_as_float(wb[k] << 16) +
+                               __uint_as_float(wa[k] & 0xffff0000u) * __uint_as_float(wb[k] & 0xffff0000u);
+                }
             }
             bias = acc;
         }
         if (r == 0) trace(p, 2);
         // ---------------- probabilities (fwd pass 1) / score gradients (bwd)
+        int stage = 0;
+        uint32_t sphase = 0;
         for (int j = 0; j < nch; ++j) {
             const int c0 = j * BKV;
-            float v[64];
-            if constexpr (BWD) load_p64(prow + c0, v);  // in flight while the MMA finishes
             uint32_t ra[32], rb[32];
             mbar_wait(&sfull[buf], bphase);
             tc_fence_after();
@@ -322,6 +327,7 @@ __global__ void __launch_bounds__(kThreads, 2)
                 bphase ^= 1;
             }
             if constexpr (!BWD) {
+                float v[64];
                 if (c0 + BKV <= valid) {
 #pragma unroll
                     for (int jj = 0; jj < 32; ++jj) {
@@ -335,25 +341,56 @@ __global__ void __launch_bounds__(kThreads, 2)
                         v[32 + jj] = (c0 + 32 + jj < valid) ? fast_exp2(fmaf(__uint_as_float(rb[jj]), cs, -bias)) : 0.f;
                     }
                 }
-            } else {
 #pragma unroll
-                for (int jj = 0; jj < 32; ++jj) {
-                    v[jj] = p.scale * v[jj] * (__uint_as_float(ra[jj]) - bias);
-                    v[32 + jj] = p.scale * v[32 + jj] * (__uint_as_float(rb[jj]) - bias);
+                for (int h = 0; h < 2; ++h) {
+                    uint8_t* slot = stg + slot_idx * kSlot;
+                    slot_idx ^= 1;
+                    if (lane == 0) bulk_wait_read<1>();  // the store issued from this slot two boxes ago has read it
+                    __syncwarp();
+                    stage_bf16(slot, lane, v + 32 * h);
+                    fence_async_smem();
+                    __syncwarp();
+                    if (lane == 0) {
+                        tma_store_2d(&tma_out, slot, c0 + 32 * h, out_row);
+                        bulk_commit();
+                    }
                 }
-            }
+            } else {
+                // this row's 64 P values sit in the stage's P chunk (128-B rows, SWIZZLE_128B:
+                // 16-B piece k of row r at k ^ (r & 7)); dS overwrites them in place and
+                // the warp's 32 x 64 box is stored from there
+                const uint32_t prow_s = smem_u32(sb + stage * Y::kStageBytes + kChunkBytes) + r * 128;
 #pragma unroll
-            for (int h = 0; h < 2; ++h) {
-                uint8_t* slot = stg + slot_idx * kSlot;
-                slot_idx ^= 1;
-                if (lane == 0) bulk_wait_read<1>();  // the store issued from this slot two boxes ago has read it
-                __syncwarp();
-                stage_bf16(slot, lane, v + 32 * h);
+                for (int k = 0; k < 8; ++k) {
+                    const uint32_t addr = prow_s + ((k ^ (r & 7)) << 4);
+                    uint32_t w0, w1, w2, w3;
+                    asm volatile("ld.shared.v4.b32 {%0,%1,%2,%3}, [%4];"
+                                 : "=r"(w0), "=r"(w1), "=r"(w2), "=r"(w3)
+                                 : "r"(addr));
+                    const uint32_t w[4] = {w0, w1, w2, w3};
+                    float o[8];
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) {
+                        const int c = k * 8 + 2 * e;  // column inside the chunk
+                        const float d0 = __uint_as_float(c < 32 ? ra[c] : rb[c - 32]);
+                        const float d1 = __uint_as_float(c + 1 < 32 ? ra[c + 1] : rb[c - 31]);
+                        o[2 * e] = p.scale * __uint_as_float(w[e] << 16) * (d0 - bias);
+                        o[2 * e + 1] = p.scale * __uint_as_float(w[e] & 0xffff0000u) * (d1 - bias);
+                    }
+                    st_shared_v4(addr, pack_bf16(o[0], o[1]), pack_bf16(o[2], o[3]), pack_bf16(o[4], o[5]),
+                                 pack_bf16(o[6], o[7]));
+                }
                 fence_async_smem();
                 __syncwarp();
                 if (lane == 0) {
-                    tma_store_2d(&tma_out, slot, c0 + 32 * h, out_row);
+                    tma_store_2d(&tma_out, sb + stage * Y::kStageBytes + kChunkBytes + q * 32 * 128, c0, out_row);
                     bulk_commit();
+                    bulk_wait_read<0>();  // the box has left smem: the stage may be refilled
+                    mbar_arrive(&empty[stage]);
+                }
+                if (++stage == kStages) {
+                    stage = 0;
+                    sphase ^= 1;
                 }
             }
         }
@@ -463,32 +500,27 @@ int launch(const void* a, int lda, int a_cols, int a_col0, const void* b, int ld
                 lda % 8))
         return invalid("attention: dO and O must be 16-byte aligned bf16 rows");
     const long long T = static_cast<long long>(B) * L, rows_out = static_cast<long long>(B) * H * L;
-    CUtensorMap ta, tb, to;
+    CUtensorMap ta, tb, tp{}, to;
+    // forward P: 32 x 32 boxes (SWIZZLE_64B staging); backward dS: 32 rows x 64 keys, in place of
+    // the P chunk loaded with 128 x 64 boxes (SWIZZLE_128B)
     if (map_bf16(&ta, a, T, a_cols, lda, 64, BQ, CU_TENSOR_MAP_SWIZZLE_128B) ||
         map_bf16(&tb, b, T, b_cols, ldb, 64, BKV, CU_TENSOR_MAP_SWIZZLE_128B) ||
-        map_bf16(&to, out, rows_out, L, L, 32, 32, CU_TENSOR_MAP_SWIZZLE_64B))
+        (BWD ? map_bf16(&to, out, rows_out, L, L, 64, 32, CU_TENSOR_MAP_SWIZZLE_128B)
+             : map_bf16(&to, out, rows_out, L, L, 32, 32, CU_TENSOR_MAP_SWIZZLE_64B)))
         return invalid("attention: tensor map encoding failed");
+    if (BWD && map_bf16(&tp, pin, rows_out, L, L, 64, BQ, CU_TENSOR_MAP_SWIZZLE_128B))
+        return invalid("attention: tensor map encoding failed (P)");
     auto kern = k_attn_chunks<BWD>;
+    constexpr int kSmem = Lay<BWD>::kSmem;
     static bool attr = false;
     if (!attr) {
         SWARM_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem));
+        SWARM_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
         attr = true;
     }
-    Params p{B,
-             H,
-             L,
-             dh,
-             causal,
-             a_col0,
-             b_col0,
-             scale,
-             static_cast<const __nv_bfloat16*>(pin),
-             static_cast<const __nv_bfloat16*>(a),
-             static_cast<const __nv_bfloat16*>(o),
-             lda,
-             ld_o,
+    Params p{B, H, L, dh, causal, a_col0, b_col0, scale, static_cast<const __nv_bfloat16*>(o), ld_o,
              trace_enabled() ? 1 : 0};
-    SWARM_CUDA_TRY(launch_pdl(kern, dim3(B * H * (L / BQ)), dim3(kThreads), kSmem, st, ta, tb, to, p));
+    SWARM_CUDA_TRY(launch_pdl(kern, dim3(B * H * (L / BQ)), dim3(kThreads), kSmem, st, ta, tb, tp, to, p));
     SWARM_LAUNCH_CHECK("k_attn_chunks");
     return SWARM_OK;
 }
