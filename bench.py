@@ -302,6 +302,49 @@ TRAIN_STAGES = 4
 TRAIN_MICROBATCHES = 32
 
 
+def cpu_block_reference_steps(model: str, steps: int, warmup: int, total_budget_s: float = 90.0):
+    """--impl reference, train: the CPU block oracle timed as K steps after W
+    warm-ups, each step a bounded sample (whole-microbatch fwd+bwd passes through
+    one block, as many as fit the per-step share of ~90 s), extrapolated per token
+    to the full model exactly like cpu_block_baseline."""
+    import torch
+
+    from oracle import block_oracle as BO
+    from paper_2301_11913_b200.swarm import PRESETS
+    m = PRESETS[model]
+    threads = os.cpu_count() or 1
+    torch.set_num_threads(threads)
+    g = torch.Generator().manual_seed(0)
+    d, F = m.d_model, m.d_ffn
+    W = {"wqkv": torch.randn(3 * d, d, generator=g) * 0.02, "wo": torch.randn(d, d, generator=g) * 0.02,
+         "w1": torch.randn(F, d, generator=g) * 0.02, "w2": torch.randn(d, F, generator=g) * 0.02,
+         "ln1_g": torch.ones(d), "ln1_b": torch.zeros(d), "ln2_g": torch.ones(d), "ln2_b": torch.zeros(d)}
+    for v in W.values():
+        v.requires_grad_(True)
+    x = torch.randn(m.tokens, d, generator=g, requires_grad=True)
+
+    def one():
+        y = BO.block(x, W, m.micro_batch, m.seq_len, m.n_heads, True)
+        y.backward(torch.ones_like(y))
+
+    t_one = None
+    for _ in range(max(1, warmup)):
+        t0 = time.perf_counter()
+        one()
+        t_one = time.perf_counter() - t0
+    reps = max(1, int(total_budget_s / max(1, steps + warmup) / t_one))
+    t0 = time.perf_counter()
+    for _ in range(steps * reps):
+        one()
+    dt = (time.perf_counter() - t0) / (steps * reps)
+    layers = m.layers_per_stage * TRAIN_STAGES
+    tok_s = m.tokens / (dt * layers)
+    sample = (f"fp32 torch-CPU block oracle: {steps} step(s) x {reps} fwd+bwd pass(es) of a {m.tokens}-token "
+              f"microbatch through one d={d} block ({dt:.2f} s each) after {max(1, warmup)} warm-up pass(es), "
+              f"extrapolated to {layers} layers")
+    return tok_s, threads, sample
+
+
 def cpu_block_baseline(model: str, budget_s: float = 20.0):
     """The fp32 CPU block oracle (oracle/block_oracle.py, torch CPU on all host
     threads) timed on a bounded sample: fwd+bwd of whole microbatches through
@@ -336,6 +379,18 @@ def cpu_block_baseline(model: str, budget_s: float = 20.0):
     sample = (f"fp32 torch-CPU block oracle, fwd+bwd of {reps} microbatch(es) of {m.tokens} tokens through one "
               f"d={d} block ({dt:.2f} s each), extrapolated to {layers} layers")
     return tok_s, threads, sample
+
+
+def train_config(args) -> dict:
+    """The configs[2] workload description shared by both arms' JSON lines."""
+    from paper_2301_11913_b200.swarm import PRESETS
+    m = PRESETS[args.model]
+    S, M = args.stages, args.microbatches
+    return {"workload": f"BASELINE configs[2]: {S} stages, {m.layers_per_stage} layers/stage, d_model {m.d_model}, "
+                        f"{m.n_heads} heads, seq {m.seq_len}, int8 boundary codec, stochastic wiring + intra-stage "
+                        "all-reduce",
+            "model": args.model, "global_batch": M * m.micro_batch, "micro_batch": m.micro_batch,
+            "microbatches_per_step": M, "seq_len": m.seq_len, "tokens_per_step": M * m.tokens, "vocab": m.vocab}
 
 
 def bench_train(args, world, rank, local):
@@ -432,12 +487,7 @@ def bench_train(args, world, rank, local):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
         "data": "synthetic tokens uniform over the vocab, random-init weights",
-        "config": {"workload": f"BASELINE configs[2]: {S} stages, {mcfg.layers_per_stage} layers/stage, "
-                               f"d_model {mcfg.d_model}, {mcfg.n_heads} heads, seq {mcfg.seq_len}, int8 boundary codec, "
-                               "stochastic wiring + intra-stage all-reduce",
-                   "model": args.model, "global_batch": M * mcfg.micro_batch, "micro_batch": mcfg.micro_batch,
-                   "microbatches_per_step": M, "seq_len": mcfg.seq_len, "tokens_per_step": tokens_step,
-                   "vocab": mcfg.vocab, "parallelism": placement, "optimizer": "AdamW (fused, fp32 master)",
+        "config": {**train_config(args), "parallelism": placement, "optimizer": "AdamW (fused, fp32 master)",
                    "l2": "per-step working set (weights + activations, GBs) far exceeds L2; no flush needed",
                    "mean_loss": mean_loss, "model_tflops_per_s": model_tflops,
                    "model_flops_per_token": mcfg.flops_per_token(S)},
@@ -555,21 +605,23 @@ def run_reference(args, world, rank):
     if args.workload == "train":
         from paper_2301_11913_b200.swarm import PRESETS
         m = PRESETS[args.model]
-        tok_s, thr, sample = cpu_block_baseline(args.model, budget_s=30.0)
+        tok_s, thr, sample = cpu_block_reference_steps(args.model, args.steps, args.warmup)
         return {"impl": "reference", "metric": "training tokens/s (SWARM pipeline)", "value": tok_s,
-                "unit": "tokens/s", "n_gpus": world, "steps": 1, "warmup": 0,
+                "unit": "tokens/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
                 "ms_per_step": TRAIN_MICROBATCHES * m.tokens / tok_s * 1e3, "higher_is_better": True,
                 "scaling": "strong", "vs_baseline": None, "dtype": "f32 (CPU)", "data": "synthetic",
-                "config": {"workload": "CPU block oracle on a bounded sample of configs[2]", "model": args.model},
+                "config": {**train_config(args), "parallelism": "CPU (rank 0 only)"},
                 "cpu_baseline": {"value": tok_s, "unit": "tokens/s", "cores": thr, "kind": "port", "sample": sample},
                 "e2e": {"value": tok_s, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     threads = os.cpu_count() or 1
-    steps = max(1, min(args.steps, 3))
-    gbs, kind, thr, sample = cpu_reference_codec(steps, min(args.warmup, 1), threads)
+    # each step is the bounded 256 MiB sample (~0.07 s on 16 threads): K steps fit a few minutes;
+    # the cap only guards an extreme K
+    steps = max(1, min(args.steps, 2000))
+    gbs, kind, thr, sample = cpu_reference_codec(steps, min(args.warmup, 3), threads)
     bytes_step = (CODEC_BYTES_Q + CODEC_BYTES_DQ) * (CPU_SAMPLE_N / CODEC_N)
     return {"impl": "reference",
             "metric": "int8 codec GB/s (blockwise absmax quantize+dequantize, algorithmic bytes)",
-            "value": gbs, "unit": "GB/s", "n_gpus": world, "steps": steps, "warmup": min(args.warmup, 1),
+            "value": gbs, "unit": "GB/s", "n_gpus": world, "steps": steps, "warmup": min(args.warmup, 3),
             "ms_per_step": bytes_step / (gbs * 1e9) * 1e3, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64 (reference std::vector<double>)", "data": "synthetic",
             "config": {"workload": "codec sweep, reference CPU path on a bounded sample", "block_size": CODEC_BS},
