@@ -24,6 +24,7 @@
 #include <algorithm>
 #include <cstdlib>
 #include <unordered_map>
+#include <utility>
 
 #include "common.cuh"
 #include "sm100.cuh"
@@ -68,6 +69,49 @@ __device__ __forceinline__ float fast_exp2(float x) {
     float y;
     asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
     return y;
+}
+
+// 2^x for x <= 0 on the FMA pipe (FlashAttention-4's trick to relieve the SFU):
+// x = n + f with n = rint(x) via the 1.5 * 2^23 magic add, 2^f on [-0.5, 0.5] by a
+// degree-3 minimax polynomial (max relative error 2.1e-4, far below bf16's 2^-8),
+// then n is added to the exponent field.  x is clamped at -125 (result ~2^-125).
+__device__ __forceinline__ float poly_exp2(float x) {
+    x = fmaxf(x, -125.f);
+    const float t = __fadd_rn(x, 12582912.f);
+    const float f = __fsub_rn(x, __fsub_rn(t, 12582912.f));
+    const float p = fmaf(fmaf(fmaf(5.484800413e-02f, f, 2.418066114e-01f), f, 6.932482123e-01f), f, 9.999886751e-01f);
+    return __int_as_float(__float_as_int(p) + (__float_as_int(t) << 23));
+}
+// a quarter of the exponentials go to the FMA pipe, the rest to the SFU
+template <int J>
+__device__ __forceinline__ float mixed_exp2(float x) {
+    if constexpr ((J & 3) == 0) return poly_exp2(x);
+    else return fast_exp2(x);
+}
+
+template <int... J>
+__device__ __forceinline__ float sum_exp2_impl(const uint32_t (&ra)[32], const uint32_t (&rb)[32], float cs, float nb,
+                                               std::integer_sequence<int, J...>) {
+    float acc[2] = {0.f, 0.f};
+    ((acc[J & 1] += mixed_exp2<J>(fmaf(__uint_as_float(ra[J]), cs, nb)) +
+                    mixed_exp2<J + 1>(fmaf(__uint_as_float(rb[J]), cs, nb))),
+     ...);
+    return acc[0] + acc[1];
+}
+// sum over the 64 scores of a chunk of 2^(s * cs + nb)
+__device__ __forceinline__ float sum_exp2_64(const uint32_t (&ra)[32], const uint32_t (&rb)[32], float cs, float nb) {
+    return sum_exp2_impl(ra, rb, cs, nb, std::make_integer_sequence<int, 32>{});
+}
+template <int... J>
+__device__ __forceinline__ void exp2_impl(const uint32_t (&ra)[32], const uint32_t (&rb)[32], float cs, float nb,
+                                          float* v, std::integer_sequence<int, J...>) {
+    ((v[J] = mixed_exp2<J>(fmaf(__uint_as_float(ra[J]), cs, nb)),
+      v[32 + J] = mixed_exp2<J + 2>(fmaf(__uint_as_float(rb[J]), cs, nb))),
+     ...);
+}
+__device__ __forceinline__ void exp2_64(const uint32_t (&ra)[32], const uint32_t (&rb)[32], float cs, float nb,
+                                        float* v) {
+    exp2_impl(ra, rb, cs, nb, v, std::make_integer_sequence<int, 32>{});
 }
 
 __device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
@@ -265,10 +309,7 @@ __global__ void __launch_bounds__(kThreads, 2)
                 const float nmu = fmaxf(mu, cm * cs);
                 float add = 0.f;
                 if (full) {
-#pragma unroll
-                    for (int jj = 0; jj < 32; ++jj)
-                        add += fast_exp2(fmaf(__uint_as_float(ra[jj]), cs, -nmu)) +
-                               fast_exp2(fmaf(__uint_as_float(rb[jj]), cs, -nmu));
+                    add = sum_exp2_64(ra, rb, cs, -nmu);
                 } else {
 #pragma unroll
                     for (int jj = 0; jj < 32; ++jj) {
@@ -329,11 +370,7 @@ __global__ void __launch_bounds__(kThreads, 2)
             if constexpr (!BWD) {
                 float v[64];
                 if (c0 + BKV <= valid) {
-#pragma unroll
-                    for (int jj = 0; jj < 32; ++jj) {
-                        v[jj] = fast_exp2(fmaf(__uint_as_float(ra[jj]), cs, -bias));
-                        v[32 + jj] = fast_exp2(fmaf(__uint_as_float(rb[jj]), cs, -bias));
-                    }
+                    exp2_64(ra, rb, cs, -bias, v);
                 } else {
 #pragma unroll
                     for (int jj = 0; jj < 32; ++jj) {
