@@ -480,6 +480,11 @@ def bench_train(args, world, rank, local):
                        "calls_per_step": int(cn * visits_per_stage)}
                  for cat, (cms, cn) in pipe.last_breakdown.items()}
     model_tflops = value * mcfg.flops_per_token(S) / 1e12
+    gemm_traffic = {}
+    prof = os.path.join(ROOT, "profiles", "ncu_gemm_qkv_traffic.json")
+    if os.path.exists(prof):  # DRAM bytes of one representative launch (QKV) from the committed ncu capture
+        with open(prof) as f:
+            gemm_traffic = json.load(f)
     placement = (f"{S} stages x {pipe.P} peer(s) per stage" if world >= S else
                  f"{world} GPU(s) x {S // world} stage(s) each")
     line = {
@@ -493,7 +498,8 @@ def bench_train(args, world, rank, local):
                    "model_flops_per_token": mcfg.flops_per_token(S)},
         "roofline": {"bound": "tensor", "kernel": "k_gemm (tcgen05 bf16, every block/attention/head GEMM)",
                      "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
-                     "traffic": None, "peak_source": pk["source"] + " bf16 sustained",
+                     "traffic": gemm_traffic.get("dram_bytes_per_launch"),
+                     "traffic_note": gemm_traffic.get("note"), "peak_source": pk["source"] + " bf16 sustained",
                      "gemm_share_of_step": gemm_share,
                      "note": "GEMM events bracket every GEMM of the first visit of each (stage, direction) per step "
                              "(run eagerly); the other visits replay CUDA graphs of the same kernels",
