@@ -101,7 +101,8 @@ int swarm_layer_norm_forward(const void* x, int dtype, size_t rows, size_t cols,
 /* dx = LN'(dy) (+ dres when non-NULL: the residual branch's gradient, fused),
  * dgain/dbias (float, cols) written, or added when `accumulate` != 0 (gradient
  * accumulation over microbatches).  `workspace` >= swarm_layer_norm_backward_workspace()
- * bytes of device memory. */
+ * bytes of device memory, zero-filled before its first use (the call leaves it zeroed
+ * again; it must not be shared by concurrent calls). */
 size_t swarm_layer_norm_backward_workspace(size_t rows, size_t cols);
 int swarm_layer_norm_backward(const void* dy, const void* x, int dtype, size_t rows, size_t cols,
                               const float* gain, const float* mean, const float* rstd, const void* dres,

@@ -269,34 +269,6 @@ __global__ void k_col_reduce(const float* __restrict__ part, int nparts, int col
     out[c] = accumulate ? out[c] + s : s;
 }
 
-// Sum of nparts rows of two [nparts, cols] partial arrays (gain and bias
-// gradients) in one launch: CTA = 32 columns x 8 warps, warp w sums parts
-// w, w+8, ... (coalesced 128-B rows), then the 8 warp sums meet in smem in a
-// fixed order (deterministic).  blockIdx.y selects the array.
-__global__ void __launch_bounds__(256) k_col_reduce2(const float* __restrict__ part_g, const float* __restrict__ part_b,
-                                                     int nparts, int cols, float* __restrict__ out_g,
-                                                     float* __restrict__ out_b, int accumulate) {
-    pdl_trigger();
-    pdl_wait();
-    __shared__ float red[8][33];
-    const float* part = blockIdx.y ? part_b : part_g;
-    float* out = blockIdx.y ? out_b : out_g;
-    if (!out) return;
-    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    const int c = blockIdx.x * 32 + lane;
-    float s = 0.f;
-    if (c < cols)
-        for (int p = w; p < nparts; p += 8) s += part[static_cast<size_t>(p) * cols + c];
-    red[w][lane] = s;
-    __syncthreads();
-    if (w == 0 && c < cols) {
-        float t = 0.f;
-#pragma unroll
-        for (int k = 0; k < 8; ++k) t += red[k][lane];
-        out[c] = accumulate ? out[c] + t : t;
-    }
-}
-
 // fp64 API path: one CTA per row, three passes over global, verbatim formula.
 __global__ void k_ln_fwd_f64(const double* __restrict__ x, int rows, int cols, const double* __restrict__ gain,
                              const double* __restrict__ bias, double eps, double* __restrict__ out) {
@@ -495,10 +467,15 @@ __global__ void __launch_bounds__(256) k_ln_bwd_dx_w(const uint4* __restrict__ d
 
 // dgain/dbias partials: CTA (column strip of 64, row split) with 8 column
 // vectors x 32 row lanes; deterministic (fixed reduction order).
+// The last CTA of each 64-column strip to finish (a self-resetting arrival
+// counter per strip) sums the strip's split partials in split order and writes
+// / accumulates dgain, dbias: one launch, still deterministic.
 __global__ void __launch_bounds__(256) k_ln_bwd_dgb(const uint4* __restrict__ dy, const uint4* __restrict__ x, int rows,
                                                     int cols, const float* __restrict__ mean,
                                                     const float* __restrict__ rstd, int rows_per_split,
-                                                    float* __restrict__ part_g, float* __restrict__ part_b) {
+                                                    float* __restrict__ part_g, float* __restrict__ part_b,
+                                                    int* __restrict__ strip_count, float* __restrict__ dg,
+                                                    float* __restrict__ db, int accumulate) {
     pdl_trigger();
     pdl_wait();
     __shared__ float sg[32][65], sb[32][65];
@@ -534,6 +511,44 @@ __global__ void __launch_bounds__(256) k_ln_bwd_dgb(const uint4* __restrict__ dy
         const int gcol = blockIdx.x * 64 + col;
         if (gcol < cols) (isg ? part_g : part_b)[static_cast<size_t>(blockIdx.y) * cols + gcol] = acc;
     }
+    __threadfence();
+    __syncthreads();
+    __shared__ int is_last;
+    if (threadIdx.x == 0) is_last = atomicAdd(&strip_count[blockIdx.x], 1) == static_cast<int>(gridDim.y) - 1;
+    __syncthreads();
+    if (!is_last) return;
+    __threadfence();
+    // 128 outputs (64 columns x {gain, bias}) x 2 halves of the splits; each half
+    // keeps 4 loads in flight, the halves meet in smem in a fixed order
+    {
+        const int o = threadIdx.x & 127, hsel = threadIdx.x >> 7;
+        const int col = o & 63;
+        const bool isg = o < 64;
+        const int gcol = blockIdx.x * 64 + col;
+        const int ns = static_cast<int>(gridDim.y), k0 = hsel ? ns / 2 : 0, k1 = hsel ? ns : ns / 2;
+        float acc = 0.f;
+        if (gcol < cols) {
+            const float* part = (isg ? part_g : part_b) + gcol;
+            int k = k0;
+            for (; k + 4 <= k1; k += 4) {
+                const float a0 = __ldcg(part + static_cast<size_t>(k) * cols);
+                const float a1 = __ldcg(part + static_cast<size_t>(k + 1) * cols);
+                const float a2 = __ldcg(part + static_cast<size_t>(k + 2) * cols);
+                const float a3 = __ldcg(part + static_cast<size_t>(k + 3) * cols);
+                acc += ((a0 + a1) + (a2 + a3));
+            }
+            for (; k < k1; ++k) acc += __ldcg(part + static_cast<size_t>(k) * cols);
+        }
+        float* red = &sg[0][0];  // reuse the partial tile (32 x 65 floats) for the 2 x 128 half sums
+        red[hsel * 128 + o] = acc;
+        __syncthreads();
+        if (hsel == 0 && gcol < cols) {
+            float* out = isg ? dg : db;
+            const float t = red[o] + red[128 + o];
+            if (out) out[gcol] = accumulate ? out[gcol] + t : t;
+        }
+    }
+    if (threadIdx.x == 0) strip_count[blockIdx.x] = 0;  // ready for the next launch
 }
 
 template <int NV>
@@ -588,6 +603,7 @@ int ln_fwd_launch(const T* x, int rows, int cols, const float* g, const float* b
     return SWARM_OK;
 }
 
+constexpr size_t kLnCounterBytes = 4096;
 int ln_bwd_parts(size_t rows) { return static_cast<int>(std::min<size_t>(rows, 2 * 148)); }
 
 template <typename T>
@@ -602,15 +618,13 @@ int ln_bwd_launch(const T* dy, const T* x, int rows, int cols, const float* g, c
             if (dg || db) {
                 const int splits = std::max(1, std::min(ln_bwd_parts(rows), (rows + 63) / 64));
                 const int rps = (rows + splits - 1) / splits;
-                float* pg = ws;
-                float* pb = ws + static_cast<size_t>(splits) * cols;
+                int* strips = reinterpret_cast<int*>(ws);  // fixed counter area, see swarm_layer_norm_backward_workspace
+                float* pg = ws + kLnCounterBytes / sizeof(float);
+                float* pb = pg + static_cast<size_t>(splits) * cols;
                 launch_pdl(k_ln_bwd_dgb, dim3((cols + 63) / 64, splits), dim3(256), 0, st,
                            reinterpret_cast<const uint4*>(dy), reinterpret_cast<const uint4*>(x), rows, cols, mean,
-                           rstd, rps, pg, pb);
+                           rstd, rps, pg, pb, strips, dg, db, accumulate);
                 SWARM_LAUNCH_CHECK("k_ln_bwd_dgb");
-                launch_pdl(k_col_reduce2, dim3((cols + 31) / 32, 2), dim3(256), 0, st, pg, pb, splits, cols, dg, db,
-                           accumulate);
-                SWARM_LAUNCH_CHECK("k_col_reduce2");
             }
             return SWARM_OK;
         }
@@ -618,8 +632,8 @@ int ln_bwd_launch(const T* dy, const T* x, int rows, int cols, const float* g, c
     const int parts = ln_bwd_parts(rows);
     const int rpc = (rows + parts - 1) / parts;
     const int grid = (rows + rpc - 1) / rpc;
-    float* pg = ws;
-    float* pb = ws + static_cast<size_t>(parts) * cols;
+    float* pg = ws + kLnCounterBytes / sizeof(float);
+    float* pb = pg + static_cast<size_t>(parts) * cols;
     constexpr int V = sizeof(T) == 2 ? 8 : 4;
     if (cols % V == 0 && al(x, 16) && al(dy, 16) && al(dx, 16) && (!dres || al(dres, 16)))
         k_ln_bwd<T, V><<<grid, kLnThreads, 0, st>>>(dy, x, rows, cols, g, mean, rstd, dres, dx, pg, pb, rpc);
@@ -734,7 +748,10 @@ int swarm_matvec_f64(const double* x, size_t rows, const double* w, size_t cols,
 }
 
 size_t swarm_layer_norm_backward_workspace(size_t rows, size_t cols) {
-    return 2 * static_cast<size_t>(ln_bwd_parts(rows)) * cols * sizeof(float);
+    // a fixed area of arrival counters (one per 64-column strip, any width up to 64K
+    // columns, so one workspace serves calls of different widths), then the split
+    // partials of dgain and dbias
+    return kLnCounterBytes + 2 * static_cast<size_t>(ln_bwd_parts(rows)) * cols * sizeof(float);
 }
 
 int swarm_layer_norm_backward(const void* dy, const void* x, int dtype, size_t rows, size_t cols, const float* gain,

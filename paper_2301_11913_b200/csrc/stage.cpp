@@ -79,8 +79,9 @@ struct swarm_stage {
     // fill the SMs the data-gradient chain leaves idle (GEMM wave tails)
     cudaStream_t side = nullptr;
     void* skws[2] = {nullptr, nullptr};  // GEMM stream-K scratch: visit stream, side stream
-    cudaEvent_t ev_fork[4] = {nullptr, nullptr, nullptr, nullptr};
+    cudaEvent_t ev_fork[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
     cudaEvent_t ev_join = nullptr;
+    cudaEvent_t ev_dq = nullptr;  // dQ (side stream) complete
     // visit profiling (bench.py's live roofline and step breakdown): event pairs
     // around each GEMM (category 0) and each other kernel call of a profiled visit
     bool prof_on = false;
@@ -302,6 +303,12 @@ int fork_side(swarm_stage* s, cudaStream_t main, int i) {
     if (cudaEventRecord(s->ev_fork[i], main) != cudaSuccess) return SWARM_E_CUDA;
     return cudaStreamWaitEvent(s->side, s->ev_fork[i], 0) == cudaSuccess ? SWARM_OK : SWARM_E_CUDA;
 }
+// main waits for the side stream up to this point (event `e` recorded on it)
+int wait_side(swarm_stage* s, cudaStream_t main, cudaEvent_t e) {
+    if (t_prof) return SWARM_OK;
+    if (cudaEventRecord(e, s->side) != cudaSuccess) return SWARM_E_CUDA;
+    return cudaStreamWaitEvent(main, e, 0) == cudaSuccess ? SWARM_OK : SWARM_E_CUDA;
+}
 // main waits for everything enqueued on the side stream so far
 int join_side(swarm_stage* s, cudaStream_t main) {
     if (t_prof) return SWARM_OK;
@@ -376,13 +383,16 @@ int block_backward(swarm_stage* s, const Act& A, const bf16* dy, bf16* dx, const
                 1.f, st));
         PTRY(SWARM_PROF_ATTENTION, st, swarm_attn_softmax_backward(A.P, s->dP, BHL, L, scale, s->dS, st));
     }
-    // dQ = dS K ; dK = dS^T Q ; dV = P^T dO   (all read in place, written into dqkv)
+    // dQ = dS K ; dK = dS^T Q ; dV = P^T dO   (all read in place, written into dqkv); dQ runs on the
+    // side stream beside dK, dV (three independent GEMMs of 1.7 waves each fill each other's tails)
+    TRY(fork_side(s, st, 4));
     TRY(bmm(s, L, dh, L, {{s->dS, L, BHL, L, false}, H * L, L, 0, 0}, {{A.qkv + d, 3 * d, T, d, true}, L, 0, 0, dh},
-            s->dqkv, 3 * d, L, 0, 0, dh, SWARM_EPI_STORE_BF16, 1.f, st, 1));
+            s->dqkv, 3 * d, L, 0, 0, dh, SWARM_EPI_STORE_BF16, 1.f, side_of(s, st), 1));
     TRY(bmm(s, L, dh, L, {{s->dS, L, BHL, L, true}, H * L, L, 0, 0}, {{A.qkv, 3 * d, T, d, true}, L, 0, 0, dh},
             s->dqkv + d, 3 * d, L, 0, 0, dh, SWARM_EPI_STORE_BF16, 1.f, st, 2));
     TRY(bmm(s, L, dh, L, {{A.P, L, BHL, L, true}, H * L, L, 0, 0}, {{s->dO, d, T, d, true}, L, 0, 0, dh},
             s->dqkv + 2 * d, 3 * d, L, 0, 0, dh, SWARM_EPI_STORE_BF16, 1.f, st, 2));
+    TRY(wait_side(s, st, s->ev_dq));  // dqkv complete on main (the dWqkv fork below then carries it to the side)
     // da = dqkv Wqkv ; dWqkv += dqkv^T a
     TRY(fork_side(s, st, 3));
     TRY(mm(3 * d, d, T, {s->dqkv, 3 * d, T, 3 * d, true}, {A.a, d, T, d, true}, G + W.wqkv, d, SWARM_EPI_ACCUM_F32,
@@ -599,6 +609,7 @@ int create(const swarm_stage_config* c, swarm_stage* s) {
     for (auto& e : s->ev_fork)
         if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) return SWARM_E_CUDA;
     if (cudaEventCreateWithFlags(&s->ev_join, cudaEventDisableTiming) != cudaSuccess) return SWARM_E_CUDA;
+    if (cudaEventCreateWithFlags(&s->ev_dq, cudaEventDisableTiming) != cudaSuccess) return SWARM_E_CUDA;
     TRY(init_params(s, nullptr));
     if (cudaStreamSynchronize(nullptr) != cudaSuccess) return SWARM_E_CUDA;
     return SWARM_OK;
@@ -628,6 +639,7 @@ void swarm_stage_destroy(swarm_stage_t s) {
     for (cudaEvent_t e : s->ev_fork)
         if (e) cudaEventDestroy(e);
     if (s->ev_join) cudaEventDestroy(s->ev_join);
+    if (s->ev_dq) cudaEventDestroy(s->ev_dq);
     if (s->side) cudaStreamDestroy(s->side);
     for (void* p : s->allocations) cudaFree(p);
     delete s;

@@ -118,7 +118,7 @@ def layer_norm_backward(dy: torch.Tensor, x: torch.Tensor, gain: torch.Tensor | 
         dx = torch.empty_like(x)
     dg = torch.empty(cols, dtype=torch.float32, device=x.device)
     db = torch.empty(cols, dtype=torch.float32, device=x.device)
-    ws = torch.empty(L.lib().swarm_layer_norm_backward_workspace(rows, cols), dtype=torch.uint8, device=x.device)
+    ws = torch.zeros(L.lib().swarm_layer_norm_backward_workspace(rows, cols), dtype=torch.uint8, device=x.device)
     rc = L.lib().swarm_layer_norm_backward(_ptr(dy), _ptr(x), _DT[x.dtype], rows, cols, _ptr(gain), _ptr(mean),
                                            _ptr(rstd), _ptr(dres), _ptr(dx), _ptr(dg), _ptr(db), 0, _ptr(ws),
                                            _stream())

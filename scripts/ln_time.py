@@ -13,7 +13,7 @@ g = torch.randn(cols, device="cuda"); b = torch.randn(cols, device="cuda")
 y = torch.empty_like(x); mu = torch.empty(rows, device="cuda"); rs = torch.empty(rows, device="cuda")
 dy = torch.randn_like(x); dres = torch.randn_like(x); dx = torch.empty_like(x)
 dg = torch.zeros(cols, device="cuda"); db = torch.zeros(cols, device="cuda")
-ws = torch.empty(L.lib().swarm_layer_norm_backward_workspace(rows, cols), dtype=torch.uint8, device="cuda")
+ws = torch.zeros(L.lib().swarm_layer_norm_backward_workspace(rows, cols), dtype=torch.uint8, device="cuda")
 lib = L.lib()
 def fwd(st):
     lib.swarm_layer_norm_forward(_ptr(x), _DT[x.dtype], rows, cols, _ptr(g), _ptr(b), 1e-5, _ptr(y), _ptr(mu), _ptr(rs), st)
