@@ -302,7 +302,7 @@ TRAIN_STAGES = 4
 TRAIN_MICROBATCHES = 32
 
 
-def cpu_block_reference_steps(model: str, steps: int, warmup: int, total_budget_s: float = 90.0):
+def cpu_block_reference_steps(m, steps: int, warmup: int, total_budget_s: float = 90.0):
     """--impl reference, train: the CPU block oracle timed as K steps after W
     warm-ups, each step a bounded sample (whole-microbatch fwd+bwd passes through
     one block, as many as fit the per-step share of ~90 s), extrapolated per token
@@ -310,8 +310,6 @@ def cpu_block_reference_steps(model: str, steps: int, warmup: int, total_budget_
     import torch
 
     from oracle import block_oracle as BO
-    from paper_2301_11913_b200.swarm import PRESETS
-    m = PRESETS[model]
     threads = os.cpu_count() or 1
     torch.set_num_threads(threads)
     g = torch.Generator().manual_seed(0)
@@ -345,7 +343,7 @@ def cpu_block_reference_steps(model: str, steps: int, warmup: int, total_budget_
     return tok_s, threads, sample
 
 
-def cpu_block_baseline(model: str, budget_s: float = 20.0):
+def cpu_block_baseline(m, budget_s: float = 20.0):
     """The fp32 CPU block oracle (oracle/block_oracle.py, torch CPU on all host
     threads) timed on a bounded sample: fwd+bwd of whole microbatches through
     ONE transformer block of the named config, extrapolated per token to the
@@ -354,8 +352,6 @@ def cpu_block_baseline(model: str, budget_s: float = 20.0):
     import torch
 
     from oracle import block_oracle as BO
-    from paper_2301_11913_b200.swarm import PRESETS
-    m = PRESETS[model]
     threads = os.cpu_count() or 1
     torch.set_num_threads(threads)
     g = torch.Generator().manual_seed(0)
@@ -381,14 +377,26 @@ def cpu_block_baseline(model: str, budget_s: float = 20.0):
     return tok_s, threads, sample
 
 
-def train_config(args) -> dict:
-    """The configs[2] workload description shared by both arms' JSON lines."""
+def model_config(args):
+    """The named preset, with the microbatch size overridden by --micro-batch
+    (configs[2] at B=4, swept over 1, 2, 4, 8)."""
+    import dataclasses
+
     from paper_2301_11913_b200.swarm import PRESETS
     m = PRESETS[args.model]
+    mb = getattr(args, "micro_batch", None)
+    return dataclasses.replace(m, micro_batch=mb) if mb else m
+
+
+def train_config(args) -> dict:
+    """The configs[2] workload description shared by both arms' JSON lines."""
+    m = model_config(args)
     S, M = args.stages, args.microbatches
-    return {"workload": f"BASELINE configs[2]: {S} stages, {m.layers_per_stage} layers/stage, d_model {m.d_model}, "
-                        f"{m.n_heads} heads, seq {m.seq_len}, int8 boundary codec, stochastic wiring + intra-stage "
-                        "all-reduce",
+    which = {"C": "configs[2]", "D": "configs[3] (paper scale)", "tiny": "configs[0] (tiny)"}[args.model]
+    layers = f"{m.layers_per_stage} {'shared ' if m.shared_layers else ''}layers/stage"
+    codec = f"maxout k={m.maxout_k} + int8 boundary codec" if m.maxout_k > 1 else "int8 boundary codec"
+    return {"workload": f"BASELINE {which}: {S} stages, {layers}, d_model {m.d_model}, {m.n_heads} heads, "
+                        f"seq {m.seq_len}, {codec}, stochastic wiring + intra-stage all-reduce",
             "model": args.model, "global_batch": M * m.micro_batch, "micro_batch": m.micro_batch,
             "microbatches_per_step": M, "seq_len": m.seq_len, "tokens_per_step": M * m.tokens, "vocab": m.vocab}
 
@@ -402,7 +410,7 @@ def bench_train(args, world, rank, local):
     dev = torch.device("cuda", local)
     torch.cuda.set_device(dev)
     L = _lib.lib()
-    mcfg = PRESETS[args.model]
+    mcfg = model_config(args)
     M = args.microbatches
     S = args.stages
     pipe = SwarmPipeline(mcfg, S, n_microbatches=M, seed=1, lr=1e-4, profile=True)
@@ -516,7 +524,7 @@ def bench_train(args, world, rank, local):
         "gpu_launches": int(launches), "clocks": clocks,
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        tok_s, thr, sample = cpu_block_baseline(args.model)
+        tok_s, thr, sample = cpu_block_baseline(mcfg)
         line["cpu_baseline"] = {"value": tok_s, "unit": "tokens/s", "cores": thr, "kind": "port", "sample": sample}
     return line
 
@@ -543,7 +551,7 @@ def bench_failure(args, world, rank, local):
         raise SystemExit("failure workload needs >= 2 peers per stage on average (world >= 2*stages)")
     per = world // S
     layout = [per + 1, per - 1] + [per] * (S - 2)  # stage 1 short one peer
-    mcfg = PRESETS[args.model]
+    mcfg = model_config(args)
     M = args.microbatches
     pipe = SwarmPipeline(mcfg, S, n_microbatches=M, seed=1, lr=1e-4, layout=layout, max_slots=M)
     tok, tgt = synthetic_batch(mcfg, M, seed=7, device=dev)
@@ -610,8 +618,8 @@ def run_reference(args, world, rank):
         return None
     if args.workload == "train":
         from paper_2301_11913_b200.swarm import PRESETS
-        m = PRESETS[args.model]
-        tok_s, thr, sample = cpu_block_reference_steps(args.model, args.steps, args.warmup)
+        m = model_config(args)
+        tok_s, thr, sample = cpu_block_reference_steps(m, args.steps, args.warmup)
         return {"impl": "reference", "metric": "training tokens/s (SWARM pipeline)", "value": tok_s,
                 "unit": "tokens/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
                 "ms_per_step": TRAIN_MICROBATCHES * m.tokens / tok_s * 1e3, "higher_is_better": True,
@@ -644,6 +652,7 @@ def main():
     ap.add_argument("--workload", default="train", choices=["train", "codec", "failure"])
     ap.add_argument("--model", default="C", choices=["C", "D", "tiny"])
     ap.add_argument("--microbatches", type=int, default=TRAIN_MICROBATCHES)
+    ap.add_argument("--micro-batch", type=int, default=None, help="sequences per microbatch (default: the preset's)")
     ap.add_argument("--stages", type=int, default=TRAIN_STAGES, help="pipeline stages (default 4, SURVEY §8(d))")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-codec", action="store_true", help="train: skip the codec sub-measurement")

@@ -315,6 +315,10 @@ __global__ void k_matvec_f64(const double* __restrict__ x, int rows, const doubl
 bool al(const void* p, size_t a) { return (reinterpret_cast<uintptr_t>(p) % a) == 0; }
 
 // ---------------------------------------------- warp-per-row bf16 LayerNorm --
+// Small CTAs (2 warps = 2 rows) so the single wave of rows spreads evenly over
+// the SMs (8-warp CTAs left some SMs with twice the rows of others).
+constexpr int kLnWarpThreads = 64;
+constexpr int kLnRowsPerCta = kLnWarpThreads / 32;
 // cols = 256*NV: each lane holds NV 16-byte vectors (8 bf16) of the row, so a
 // row needs no block barrier and each warp keeps 2*NV loads in flight.  This is
 // the training path (d_model 256..4096); the block-per-row kernels above remain
@@ -356,7 +360,7 @@ __device__ __forceinline__ float wsum(float v) {
 }
 
 template <int NV>
-__global__ void __launch_bounds__(256) k_ln_fwd_w(const uint4* __restrict__ x, int rows, const float* __restrict__ g,
+__global__ void __launch_bounds__(kLnWarpThreads) k_ln_fwd_w(const uint4* __restrict__ x, int rows, const float* __restrict__ g,
                                                   const float* __restrict__ b, float eps, uint4* __restrict__ out,
                                                   float* __restrict__ mean_out, float* __restrict__ rstd_out) {
     pdl_trigger();
@@ -399,7 +403,7 @@ __global__ void __launch_bounds__(256) k_ln_fwd_w(const uint4* __restrict__ x, i
 
 // dx = rstd * (g*dy - mean(g*dy) - xhat * mean(g*dy*xhat)) (+ dres)
 template <int NV>
-__global__ void __launch_bounds__(256) k_ln_bwd_dx_w(const uint4* __restrict__ dy, const uint4* __restrict__ x, int rows,
+__global__ void __launch_bounds__(kLnWarpThreads) k_ln_bwd_dx_w(const uint4* __restrict__ dy, const uint4* __restrict__ x, int rows,
                                                      const float* __restrict__ g, const float* __restrict__ mean,
                                                      const float* __restrict__ rstd, const uint4* __restrict__ dres,
                                                      uint4* __restrict__ dx) {
@@ -554,16 +558,16 @@ __global__ void __launch_bounds__(256) k_ln_bwd_dgb(const uint4* __restrict__ dy
 template <int NV>
 void ln_fwd_w(const __nv_bfloat16* x, int rows, const float* g, const float* b, float eps, __nv_bfloat16* out,
               float* mean, float* rstd, cudaStream_t st) {
-    const unsigned grid = static_cast<unsigned>(std::min((rows + 7) / 8, 148 * 8));
-    launch_pdl(k_ln_fwd_w<NV>, dim3(grid), dim3(256), 0, st, reinterpret_cast<const uint4*>(x), rows, g, b, eps,
+    const unsigned grid = static_cast<unsigned>(std::min((rows + kLnRowsPerCta - 1) / kLnRowsPerCta, 148 * 32));
+    launch_pdl(k_ln_fwd_w<NV>, dim3(grid), dim3(kLnWarpThreads), 0, st, reinterpret_cast<const uint4*>(x), rows, g, b, eps,
                reinterpret_cast<uint4*>(out), mean, rstd);
 }
 
 template <int NV>
 void ln_bwd_dx_w(const __nv_bfloat16* dy, const __nv_bfloat16* x, int rows, const float* g, const float* mean,
                  const float* rstd, const __nv_bfloat16* dres, __nv_bfloat16* dx, cudaStream_t st) {
-    const unsigned grid = static_cast<unsigned>(std::min((rows + 7) / 8, 148 * 8));
-    launch_pdl(k_ln_bwd_dx_w<NV>, dim3(grid), dim3(256), 0, st, reinterpret_cast<const uint4*>(dy),
+    const unsigned grid = static_cast<unsigned>(std::min((rows + kLnRowsPerCta - 1) / kLnRowsPerCta, 148 * 32));
+    launch_pdl(k_ln_bwd_dx_w<NV>, dim3(grid), dim3(kLnWarpThreads), 0, st, reinterpret_cast<const uint4*>(dy),
                reinterpret_cast<const uint4*>(x), rows, g, mean, rstd, reinterpret_cast<const uint4*>(dres),
                reinterpret_cast<uint4*>(dx));
 }
