@@ -927,16 +927,21 @@ int encode_2d_out_uncached(CUtensorMap* m, const void* ptr, long long rows, long
     return r == CUDA_SUCCESS ? SWARM_OK : SWARM_E_INVALID;
 }
 
-// Stream-K runs only when the caller passes a workspace (the stage executor
-// does so under SWARM_GEMM_STREAMK=1).  Measured on B200 it does not pay for
-// the block shapes: the data-parallel tail wave runs faster than a full wave
-// (fewer clusters share L2 bandwidth), so there is little quantization loss to
-// recover, and the fixup adds traffic (profiles/r01_gemm_experiments.md).
+// Stream-K runs only when the caller passes a workspace; see the policy in
+// swarm_gemm_bf16 and the measurements in profiles/r01_gemm_experiments.md.
 // Stream-K scratch layout (caller-owned, see swarm_gemm_args.workspace):
 // [arrival counters | ready flags | partial accumulators].
 constexpr int kMaxClusters = 128;
 constexpr size_t kSkFlagBytes = 65536;
 static_assert(kMaxClusters * 8 * 3 * sizeof(int) <= kSkFlagBytes, "flag area");
+int streamk_mode() {  // SWARM_GEMM_STREAMK: 0 never, 1 whenever shorter, unset: when it pays >= 25%
+    static const int m = [] {
+        const char* e = getenv("SWARM_GEMM_STREAMK");
+        return e ? (e[0] == '0' ? 0 : 1) : 2;
+    }();
+    return m;
+}
+
 size_t sk_bytes(int clusters) {
     return kSkFlagBytes + static_cast<size_t>(clusters) * 2 * 2 * 128 * PAIR_BN * sizeof(float);
 }
@@ -1123,7 +1128,32 @@ extern "C" int swarm_gemm_bf16(const swarm_gemm_args* a, swarm_stream_t stream) 
     // two pairs per cluster sharing A by TMA multicast when N splits into an even
     // number of 256-wide tiles (halves the A traffic from L2 per SM)
     const int pair_tiles_n = (a->n + PAIR_BN - 1) / PAIR_BN;
-    const int npair = (pair && multicast_mode() && pair_tiles_n % 2 == 0) ? 2 : 1;
+    // Stream-K tail (pair tiles, needs the caller's workspace): whole waves of 256x256
+    // tiles stay data-parallel, the last partial wave's tiles are cut into k-block
+    // ranges spread evenly over every cluster.  It pays when a GEMM has few tiles and a
+    // long K (configs[3]: 512 x 4096 x 16384 = 32 tiles of 256 k-blocks on 74 clusters);
+    // for the configs[2] shapes the data-parallel tail is cheaper than it looks (the
+    // last wave runs with the L2 feed to itself), so by default stream-K is chosen only
+    // when it removes >= 25% of the k-block critical path (SWARM_GEMM_STREAMK=0 never,
+    // =1 whenever it shortens the path at all).
+    const int kblocks = (a->k + BK - 1) / BK;
+    bool use_sk = false;
+    int sk_C = 0, sk_waves = 0, sk_rem = 0;
+    if (pair && a->workspace && streamk_mode() != 0 &&
+        a->workspace_bytes >= sk_bytes(std::min(num_sms() / 2, kMaxClusters)) &&
+        (reinterpret_cast<uintptr_t>(a->workspace) & 255) == 0) {
+        const long long tiles1 = static_cast<long long>((a->m + 255) / 256) * pair_tiles_n * a->batch;
+        sk_C = std::min(max_pair_clusters(), kMaxClusters);
+        sk_waves = static_cast<int>(tiles1 / sk_C);
+        sk_rem = static_cast<int>(tiles1 % sk_C);
+        const long long w = static_cast<long long>(sk_rem) * kblocks;
+        const long long per = w / sk_C;
+        const long long t_dp = static_cast<long long>(sk_waves + (sk_rem ? 1 : 0)) * kblocks;
+        const long long t_sk = static_cast<long long>(sk_waves) * kblocks + (w + sk_C - 1) / sk_C + 2;  // +2: fixup
+        const bool pays = streamk_mode() == 1 ? t_sk < t_dp : 4 * t_sk <= 3 * t_dp;
+        use_sk = sk_rem && per >= 4 && per * (kMaxSkParts - 1) >= kblocks && pays;
+    }
+    const int npair = (pair && !use_sk && multicast_mode() && pair_tiles_n % 2 == 0) ? 2 : 1;
     CUtensorMap ta, tb;
     int rc = encode_2d(&ta, a->a, ar, ac, a->lda, 64, a->a_mn_major ? BK : (npair == 2 ? 64 : BM));
     if (rc) return rc;
@@ -1176,35 +1206,20 @@ extern "C" int swarm_gemm_bf16(const swarm_gemm_args* a, swarm_stream_t stream) 
         if (rc == SWARM_OK && a->epilogue == SWARM_EPI_GELU) rc = encode_2d_out(&tu, a->aux, d_rows, d_cols, a->ldd, false);
         if (rc != SWARM_OK) p.tma_epi = 0;  // fall back to direct stores
     }
-    // Stream-K tail: whole waves of 256x256 tiles stay data-parallel; the last,
-    // partial wave's tiles are cut into k-block ranges spread evenly over every
-    // cluster (e.g. 256 tiles on 74 clusters: 3 waves + 34 tiles x 32 k-blocks
-    // / 74 = 14.7 k-blocks each instead of a fourth, half-empty wave).
     p.dp_tiles = p.total_tiles;
     p.sk_tiles = 0;
     p.sk_iters = 0;
     cudaStream_t st = as_stream(stream);
     const int resident = npair == 1 ? max_pair_clusters() : max_quad_clusters();
     int grid_clusters = std::min(p.total_tiles, resident);
-    if (pair && npair == 1 && a->workspace &&
-        a->workspace_bytes >= sk_bytes(std::min(num_sms() / 2, kMaxClusters)) &&
-        (reinterpret_cast<uintptr_t>(a->workspace) & 255) == 0) {
-        const int C = std::min(resident, kMaxClusters);
-        const int waves = p.total_tiles / C, rem = p.total_tiles % C;
-        const int kb = p.k_blocks;
-        const long long w = static_cast<long long>(rem) * kb;
-        const int per = static_cast<int>(w / C);
-        const long long t_dp = static_cast<long long>(waves + (rem ? 1 : 0)) * kb;
-        const long long t_sk = static_cast<long long>(waves) * kb + (w + C - 1) / C + 2;  // +2: fixup
-        if (rem && per >= 4 && per * (kMaxSkParts - 1) >= kb && t_sk < t_dp) {
-            p.dp_tiles = waves * C;
-            p.sk_tiles = rem;
-            p.sk_iters = static_cast<int>(w);
-            p.sk_cnt = static_cast<int*>(a->workspace);
-            p.sk_ready = p.sk_cnt + kMaxClusters * 8;
-            p.ws = reinterpret_cast<float*>(static_cast<uint8_t*>(a->workspace) + kSkFlagBytes);
-            grid_clusters = C;
-        }
+    if (use_sk) {
+        p.dp_tiles = sk_waves * sk_C;
+        p.sk_tiles = sk_rem;
+        p.sk_iters = sk_rem * p.k_blocks;
+        p.sk_cnt = static_cast<int*>(a->workspace);
+        p.sk_ready = p.sk_cnt + kMaxClusters * 8;
+        p.ws = reinterpret_cast<float*>(static_cast<uint8_t*>(a->workspace) + kSkFlagBytes);
+        grid_clusters = sk_C;
     }
     if (pair && npair == 2) return dispatch_pair<2>(a->a_mn_major, a->b_mn_major, ta, tb, td, tu, p, grid_clusters, st);
     if (pair) return dispatch_pair<1>(a->a_mn_major, a->b_mn_major, ta, tb, td, tu, p, grid_clusters, st);

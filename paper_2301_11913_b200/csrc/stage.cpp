@@ -187,16 +187,8 @@ struct ProfOp {
         TRY(expr);                 \
     } while (0)
 
-bool streamk_requested() {
-    static const bool on = [] {
-        const char* e = getenv("SWARM_GEMM_STREAMK");
-        return e && e[0] == '1';
-    }();
-    return on;
-}
-
 int run_gemm(swarm_gemm_args g, cudaStream_t st) {
-    if (t_cur && streamk_requested()) {  // the visit stream and the side stream each own a stream-K scratch
+    if (t_cur) {  // the visit stream and the side stream each own a stream-K scratch
         g.workspace = t_cur->skws[st == t_cur->side ? 1 : 0];
         g.workspace_bytes = swarm_gemm_workspace_bytes();
     }
@@ -602,7 +594,6 @@ int create(const swarm_stage_config* c, swarm_stage* s) {
     }
     if (cudaStreamCreateWithFlags(&s->side, cudaStreamNonBlocking) != cudaSuccess) return SWARM_E_CUDA;
     for (void*& w : s->skws) {
-        if (!streamk_requested()) break;
         TRY(dmalloc(s, &w, swarm_gemm_workspace_bytes()));
         if (cudaMemset(w, 0, swarm_gemm_workspace_bytes()) != cudaSuccess) return SWARM_E_CUDA;
     }

@@ -30,9 +30,8 @@ def batched(M, N, K, batch, a_t, b_t, epi):
     g.d, g.ldd, g.rd0 = out.data_ptr(), N, M
     g.alpha, g.epilogue = 1.0, epi
     g.aux = None
-    if os.environ.get("SWARM_GEMM_STREAMK") == "1":  # stream-K scratch (opt-in)
-        ws = ops.gemm_workspace()
-        g.workspace, g.workspace_bytes = ws.data_ptr(), ws.numel()
+    ws = ops.gemm_workspace()  # as the stage executor does: the kernel's policy decides on stream-K
+    g.workspace, g.workspace_bytes = ws.data_ptr(), ws.numel()
     return (a, b, out), lambda: ops.gemm_raw(g)
 
 

@@ -100,8 +100,11 @@ def test_gemm_batched_heads(cuda):
 
 # Stream-K tail (csrc/gemm.cu): shapes whose 256x256 tile count leaves a partial
 # last wave on 74 SM pairs, so the tail tiles are split along K across clusters.
-SK_SHAPES = [(2048, 2048, 2048), (2048, 8192, 2048), (2048, 6144, 2048), (2048, 2048, 8192), (8192, 2048, 2048),
-             (4096, 2304, 1024), (768, 3328, 4096), (1000, 2000, 1000)]
+# The first shapes take the stream-K path under the default policy (few tiles, long K:
+# configs[3]'s 512-token GEMMs); the rest only when forced (SWARM_GEMM_STREAMK=1,
+# test_gemm_kernel_variants).
+SK_SHAPES = [(512, 4096, 16384), (512, 4096, 4096), (768, 3328, 4096), (1000, 2000, 1000), (2048, 2048, 8192),
+             (4096, 2304, 1024)]
 
 
 @pytest.mark.parametrize("m,n,k", SK_SHAPES)
@@ -208,7 +211,7 @@ import math, sys, torch
 sys.path.insert(0, {root!r})
 from paper_2301_11913_b200 import _lib as L, ops
 torch.manual_seed(0)
-for (m, n, k) in [(2048, 2048, 2048), (512, 6144, 2048), (768, 1280, 4096), (200, 300, 96)]:
+for (m, n, k) in [(2048, 2048, 2048), (512, 6144, 2048), (768, 1280, 4096), (200, 300, 96), (512, 4096, 8192)]:
     for a_t, b_t in [(False, False), (False, True), (True, True)]:
         if (a_t and m % 8) or (b_t and n % 8) or k % 8:
             continue  # rows must be 16-byte aligned
@@ -217,21 +220,23 @@ for (m, n, k) in [(2048, 2048, 2048), (512, 6144, 2048), (768, 1280, 4096), (200
         A = a.float().t() if a_t else a.float()
         B = b.float().t() if b_t else b.float()
         ref = A @ B.t()
-        out = ops.gemm(a, b, a_t=a_t, b_t=b_t, epilogue=L.EPI_STORE_F32)
+        out = ops.gemm(a, b, a_t=a_t, b_t=b_t, epilogue=L.EPI_STORE_F32, streamk=True)
         torch.testing.assert_close(out, ref, rtol=1e-4, atol=1e-4 * math.sqrt(k))
         acc = torch.ones(m, n, device="cuda")
-        ops.gemm(a, b, a_t=a_t, b_t=b_t, epilogue=L.EPI_ACCUM_F32, out=acc)
+        ops.gemm(a, b, a_t=a_t, b_t=b_t, epilogue=L.EPI_ACCUM_F32, out=acc, streamk=True)
         torch.testing.assert_close(acc, ref + 1, rtol=1e-4, atol=1e-4 * math.sqrt(k))
 print("ok")
 """
 
 
 @pytest.mark.parametrize("env", [{"SWARM_GEMM_MCAST": "0"}, {"SWARM_GEMM_PAIR": "0"},
-                                 {"SWARM_GEMM_TMA_EPI": "0"}, {"SWARM_PDL": "0"}])
+                                 {"SWARM_GEMM_TMA_EPI": "0"}, {"SWARM_PDL": "0"}, {"SWARM_GEMM_STREAMK": "1"},
+                                 {"SWARM_GEMM_STREAMK": "0"}])
 def test_gemm_kernel_variants(cuda, env):
     """The non-default kernel variants (2-CTA pairs without multicast, 1-CTA
-    tiles, direct-store epilogue, no programmatic dependent launch) stay correct;
-    the selection is read once per process, hence a subprocess per variant."""
+    tiles, direct-store epilogue, no programmatic dependent launch, stream-K
+    forced on / off) stay correct; the selection is read once per process,
+    hence a subprocess per variant."""
     import os
     import subprocess
     import sys
