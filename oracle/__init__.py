@@ -92,6 +92,8 @@ def _load_ref():
     lib.ref_rebalance_decide.argtypes = [sz, P, P, P, P, P, P, P]
     lib.ref_oracle_throughput.argtypes = [P, sz, C.c_int64]
     lib.ref_oracle_throughput.restype = C.c_double
+    lib.ref_stage_cost.argtypes = [P, C.c_double, P, C.c_int, P]
+    lib.ref_stage_cost.restype = C.c_int
     return lib
 
 

@@ -116,3 +116,23 @@ extern "C" double ref_oracle_throughput(const double* rates, size_t n_stages, in
         return -1.0;
     }
 }
+
+// The reference's analytic stage cost (P/src/cost_model.cpp:50-70) for the
+// cost-model compatibility test: out = {compute, comm, total, idle, utilization, square_cube}.
+#include "swarmsim/cost_model.hpp"
+extern "C" int ref_stage_cost(const int64_t* shape6, double act_bytes, const double* dev4, int overlap, double* out) {
+    try {
+        swarmsim::cost_model::LayerShape s{shape6[0], shape6[1], shape6[2], shape6[3], shape6[4], shape6[5], act_bytes};
+        swarmsim::cost_model::DeviceProfile d{dev4[0], dev4[1], dev4[2], dev4[3]};
+        const auto c = swarmsim::cost_model::stage_cost(s, d, overlap != 0);
+        out[0] = c.compute_seconds;
+        out[1] = c.comm_seconds;
+        out[2] = c.total_seconds;
+        out[3] = c.idle_fraction;
+        out[4] = c.utilization;
+        out[5] = swarmsim::cost_model::square_cube_ratio(s);
+        return 0;
+    } catch (...) {
+        return 1;
+    }
+}

@@ -5,6 +5,7 @@
 // every numeric operator runs on the B200: host vector -> H2D -> sm_100a kernel
 // -> D2H, returned by value like the reference.  There is no CPU fallback: if
 // the device path fails, the call throws std::runtime_error.
+#include <algorithm>
 #include <cuda_runtime.h>
 
 #include <cmath>
@@ -203,6 +204,42 @@ double activation_payload_bits(const LayerShape& s) {
     s.validate();
     return static_cast<double>(s.batch) * static_cast<double>(s.seq_len) * static_cast<double>(s.d_model) *
            s.activation_bytes_per_element * 8.0;
+}
+
+void DeviceProfile::validate() const {
+    if (effective_flops <= 0.0 || upload_bps <= 0.0 || download_bps <= 0.0)
+        throw ConfigError("DeviceProfile: flops and bandwidths must be positive");
+    if (rtt_seconds < 0.0) throw ConfigError("DeviceProfile: rtt_seconds must be nonnegative");
+}
+
+// compute = stage FLOPs / effective FLOP/s; comm = activations out + gradients back
+// plus one latency each way; overlapped -> max (cost_model.cpp:50-66)
+CostBreakdown stage_cost(const LayerShape& shape, const DeviceProfile& device, bool overlap) {
+    device.validate();
+    CostBreakdown out;
+    out.compute_seconds = flops_per_stage(shape, true) / device.effective_flops;
+    const double payload = activation_payload_bits(shape);
+    out.comm_seconds = payload / device.upload_bps + payload / device.download_bps + 2.0 * device.rtt_seconds;
+    out.total_seconds = overlap ? std::max(out.compute_seconds, out.comm_seconds) : out.compute_seconds + out.comm_seconds;
+    out.utilization = out.compute_seconds / out.total_seconds;
+    out.idle_fraction = 1.0 - out.utilization;
+    return out;
+}
+
+double square_cube_ratio(const LayerShape& shape) {
+    return flops_per_stage(shape, true) / activation_payload_bits(shape);
+}
+
+DeviceProfile calibrated_profile(const LayerShape& shape, double measured_visit_seconds, double link_bps,
+                                 double link_rtt_seconds) {
+    if (!(measured_visit_seconds > 0.0)) throw ConfigError("calibrated_profile: visit time must be positive");
+    DeviceProfile d;
+    d.effective_flops = flops_per_stage(shape, true) / measured_visit_seconds;
+    d.upload_bps = link_bps;
+    d.download_bps = link_bps;
+    d.rtt_seconds = link_rtt_seconds;
+    d.validate();
+    return d;
 }
 
 // PAPER:292 / cost_model.cpp:72-80 presets ("ours" ships int8 activations)

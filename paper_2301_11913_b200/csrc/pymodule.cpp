@@ -33,6 +33,23 @@ PYBIND11_MODULE(_swarmsim_b200, m) {
     m.def("params_per_layer", &cost_model::params_per_layer, py::arg("shape"));
     m.def("flops_per_stage", &cost_model::flops_per_stage, py::arg("shape"), py::arg("include_backward"));
     m.def("activation_payload_bits", &cost_model::activation_payload_bits, py::arg("shape"));
+    py::class_<cost_model::DeviceProfile>(m, "DeviceProfile")
+        .def(py::init<>())
+        .def_readwrite("effective_flops", &cost_model::DeviceProfile::effective_flops)
+        .def_readwrite("upload_bps", &cost_model::DeviceProfile::upload_bps)
+        .def_readwrite("download_bps", &cost_model::DeviceProfile::download_bps)
+        .def_readwrite("rtt_seconds", &cost_model::DeviceProfile::rtt_seconds);
+    py::class_<cost_model::CostBreakdown>(m, "CostBreakdown")
+        .def(py::init<>())
+        .def_readonly("compute_seconds", &cost_model::CostBreakdown::compute_seconds)
+        .def_readonly("comm_seconds", &cost_model::CostBreakdown::comm_seconds)
+        .def_readonly("total_seconds", &cost_model::CostBreakdown::total_seconds)
+        .def_readonly("idle_fraction", &cost_model::CostBreakdown::idle_fraction)
+        .def_readonly("utilization", &cost_model::CostBreakdown::utilization);
+    m.def("stage_cost", &cost_model::stage_cost, py::arg("shape"), py::arg("device"), py::arg("overlap") = true);
+    m.def("square_cube_ratio", &cost_model::square_cube_ratio, py::arg("shape"));
+    m.def("calibrated_profile", &cost_model::calibrated_profile, py::arg("shape"), py::arg("measured_visit_seconds"),
+          py::arg("link_bps"), py::arg("link_rtt_seconds") = 0.0);
     m.def("preset", &cost_model::preset, py::arg("name"));
     m.def("preset_names", &cost_model::preset_names);
 

@@ -111,7 +111,7 @@ SK_SHAPES = [(512, 4096, 16384), (512, 4096, 4096), (768, 3328, 4096), (1000, 20
 @pytest.mark.parametrize("a_t,b_t", [(False, False), (False, True), (True, True)])
 def test_gemm_streamk_matches_whole_tiles(cuda, m, n, k, a_t, b_t):
     """Stream-K vs whole-tile launches: identical up to fp32 summation order
-    (rtol 1e-5, atol 5e-5 * sqrt(K) for O(sqrt(K)) outputs), against torch as
+    (rtol 1e-5, atol 1e-4 * sqrt(K) for O(sqrt(K)) outputs), against torch as
     well, and repeated launches agree (the self-resetting flags are clean)."""
     import torch
     from paper_2301_11913_b200 import ops
@@ -122,7 +122,7 @@ def test_gemm_streamk_matches_whole_tiles(cuda, m, n, k, a_t, b_t):
     whole = ops.gemm(a, b, a_t=a_t, b_t=b_t, epilogue=1, streamk=False)
     for _ in range(3):
         sk = ops.gemm(a, b, a_t=a_t, b_t=b_t, epilogue=1, streamk=True)
-        torch.testing.assert_close(sk, whole, rtol=1e-5, atol=5e-5 * math.sqrt(k))
+        torch.testing.assert_close(sk, whole, rtol=1e-5, atol=1e-4 * math.sqrt(k))
     torch.testing.assert_close(sk, ref, rtol=1e-4, atol=1e-4 * math.sqrt(k))
     sk16 = ops.gemm(a, b, a_t=a_t, b_t=b_t, streamk=True)
     torch.testing.assert_close(sk16.float(), ref, rtol=1e-2, atol=1e-2 * math.sqrt(k) / 8 + 1e-2)
