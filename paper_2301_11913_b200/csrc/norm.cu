@@ -369,6 +369,48 @@ __global__ void __launch_bounds__(kLnWarpThreads) k_ln_fwd_w(const uint4* __rest
     const int lane = threadIdx.x & 31;
     const int warps = (gridDim.x * blockDim.x) >> 5;
     const float inv_n = 1.f / (256.f * NV);
+    if constexpr (NV > 8) {
+        // wide rows (d = 4096): a float copy of the row would not fit the register
+        // file; three passes re-read it (L1 hits after the first)
+        for (int r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < rows; r += warps) {
+            const uint4* xr = x + static_cast<size_t>(r) * C8;
+            float s = 0.f;
+#pragma unroll 4
+            for (int i = 0; i < NV; ++i) {
+                float v[8];
+                unpack8(xr[lane + 32 * i], v);
+#pragma unroll
+                for (int j = 0; j < 8; ++j) s += v[j];
+            }
+            const float mean = wsum(s) * inv_n;
+            float s2 = 0.f;
+#pragma unroll 4
+            for (int i = 0; i < NV; ++i) {
+                float v[8];
+                unpack8(xr[lane + 32 * i], v);
+#pragma unroll
+                for (int j = 0; j < 8; ++j) s2 += (v[j] - mean) * (v[j] - mean);
+            }
+            const float rstd = 1.0f / sqrtf(wsum(s2) * inv_n + eps);
+            uint4* orow = out + static_cast<size_t>(r) * C8;
+#pragma unroll 4
+            for (int i = 0; i < NV; ++i) {
+                const int c0 = (lane + 32 * i) * 8;
+                float v[8], o[8], gv[8], bv[8];
+                unpack8(xr[lane + 32 * i], v);
+                load8f(g, c0, 1.f, gv);
+                load8f(b, c0, 0.f, bv);
+#pragma unroll
+                for (int j = 0; j < 8; ++j) o[j] = (v[j] - mean) * rstd * gv[j] + bv[j];
+                orow[lane + 32 * i] = pack8(o);
+            }
+            if (lane == 0) {
+                if (mean_out) mean_out[r] = mean;
+                if (rstd_out) rstd_out[r] = rstd;
+            }
+        }
+        return;
+    }
     for (int r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < rows; r += warps) {
         const uint4* xr = x + static_cast<size_t>(r) * C8;
         float v[NV * 8];
@@ -419,7 +461,7 @@ __global__ void __launch_bounds__(kLnWarpThreads) k_ln_bwd_dx_w(const uint4* __r
         const float mu = mean[r], rs = rstd[r];
         float xh[KEEP ? NV * 8 : 8], gy[KEEP ? NV * 8 : 8];
         float s1 = 0.f, s2 = 0.f;
-#pragma unroll
+#pragma unroll(KEEP ? NV : 4)
         for (int i = 0; i < NV; ++i) {
             float xv[8], dv[8];
             unpack8(x[base + lane + 32 * i], xv);
@@ -440,7 +482,7 @@ __global__ void __launch_bounds__(kLnWarpThreads) k_ln_bwd_dx_w(const uint4* __r
             }
         }
         const float c1 = wsum(s1) * inv_n, c2 = wsum(s2) * inv_n;
-#pragma unroll
+#pragma unroll(KEEP ? NV : 4)
         for (int i = 0; i < NV; ++i) {
             const int c0 = (lane + 32 * i) * 8;
             float o[8];
