@@ -388,6 +388,79 @@ def model_config(args):
     return dataclasses.replace(m, micro_batch=mb) if mb else m
 
 
+def measure_link(world, rank, nbytes=4 << 20, reps=20):
+    """Stage-to-stage transport rate: rank 0 -> rank 1 NCCL send/recv of a
+    wire-message-sized buffer (configs[2]: 4 MiB codes + scales), timed on the
+    device; returns (bytes/s, seconds per message) or None at world 1."""
+    if world < 2:
+        return None
+    import torch
+    import torch.distributed as dist
+    buf = torch.empty(nbytes, dtype=torch.uint8, device="cuda")
+    res = None
+    for it in range(2):  # warm-up round, then the timed round
+        barrier(world)
+        t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        t0.record()
+        for _ in range(reps):
+            if rank == 0:
+                dist.send(buf, 1)
+            elif rank == 1:
+                dist.recv(buf, 0)
+        t1.record()
+        torch.cuda.synchronize()
+        if it == 1:
+            sec = max_over_ranks(t0.elapsed_time(t1) / 1e3 / reps if rank < 2 else 0.0, world)
+            res = (nbytes / sec, sec)
+    return res
+
+
+def cost_model_report(mcfg, S, M, world, step_s, link):
+    """the reference's analytic stage cost calibrated on this run.
+    At one GPU every (microbatch, stage) visit runs back to back, so the measured
+    step / (M*S) is the fwd+bwd visit (head, embedding and optimizer amortised in);
+    effective_flops follows from the reference's own FLOP convention.  With the
+    measured (or, at one GPU, committed) link rate, stage_cost gives the
+    compute/comm split and the GPipe step for other GPU counts is predicted as
+    (M/P + S/G_s - 1) x (visits per rank per microbatch) x visit + gradient all-reduce."""
+    from paper_2301_11913_b200 import _swarmsim_b200 as X
+    shape = X.LayerShape()
+    shape.d_model, shape.d_ffn, shape.n_heads = mcfg.d_model, mcfg.d_ffn, mcfg.n_heads
+    shape.seq_len, shape.batch, shape.layers_per_stage = mcfg.seq_len, mcfg.micro_batch, mcfg.layers_per_stage
+    k = mcfg.maxout_k if mcfg.maxout_k > 1 else 1
+    shape.activation_bytes_per_element = (1.0 + 4.0 / mcfg.block_size) / k  # int8 codes + fp32 scales (per maxout)
+    src = "measured this run (rank 0 -> 1 NCCL send/recv, 4 MiB)"
+    if link is None:
+        prof = os.path.join(ROOT, "profiles", "r01_link.json")
+        if os.path.exists(prof):
+            with open(prof) as f:
+                link = tuple(json.load(f)["link"])
+            src = "profiles/r01_link.json (measured on 2 B200s)"
+        else:
+            link, src = (450e9, 10e-6), "nominal (no peer in this run)"
+    if world != 1:
+        return {"link_bps": link[0], "link_source": src}
+    visit = step_s / (M * S)
+    prof = X.calibrated_profile(shape, visit, link[0], 0.0)  # NVLink latency is negligible at 4 MiB
+    c = X.stage_cost(shape, prof, False)
+    grad_bytes = 4.0 * mcfg.params_per_layer() * (1 if mcfg.shared_layers else mcfg.layers_per_stage)
+    pred = {}
+    for G in (1, 2, 4, 8):
+        P = max(1, G // S)
+        per_rank = max(1, S // G)  # stages hosted per rank
+        t = (M / P + min(G, S) - 1) * per_rank * c.total_seconds
+        if P > 1:
+            t += 2.0 * grad_bytes * (P - 1) / P / link[0]  # ring all-reduce of the fp32 gradient arena
+        pred[str(G)] = M * mcfg.tokens / t
+    return {"calibrated_effective_flops": prof.effective_flops, "link_bps": link[0], "link_source": src,
+            "visit_s": visit, "stage_cost": {"compute_s": c.compute_seconds, "comm_s": c.comm_seconds,
+                                             "utilization": c.utilization},
+            "square_cube_ratio_flop_per_bit": X.square_cube_ratio(shape),
+            "predicted_tokens_per_s": pred,
+            "note": "GPipe step (M/P + min(G,S) - 1) x stages-per-rank x visit + fp32 gradient all-reduce; "
+                    "the driver's scaling run measures the same N"}
+
+
 def train_config(args) -> dict:
     """The configs[2] workload description shared by both arms' JSON lines."""
     m = model_config(args)
@@ -474,6 +547,8 @@ def bench_train(args, world, rank, local):
     visits_per_stage = (M // pipe.P) if not pipe.all_local else M
     gemm_share = (gemm_ms / args.steps) * visits_per_stage / (t0.elapsed_time(t1) / args.steps) \
         if gemm_ms > 0 else None
+    link = measure_link(world, rank)
+    cost_model = cost_model_report(mcfg, S, M, world, (ms / args.steps) / 1e3, link)
     # per-category kernel time, from one extra untimed step whose profiled visits
     # start behind a GPU spin (no host-launch gaps inside the events), scaled to
     # every visit of a step
@@ -521,7 +596,7 @@ def bench_train(args, world, rank, local):
         "e2e": {"value": e2e_val, "unit": "tokens/s", "h2d_bytes_per_step": int(tok.numel() * 8),
                 "d2h_bytes_per_step": 4, "path": "SwarmPipeline.step with tokens/targets copied from pinned host "
                                                  "memory and the loss read back every step"},
-        "gpu_launches": int(launches), "clocks": clocks,
+        "gpu_launches": int(launches), "clocks": clocks, "cost_model": cost_model,
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         tok_s, thr, sample = cpu_block_baseline(mcfg)
