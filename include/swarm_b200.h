@@ -151,9 +151,9 @@ typedef struct {
        kernel leaves it zeroed again); never shared by GEMMs that can run
        concurrently.  With it, the last partial wave of 256x256 tiles is split
        along K across every SM pair (results identical up to fp32 summation
-       order).  The kernel uses it only where it shortens the k-block critical
-       path by >= 25% (few tiles, long K); SWARM_GEMM_STREAMK=0 / 1 force never /
-       whenever shorter. */
+       order).  The kernel uses it only where it wins after paying for the fixup
+       (few tiles, long K); SWARM_GEMM_STREAMK=0 / 1 force never / whenever the
+       k-block path is shorter. */
     void* workspace;
     size_t workspace_bytes;
 } swarm_gemm_args;

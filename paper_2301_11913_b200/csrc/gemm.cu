@@ -1133,9 +1133,9 @@ extern "C" int swarm_gemm_bf16(const swarm_gemm_args* a, swarm_stream_t stream) 
     // ranges spread evenly over every cluster.  It pays when a GEMM has few tiles and a
     // long K (configs[3]: 512 x 4096 x 16384 = 32 tiles of 256 k-blocks on 74 clusters);
     // for the configs[2] shapes the data-parallel tail is cheaper than it looks (the
-    // last wave runs with the L2 feed to itself), so by default stream-K is chosen only
-    // when it removes >= 25% of the k-block critical path (SWARM_GEMM_STREAMK=0 never,
-    // =1 whenever it shortens the path at all).
+    // last wave runs with the L2 feed to itself) and the fixup costs ~40 k-block times,
+    // so by default stream-K is chosen only when it still wins by 10% after paying for
+    // the fixup (SWARM_GEMM_STREAMK=0 never, =1 whenever the k-block path is shorter).
     const int kblocks = (a->k + BK - 1) / BK;
     bool use_sk = false;
     int sk_C = 0, sk_waves = 0, sk_rem = 0;
@@ -1149,8 +1149,10 @@ extern "C" int swarm_gemm_bf16(const swarm_gemm_args* a, swarm_stream_t stream) 
         const long long w = static_cast<long long>(sk_rem) * kblocks;
         const long long per = w / sk_C;
         const long long t_dp = static_cast<long long>(sk_waves + (sk_rem ? 1 : 0)) * kblocks;
-        const long long t_sk = static_cast<long long>(sk_waves) * kblocks + (w + sk_C - 1) / sk_C + 2;  // +2: fixup
-        const bool pays = streamk_mode() == 1 ? t_sk < t_dp : 4 * t_sk <= 3 * t_dp;
+        const long long t_sk = static_cast<long long>(sk_waves) * kblocks + (w + sk_C - 1) / sk_C;
+        // the fixup (every split tile's fp32 partials written and read back through L2)
+        // measured ~10-13 us on B200 = ~40 k-block times (scripts/streamk_diag_D.py)
+        const bool pays = streamk_mode() == 1 ? t_sk + 2 < t_dp : 10 * (t_sk + 40) <= 9 * t_dp;
         use_sk = sk_rem && per >= 4 && per * (kMaxSkParts - 1) >= kblocks && pays;
     }
     const int npair = (pair && !use_sk && multicast_mode() && pair_tiles_n % 2 == 0) ? 2 : 1;

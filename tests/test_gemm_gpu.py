@@ -100,8 +100,8 @@ def test_gemm_batched_heads(cuda):
 
 # Stream-K tail (csrc/gemm.cu): shapes whose 256x256 tile count leaves a partial
 # last wave on 74 SM pairs, so the tail tiles are split along K across clusters.
-# The first shapes take the stream-K path under the default policy (few tiles, long K:
-# configs[3]'s 512-token GEMMs); the rest only when forced (SWARM_GEMM_STREAMK=1,
+# The first shape takes the stream-K path under the default policy (few tiles, long K:
+# configs[3]'s 512 x 4096 x 16384); the rest only when forced (SWARM_GEMM_STREAMK=1,
 # test_gemm_kernel_variants).
 SK_SHAPES = [(512, 4096, 16384), (512, 4096, 4096), (768, 3328, 4096), (1000, 2000, 1000), (2048, 2048, 8192),
              (4096, 2304, 1024)]
