@@ -553,6 +553,12 @@ def bench_train(args, world, rank, local):
     # start behind a GPU spin (no host-launch gaps inside the events), scaled to
     # every visit of a step
     step_ms_rank = t0.elapsed_time(t1) / args.steps
+    # phase split of one untimed step on this rank (visits + transport / all-reduce / optimizer)
+    pipe.time_phases = True
+    pipe.step(tok, tgt)
+    pipe.time_phases = False
+    phases = pipe.phase_read()
+    phases = {k: max_over_ranks(v, world) for k, v in phases.items()}
     pipe.profile_read()  # drop the e2e steps' events
     pipe.prof_spin_ns = 5_000_000
     pipe.step(tok, tgt)
@@ -597,6 +603,7 @@ def bench_train(args, world, rank, local):
                 "d2h_bytes_per_step": 4, "path": "SwarmPipeline.step with tokens/targets copied from pinned host "
                                                  "memory and the loss read back every step"},
         "gpu_launches": int(launches), "clocks": clocks, "cost_model": cost_model,
+        "step_phases_ms": {**phases, "note": "one untimed step, max over ranks, device events on the compute stream"},
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         tok_s, thr, sample = cpu_block_baseline(mcfg)

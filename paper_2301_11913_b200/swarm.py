@@ -252,6 +252,8 @@ class SwarmPipeline:
         self._warm: set = set()
         self._profiled: set = set()
         self.prof_spin_ns = 0  # >0: profiled visits start behind a GPU spin of this length
+        self.time_phases = False  # record per-step phase events (phase_read)
+        self._phase_events: list = []
         probe = next(iter(self.stages.values()), None) or self._new_stage(0, slots=1)
         self.wire_bytes = probe.wire_bytes
         tokens = mcfg.tokens
@@ -372,16 +374,40 @@ class SwarmPipeline:
         routes = self.plan()
         self._profiled.clear()
         scale = loss_scale if loss_scale is not None else 1.0 / (self.M * self.m.tokens)
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)] if self.time_phases else None
+        if ev:
+            ev[0].record()
         if self.all_local:
             self._step_local(routes, tokens, targets, scale)
         else:
             self._step_pipelined(routes, tokens, targets, scale)
+        if ev:
+            ev[1].record()
         for s, st in self.stages.items():
             if s in self.stage_group:
                 dist.all_reduce(st.grads(), op=dist.ReduceOp.SUM, group=self.stage_group[s])
+        if ev:
+            ev[2].record()
+        for st in self.stages.values():
             # every peer holds the sum over ITS microbatches of d(loss/(M*T)); the SUM over
             # the stage peers is the full-batch gradient, so no further scaling
             st.optimizer_step(grad_scale=1.0)
+        if ev:
+            ev[3].record()
+            self._phase_events.append(ev)
+
+    def phase_read(self) -> dict:
+        """Per-step device time of this rank's phases since the last read (ms):
+        stage visits + transport, gradient all-reduce, optimizer (time_phases=True)."""
+        torch.cuda.synchronize()
+        out = {"visits_ms": 0.0, "allreduce_ms": 0.0, "optimizer_ms": 0.0}
+        for ev in self._phase_events:
+            out["visits_ms"] += ev[0].elapsed_time(ev[1])
+            out["allreduce_ms"] += ev[1].elapsed_time(ev[2])
+            out["optimizer_ms"] += ev[2].elapsed_time(ev[3])
+        n = max(1, len(self._phase_events))
+        self._phase_events = []
+        return {k: v / n for k, v in out.items()}
 
     # ---------------------------------------------------------------- visits
     def _run(self, key, fn) -> None:
