@@ -1,0 +1,7 @@
+cd $GRAFT_REPO_ROOT
+timeout -k 5 900 python -m pytest tests -m gpu -x -q -p no:cacheprovider > gpurun_out/t47_all.log 2>&1; echo "rc=$?" >> gpurun_out/t47_all.log
+R2="python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29547"
+R4="python -m torch.distributed.run --nnodes=1 --nproc-per-node 4 --master-addr 127.0.0.1 --master-port 29548"
+timeout -k 10 900 $R4 bench.py --gpus 4 > gpurun_out/b47_n4.log 2>&1; echo "rc=$?" >> gpurun_out/b47_n4.log
+timeout -k 10 900 $R4 bench.py --gpus 4 --stages 2 > gpurun_out/b47_n4_s2.log 2>&1; echo "rc=$?" >> gpurun_out/b47_n4_s2.log
+timeout -k 10 900 $R2 bench.py --gpus 2 > gpurun_out/b47_n2.log 2>&1; echo "rc=$?" >> gpurun_out/b47_n2.log
