@@ -486,7 +486,7 @@ def bench_train(args, world, rank, local):
     mcfg = model_config(args)
     M = args.microbatches
     S = args.stages
-    pipe = SwarmPipeline(mcfg, S, n_microbatches=M, seed=1, lr=1e-4, profile=True)
+    pipe = SwarmPipeline(mcfg, S, n_microbatches=M, seed=1, lr=1e-4, profile=True, dpu=args.dpu)
     tok, tgt = synthetic_batch(mcfg, M, seed=7, device=dev)
     stream = torch.cuda.current_stream()
     for _ in range(args.warmup):
@@ -505,6 +505,7 @@ def bench_train(args, world, rank, local):
     t0.record(stream)
     for _ in range(args.steps):
         pipe.step(tok, tgt)
+    pipe.drain_updates()  # delayed updates: the last step's all-reduce + optimizer are inside the timed region
     t1.record(stream)
     torch.cuda.synchronize()
     barrier(world)
@@ -535,6 +536,7 @@ def bench_train(args, world, rank, local):
         dtok.copy_(htok, non_blocking=True)
         dtgt.copy_(htgt, non_blocking=True)
         pipe.step(dtok, dtgt)
+        pipe.drain_updates()
         hloss.copy_(pipe.loss_sum, non_blocking=True)
         torch.cuda.current_stream().synchronize()
     e2e_s = max_over_ranks(time.perf_counter() - w0, world)
@@ -581,7 +583,8 @@ def bench_train(args, world, rank, local):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
         "data": "synthetic tokens uniform over the vocab, random-init weights",
-        "config": {**train_config(args), "parallelism": placement, "optimizer": "AdamW (fused, fp32 master)",
+        "config": {**train_config(args), "parallelism": placement,
+                   "optimizer": "AdamW (fused, fp32 master)" + (", delayed parameter updates (1 step)" if args.dpu else ""),
                    "l2": "per-step working set (weights + activations, GBs) far exceeds L2; no flush needed",
                    "mean_loss": mean_loss, "model_tflops_per_s": model_tflops,
                    "model_flops_per_token": mcfg.flops_per_token(S)},
@@ -735,6 +738,8 @@ def main():
     ap.add_argument("--model", default="C", choices=["C", "D", "tiny"])
     ap.add_argument("--microbatches", type=int, default=TRAIN_MICROBATCHES)
     ap.add_argument("--micro-batch", type=int, default=None, help="sequences per microbatch (default: the preset's)")
+    ap.add_argument("--dpu", action="store_true",
+                    help="train: delayed parameter updates (PAPER:204): all-reduce + AdamW of step t overlap step t+1")
     ap.add_argument("--stages", type=int, default=TRAIN_STAGES, help="pipeline stages (default 4, SURVEY §8(d))")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-codec", action="store_true", help="train: skip the codec sub-measurement")

@@ -281,8 +281,20 @@ void* swarm_stage_params_bf16(swarm_stage_t st);
  * downloads from a stage-mate (P/src/rebalancer.cpp:71-75 counts these bytes) */
 int swarm_stage_optimizer_state(swarm_stage_t st, float** m, float** v, int* step);
 int swarm_stage_set_step(swarm_stage_t st, int step);
-/* re-derive the bf16 shadow from the fp32 master (after loading / receiving weights) */
+/* re-derive the bf16 shadow from the fp32 master (after loading / receiving weights);
+ * with two banks enabled, both shadows */
 int swarm_stage_sync_shadow(swarm_stage_t st, swarm_stream_t stream);
+/* Delayed parameter updates.  enable_banks allocates a
+ * second bf16 shadow and a second gradient arena (both copies of bank 0).  Visits
+ * read the weights of, and accumulate gradients into, the bank selected by
+ * set_bank; optimizer_step_bank applies bank b's gradients to the fp32 master,
+ * writes the result into bank b's shadow and zeroes bank b's gradients.  Step t
+ * uses bank t % 2, so the optimizer of step t (bank t % 2) can run while step t+1
+ * computes on the other bank: step t+1 sees the weights of step t-1's update. */
+int swarm_stage_enable_banks(swarm_stage_t st, swarm_stream_t stream);
+int swarm_stage_set_bank(swarm_stage_t st, int bank);
+float* swarm_stage_grads_bank(swarm_stage_t st, int bank);
+int swarm_stage_optimizer_step_bank(swarm_stage_t st, int bank, float grad_scale, swarm_stream_t stream);
 /* enumerate parameter tensors: index -> name, offset (elements), rows, cols */
 int swarm_stage_param_info(swarm_stage_t st, int index, const char** name, size_t* offset, size_t* rows,
                            size_t* cols);

@@ -77,6 +77,10 @@ SIGNATURES = {
     "swarm_stage_params": (P, [P]),
     "swarm_stage_params_bf16": (P, [P]),
     "swarm_stage_sync_shadow": (I, [P, P]),
+    "swarm_stage_enable_banks": (I, [P, P]),
+    "swarm_stage_set_bank": (I, [P, I]),
+    "swarm_stage_grads_bank": (P, [P, I]),
+    "swarm_stage_optimizer_step_bank": (I, [P, I, F, P]),
     "swarm_stage_param_info": (I, [P, I, C.POINTER(C.c_char_p), C.POINTER(SZ), C.POINTER(SZ), C.POINTER(SZ)]),
     "swarm_stage_activation": (I, [P, I, I, C.c_char_p, C.POINTER(P), C.POINTER(SZ)]),
     "swarm_stage_profile": (None, [P, I]),

@@ -65,6 +65,11 @@ struct swarm_stage {
     size_t bn_in_g = 0, bn_in_b = 0, bn_wd = 0, bn_out_g = 0, bn_out_b = 0;
     float *p32 = nullptr, *grad = nullptr, *m = nullptr, *v = nullptr;
     bf16* p16 = nullptr;
+    // delayed parameter updates: two shadow / gradient banks; p16 / grad point at the current one
+    bf16* p16b[2] = {nullptr, nullptr};
+    float* gradb[2] = {nullptr, nullptr};
+    bool banks = false;
+    int bank = 0;
     std::vector<Slot> slots;
     // workspaces (one visit at a time per stage)
     float *S = nullptr, *dP = nullptr, *logits = nullptr;
@@ -687,7 +692,45 @@ float* swarm_stage_params(swarm_stage_t s) { return s->p32; }
 void* swarm_stage_params_bf16(swarm_stage_t s) { return s->p16; }
 
 int swarm_stage_sync_shadow(swarm_stage_t s, swarm_stream_t stream) {
-    return swarm_cast_f32_bf16(s->p32, s->p16, s->nparams, stream);
+    if (!s->banks) return swarm_cast_f32_bf16(s->p32, s->p16, s->nparams, stream);
+    for (bf16* p : s->p16b) TRY(swarm_cast_f32_bf16(s->p32, p, s->nparams, stream));
+    return SWARM_OK;
+}
+
+int swarm_stage_enable_banks(swarm_stage_t s, swarm_stream_t stream) {
+    if (s->banks) return SWARM_OK;
+    s->p16b[0] = s->p16;
+    s->gradb[0] = s->grad;
+    TRY(alloc(s, &s->p16b[1], s->nparams));
+    TRY(alloc(s, &s->gradb[1], s->nparams));  // zero-filled by dmalloc
+    const cudaStream_t st = static_cast<cudaStream_t>(stream);
+    if (cudaMemcpyAsync(s->p16b[1], s->p16b[0], s->nparams * sizeof(bf16), cudaMemcpyDeviceToDevice, st) !=
+        cudaSuccess)
+        return SWARM_E_CUDA;
+    s->banks = true;
+    return SWARM_OK;
+}
+
+int swarm_stage_set_bank(swarm_stage_t s, int bank) {
+    if (bank < 0 || bank > 1 || (bank == 1 && !s->banks)) return fail("set_bank: bank must be 0, or 1 after enable_banks");
+    s->bank = bank;
+    s->p16 = s->banks ? s->p16b[bank] : s->p16;
+    s->grad = s->banks ? s->gradb[bank] : s->grad;
+    return SWARM_OK;
+}
+
+float* swarm_stage_grads_bank(swarm_stage_t s, int bank) {
+    if (!s->banks) return bank == 0 ? s->grad : nullptr;
+    return (bank == 0 || bank == 1) ? s->gradb[bank] : nullptr;
+}
+
+int swarm_stage_optimizer_step_bank(swarm_stage_t s, int bank, float grad_scale, swarm_stream_t stream) {
+    if (!s->banks) return bank == 0 ? swarm_stage_optimizer_step(s, grad_scale, stream) : fail("optimizer_step_bank: no banks");
+    if (bank < 0 || bank > 1) return fail("optimizer_step_bank: bank must be 0 or 1");
+    s->step += 1;
+    const auto& c = s->cfg;
+    return swarm_adamw_step(s->p32, s->p16b[bank], s->gradb[bank], s->m, s->v, s->nparams, c.lr, c.beta1, c.beta2,
+                            c.eps, c.weight_decay, s->step, grad_scale, 1, stream);
 }
 
 int swarm_stage_param_info(swarm_stage_t s, int index, const char** name, size_t* offset, size_t* rows, size_t* cols) {

@@ -187,6 +187,35 @@ __global__ void k_adamw(float* __restrict__ p32, __nv_bfloat16* __restrict__ p16
     }
 }
 
+// 4 parameters per thread per iteration: 16-B loads of p32 / grad / m / v and an
+// 8-B store of the bf16 shadow (the scalar kernel ran at ~65% of HBM bandwidth)
+__global__ void k_adamw4(float4* __restrict__ p32, uint2* __restrict__ p16, float4* __restrict__ grad,
+                         float4* __restrict__ m, float4* __restrict__ v, size_t n4, float lr, float b1, float b2,
+                         float eps, float wd, float inv_bc1, float inv_sqrt_bc2, float gscale, int zero_grad) {
+    for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n4;
+         i += static_cast<size_t>(gridDim.x) * blockDim.x) {
+        const float4 g4 = grad[i], m4 = m[i], v4 = v[i], p4 = p32[i];
+        const float gs[4] = {g4.x, g4.y, g4.z, g4.w}, ms[4] = {m4.x, m4.y, m4.z, m4.w};
+        const float vs[4] = {v4.x, v4.y, v4.z, v4.w}, ps[4] = {p4.x, p4.y, p4.z, p4.w};
+        float mo[4], vo[4], po[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const float g = gs[k] * gscale;
+            mo[k] = b1 * ms[k] + (1.f - b1) * g;
+            vo[k] = b2 * vs[k] + (1.f - b2) * g * g;
+            po[k] = ps[k] - lr * ((mo[k] * inv_bc1) / (sqrtf(vo[k]) * inv_sqrt_bc2 + eps) + wd * ps[k]);
+        }
+        m[i] = make_float4(mo[0], mo[1], mo[2], mo[3]);
+        v[i] = make_float4(vo[0], vo[1], vo[2], vo[3]);
+        p32[i] = make_float4(po[0], po[1], po[2], po[3]);
+        if (p16) {
+            const __nv_bfloat162 a = __floats2bfloat162_rn(po[0], po[1]), b = __floats2bfloat162_rn(po[2], po[3]);
+            p16[i] = make_uint2(*reinterpret_cast<const uint32_t*>(&a), *reinterpret_cast<const uint32_t*>(&b));
+        }
+        if (zero_grad) grad[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+}
+
 // ------------------------------------------------------------------- init --
 __device__ __forceinline__ uint64_t splitmix64(uint64_t x) {
     x += 0x9E3779B97F4A7C15ull;
@@ -276,6 +305,18 @@ int swarm_adamw_step(float* p32, void* p16, float* grad, float* m, float* v, siz
     if (n == 0) return SWARM_OK;
     const float bc1 = 1.f - std::pow(beta1, static_cast<float>(step));
     const float bc2 = 1.f - std::pow(beta2, static_cast<float>(step));
+    const bool vec = n % 4 == 0 && !((reinterpret_cast<uintptr_t>(p32) | reinterpret_cast<uintptr_t>(grad) |
+                                      reinterpret_cast<uintptr_t>(m) | reinterpret_cast<uintptr_t>(v)) & 15) &&
+                     !(reinterpret_cast<uintptr_t>(p16) & 7);
+    if (vec) {
+        // m / bc1 / (sqrt(v / bc2) + eps) == m * (1/bc1) / (sqrt(v) * (1/sqrt(bc2)) + eps)
+        k_adamw4<<<grid_for(n / 4, 256, 148u * 16u), 256, 0, as_stream(stream)>>>(
+            reinterpret_cast<float4*>(p32), static_cast<uint2*>(p16), reinterpret_cast<float4*>(grad),
+            reinterpret_cast<float4*>(m), reinterpret_cast<float4*>(v), n / 4, lr, beta1, beta2, eps, weight_decay,
+            1.f / bc1, 1.f / std::sqrt(bc2), grad_scale, zero_grad);
+        SWARM_LAUNCH_CHECK("k_adamw4");
+        return SWARM_OK;
+    }
     k_adamw<<<grid_for(n, 256, 148u * 16u), 256, 0, as_stream(stream)>>>(
         p32, static_cast<__nv_bfloat16*>(p16), grad, m, v, n, lr, beta1, beta2, eps, weight_decay, bc1, bc2,
         grad_scale, zero_grad);

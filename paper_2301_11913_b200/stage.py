@@ -121,6 +121,23 @@ class Stage:
     def sync_shadow(self, stream=None) -> None:
         L.check(self.lib.swarm_stage_sync_shadow(self.h, _stream(stream)), "stage_sync_shadow")
 
+    # -- delayed parameter updates (two shadow / gradient banks) ---------------
+    def enable_banks(self, stream=None) -> None:
+        L.check(self.lib.swarm_stage_enable_banks(self.h, _stream(stream)), "stage_enable_banks")
+
+    def set_bank(self, bank: int) -> None:
+        L.check(self.lib.swarm_stage_set_bank(self.h, bank), "stage_set_bank")
+
+    def grads_bank(self, bank: int) -> torch.Tensor:
+        ptr = self.lib.swarm_stage_grads_bank(self.h, bank)
+        if not ptr:
+            raise ValueError(f"no gradient bank {bank}")
+        return device_view(ptr, self.n_params, torch.float32, self.device)
+
+    def optimizer_step_bank(self, bank: int, grad_scale: float = 1.0, stream=None) -> None:
+        L.check(self.lib.swarm_stage_optimizer_step_bank(self.h, bank, grad_scale, _stream(stream)),
+                "stage_optimizer_step_bank")
+
     # -- state ---------------------------------------------------------------
     def grads(self) -> torch.Tensor:
         return device_view(self.lib.swarm_stage_grads(self.h), self.n_params, torch.float32, self.device)

@@ -218,7 +218,7 @@ class SwarmPipeline:
     def __init__(self, mcfg: ModelConfig, n_stages: int = 4, *, n_microbatches: int = 16, n_trainers: int | None = None,
                  seed: int = 0, lr: float = 1e-4, weight_decay: float = 0.0, gamma: float = 0.1, epsilon: float = 1.0,
                  modeled_flops: float = 1.0e15, profile: bool = False, use_graphs: bool = True,
-                 layout: list | None = None, max_slots: int | None = None):
+                 layout: list | None = None, max_slots: int | None = None, dpu: bool = False):
         self.m = mcfg
         self.S = n_stages
         self.M = n_microbatches
@@ -269,6 +269,17 @@ class SwarmPipeline:
         self.last_routes: list[list[int]] = []
         self.visits = [0] * len(self.pl.stage_of)  # forward visits per peer since the last rebalance
         self.events: list[dict] = []               # membership log (failures, migrations)
+        # Delayed parameter updates: step t computes on
+        # bank t % 2 while the all-reduce + AdamW of step t-1 run on a separate stream;
+        # step t therefore sees the weights of step t-2's update (one step of delay).
+        self.dpu = dpu
+        self.t = 0
+        if dpu:
+            self.update_stream = torch.cuda.Stream(device=self.device)
+            self.update_done = [None, None]  # event: optimizer of the last step that used bank b
+            for st in self.stages.values():
+                st.enable_banks()
+            torch.cuda.synchronize()
 
     def _new_stage(self, s: int, slots: int | None = None) -> Stage:
         m = self.m
@@ -297,6 +308,8 @@ class SwarmPipeline:
     def fail_peer(self, pid: int) -> None:
         """A peer leaves (sim.cpp:583-625 kill_worker): every router forgets it,
         its stage's all-reduce group shrinks, and the rank stops serving."""
+        if self.dpu:
+            raise NotImplementedError("membership changes with delayed parameter updates")
         torch.cuda.synchronize()
         self.planner.remove(pid)
         self.pl.alive.discard(pid)
@@ -326,6 +339,8 @@ class SwarmPipeline:
         routers ban the mover, it rebuilds its stage executor for `to_stage`
         and downloads params + AdamW moments + step from the lowest-id live
         stage-mate (NCCL point-to-point), groups are rebuilt, routers re-add it."""
+        if self.dpu:
+            raise NotImplementedError("membership changes with delayed parameter updates")
         torch.cuda.synchronize()
         if self.world < self.S:
             raise RuntimeError("migration needs one peer per rank (world >= stages)")
@@ -371,6 +386,8 @@ class SwarmPipeline:
     def step(self, tokens: torch.Tensor, targets: torch.Tensor, loss_scale: float | None = None) -> None:
         """One optimizer step over M microbatches.  tokens/targets: int32
         [M, B*L] on this device (only read by the first / last stage)."""
+        if self.dpu:
+            return self._step_dpu(tokens, targets, loss_scale)
         routes = self.plan()
         self._profiled.clear()
         scale = loss_scale if loss_scale is not None else 1.0 / (self.M * self.m.tokens)
@@ -395,6 +412,46 @@ class SwarmPipeline:
         if ev:
             ev[3].record()
             self._phase_events.append(ev)
+
+    def _step_dpu(self, tokens, targets, loss_scale) -> None:
+        """One step with delayed parameter updates: visits on bank t % 2 (after the
+        optimizer that last wrote that bank, two steps ago, has finished), then the
+        stage all-reduce + AdamW of this bank queued on the update stream."""
+        bank = self.t % 2
+        cur = torch.cuda.current_stream()
+        if self.update_done[bank] is not None:
+            cur.wait_event(self.update_done[bank])
+        for st in self.stages.values():
+            st.set_bank(bank)
+        routes = self.plan()
+        self._profiled.clear()
+        scale = loss_scale if loss_scale is not None else 1.0 / (self.M * self.m.tokens)
+        if self.all_local:
+            self._step_local(routes, tokens, targets, scale)
+        else:
+            self._step_pipelined(routes, tokens, targets, scale)
+        visits_done = torch.cuda.Event()
+        visits_done.record(cur)
+        with torch.cuda.stream(self.update_stream):
+            self.update_stream.wait_event(visits_done)
+            for s, st in self.stages.items():
+                if s in self.stage_group:
+                    dist.all_reduce(st.grads_bank(bank), op=dist.ReduceOp.SUM, group=self.stage_group[s])
+            for st in self.stages.values():
+                st.optimizer_step_bank(bank, grad_scale=1.0, stream=self.update_stream)
+            done = torch.cuda.Event()
+            done.record(self.update_stream)
+        self.update_done[bank] = done
+        self.t += 1
+
+    def drain_updates(self) -> None:
+        """Make the current stream wait for every queued delayed update (end of a
+        timed region: the last step's optimizer is part of its cost)."""
+        if self.dpu:
+            cur = torch.cuda.current_stream()
+            for e in self.update_done:
+                if e is not None:
+                    cur.wait_event(e)
 
     def phase_read(self) -> dict:
         """Per-step device time of this rank's phases since the last read (ms):
@@ -439,16 +496,20 @@ class SwarmPipeline:
         g.replay()
         self.replayed_kernels += self.graph_kernels[key]
 
+    def _bank(self) -> int:  # captured graphs bake the bank's weight / gradient pointers
+        return self.t % 2 if self.dpu else 0
+
     def _fwd(self, s, slot, inp, out=None, targets=None, scale=1.0) -> None:
         st = self.stages[s]
-        key = (s, "f", slot, inp.data_ptr(), None if out is None else out.data_ptr(),
+        key = (s, "f", slot, self._bank(), inp.data_ptr(), None if out is None else out.data_ptr(),
                None if targets is None else targets.data_ptr())
         self._run(key, lambda: st.forward(slot, inp, out=out, targets=targets, loss_sum=self.loss_sum,
                                           loss_scale=scale))
 
     def _bwd(self, s, slot, gin=None, gout=None) -> None:
         st = self.stages[s]
-        key = (s, "b", slot, None if gin is None else gin.data_ptr(), None if gout is None else gout.data_ptr())
+        key = (s, "b", slot, self._bank(), None if gin is None else gin.data_ptr(),
+               None if gout is None else gout.data_ptr())
         self._run(key, lambda: st.backward(slot, grad_in=gin, grad_out=gout))
 
     def _step_local(self, routes, tokens, targets, scale) -> None:

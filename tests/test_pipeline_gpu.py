@@ -41,3 +41,30 @@ def test_stage_wire_bf16_path(cuda):
         s1.forward(0, a, targets=tok, loss_sum=loss, loss_scale=1.0)
         outs[wire] = loss.item()
     assert abs(outs[WIRE_BF16] - outs[WIRE_INT8]) <= 2e-3 * abs(outs[WIRE_BF16])
+
+
+def test_delayed_parameter_updates(cuda):
+    """Delayed parameter updates: with a fixed batch, step 1 runs on
+    the initial weights again (its loss equals step 0's) and step 2 on the weights
+    of step 0's update (its loss equals the synchronous run's step 1), while the
+    all-reduce + AdamW of each step overlap the next step on a side stream."""
+    import torch
+    from paper_2301_11913_b200.swarm import PRESETS, SwarmPipeline, synthetic_batch
+    m = PRESETS["tiny"]
+    tok, _ = synthetic_batch(m, 4, seed=1, device=cuda)
+    tgt = torch.roll(tok, -1, dims=1)
+    runs = {}
+    for dpu in (False, True):
+        pipe = SwarmPipeline(m, 4, n_microbatches=4, seed=3, lr=3e-3, dpu=dpu)
+        losses = []
+        for _ in range(5):
+            pipe.loss_sum.zero_()
+            pipe.step(tok, tgt)
+            pipe.drain_updates()
+            losses.append(pipe.loss_sum.item() / pipe.tokens_per_step())
+        runs[dpu] = losses
+    sync, dpu = runs[False], runs[True]
+    assert dpu[0] == pytest.approx(sync[0], rel=1e-6)
+    assert dpu[1] == pytest.approx(sync[0], rel=1e-6)
+    assert dpu[2] == pytest.approx(sync[1], rel=1e-6)
+    assert dpu[4] < dpu[0] - 0.1, dpu  # it still trains
