@@ -12,6 +12,7 @@
 #include <cstring>
 #include <new>
 #include <string>
+#include <unordered_map>
 #include <vector>
 
 #include "swarm_b200.h"
@@ -70,6 +71,12 @@ struct swarm_stage {
     float* gradb[2] = {nullptr, nullptr};
     bool banks = false;
     int bank = 0;
+    // LayerNorm gains / biases are read in fp32 from the master; with banks each
+    // bank keeps its own compact copy (the master is being updated concurrently)
+    std::vector<std::pair<size_t, size_t>> ln_slices;  // (arena offset, elements)
+    std::unordered_map<size_t, size_t> ln_compact;    // arena offset -> compact offset
+    size_t ln_total = 0;
+    float* lnv[2] = {nullptr, nullptr};
     std::vector<Slot> slots;
     // workspaces (one visit at a time per stage)
     float *S = nullptr, *dP = nullptr, *logits = nullptr;
@@ -136,9 +143,29 @@ int alloc(swarm_stage* s, T** p, size_t count) {
     return SWARM_OK;
 }
 
+// fp32 LayerNorm parameter at arena offset `off` as the current visit must read it
+const float* ln_param(const swarm_stage* s, size_t off) {
+    if (!s->banks) return s->p32 + off;
+    return s->lnv[s->bank] + s->ln_compact.at(off);
+}
+
+// refresh bank b's compact LayerNorm copy from the fp32 master
+int refresh_ln(swarm_stage* s, int b, cudaStream_t st) {
+    for (const auto& [off, n] : s->ln_slices)
+        if (cudaMemcpyAsync(s->lnv[b] + s->ln_compact.at(off), s->p32 + off, n * sizeof(float),
+                            cudaMemcpyDeviceToDevice, st) != cudaSuccess)
+            return SWARM_E_CUDA;
+    return SWARM_OK;
+}
+
 size_t add_tensor(swarm_stage* s, const std::string& name, size_t rows, size_t cols) {
     const size_t off = s->nparams;
     s->tensors.push_back({name, off, rows, cols});
+    if (rows == 1) {  // LayerNorm gain / bias
+        s->ln_compact[off] = s->ln_total;
+        s->ln_slices.emplace_back(off, cols);
+        s->ln_total += (cols + 63) & ~size_t(63);
+    }
     s->nparams += (rows * cols + 63) & ~size_t(63);  // 256-byte aligned fp32 / 128-byte bf16 slices
     return off;
 }
@@ -317,8 +344,7 @@ int join_side(swarm_stage* s, cudaStream_t main) {
 int block_forward(swarm_stage* s, Act& A, bf16* y, const LayerW& W, cudaStream_t st) {
     const int T = s->T, d = s->d, H = s->H, dh = s->dh, F = s->F, L = s->L;
     const bf16* p16 = s->p16;
-    const float* p32 = s->p32;
-    PTRY(SWARM_PROF_LAYERNORM, st, swarm_layer_norm_forward(A.x, SWARM_DTYPE_BF16, T, d, p32 + W.ln1g, p32 + W.ln1b, 1e-5, A.a, A.mu1, A.rs1, st));
+    PTRY(SWARM_PROF_LAYERNORM, st, swarm_layer_norm_forward(A.x, SWARM_DTYPE_BF16, T, d, ln_param(s, W.ln1g), ln_param(s, W.ln1b), 1e-5, A.a, A.mu1, A.rs1, st));
     TRY(mm(T, 3 * d, d, {A.a, d, T, d, false}, {p16 + W.wqkv, d, 3 * d, d, false}, A.qkv, 3 * d,
            SWARM_EPI_STORE_BF16, nullptr, 1.f, st));
     const float scale = 1.f / std::sqrt(static_cast<float>(dh));
@@ -337,7 +363,7 @@ int block_forward(swarm_stage* s, Act& A, bf16* y, const LayerW& W, cudaStream_t
             {{A.qkv + 2 * d, 3 * d, T, d, true}, L, 0, 0, dh}, A.o, d, L, 0, 0, dh, SWARM_EPI_STORE_BF16, 1.f, st, 1));
     // h = x + O Wo^T
     TRY(mm(T, d, d, {A.o, d, T, d, false}, {p16 + W.wo, d, d, d, false}, A.h, d, SWARM_EPI_RESIDUAL, A.x, 1.f, st));
-    PTRY(SWARM_PROF_LAYERNORM, st, swarm_layer_norm_forward(A.h, SWARM_DTYPE_BF16, T, d, p32 + W.ln2g, p32 + W.ln2b, 1e-5, A.c, A.mu2, A.rs2, st));
+    PTRY(SWARM_PROF_LAYERNORM, st, swarm_layer_norm_forward(A.h, SWARM_DTYPE_BF16, T, d, ln_param(s, W.ln2g), ln_param(s, W.ln2b), 1e-5, A.c, A.mu2, A.rs2, st));
     // u = c W1^T, g = gelu(u)
     TRY(mm(T, F, d, {A.c, d, T, d, false}, {p16 + W.w1, d, F, d, false}, A.g, F, SWARM_EPI_GELU, A.u, 1.f, st));
     // y = h + g W2^T
@@ -350,7 +376,6 @@ int block_forward(swarm_stage* s, Act& A, bf16* y, const LayerW& W, cudaStream_t
 int block_backward(swarm_stage* s, const Act& A, const bf16* dy, bf16* dx, const LayerW& W, cudaStream_t st) {
     const int T = s->T, d = s->d, H = s->H, dh = s->dh, F = s->F, L = s->L, BHL = s->B * s->H * s->L;
     const bf16* p16 = s->p16;
-    const float* p32 = s->p32;
     float* G = s->grad;
     cudaStream_t sd = side_of(s, st);  // weight gradients
     // MLP: du = (dy W2) * gelu'(u); dW2 += dy^T g; dc = du W1; dW1 += du^T c
@@ -362,7 +387,7 @@ int block_backward(swarm_stage* s, const Act& A, const bf16* dy, bf16* dx, const
     TRY(mm(T, d, F, {s->du, F, T, F, false}, {p16 + W.w1, d, F, d, true}, s->dc, d, SWARM_EPI_STORE_BF16, nullptr, 1.f,
            st));
     // dh = LN2'(dc) + dy
-    PTRY(SWARM_PROF_LAYERNORM, st, swarm_layer_norm_backward(s->dc, A.h, SWARM_DTYPE_BF16, T, d, p32 + W.ln2g, A.mu2, A.rs2, dy, s->dhid,
+    PTRY(SWARM_PROF_LAYERNORM, st, swarm_layer_norm_backward(s->dc, A.h, SWARM_DTYPE_BF16, T, d, ln_param(s, W.ln2g), A.mu2, A.rs2, dy, s->dhid,
                                   G + W.ln2g, G + W.ln2b, 1, s->lnws, st));
     // attention output projection
     TRY(fork_side(s, st, 2));
@@ -397,7 +422,7 @@ int block_backward(swarm_stage* s, const Act& A, const bf16* dy, bf16* dx, const
     TRY(mm(T, d, 3 * d, {s->dqkv, 3 * d, T, 3 * d, false}, {p16 + W.wqkv, d, 3 * d, d, true}, s->da, d,
            SWARM_EPI_STORE_BF16, nullptr, 1.f, st));
     // dx = LN1'(da) + dh
-    PTRY(SWARM_PROF_LAYERNORM, st, swarm_layer_norm_backward(s->da, A.x, SWARM_DTYPE_BF16, T, d, p32 + W.ln1g, A.mu1, A.rs1, s->dhid, dx,
+    PTRY(SWARM_PROF_LAYERNORM, st, swarm_layer_norm_backward(s->da, A.x, SWARM_DTYPE_BF16, T, d, ln_param(s, W.ln1g), A.mu1, A.rs1, s->dhid, dx,
                                   G + W.ln1g, G + W.ln1b, 1, s->lnws, st));
     // the next layer overwrites the workspaces the weight gradients read
     return join_side(s, st);
@@ -694,6 +719,7 @@ void* swarm_stage_params_bf16(swarm_stage_t s) { return s->p16; }
 int swarm_stage_sync_shadow(swarm_stage_t s, swarm_stream_t stream) {
     if (!s->banks) return swarm_cast_f32_bf16(s->p32, s->p16, s->nparams, stream);
     for (bf16* p : s->p16b) TRY(swarm_cast_f32_bf16(s->p32, p, s->nparams, stream));
+    for (int b = 0; b < 2; ++b) TRY(refresh_ln(s, b, static_cast<cudaStream_t>(stream)));
     return SWARM_OK;
 }
 
@@ -704,6 +730,9 @@ int swarm_stage_enable_banks(swarm_stage_t s, swarm_stream_t stream) {
     TRY(alloc(s, &s->p16b[1], s->nparams));
     TRY(alloc(s, &s->gradb[1], s->nparams));  // zero-filled by dmalloc
     const cudaStream_t st = static_cast<cudaStream_t>(stream);
+    for (float*& l : s->lnv) TRY(alloc(s, &l, s->ln_total));
+    TRY(refresh_ln(s, 0, st));
+    TRY(refresh_ln(s, 1, st));
     if (cudaMemcpyAsync(s->p16b[1], s->p16b[0], s->nparams * sizeof(bf16), cudaMemcpyDeviceToDevice, st) !=
         cudaSuccess)
         return SWARM_E_CUDA;
@@ -729,8 +758,9 @@ int swarm_stage_optimizer_step_bank(swarm_stage_t s, int bank, float grad_scale,
     if (bank < 0 || bank > 1) return fail("optimizer_step_bank: bank must be 0 or 1");
     s->step += 1;
     const auto& c = s->cfg;
-    return swarm_adamw_step(s->p32, s->p16b[bank], s->gradb[bank], s->m, s->v, s->nparams, c.lr, c.beta1, c.beta2,
-                            c.eps, c.weight_decay, s->step, grad_scale, 1, stream);
+    TRY(swarm_adamw_step(s->p32, s->p16b[bank], s->gradb[bank], s->m, s->v, s->nparams, c.lr, c.beta1, c.beta2,
+                         c.eps, c.weight_decay, s->step, grad_scale, 1, stream));
+    return refresh_ln(s, bank, static_cast<cudaStream_t>(stream));
 }
 
 int swarm_stage_param_info(swarm_stage_t s, int index, const char** name, size_t* offset, size_t* rows, size_t* cols) {
@@ -782,7 +812,7 @@ int swarm_stage_forward(swarm_stage_t s, int slot, const void* in, const int32_t
         // receiver: x0 = LN_d(dequant(wire)) W_d^T   (d/k -> d)
         const int w = s->wire_w;
         PTRY(SWARM_PROF_OTHER, st, wire_decode(s, in, sl.mi, st));
-        PTRY(SWARM_PROF_LAYERNORM, st, swarm_layer_norm_forward(sl.mi, SWARM_DTYPE_BF16, T, w, s->p32 + s->bn_in_g, s->p32 + s->bn_in_b, 1e-5,
+        PTRY(SWARM_PROF_LAYERNORM, st, swarm_layer_norm_forward(sl.mi, SWARM_DTYPE_BF16, T, w, ln_param(s, s->bn_in_g), ln_param(s, s->bn_in_b), 1e-5,
                                      sl.ni, sl.mud, sl.rsd, st));
         TRY(mm(T, d, w, {sl.ni, w, T, w, false}, {s->p16 + s->bn_wd, w, d, w, false}, sl.layer[0].x, d,
                SWARM_EPI_STORE_BF16, nullptr, 1.f, st));
@@ -800,7 +830,7 @@ int swarm_stage_forward(swarm_stage_t s, int slot, const void* in, const int32_t
             return wire_encode(s, sl.out, out, st);
         }
         // sender: wire = int8(maxout_k(LN_c(out)))
-        PTRY(SWARM_PROF_LAYERNORM, st, swarm_layer_norm_forward(sl.out, SWARM_DTYPE_BF16, T, d, s->p32 + s->bn_out_g, s->p32 + s->bn_out_b, 1e-5,
+        PTRY(SWARM_PROF_LAYERNORM, st, swarm_layer_norm_forward(sl.out, SWARM_DTYPE_BF16, T, d, ln_param(s, s->bn_out_g), ln_param(s, s->bn_out_b), 1e-5,
                                      sl.z, sl.muc, sl.rsc, st));
         PTRY(SWARM_PROF_OTHER, st, swarm_maxout_forward(sl.z, SWARM_DTYPE_BF16, static_cast<size_t>(T) * d, s->cfg.maxout_k, sl.mo, sl.am,
                                  st));
@@ -809,7 +839,7 @@ int swarm_stage_forward(swarm_stage_t s, int slot, const void* in, const int32_t
     }
     if (!targets) return fail("forward: last stage needs targets");
     // final LN + LM head + cross-entropy, with the head's backward fused in
-    PTRY(SWARM_PROF_LAYERNORM, st, swarm_layer_norm_forward(sl.out, SWARM_DTYPE_BF16, T, d, s->p32 + s->lnfg, s->p32 + s->lnfb, 1e-5, sl.xf,
+    PTRY(SWARM_PROF_LAYERNORM, st, swarm_layer_norm_forward(sl.out, SWARM_DTYPE_BF16, T, d, ln_param(s, s->lnfg), ln_param(s, s->lnfb), 1e-5, sl.xf,
                                  sl.muf, sl.rsf, st));
     TRY(mm(T, s->V, d, {sl.xf, d, T, d, false}, {s->p16 + s->head, d, s->V, d, false}, s->logits, s->V,
            SWARM_EPI_STORE_F32, nullptr, 1.f, st));
@@ -830,7 +860,7 @@ int swarm_stage_backward(swarm_stage_t s, int slot, const void* grad_in, void* g
     const int T = s->T, d = s->d, n = s->cfg.n_layers;
     int cur = 0;
     if (s->cfg.is_last) {
-        PTRY(SWARM_PROF_LAYERNORM, st, swarm_layer_norm_backward(sl.dxf, sl.out, SWARM_DTYPE_BF16, T, d, s->p32 + s->lnfg, sl.muf, sl.rsf, nullptr,
+        PTRY(SWARM_PROF_LAYERNORM, st, swarm_layer_norm_backward(sl.dxf, sl.out, SWARM_DTYPE_BF16, T, d, ln_param(s, s->lnfg), sl.muf, sl.rsf, nullptr,
                                       s->gy[0], s->grad + s->lnfg, s->grad + s->lnfb, 1, s->lnws, st));
     } else {
         if (!grad_in) return fail("backward: null gradient message");
@@ -839,7 +869,7 @@ int swarm_stage_backward(swarm_stage_t s, int slot, const void* grad_in, void* g
             PTRY(SWARM_PROF_OTHER, st, wire_decode(s, grad_in, s->wtmp, st));
             PTRY(SWARM_PROF_OTHER, st, swarm_maxout_backward(s->wtmp, SWARM_DTYPE_BF16, sl.am, static_cast<size_t>(T) * s->wire_w,
                                       s->cfg.maxout_k, s->dc, st));
-            PTRY(SWARM_PROF_LAYERNORM, st, swarm_layer_norm_backward(s->dc, sl.out, SWARM_DTYPE_BF16, T, d, s->p32 + s->bn_out_g, sl.muc, sl.rsc,
+            PTRY(SWARM_PROF_LAYERNORM, st, swarm_layer_norm_backward(s->dc, sl.out, SWARM_DTYPE_BF16, T, d, ln_param(s, s->bn_out_g), sl.muc, sl.rsc,
                                           nullptr, s->gy[0], s->grad + s->bn_out_g, s->grad + s->bn_out_b, 1, s->lnws,
                                           st));
         } else {
@@ -866,7 +896,7 @@ int swarm_stage_backward(swarm_stage_t s, int slot, const void* grad_in, void* g
            1.f, st));
     TRY(mm(T, w, d, {dx0, d, T, d, false}, {s->p16 + s->bn_wd, w, d, w, true}, s->wtmp, w, SWARM_EPI_STORE_BF16,
            nullptr, 1.f, st));
-    PTRY(SWARM_PROF_LAYERNORM, st, swarm_layer_norm_backward(s->wtmp, sl.mi, SWARM_DTYPE_BF16, T, w, s->p32 + s->bn_in_g, sl.mud, sl.rsd, nullptr,
+    PTRY(SWARM_PROF_LAYERNORM, st, swarm_layer_norm_backward(s->wtmp, sl.mi, SWARM_DTYPE_BF16, T, w, ln_param(s, s->bn_in_g), sl.mud, sl.rsd, nullptr,
                                   s->dqkv, s->grad + s->bn_in_g, s->grad + s->bn_in_b, 1, s->lnws, st));
     ProfOp po(SWARM_PROF_OTHER, st);
     return wire_encode(s, s->dqkv, grad_out, st);
