@@ -25,7 +25,7 @@ class GemmArgs(C.Structure):
         ("b", C.c_void_p), ("ldb", C.c_int), ("b_mn_major", C.c_int), ("b_rows", C.c_int), ("b_cols", C.c_int),
         ("rb0", C.c_int), ("rb1", C.c_int), ("cb0", C.c_int), ("cb1", C.c_int),
         ("d", C.c_void_p), ("ldd", C.c_int), ("rd0", C.c_int), ("rd1", C.c_int), ("cd0", C.c_int), ("cd1", C.c_int),
-        ("aux", C.c_void_p), ("alpha", C.c_float), ("epilogue", C.c_int), ("k_tri", C.c_int),
+        ("aux", C.c_void_p), ("alpha", C.c_float), ("epilogue", C.c_int), ("k_tri", C.c_int), ("a2", C.c_void_p), ("b2", C.c_void_p),
         ("workspace", C.c_void_p), ("workspace_bytes", C.c_size_t)]
 
 
@@ -78,6 +78,9 @@ SIGNATURES = {
     "swarm_stage_params_bf16": (P, [P]),
     "swarm_stage_sync_shadow": (I, [P, P]),
     "swarm_stage_enable_banks": (I, [P, P]),
+    "swarm_stage_enable_wgrad_pairing": (I, [P]),
+    "swarm_stage_backward_ex": (I, [P, I, P, P, I, I, I, I, P]),
+    "swarm_stage_flush_wgrad": (I, [P, I, I, P]),
     "swarm_stage_set_bank": (I, [P, I]),
     "swarm_stage_grads_bank": (P, [P, I]),
     "swarm_stage_optimizer_step_bank": (I, [P, I, F, P]),

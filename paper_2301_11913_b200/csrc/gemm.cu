@@ -58,6 +58,7 @@ struct Params {
     int* sk_cnt;    // [sk_tile][half][warp] arrival counters (self-resetting)
     int* sk_ready;  // [cluster][first|last][half][warp] partial-ready flags (self-resetting)
     int k_tri;    // swarm_gemm_args.k_tri (1-CTA kernel): skip all-zero k-blocks of a triangular A
+    int kb_half;  // two-segment K (pair kernel): k-blocks >= kb_half come from tma_a2 / tma_b2 (0 = one segment)
     int dbg;      // SWARM_GEMM_DBG (experiments only): 1 skip output stores, 2 skip MMAs, 4 skip TMA loads,
                   // 8 stream-K units store directly (no fixup), 16 fixup without waiting for partials
 };
@@ -568,7 +569,8 @@ struct Cfg2 {
 template <bool A_MN, bool B_MN, int NPAIR>
 __global__ void __launch_bounds__(kThreads, 1)
     k_gemm2(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUtensorMap tma_b,
-            const __grid_constant__ CUtensorMap tma_d, const __grid_constant__ CUtensorMap tma_u, const Params p) {
+            const __grid_constant__ CUtensorMap tma_d, const __grid_constant__ CUtensorMap tma_u,
+            const __grid_constant__ CUtensorMap tma_a2, const __grid_constant__ CUtensorMap tma_b2, const Params p) {
     using C = Cfg2;
     pdl_trigger();
     extern __shared__ uint8_t smem_raw[];
@@ -598,6 +600,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (warp == 0 && lane == 0) {
         tma_prefetch(&tma_a);
         tma_prefetch(&tma_b);
+        if (p.kb_half) {
+            tma_prefetch(&tma_a2);
+            tma_prefetch(&tma_b2);
+        }
         for (int s = 0; s < C::STAGES; ++s) {
             mbar_init(&full[s], 1);
             mbar_init(&empty[s], NPAIR);  // every pair's MMA frees a stage its A multicast wrote
@@ -648,32 +654,36 @@ __global__ void __launch_bounds__(kThreads, 1)
                     const uint32_t bar = pair_leader_addr(&full[stage]);
                     uint8_t* a_dst = sa + stage * C::A_BYTES;
                     uint8_t* b_dst = sb + stage * C::B_BYTES;
+                    // two-segment K (paired microbatches): the second half of K lives in other buffers
+                    const bool seg2 = p.kb_half && kb >= p.kb_half;
+                    const CUtensorMap* ma = seg2 ? &tma_a2 : &tma_a;
+                    const CUtensorMap* mb = seg2 ? &tma_b2 : &tma_b;
+                    const int kk = seg2 ? kb - p.kb_half : kb;
                     if constexpr (NPAIR == 1) {
                         if constexpr (!A_MN) {
-                            tma_load_2d_pair(a_dst, &tma_a, bar, ca + kb * BK, ra + m0);
+                            tma_load_2d_pair(a_dst, ma, bar, ca + kk * BK, ra + m0);
                         } else {
 #pragma unroll
                             for (int j = 0; j < 2; ++j)
-                                tma_load_2d_pair(a_dst + j * (64 * BK * 2), &tma_a, bar, ca + m0 + j * 64,
-                                                 ra + kb * BK);
+                                tma_load_2d_pair(a_dst + j * (64 * BK * 2), ma, bar, ca + m0 + j * 64, ra + kk * BK);
                         }
                     } else {
                         // both pairs need this A half: each pair loads one 64-row (K-major) or
                         // 64-column (MN-major) piece and multicasts it to the same half of every pair
                         const uint16_t mc = static_cast<uint16_t>(0x5u << half);
                         if constexpr (!A_MN)
-                            tma_load_2d_pair_mc(a_dst + pair * (64 * 128), &tma_a, bar, ca + kb * BK, ra + m0 + pair * 64,
+                            tma_load_2d_pair_mc(a_dst + pair * (64 * 128), ma, bar, ca + kk * BK, ra + m0 + pair * 64,
                                                 mc);
                         else
-                            tma_load_2d_pair_mc(a_dst + pair * (64 * BK * 2), &tma_a, bar, ca + m0 + pair * 64,
-                                                ra + kb * BK, mc);
+                            tma_load_2d_pair_mc(a_dst + pair * (64 * BK * 2), ma, bar, ca + m0 + pair * 64,
+                                                ra + kk * BK, mc);
                     }
                     if constexpr (!B_MN) {
-                        tma_load_2d_pair(b_dst, &tma_b, bar, cb + kb * BK, rb + n0);
+                        tma_load_2d_pair(b_dst, mb, bar, cb + kk * BK, rb + n0);
                     } else {
 #pragma unroll
                         for (int j = 0; j < 2; ++j)
-                            tma_load_2d_pair(b_dst + j * (64 * BK * 2), &tma_b, bar, cb + n0 + j * 64, rb + kb * BK);
+                            tma_load_2d_pair(b_dst + j * (64 * BK * 2), mb, bar, cb + n0 + j * 64, rb + kk * BK);
                     }
                     if (++stage == C::STAGES) {
                         stage = 0;
@@ -982,7 +992,7 @@ int launch(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& td, 
 
 template <bool A_MN, bool B_MN, int NPAIR>
 int launch_pair(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& td, const CUtensorMap& tu,
-                const Params& p, int clusters, cudaStream_t st) {
+                const CUtensorMap& ta2, const CUtensorMap& tb2, const Params& p, int clusters, cudaStream_t st) {
     auto kern = k_gemm2<A_MN, B_MN, NPAIR>;
     static bool attr = false;
     if (!attr) {
@@ -1001,7 +1011,7 @@ int launch_pair(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap&
     attrs[0].val.clusterDim.z = 1;
     cfg.attrs = attrs;
     cfg.numAttrs = 1 + pdl_attr(&attrs[1]);
-    SWARM_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, ta, tb, td, tu, p));
+    SWARM_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, ta, tb, td, tu, ta2, tb2, p));
     SWARM_LAUNCH_CHECK("k_gemm2");
     return SWARM_OK;
 }
@@ -1048,11 +1058,12 @@ int max_quad_clusters() {  // 4-CTA clusters of the multicast variant
 
 template <int NPAIR>
 int dispatch_pair(bool amn, bool bmn, const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& td,
-                  const CUtensorMap& tu, const Params& p, int clusters, cudaStream_t st) {
-    if (!amn && !bmn) return launch_pair<false, false, NPAIR>(ta, tb, td, tu, p, clusters, st);
-    if (!amn && bmn) return launch_pair<false, true, NPAIR>(ta, tb, td, tu, p, clusters, st);
-    if (amn && !bmn) return launch_pair<true, false, NPAIR>(ta, tb, td, tu, p, clusters, st);
-    return launch_pair<true, true, NPAIR>(ta, tb, td, tu, p, clusters, st);
+                  const CUtensorMap& tu, const CUtensorMap& ta2, const CUtensorMap& tb2, const Params& p, int clusters,
+                  cudaStream_t st) {
+    if (!amn && !bmn) return launch_pair<false, false, NPAIR>(ta, tb, td, tu, ta2, tb2, p, clusters, st);
+    if (!amn && bmn) return launch_pair<false, true, NPAIR>(ta, tb, td, tu, ta2, tb2, p, clusters, st);
+    if (amn && !bmn) return launch_pair<true, false, NPAIR>(ta, tb, td, tu, ta2, tb2, p, clusters, st);
+    return launch_pair<true, true, NPAIR>(ta, tb, td, tu, ta2, tb2, p, clusters, st);
 }
 
 // 4-CTA clusters (two pairs side by side in N sharing each A sub-tile by TMA
@@ -1111,15 +1122,36 @@ extern "C" int swarm_gemm_bf16(const swarm_gemm_args* a, swarm_stream_t stream) 
     if (a->k_tri < 0 || a->k_tri > 2 || (a->k_tri && a->m != a->k)) return invalid("gemm: k_tri needs M == K");
     if (a->lda % 8 || a->ldb % 8 || (reinterpret_cast<uintptr_t>(a->a) & 15) || (reinterpret_cast<uintptr_t>(a->b) & 15))
         return invalid("gemm: A/B rows must be 16-byte aligned");
-    // storage extents
+    const bool two_seg = a->a2 || a->b2;
+    if (two_seg) {
+        if (!a->a2 || !a->b2 || a->batch != 1 || a->k % (2 * BK) || a->k_tri ||
+            (reinterpret_cast<uintptr_t>(a->a2) & 15) || (reinterpret_cast<uintptr_t>(a->b2) & 15))
+            return invalid("gemm: two K segments need a2 and b2, batch 1, K a multiple of 128, no k_tri");
+        if (!(a->m > 128 && a->n > 128 && pair_enabled())) {
+            // the 1-CTA kernel has no second segment: two launches, the second accumulating
+            if (a->epilogue != SWARM_EPI_ACCUM_F32 && a->epilogue != SWARM_EPI_STORE_F32)
+                return invalid("gemm: two K segments on small tiles need an fp32 epilogue");
+            swarm_gemm_args h = *a;
+            h.a2 = h.b2 = nullptr;
+            h.k = a->k / 2;
+            int rc = swarm_gemm_bf16(&h, stream);
+            if (rc) return rc;
+            h.a = a->a2;
+            h.b = a->b2;
+            h.epilogue = SWARM_EPI_ACCUM_F32;
+            return swarm_gemm_bf16(&h, stream);
+        }
+    }
+    // storage extents (per K segment)
+    const long long kseg = two_seg ? a->k / 2 : a->k;
     long long ar = a->a_rows, ac = a->a_cols, br = a->b_rows, bc = a->b_cols;
     if (ar == 0 || ac == 0) {
-        ar = a->a_mn_major ? a->k : a->m;
-        ac = a->a_mn_major ? a->m : a->k;
+        ar = a->a_mn_major ? kseg : a->m;
+        ac = a->a_mn_major ? a->m : kseg;
     }
     if (br == 0 || bc == 0) {
-        br = a->b_mn_major ? a->k : a->n;
-        bc = a->b_mn_major ? a->n : a->k;
+        br = a->b_mn_major ? kseg : a->n;
+        bc = a->b_mn_major ? a->n : kseg;
     }
     // 2-CTA pair tiles (256 x 256) when both M and N fill them; else one CTA, 128 x BN
     const bool pair = pair_enabled() && a->m > 128 && a->n > 128;
@@ -1157,10 +1189,18 @@ extern "C" int swarm_gemm_bf16(const swarm_gemm_args* a, swarm_stream_t stream) 
     }
     const int npair = (pair && !use_sk && multicast_mode() && pair_tiles_n % 2 == 0) ? 2 : 1;
     CUtensorMap ta, tb;
-    int rc = encode_2d(&ta, a->a, ar, ac, a->lda, 64, a->a_mn_major ? BK : (npair == 2 ? 64 : BM));
+    const int box_a = a->a_mn_major ? BK : (npair == 2 ? 64 : BM), box_b = a->b_mn_major ? BK : (pair ? 128 : BN);
+    int rc = encode_2d(&ta, a->a, ar, ac, a->lda, 64, box_a);
     if (rc) return rc;
-    rc = encode_2d(&tb, a->b, br, bc, a->ldb, 64, a->b_mn_major ? BK : (pair ? 128 : BN));
+    rc = encode_2d(&tb, a->b, br, bc, a->ldb, 64, box_b);
     if (rc) return rc;
+    CUtensorMap ta2 = ta, tb2 = tb;
+    if (two_seg) {
+        rc = encode_2d(&ta2, a->a2, ar, ac, a->lda, 64, box_a);
+        if (rc) return rc;
+        rc = encode_2d(&tb2, a->b2, br, bc, a->ldb, 64, box_b);
+        if (rc) return rc;
+    }
     Params p{};
     p.m = a->m;
     p.n = a->n;
@@ -1178,6 +1218,7 @@ extern "C" int swarm_gemm_bf16(const swarm_gemm_args* a, swarm_stream_t stream) 
     p.rd0 = a->rd0; p.rd1 = a->rd1; p.cd0 = a->cd0; p.cd1 = a->cd1;
     p.aux = a->aux;
     p.k_tri = pair ? 0 : a->k_tri;  // the pair kernel computes the zero blocks (still exact)
+    p.kb_half = two_seg ? static_cast<int>(kseg / BK) : 0;
     p.alpha = a->alpha;
     p.epi = a->epilogue;
     const int esz = (a->epilogue == SWARM_EPI_STORE_F32 || a->epilogue == SWARM_EPI_ACCUM_F32) ? 4 : 2;
@@ -1223,8 +1264,9 @@ extern "C" int swarm_gemm_bf16(const swarm_gemm_args* a, swarm_stream_t stream) 
         p.ws = reinterpret_cast<float*>(static_cast<uint8_t*>(a->workspace) + kSkFlagBytes);
         grid_clusters = sk_C;
     }
-    if (pair && npair == 2) return dispatch_pair<2>(a->a_mn_major, a->b_mn_major, ta, tb, td, tu, p, grid_clusters, st);
-    if (pair) return dispatch_pair<1>(a->a_mn_major, a->b_mn_major, ta, tb, td, tu, p, grid_clusters, st);
+    if (pair && npair == 2)
+        return dispatch_pair<2>(a->a_mn_major, a->b_mn_major, ta, tb, td, tu, ta2, tb2, p, grid_clusters, st);
+    if (pair) return dispatch_pair<1>(a->a_mn_major, a->b_mn_major, ta, tb, td, tu, ta2, tb2, p, grid_clusters, st);
     if (BN == 128) return dispatch<128>(a->a_mn_major, a->b_mn_major, ta, tb, td, tu, p, st);
     return dispatch<256>(a->a_mn_major, a->b_mn_major, ta, tb, td, tu, p, st);
 }

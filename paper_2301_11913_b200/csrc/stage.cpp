@@ -26,6 +26,11 @@ struct TensorInfo {
     size_t off, rows, cols;
 };
 
+// one layer's backward gradients that its weight gradients read (paired mode)
+struct Stash {
+    bf16 *dy = nullptr, *du = nullptr, *dhid = nullptr, *dqkv = nullptr;
+};
+
 struct LayerW {
     size_t wqkv, wo, w1, w2, ln1g, ln1b, ln2g, ln2b;
 };
@@ -73,6 +78,9 @@ struct swarm_stage {
     int bank = 0;
     // LayerNorm gains / biases are read in fp32 from the master; with banks each
     // bank keeps its own compact copy (the master is being updated concurrently)
+    // paired weight gradients: per layer, the backward's dY tensors of a deferred
+    // visit (two sets: the pending visit's and the current one's)
+    std::vector<Stash> stash[2];
     std::vector<std::pair<size_t, size_t>> ln_slices;  // (arena offset, elements)
     std::unordered_map<size_t, size_t> ln_compact;    // arena offset -> compact offset
     size_t ln_total = 0;
@@ -269,6 +277,33 @@ int mm(int M, int N, int K, Op a, Op b, void* d, int ldd, int epi, const void* a
     return run_gemm(g, st);
 }
 
+// Weight gradient over two microbatches: K = 2T split into (a, b) then (a2, b2)
+int mm2(int M, int N, int K2, Op a, Op b, const void* a2, const void* b2, float* d, int ldd, cudaStream_t st) {
+    swarm_gemm_args g{};
+    g.m = M;
+    g.n = N;
+    g.k = K2;
+    g.batch = 1;
+    g.bh = 1;
+    g.a = a.p;
+    g.lda = a.ld;
+    g.a_mn_major = a.mn;
+    g.a_rows = a.rows;
+    g.a_cols = a.cols;
+    g.b = b.p;
+    g.ldb = b.ld;
+    g.b_mn_major = b.mn;
+    g.b_rows = b.rows;
+    g.b_cols = b.cols;
+    g.a2 = a2;
+    g.b2 = b2;
+    g.d = d;
+    g.ldd = ldd;
+    g.alpha = 1.f;
+    g.epilogue = SWARM_EPI_ACCUM_F32;
+    return run_gemm(g, st);
+}
+
 // Attention GEMM batched over z = b*H + h.  Offsets in storage coordinates:
 // token-major operands move by L rows per batch and dh columns per head;
 // [B*H*L, L] score-like operands move by H*L rows per batch and L per head.
@@ -373,26 +408,54 @@ int block_forward(swarm_stage* s, Act& A, bf16* y, const LayerW& W, cudaStream_t
 
 // --------------------------------------------------------- block backward --
 // dy: gradient w.r.t. the block output; dx: gradient w.r.t. the block input.
-int block_backward(swarm_stage* s, const Act& A, const bf16* dy, bf16* dx, const LayerW& W, cudaStream_t st) {
+// The four weight-gradient GEMMs of a block: dW += dY^T X.  mode SWARM_WGRAD_NOW:
+// this microbatch alone; DEFER: none (the dY tensors stay stashed for the next
+// visit); PAIR: K = 2T over the pending visit's stash (first) and this one's.
+struct WgradPlan {
+    int mode = SWARM_WGRAD_NOW;
+    const Act* prev = nullptr;  // the pending visit's activations of this layer
+    const Stash* ps = nullptr;  // ... and its stashed dY
+};
+
+int wgrad(swarm_stage* s, const WgradPlan& wp, int M, int N, Op dy, Op x, Op dy_prev, Op x_prev, float* out, int ldo,
+          cudaStream_t sd) {
+    const int T = s->T;
+    if (wp.mode == SWARM_WGRAD_DEFER) return SWARM_OK;
+    if (wp.mode == SWARM_WGRAD_NOW) return mm(M, N, T, dy, x, out, ldo, SWARM_EPI_ACCUM_F32, nullptr, 1.f, sd);
+    return mm2(M, N, 2 * T, dy_prev, x_prev, dy.p, x.p, out, ldo, sd);
+}
+
+int block_backward(swarm_stage* s, const Act& A, const bf16* dy, bf16* dx, const LayerW& W, cudaStream_t st,
+                   const WgradPlan& wp = WgradPlan{}, const Stash* cs = nullptr) {
     const int T = s->T, d = s->d, H = s->H, dh = s->dh, F = s->F, L = s->L, BHL = s->B * s->H * s->L;
     const bf16* p16 = s->p16;
     float* G = s->grad;
     cudaStream_t sd = side_of(s, st);  // weight gradients
+    // dY tensors the weight gradients read: per-visit workspaces, or this layer's stash
+    bf16* du = cs ? cs->du : s->du;
+    bf16* dhid = cs ? cs->dhid : s->dhid;
+    bf16* dqkv = cs ? cs->dqkv : s->dqkv;
+    const Act* PA = wp.prev;
+    const Stash* ps = wp.ps;
+    const bool pr = wp.mode == SWARM_WGRAD_PAIR;
     // MLP: du = (dy W2) * gelu'(u); dW2 += dy^T g; dc = du W1; dW1 += du^T c
     TRY(fork_side(s, st, 0));
-    TRY(mm(d, F, T, {dy, d, T, d, true}, {A.g, F, T, F, true}, G + W.w2, F, SWARM_EPI_ACCUM_F32, nullptr, 1.f, sd));
-    TRY(mm(T, F, d, {dy, d, T, d, false}, {p16 + W.w2, F, d, F, true}, s->du, F, SWARM_EPI_DGELU, A.u, 1.f, st));
+    TRY(wgrad(s, wp, d, F, {dy, d, T, d, true}, {A.g, F, T, F, true}, {pr ? ps->dy : nullptr, d, T, d, true},
+              {pr ? PA->g : nullptr, F, T, F, true}, G + W.w2, F, sd));
+    TRY(mm(T, F, d, {dy, d, T, d, false}, {p16 + W.w2, F, d, F, true}, du, F, SWARM_EPI_DGELU, A.u, 1.f, st));
     TRY(fork_side(s, st, 1));
-    TRY(mm(F, d, T, {s->du, F, T, F, true}, {A.c, d, T, d, true}, G + W.w1, d, SWARM_EPI_ACCUM_F32, nullptr, 1.f, sd));
-    TRY(mm(T, d, F, {s->du, F, T, F, false}, {p16 + W.w1, d, F, d, true}, s->dc, d, SWARM_EPI_STORE_BF16, nullptr, 1.f,
+    TRY(wgrad(s, wp, F, d, {du, F, T, F, true}, {A.c, d, T, d, true}, {pr ? ps->du : nullptr, F, T, F, true},
+              {pr ? PA->c : nullptr, d, T, d, true}, G + W.w1, d, sd));
+    TRY(mm(T, d, F, {du, F, T, F, false}, {p16 + W.w1, d, F, d, true}, s->dc, d, SWARM_EPI_STORE_BF16, nullptr, 1.f,
            st));
     // dh = LN2'(dc) + dy
-    PTRY(SWARM_PROF_LAYERNORM, st, swarm_layer_norm_backward(s->dc, A.h, SWARM_DTYPE_BF16, T, d, ln_param(s, W.ln2g), A.mu2, A.rs2, dy, s->dhid,
+    PTRY(SWARM_PROF_LAYERNORM, st, swarm_layer_norm_backward(s->dc, A.h, SWARM_DTYPE_BF16, T, d, ln_param(s, W.ln2g), A.mu2, A.rs2, dy, dhid,
                                   G + W.ln2g, G + W.ln2b, 1, s->lnws, st));
     // attention output projection
     TRY(fork_side(s, st, 2));
-    TRY(mm(d, d, T, {s->dhid, d, T, d, true}, {A.o, d, T, d, true}, G + W.wo, d, SWARM_EPI_ACCUM_F32, nullptr, 1.f, sd));
-    TRY(mm(T, d, d, {s->dhid, d, T, d, false}, {p16 + W.wo, d, d, d, true}, s->dO, d, SWARM_EPI_STORE_BF16, nullptr, 1.f,
+    TRY(wgrad(s, wp, d, d, {dhid, d, T, d, true}, {A.o, d, T, d, true}, {pr ? ps->dhid : nullptr, d, T, d, true},
+              {pr ? PA->o : nullptr, d, T, d, true}, G + W.wo, d, sd));
+    TRY(mm(T, d, d, {dhid, d, T, d, false}, {p16 + W.wo, d, d, d, true}, s->dO, d, SWARM_EPI_STORE_BF16, nullptr, 1.f,
            st));
     // dP = dO V^T ; dS = scale * P (dP - rowsum(P dP))
     const float scale = 1.f / std::sqrt(static_cast<float>(dh));
@@ -409,20 +472,21 @@ int block_backward(swarm_stage* s, const Act& A, const bf16* dy, bf16* dx, const
     // side stream beside dK, dV (three independent GEMMs of 1.7 waves each fill each other's tails)
     TRY(fork_side(s, st, 4));
     TRY(bmm(s, L, dh, L, {{s->dS, L, BHL, L, false}, H * L, L, 0, 0}, {{A.qkv + d, 3 * d, T, d, true}, L, 0, 0, dh},
-            s->dqkv, 3 * d, L, 0, 0, dh, SWARM_EPI_STORE_BF16, 1.f, side_of(s, st), 1));
+            dqkv, 3 * d, L, 0, 0, dh, SWARM_EPI_STORE_BF16, 1.f, side_of(s, st), 1));
     TRY(bmm(s, L, dh, L, {{s->dS, L, BHL, L, true}, H * L, L, 0, 0}, {{A.qkv, 3 * d, T, d, true}, L, 0, 0, dh},
-            s->dqkv + d, 3 * d, L, 0, 0, dh, SWARM_EPI_STORE_BF16, 1.f, st, 2));
+            dqkv + d, 3 * d, L, 0, 0, dh, SWARM_EPI_STORE_BF16, 1.f, st, 2));
     TRY(bmm(s, L, dh, L, {{A.P, L, BHL, L, true}, H * L, L, 0, 0}, {{s->dO, d, T, d, true}, L, 0, 0, dh},
-            s->dqkv + 2 * d, 3 * d, L, 0, 0, dh, SWARM_EPI_STORE_BF16, 1.f, st, 2));
+            dqkv + 2 * d, 3 * d, L, 0, 0, dh, SWARM_EPI_STORE_BF16, 1.f, st, 2));
     TRY(wait_side(s, st, s->ev_dq));  // dqkv complete on main (the dWqkv fork below then carries it to the side)
     // da = dqkv Wqkv ; dWqkv += dqkv^T a
     TRY(fork_side(s, st, 3));
-    TRY(mm(3 * d, d, T, {s->dqkv, 3 * d, T, 3 * d, true}, {A.a, d, T, d, true}, G + W.wqkv, d, SWARM_EPI_ACCUM_F32,
-           nullptr, 1.f, sd));
-    TRY(mm(T, d, 3 * d, {s->dqkv, 3 * d, T, 3 * d, false}, {p16 + W.wqkv, d, 3 * d, d, true}, s->da, d,
+    TRY(wgrad(s, wp, 3 * d, d, {dqkv, 3 * d, T, 3 * d, true}, {A.a, d, T, d, true},
+              {pr ? ps->dqkv : nullptr, 3 * d, T, 3 * d, true}, {pr ? PA->a : nullptr, d, T, d, true}, G + W.wqkv, d,
+              sd));
+    TRY(mm(T, d, 3 * d, {dqkv, 3 * d, T, 3 * d, false}, {p16 + W.wqkv, d, 3 * d, d, true}, s->da, d,
            SWARM_EPI_STORE_BF16, nullptr, 1.f, st));
     // dx = LN1'(da) + dh
-    PTRY(SWARM_PROF_LAYERNORM, st, swarm_layer_norm_backward(s->da, A.x, SWARM_DTYPE_BF16, T, d, ln_param(s, W.ln1g), A.mu1, A.rs1, s->dhid, dx,
+    PTRY(SWARM_PROF_LAYERNORM, st, swarm_layer_norm_backward(s->da, A.x, SWARM_DTYPE_BF16, T, d, ln_param(s, W.ln1g), A.mu1, A.rs1, dhid, dx,
                                   G + W.ln1g, G + W.ln1b, 1, s->lnws, st));
     // the next layer overwrites the workspaces the weight gradients read
     return join_side(s, st);
@@ -853,15 +917,67 @@ int swarm_stage_forward(swarm_stage_t s, int slot, const void* in, const int32_t
 }
 
 int swarm_stage_backward(swarm_stage_t s, int slot, const void* grad_in, void* grad_out, swarm_stream_t stream) {
+    return swarm_stage_backward_ex(s, slot, grad_in, grad_out, SWARM_WGRAD_NOW, 0, -1, 0, stream);
+}
+
+int swarm_stage_enable_wgrad_pairing(swarm_stage_t s) {
+    if (!s->stash[0].empty()) return SWARM_OK;
+    const size_t T = s->T, d = s->d, F = s->F;
+    for (auto& set : s->stash) {
+        set.resize(s->cfg.n_layers);
+        for (Stash& x : set) {
+            TRY(alloc(s, &x.dy, T * d));
+            TRY(alloc(s, &x.du, T * F));
+            TRY(alloc(s, &x.dhid, T * d));
+            TRY(alloc(s, &x.dqkv, 3 * T * d));
+        }
+    }
+    return SWARM_OK;
+}
+
+int swarm_stage_flush_wgrad(swarm_stage_t s, int slot, int set, swarm_stream_t stream) {
+    if (s->stash[0].empty()) return fail("flush_wgrad: pairing not enabled");
+    if (slot < 0 || slot >= static_cast<int>(s->slots.size()) || set < 0 || set > 1) return fail("flush_wgrad: bad slot/set");
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    ProfScope prof(s);
+    const int T = s->T, d = s->d, F = s->F, n = s->cfg.n_layers;
+    float* G = s->grad;
+    for (int l = 0; l < n; ++l) {
+        const Act& A = s->slots[slot].layer[l];
+        const Stash& x = s->stash[set][l];
+        const LayerW& W = weights(s, l);
+        TRY(mm(d, F, T, {x.dy, d, T, d, true}, {A.g, F, T, F, true}, G + W.w2, F, SWARM_EPI_ACCUM_F32, nullptr, 1.f, st));
+        TRY(mm(F, d, T, {x.du, F, T, F, true}, {A.c, d, T, d, true}, G + W.w1, d, SWARM_EPI_ACCUM_F32, nullptr, 1.f, st));
+        TRY(mm(d, d, T, {x.dhid, d, T, d, true}, {A.o, d, T, d, true}, G + W.wo, d, SWARM_EPI_ACCUM_F32, nullptr, 1.f, st));
+        TRY(mm(3 * d, d, T, {x.dqkv, 3 * d, T, 3 * d, true}, {A.a, d, T, d, true}, G + W.wqkv, d, SWARM_EPI_ACCUM_F32,
+               nullptr, 1.f, st));
+    }
+    return SWARM_OK;
+}
+
+int swarm_stage_backward_ex(swarm_stage_t s, int slot, const void* grad_in, void* grad_out, int wgrad_mode, int set,
+                            int prev_slot, int prev_set, swarm_stream_t stream) {
     if (slot < 0 || slot >= static_cast<int>(s->slots.size())) return fail("backward: bad slot");
+    if (wgrad_mode < SWARM_WGRAD_NOW || wgrad_mode > SWARM_WGRAD_PAIR) return fail("backward: bad wgrad mode");
+    if (wgrad_mode != SWARM_WGRAD_NOW) {
+        if (s->stash[0].empty()) return fail("backward: wgrad pairing not enabled");
+        if (set < 0 || set > 1) return fail("backward: bad stash set");
+        if (wgrad_mode == SWARM_WGRAD_PAIR &&
+            (prev_slot < 0 || prev_slot >= static_cast<int>(s->slots.size()) || prev_set < 0 || prev_set > 1 ||
+             prev_set == set || prev_slot == slot))
+            return fail("backward: pairing needs a distinct pending slot and stash set");
+    }
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     ProfScope prof(s);
     Slot& sl = s->slots[slot];
     const int T = s->T, d = s->d, n = s->cfg.n_layers;
+    const bool stashed = wgrad_mode != SWARM_WGRAD_NOW;
+    // the gradient entering the last layer: a workspace, or that layer's stash
+    bf16* g_in = stashed ? s->stash[set][n - 1].dy : s->gy[0];
     int cur = 0;
     if (s->cfg.is_last) {
         PTRY(SWARM_PROF_LAYERNORM, st, swarm_layer_norm_backward(sl.dxf, sl.out, SWARM_DTYPE_BF16, T, d, ln_param(s, s->lnfg), sl.muf, sl.rsf, nullptr,
-                                      s->gy[0], s->grad + s->lnfg, s->grad + s->lnfb, 1, s->lnws, st));
+                                      g_in, s->grad + s->lnfg, s->grad + s->lnfb, 1, s->lnws, st));
     } else {
         if (!grad_in) return fail("backward: null gradient message");
         if (s->bneck) {
@@ -870,15 +986,31 @@ int swarm_stage_backward(swarm_stage_t s, int slot, const void* grad_in, void* g
             PTRY(SWARM_PROF_OTHER, st, swarm_maxout_backward(s->wtmp, SWARM_DTYPE_BF16, sl.am, static_cast<size_t>(T) * s->wire_w,
                                       s->cfg.maxout_k, s->dc, st));
             PTRY(SWARM_PROF_LAYERNORM, st, swarm_layer_norm_backward(s->dc, sl.out, SWARM_DTYPE_BF16, T, d, ln_param(s, s->bn_out_g), sl.muc, sl.rsc,
-                                          nullptr, s->gy[0], s->grad + s->bn_out_g, s->grad + s->bn_out_b, 1, s->lnws,
+                                          nullptr, g_in, s->grad + s->bn_out_g, s->grad + s->bn_out_b, 1, s->lnws,
                                           st));
         } else {
-            PTRY(SWARM_PROF_OTHER, st, wire_decode(s, grad_in, s->gy[0], st));
+            PTRY(SWARM_PROF_OTHER, st, wire_decode(s, grad_in, g_in, st));
         }
     }
-    for (int l = n - 1; l >= 0; --l) {
-        TRY(block_backward(s, sl.layer[l], s->gy[cur], s->gy[cur ^ 1], weights(s, l), st));
-        cur ^= 1;
+    if (!stashed) {
+        for (int l = n - 1; l >= 0; --l) {
+            TRY(block_backward(s, sl.layer[l], s->gy[cur], s->gy[cur ^ 1], weights(s, l), st));
+            cur ^= 1;
+        }
+    } else {
+        // layer l's input gradient lives in stash[set][l].dy (its weight gradients read it);
+        // layer 0's output gradient goes to the workspace the tail below consumes
+        for (int l = n - 1; l >= 0; --l) {
+            WgradPlan wp;
+            wp.mode = wgrad_mode;
+            if (wgrad_mode == SWARM_WGRAD_PAIR) {
+                wp.prev = &s->slots[prev_slot].layer[l];
+                wp.ps = &s->stash[prev_set][l];
+            }
+            bf16* dx = l > 0 ? s->stash[set][l - 1].dy : s->gy[0];
+            TRY(block_backward(s, sl.layer[l], s->stash[set][l].dy, dx, weights(s, l), st, wp, &s->stash[set][l]));
+        }
+        cur = 0;
     }
     if (s->cfg.is_first) {
         ProfOp po(SWARM_PROF_OTHER, st);

@@ -115,6 +115,22 @@ class Stage:
                                            None if grad_out is None else grad_out.data_ptr(), _stream(stream))
         L.check(rc, "stage_backward")
 
+    # -- paired weight gradients ----------------------------------------------
+    WGRAD_NOW, WGRAD_DEFER, WGRAD_PAIR = 0, 1, 2
+
+    def enable_wgrad_pairing(self) -> None:
+        L.check(self.lib.swarm_stage_enable_wgrad_pairing(self.h), "stage_enable_wgrad_pairing")
+
+    def backward_ex(self, slot: int, grad_in=None, grad_out=None, *, mode: int = 0, set: int = 0, prev_slot: int = -1,
+                    prev_set: int = 0, stream=None) -> None:
+        rc = self.lib.swarm_stage_backward_ex(self.h, slot, None if grad_in is None else grad_in.data_ptr(),
+                                              None if grad_out is None else grad_out.data_ptr(), mode, set, prev_slot,
+                                              prev_set, _stream(stream))
+        L.check(rc, "stage_backward_ex")
+
+    def flush_wgrad(self, slot: int, set: int, stream=None) -> None:
+        L.check(self.lib.swarm_stage_flush_wgrad(self.h, slot, set, _stream(stream)), "stage_flush_wgrad")
+
     def optimizer_step(self, grad_scale: float = 1.0, stream=None) -> None:
         L.check(self.lib.swarm_stage_optimizer_step(self.h, grad_scale, _stream(stream)), "stage_optimizer_step")
 

@@ -218,7 +218,8 @@ class SwarmPipeline:
     def __init__(self, mcfg: ModelConfig, n_stages: int = 4, *, n_microbatches: int = 16, n_trainers: int | None = None,
                  seed: int = 0, lr: float = 1e-4, weight_decay: float = 0.0, gamma: float = 0.1, epsilon: float = 1.0,
                  modeled_flops: float = 1.0e15, profile: bool = False, use_graphs: bool = True,
-                 layout: list | None = None, max_slots: int | None = None, dpu: bool = False):
+                 layout: list | None = None, max_slots: int | None = None, dpu: bool = False,
+                 pair_wgrad: bool = True):
         self.m = mcfg
         self.S = n_stages
         self.M = n_microbatches
@@ -235,9 +236,12 @@ class SwarmPipeline:
         self.all_local = len(self.local_stages) == S and self.P == 1  # sole peer of every stage
         self.n_trainers = n_trainers or self.P
         # activation slots: a peer holds every microbatch routed to it in a step
+        # paired weight gradients (K = 2T GEMMs over two backward visits) need the
+        # deferred visit's activations intact: at one GPU, two slots used alternately
+        self.pair_wgrad = pair_wgrad
         if max_slots is None:
-            max_slots = 1 if self.all_local else (self.M if self.P == 1 or layout is not None
-                                                  else math.ceil(self.M / self.P) + 2)
+            max_slots = (2 if pair_wgrad else 1) if self.all_local else (
+                self.M if self.P == 1 or layout is not None else math.ceil(self.M / self.P) + 2)
         self.max_slots = max_slots
         self.stages: dict[int, Stage] = {s: self._new_stage(s) for s in self.local_stages}
         # CUDA graphs: a visit enqueues ~200 kernels; replaying a captured graph
@@ -272,6 +276,8 @@ class SwarmPipeline:
         # Delayed parameter updates: step t computes on
         # bank t % 2 while the all-reduce + AdamW of step t-1 run on a separate stream;
         # step t therefore sees the weights of step t-2's update (one step of delay).
+        self._pend: dict = {}      # stage -> (slot, stash set) of a visit whose weight gradients wait for a partner
+        self._wset: dict = {}     # stage -> stash set the next backward visit writes
         self.dpu = dpu
         self.t = 0
         if dpu:
@@ -289,7 +295,10 @@ class SwarmPipeline:
                           max_slots=slots or self.max_slots, wire=m.wire, block_size=m.block_size,
                           maxout_k=m.maxout_k, lr=self.lr, weight_decay=self.weight_decay,
                           seed=self.seed * 1000 + s)  # every replica of a stage starts identical
-        return Stage(cfg, self.device)
+        st = Stage(cfg, self.device)
+        if self.pair_wgrad and slots is None:
+            st.enable_wgrad_pairing()
+        return st
 
     def _build_groups(self) -> None:
         """Per-stage gradient all-reduce groups over the live members (collective:
@@ -508,23 +517,47 @@ class SwarmPipeline:
 
     def _bwd(self, s, slot, gin=None, gout=None) -> None:
         st = self.stages[s]
+        if not self.pair_wgrad:
+            key = (s, "b", slot, self._bank(), None if gin is None else gin.data_ptr(),
+                   None if gout is None else gout.data_ptr())
+            self._run(key, lambda: st.backward(slot, grad_in=gin, grad_out=gout))
+            return
+        # weight gradients of two backward visits per stage run as one K = 2T GEMM each:
+        # the first visit defers (stashing its dY), the second pairs with it
+        wset = self._wset.get(s, 0)
+        pend = self._pend.get(s)
+        mode, (pslot, pset) = (Stage.WGRAD_DEFER, (-1, 0)) if pend is None else (Stage.WGRAD_PAIR, pend)
         key = (s, "b", slot, self._bank(), None if gin is None else gin.data_ptr(),
-               None if gout is None else gout.data_ptr())
-        self._run(key, lambda: st.backward(slot, grad_in=gin, grad_out=gout))
+               None if gout is None else gout.data_ptr(), mode, wset, pslot, pset)
+        self._run(key, lambda: st.backward_ex(slot, gin, gout, mode=mode, set=wset, prev_slot=pslot, prev_set=pset))
+        self._pend[s] = (slot, wset) if pend is None else None
+        self._wset[s] = wset ^ 1
+
+    def _flush_wgrad(self) -> None:
+        """A stage's last unpaired backward visit: its weight gradients alone."""
+        for s, pend in list(self._pend.items()):
+            if pend is None:
+                continue
+            st = self.stages[s]
+            slot, wset = pend
+            self._run((s, "w", slot, self._bank(), wset), lambda: st.flush_wgrad(slot, wset))
+            self._pend[s] = None
 
     def _step_local(self, routes, tokens, targets, scale) -> None:
         # every stage lives here: run each microbatch depth-first (fwd 0..S-1,
         # bwd S-1..0) so one activation slot per stage suffices
         a, g = self.act[0], self.grd[0]
         for mb in range(self.M):
+            slot = mb % self.max_slots  # paired weight gradients: the previous microbatch's slot stays intact
             for s in range(self.S):
                 inp = tokens[mb] if s == 0 else a
                 if s == self.S - 1:
-                    self._fwd(s, 0, inp, targets=targets[mb], scale=scale)
+                    self._fwd(s, slot, inp, targets=targets[mb], scale=scale)
                 else:
-                    self._fwd(s, 0, inp, out=a)
+                    self._fwd(s, slot, inp, out=a)
             for s in reversed(range(self.S)):
-                self._bwd(s, 0, None if s == self.S - 1 else g, None if s == 0 else g)
+                self._bwd(s, slot, None if s == self.S - 1 else g, None if s == 0 else g)
+        self._flush_wgrad()
 
     def _step_pipelined(self, routes, tokens, targets, scale) -> None:
         """GPipe order over this rank's visits: all forwards by ascending
@@ -576,6 +609,7 @@ class SwarmPipeline:
                     pending.append(dist.isend(gout, dst))
         for w in pending:
             w.wait()
+        self._flush_wgrad()
 
     # ------------------------------------------------------------- metrics
     def profile_read(self):

@@ -244,3 +244,37 @@ def test_gemm_kernel_variants(cuda, env):
     r = subprocess.run([sys.executable, "-c", _VARIANT_CHECK.format(root=root)], env={**os.environ, **env},
                        capture_output=True, text=True, timeout=300)
     assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr
+
+
+@pytest.mark.parametrize("m,n,t", [(2048, 8192, 2048), (6144, 2048, 2048), (2048, 2048, 512), (256, 1024, 128),
+                                   (128, 512, 256)])
+@pytest.mark.parametrize("a_t,b_t", [(True, True), (False, False)])
+def test_gemm_two_k_segments(cuda, m, n, t, a_t, b_t):
+    """Paired weight gradients: K = 2t split over two buffer pairs (a, b) and (a2, b2)
+    equals the GEMM over the concatenation (fp32 reduce-add epilogue, as in the
+    executor), on the pair kernel and on the small-tile fallback."""
+    import torch
+    from paper_2301_11913_b200 import _lib as L, ops
+    torch.manual_seed(m + n + t)
+    k = 2 * t
+    A = torch.randn((k, m) if a_t else (m, k), device="cuda").bfloat16()
+    B = torch.randn((k, n) if b_t else (n, k), device="cuda").bfloat16()
+    # the two halves in separate allocations
+    if a_t:
+        a1, a2 = A[:t].clone(), A[t:].clone()
+    else:
+        a1, a2 = A[:, :t].contiguous(), A[:, t:].contiguous()
+    if b_t:
+        b1, b2 = B[:t].clone(), B[t:].clone()
+    else:
+        b1, b2 = B[:, :t].contiguous(), B[:, t:].contiguous()
+    acc = torch.ones(m, n, device="cuda")
+    g = L.GemmArgs()
+    g.m, g.n, g.k, g.batch, g.bh = m, n, k, 1, 1
+    g.a, g.lda, g.a_mn_major, g.a_rows, g.a_cols = a1.data_ptr(), a1.stride(0), int(a_t), a1.shape[0], a1.shape[1]
+    g.b, g.ldb, g.b_mn_major, g.b_rows, g.b_cols = b1.data_ptr(), b1.stride(0), int(b_t), b1.shape[0], b1.shape[1]
+    g.a2, g.b2 = a2.data_ptr(), b2.data_ptr()
+    g.d, g.ldd, g.alpha, g.epilogue = acc.data_ptr(), n, 1.0, L.EPI_ACCUM_F32
+    ops.gemm_raw(g)
+    ref = ref_mm(A, B, a_t, b_t) + 1
+    torch.testing.assert_close(acc, ref, rtol=1e-4, atol=1e-4 * math.sqrt(k))
