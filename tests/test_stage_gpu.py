@@ -229,3 +229,39 @@ def test_two_stage_maxout_bottleneck(cuda):
     m_ref.backward(dec(s0, grad).double().cpu())
     for name, off, r, c in s0.param_info():
         assert rel(grad_of(s0, name, r), P0[name].grad) <= GRAD_TOL_MAXOUT_UPSTREAM, name
+
+
+@pytest.mark.parametrize("shape", [dict(), dict(d_model=512, n_heads=4, d_ffn=2048, seq_len=256, micro_batch=2)])
+def test_paired_weight_gradients_match_per_microbatch(cuda, shape):
+    """Deferring a visit's weight gradients and issuing them paired with the next
+    visit's (two-segment K GEMMs), or alone via flush_wgrad, accumulates the same
+    gradients as per-visit weight gradients (fp32 summation order only)."""
+    import torch
+    from paper_2301_11913_b200.stage import Stage
+    g = torch.Generator().manual_seed(11)
+    cfgs = [tiny_cfg(**shape) for _ in range(3)]
+    tok = [torch.randint(0, cfgs[0].vocab, (cfgs[0].tokens,), generator=g).int().cuda() for _ in range(2)]
+    grads = []
+    for variant in ("now", "pair", "flush"):
+        st = Stage(tiny_cfg(**shape))
+        if variant != "now":
+            st.enable_wgrad_pairing()
+        loss = torch.zeros(1, device="cuda")
+        for slot in (0, 1):
+            st.forward(slot, tok[slot], targets=torch.roll(tok[slot], -1), loss_sum=loss, loss_scale=1e-3)
+        if variant == "now":
+            st.backward(1)
+            st.backward(0)
+        elif variant == "pair":
+            st.backward_ex(1, mode=Stage.WGRAD_DEFER, set=0)
+            st.backward_ex(0, mode=Stage.WGRAD_PAIR, set=1, prev_slot=1, prev_set=0)
+        else:
+            st.backward_ex(1, mode=Stage.WGRAD_DEFER, set=0)
+            st.flush_wgrad(1, 0)
+            st.backward_ex(0, mode=Stage.WGRAD_DEFER, set=1)
+            st.flush_wgrad(0, 1)
+        torch.cuda.synchronize()
+        grads.append(st.grads().clone())
+    scale = float(grads[0].abs().max())
+    for other in grads[1:]:
+        torch.testing.assert_close(other, grads[0], rtol=1e-4, atol=1e-5 * scale)
