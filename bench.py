@@ -545,10 +545,9 @@ def bench_train(args, world, rank, local):
     pk = peaks()
     peak = pk["bf16_tflops_sustained"] or pk["bf16_tflops"]
     achieved = gemm_flops / (gemm_ms / 1e3) / 1e12 if gemm_ms > 0 else 0.0
-    # profiled visits are 1 per (stage, direction) per step; scale to all visits of this rank
-    visits_per_stage = (M // pipe.P) if not pipe.all_local else M
-    gemm_share = (gemm_ms / args.steps) * visits_per_stage / (t0.elapsed_time(t1) / args.steps) \
-        if gemm_ms > 0 else None
+    # one profiled visit per (stage, visit kind) per step, its events weighted by the number of
+    # visits of that kind: gemm_ms is already this rank's GEMM time of whole steps
+    gemm_share = (gemm_ms / args.steps) / (t0.elapsed_time(t1) / args.steps) if gemm_ms > 0 else None
     link = measure_link(world, rank)
     cost_model = cost_model_report(mcfg, S, M, world, (ms / args.steps) / 1e3, link)
     # per-category kernel time, from one extra untimed step whose profiled visits
@@ -566,9 +565,7 @@ def bench_train(args, world, rank, local):
     pipe.step(tok, tgt)
     pipe.prof_spin_ns = 0
     pipe.profile_read()
-    breakdown = {cat: {"ms_per_step": cms * visits_per_stage,
-                       "share_of_step": cms * visits_per_stage / step_ms_rank,
-                       "calls_per_step": int(cn * visits_per_stage)}
+    breakdown = {cat: {"ms_per_step": cms, "share_of_step": cms / step_ms_rank, "profiled_calls": int(cn)}
                  for cat, (cms, cn) in pipe.last_breakdown.items()}
     model_tflops = value * mcfg.flops_per_token(S) / 1e12
     gemm_traffic = {}
@@ -593,12 +590,13 @@ def bench_train(args, world, rank, local):
                      "traffic": gemm_traffic.get("dram_bytes_per_launch"),
                      "traffic_note": gemm_traffic.get("note"), "peak_source": pk["source"] + " bf16 sustained",
                      "gemm_share_of_step": gemm_share,
-                     "note": "GEMM events bracket every GEMM of the first visit of each (stage, direction) per step "
-                             "(run eagerly); the other visits replay CUDA graphs of the same kernels",
+                     "note": "GEMM events bracket every GEMM of the first visit of each (stage, visit kind) per step "
+                             "(run eagerly), weighted by the visits of that kind per step; the other visits replay "
+                             "CUDA graphs of the same kernels",
                      "gemm_launches": gemm_n, "gemm_flops": gemm_flops, "gemm_ms": gemm_ms},
         "step_breakdown": {"note": "isolated kernel time per category on this rank (one untimed step whose first "
-                                   "visit per (stage, direction) is issued eagerly behind a GPU spin, side stream "
-                                   "folded onto the visit stream), scaled to all visits of a step; sums can exceed "
+                                   "visit per (stage, visit kind) is issued eagerly behind a GPU spin, side stream "
+                                   "folded onto the visit stream), weighted to all visits of a step; sums can exceed "
                                    "the step where the side stream overlaps; the step also holds optimizer, "
                                    "all-reduce, transport and pipeline bubbles",
                            **breakdown},

@@ -335,6 +335,10 @@ int swarm_stage_param_info(swarm_stage_t st, int index, const char** name, size_
 #define SWARM_PROF_OTHER 3      /* embedding, codec / wire, maxout, cross-entropy */
 #define SWARM_PROF_CATEGORIES 4
 void swarm_stage_profile(swarm_stage_t st, int enable);
+/* weight applied to the time / FLOPs of events recorded from now on (profile_read
+ * returns weighted sums): the number of visits of the profiled kind per step, so
+ * one profiled visit per kind stands for all of them */
+void swarm_stage_profile_weight(swarm_stage_t st, double weight);
 int swarm_stage_profile_read(swarm_stage_t st, double* gemm_ms, double* gemm_flops, uint64_t* gemm_launches);
 /* measurement utility: occupy `stream` for `ns` nanoseconds (one spinning
    thread) so the kernels issued behind it run back to back, free of host

@@ -92,6 +92,7 @@ SIGNATURES = {
     "swarm_wire_parse_header": (I, [P, C.POINTER(C.c_uint32), C.POINTER(C.c_uint32), C.POINTER(I), C.POINTER(I)]),
     "swarm_stage_profile_read": (I, [P, C.POINTER(D), C.POINTER(D), C.POINTER(C.c_uint64)]),
     "swarm_stage_profile_breakdown": (None, [P, P, P]),
+    "swarm_stage_profile_weight": (None, [P, D]),
     "swarm_gpu_spin": (I, [C.c_uint64, P]),
     "swarm_router_last_error": (C.c_char_p, []),
     "swarm_router_create": (I, [SZ, D, D, C.POINTER(P)]),

@@ -108,6 +108,8 @@ struct swarm_stage {
     std::vector<cudaEvent_t> prof_events;
     std::vector<double> prof_flops;
     std::vector<int> prof_cat;
+    std::vector<double> prof_w;  // weight of each event pair (visits of this kind per step)
+    double prof_weight = 1.0;
     size_t prof_used = 0;
     double prof_last_ms[SWARM_PROF_CATEGORIES] = {};
     uint64_t prof_last_n[SWARM_PROF_CATEGORIES] = {};
@@ -208,6 +210,7 @@ int prof_begin(int cat, cudaStream_t st) {
     cudaEventRecord(s->prof_events[2 * s->prof_used], st);
     s->prof_cat.push_back(cat);
     s->prof_flops.push_back(0.0);
+    s->prof_w.push_back(s->prof_weight);
     return SWARM_OK;
 }
 void prof_end(cudaStream_t st) {
@@ -743,6 +746,7 @@ int swarm_wire_parse_header(const void* header, uint32_t* n_elems, uint32_t* blo
 }
 
 void swarm_stage_profile(swarm_stage_t s, int enable) { s->prof_on = enable != 0; }
+void swarm_stage_profile_weight(swarm_stage_t s, double weight) { s->prof_weight = weight; }
 
 int swarm_stage_profile_read(swarm_stage_t s, double* gemm_ms, double* gemm_flops, uint64_t* gemm_launches) {
     double fl = 0.0;
@@ -752,9 +756,9 @@ int swarm_stage_profile_read(swarm_stage_t s, double* gemm_ms, double* gemm_flop
         if (cudaEventSynchronize(s->prof_events[2 * i + 1]) != cudaSuccess) return SWARM_E_CUDA;
         float e = 0.f;
         cudaEventElapsedTime(&e, s->prof_events[2 * i], s->prof_events[2 * i + 1]);
-        ms[s->prof_cat[i]] += e;
+        ms[s->prof_cat[i]] += e * s->prof_w[i];
         n[s->prof_cat[i]] += 1;
-        fl += s->prof_flops[i];
+        fl += s->prof_flops[i] * s->prof_w[i];
     }
     if (gemm_ms) *gemm_ms = ms[SWARM_PROF_GEMM];
     if (gemm_flops) *gemm_flops = fl;
@@ -766,6 +770,7 @@ int swarm_stage_profile_read(swarm_stage_t s, double* gemm_ms, double* gemm_flop
     s->prof_used = 0;
     s->prof_flops.clear();
     s->prof_cat.clear();
+    s->prof_w.clear();
     return SWARM_OK;
 }
 

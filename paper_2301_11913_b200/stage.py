@@ -193,6 +193,9 @@ class Stage:
     def profile(self, enable: bool = True) -> None:
         self.lib.swarm_stage_profile(self.h, int(enable))
 
+    def profile_weight(self, weight: float) -> None:
+        self.lib.swarm_stage_profile_weight(self.h, float(weight))
+
     def profile_read(self):
         """(gemm_ms, gemm_flops, gemm_launches) since the last read (synchronises)."""
         ms, fl, n = C.c_double(), C.c_double(), C.c_uint64()

@@ -277,6 +277,7 @@ class SwarmPipeline:
         # bank t % 2 while the all-reduce + AdamW of step t-1 run on a separate stream;
         # step t therefore sees the weights of step t-2's update (one step of delay).
         self._pend: dict = {}      # stage -> (slot, stash set) of a visit whose weight gradients wait for a partner
+        self._nvis: dict = {}      # stage -> visits per direction this step (profile weights)
         self._wset: dict = {}     # stage -> stash set the next backward visit writes
         self.dpu = dpu
         self.t = 0
@@ -476,17 +477,23 @@ class SwarmPipeline:
         return {k: v / n for k, v in out.items()}
 
     # ---------------------------------------------------------------- visits
-    def _run(self, key, fn) -> None:
+    def _run(self, key, fn, prof=None) -> None:
+        """Run a visit: eagerly the first time (warm-up) and, with `profile`, once per
+        (stage, visit kind) per step with events weighted by `prof` = (kind, visits of
+        that kind this step), so the profiled visits stand for the whole step;
+        otherwise replay its captured CUDA graph."""
         s, kind = key[0], key[1]
-        eager_prof = self.profile and (s, kind) not in self._profiled
+        pkind, weight = prof if prof is not None else (kind, 1.0)
+        eager_prof = self.profile and (s, pkind) not in self._profiled
         if eager_prof or not self.use_graphs or (s, kind) not in self._warm:
             st = self.stages[s]
             if eager_prof:
                 if self.prof_spin_ns:  # let the host run ahead: kernels queue back to back
                     L.check(L.lib().swarm_gpu_spin(int(self.prof_spin_ns), torch.cuda.current_stream().cuda_stream),
                             "gpu_spin")
+                st.profile_weight(weight)
                 st.profile(True)
-                self._profiled.add((s, kind))
+                self._profiled.add((s, pkind))
             fn()
             if eager_prof:
                 st.profile(False)  # keep the events recorded so far; stop adding
@@ -513,14 +520,14 @@ class SwarmPipeline:
         key = (s, "f", slot, self._bank(), inp.data_ptr(), None if out is None else out.data_ptr(),
                None if targets is None else targets.data_ptr())
         self._run(key, lambda: st.forward(slot, inp, out=out, targets=targets, loss_sum=self.loss_sum,
-                                          loss_scale=scale))
+                                          loss_scale=scale), prof=("f", self._nvis.get(s, 1)))
 
     def _bwd(self, s, slot, gin=None, gout=None) -> None:
         st = self.stages[s]
         if not self.pair_wgrad:
             key = (s, "b", slot, self._bank(), None if gin is None else gin.data_ptr(),
                    None if gout is None else gout.data_ptr())
-            self._run(key, lambda: st.backward(slot, grad_in=gin, grad_out=gout))
+            self._run(key, lambda: st.backward(slot, grad_in=gin, grad_out=gout), prof=("b", self._nvis.get(s, 1)))
             return
         # weight gradients of two backward visits per stage run as one K = 2T GEMM each:
         # the first visit defers (stashing its dY), the second pairs with it
@@ -529,7 +536,9 @@ class SwarmPipeline:
         mode, (pslot, pset) = (Stage.WGRAD_DEFER, (-1, 0)) if pend is None else (Stage.WGRAD_PAIR, pend)
         key = (s, "b", slot, self._bank(), None if gin is None else gin.data_ptr(),
                None if gout is None else gout.data_ptr(), mode, wset, pslot, pset)
-        self._run(key, lambda: st.backward_ex(slot, gin, gout, mode=mode, set=wset, prev_slot=pslot, prev_set=pset))
+        n = self._nvis.get(s, 1)
+        self._run(key, lambda: st.backward_ex(slot, gin, gout, mode=mode, set=wset, prev_slot=pslot, prev_set=pset),
+                  prof=(f"b{mode}", (n + 1) // 2 if mode == Stage.WGRAD_DEFER else n // 2))
         self._pend[s] = (slot, wset) if pend is None else None
         self._wset[s] = wset ^ 1
 
@@ -540,13 +549,14 @@ class SwarmPipeline:
                 continue
             st = self.stages[s]
             slot, wset = pend
-            self._run((s, "w", slot, self._bank(), wset), lambda: st.flush_wgrad(slot, wset))
+            self._run((s, "w", slot, self._bank(), wset), lambda: st.flush_wgrad(slot, wset), prof=("w", 1))
             self._pend[s] = None
 
     def _step_local(self, routes, tokens, targets, scale) -> None:
         # every stage lives here: run each microbatch depth-first (fwd 0..S-1,
         # bwd S-1..0) so one activation slot per stage suffices
         a, g = self.act[0], self.grd[0]
+        self._nvis = {s: self.M for s in range(self.S)}
         for mb in range(self.M):
             slot = mb % self.max_slots  # paired weight gradients: the previous microbatch's slot stays intact
             for s in range(self.S):
@@ -565,6 +575,7 @@ class SwarmPipeline:
         ranks therefore posts its sends and receives in the same order, and
         the visit graph is acyclic, so NCCL point-to-point cannot deadlock."""
         mine = visit_schedule(self.pl, routes, self.rank)
+        self._nvis = {s: sum(1 for _, t in mine if t == s) for s in self.local_stages}
         slot = {}
         count = {s: 0 for s in self.local_stages}
         for mb, s in mine:
