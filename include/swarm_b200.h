@@ -100,7 +100,9 @@ int swarm_layer_norm_forward(const void* x, int dtype, size_t rows, size_t cols,
                              swarm_stream_t stream);
 /* dx = LN'(dy) (+ dres when non-NULL: the residual branch's gradient, fused),
  * dgain/dbias (float, cols) written, or added when `accumulate` != 0 (gradient
- * accumulation over microbatches).  `workspace` >= swarm_layer_norm_backward_workspace()
+ * accumulation over microbatches).  Either part may be skipped: dgain = dbias =
+ * NULL computes dx only; dx = NULL (bf16 rows of width 256k <= 4096) computes the
+ * gain/bias gradients only, so they can run on another stream.  `workspace` >= swarm_layer_norm_backward_workspace()
  * bytes of device memory, zero-filled before its first use (the call leaves it zeroed
  * again; it must not be shared by concurrent calls). */
 size_t swarm_layer_norm_backward_workspace(size_t rows, size_t cols);

@@ -658,9 +658,9 @@ int ln_bwd_launch(const T* dy, const T* x, int rows, int cols, const float* g, c
     if constexpr (sizeof(T) == 2) {
         if (warp_ln_ok(cols) && al(x, 16) && al(dy, 16) && al(dx, 16) && (!dres || al(dres, 16)) && (!g || al(g, 16)) &&
             dispatch_nv(cols / 256, [&](auto nv) {
-                ln_bwd_dx_w<decltype(nv)::value>(dy, x, rows, g, mean, rstd, dres, dx, st);
+                if (dx) ln_bwd_dx_w<decltype(nv)::value>(dy, x, rows, g, mean, rstd, dres, dx, st);
             })) {
-            SWARM_LAUNCH_CHECK("k_ln_bwd_dx_w");
+            if (dx) SWARM_LAUNCH_CHECK("k_ln_bwd_dx_w");
             if (dg || db) {
                 const int splits = std::max(1, std::min(ln_bwd_parts(rows), (rows + 63) / 64));
                 const int rps = (rows + splits - 1) / splits;
@@ -675,6 +675,7 @@ int ln_bwd_launch(const T* dy, const T* x, int rows, int cols, const float* g, c
             return SWARM_OK;
         }
     }
+    if (!dx) return invalid("layer_norm backward: dx may be omitted only for bf16 rows of width 256k <= 4096");
     const int parts = ln_bwd_parts(rows);
     const int rpc = (rows + parts - 1) / parts;
     const int grid = (rows + rpc - 1) / rpc;

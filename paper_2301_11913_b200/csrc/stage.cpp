@@ -99,7 +99,7 @@ struct swarm_stage {
     // fill the SMs the data-gradient chain leaves idle (GEMM wave tails)
     cudaStream_t side = nullptr;
     void* skws[2] = {nullptr, nullptr};  // GEMM stream-K scratch: visit stream, side stream
-    cudaEvent_t ev_fork[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
+    cudaEvent_t ev_fork[7] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
     cudaEvent_t ev_join = nullptr;
     cudaEvent_t ev_dq = nullptr;  // dQ (side stream) complete
     // visit profiling (bench.py's live roofline and step breakdown): event pairs
@@ -451,9 +451,13 @@ int block_backward(swarm_stage* s, const Act& A, const bf16* dy, bf16* dx, const
               {pr ? PA->c : nullptr, d, T, d, true}, G + W.w1, d, sd));
     TRY(mm(T, d, F, {du, F, T, F, false}, {p16 + W.w1, d, F, d, true}, s->dc, d, SWARM_EPI_STORE_BF16, nullptr, 1.f,
            st));
-    // dh = LN2'(dc) + dy
+    // dh = LN2'(dc) + dy on the visit stream; LN2's gain / bias gradients (a second pass
+    // over dc and h, off the critical path) on the side stream
     PTRY(SWARM_PROF_LAYERNORM, st, swarm_layer_norm_backward(s->dc, A.h, SWARM_DTYPE_BF16, T, d, ln_param(s, W.ln2g), A.mu2, A.rs2, dy, dhid,
-                                  G + W.ln2g, G + W.ln2b, 1, s->lnws, st));
+                                  nullptr, nullptr, 1, s->lnws, st));
+    TRY(fork_side(s, st, 5));
+    PTRY(SWARM_PROF_LAYERNORM, sd, swarm_layer_norm_backward(s->dc, A.h, SWARM_DTYPE_BF16, T, d, ln_param(s, W.ln2g), A.mu2, A.rs2, nullptr, nullptr,
+                                  G + W.ln2g, G + W.ln2b, 1, s->lnws, sd));
     // attention output projection
     TRY(fork_side(s, st, 2));
     TRY(wgrad(s, wp, d, d, {dhid, d, T, d, true}, {A.o, d, T, d, true}, {pr ? ps->dhid : nullptr, d, T, d, true},
@@ -488,9 +492,12 @@ int block_backward(swarm_stage* s, const Act& A, const bf16* dy, bf16* dx, const
               sd));
     TRY(mm(T, d, 3 * d, {dqkv, 3 * d, T, 3 * d, false}, {p16 + W.wqkv, d, 3 * d, d, true}, s->da, d,
            SWARM_EPI_STORE_BF16, nullptr, 1.f, st));
-    // dx = LN1'(da) + dh
+    // dx = LN1'(da) + dh; LN1's gain / bias gradients on the side stream
     PTRY(SWARM_PROF_LAYERNORM, st, swarm_layer_norm_backward(s->da, A.x, SWARM_DTYPE_BF16, T, d, ln_param(s, W.ln1g), A.mu1, A.rs1, dhid, dx,
-                                  G + W.ln1g, G + W.ln1b, 1, s->lnws, st));
+                                  nullptr, nullptr, 1, s->lnws, st));
+    TRY(fork_side(s, st, 6));
+    PTRY(SWARM_PROF_LAYERNORM, sd, swarm_layer_norm_backward(s->da, A.x, SWARM_DTYPE_BF16, T, d, ln_param(s, W.ln1g), A.mu1, A.rs1, nullptr, nullptr,
+                                  G + W.ln1g, G + W.ln1b, 1, s->lnws, sd));
     // the next layer overwrites the workspaces the weight gradients read
     return join_side(s, st);
 }
