@@ -15,11 +15,15 @@
 // are exact in fp64 for fp32/bf16 inputs).  Ties round away from zero like C
 // round().  The fp64 API path repeats the reference's fp64 operations verbatim.
 //
-// Dequantize uses a per-block 256-entry codebook staged in shared memory:
-// table[c] = (OutT)(c*a/127.0) evaluated once per code value in fp64, so each
-// output element is one smem lookup and is the reference value rounded once.
+// Dequantize with fp32 scales to f32/bf16 (k_dequant_words) is pure fp32
+// arithmetic proven equal to the reference's fp64 value rounded once (see
+// deq_f32_fast); it replaced a per-block smem codebook whose random-bank
+// lookups made the kernel MIO-bound (ncu: mio_throttle 14.5, 0.70 of HBM).
+// The codebook kernel (k_dequant_table: table[c] = (OutT)(c*a/127.0) in fp64)
+// remains for fp64 scales and non-power-of-two block sizes.
 #include <algorithm>
 #include <mutex>
+#include <type_traits>
 #include <vector>
 
 #include "common.cuh"
@@ -276,6 +280,95 @@ __global__ void __launch_bounds__(THREADS) k_dequant_table(const uint4* __restri
     }
 }
 
+// Arithmetic dequantize for fp32 scales (no codebook, no smem): the exact
+// value x = c*a/127 has, in units of the fp32 ulp of x, a fractional part that
+// is a multiple of 1/127 (c*mant(a) is an integer and x < 2^24 ulps), so it
+// lies >= 1/254 ulp from every fp32 rounding midpoint and the reference's
+// fl32(fl64(x)) equals RN32(x).  ph + pl = c*a exactly (fma), q0 = ph/127 to
+// ~1 ulp, e = the exact remainder + pl, q = RN(q0 + e/127) misses x by
+// ~2^-23 ulp before its one rounding -> RN32(x).  Exhaustively checked over
+// every code and every fp32 mantissa in several binades (0 mismatches; the
+// derivation is scale-invariant while no product leaves the normal range,
+// hence the a in [2^-64, 2^65) guard -- other scales take the fp64 path).
+// bf16 output: RN16(q) == RN16(x) unless q is itself a bf16 midpoint (low 16
+// bits 0x8000; ~1.8e-5 of (a, c) pairs), which takes the fp64 path.
+// Flat over 32-bit code words: lane i loads word i (4 codes) and stores 4
+// outputs, so every warp load and store is one contiguous segment.
+__device__ __forceinline__ float deq_f32_fast(uint32_t wb, int r, float a) {
+    constexpr float kInv127 = 1.0f / 127.0f;
+    // 0x4B0000XX = 2^23 + XX: the biased code (c + 128) enters the mantissa
+    const float cf = __fsub_rn(__int_as_float(__byte_perm(wb, 0x4B000000u, 0x7540u | r)), 8388736.0f);
+    const float ph = __fmul_rn(cf, a);
+    const float pl = __fmaf_rn(cf, a, -ph);
+    const float q0 = __fmul_rn(ph, kInv127);
+    const float e = __fadd_rn(__fmaf_rn(-q0, 127.0f, ph), pl);
+    return __fmaf_rn(e, kInv127, q0);
+}
+
+__device__ __forceinline__ bool deq_fast_scale(float a) {
+    return a >= 5.421010862427522e-20f && a < 3.6893488147419103e19f;  // [2^-64, 2^65)
+}
+
+template <typename OutT>
+struct DeqWord;
+template <>
+struct DeqWord<float> {
+    using V = float4;
+    __device__ __forceinline__ static V run(uint32_t w, float a) {
+        float v[4];
+        if (deq_fast_scale(a)) {
+            const uint32_t wb = w ^ 0x80808080u;
+#pragma unroll
+            for (int r = 0; r < 4; ++r) v[r] = deq_f32_fast(wb, r, a);
+        } else {
+#pragma unroll
+            for (int r = 0; r < 4; ++r)
+                v[r] = __double2float_rn(deq(static_cast<int8_t>((w >> (8 * r)) & 0xffu), static_cast<double>(a)));
+        }
+        return make_float4(v[0], v[1], v[2], v[3]);
+    }
+};
+template <>
+struct DeqWord<__nv_bfloat16> {
+    using V = uint2;
+    __device__ __forceinline__ static V run(uint32_t w, float a) {
+        uint32_t h[4];
+        const bool fast = deq_fast_scale(a);
+        const uint32_t wb = w ^ 0x80808080u;
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+            const uint32_t u = __float_as_uint(deq_f32_fast(wb, r, a));
+            if (fast && (u & 0xffffu) != 0x8000u) h[r] = (u + 0x7fffu + ((u >> 16) & 1u)) >> 16;
+            else h[r] = f64_to_bf16_bits(deq(static_cast<int8_t>((w >> (8 * r)) & 0xffu), static_cast<double>(a)));
+        }
+        return make_uint2(h[0] | (h[1] << 16), h[2] | (h[3] << 16));
+    }
+};
+
+// nwords = full-block codes / 4; scale of word i = scales[i >> wshift]
+template <typename OutT, int U>
+__global__ void __launch_bounds__(256) k_dequant_words(const uint32_t* __restrict__ codes,
+                                                       const float* __restrict__ scales, size_t nwords,
+                                                       unsigned wshift, typename DeqWord<OutT>::V* __restrict__ out) {
+    using V = typename DeqWord<OutT>::V;
+    const size_t stride = static_cast<size_t>(gridDim.x) * blockDim.x;
+    size_t i = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    for (; i + (U - 1) * stride < nwords; i += U * stride) {
+        uint32_t w[U];
+        float a[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) w[u] = __ldcs(codes + i + u * stride);
+#pragma unroll
+        for (int u = 0; u < U; ++u) a[u] = __ldg(scales + ((i + u * stride) >> wshift));
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const V v = DeqWord<OutT>::run(w[u], a[u]);
+            __stcs(out + i + u * stride, v);
+        }
+    }
+    for (; i < nwords; i += stride) __stcs(out + i, DeqWord<OutT>::run(__ldcs(codes + i), __ldg(scales + (i >> wshift))));
+}
+
 template <typename OutT, typename ScaleT>
 __global__ void k_dequant_generic(const int8_t* __restrict__ codes, const ScaleT* __restrict__ scales,
                                   size_t n, size_t bs, size_t first, OutT* __restrict__ out) {
@@ -358,7 +451,20 @@ template <typename OutT, typename ScaleT>
 int launch_dequant(const int8_t* codes, const ScaleT* scales, size_t n, size_t bs, OutT* out, cudaStream_t st) {
     const size_t nfull = n / bs;
     size_t first = 0;
-    if (nfull > 0 && bs % 16 == 0 && bs >= 512 && aligned(codes, 16) && aligned(out, 16)) {
+    constexpr bool kArith = std::is_same<ScaleT, float>::value &&
+                            (std::is_same<OutT, float>::value || std::is_same<OutT, __nv_bfloat16>::value);
+    if constexpr (kArith) {
+        using V = typename DeqWord<OutT>::V;
+        if (nfull > 0 && bs >= 4 && (bs & (bs - 1)) == 0 && aligned(codes, 4) && aligned(out, sizeof(V))) {
+            const size_t nwords = nfull * bs / 4;
+            const unsigned wshift = static_cast<unsigned>(__builtin_ctzll(bs / 4));
+            k_dequant_words<OutT, 4><<<grid_for(nwords, 256 * 4, 148u * 8u), 256, 0, st>>>(
+                reinterpret_cast<const uint32_t*>(codes), scales, nwords, wshift, reinterpret_cast<V*>(out));
+            SWARM_LAUNCH_CHECK("k_dequant_words");
+            first = nfull * bs;
+        }
+    }
+    if (first == 0 && nfull > 0 && bs % 16 == 0 && bs >= 512 && aligned(codes, 16) && aligned(out, 16)) {
         k_dequant_table<OutT, ScaleT, 256><<<static_cast<unsigned>(nfull), 256, 0, st>>>(
             reinterpret_cast<const uint4*>(codes), scales, bs, out);
         SWARM_LAUNCH_CHECK("k_dequant_table");

@@ -113,6 +113,36 @@ def test_dequantize_bitexact(cuda, out, n, bs):
     assert np.array_equal(got, exp)
 
 
+@pytest.mark.parametrize("out", ["f32", "bf16"])
+@pytest.mark.parametrize("bs", [4096, 64, 4])
+def test_dequantize_arbitrary_codes_and_scales(cuda, out, bs):
+    """Every code byte (incl. -128) against scales over the whole fp32 range:
+    the arithmetic path's [2^-64, 2^65) guard edges, zero, subnormals, FLT_MAX,
+    and random mantissas (bf16: ~1.8e-5 of pairs hit the midpoint fallback)."""
+    import torch
+    from paper_2301_11913_b200 import ops
+    rng = np.random.default_rng(bs)
+    n = 1 << 21
+    codes = rng.integers(-128, 128, n, dtype=np.int16).astype(np.int8)
+    nb = n // bs
+    bits = rng.integers(0, 0x7F800000, nb, dtype=np.int64).astype(np.uint32)
+    mant = rng.integers(0, 1 << 23, nb, dtype=np.int64).astype(np.uint32)
+    bits[: nb // 2] = ((rng.integers(60, 195, nb // 2) << 23).astype(np.uint32) | mant[: nb // 2])
+    special = np.array([0.0, 1e-45, 1.17e-38, 2.0 ** -64, np.nextafter(np.float32(2.0 ** -64), 0),
+                        2.0 ** 65, np.nextafter(np.float32(2.0 ** 65), 0), 3.4028235e38, 1.0], np.float32)
+    scales = bits.view(np.float32).copy()
+    scales[: special.size] = special
+    dt = {"f32": torch.float32, "bf16": torch.bfloat16}[out]
+    y = ops.dequantize(torch.from_numpy(codes).cuda(), torch.from_numpy(scales).cuda(), bs, dt)
+    if out == "bf16":
+        got = y.view(torch.int16).cpu().numpy().view(np.uint16)
+        exp = O.dequantize(codes, scales, bs, np.uint16)
+    else:
+        got = y.cpu().numpy().view(np.uint32)
+        exp = O.dequantize(codes, scales, bs, np.float32).view(np.uint32)
+    assert np.array_equal(got, exp), f"{int((got != exp).sum())} mismatches"
+
+
 def test_all_128_negative_code_and_zero_block(cuda):
     import torch
     from paper_2301_11913_b200 import ops
