@@ -370,6 +370,47 @@ int swarm_router_peer_state(swarm_router_t r, uint64_t peer, double* ema, double
 int swarm_rebalance_decide(size_t n_stages, const size_t* offsets, const uint64_t* peers, const double* queues,
                            uint64_t* mover, size_t* from_stage, size_t* to_stage, size_t* op_count);
 
+/* ---- engine-driven executor schedule ----------------------
+ * The reference's discrete-event engine (P/src/sim.cpp:199-761: Engine::run,
+ * start_service :395-403, dispatch_current :405-436, on_stage_complete
+ * :472-491, advance_trainer :493-510, AllReduceTick :245-250) restated for a
+ * static population, with the real executor attached where the reference
+ * advances simulated time.  Records come out in event-processing order; every
+ * rank running the same engine on the same seed sees the same sequence.
+ * Workers are SimConfig::initial_peers flattened stage by stage (PeerId ==
+ * index, as Engine::add_worker assigns them). */
+#define SWARM_ENG_START 0      /* worker begins the visit (trainer, stage, backward); time..end_time modeled */
+#define SWARM_ENG_HOP 1        /* trainer's input dispatched to `worker`'s queue; from_worker produced it (-1: new microbatch) */
+#define SWARM_ENG_DONE 2       /* trainer's microbatch finished (backward at stage 0 on `worker`) */
+#define SWARM_ENG_ALLREDUCE 3  /* stage-wide all-reduce tick; starts stall until end_time */
+typedef struct {
+    double time;
+    double end_time;
+    int32_t kind;
+    int32_t backward;
+    uint32_t trainer;
+    uint32_t stage;
+    int64_t worker;
+    int64_t from_worker;
+    uint64_t microbatch; /* the trainer's microbatch counter */
+} swarm_engine_record;
+typedef struct swarm_engine* swarm_engine_t;
+const char* swarm_engine_last_error(void);
+/* SimConfig fields: n_stages, initial_peers (worker_stage/worker_speed, speed may be NULL = 1.0),
+ * forward_service_seconds, backward_multiplier, trainers_per_peer, allreduce_period/_stall,
+ * duration_seconds, bucket_seconds; seed = sim::run's seed.  Errors: SWARM_E_INVALID (ConfigError). */
+int swarm_engine_create(size_t n_stages, size_t n_workers, const size_t* worker_stage, const double* worker_speed,
+                        double forward_seconds, double backward_multiplier, size_t trainers_per_peer,
+                        double allreduce_period, double allreduce_stall, double duration_seconds,
+                        double bucket_seconds, uint64_t seed, swarm_engine_t* out);
+void swarm_engine_destroy(swarm_engine_t e);
+size_t swarm_engine_n_trainers(swarm_engine_t e);
+/* up to `cap` next records (n = 0: the run reached duration_seconds) */
+int swarm_engine_next(swarm_engine_t e, swarm_engine_record* records, size_t cap, size_t* n);
+/* SimResult::dispatched / completed / throughput.completed (per bucket) so far */
+int swarm_engine_summary(swarm_engine_t e, uint64_t* dispatched, uint64_t* completed, double* buckets,
+                         size_t n_buckets, double* now);
+
 #ifdef __cplusplus
 }
 #endif

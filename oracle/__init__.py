@@ -94,6 +94,8 @@ def _load_ref():
     lib.ref_oracle_throughput.restype = C.c_double
     lib.ref_stage_cost.argtypes = [P, C.c_double, P, C.c_int, P]
     lib.ref_stage_cost.restype = C.c_int
+    lib.ref_sim_run.argtypes = [C.c_char_p, C.c_uint64, P, P, P, sz, P]
+    lib.ref_sim_run.restype = C.c_int
     return lib
 
 

@@ -136,3 +136,26 @@ extern "C" int ref_stage_cost(const int64_t* shape6, double act_bytes, const dou
         return 1;
     }
 }
+
+// The reference's discrete-event engine, unmodified (P/src/sim.cpp:811-830):
+// SimConfig from the reference's own JSON schema (SimConfig::from_json,
+// sim.cpp:920-992), one sim::run(config, seed).  Used by tests/test_engine.py to
+// pin the B200 executor schedule (csrc/engine.cpp) decision-for-decision.
+// Returns 0 ok, 1 ConfigError/ParseError, 3 other; buckets gets up to n_buckets.
+#include <string>
+extern "C" int ref_sim_run(const char* json, uint64_t seed, uint64_t* dispatched, uint64_t* completed,
+                           double* buckets, size_t n_buckets, size_t* n_buckets_out) {
+    try {
+        const auto cfg = swarmsim::sim::SimConfig::from_json(std::string(json));
+        const auto r = swarmsim::sim::run(cfg, seed);
+        *dispatched = r.dispatched;
+        *completed = r.completed;
+        *n_buckets_out = r.throughput.completed.size();
+        for (size_t i = 0; i < n_buckets && i < r.throughput.completed.size(); ++i) buckets[i] = r.throughput.completed[i];
+        return 0;
+    } catch (const swarmsim::ConfigError&) {
+        return 1;
+    } catch (const std::exception&) {
+        return 3;
+    }
+}

@@ -37,6 +37,14 @@ class StageConfigC(C.Structure):
                [("seed", C.c_uint64)]
 
 
+class EngineRecord(C.Structure):
+    _fields_ = [("time", C.c_double), ("end_time", C.c_double), ("kind", C.c_int32), ("backward", C.c_int32),
+                ("trainer", C.c_uint32), ("stage", C.c_uint32), ("worker", C.c_int64), ("from_worker", C.c_int64),
+                ("microbatch", C.c_uint64)]
+
+
+ENG_START, ENG_HOP, ENG_DONE, ENG_ALLREDUCE = range(4)
+
 # (name, restype, argtypes) for every symbol include/swarm_b200.h declares
 P, SZ, I, U32P, U8P, F, D = C.c_void_p, C.c_size_t, C.c_int, C.c_void_p, C.c_void_p, C.c_float, C.c_double
 SIGNATURES = {
@@ -105,6 +113,12 @@ SIGNATURES = {
     "swarm_router_record_response": (I, [P, C.c_uint64, D]),
     "swarm_router_peer_state": (I, [P, C.c_uint64, C.POINTER(D), C.POINTER(D)]),
     "swarm_rebalance_decide": (I, [SZ, P, P, P, C.POINTER(C.c_uint64), C.POINTER(SZ), C.POINTER(SZ), C.POINTER(SZ)]),
+    "swarm_engine_last_error": (C.c_char_p, []),
+    "swarm_engine_create": (I, [SZ, SZ, P, P, D, D, SZ, D, D, D, D, C.c_uint64, C.POINTER(P)]),
+    "swarm_engine_destroy": (None, [P]),
+    "swarm_engine_n_trainers": (SZ, [P]),
+    "swarm_engine_next": (I, [P, C.POINTER(EngineRecord), SZ, C.POINTER(SZ)]),
+    "swarm_engine_summary": (I, [P, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64), P, SZ, C.POINTER(D)]),
 }
 
 _lib = None
