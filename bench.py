@@ -612,6 +612,74 @@ def bench_train(args, world, rank, local):
     return line
 
 
+# ----------------------------------------------------------------- engine
+def bench_engine(args, world, rank, local):
+    """asynchronous SWARM training driven by the reference's event
+    engine (csrc/engine.cpp, decision-identical to sim::run): trainers keep one
+    microbatch each in flight, peers serve FIFO queues, stage peers all-reduce +
+    AdamW at every AllReduceTick.  A "step" = M microbatch completions (the same
+    65,536 tokens as the train workload); the tick period is sized so a stage serves
+    ~M microbatches between ticks."""
+    import torch
+
+    from paper_2301_11913_b200.executor import EngineExecutor
+    from paper_2301_11913_b200.swarm import Placement
+    dev = torch.device("cuda", local)
+    torch.cuda.set_device(dev)
+    mcfg = model_config(args)
+    S, M = args.stages, args.microbatches
+    P = Placement(world, S).P
+    bm = 2.0
+    ex = EngineExecutor(mcfg, S, trainers_per_peer=args.trainers_per_peer, seed=1, lr=1e-4, forward_seconds=1.0,
+                        backward_multiplier=bm, allreduce_period=M * (1.0 + bm) / P, allreduce_stall=0.05)
+    stream = torch.cuda.current_stream()
+    ex.run(M * args.warmup)
+    ex.finish()
+    torch.cuda.synchronize()
+    ex.loss_sum.zero_()
+    clk = ClockSampler(local)
+    clk.start()
+    time.sleep(0.3)
+    barrier(world)
+    torch.cuda.synchronize()
+    n0 = ex.kernels_launched()
+    v0, r0, t_0 = ex.engine.summary()["now"], ex.records, ex.optimizer_steps
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    t0.record(stream)
+    done = ex.run(M * args.steps)
+    ex.finish()
+    t1.record(stream)
+    torch.cuda.synchronize()
+    barrier(world)
+    clocks = clk.stop()
+    ms = max_over_ranks(t0.elapsed_time(t1), world)
+    tokens = done * mcfg.tokens
+    value = tokens / (ms / 1e3)
+    loss = ex.loss_sum.clone()
+    if world > 1:
+        import torch.distributed as dist
+        dist.all_reduce(loss)
+    line = {
+        "metric": "training tokens/s (SWARM pipeline, engine-driven asynchronous)", "value": value,
+        "unit": "tokens/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+        "dtype": "bf16", "data": "synthetic tokens uniform over the vocab (per-trainer pool), random-init weights",
+        "config": {**train_config(args), "parallelism": (f"{S} stages x {P} peer(s) per stage" if world >= S else
+                                                         f"{world} GPU(s) x {S // world} stage(s) each"),
+                   "trainers": ex.T, "trainers_per_peer": args.trainers_per_peer,
+                   "schedule": "reference DES engine (static population), forward 1.0 / backward 2.0 virtual s, "
+                               f"AllReduceTick every {M * (1.0 + bm) / P:g} virtual s",
+                   "mean_loss": float(loss.item()) / max(tokens, 1),
+                   "model_tflops_per_s": value * mcfg.flops_per_token(S) / 1e12,
+                   "l2": "per-step working set far exceeds L2; no flush needed"},
+        "engine": {"records": ex.records - r0, "virtual_seconds": ex.engine.summary()["now"] - v0,
+                   "optimizer_steps_rank": ex.optimizer_steps - t_0, "microbatches": done},
+        "gpu_launches": int(ex.kernels_launched() - n0), "clocks": clocks,
+    }
+    return line
+
+
 # ----------------------------------------------------------------- failure
 def bench_failure(args, world, rank, local):
     """BASELINE configs[4]: peer failure + adaptive
@@ -732,7 +800,8 @@ def main():
     ap.add_argument("--steps", type=int, default=None)
     ap.add_argument("--warmup", type=int, default=None)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="train", choices=["train", "codec", "failure"])
+    ap.add_argument("--workload", default="train", choices=["train", "codec", "failure", "engine"])
+    ap.add_argument("--trainers-per-peer", type=int, default=2, help="engine: trainers per peer (sim trainers_per_peer)")
     ap.add_argument("--model", default="C", choices=["C", "D", "tiny"])
     ap.add_argument("--microbatches", type=int, default=TRAIN_MICROBATCHES)
     ap.add_argument("--micro-batch", type=int, default=None, help="sequences per microbatch (default: the preset's)")
@@ -743,9 +812,9 @@ def main():
     ap.add_argument("--no-codec", action="store_true", help="train: skip the codec sub-measurement")
     args = ap.parse_args()
     if args.steps is None:
-        args.steps = {"train": 6, "failure": 3}.get(args.workload, 1000)
+        args.steps = {"train": 6, "failure": 3, "engine": 6}.get(args.workload, 1000)
     if args.warmup is None:
-        args.warmup = {"train": 3, "failure": 3}.get(args.workload, 10)
+        args.warmup = {"train": 3, "failure": 3, "engine": 3}.get(args.workload, 10)
     args.warmup = max(args.warmup, 3)
     world, rank, local = dist_setup(args)
     if args.impl == "reference":
@@ -754,6 +823,8 @@ def main():
         line = bench_codec(args, world, rank, local)
     elif args.workload == "failure":
         line = bench_failure(args, world, rank, local)
+    elif args.workload == "engine":
+        line = bench_engine(args, world, rank, local)
     else:
         line = bench_train(args, world, rank, local)
         if not args.no_codec:

@@ -26,6 +26,7 @@
 #include <cmath>
 #include <cstdint>
 #include <deque>
+#include <limits>
 #include <queue>
 #include <random>
 #include <string>
@@ -94,6 +95,7 @@ struct swarm_engine {
     std::priority_queue<Event, std::vector<Event>, EventLater> events;
     uint64_t next_seq = 0;
     double now = 0.0, stall_until = 0.0;
+    double tick_next = std::numeric_limits<double>::infinity();  // next AllReduceTick (infinite: none)
     uint64_t dispatched = 0, completed = 0;
     std::vector<double> buckets;
     std::deque<swarm_engine_record> out;
@@ -216,12 +218,24 @@ struct swarm_engine {
     // process events until `want` records are buffered or the run ends
     int pump(size_t want) {
         while (!finished && out.size() < want) {
-            if (events.empty()) {
+            // all-reduce ticks are generated lazily: the reference pushes them all up
+            // front (sim.cpp:245-250), but a tick only ever ties another event on time,
+            // where the kind decides, so its sequence number never matters
+            const bool tick = tick_next < duration &&
+                              (events.empty() || tick_next < events.top().time ||
+                               (tick_next == events.top().time && kAllReduceTick < events.top().kind));
+            if (!tick && events.empty()) {
                 finished = true;
                 break;
             }
-            const Event ev = events.top();
-            events.pop();
+            Event ev{};
+            if (tick) {
+                ev = Event{tick_next, kAllReduceTick, 0, 0, 0};
+                tick_next += ar_period;
+            } else {
+                ev = events.top();
+                events.pop();
+            }
             if (ev.time > duration) {  // sim.cpp:262
                 finished = true;
                 break;
@@ -303,8 +317,7 @@ int swarm_engine_create(size_t n_stages, size_t n_workers, const size_t* worker_
         }
     }
     // Engine::run (sim.cpp:235-259): all-reduce ticks, then staggered trainer starts
-    if (allreduce_period > 0.0 && allreduce_stall > 0.0)
-        for (double t = allreduce_period; t < duration_seconds; t += allreduce_period) e->push(t, kAllReduceTick, 0, 0);
+    if (allreduce_period > 0.0 && allreduce_stall > 0.0) e->tick_next = allreduce_period;
     const double stagger = static_cast<double>(n_stages) * (1.0 + backward_multiplier) * forward_seconds;
     for (size_t i = 0; i < e->trainers.size(); ++i) e->push(e->uniform01() * stagger, kTrainerStart, i, 0);
     *out = e;

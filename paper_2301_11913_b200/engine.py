@@ -68,9 +68,12 @@ class Engine:
         self._buf = (_lib.EngineRecord * 1024)()
 
     def __del__(self):
-        if getattr(self, "h", None):
-            _lib.lib().swarm_engine_destroy(self.h)
-            self.h = None
+        try:
+            if getattr(self, "h", None):
+                _lib.lib().swarm_engine_destroy(self.h)
+                self.h = None
+        except Exception:  # interpreter shutdown
+            pass
 
     def next(self, cap: int = 1024) -> list:
         """Up to `cap` next records ([] once the run reached duration_seconds)."""

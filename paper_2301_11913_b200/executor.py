@@ -1,0 +1,317 @@
+"""Engine-driven executor: the reference's discrete-event
+engine decides, the GPUs execute.
+
+The reference advances simulated time where a peer would run a stage visit
+(`Engine::start_service` / `on_stage_complete`, P/src/sim.cpp:395-403,472-491),
+moves a trainer to the next peer in `dispatch_current` (:405-436) and stalls
+every stage at an `AllReduceTick` (:245-250).  Here every rank runs the same
+C++ engine (csrc/engine.cpp, decision-identical to sim::run) and attaches real
+work at exactly those points, in the engine's record order:
+
+* START  -> the serving peer's rank runs the stage visit (forward or backward)
+            on its compute stream (CUDA-graph replay per (peer, kind, trainer));
+* HOP    -> the trainer's wire message (int8 codes ‖ fp32 scales ‖ header)
+            moves from the producing peer to the chosen peer: NCCL isend after
+            the producing visit, irecv on a receive stream that only waits for the
+            previous reader of that buffer; the consuming visit waits for it;
+* ALLREDUCE -> each stage's peers all-reduce their fp32 gradient arena and take
+            an AdamW step over the microbatches their stage served since the
+            last tick (SWARM's asynchronous accumulate-then-average);
+* DONE   -> a microbatch finished (loss already accumulated on the last stage).
+
+This is asynchronous SWARM training: no per-step barrier, trainers keep their
+microbatches moving, peers serve queued visits in FIFO order.  Every
+dependency points to an earlier record, and every rank issues its halves of a
+point-to-point transfer at the same record, so NCCL cannot deadlock.
+
+Buffers: activation slot = trainer id on every peer (a trainer has at most
+one microbatch in flight); wire messages per (trainer, boundary, direction).
+"""
+from __future__ import annotations
+
+import torch
+import torch.distributed as dist
+
+from . import _lib as L
+from .engine import ALLREDUCE, DONE, HOP, START, Engine, EngineConfig
+from .stage import Stage, StageConfig
+from .swarm import ModelConfig, Placement
+
+
+def wire_key(S: int, t: int, stage: int, backward: bool):
+    """The wire message the visit (t, stage, backward) reads, or None: ("a", t, b)
+    crosses boundary b forward (stage b -> b+1), ("g", t, b) backward."""
+    if backward:
+        return None if stage == S - 1 else ("g", t, stage)
+    return None if stage == 0 else ("a", t, stage - 1)
+
+
+def hop_action(pl: Placement, S: int, r, rank: int):
+    """What `rank` does at HOP record r: ("send", dst_rank, key), ("recv",
+    src_rank, key) or None (new microbatch, turnaround, same-rank hop, or not
+    involved)."""
+    src, dst = r.from_worker, r.worker
+    if src < 0 or src == dst:
+        return None
+    rs, rd = pl.rank_of_peer(src), pl.rank_of_peer(dst)
+    if rs == rd:
+        return None
+    key = wire_key(S, r.trainer, r.stage, bool(r.backward))
+    if rs == rank:
+        return ("send", rd, key)
+    if rd == rank:
+        return ("recv", rs, key)
+    return None
+
+
+class EngineExecutor:
+    def __init__(self, mcfg: ModelConfig, n_stages: int = 4, *, trainers_per_peer: int = 1, seed: int = 0,
+                 lr: float = 1e-4, weight_decay: float = 0.0, forward_seconds: float = 1.0,
+                 backward_multiplier: float = 2.0, allreduce_period: float = 0.0, allreduce_stall: float = 0.0,
+                 duration_seconds: float = 1e9, use_graphs: bool = True, n_pool: int = 16,
+                 tokens: torch.Tensor | None = None, targets: torch.Tensor | None = None):
+        self.m = mcfg
+        self.S = n_stages
+        self.seed = seed
+        self.world = dist.get_world_size() if dist.is_initialized() else 1
+        self.rank = dist.get_rank() if dist.is_initialized() else 0
+        self.device = torch.device("cuda", torch.cuda.current_device())
+        self.pl = Placement(self.world, n_stages)
+        S = n_stages
+        self.ecfg = EngineConfig(n_stages=S, initial_peers=[[1.0] * self.pl.layout[s] for s in range(S)],
+                                 forward_service_seconds=forward_seconds, backward_multiplier=backward_multiplier,
+                                 trainers_per_peer=trainers_per_peer, allreduce_period=allreduce_period,
+                                 allreduce_stall=allreduce_stall, duration_seconds=duration_seconds,
+                                 bucket_seconds=max(duration_seconds / 64, 1e-9))
+        self.engine = Engine(self.ecfg, seed)
+        self.T = self.engine.n_trainers
+        self.local = [pid for pid in range(len(self.pl.stage_of)) if self.pl.rank_of_peer(pid) == self.rank]
+        self.stages: dict[int, Stage] = {}
+        for pid in self.local:
+            s = self.pl.stage_of_peer(pid)
+            cfg = StageConfig(d_model=mcfg.d_model, n_heads=mcfg.n_heads, d_ffn=mcfg.d_ffn, seq_len=mcfg.seq_len,
+                              micro_batch=mcfg.micro_batch, n_layers=mcfg.layers_per_stage,
+                              shared_layers=mcfg.shared_layers, vocab=mcfg.vocab, is_first=int(s == 0),
+                              is_last=int(s == S - 1), causal=mcfg.causal, max_slots=self.T, wire=mcfg.wire,
+                              block_size=mcfg.block_size, maxout_k=mcfg.maxout_k, lr=lr,
+                              weight_decay=weight_decay, seed=seed * 1000 + s)  # stage replicas start identical
+            self.stages[pid] = Stage(cfg, self.device)
+        wb = next(iter(self.stages.values())).wire_bytes if self.stages else Stage(
+            StageConfig(d_model=mcfg.d_model, n_heads=mcfg.n_heads, d_ffn=mcfg.d_ffn, seq_len=mcfg.seq_len,
+                        micro_batch=mcfg.micro_batch, n_layers=1, vocab=mcfg.vocab, wire=mcfg.wire,
+                        block_size=mcfg.block_size, maxout_k=mcfg.maxout_k), self.device).wire_bytes
+        self.wire_bytes = wb
+        # wire messages: act[t][b] crosses boundary b (stage b -> b+1), grd[t][b] the other way
+        self.act = [[torch.empty(wb, dtype=torch.uint8, device=self.device) for _ in range(S - 1)]
+                    for _ in range(self.T)]
+        self.grd = [[torch.empty(wb, dtype=torch.uint8, device=self.device) for _ in range(S - 1)]
+                    for _ in range(self.T)]
+        # synthetic data pool (identical on every rank); microbatch (t, k) uses pool[(t * 7 + k) % n_pool]
+        if tokens is None:
+            g = torch.Generator(device="cpu").manual_seed(seed + 17)
+            tokens = torch.randint(0, mcfg.vocab, (n_pool, mcfg.tokens), generator=g, dtype=torch.int32)
+            targets = torch.roll(tokens, -1, dims=1)
+        self.pool_tok, self.pool_tgt = tokens.to(self.device), targets.to(self.device)
+        self.tok = [torch.empty(mcfg.tokens, dtype=torch.int32, device=self.device) for _ in range(self.T)]
+        self.tgt = [torch.empty(mcfg.tokens, dtype=torch.int32, device=self.device) for _ in range(self.T)]
+        self.loss_sum = torch.zeros(1, dtype=torch.float32, device=self.device)
+        self.recv_stream = torch.cuda.Stream(device=self.device)
+        self._recv: dict = {}      # buffer key -> pending irecv work (the consumer waits on it)
+        self._send: dict = {}      # buffer key -> pending isend work (the next writer waits on it)
+        self._read: dict = {}      # buffer key -> event after the last local reader
+        self.groups: dict = {}
+        if self.world >= S and dist.is_initialized():
+            for s in range(S):
+                members = self.pl.members(s)
+                g = dist.new_group(members) if len(members) > 1 else None
+                if g is not None and self.rank in members:
+                    self.groups[s] = g
+        self.served = [0] * S      # backward visits per stage since the last tick (global count)
+        self.bwd_log = [[] for _ in range(S)]  # (trainer, microbatch) of every backward visit, per stage
+        self.visit_log = []                     # (trainer, microbatch, stage, backward, peer) of every visit
+        self.use_graphs = use_graphs
+        self.graphs: dict = {}
+        self.graph_kernels: dict = {}
+        self._warm: set = set()
+        self.captured_kernels = 0
+        self.replayed_kernels = 0
+        self.completed = 0          # microbatches finished (global, from the schedule)
+        self.visits_local = 0
+        self.ticks = 0
+        self.optimizer_steps = 0
+        self.records = 0
+
+    # ------------------------------------------------------------ helpers
+    def _pool_index(self, t: int, k: int) -> int:
+        return (t * 7 + k) % self.pool_tok.shape[0]
+
+    def _buf(self, t: int, stage: int, backward: bool):
+        return wire_key(self.S, t, stage, backward)
+
+    def _tensor(self, key):
+        kind, t, b = key
+        return (self.act if kind == "a" else self.grd)[t][b]
+
+    def _replay(self, key, fn) -> None:
+        if not self.use_graphs or key not in self._warm:
+            fn()
+            self._warm.add(key)
+            return
+        g = self.graphs.get(key)
+        if g is None:
+            n0 = L.lib().swarm_launch_count()
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                fn()
+            n = L.lib().swarm_launch_count() - n0
+            self.graph_kernels[key] = n
+            self.captured_kernels += n
+            self.graphs[key] = g
+        g.replay()
+        self.replayed_kernels += self.graph_kernels[key]
+
+    # ------------------------------------------------------------ records
+    def _start(self, r) -> None:
+        s, t, pid, bwd = r.stage, r.trainer, r.worker, bool(r.backward)
+        if bwd:
+            self.served[s] += 1
+            self.bwd_log[s].append((t, int(r.microbatch)))
+        self.visit_log.append((t, int(r.microbatch), s, bwd, pid))
+        if pid not in self.stages:
+            return
+        st = self.stages[pid]
+        cur = torch.cuda.current_stream()
+        inkey = self._buf(t, s, bwd)
+        if inkey is not None and inkey in self._recv:
+            self._recv.pop(inkey).wait()  # compute stream waits for the transfer
+        outkey = None
+        if bwd and s > 0:
+            outkey = ("g", t, s - 1)
+        elif not bwd and s < self.S - 1:
+            outkey = ("a", t, s)
+        if outkey is not None and outkey in self._send:
+            self._send.pop(outkey).wait()  # the previous message from this buffer has left
+        if not bwd:
+            if s == 0:
+                k = self._pool_index(t, r.microbatch)
+                self.tok[t].copy_(self.pool_tok[k], non_blocking=True)
+            if s == self.S - 1:
+                k = self._pool_index(t, r.microbatch)
+                self.tgt[t].copy_(self.pool_tgt[k], non_blocking=True)
+            inp = self.tok[t] if s == 0 else self._tensor(inkey)
+            out = None if outkey is None else self._tensor(outkey)
+            tg = self.tgt[t] if s == self.S - 1 else None
+            scale = 1.0 / self.m.tokens
+            self._replay((pid, "f", t), lambda: st.forward(t, inp, out=out, targets=tg, loss_sum=self.loss_sum,
+                                                           loss_scale=scale))
+        else:
+            gin = None if inkey is None else self._tensor(inkey)
+            gout = None if outkey is None else self._tensor(outkey)
+            self._replay((pid, "b", t), lambda: st.backward(t, grad_in=gin, grad_out=gout))
+        if inkey is not None:
+            ev = torch.cuda.Event()
+            ev.record(cur)
+            self._read[inkey] = ev
+        self.visits_local += 1
+
+    def _hop(self, r) -> None:
+        # same-rank hops need nothing: the consumer reads the producer's buffer in stream order
+        act = hop_action(self.pl, self.S, r, self.rank)
+        if act is None:
+            return
+        op, peer, key = act
+        if op == "send":
+            self._send[key] = dist.isend(self._tensor(key), peer)  # NCCL stream waits for the producing visit
+        else:
+            with torch.cuda.stream(self.recv_stream):
+                ev = self._read.pop(key, None)
+                if ev is not None:
+                    self.recv_stream.wait_event(ev)  # the previous reader of this buffer is done
+                self._recv[key] = dist.irecv(self._tensor(key), peer)
+
+    def _allreduce(self, r) -> None:
+        self.ticks += 1
+        for pid, st in self.stages.items():
+            s = self.pl.stage_of_peer(pid)
+            n = self.served[s]
+            if n == 0:
+                continue
+            if s in self.groups:
+                dist.all_reduce(st.grads(), op=dist.ReduceOp.SUM, group=self.groups[s])
+            st.optimizer_step(grad_scale=1.0 / n)  # mean over the stage's microbatches since the last tick
+            self.optimizer_steps += 1
+        self.served = [0] * self.S
+
+    def run(self, n_microbatches: int) -> int:
+        """Process engine records until `n_microbatches` more microbatches have
+        completed (or the engine's duration ends).  Returns the number completed."""
+        target = self.completed + n_microbatches
+        while self.completed < target:
+            batch = self.engine.next(1)
+            if not batch:
+                break
+            r = batch[0]
+            self.records += 1
+            if r.kind == START:
+                self._start(r)
+            elif r.kind == HOP:
+                self._hop(r)
+            elif r.kind == ALLREDUCE:
+                self._allreduce(r)
+            elif r.kind == DONE:
+                self.completed += 1
+        return self.completed - (target - n_microbatches)
+
+    def finish(self) -> None:
+        """Wait for outstanding transfers (end of a timed region)."""
+        for w in list(self._send.values()) + list(self._recv.values()):
+            w.wait()
+        self._send.clear()
+        self._recv.clear()
+
+    def kernels_launched(self) -> int:
+        return L.lib().swarm_launch_count() - self.captured_kernels + self.replayed_kernels
+
+
+def sequential_reference_grads(ex: EngineExecutor) -> dict:
+    """Verification helper: every peer's gradient over exactly the visits the
+    schedule ran on it, recomputed sequentially on fresh replicas (same seeds,
+    one slot, no optimizer step), one microbatch at a time along its route.
+    The last stage's forward also accumulates the LM-head gradient, so every
+    microbatch that reached the last stage counts there even if its backward
+    had not started.  Returns {peer: fp32 gradient arena}.  Valid while no
+    ALLREDUCE tick changed the weights."""
+    S, m = ex.S, ex.m
+    ref = {}
+    for pid in range(len(ex.pl.stage_of)):
+        s = ex.pl.stage_of_peer(pid)
+        cfg = StageConfig(d_model=m.d_model, n_heads=m.n_heads, d_ffn=m.d_ffn, seq_len=m.seq_len,
+                          micro_batch=m.micro_batch, n_layers=m.layers_per_stage, shared_layers=m.shared_layers,
+                          vocab=m.vocab, is_first=int(s == 0), is_last=int(s == S - 1), causal=m.causal,
+                          max_slots=1, wire=m.wire, block_size=m.block_size, maxout_k=m.maxout_k,
+                          seed=ex.seed * 1000 + s)
+        ref[pid] = Stage(cfg, ex.device)
+    fwd, bwd, order = {}, {}, []
+    for t, k, s, b, pid in ex.visit_log:
+        (bwd if b else fwd).setdefault((t, k), {})[s] = pid
+        if not b and s == S - 1:
+            order.append((t, k))
+    any_st = next(iter(ref.values()))
+    a = [any_st.new_wire() for _ in range(max(S - 1, 1))]
+    g = [any_st.new_wire() for _ in range(max(S - 1, 1))]
+    loss = torch.zeros(1, dtype=torch.float32, device=ex.device)
+    for t, k in order:
+        idx = ex._pool_index(t, k)
+        route = fwd[(t, k)]
+        for s in range(S):
+            st = ref[route[s]]
+            inp = ex.pool_tok[idx] if s == 0 else a[s - 1]
+            if s == S - 1:
+                st.forward(0, inp, targets=ex.pool_tgt[idx], loss_sum=loss, loss_scale=1.0 / m.tokens)
+            else:
+                st.forward(0, inp, out=a[s])
+        for s in sorted(bwd.get((t, k), {}), reverse=True):
+            assert bwd[(t, k)][s] == route[s]  # backward retraces the forward route
+            ref[route[s]].backward(0, grad_in=None if s == S - 1 else g[s], grad_out=None if s == 0 else g[s - 1])
+    torch.cuda.synchronize()
+    return {pid: st.grads().clone() for pid, st in ref.items()}
