@@ -284,7 +284,7 @@ def bench_codec(args, world, rank, local):
         "roofline": {"bound": "hbm", "kernel": "k_quant_f32<256,4> (K1 quantize)", "achieved": q_gbs,
                      "peak": pk["hbm_gbs"], "unit": "GB/s", "frac": q_gbs / pk["hbm_gbs"], "traffic": traffic,
                      "peak_source": pk["source"], "bytes_per_launch": CODEC_BYTES_Q, "launch_ms": q_ms,
-                     "dequant": {"kernel": "k_dequant_words (K2)", "achieved": dq_gbs, "frac": dq_gbs / pk["hbm_gbs"],
+                     "dequant": {"kernel": "k_dequant_blocks (K2)", "achieved": dq_gbs, "frac": dq_gbs / pk["hbm_gbs"],
                                  "launch_ms": dq_ms}},
         "e2e": {"value": e2e_val, "unit": "GB/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                 "path": "swarm_quantize_blockwise_host + swarm_dequantize_blockwise_host, pinned host buffers"},

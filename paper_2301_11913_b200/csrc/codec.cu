@@ -15,9 +15,9 @@
 // are exact in fp64 for fp32/bf16 inputs).  Ties round away from zero like C
 // round().  The fp64 API path repeats the reference's fp64 operations verbatim.
 //
-// Dequantize with fp32 scales to f32/bf16 (k_dequant_words) is pure fp32
-// arithmetic proven equal to the reference's fp64 value rounded once (see
-// deq_f32_fast); it replaced a per-block smem codebook whose random-bank
+// Dequantize with fp32 scales to f32/bf16 (k_dequant_blocks / _words) is pure
+// fp32 arithmetic proven equal to the reference's fp64 value rounded once (see
+// DeqSplit); it replaced a per-block smem codebook whose random-bank
 // lookups made the kernel MIO-bound (ncu: mio_throttle 14.5, 0.70 of HBM).
 // The codebook kernel (k_dequant_table: table[c] = (OutT)(c*a/127.0) in fp64)
 // remains for fp64 scales and non-power-of-two block sizes.
@@ -284,42 +284,42 @@ __global__ void __launch_bounds__(THREADS) k_dequant_table(const uint4* __restri
 // value x = c*a/127 has, in units of the fp32 ulp of x, a fractional part that
 // is a multiple of 1/127 (c*mant(a) is an integer and x < 2^24 ulps), so it
 // lies >= 1/254 ulp from every fp32 rounding midpoint and the reference's
-// fl32(fl64(x)) equals RN32(x).  ph + pl = c*a exactly (fma), q0 = ph/127 to
-// ~1 ulp, e = the exact remainder + pl, q = RN(q0 + e/127) misses x by
-// ~2^-23 ulp before its one rounding -> RN32(x).  Exhaustively checked over
-// every code and every fp32 mantissa in several binades (0 mismatches; the
-// derivation is scale-invariant while no product leaves the normal range,
-// hence the a in [2^-64, 2^65) guard -- other scales take the fp64 path).
-// bf16 output: RN16(q) == RN16(x) unless q is itself a bf16 midpoint (low 16
-// bits 0x8000; ~1.8e-5 of (a, c) pairs), which takes the fp64 path.
-// Flat over 32-bit code words: lane i loads word i (4 codes) and stores 4
-// outputs, so every warp load and store is one contiguous segment.
-__device__ __forceinline__ float deq_f32_fast(uint32_t wb, int r, float a) {
-    constexpr float kInv127 = 1.0f / 127.0f;
-    // 0x4B0000XX = 2^23 + XX: the biased code (c + 128) enters the mantissa
-    const float cf = __fsub_rn(__int_as_float(__byte_perm(wb, 0x4B000000u, 0x7540u | r)), 8388736.0f);
-    const float ph = __fmul_rn(cf, a);
-    const float pl = __fmaf_rn(cf, a, -ph);
-    const float q0 = __fmul_rn(ph, kInv127);
-    const float e = __fadd_rn(__fmaf_rn(-q0, 127.0f, ph), pl);
-    return __fmaf_rn(e, kInv127, q0);
-}
-
-__device__ __forceinline__ bool deq_fast_scale(float a) {
-    return a >= 5.421010862427522e-20f && a < 3.6893488147419103e19f;  // [2^-64, 2^65)
-}
+// fl32(fl64(x)) equals RN32(x).  Per block a/127 is split as A1 + A2 (A1 =
+// a*(1/127), A2 = (a - 127*A1)*(1/127) from the exact fma remainder), so
+// c*A1 + c*A2 misses x by ~2^-40 ulp and q = fma(c, A1, c*A2) -- one
+// rounding -- is RN32(x).  Exhaustively checked over every code and every fp32
+// mantissa in several binades (scripts/deq_exhaustive.c, 0 mismatches); the
+// derivation is scale-invariant while nothing leaves the normal range, hence the
+// a in [2^-64, 2^65) guard -- other scales take the fp64 path.  bf16 output:
+// RN16(q) == RN16(x) unless q is itself a bf16 midpoint (low 16 bits 0x8000;
+// ~1.8e-5 of (a, c) pairs), which takes the fp64 path.
+struct DeqSplit {
+    float a1, a2;
+    bool fast;
+    __device__ __forceinline__ explicit DeqSplit(float a) {
+        constexpr float kInv127 = 1.0f / 127.0f;
+        fast = a >= 5.421010862427522e-20f && a < 3.6893488147419103e19f;  // [2^-64, 2^65)
+        a1 = __fmul_rn(a, kInv127);
+        a2 = __fmul_rn(__fmaf_rn(-a1, 127.0f, a), kInv127);
+    }
+    // byte r of the biased word (codes ^ 0x80808080): 0x4B0000XX = 2^23 + (c + 128)
+    __device__ __forceinline__ float operator()(uint32_t wb, int r) const {
+        const float cf = __fsub_rn(__int_as_float(__byte_perm(wb, 0x4B000000u, 0x7540u | r)), 8388736.0f);
+        return __fmaf_rn(cf, a1, __fmul_rn(cf, a2));
+    }
+};
 
 template <typename OutT>
 struct DeqWord;
 template <>
 struct DeqWord<float> {
     using V = float4;
-    __device__ __forceinline__ static V run(uint32_t w, float a) {
+    __device__ __forceinline__ static V run(uint32_t w, const DeqSplit& d, float a) {
         float v[4];
-        if (deq_fast_scale(a)) {
+        if (d.fast) {
             const uint32_t wb = w ^ 0x80808080u;
 #pragma unroll
-            for (int r = 0; r < 4; ++r) v[r] = deq_f32_fast(wb, r, a);
+            for (int r = 0; r < 4; ++r) v[r] = d(wb, r);
         } else {
 #pragma unroll
             for (int r = 0; r < 4; ++r)
@@ -331,21 +331,41 @@ struct DeqWord<float> {
 template <>
 struct DeqWord<__nv_bfloat16> {
     using V = uint2;
-    __device__ __forceinline__ static V run(uint32_t w, float a) {
+    __device__ __forceinline__ static V run(uint32_t w, const DeqSplit& d, float a) {
         uint32_t h[4];
-        const bool fast = deq_fast_scale(a);
         const uint32_t wb = w ^ 0x80808080u;
 #pragma unroll
         for (int r = 0; r < 4; ++r) {
-            const uint32_t u = __float_as_uint(deq_f32_fast(wb, r, a));
-            if (fast && (u & 0xffffu) != 0x8000u) h[r] = (u + 0x7fffu + ((u >> 16) & 1u)) >> 16;
+            const uint32_t u = __float_as_uint(d(wb, r));
+            if (d.fast && (u & 0xffffu) != 0x8000u) h[r] = (u + 0x7fffu + ((u >> 16) & 1u)) >> 16;
             else h[r] = f64_to_bf16_bits(deq(static_cast<int8_t>((w >> (8 * r)) & 0xffu), static_cast<double>(a)));
         }
         return make_uint2(h[0] | (h[1] << 16), h[2] | (h[3] << 16));
     }
 };
 
-// nwords = full-block codes / 4; scale of word i = scales[i >> wshift]
+// block sizes 1024 * WPT: one CTA per block; every thread loads its WPT code
+// words (lane-contiguous, 512 B per warp load) before any math, splits the
+// block's scale once, and stores 16-B (f32) / 8-B (bf16) vectors
+template <typename OutT, int WPT>
+__global__ void __launch_bounds__(256) k_dequant_blocks(const uint32_t* __restrict__ codes,
+                                                        const float* __restrict__ scales, size_t nblocks,
+                                                        typename DeqWord<OutT>::V* __restrict__ out) {
+    using V = typename DeqWord<OutT>::V;
+    constexpr int WPB = 256 * WPT;
+    for (size_t b = blockIdx.x; b < nblocks; b += gridDim.x) {  // one pass per CTA unless grid.x is capped
+        uint32_t w[WPT];
+#pragma unroll
+        for (int k = 0; k < WPT; ++k) w[k] = __ldcs(codes + b * WPB + threadIdx.x + k * 256);
+        const float a = __ldg(scales + b);
+        const DeqSplit d(a);
+        V* ob = out + b * WPB + threadIdx.x;
+#pragma unroll
+        for (int k = 0; k < WPT; ++k) __stcs(ob + k * 256, DeqWord<OutT>::run(w[k], d, a));
+    }
+}
+
+// any power-of-two block size: flat over 32-bit words, scale of word i = scales[i >> wshift]
 template <typename OutT, int U>
 __global__ void __launch_bounds__(256) k_dequant_words(const uint32_t* __restrict__ codes,
                                                        const float* __restrict__ scales, size_t nwords,
@@ -361,12 +381,12 @@ __global__ void __launch_bounds__(256) k_dequant_words(const uint32_t* __restric
 #pragma unroll
         for (int u = 0; u < U; ++u) a[u] = __ldg(scales + ((i + u * stride) >> wshift));
 #pragma unroll
-        for (int u = 0; u < U; ++u) {
-            const V v = DeqWord<OutT>::run(w[u], a[u]);
-            __stcs(out + i + u * stride, v);
-        }
+        for (int u = 0; u < U; ++u) __stcs(out + i + u * stride, DeqWord<OutT>::run(w[u], DeqSplit(a[u]), a[u]));
     }
-    for (; i < nwords; i += stride) __stcs(out + i, DeqWord<OutT>::run(__ldcs(codes + i), __ldg(scales + (i >> wshift))));
+    for (; i < nwords; i += stride) {
+        const float a = __ldg(scales + (i >> wshift));
+        __stcs(out + i, DeqWord<OutT>::run(__ldcs(codes + i), DeqSplit(a), a));
+    }
 }
 
 template <typename OutT, typename ScaleT>
@@ -456,11 +476,22 @@ int launch_dequant(const int8_t* codes, const ScaleT* scales, size_t n, size_t b
     if constexpr (kArith) {
         using V = typename DeqWord<OutT>::V;
         if (nfull > 0 && bs >= 4 && (bs & (bs - 1)) == 0 && aligned(codes, 4) && aligned(out, sizeof(V))) {
-            const size_t nwords = nfull * bs / 4;
-            const unsigned wshift = static_cast<unsigned>(__builtin_ctzll(bs / 4));
-            k_dequant_words<OutT, 4><<<grid_for(nwords, 256 * 4, 148u * 8u), 256, 0, st>>>(
-                reinterpret_cast<const uint32_t*>(codes), scales, nwords, wshift, reinterpret_cast<V*>(out));
-            SWARM_LAUNCH_CHECK("k_dequant_words");
+            const auto* c32 = reinterpret_cast<const uint32_t*>(codes);
+            auto* ov = reinterpret_cast<V*>(out);
+            // one CTA per block: measured 6.68 TB/s vs 5.29 for persistent CTAs walking
+            // blocks (1 GiB f32; the hardware CTA scheduler balances the write stream better)
+            const unsigned g = grid_for(nfull, 1, 0x7fffffffu);
+            if (bs == 4096) k_dequant_blocks<OutT, 4><<<g, 256, 0, st>>>(c32, scales, nfull, ov);
+            else if (bs == 2048) k_dequant_blocks<OutT, 2><<<g, 256, 0, st>>>(c32, scales, nfull, ov);
+            else if (bs == 8192) k_dequant_blocks<OutT, 8><<<g, 256, 0, st>>>(c32, scales, nfull, ov);
+            else if (bs == 1024) k_dequant_blocks<OutT, 1><<<g, 256, 0, st>>>(c32, scales, nfull, ov);
+            else {
+                const size_t nwords = nfull * bs / 4;
+                const unsigned wshift = static_cast<unsigned>(__builtin_ctzll(bs / 4));
+                k_dequant_words<OutT, 4><<<grid_for(nwords, 256 * 4, 0x7fffffffu), 256, 0, st>>>(c32, scales, nwords,
+                                                                                                 wshift, ov);
+            }
+            SWARM_LAUNCH_CHECK("k_dequant_blocks/words");
             first = nfull * bs;
         }
     }
