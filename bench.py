@@ -810,6 +810,7 @@ def main():
     ap.add_argument("--stages", type=int, default=TRAIN_STAGES, help="pipeline stages (default 4, SURVEY §8(d))")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-codec", action="store_true", help="train: skip the codec sub-measurement")
+    ap.add_argument("--no-engine", action="store_true", help="train: skip the engine-driven asynchronous sub-measurement")
     args = ap.parse_args()
     if args.steps is None:
         args.steps = {"train": 6, "failure": 3, "engine": 6}.get(args.workload, 1000)
@@ -827,6 +828,19 @@ def main():
         line = bench_engine(args, world, rank, local)
     else:
         line = bench_train(args, world, rank, local)
+        if not args.no_engine:
+            import gc
+
+            import torch
+            gc.collect()
+            torch.cuda.empty_cache()
+            e = bench_engine(argparse.Namespace(**{**vars(args), "steps": 3, "warmup": 2}), world, rank, local)
+            line["engine_async"] = {k: e[k] for k in ("metric", "value", "unit", "ms_per_step", "steps", "engine",
+                                                      "gpu_launches")}
+            line["engine_async"]["note"] = ("SURVEY §8(f)1: the same configs[2] model trained asynchronously in the "
+                                            "reference DES engine's record order (bench.py --workload engine)")
+            gc.collect()
+            torch.cuda.empty_cache()
         if not args.no_codec:
             c = bench_codec(argparse.Namespace(steps=200, warmup=5, no_cpu_baseline=True, e2e_steps=0), world, rank,
                             local)
