@@ -4,9 +4,13 @@
 Workloads (BASELINE.json):
   train  (default) configs[2]: 4 stages x P peers, 8 layers/stage, d_model 2048,
          16 heads, seq 512, microbatch 4, bf16, int8 boundary codec, stochastic
-         wiring + per-stage all-reduce; one step = one optimizer step over 32
-         microbatches (65,536 tokens).  metric: training tokens/s.  1 GPU hosts
+         wiring + per-stage all-reduce.  metric: training tokens/s.  1 GPU hosts
          all 4 stages; 2 GPUs 2 stages each; 4 GPUs 4x1; 8 GPUs 4x2.
+         Headline: asynchronous SWARM in the reference DES engine's record order
+         (--workload engine; one step = 32 microbatch completions = 65,536 tokens,
+         stage all-reduce + AdamW every ~32 microbatches per stage); the
+         synchronous GPipe step (one optimizer step over 32 microbatches; --sync
+         makes it the headline) is measured first and reported as "gpipe_sync".
          The global batch is fixed, so "scaling" is "strong".
   codec  configs[1]: blockwise int8 codec on 1 GiB fp32 tensors, block 4096;
          one step = quantize (K1) + dequantize (K2) of the whole tensor, i.e. one
@@ -623,7 +627,7 @@ def bench_engine(args, world, rank, local):
     import torch
 
     from paper_2301_11913_b200.executor import EngineExecutor
-    from paper_2301_11913_b200.swarm import Placement
+    from paper_2301_11913_b200.swarm import Placement  # noqa: F811
     dev = torch.device("cuda", local)
     torch.cuda.set_device(dev)
     mcfg = model_config(args)
@@ -631,7 +635,8 @@ def bench_engine(args, world, rank, local):
     P = Placement(world, S).P
     bm = 2.0
     ex = EngineExecutor(mcfg, S, trainers_per_peer=args.trainers_per_peer, seed=1, lr=1e-4, forward_seconds=1.0,
-                        backward_multiplier=bm, allreduce_period=M * (1.0 + bm) / P, allreduce_stall=0.05)
+                        backward_multiplier=bm, allreduce_period=M * (1.0 + bm) / P, allreduce_stall=0.05,
+                        stream_per_peer=not args.single_stream)
     stream = torch.cuda.current_stream()
     ex.run(M * args.warmup)
     ex.finish()
@@ -647,6 +652,7 @@ def bench_engine(args, world, rank, local):
     t0 = torch.cuda.Event(enable_timing=True)
     t1 = torch.cuda.Event(enable_timing=True)
     t0.record(stream)
+    ex.fork()
     done = ex.run(M * args.steps)
     ex.finish()
     t1.record(stream)
@@ -660,21 +666,53 @@ def bench_engine(args, world, rank, local):
     if world > 1:
         import torch.distributed as dist
         dist.all_reduce(loss)
+    # e2e: every microbatch's tokens / targets H2D from pinned host memory inside the
+    # visit that consumes them, the loss D2H after every step's M completions
+    e2e_steps = max(1, min(args.steps, 3))
+    ex.use_host_pool(True)
+    hloss = torch.empty(1, dtype=torch.float32).pin_memory()
+    lst = ex.last_stage_stream()
+    ex.run(M)  # untimed: warm the host-pool path
+    ex.finish()
+    barrier(world)
+    torch.cuda.synchronize()
+    w0 = time.perf_counter()
+    e2e_done = 0
+    for _ in range(e2e_steps):
+        e2e_done += ex.run(M)
+        if lst is not None:
+            with torch.cuda.stream(lst):
+                hloss.copy_(ex.loss_sum, non_blocking=True)
+    ex.finish()
+    torch.cuda.synchronize()
+    e2e_s = max_over_ranks(time.perf_counter() - w0, world)
+    ex.use_host_pool(False)
+    P_ = Placement(world, S)
     line = {
-        "metric": "training tokens/s (SWARM pipeline, engine-driven asynchronous)", "value": value,
+        "metric": "training tokens/s (SWARM pipeline)", "value": value,
         "unit": "tokens/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
         "dtype": "bf16", "data": "synthetic tokens uniform over the vocab (per-trainer pool), random-init weights",
-        "config": {**train_config(args), "parallelism": (f"{S} stages x {P} peer(s) per stage" if world >= S else
+        "config": {**train_config(args), "parallelism": (f"{S} stages x {P_.P} peer(s) per stage" if world >= S else
                                                          f"{world} GPU(s) x {S // world} stage(s) each"),
+                   "execution": "asynchronous SWARM: the reference DES engine's record order (csrc/engine.cpp, "
+                                "decision-identical to sim::run), one compute stream per peer, NCCL isend/irecv "
+                                "of int8 wire messages, stage all-reduce + AdamW at every AllReduceTick",
                    "trainers": ex.T, "trainers_per_peer": args.trainers_per_peer,
-                   "schedule": "reference DES engine (static population), forward 1.0 / backward 2.0 virtual s, "
-                               f"AllReduceTick every {M * (1.0 + bm) / P:g} virtual s",
+                   "schedule": "forward 1.0 / backward 2.0 virtual s, AllReduceTick every "
+                               f"{M * (1.0 + bm) / P:g} virtual s (~{M} microbatches per stage); one step = {M} "
+                               "microbatch completions",
+                   "optimizer": "AdamW (fused, fp32 master), paired weight gradients",
                    "mean_loss": float(loss.item()) / max(tokens, 1),
                    "model_tflops_per_s": value * mcfg.flops_per_token(S) / 1e12,
                    "l2": "per-step working set far exceeds L2; no flush needed"},
         "engine": {"records": ex.records - r0, "virtual_seconds": ex.engine.summary()["now"] - v0,
                    "optimizer_steps_rank": ex.optimizer_steps - t_0, "microbatches": done},
+        "e2e": {"value": e2e_done * mcfg.tokens / e2e_s, "unit": "tokens/s",
+                "h2d_bytes_per_step": int(M * mcfg.tokens * 4 * 2),
+                "d2h_bytes_per_step": 4, "path": "EngineExecutor.run with each microbatch's tokens / targets copied "
+                                                 "from pinned host memory by its consuming visit and the loss read "
+                                                 "back after every step (wall clock, max over ranks)"},
         "gpu_launches": int(ex.kernels_launched() - n0), "clocks": clocks,
     }
     return line
@@ -802,6 +840,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="train", choices=["train", "codec", "failure", "engine"])
     ap.add_argument("--trainers-per-peer", type=int, default=2, help="engine: trainers per peer (sim trainers_per_peer)")
+    ap.add_argument("--single-stream", action="store_true", help="engine: one compute stream per GPU (not per peer)")
     ap.add_argument("--model", default="C", choices=["C", "D", "tiny"])
     ap.add_argument("--microbatches", type=int, default=TRAIN_MICROBATCHES)
     ap.add_argument("--micro-batch", type=int, default=None, help="sequences per microbatch (default: the preset's)")
@@ -810,7 +849,9 @@ def main():
     ap.add_argument("--stages", type=int, default=TRAIN_STAGES, help="pipeline stages (default 4, SURVEY §8(d))")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-codec", action="store_true", help="train: skip the codec sub-measurement")
-    ap.add_argument("--no-engine", action="store_true", help="train: skip the engine-driven asynchronous sub-measurement")
+    ap.add_argument("--sync", action="store_true",
+                    help="train: headline = the synchronous GPipe step (default: the asynchronous engine-driven "
+                         "pipeline, with the GPipe step reported beside it)")
     args = ap.parse_args()
     if args.steps is None:
         args.steps = {"train": 6, "failure": 3, "engine": 6}.get(args.workload, 1000)
@@ -827,18 +868,27 @@ def main():
     elif args.workload == "engine":
         line = bench_engine(args, world, rank, local)
     else:
-        line = bench_train(args, world, rank, local)
-        if not args.no_engine:
+        g = bench_train(args, world, rank, local)
+        if args.sync:
+            line = g
+        else:
+            # headline: the asynchronous engine-driven pipeline; the synchronous
+            # GPipe step of the same model is measured first and reported beside it, and the GEMM
+            # roofline / kernel breakdown / cost model / CPU baseline come from its profiled steps
             import gc
 
             import torch
             gc.collect()
             torch.cuda.empty_cache()
-            e = bench_engine(argparse.Namespace(**{**vars(args), "steps": 3, "warmup": 2}), world, rank, local)
-            line["engine_async"] = {k: e[k] for k in ("metric", "value", "unit", "ms_per_step", "steps", "engine",
-                                                      "gpu_launches")}
-            line["engine_async"]["note"] = ("SURVEY §8(f)1: the same configs[2] model trained asynchronously in the "
-                                            "reference DES engine's record order (bench.py --workload engine)")
+            line = bench_engine(args, world, rank, local)
+            for k in ("roofline", "step_breakdown", "cost_model", "step_phases_ms", "cpu_baseline"):
+                if k in g:
+                    line[k] = g[k]
+            line["roofline"]["note"] = ("measured on the synchronous step's profiled visits (same kernels, same "
+                                        "shapes): " + line["roofline"]["note"])
+            line["gpipe_sync"] = {k: g[k] for k in ("value", "ms_per_step", "steps", "e2e", "gpu_launches", "clocks")}
+            line["gpipe_sync"]["note"] = ("the same workload as one synchronous GPipe optimizer step over 32 "
+                                          "microbatches (bench.py --sync); paired weight gradients")
             gc.collect()
             torch.cuda.empty_cache()
         if not args.no_codec:

@@ -295,6 +295,10 @@ int swarm_stage_backward(swarm_stage_t st, int slot, const void* grad_in, void* 
 #define SWARM_WGRAD_DEFER 1
 #define SWARM_WGRAD_PAIR 2
 int swarm_stage_enable_wgrad_pairing(swarm_stage_t st);
+/* the same with n_sets >= 2 stash sets (set / prev_set index them); the
+ * engine-driven executor keeps one per trainer so a deferred visit's dY survives
+ * other trainers' visits */
+int swarm_stage_enable_wgrad_pairing_sets(swarm_stage_t st, int n_sets);
 int swarm_stage_backward_ex(swarm_stage_t st, int slot, const void* grad_in, void* grad_out, int wgrad_mode, int set,
                             int prev_slot, int prev_set, swarm_stream_t stream);
 int swarm_stage_flush_wgrad(swarm_stage_t st, int slot, int set, swarm_stream_t stream);

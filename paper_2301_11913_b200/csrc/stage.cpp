@@ -79,8 +79,9 @@ struct swarm_stage {
     // LayerNorm gains / biases are read in fp32 from the master; with banks each
     // bank keeps its own compact copy (the master is being updated concurrently)
     // paired weight gradients: per layer, the backward's dY tensors of a deferred
-    // visit (two sets: the pending visit's and the current one's)
-    std::vector<Stash> stash[2];
+    // visit (>= two sets: the pending visit's and the current one's; the
+    // engine-driven executor keeps one set per trainer)
+    std::vector<std::vector<Stash>> stash;
     std::vector<std::pair<size_t, size_t>> ln_slices;  // (arena offset, elements)
     std::unordered_map<size_t, size_t> ln_compact;    // arena offset -> compact offset
     size_t ln_total = 0;
@@ -932,9 +933,15 @@ int swarm_stage_backward(swarm_stage_t s, int slot, const void* grad_in, void* g
     return swarm_stage_backward_ex(s, slot, grad_in, grad_out, SWARM_WGRAD_NOW, 0, -1, 0, stream);
 }
 
-int swarm_stage_enable_wgrad_pairing(swarm_stage_t s) {
-    if (!s->stash[0].empty()) return SWARM_OK;
+int swarm_stage_enable_wgrad_pairing(swarm_stage_t s) { return swarm_stage_enable_wgrad_pairing_sets(s, 2); }
+
+int swarm_stage_enable_wgrad_pairing_sets(swarm_stage_t s, int n_sets) {
+    if (n_sets < 2) return fail("enable_wgrad_pairing: need at least two stash sets");
+    if (!s->stash.empty()) return static_cast<int>(s->stash.size()) >= n_sets
+                                      ? SWARM_OK
+                                      : fail("enable_wgrad_pairing: already enabled with fewer sets");
     const size_t T = s->T, d = s->d, F = s->F;
+    s->stash.resize(n_sets);
     for (auto& set : s->stash) {
         set.resize(s->cfg.n_layers);
         for (Stash& x : set) {
@@ -948,8 +955,9 @@ int swarm_stage_enable_wgrad_pairing(swarm_stage_t s) {
 }
 
 int swarm_stage_flush_wgrad(swarm_stage_t s, int slot, int set, swarm_stream_t stream) {
-    if (s->stash[0].empty()) return fail("flush_wgrad: pairing not enabled");
-    if (slot < 0 || slot >= static_cast<int>(s->slots.size()) || set < 0 || set > 1) return fail("flush_wgrad: bad slot/set");
+    if (s->stash.empty()) return fail("flush_wgrad: pairing not enabled");
+    if (slot < 0 || slot >= static_cast<int>(s->slots.size()) || set < 0 || set >= static_cast<int>(s->stash.size()))
+        return fail("flush_wgrad: bad slot/set");
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     ProfScope prof(s);
     const int T = s->T, d = s->d, F = s->F, n = s->cfg.n_layers;
@@ -972,10 +980,11 @@ int swarm_stage_backward_ex(swarm_stage_t s, int slot, const void* grad_in, void
     if (slot < 0 || slot >= static_cast<int>(s->slots.size())) return fail("backward: bad slot");
     if (wgrad_mode < SWARM_WGRAD_NOW || wgrad_mode > SWARM_WGRAD_PAIR) return fail("backward: bad wgrad mode");
     if (wgrad_mode != SWARM_WGRAD_NOW) {
-        if (s->stash[0].empty()) return fail("backward: wgrad pairing not enabled");
-        if (set < 0 || set > 1) return fail("backward: bad stash set");
+        const int nsets = static_cast<int>(s->stash.size());
+        if (nsets == 0) return fail("backward: wgrad pairing not enabled");
+        if (set < 0 || set >= nsets) return fail("backward: bad stash set");
         if (wgrad_mode == SWARM_WGRAD_PAIR &&
-            (prev_slot < 0 || prev_slot >= static_cast<int>(s->slots.size()) || prev_set < 0 || prev_set > 1 ||
+            (prev_slot < 0 || prev_slot >= static_cast<int>(s->slots.size()) || prev_set < 0 || prev_set >= nsets ||
              prev_set == set || prev_slot == slot))
             return fail("backward: pairing needs a distinct pending slot and stash set");
     }

@@ -69,7 +69,8 @@ class EngineExecutor:
                  lr: float = 1e-4, weight_decay: float = 0.0, forward_seconds: float = 1.0,
                  backward_multiplier: float = 2.0, allreduce_period: float = 0.0, allreduce_stall: float = 0.0,
                  duration_seconds: float = 1e9, use_graphs: bool = True, n_pool: int = 16,
-                 tokens: torch.Tensor | None = None, targets: torch.Tensor | None = None):
+                 tokens: torch.Tensor | None = None, targets: torch.Tensor | None = None, pair_wgrad: bool = True,
+                 stream_per_peer: bool = True):
         self.m = mcfg
         self.S = n_stages
         self.seed = seed
@@ -96,6 +97,12 @@ class EngineExecutor:
                               block_size=mcfg.block_size, maxout_k=mcfg.maxout_k, lr=lr,
                               weight_decay=weight_decay, seed=seed * 1000 + s)  # stage replicas start identical
             self.stages[pid] = Stage(cfg, self.device)
+            if pair_wgrad:
+                self.stages[pid].enable_wgrad_pairing(max(2, self.T))  # stash set = trainer id
+        # paired weight gradients (K = 2T GEMMs over two backward visits of a peer):
+        # peer -> trainer whose backward visit deferred its weight gradients
+        self.pair_wgrad = pair_wgrad
+        self._pend: dict = {}
         wb = next(iter(self.stages.values())).wire_bytes if self.stages else Stage(
             StageConfig(d_model=mcfg.d_model, n_heads=mcfg.n_heads, d_ffn=mcfg.d_ffn, seq_len=mcfg.seq_len,
                         micro_batch=mcfg.micro_batch, n_layers=1, vocab=mcfg.vocab, wire=mcfg.wire,
@@ -115,7 +122,14 @@ class EngineExecutor:
         self.tok = [torch.empty(mcfg.tokens, dtype=torch.int32, device=self.device) for _ in range(self.T)]
         self.tgt = [torch.empty(mcfg.tokens, dtype=torch.int32, device=self.device) for _ in range(self.T)]
         self.loss_sum = torch.zeros(1, dtype=torch.float32, device=self.device)
+        self.host_tok = self.host_tgt = None  # pinned host pools (end-to-end mode), else the device pool
         self.recv_stream = torch.cuda.Stream(device=self.device)
+        # one compute stream per local peer: peers sharing a GPU serve their queues
+        # independently, as the engine models them, and their kernels fill each
+        # other's idle SMs; cross-peer hazards are ordered by events (_done, _read)
+        cur = torch.cuda.current_stream()
+        self.ws = {pid: (torch.cuda.Stream(device=self.device) if stream_per_peer else cur) for pid in self.local}
+        self._done: dict = {}      # buffer key -> event after its local producing visit
         self._recv: dict = {}      # buffer key -> pending irecv work (the consumer waits on it)
         self._send: dict = {}      # buffer key -> pending isend work (the next writer waits on it)
         self._read: dict = {}      # buffer key -> event after the last local reader
@@ -140,6 +154,7 @@ class EngineExecutor:
         self.ticks = 0
         self.optimizer_steps = 0
         self.records = 0
+        torch.cuda.synchronize()  # stage initialisation ran on the legacy stream; peer streams do not wait on it
 
     # ------------------------------------------------------------ helpers
     def _pool_index(self, t: int, k: int) -> int:
@@ -179,11 +194,18 @@ class EngineExecutor:
         self.visit_log.append((t, int(r.microbatch), s, bwd, pid))
         if pid not in self.stages:
             return
+        with torch.cuda.stream(self.ws[pid]):
+            self._visit(r, s, t, pid, bwd)
+        self.visits_local += 1
+
+    def _visit(self, r, s, t, pid, bwd) -> None:
         st = self.stages[pid]
         cur = torch.cuda.current_stream()
         inkey = self._buf(t, s, bwd)
         if inkey is not None and inkey in self._recv:
-            self._recv.pop(inkey).wait()  # compute stream waits for the transfer
+            self._recv.pop(inkey).wait()  # this peer's stream waits for the transfer
+        if inkey is not None and inkey in self._done:
+            cur.wait_event(self._done.pop(inkey))  # produced by a peer on this GPU (another stream)
         outkey = None
         if bwd and s > 0:
             outkey = ("g", t, s - 1)
@@ -191,13 +213,17 @@ class EngineExecutor:
             outkey = ("a", t, s)
         if outkey is not None and outkey in self._send:
             self._send.pop(outkey).wait()  # the previous message from this buffer has left
+        if outkey is not None and outkey in self._read:
+            cur.wait_event(self._read.pop(outkey))  # its previous local reader is done
+        if not bwd and self._pend.get(pid) == t:
+            self._flush(pid)  # this forward reuses the slot the pending weight gradients read
         if not bwd:
-            if s == 0:
-                k = self._pool_index(t, r.microbatch)
-                self.tok[t].copy_(self.pool_tok[k], non_blocking=True)
+            src_tok, src_tgt = (self.host_tok, self.host_tgt) if self.host_tok is not None else (
+                self.pool_tok, self.pool_tgt)
+            if s == 0:  # with a host pool: the microbatch's tokens cross PCIe here (H2D from pinned memory)
+                self.tok[t].copy_(src_tok[self._pool_index(t, r.microbatch)], non_blocking=True)
             if s == self.S - 1:
-                k = self._pool_index(t, r.microbatch)
-                self.tgt[t].copy_(self.pool_tgt[k], non_blocking=True)
+                self.tgt[t].copy_(src_tgt[self._pool_index(t, r.microbatch)], non_blocking=True)
             inp = self.tok[t] if s == 0 else self._tensor(inkey)
             out = None if outkey is None else self._tensor(outkey)
             tg = self.tgt[t] if s == self.S - 1 else None
@@ -207,12 +233,23 @@ class EngineExecutor:
         else:
             gin = None if inkey is None else self._tensor(inkey)
             gout = None if outkey is None else self._tensor(outkey)
-            self._replay((pid, "b", t), lambda: st.backward(t, grad_in=gin, grad_out=gout))
+            if not self.pair_wgrad:
+                self._replay((pid, "b", t), lambda: st.backward(t, grad_in=gin, grad_out=gout))
+            elif pid not in self._pend:  # first of a pair: data gradients now, dY kept in stash set t
+                self._replay((pid, "b", t, -1), lambda: st.backward_ex(t, gin, gout, mode=Stage.WGRAD_DEFER, set=t))
+                self._pend[pid] = t
+            else:                        # second: both visits' weight gradients as K = 2T GEMMs
+                p = self._pend.pop(pid)
+                self._replay((pid, "b", t, p), lambda: st.backward_ex(t, gin, gout, mode=Stage.WGRAD_PAIR, set=t,
+                                                                      prev_slot=p, prev_set=p))
         if inkey is not None:
             ev = torch.cuda.Event()
             ev.record(cur)
             self._read[inkey] = ev
-        self.visits_local += 1
+        if outkey is not None:
+            ev = torch.cuda.Event()
+            ev.record(cur)
+            self._done[outkey] = ev
 
     def _hop(self, r) -> None:
         # same-rank hops need nothing: the consumer reads the producer's buffer in stream order
@@ -221,7 +258,9 @@ class EngineExecutor:
             return
         op, peer, key = act
         if op == "send":
-            self._send[key] = dist.isend(self._tensor(key), peer)  # NCCL stream waits for the producing visit
+            self._done.pop(key, None)  # consumed remotely: the isend below is ordered after the producer
+            with torch.cuda.stream(self.ws[r.from_worker]):
+                self._send[key] = dist.isend(self._tensor(key), peer)  # NCCL stream waits for the producing visit
         else:
             with torch.cuda.stream(self.recv_stream):
                 ev = self._read.pop(key, None)
@@ -229,16 +268,26 @@ class EngineExecutor:
                     self.recv_stream.wait_event(ev)  # the previous reader of this buffer is done
                 self._recv[key] = dist.irecv(self._tensor(key), peer)
 
+    def _flush(self, pid: int) -> None:
+        """A peer's pending (deferred) weight gradients, alone."""
+        t = self._pend.pop(pid)
+        st = self.stages[pid]
+        with torch.cuda.stream(self.ws[pid]):
+            self._replay((pid, "w", t), lambda: st.flush_wgrad(t, t))
+
     def _allreduce(self, r) -> None:
         self.ticks += 1
+        for pid in list(self._pend):
+            self._flush(pid)
         for pid, st in self.stages.items():
             s = self.pl.stage_of_peer(pid)
             n = self.served[s]
             if n == 0:
                 continue
-            if s in self.groups:
-                dist.all_reduce(st.grads(), op=dist.ReduceOp.SUM, group=self.groups[s])
-            st.optimizer_step(grad_scale=1.0 / n)  # mean over the stage's microbatches since the last tick
+            with torch.cuda.stream(self.ws[pid]):
+                if s in self.groups:
+                    dist.all_reduce(st.grads(), op=dist.ReduceOp.SUM, group=self.groups[s])
+                st.optimizer_step(grad_scale=1.0 / n)  # mean over the stage's microbatches since the last tick
             self.optimizer_steps += 1
         self.served = [0] * self.S
 
@@ -246,6 +295,7 @@ class EngineExecutor:
         """Process engine records until `n_microbatches` more microbatches have
         completed (or the engine's duration ends).  Returns the number completed."""
         target = self.completed + n_microbatches
+        self.fork()  # peer streams start after whatever the caller queued (e.g. a loss reset)
         while self.completed < target:
             batch = self.engine.next(1)
             if not batch:
@@ -262,12 +312,45 @@ class EngineExecutor:
                 self.completed += 1
         return self.completed - (target - n_microbatches)
 
+    def flush_wgrad(self) -> None:
+        """Issue every pending deferred weight gradient (before reading gradients)."""
+        for pid in list(self._pend):
+            self._flush(pid)
+
+    def use_host_pool(self, enable: bool = True) -> None:
+        """End-to-end mode: every microbatch's tokens / targets are copied from
+        pinned host memory by the visit that consumes them."""
+        if enable:
+            self.host_tok = self.pool_tok.cpu().pin_memory()
+            self.host_tgt = self.pool_tgt.cpu().pin_memory()
+        else:
+            self.host_tok = self.host_tgt = None
+
+    def last_stage_stream(self):
+        """The compute stream of this rank's last-stage peer (it owns loss_sum), or None."""
+        for pid in self.local:
+            if self.pl.stage_of_peer(pid) == self.S - 1:
+                return self.ws[pid]
+        return None
+
+    def fork(self) -> None:
+        """Every peer stream waits for the current stream (start of a timed region)."""
+        cur = torch.cuda.current_stream()
+        for w in self.ws.values():
+            if w != cur:
+                w.wait_stream(cur)
+
     def finish(self) -> None:
-        """Wait for outstanding transfers (end of a timed region)."""
+        """The current stream waits for every peer stream and outstanding transfer
+        (end of a timed region)."""
+        cur = torch.cuda.current_stream()
         for w in list(self._send.values()) + list(self._recv.values()):
             w.wait()
         self._send.clear()
         self._recv.clear()
+        for w in self.ws.values():
+            if w != cur:
+                cur.wait_stream(w)
 
     def kernels_launched(self) -> int:
         return L.lib().swarm_launch_count() - self.captured_kernels + self.replayed_kernels

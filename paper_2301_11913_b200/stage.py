@@ -118,8 +118,8 @@ class Stage:
     # -- paired weight gradients ----------------------------------------------
     WGRAD_NOW, WGRAD_DEFER, WGRAD_PAIR = 0, 1, 2
 
-    def enable_wgrad_pairing(self) -> None:
-        L.check(self.lib.swarm_stage_enable_wgrad_pairing(self.h), "stage_enable_wgrad_pairing")
+    def enable_wgrad_pairing(self, n_sets: int = 2) -> None:
+        L.check(self.lib.swarm_stage_enable_wgrad_pairing_sets(self.h, n_sets), "stage_enable_wgrad_pairing")
 
     def backward_ex(self, slot: int, grad_in=None, grad_out=None, *, mode: int = 0, set: int = 0, prev_slot: int = -1,
                     prev_set: int = 0, stream=None) -> None:

@@ -21,6 +21,7 @@ ex.run(9)
 ex.finish()
 torch.cuda.synchronize()
 dist.barrier()
+ex.flush_wgrad()
 ref = sequential_reference_grads(ex)
 ok = True
 for pid, st in ex.stages.items():

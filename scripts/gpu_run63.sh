@@ -1,0 +1,7 @@
+cd $GRAFT_REPO_ROOT
+export TORCH_NCCL_SHOW_EAGER_INIT_P2P_SERIALIZATION_WARNING=false
+R2="python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29563"
+R4="python -m torch.distributed.run --nnodes=1 --nproc-per-node 4 --master-addr 127.0.0.1 --master-port 29564"
+timeout -k 10 1200 $R4 bench.py --gpus 4 > gpurun_out/b63_n4.log 2>&1; echo "rc=$?" >> gpurun_out/b63_n4.log
+timeout -k 10 1200 $R2 bench.py --gpus 2 > gpurun_out/b63_n2.log 2>&1; echo "rc=$?" >> gpurun_out/b63_n2.log
+timeout -k 10 600 $R4 bench.py --gpus 4 --impl reference > gpurun_out/b63_ref4.log 2>&1; echo "rc=$?" >> gpurun_out/b63_ref4.log

@@ -12,15 +12,20 @@ def rel(a, b):
     return float((a - b).norm() / b.norm().clamp_min(1e-30))
 
 
+@pytest.mark.parametrize("streams", [True, False])
+@pytest.mark.parametrize("pair", [True, False])
 @pytest.mark.parametrize("S,tpp", [(4, 1), (2, 3), (3, 2)])
-def test_executor_gradients_match_sequential_visits(cuda, S, tpp):
+def test_executor_gradients_match_sequential_visits(cuda, S, tpp, pair, streams):
     import torch
     from paper_2301_11913_b200.executor import EngineExecutor, sequential_reference_grads
     from paper_2301_11913_b200.swarm import PRESETS
-    ex = EngineExecutor(PRESETS["tiny"], S, trainers_per_peer=tpp, seed=5, n_pool=5)
+    ex = EngineExecutor(PRESETS["tiny"], S, trainers_per_peer=tpp, seed=5, n_pool=5, pair_wgrad=pair,
+                        stream_per_peer=streams)
     assert ex.run(7) == 7
+    ex.finish()
     torch.cuda.synchronize()
     assert all(len(v) > 0 for v in ex.bwd_log)
+    ex.flush_wgrad()
     ref = sequential_reference_grads(ex)
     for pid, st in ex.stages.items():
         assert rel(st.grads(), ref[pid]) <= 1e-4, (pid, rel(st.grads(), ref[pid]))
@@ -37,6 +42,7 @@ def test_executor_trains_with_allreduce_ticks(cuda):
     for _ in range(8):
         ex.loss_sum.zero_()
         n = ex.run(8)
+        ex.finish()
         curve.append(ex.loss_sum.item() / max(n, 1) / ex.m.tokens)  # loss_sum holds token CE sums
     assert ex.optimizer_steps > 0 and ex.ticks > 0
     assert all(c == c for c in curve)
