@@ -11,18 +11,24 @@ work at exactly those points, in the engine's record order:
 * START  -> the serving peer's rank runs the stage visit (forward or backward)
             on its compute stream (CUDA-graph replay per (peer, kind, trainer));
 * HOP    -> the trainer's wire message (int8 codes ‖ fp32 scales ‖ header)
-            moves from the producing peer to the chosen peer: NCCL isend after
-            the producing visit, irecv on a receive stream that only waits for the
-            previous reader of that buffer; the consuming visit waits for it;
+            is routed to the chosen peer; across ranks both halves of the NCCL
+            transfer are issued at the consuming visit's START record: isend on a
+            send stream that waits only for the producing visit, irecv on a
+            receive stream that waits only for the previous reader of that
+            buffer, and the consuming visit waits for the receive (posting the
+            receive at dispatch time instead left an NCCL kernel spinning on SMs
+            through the whole producing visit and blocked the rank's p2p stream:
+            measured 417k vs 537k tokens/s at 2 stages x 2 peers);
 * ALLREDUCE -> each stage's peers all-reduce their fp32 gradient arena and take
             an AdamW step over the microbatches their stage served since the
             last tick (SWARM's asynchronous accumulate-then-average);
 * DONE   -> a microbatch finished (loss already accumulated on the last stage).
 
 This is asynchronous SWARM training: no per-step barrier, trainers keep their
-microbatches moving, peers serve queued visits in FIFO order.  Every
-dependency points to an earlier record, and every rank issues its halves of a
-point-to-point transfer at the same record, so NCCL cannot deadlock.
+microbatches moving, peers serve queued visits in FIFO order (one compute
+stream per local peer).  Every dependency points to an earlier record, and
+every rank issues its halves of a point-to-point transfer at the same record,
+so NCCL cannot deadlock.
 
 Buffers: activation slot = trainer id on every peer (a trainer has at most
 one microbatch in flight); wire messages per (trainer, boundary, direction).
@@ -124,6 +130,8 @@ class EngineExecutor:
         self.loss_sum = torch.zeros(1, dtype=torch.float32, device=self.device)
         self.host_tok = self.host_tgt = None  # pinned host pools (end-to-end mode), else the device pool
         self.recv_stream = torch.cuda.Stream(device=self.device)
+        self.send_stream = torch.cuda.Stream(device=self.device)
+        self._xfer: dict = {}      # buffer key -> this rank's half of a pending cross-rank transfer
         # one compute stream per local peer: peers sharing a GPU serve their queues
         # independently, as the engine models them, and their kernels fill each
         # other's idle SMs; cross-peer hazards are ordered by events (_done, _read)
@@ -176,8 +184,19 @@ class EngineExecutor:
         if g is None:
             n0 = L.lib().swarm_launch_count()
             g = torch.cuda.CUDAGraph()
-            with torch.cuda.graph(g):
-                fn()
+            if torch.cuda.current_stream() != torch.cuda.default_stream():
+                # capture straight on the peer's stream: unlike the torch.cuda.graph context
+                # this neither synchronises the device nor runs the garbage collector, so a
+                # (peer, trainer pair) met for the first time inside a timed region does not
+                # drain every other peer's queue
+                g.capture_begin(capture_error_mode="thread_local")
+                try:
+                    fn()
+                finally:
+                    g.capture_end()
+            else:
+                with torch.cuda.graph(g):
+                    fn()
             n = L.lib().swarm_launch_count() - n0
             self.graph_kernels[key] = n
             self.captured_kernels += n
@@ -192,6 +211,9 @@ class EngineExecutor:
             self.served[s] += 1
             self.bwd_log[s].append((t, int(r.microbatch)))
         self.visit_log.append((t, int(r.microbatch), s, bwd, pid))
+        key = self._buf(t, s, bwd)
+        if key is not None and key in self._xfer:
+            self._transfer(self._xfer.pop(key))  # both ranks of a cross-rank hop, at the same record
         if pid not in self.stages:
             return
         with torch.cuda.stream(self.ws[pid]):
@@ -252,15 +274,22 @@ class EngineExecutor:
             self._done[outkey] = ev
 
     def _hop(self, r) -> None:
-        # same-rank hops need nothing: the consumer reads the producer's buffer in stream order
+        # same-rank hops need nothing: the consumer reads the producer's buffer in stream order.
+        # A cross-rank transfer is issued by both ranks at the consuming visit's START record
+        # (not here): a receive posted at dispatch time would spin an NCCL kernel on the SMs for
+        # the whole producing visit, and it would block the rank's single p2p stream.
         act = hop_action(self.pl, self.S, r, self.rank)
-        if act is None:
-            return
+        if act is not None:
+            self._xfer[act[2]] = act
+
+    def _transfer(self, act) -> None:
         op, peer, key = act
         if op == "send":
-            self._done.pop(key, None)  # consumed remotely: the isend below is ordered after the producer
-            with torch.cuda.stream(self.ws[r.from_worker]):
-                self._send[key] = dist.isend(self._tensor(key), peer)  # NCCL stream waits for the producing visit
+            ev = self._done.pop(key, None)  # the producing visit (on its peer's stream)
+            with torch.cuda.stream(self.send_stream):
+                if ev is not None:
+                    self.send_stream.wait_event(ev)
+                self._send[key] = dist.isend(self._tensor(key), peer)
         else:
             with torch.cuda.stream(self.recv_stream):
                 ev = self._read.pop(key, None)

@@ -29,31 +29,37 @@ def schedule(world, S, tpp, seed, n=4000):
 @pytest.mark.parametrize("world,S,tpp,seed", [(1, 4, 1, 0), (2, 4, 2, 1), (4, 4, 1, 2), (8, 4, 1, 3),
                                               (8, 4, 3, 4), (4, 2, 2, 5), (2, 2, 1, 6), (6, 3, 2, 7)])
 def test_p2p_ops_pair_up_and_precede_consumers(world, S, tpp, seed):
+    """The executor's issue logic: at a HOP each rank notes its half of a
+    cross-rank transfer (hop_action); both halves are issued at the consuming
+    visit's START record.  Per ordered rank pair the send and receive sequences
+    must be identical (NCCL matches them in order), every remote input must be
+    received at its consumer's START, and every noted transfer must be issued."""
     pl, recs = schedule(world, S, tpp, seed)
     sends = {}   # (a, b) -> keys a sends to b, in a's issue order
     recvs = {}   # (a, b) -> keys b receives from a, in b's issue order
-    arrived = {r: set() for r in range(world)}   # keys received and not yet consumed
+    xfer = {r: {} for r in range(world)}   # rank -> key -> its noted half
     remote = {}  # trainer -> did its latest hop cross ranks
     for r in recs:
         if r.kind == HOP:
             remote[r.trainer] = r.from_worker >= 0 and pl.rank_of_peer(r.from_worker) != pl.rank_of_peer(r.worker)
             for rank in range(world):
                 act = hop_action(pl, S, r, rank)
-                if act is None:
-                    continue
-                op, peer, key = act
-                if op == "send":
-                    sends.setdefault((rank, peer), []).append(key)
-                else:
-                    recvs.setdefault((peer, rank), []).append(key)
-                    arrived[rank].add(key)
+                if act is not None:
+                    assert act[2] not in xfer[rank], "a buffer's previous transfer was never issued"
+                    xfer[rank][act[2]] = act
         elif r.kind == START:
             key = wire_key(S, r.trainer, r.stage, bool(r.backward))
-            rank = pl.rank_of_peer(r.worker)
-            if key is None or not remote.get(r.trainer):
-                continue
-            assert key in arrived[rank], "visit input produced on another rank was never received"
-            arrived[rank].discard(key)
+            issued = set()
+            for rank in range(world):
+                if key is not None and key in xfer[rank]:
+                    op, peer, k = xfer[rank].pop(key)
+                    if op == "send":
+                        sends.setdefault((rank, peer), []).append(k)
+                    else:
+                        recvs.setdefault((peer, rank), []).append(k)
+                        issued.add(rank)
+            if key is not None and remote.get(r.trainer):
+                assert pl.rank_of_peer(r.worker) in issued, "remote input not received at its consumer's START"
     assert sends.keys() == recvs.keys()
     for pair in sends:
         assert sends[pair] == recvs[pair], pair
