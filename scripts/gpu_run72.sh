@@ -1,0 +1,12 @@
+cd $GRAFT_REPO_ROOT
+export TORCH_NCCL_SHOW_EAGER_INIT_P2P_SERIALIZATION_WARNING=false
+timeout -k 5 900 python -m pytest tests -m gpu -x -q -p no:cacheprovider > gpurun_out/t72_all.log 2>&1; echo "rc=$?" >> gpurun_out/t72_all.log
+timeout -k 5 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke72.log 2>&1; echo "rc=$?" >> gpurun_out/smoke72.log
+timeout -k 10 1500 python bench.py > gpurun_out/b72_n1.log 2>&1; echo "rc=$?" >> gpurun_out/b72_n1.log
+timeout -k 10 900 python bench.py --impl reference > gpurun_out/b72_ref1.log 2>&1; echo "rc=$?" >> gpurun_out/b72_ref1.log
+R2="python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29579"
+R4="python -m torch.distributed.run --nnodes=1 --nproc-per-node 4 --master-addr 127.0.0.1 --master-port 29580"
+timeout -k 10 1500 $R2 bench.py --gpus 2 > gpurun_out/b72_n2.log 2>&1; echo "rc=$?" >> gpurun_out/b72_n2.log
+timeout -k 10 1500 $R4 bench.py --gpus 4 > gpurun_out/b72_n4.log 2>&1; echo "rc=$?" >> gpurun_out/b72_n4.log
+timeout -k 10 900 $R4 bench.py --gpus 4 --workload failure > gpurun_out/b72_failure4.log 2>&1; echo "rc=$?" >> gpurun_out/b72_failure4.log
+timeout -k 10 900 $R4 bench.py --gpus 4 --workload codec > gpurun_out/b72_codec4.log 2>&1; echo "rc=$?" >> gpurun_out/b72_codec4.log
