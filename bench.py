@@ -660,7 +660,9 @@ def bench_engine(args, world, rank, local):
                         backward_multiplier=bm, allreduce_period=M * (1.0 + bm) / P, allreduce_stall=0.05,
                         stream_per_peer=not args.single_stream)
     stream = torch.cuda.current_stream()
-    ex.run(M * args.warmup)
+    # untimed warm-up: W steps plus two more, so that the visit graphs of most
+    # (peer, trainer pair) combinations are captured before the timed region
+    ex.run(M * (args.warmup + 2))
     ex.finish()
     torch.cuda.synchronize()
     ex.loss_sum.zero_()
