@@ -672,7 +672,7 @@ def bench_engine(args, world, rank, local):
     barrier(world)
     torch.cuda.synchronize()
     n0 = ex.kernels_launched()
-    v0, r0, t_0 = ex.engine.summary()["now"], ex.records, ex.optimizer_steps
+    v0, r0, t_0, c0 = ex.engine.summary()["now"], ex.records, ex.optimizer_steps, ex.captures
     t0 = torch.cuda.Event(enable_timing=True)
     t1 = torch.cuda.Event(enable_timing=True)
     t0.record(stream)
@@ -731,7 +731,8 @@ def bench_engine(args, world, rank, local):
                    "model_tflops_per_s": value * mcfg.flops_per_token(S) / 1e12,
                    "l2": "per-step working set far exceeds L2; no flush needed"},
         "engine": {"records": ex.records - r0, "virtual_seconds": ex.engine.summary()["now"] - v0,
-                   "optimizer_steps_rank": ex.optimizer_steps - t_0, "microbatches": done},
+                   "optimizer_steps_rank": ex.optimizer_steps - t_0, "microbatches": done,
+                   "graph_captures_in_timed_region_rank0": ex.captures - c0},
         "e2e": {"value": e2e_done * mcfg.tokens / e2e_s, "unit": "tokens/s",
                 "h2d_bytes_per_step": int(M * mcfg.tokens * 4 * 2),
                 "d2h_bytes_per_step": 4, "path": "EngineExecutor.run with each microbatch's tokens / targets copied "

@@ -157,6 +157,7 @@ class EngineExecutor:
         self._warm: set = set()
         self.captured_kernels = 0
         self.replayed_kernels = 0
+        self.captures = 0           # visit graphs captured so far
         self.completed = 0          # microbatches finished (global, from the schedule)
         self.visits_local = 0
         self.ticks = 0
@@ -198,6 +199,7 @@ class EngineExecutor:
                 with torch.cuda.graph(g):
                     fn()
             n = L.lib().swarm_launch_count() - n0
+            self.captures += 1
             self.graph_kernels[key] = n
             self.captured_kernels += n
             self.graphs[key] = g
