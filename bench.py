@@ -236,6 +236,35 @@ def bench_codec(args, world, rank, local):
     q_gbs = CODEC_BYTES_Q / (q_ms / 1e3) / 1e9
     dq_gbs = CODEC_BYTES_DQ / (dq_ms / 1e3) / 1e9
 
+    # configs[1] sweep, 1 MiB .. 1 GiB of fp32 (2^18 .. 2^28 elements): per-launch
+    # CUDA events, L2 flushed (a 256 MiB write) before every timed pair so that the
+    # small sizes are measured from HBM, not from the 126 MB L2
+    sweep = []
+    flush = torch.empty(64 << 20, dtype=torch.float32, device=dev)
+    for lg in range(18, 29, 2):
+        n = 1 << lg
+        xs, cs, ss, ys = x[:n], codes[:n], scales[:n // CODEC_BS], y[:n]
+        reps = 20
+        evp = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(reps)]
+        for i in range(reps + 2):
+            flush.fill_(float(i))
+            e = evp[i - 2] if i >= 2 else None
+            if e:
+                e[0].record(stream)
+            ops.quantize(xs, CODEC_BS, codes=cs, scales=ss)
+            if e:
+                e[1].record(stream)
+            ops.dequantize(cs, ss, CODEC_BS, out=ys)
+            if e:
+                e[2].record(stream)
+        torch.cuda.synchronize()
+        qus = statistics.median(e[0].elapsed_time(e[1]) for e in evp) * 1e3
+        dqus = statistics.median(e[1].elapsed_time(e[2]) for e in evp) * 1e3
+        bq = 5 * n + 4 * (n // CODEC_BS)
+        sweep.append({"elements": n, "fp32_mib": n * 4 / 2 ** 20, "quantize_us": qus, "dequantize_us": dqus,
+                      "quantize_gbs": bq / (qus * 1e-6) / 1e9, "dequantize_gbs": bq / (dqus * 1e-6) / 1e9})
+    del flush
+
     # parity guard: a fast wrong kernel is not a result
     idx = torch.arange(0, CODEC_N // CODEC_BS, 997, device=dev)
     err = (y.view(-1, CODEC_BS)[idx] - x.view(-1, CODEC_BS)[idx]).abs().amax(1)
@@ -293,6 +322,9 @@ def bench_codec(args, world, rank, local):
         "e2e": {"value": e2e_val, "unit": "GB/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                 "path": "swarm_quantize_blockwise_host + swarm_dequantize_blockwise_host, pinned host buffers"},
         "gpu_launches": int(launches), "clocks": clocks, "parity_ok": ok,
+        "sweep": {"note": "configs[1] sizes 1 MiB-1 GiB fp32, block 4096, median of 20 launches each, L2 flushed "
+                          "before each; algorithmic bytes 5.0009765625 B/element per direction; sizes below a few "
+                          "hundred MiB are launch/latency-bound", "points": sweep},
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         threads = os.cpu_count() or 1
