@@ -180,14 +180,22 @@ __global__ void __launch_bounds__(kCeThreads) k_cross_entropy_v(const float4* __
     const int v4 = vocab >> 2;
     const float4* x = logits + static_cast<size_t>(row) * v4;
     float m = -INFINITY, s = 0.f;
-    for (int j = threadIdx.x; j < v4; j += kCeThreads) {
-        const float4 v = x[j];
+    auto fold = [&](const float4 v) {
         const float mx = fmaxf(fmaxf(v.x, v.y), fmaxf(v.z, v.w));
         const float mm = fmaxf(m, mx);
         s = (m == -INFINITY ? 0.f : s * __expf(m - mm)) + __expf(v.x - mm) + __expf(v.y - mm) + __expf(v.z - mm) +
             __expf(v.w - mm);
         m = mm;
+    };
+    int j = threadIdx.x;
+    for (; j + 3 * kCeThreads < v4; j += 4 * kCeThreads) {  // four 16-B loads in flight per thread
+        const float4 a = x[j], b = x[j + kCeThreads], c = x[j + 2 * kCeThreads], e = x[j + 3 * kCeThreads];
+        fold(a);
+        fold(b);
+        fold(c);
+        fold(e);
     }
+    for (; j < v4; j += kCeThreads) fold(x[j]);
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
         const float m2 = __shfl_xor_sync(0xffffffffu, m, o), s2 = __shfl_xor_sync(0xffffffffu, s, o);
@@ -353,7 +361,14 @@ int swarm_cross_entropy(const float* logits, const int32_t* targets, size_t rows
     if (vocab == 0) return invalid("cross_entropy: empty vocab");
     if (rows == 0) return SWARM_OK;
     if (vocab % 8 == 0 && !(reinterpret_cast<uintptr_t>(logits) & 15) && !(reinterpret_cast<uintptr_t>(dlogits) & 15)) {
-        k_cross_entropy_v<<<static_cast<unsigned>(rows), kCeThreads, 0, as_stream(stream)>>>(
+        // at most 2 rows per SM in flight (the unused dynamic smem only caps occupancy): 296 rows x
+        // 200 KB stay L2-resident between the two passes over a row, 4 per SM would not
+        static const int ce_smem = [] {
+            const int b = 96 * 1024;
+            cudaFuncSetAttribute(k_cross_entropy_v, cudaFuncAttributeMaxDynamicSharedMemorySize, b);
+            return b;
+        }();
+        k_cross_entropy_v<<<static_cast<unsigned>(rows), kCeThreads, ce_smem, as_stream(stream)>>>(
             reinterpret_cast<const float4*>(logits), targets, static_cast<int>(vocab), grad_scale, loss_sum,
             static_cast<uint4*>(dlogits));
         SWARM_LAUNCH_CHECK("k_cross_entropy_v");
