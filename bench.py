@@ -489,18 +489,24 @@ def cost_model_report(mcfg, S, M, world, step_s, link):
             t += 2.0 * grad_bytes * (P - 1) / P / link[0]  # ring all-reduce of the fp32 gradient arena
         pred[str(G)] = M * mcfg.tokens / t
     # the asynchronous pipeline as the reference engine sees it (csrc/engine.cpp, decision-
-    # identical to sim::run): one GPU per peer, the calibrated visit split 1:2 fwd:bwd,
-    # 2 trainers per peer, a tick every ~M microbatches per stage stalling for the all-reduce
+    # identical to sim::run): one GPU per peer, 2 trainers per peer, a tick every ~M
+    # microbatches per stage stalling for the all-reduce.  Peer speeds (SimConfig PeerSpec)
+    # carry the model's stage imbalance: the last stage also runs the LM head, whose FLOPs
+    # add V*d / (layers * params_per_layer) to a block stage's; the calibrated visit is the
+    # average over all stages, so the block-stage visit is avg * S / (S - 1 + head_ratio)
     from paper_2301_11913_b200.engine import Engine, EngineConfig
+    head_ratio = 1.0 + mcfg.vocab * mcfg.d_model / (mcfg.layers_per_stage * mcfg.params_per_layer())
+    base = c.total_seconds * S / (S - 1 + head_ratio)
     eng = {}
     for G in (4, 8):
         P = G // S
         if P < 1:
             continue
-        fwd = c.total_seconds / 3.0
+        fwd = base / 3.0
         stall = 2.0 * grad_bytes * (P - 1) / P / link[0] if P > 1 else 1e-9
-        dur = 400.0 * M * c.total_seconds / P
-        e = Engine(EngineConfig(n_stages=S, initial_peers=[[1.0] * P for _ in range(S)], forward_service_seconds=fwd,
+        dur = 400.0 * M * base / P
+        peers = [[1.0] * P for _ in range(S - 1)] + [[1.0 / head_ratio] * P]
+        e = Engine(EngineConfig(n_stages=S, initial_peers=peers, forward_service_seconds=fwd,
                                 trainers_per_peer=2, allreduce_period=M * 3.0 * fwd / P, allreduce_stall=stall,
                                 duration_seconds=dur, bucket_seconds=dur / 8), seed=1)
         while e.next(4096):
@@ -508,14 +514,14 @@ def cost_model_report(mcfg, S, M, world, step_s, link):
         sm = e.summary()
         eng[str(G)] = sm["completed"] * mcfg.tokens / dur
     return {"calibrated_effective_flops": prof.effective_flops, "link_bps": link[0], "link_source": src,
-            "engine_predicted_tokens_per_s": eng,
+            "engine_predicted_tokens_per_s": eng, "head_stage_ratio": head_ratio,
             "visit_s": visit, "stage_cost": {"compute_s": c.compute_seconds, "comm_s": c.comm_seconds,
                                              "utilization": c.utilization},
             "square_cube_ratio_flop_per_bit": X.square_cube_ratio(shape),
             "predicted_tokens_per_s": pred,
             "note": "predicted_tokens_per_s: GPipe step (M/P + min(G,S) - 1) x stages-per-rank x visit + fp32 "
                     "gradient all-reduce; engine_predicted_tokens_per_s: the DES engine's completions over a long "
-                    "run at the calibrated visit (equal stages: the LM-head stage's extra work is averaged in); "
+                    "run at the calibrated visit, the last stage's peers slowed by head_stage_ratio; "
                     "the driver's scaling run measures the same N"}
 
 
