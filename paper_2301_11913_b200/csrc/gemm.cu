@@ -1154,9 +1154,8 @@ extern "C" int swarm_gemm_bf16(const swarm_gemm_args* a, swarm_stream_t stream) 
         bc = a->b_mn_major ? a->n : kseg;
     }
     // 2-CTA pair tiles (256 x 256) when both M and N fill them; else one CTA, 128 x BN
-    const bool pair = pair_enabled() && a->m > 128 && a->n > 128;
-    const int BN = pair ? PAIR_BN : (a->n <= 128 ? 128 : 256);
-    const int TM = pair ? 256 : BM;
+    bool pair = pair_enabled() && a->m > 128 && a->n > 128;
+    bool narrow = false;  // one-CTA 128 x 128 tiles instead of pair tiles (few-tile shapes, below)
     // two pairs per cluster sharing A by TMA multicast when N splits into an even
     // number of 256-wide tiles (halves the A traffic from L2 per SM)
     const int pair_tiles_n = (a->n + PAIR_BN - 1) / PAIR_BN;
@@ -1187,7 +1186,24 @@ extern "C" int swarm_gemm_bf16(const swarm_gemm_args* a, swarm_stream_t stream) 
         const bool pays = streamk_mode() == 1 ? t_sk + 2 < t_dp : 10 * (t_sk + 40) <= 9 * t_dp;
         use_sk = sk_rem && per >= 4 && per * (kMaxSkParts - 1) >= kblocks && pays;
     }
+    // Few-tile shapes without a paying stream-K split (configs[3]'s o / o-dgrad: 512 x 4096,
+    // 32 pair tiles on 74 clusters) fill more SMs with one-CTA 128 x 128 tiles.  Measured
+    // per-SM rate of those is ~0.62 of a pair tile's (610 vs 760 TFLOP/s on 512x4096x4096,
+    // scripts/gemm_shapes.py), so they are chosen when wave utilisation x 0.62 still wins.
+    if (pair && !use_sk && !two_seg) {
+        const long long pt = static_cast<long long>((a->m + 255) / 256) * pair_tiles_n * a->batch;
+        const long long nt = static_cast<long long>((a->m + 127) / 128) * ((a->n + 127) / 128) * a->batch;
+        const long long pc = max_pair_clusters(), sc = num_sms();
+        const double u_pair = static_cast<double>(pt) / (((pt + pc - 1) / pc) * pc);
+        const double u_narrow = static_cast<double>(nt) / (((nt + sc - 1) / sc) * sc);
+        if (u_narrow * 0.62 > u_pair) {
+            pair = false;
+            narrow = true;
+        }
+    }
     const int npair = (pair && !use_sk && multicast_mode() && pair_tiles_n % 2 == 0) ? 2 : 1;
+    const int BN = pair ? PAIR_BN : (a->n <= 128 || narrow ? 128 : 256);
+    const int TM = pair ? 256 : BM;
     CUtensorMap ta, tb;
     const int box_a = a->a_mn_major ? BK : (npair == 2 ? 64 : BM), box_b = a->b_mn_major ? BK : (pair ? 128 : BN);
     int rc = encode_2d(&ta, a->a, ar, ac, a->lda, 64, box_a);
