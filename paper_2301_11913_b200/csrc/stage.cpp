@@ -67,6 +67,7 @@ struct swarm_stage {
     std::vector<LayerW> layers;
     size_t emb = 0, lnfg = 0, lnfb = 0, head = 0;
     bool bneck = false;  // maxout bottleneck at the boundaries
+    bool stacked = false;  // layer-shared: stacked weight-gradient inputs (one K = n_layers*T GEMM per weight)
     int wire_w = 0;      // features per token on the wire (d, or d / maxout_k)
     size_t bn_in_g = 0, bn_in_b = 0, bn_wd = 0, bn_out_g = 0, bn_out_b = 0;
     float *p32 = nullptr, *grad = nullptr, *m = nullptr, *v = nullptr;
@@ -583,6 +584,7 @@ int create(const swarm_stage_config* c, swarm_stage* s) {
     const int d = s->d, F = s->F;
     // parameter layout
     s->bneck = c->maxout_k > 1;
+    s->stacked = c->shared_layers && c->n_layers > 1;
     if (s->bneck && (d % c->maxout_k || (d / c->maxout_k) % 64 || c->maxout_k > 255))
         return fail("stage: maxout_k must divide d_model into a multiple of 64");
     s->wire_w = s->bneck ? d / c->maxout_k : d;
@@ -623,18 +625,34 @@ int create(const swarm_stage_config* c, swarm_stage* s) {
     // activation slots
     const size_t T = s->T, Td = T * d, TF = T * F, BHLL = static_cast<size_t>(s->B) * s->H * s->L * s->L;
     s->slots.resize(c->max_slots);
+    // layer-shared stages keep the weight-gradient inputs (a, o, c, g) of all
+    // applications stacked in application order, so one GEMM with K = n_layers * T
+    // computes a shared weight's gradient (stacked_wgrad)
+    const size_t nl = static_cast<size_t>(c->n_layers);
     for (auto& sl : s->slots) {
         sl.layer.resize(c->n_layers);
-        for (auto& A : sl.layer) {
+        bf16 *sa = nullptr, *so = nullptr, *sc = nullptr, *sg = nullptr;
+        if (s->stacked) {
+            TRY(alloc(s, &sa, nl * Td));
+            TRY(alloc(s, &so, nl * Td));
+            TRY(alloc(s, &sc, nl * Td));
+            TRY(alloc(s, &sg, nl * TF));
+        }
+        for (size_t l = 0; l < nl; ++l) {
+            Act& A = sl.layer[l];
             TRY(alloc(s, &A.x, Td));
-            TRY(alloc(s, &A.a, Td));
+            if (s->stacked) A.a = sa + l * Td;
+            else TRY(alloc(s, &A.a, Td));
             TRY(alloc(s, &A.qkv, 3 * Td));
             TRY(alloc(s, &A.P, BHLL));
-            TRY(alloc(s, &A.o, Td));
+            if (s->stacked) A.o = so + l * Td;
+            else TRY(alloc(s, &A.o, Td));
             TRY(alloc(s, &A.h, Td));
-            TRY(alloc(s, &A.c, Td));
+            if (s->stacked) A.c = sc + l * Td;
+            else TRY(alloc(s, &A.c, Td));
             TRY(alloc(s, &A.u, TF));
-            TRY(alloc(s, &A.g, TF));
+            if (s->stacked) A.g = sg + l * TF;
+            else TRY(alloc(s, &A.g, TF));
             TRY(alloc(s, &A.mu1, T));
             TRY(alloc(s, &A.rs1, T));
             TRY(alloc(s, &A.mu2, T));
@@ -940,10 +958,20 @@ int swarm_stage_enable_wgrad_pairing_sets(swarm_stage_t s, int n_sets) {
     if (!s->stash.empty()) return static_cast<int>(s->stash.size()) >= n_sets
                                       ? SWARM_OK
                                       : fail("enable_wgrad_pairing: already enabled with fewer sets");
-    const size_t T = s->T, d = s->d, F = s->F;
+    const size_t T = s->T, d = s->d, F = s->F, nl = static_cast<size_t>(s->cfg.n_layers);
     s->stash.resize(n_sets);
     for (auto& set : s->stash) {
-        set.resize(s->cfg.n_layers);
+        set.resize(nl);
+        if (s->stacked) {  // application order, contiguous: the stacked GEMMs read each as one K = n*T operand
+            bf16 *dy, *du, *dh, *dq;
+            TRY(alloc(s, &dy, nl * T * d));
+            TRY(alloc(s, &du, nl * T * F));
+            TRY(alloc(s, &dh, nl * T * d));
+            TRY(alloc(s, &dq, nl * 3 * T * d));
+            for (size_t l = 0; l < nl; ++l)
+                set[l] = Stash{dy + l * T * d, du + l * T * F, dh + l * T * d, dq + l * 3 * T * d};
+            continue;
+        }
         for (Stash& x : set) {
             TRY(alloc(s, &x.dy, T * d));
             TRY(alloc(s, &x.du, T * F));
@@ -954,6 +982,34 @@ int swarm_stage_enable_wgrad_pairing_sets(swarm_stage_t s, int n_sets) {
     return SWARM_OK;
 }
 
+namespace {
+// Layer-shared stage: the shared weights' gradients over every application of a
+// visit (or of a pending visit and this one) as one GEMM per weight, dW += sum_l
+// dY_l^T X_l with K = n_layers * T (2 n_layers T for a pair), reading the stacked
+// activations and stash.  Replaces n_layers K = T GEMMs that each read and wrote
+// the whole fp32 gradient of the weight (configs[3]: 16 x 268 MB per FFN weight).
+int stacked_wgrad(swarm_stage* s, const Slot& cur, const std::vector<Stash>& cs, const Slot* prev,
+                  const std::vector<Stash>* ps, cudaStream_t sd) {
+    const int d = s->d, F = s->F, nT = s->cfg.n_layers * s->T;
+    float* G = s->grad;
+    const LayerW& W = weights(s, 0);
+    auto one = [&](int M, int N, int ldy, const bf16* dy, const bf16* pdy, int ldx, const bf16* x, const bf16* px,
+                   size_t off, int ldo) {
+        if (!prev) return mm(M, N, nT, {dy, ldy, nT, ldy, true}, {x, ldx, nT, ldx, true}, G + off, ldo,
+                             SWARM_EPI_ACCUM_F32, nullptr, 1.f, sd);
+        return mm2(M, N, 2 * nT, {pdy, ldy, nT, ldy, true}, {px, ldx, nT, ldx, true}, dy, x, G + off, ldo, sd);
+    };
+    const Act& A = cur.layer[0];
+    const Act* P = prev ? &prev->layer[0] : nullptr;
+    const Stash& c0 = cs[0];
+    const Stash* p0 = ps ? &(*ps)[0] : nullptr;
+    TRY(one(d, F, d, c0.dy, p0 ? p0->dy : nullptr, F, A.g, P ? P->g : nullptr, W.w2, F));
+    TRY(one(F, d, F, c0.du, p0 ? p0->du : nullptr, d, A.c, P ? P->c : nullptr, W.w1, d));
+    TRY(one(d, d, d, c0.dhid, p0 ? p0->dhid : nullptr, d, A.o, P ? P->o : nullptr, W.wo, d));
+    return one(3 * d, d, 3 * d, c0.dqkv, p0 ? p0->dqkv : nullptr, d, A.a, P ? P->a : nullptr, W.wqkv, d);
+}
+}  // namespace
+
 int swarm_stage_flush_wgrad(swarm_stage_t s, int slot, int set, swarm_stream_t stream) {
     if (s->stash.empty()) return fail("flush_wgrad: pairing not enabled");
     if (slot < 0 || slot >= static_cast<int>(s->slots.size()) || set < 0 || set >= static_cast<int>(s->stash.size()))
@@ -962,6 +1018,7 @@ int swarm_stage_flush_wgrad(swarm_stage_t s, int slot, int set, swarm_stream_t s
     ProfScope prof(s);
     const int T = s->T, d = s->d, F = s->F, n = s->cfg.n_layers;
     float* G = s->grad;
+    if (s->stacked) return stacked_wgrad(s, s->slots[slot], s->stash[set], nullptr, nullptr, st);
     for (int l = 0; l < n; ++l) {
         const Act& A = s->slots[slot].layer[l];
         const Stash& x = s->stash[set][l];
@@ -1023,13 +1080,18 @@ int swarm_stage_backward_ex(swarm_stage_t s, int slot, const void* grad_in, void
         // layer 0's output gradient goes to the workspace the tail below consumes
         for (int l = n - 1; l >= 0; --l) {
             WgradPlan wp;
-            wp.mode = wgrad_mode;
-            if (wgrad_mode == SWARM_WGRAD_PAIR) {
+            wp.mode = s->stacked ? SWARM_WGRAD_DEFER : wgrad_mode;  // stacked: all applications at once, below
+            if (wp.mode == SWARM_WGRAD_PAIR) {
                 wp.prev = &s->slots[prev_slot].layer[l];
                 wp.ps = &s->stash[prev_set][l];
             }
             bf16* dx = l > 0 ? s->stash[set][l - 1].dy : s->gy[0];
             TRY(block_backward(s, sl.layer[l], s->stash[set][l].dy, dx, weights(s, l), st, wp, &s->stash[set][l]));
+        }
+        if (s->stacked && wgrad_mode == SWARM_WGRAD_PAIR) {
+            TRY(fork_side(s, st, 0));
+            TRY(stacked_wgrad(s, sl, s->stash[set], &s->slots[prev_slot], &s->stash[prev_set], side_of(s, st)));
+            TRY(join_side(s, st));
         }
         cur = 0;
     }

@@ -231,11 +231,13 @@ def test_two_stage_maxout_bottleneck(cuda):
         assert rel(grad_of(s0, name, r), P0[name].grad) <= GRAD_TOL_MAXOUT_UPSTREAM, name
 
 
-@pytest.mark.parametrize("shape", [dict(), dict(d_model=512, n_heads=4, d_ffn=2048, seq_len=256, micro_batch=2)])
+@pytest.mark.parametrize("shape", [dict(), dict(d_model=512, n_heads=4, d_ffn=2048, seq_len=256, micro_batch=2),
+                                   dict(shared_layers=1), dict(shared_layers=1, n_layers=4)])
 def test_paired_weight_gradients_match_per_microbatch(cuda, shape):
     """Deferring a visit's weight gradients and issuing them paired with the next
     visit's (two-segment K GEMMs), or alone via flush_wgrad, accumulates the same
-    gradients as per-visit weight gradients (fp32 summation order only)."""
+    gradients as per-visit weight gradients (fp32 summation order only).  Layer-
+    shared stages take the stacked path (one K = n_layers * T GEMM per shared weight)."""
     import torch
     from paper_2301_11913_b200.stage import Stage
     g = torch.Generator().manual_seed(11)
