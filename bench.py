@@ -694,8 +694,22 @@ def bench_engine(args, world, rank, local):
     S, M = args.stages, args.microbatches
     P = Placement(world, S).P
     bm = 2.0
+    # tick period: M microbatch completions of the engine's own schedule (its virtual
+    # completion rate for this layout, from a throwaway run without ticks), so every
+    # stage takes one optimizer step per M microbatches = 65,536 tokens, as the
+    # synchronous step does
+    from paper_2301_11913_b200.engine import Engine, EngineConfig
+    pl = Placement(world, S)
+    horizon = 400.0 * M * (1.0 + bm) / P
+    cal = Engine(EngineConfig(n_stages=S, initial_peers=[[1.0] * pl.layout[s] for s in range(S)],
+                              forward_service_seconds=1.0, backward_multiplier=bm,
+                              trainers_per_peer=args.trainers_per_peer, duration_seconds=horizon,
+                              bucket_seconds=horizon / 8), seed=1)
+    while cal.next(4096):
+        pass
+    period = M * horizon / max(cal.summary()["completed"], 1)
     ex = EngineExecutor(mcfg, S, trainers_per_peer=args.trainers_per_peer, seed=1, lr=1e-4, forward_seconds=1.0,
-                        backward_multiplier=bm, allreduce_period=M * (1.0 + bm) / P, allreduce_stall=0.05,
+                        backward_multiplier=bm, allreduce_period=period, allreduce_stall=0.05,
                         stream_per_peer=not args.single_stream)
     stream = torch.cuda.current_stream()
     # untimed warm-up: W steps plus two more, so that the visit graphs of most
@@ -716,6 +730,7 @@ def bench_engine(args, world, rank, local):
     t0.record(stream)
     ex.fork()
     done = ex.run(M * args.steps)
+    v1, r1, t_1, c1 = ex.engine.summary()["now"], ex.records, ex.optimizer_steps, ex.captures
     ex.finish()
     t1.record(stream)
     torch.cuda.synchronize()
@@ -762,15 +777,14 @@ def bench_engine(args, world, rank, local):
                                 "of int8 wire messages, stage all-reduce + AdamW at every AllReduceTick",
                    "trainers": ex.T, "trainers_per_peer": args.trainers_per_peer,
                    "schedule": "forward 1.0 / backward 2.0 virtual s, AllReduceTick every "
-                               f"{M * (1.0 + bm) / P:g} virtual s (~{M} microbatches per stage); one step = {M} "
-                               "microbatch completions",
+                               f"{period:.4g} virtual s (= {M} completions at the schedule's own rate: one optimizer "
+                               f"step per stage per {M} microbatches); one step = {M} microbatch completions",
                    "optimizer": "AdamW (fused, fp32 master), paired weight gradients",
                    "mean_loss": float(loss.item()) / max(tokens, 1),
                    "model_tflops_per_s": value * mcfg.flops_per_token(S) / 1e12,
                    "l2": "per-step working set far exceeds L2; no flush needed"},
-        "engine": {"records": ex.records - r0, "virtual_seconds": ex.engine.summary()["now"] - v0,
-                   "optimizer_steps_rank": ex.optimizer_steps - t_0, "microbatches": done,
-                   "graph_captures_in_timed_region_rank0": ex.captures - c0},
+        "engine": {"records": r1 - r0, "virtual_seconds": v1 - v0, "optimizer_steps_rank": t_1 - t_0,
+                   "microbatches": done, "graph_captures_in_timed_region_rank0": c1 - c0},
         "e2e": {"value": e2e_done * mcfg.tokens / e2e_s, "unit": "tokens/s",
                 "h2d_bytes_per_step": int(M * mcfg.tokens * 4 * 2),
                 "d2h_bytes_per_step": 4, "path": "EngineExecutor.run with each microbatch's tokens / targets copied "
