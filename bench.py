@@ -957,15 +957,22 @@ def main():
             import torch
             gc.collect()
             torch.cuda.empty_cache()
-            line = bench_engine(args, world, rank, local)
+            try:
+                line = bench_engine(args, world, rank, local)
+            except Exception as e:  # keep the measured synchronous line rather than no line
+                line = dict(g)
+                line["engine_async_error"] = repr(e)[:400]
+                g = {}
             for k in ("roofline", "step_breakdown", "cost_model", "step_phases_ms", "cpu_baseline"):
                 if k in g:
                     line[k] = g[k]
-            line["roofline"]["note"] = ("measured on the synchronous step's profiled visits (same kernels, same "
-                                        "shapes): " + line["roofline"]["note"])
-            line["gpipe_sync"] = {k: g[k] for k in ("value", "ms_per_step", "steps", "e2e", "gpu_launches", "clocks")}
-            line["gpipe_sync"]["note"] = ("the same workload as one synchronous GPipe optimizer step over 32 "
-                                          "microbatches (bench.py --sync); paired weight gradients")
+            if g:
+                line["roofline"]["note"] = ("measured on the synchronous step's profiled visits (same kernels, same "
+                                            "shapes): " + line["roofline"]["note"])
+                line["gpipe_sync"] = {k: g[k] for k in ("value", "ms_per_step", "steps", "e2e", "gpu_launches",
+                                                        "clocks")}
+                line["gpipe_sync"]["note"] = ("the same workload as one synchronous GPipe optimizer step over 32 "
+                                              "microbatches (bench.py --sync); paired weight gradients")
             gc.collect()
             torch.cuda.empty_cache()
         if not args.no_codec:
