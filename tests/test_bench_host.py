@@ -1,0 +1,42 @@
+"""Host-side bench helpers (no GPU): the calibrated cost-model report, including
+the DES engine's asynchronous prediction, is well-formed and monotone in the GPU
+count; the engine's tick period calibration gives one tick per 32 completions."""
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+
+def test_cost_model_report_predictions():
+    import bench
+    from paper_2301_11913_b200.swarm import PRESETS
+    r = bench.cost_model_report(PRESETS["C"], 4, 32, 1, 0.78, None)
+    g = r["predicted_tokens_per_s"]
+    assert g["1"] < g["2"] < g["4"] < g["8"]
+    e = r["engine_predicted_tokens_per_s"]
+    assert 0 < e["4"] < e["8"]
+    # the LM-head stage bounds the asynchronous pipeline: below 4x the 1-GPU rate at 4 GPUs
+    assert e["4"] < 4 * g["1"]
+    assert abs(r["head_stage_ratio"] - (1 + 50304 * 2048 / (8 * PRESETS["C"].params_per_layer()))) < 1e-12
+
+
+def test_engine_tick_period_matches_completions():
+    from paper_2301_11913_b200.engine import ALLREDUCE, DONE, Engine, EngineConfig
+    M, horizon = 32, 400.0 * 32 * 3
+    cfg = dict(n_stages=4, initial_peers=[[1.0]] * 4, trainers_per_peer=2)
+    cal = Engine(EngineConfig(**cfg, duration_seconds=horizon, bucket_seconds=horizon / 8), 1)
+    while cal.next(4096):
+        pass
+    period = M * horizon / cal.summary()["completed"]
+    e = Engine(EngineConfig(**cfg, allreduce_period=period, allreduce_stall=0.01, duration_seconds=50 * period,
+                            bucket_seconds=period), 1)
+    done, per_tick = 0, []
+    for r in e.records():
+        if r.kind == DONE:
+            done += 1
+        elif r.kind == ALLREDUCE:
+            per_tick.append(done)
+            done = 0
+    steady = per_tick[5:]
+    assert steady and abs(sum(steady) / len(steady) - M) <= 2
