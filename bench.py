@@ -710,7 +710,7 @@ def bench_engine(args, world, rank, local):
     period = M * horizon / max(cal.summary()["completed"], 1)
     ex = EngineExecutor(mcfg, S, trainers_per_peer=args.trainers_per_peer, seed=1, lr=1e-4, forward_seconds=1.0,
                         backward_multiplier=bm, allreduce_period=period, allreduce_stall=0.05,
-                        stream_per_peer=not args.single_stream)
+                        stream_per_peer=not args.single_stream, lanes=args.lanes)
     stream = torch.cuda.current_stream()
     # untimed warm-up: W steps plus two more, so that the visit graphs of most
     # (peer, trainer pair) combinations are captured before the timed region
@@ -775,7 +775,7 @@ def bench_engine(args, world, rank, local):
                    "execution": "asynchronous SWARM: the reference DES engine's record order (csrc/engine.cpp, "
                                 "decision-identical to sim::run), one compute stream per peer, NCCL isend/irecv "
                                 "of int8 wire messages, stage all-reduce + AdamW at every AllReduceTick",
-                   "trainers": ex.T, "trainers_per_peer": args.trainers_per_peer,
+                   "trainers": ex.T, "trainers_per_peer": args.trainers_per_peer, "lanes_per_peer": args.lanes,
                    "schedule": "forward 1.0 / backward 2.0 virtual s, AllReduceTick every "
                                f"{period:.4g} virtual s (= {M} completions at the schedule's own rate: one optimizer "
                                f"step per stage per {M} microbatches); one step = {M} microbatch completions",
@@ -918,6 +918,7 @@ def main():
     ap.add_argument("--workload", default="train", choices=["train", "codec", "failure", "engine"])
     ap.add_argument("--trainers-per-peer", type=int, default=2, help="engine: trainers per peer (sim trainers_per_peer)")
     ap.add_argument("--single-stream", action="store_true", help="engine: one compute stream per GPU (not per peer)")
+    ap.add_argument("--lanes", type=int, default=1, help="engine: visits a peer may serve concurrently (streams)")
     ap.add_argument("--model", default="C", choices=["C", "D", "tiny"])
     ap.add_argument("--microbatches", type=int, default=TRAIN_MICROBATCHES)
     ap.add_argument("--micro-batch", type=int, default=None, help="sequences per microbatch (default: the preset's)")

@@ -299,6 +299,14 @@ int swarm_stage_enable_wgrad_pairing(swarm_stage_t st);
  * engine-driven executor keeps one per trainer so a deferred visit's dY survives
  * other trainers' visits */
 int swarm_stage_enable_wgrad_pairing_sets(swarm_stage_t st, int n_sets);
+/* Lanes: n sets of visit workspaces (+ side stream / events) so that n visits of
+ * one stage can be in flight on n streams; set_lane selects the set the next
+ * visit call uses.  Visits on different lanes must use different slots; their
+ * gradient accumulation (TMA reduce-add GEMM epilogues, atomic LayerNorm and
+ * embedding gradients) is safe concurrently.  The caller orders visits that
+ * share a slot or a stash set. */
+int swarm_stage_enable_lanes(swarm_stage_t st, int n);
+int swarm_stage_set_lane(swarm_stage_t st, int lane);
 int swarm_stage_backward_ex(swarm_stage_t st, int slot, const void* grad_in, void* grad_out, int wgrad_mode, int set,
                             int prev_slot, int prev_set, swarm_stream_t stream);
 int swarm_stage_flush_wgrad(swarm_stage_t st, int slot, int set, swarm_stream_t stream);

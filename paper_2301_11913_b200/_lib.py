@@ -88,6 +88,8 @@ SIGNATURES = {
     "swarm_stage_enable_banks": (I, [P, P]),
     "swarm_stage_enable_wgrad_pairing": (I, [P]),
     "swarm_stage_enable_wgrad_pairing_sets": (I, [P, I]),
+    "swarm_stage_enable_lanes": (I, [P, I]),
+    "swarm_stage_set_lane": (I, [P, I]),
     "swarm_stage_backward_ex": (I, [P, I, P, P, I, I, I, I, P]),
     "swarm_stage_flush_wgrad": (I, [P, I, I, P]),
     "swarm_stage_set_bank": (I, [P, I]),

@@ -266,7 +266,10 @@ __global__ void k_col_reduce(const float* __restrict__ part, int nparts, int col
     if (c >= cols) return;
     float s = 0.f;
     for (int p = 0; p < nparts; ++p) s += part[static_cast<size_t>(p) * cols + c];
-    out[c] = accumulate ? out[c] + s : s;
+    // accumulate with an atomic add: one add per element per call (same value as a plain
+    // read-modify-write), but safe when two visits of a stage run concurrently (lanes)
+    if (accumulate) atomicAdd(out + c, s);
+    else out[c] = s;
 }
 
 // fp64 API path: one CTA per row, three passes over global, verbatim formula.
@@ -591,7 +594,10 @@ __global__ void __launch_bounds__(256) k_ln_bwd_dgb(const uint4* __restrict__ dy
         if (hsel == 0 && gcol < cols) {
             float* out = isg ? dg : db;
             const float t = red[o] + red[128 + o];
-            if (out) out[gcol] = accumulate ? out[gcol] + t : t;
+            if (out) {
+                if (accumulate) atomicAdd(out + gcol, t);  // see k_col_reduce
+                else out[gcol] = t;
+            }
         }
     }
     if (threadIdx.x == 0) strip_count[blockIdx.x] = 0;  // ready for the next launch

@@ -57,6 +57,20 @@ struct Slot {
     float *mud, *rsd;
 };
 
+// One visit's workspaces (+ its side stream and fork/join events).  A stage
+// keeps the active set in its fields; with lanes, set_lane swaps another set in,
+// so two visits of the stage can be in flight on two streams.
+struct Work {
+    float *S = nullptr, *dP = nullptr, *logits = nullptr;
+    bf16 *dS = nullptr, *gy[2] = {nullptr, nullptr}, *dhid = nullptr, *dc = nullptr, *du = nullptr,
+         *dqkv = nullptr, *dO = nullptr, *da = nullptr, *dlogits = nullptr, *wtmp = nullptr;
+    void* lnws = nullptr;
+    cudaStream_t side = nullptr;
+    void* skws[2] = {nullptr, nullptr};
+    cudaEvent_t ev_fork[7] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
+    cudaEvent_t ev_join = nullptr, ev_dq = nullptr;
+};
+
 }  // namespace
 
 struct swarm_stage {
@@ -104,6 +118,8 @@ struct swarm_stage {
     cudaEvent_t ev_fork[7] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
     cudaEvent_t ev_join = nullptr;
     cudaEvent_t ev_dq = nullptr;  // dQ (side stream) complete
+    std::vector<Work> lanes;      // all workspace sets when lanes are enabled (lanes[lane] is stale while active)
+    int lane = 0;
     // visit profiling (bench.py's live roofline and step breakdown): event pairs
     // around each GEMM (category 0) and each other kernel call of a profiled visit
     bool prof_on = false;
@@ -731,6 +747,58 @@ int create(const swarm_stage_config* c, swarm_stage* s) {
 
 }  // namespace
 
+namespace {
+#define SWARM_WORK_FIELDS(X) X(S) X(dP) X(logits) X(dS) X(dhid) X(dc) X(du) X(dqkv) X(dO) X(da) X(dlogits) X(wtmp) \
+    X(lnws) X(side) X(ev_join) X(ev_dq)
+void work_save(const swarm_stage* s, Work& w) {
+#define X(f) w.f = s->f;
+    SWARM_WORK_FIELDS(X)
+#undef X
+    for (int i = 0; i < 2; ++i) w.gy[i] = s->gy[i], w.skws[i] = s->skws[i];
+    for (int i = 0; i < 7; ++i) w.ev_fork[i] = s->ev_fork[i];
+}
+void work_load(swarm_stage* s, const Work& w) {
+#define X(f) s->f = w.f;
+    SWARM_WORK_FIELDS(X)
+#undef X
+    for (int i = 0; i < 2; ++i) s->gy[i] = w.gy[i], s->skws[i] = w.skws[i];
+    for (int i = 0; i < 7; ++i) s->ev_fork[i] = w.ev_fork[i];
+}
+// a second (third, ...) workspace set, sized as create() sizes the first
+int work_alloc(swarm_stage* s, Work& w) {
+    const size_t T = s->T, d = s->d, Td = T * d, TF = T * s->F, BHLL = static_cast<size_t>(s->B) * s->H * s->L * s->L;
+    if (!s->fused_attn) {
+        TRY(alloc(s, &w.S, BHLL));
+        TRY(alloc(s, &w.dP, BHLL));
+    }
+    TRY(alloc(s, &w.dS, BHLL));
+    TRY(alloc(s, &w.gy[0], Td));
+    TRY(alloc(s, &w.gy[1], Td));
+    TRY(alloc(s, &w.dhid, Td));
+    TRY(alloc(s, &w.dc, Td));
+    TRY(alloc(s, &w.du, TF));
+    TRY(alloc(s, &w.dqkv, 3 * Td));
+    TRY(alloc(s, &w.dO, Td));
+    TRY(alloc(s, &w.da, Td));
+    TRY(alloc(s, &w.wtmp, T * s->wire_w));
+    TRY(dmalloc(s, &w.lnws, swarm_layer_norm_backward_workspace(T, d)));
+    if (s->cfg.is_last) {
+        TRY(alloc(s, &w.logits, T * s->V));
+        TRY(alloc(s, &w.dlogits, T * s->V));
+    }
+    if (cudaStreamCreateWithFlags(&w.side, cudaStreamNonBlocking) != cudaSuccess) return SWARM_E_CUDA;
+    for (void*& x : w.skws) {
+        TRY(dmalloc(s, &x, swarm_gemm_workspace_bytes()));
+        if (cudaMemset(x, 0, swarm_gemm_workspace_bytes()) != cudaSuccess) return SWARM_E_CUDA;
+    }
+    for (auto& e : w.ev_fork)
+        if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) return SWARM_E_CUDA;
+    if (cudaEventCreateWithFlags(&w.ev_join, cudaEventDisableTiming) != cudaSuccess) return SWARM_E_CUDA;
+    if (cudaEventCreateWithFlags(&w.ev_dq, cudaEventDisableTiming) != cudaSuccess) return SWARM_E_CUDA;
+    return cudaDeviceSynchronize() == cudaSuccess ? SWARM_OK : SWARM_E_CUDA;
+}
+}  // namespace
+
 extern "C" {
 
 int swarm_stage_create(const swarm_stage_config* cfg, swarm_stage_t* out) {
@@ -750,11 +818,15 @@ void swarm_stage_destroy(swarm_stage_t s) {
     if (!s) return;
     cudaDeviceSynchronize();
     for (cudaEvent_t e : s->prof_events) cudaEventDestroy(e);
-    for (cudaEvent_t e : s->ev_fork)
-        if (e) cudaEventDestroy(e);
-    if (s->ev_join) cudaEventDestroy(s->ev_join);
-    if (s->ev_dq) cudaEventDestroy(s->ev_dq);
-    if (s->side) cudaStreamDestroy(s->side);
+    if (!s->lanes.empty()) work_save(s, s->lanes[s->lane]);
+    else s->lanes.resize(1), work_save(s, s->lanes[0]);
+    for (Work& w : s->lanes) {
+        for (cudaEvent_t e : w.ev_fork)
+            if (e) cudaEventDestroy(e);
+        if (w.ev_join) cudaEventDestroy(w.ev_join);
+        if (w.ev_dq) cudaEventDestroy(w.ev_dq);
+        if (w.side) cudaStreamDestroy(w.side);
+    }
     for (void* p : s->allocations) cudaFree(p);
     delete s;
 }
@@ -945,6 +1017,28 @@ int swarm_stage_forward(swarm_stage_t s, int slot, const void* in, const int32_t
     TRY(mm(T, d, s->V, {s->dlogits, s->V, T, s->V, false}, {s->p16 + s->head, d, s->V, d, true}, sl.dxf, d,
            SWARM_EPI_STORE_BF16, nullptr, 1.f, st));
     return join_side(s, st);
+}
+
+int swarm_stage_enable_lanes(swarm_stage_t s, int n) {
+    if (!s || n < 1) return fail("enable_lanes: need at least one lane");
+    if (!s->lanes.empty()) return static_cast<int>(s->lanes.size()) >= n ? SWARM_OK : fail("enable_lanes: already enabled");
+    if (n == 1) return SWARM_OK;
+    s->lanes.resize(n);
+    work_save(s, s->lanes[0]);
+    for (int i = 1; i < n; ++i) TRY(work_alloc(s, s->lanes[i]));
+    s->lane = 0;
+    return SWARM_OK;
+}
+
+int swarm_stage_set_lane(swarm_stage_t s, int lane) {
+    if (!s) return fail("set_lane: null stage");
+    if (s->lanes.empty()) return lane == 0 ? SWARM_OK : fail("set_lane: lanes not enabled");
+    if (lane < 0 || lane >= static_cast<int>(s->lanes.size())) return fail("set_lane: bad lane");
+    if (lane == s->lane) return SWARM_OK;
+    work_save(s, s->lanes[s->lane]);
+    work_load(s, s->lanes[lane]);
+    s->lane = lane;
+    return SWARM_OK;
 }
 
 int swarm_stage_backward(swarm_stage_t s, int slot, const void* grad_in, void* grad_out, swarm_stream_t stream) {

@@ -76,7 +76,7 @@ class EngineExecutor:
                  backward_multiplier: float = 2.0, allreduce_period: float = 0.0, allreduce_stall: float = 0.0,
                  duration_seconds: float = 1e9, use_graphs: bool = True, n_pool: int = 16,
                  tokens: torch.Tensor | None = None, targets: torch.Tensor | None = None, pair_wgrad: bool = True,
-                 stream_per_peer: bool = True):
+                 stream_per_peer: bool = True, lanes: int = 1):
         self.m = mcfg
         self.S = n_stages
         self.seed = seed
@@ -105,6 +105,8 @@ class EngineExecutor:
             self.stages[pid] = Stage(cfg, self.device)
             if pair_wgrad:
                 self.stages[pid].enable_wgrad_pairing(max(2, self.T))  # stash set = trainer id
+            if lanes > 1:
+                self.stages[pid].enable_lanes(lanes)
         # paired weight gradients (K = 2T GEMMs over two backward visits of a peer):
         # peer -> trainer whose backward visit deferred its weight gradients
         self.pair_wgrad = pair_wgrad
@@ -136,7 +138,16 @@ class EngineExecutor:
         # independently, as the engine models them, and their kernels fill each
         # other's idle SMs; cross-peer hazards are ordered by events (_done, _read)
         cur = torch.cuda.current_stream()
-        self.ws = {pid: (torch.cuda.Stream(device=self.device) if stream_per_peer else cur) for pid in self.local}
+        if lanes > 1 and not stream_per_peer:
+            raise ValueError("lanes need a stream per peer")
+        # lanes > 1: a peer serves up to `lanes` visits at once, each on its own stream and
+        # workspace set (round-robin); visits sharing a slot are ordered by _slot_ev
+        self.lanes = lanes
+        self.lane_ws = {pid: [torch.cuda.Stream(device=self.device) if stream_per_peer else cur
+                              for _ in range(lanes)] for pid in self.local}
+        self.ws = {pid: ls[0] for pid, ls in self.lane_ws.items()}
+        self._rr = {pid: 0 for pid in self.local}
+        self._slot_ev: dict = {}   # (peer, slot) -> event after the slot's last visit / flush
         self._done: dict = {}      # buffer key -> event after its local producing visit
         self._recv: dict = {}      # buffer key -> pending irecv work (the consumer waits on it)
         self._send: dict = {}      # buffer key -> pending isend work (the next writer waits on it)
@@ -218,11 +229,34 @@ class EngineExecutor:
             self._transfer(self._xfer.pop(key))  # both ranks of a cross-rank hop, at the same record
         if pid not in self.stages:
             return
+        lane = self._rr[pid]
+        self._rr[pid] = (lane + 1) % self.lanes
+        self.ws[pid] = self.lane_ws[pid][lane]
+        if self.lanes > 1:
+            self.stages[pid].set_lane(lane)
         with torch.cuda.stream(self.ws[pid]):
-            self._visit(r, s, t, pid, bwd)
+            if self.lanes > 1:
+                self._after_slot(pid, t)  # this slot's previous visit (e.g. the last stage's forward)
+            paired = self._visit(r, s, t, pid, bwd)
+            if self.lanes > 1:
+                self._mark_slot(pid, t)
+                if paired is not None:  # the pair read that slot's activations and stash: its next use waits
+                    self._slot_ev[(pid, paired)] = self._slot_ev[(pid, t)]
         self.visits_local += 1
 
-    def _visit(self, r, s, t, pid, bwd) -> None:
+    def _after_slot(self, pid: int, t: int) -> None:
+        ev = self._slot_ev.get((pid, t))
+        if ev is not None:
+            torch.cuda.current_stream().wait_event(ev)
+
+    def _mark_slot(self, pid: int, t: int) -> None:
+        ev = torch.cuda.Event()
+        ev.record(torch.cuda.current_stream())
+        self._slot_ev[(pid, t)] = ev
+
+    def _visit(self, r, s, t, pid, bwd):
+        """Issue one visit on the current stream; returns the slot it paired with, if any."""
+        paired = None
         st = self.stages[pid]
         cur = torch.cuda.current_stream()
         inkey = self._buf(t, s, bwd)
@@ -252,19 +286,22 @@ class EngineExecutor:
             out = None if outkey is None else self._tensor(outkey)
             tg = self.tgt[t] if s == self.S - 1 else None
             scale = 1.0 / self.m.tokens
-            self._replay((pid, "f", t), lambda: st.forward(t, inp, out=out, targets=tg, loss_sum=self.loss_sum,
+            self._replay((pid, "f", t, self._lane(pid)), lambda: st.forward(t, inp, out=out, targets=tg, loss_sum=self.loss_sum,
                                                            loss_scale=scale))
         else:
             gin = None if inkey is None else self._tensor(inkey)
             gout = None if outkey is None else self._tensor(outkey)
             if not self.pair_wgrad:
-                self._replay((pid, "b", t), lambda: st.backward(t, grad_in=gin, grad_out=gout))
+                self._replay((pid, "b", t, self._lane(pid)), lambda: st.backward(t, grad_in=gin, grad_out=gout))
             elif pid not in self._pend:  # first of a pair: data gradients now, dY kept in stash set t
-                self._replay((pid, "b", t, -1), lambda: st.backward_ex(t, gin, gout, mode=Stage.WGRAD_DEFER, set=t))
+                self._replay((pid, "b", t, -1, self._lane(pid)), lambda: st.backward_ex(t, gin, gout, mode=Stage.WGRAD_DEFER, set=t))
                 self._pend[pid] = t
             else:                        # second: both visits' weight gradients as K = 2T GEMMs
                 p = self._pend.pop(pid)
-                self._replay((pid, "b", t, p), lambda: st.backward_ex(t, gin, gout, mode=Stage.WGRAD_PAIR, set=t,
+                paired = p
+                if self.lanes > 1:
+                    self._after_slot(pid, p)  # the deferred visit's dY stash is complete
+                self._replay((pid, "b", t, p, self._lane(pid)), lambda: st.backward_ex(t, gin, gout, mode=Stage.WGRAD_PAIR, set=t,
                                                                       prev_slot=p, prev_set=p))
         if inkey is not None:
             ev = torch.cuda.Event()
@@ -274,6 +311,7 @@ class EngineExecutor:
             ev = torch.cuda.Event()
             ev.record(cur)
             self._done[outkey] = ev
+        return paired
 
     def _hop(self, r) -> None:
         # same-rank hops need nothing: the consumer reads the producer's buffer in stream order.
@@ -299,15 +337,28 @@ class EngineExecutor:
                     self.recv_stream.wait_event(ev)  # the previous reader of this buffer is done
                 self._recv[key] = dist.irecv(self._tensor(key), peer)
 
+    def _lane(self, pid: int) -> int:
+        return self.lane_ws[pid].index(self.ws[pid]) if self.lanes > 1 else 0
+
     def _flush(self, pid: int) -> None:
-        """A peer's pending (deferred) weight gradients, alone."""
+        """A peer's pending (deferred) weight gradients, alone (on the peer's current lane)."""
         t = self._pend.pop(pid)
         st = self.stages[pid]
         with torch.cuda.stream(self.ws[pid]):
-            self._replay((pid, "w", t), lambda: st.flush_wgrad(t, t))
+            if self.lanes > 1:
+                st.set_lane(self._lane(pid))
+                self._after_slot(pid, t)
+            self._replay((pid, "w", t, self._lane(pid)), lambda: st.flush_wgrad(t, t))
+            if self.lanes > 1:
+                self._mark_slot(pid, t)
 
     def _allreduce(self, r) -> None:
         self.ticks += 1
+        if self.lanes > 1:  # the tick follows every visit on every lane of the peer: join onto lane 0
+            for pid, ls in self.lane_ws.items():
+                for w in ls[1:]:
+                    ls[0].wait_stream(w)
+                self.ws[pid] = ls[0]
         for pid in list(self._pend):
             self._flush(pid)
         for pid, st in self.stages.items():
@@ -320,6 +371,10 @@ class EngineExecutor:
                     dist.all_reduce(st.grads(), op=dist.ReduceOp.SUM, group=self.groups[s])
                 st.optimizer_step(grad_scale=1.0 / n)  # mean over the stage's microbatches since the last tick
             self.optimizer_steps += 1
+        if self.lanes > 1:  # every lane's next visit sees the updated weights
+            for pid, ls in self.lane_ws.items():
+                for w in ls[1:]:
+                    w.wait_stream(ls[0])
         self.served = [0] * self.S
 
     def run(self, n_microbatches: int) -> int:
@@ -358,18 +413,23 @@ class EngineExecutor:
             self.host_tok = self.host_tgt = None
 
     def last_stage_stream(self):
-        """The compute stream of this rank's last-stage peer (it owns loss_sum), or None."""
+        """A stream ordered after every lane of this rank's last-stage peer (it owns
+        loss_sum), or None."""
         for pid in self.local:
             if self.pl.stage_of_peer(pid) == self.S - 1:
-                return self.ws[pid]
+                ls = self.lane_ws[pid]
+                for w in ls[1:]:
+                    ls[0].wait_stream(w)
+                return ls[0]
         return None
 
     def fork(self) -> None:
         """Every peer stream waits for the current stream (start of a timed region)."""
         cur = torch.cuda.current_stream()
-        for w in self.ws.values():
-            if w != cur:
-                w.wait_stream(cur)
+        for ls in self.lane_ws.values():
+            for w in ls:
+                if w != cur:
+                    w.wait_stream(cur)
 
     def finish(self) -> None:
         """The current stream waits for every peer stream and outstanding transfer
@@ -379,9 +439,10 @@ class EngineExecutor:
             w.wait()
         self._send.clear()
         self._recv.clear()
-        for w in self.ws.values():
-            if w != cur:
-                cur.wait_stream(w)
+        for ls in self.lane_ws.values():
+            for w in ls:
+                if w != cur:
+                    cur.wait_stream(w)
 
     def kernels_launched(self) -> int:
         return L.lib().swarm_launch_count() - self.captured_kernels + self.replayed_kernels

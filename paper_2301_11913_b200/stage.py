@@ -137,6 +137,13 @@ class Stage:
     def sync_shadow(self, stream=None) -> None:
         L.check(self.lib.swarm_stage_sync_shadow(self.h, _stream(stream)), "stage_sync_shadow")
 
+    # -- lanes: several visits of this stage in flight on different streams ---
+    def enable_lanes(self, n: int) -> None:
+        L.check(self.lib.swarm_stage_enable_lanes(self.h, n), "stage_enable_lanes")
+
+    def set_lane(self, lane: int) -> None:
+        L.check(self.lib.swarm_stage_set_lane(self.h, lane), "stage_set_lane")
+
     # -- delayed parameter updates (two shadow / gradient banks) ---------------
     def enable_banks(self, stream=None) -> None:
         L.check(self.lib.swarm_stage_enable_banks(self.h, _stream(stream)), "stage_enable_banks")

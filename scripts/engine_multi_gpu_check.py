@@ -16,7 +16,8 @@ torch.cuda.set_device(local)
 dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 S = int(sys.argv[1]) if len(sys.argv) > 1 else 4
 tpp = int(sys.argv[2]) if len(sys.argv) > 2 else 2
-ex = EngineExecutor(PRESETS["tiny"], S, trainers_per_peer=tpp, seed=5, n_pool=5)
+lanes = int(sys.argv[3]) if len(sys.argv) > 3 else 1
+ex = EngineExecutor(PRESETS["tiny"], S, trainers_per_peer=tpp, seed=5, n_pool=5, lanes=lanes)
 ex.run(9)
 ex.finish()
 torch.cuda.synchronize()
@@ -31,7 +32,7 @@ for pid, st in ex.stages.items():
     print(f"rank {dist.get_rank()} peer {pid} stage {s}: rel {r:.3e} visits {ex.visits_local}", flush=True)
 # with ticks: trains (finite loss)
 ex2 = EngineExecutor(PRESETS["tiny"], S, trainers_per_peer=tpp, seed=3, lr=3e-3, n_pool=2, allreduce_period=12.0,
-                     allreduce_stall=0.1)
+                     allreduce_stall=0.1, lanes=lanes)
 ex2.run(40)
 ex2.finish()
 torch.cuda.synchronize()

@@ -12,15 +12,15 @@ def rel(a, b):
     return float((a - b).norm() / b.norm().clamp_min(1e-30))
 
 
-@pytest.mark.parametrize("streams", [True, False])
+@pytest.mark.parametrize("streams,lanes", [(True, 1), (False, 1), (True, 2)])
 @pytest.mark.parametrize("pair", [True, False])
 @pytest.mark.parametrize("S,tpp", [(4, 1), (2, 3), (3, 2)])
-def test_executor_gradients_match_sequential_visits(cuda, S, tpp, pair, streams):
+def test_executor_gradients_match_sequential_visits(cuda, S, tpp, pair, streams, lanes):
     import torch
     from paper_2301_11913_b200.executor import EngineExecutor, sequential_reference_grads
     from paper_2301_11913_b200.swarm import PRESETS
     ex = EngineExecutor(PRESETS["tiny"], S, trainers_per_peer=tpp, seed=5, n_pool=5, pair_wgrad=pair,
-                        stream_per_peer=streams)
+                        stream_per_peer=streams, lanes=lanes)
     assert ex.run(7) == 7
     ex.finish()
     torch.cuda.synchronize()
@@ -32,12 +32,13 @@ def test_executor_gradients_match_sequential_visits(cuda, S, tpp, pair, streams)
     assert torch.isfinite(ex.loss_sum).all()
 
 
-def test_executor_trains_with_allreduce_ticks(cuda):
+@pytest.mark.parametrize("lanes", [1, 2])
+def test_executor_trains_with_allreduce_ticks(cuda, lanes):
     import torch
     from paper_2301_11913_b200.executor import EngineExecutor
     from paper_2301_11913_b200.swarm import PRESETS
     ex = EngineExecutor(PRESETS["tiny"], 4, trainers_per_peer=2, seed=3, lr=3e-3, n_pool=2,
-                        forward_seconds=1.0, allreduce_period=12.0, allreduce_stall=0.1)
+                        forward_seconds=1.0, allreduce_period=12.0, allreduce_stall=0.1, lanes=lanes)
     curve = []
     for _ in range(8):
         ex.loss_sum.zero_()
