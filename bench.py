@@ -918,7 +918,10 @@ def main():
     ap.add_argument("--workload", default="train", choices=["train", "codec", "failure", "engine"])
     ap.add_argument("--trainers-per-peer", type=int, default=2, help="engine: trainers per peer (sim trainers_per_peer)")
     ap.add_argument("--single-stream", action="store_true", help="engine: one compute stream per GPU (not per peer)")
-    ap.add_argument("--lanes", type=int, default=1, help="engine: visits a peer may serve concurrently (streams)")
+    ap.add_argument("--lanes", type=int, default=None,
+                    help="engine: visits a peer may serve concurrently, each on its own stream and workspace set "
+                         "(default 2 on >= 2 GPUs: +3-5%% configs[2], +10%% configs[3]; 1 on one GPU, where the "
+                         "4 peers already share the GPU on 4 streams)")
     ap.add_argument("--model", default="C", choices=["C", "D", "tiny"])
     ap.add_argument("--microbatches", type=int, default=TRAIN_MICROBATCHES)
     ap.add_argument("--micro-batch", type=int, default=None, help="sequences per microbatch (default: the preset's)")
@@ -937,6 +940,8 @@ def main():
         args.warmup = {"train": 3, "failure": 3, "engine": 3}.get(args.workload, 10)
     args.warmup = max(args.warmup, 3)
     world, rank, local = dist_setup(args)
+    if args.lanes is None:
+        args.lanes = 2 if world >= 2 else 1
     if args.impl == "reference":
         line = run_reference(args, world, rank)
     elif args.workload == "codec":
