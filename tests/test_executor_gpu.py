@@ -48,3 +48,24 @@ def test_executor_trains_with_allreduce_ticks(cuda, lanes):
     assert ex.optimizer_steps > 0 and ex.ticks > 0
     assert all(c == c for c in curve)
     assert curve[-1] < curve[0] - 0.3, curve
+
+
+@pytest.mark.parametrize("lanes", [1, 2])
+def test_executor_maxout_shared_layers_with_lanes(cuda, lanes):
+    """configs[3]'s stage features on the tiny model: maxout bottleneck at the
+    boundaries and layer-shared blocks (stacked weight gradients), two lanes per
+    peer: gradients still equal the sequential replay."""
+    import dataclasses
+
+    import torch
+    from paper_2301_11913_b200.executor import EngineExecutor, sequential_reference_grads
+    from paper_2301_11913_b200.swarm import PRESETS
+    m = dataclasses.replace(PRESETS["tiny"], maxout_k=2, shared_layers=1, layers_per_stage=3)
+    ex = EngineExecutor(m, 3, trainers_per_peer=2, seed=7, n_pool=4, lanes=lanes)
+    assert ex.run(6) == 6
+    ex.finish()
+    ex.flush_wgrad()
+    torch.cuda.synchronize()
+    ref = sequential_reference_grads(ex)
+    for pid, st in ex.stages.items():
+        assert rel(st.grads(), ref[pid]) <= 1e-4, (pid, rel(st.grads(), ref[pid]))
