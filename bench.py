@@ -712,9 +712,11 @@ def bench_engine(args, world, rank, local):
                         backward_multiplier=bm, allreduce_period=period, allreduce_stall=0.05,
                         stream_per_peer=not args.single_stream, lanes=args.lanes)
     stream = torch.cuda.current_stream()
-    # untimed warm-up: W steps plus two more, so that the visit graphs of most
-    # (peer, trainer pair) combinations are captured before the timed region
-    ex.run(M * (args.warmup + 2))
+    # untimed warm-up: W steps plus two more (eight more with several peers per stage,
+    # whose routes mix trainer pairs more), so that the visit graphs of most (peer,
+    # trainer pair, lane) combinations are captured before the timed region (a capture
+    # inside it costs host time: 29 per rank measured -2.7% at 2 stages x 2 peers)
+    ex.run(M * (args.warmup + (8 if P > 1 else 2)))
     ex.finish()
     torch.cuda.synchronize()
     ex.loss_sum.zero_()
