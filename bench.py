@@ -8,7 +8,8 @@ Workloads (BASELINE.json):
          all 4 stages; 2 GPUs 2 stages each; 4 GPUs 4x1; 8 GPUs 4x2.
          Headline: asynchronous SWARM in the reference DES engine's record order
          (--workload engine; one step = 32 microbatch completions = 65,536 tokens,
-         stage all-reduce + AdamW every ~32 microbatches per stage); the
+         stage all-reduce + AdamW every 32 microbatches per stage; one stream per
+         peer, 2 lanes per peer on >= 2 GPUs); the
          synchronous GPipe step (one optimizer step over 32 microbatches; --sync
          makes it the headline) is measured first and reported as "gpipe_sync".
          The global batch is fixed, so "scaling" is "strong".
