@@ -167,6 +167,12 @@ typedef struct {
     size_t workspace_bytes;
 } swarm_gemm_args;
 int swarm_gemm_bf16(const swarm_gemm_args* args, swarm_stream_t stream);
+/* The same contraction with fp32 operands (SIMT FFMA, fp32 accumulate): the stage
+ * executor's fp32 arithmetic mode (swarm_stage_config.fp32; BASELINE configs[0] is
+ * specified fp32).  Every epilogue keeps its meaning with fp32 in place of bf16
+ * (STORE_BF16 stores fp32; R / U are fp32); ACCUM_F32 adds atomically.  No
+ * alignment requirement beyond fp32. */
+int swarm_gemm_f32(const swarm_gemm_args* args, swarm_stream_t stream);
 size_t swarm_gemm_workspace_bytes(void);
 /* resident 2-CTA clusters of the 256x256 pair kernel on the current device (its
    persistent grid size; below SMs / 2 when GPCs strand SMs); 4-CTA clusters
@@ -183,12 +189,22 @@ int swarm_embedding_forward(const int32_t* tokens, size_t n_tokens, const void* 
 /* dtable[tokens[t],:] += dout[t,:]  (fp32 accumulate) */
 int swarm_embedding_backward(const int32_t* tokens, size_t n_tokens, const void* dout, size_t vocab, size_t d,
                              float* dtable, swarm_stream_t stream);
+/* the same for dtype F32 | BF16 tables / activations (fp32 mode: the fp32 master is the table) */
+int swarm_embedding_forward_ex(const int32_t* tokens, size_t n_tokens, const void* table, size_t vocab, size_t d,
+                               void* out, int dtype, swarm_stream_t stream);
+int swarm_embedding_backward_ex(const int32_t* tokens, size_t n_tokens, const void* dout, size_t vocab, size_t d,
+                                float* dtable, int dtype, swarm_stream_t stream);
 /* P = softmax(S) row-wise over L columns (rows = batch*heads*L); causal masks
  * column j > (row % L).  S fp32 (already scaled), P bf16. */
 int swarm_attn_softmax_forward(const float* s, size_t rows, size_t L, int causal, void* p, swarm_stream_t stream);
 /* dS = scale * P * (dP - rowsum(P*dP)), bf16 */
 int swarm_attn_softmax_backward(const void* p, const float* dp, size_t rows, size_t L, float scale, void* ds,
                                 swarm_stream_t stream);
+/* the same with P / dS of dtype F32 | BF16 (fp32 mode: accurate expf) */
+int swarm_attn_softmax_forward_ex(const float* s, size_t rows, size_t L, int causal, void* p, int p_dtype,
+                                  swarm_stream_t stream);
+int swarm_attn_softmax_backward_ex(const void* p, const float* dp, size_t rows, size_t L, float scale, void* ds,
+                                   int dtype, swarm_stream_t stream);
 /* Fused attention scores (tcgen05; L % 128 == 0, L <= 1024, d_head % 64 == 0, d_head <= 128):
  *   P[z*L + i, j] = softmax_j(scale * q_z[i] . k_z[j])  (bf16 [B*H*L, L], causal masks j > i)
  * with q_z = q[b*L + i, h*d_head : (h+1)*d_head] for z = b*H + h (row stride ld, n_cols
@@ -209,6 +225,9 @@ int swarm_attn_scores_softmax_backward(const void* dO, int ld_do, const void* v,
  * dlogits (bf16, optional) = grad_scale * (softmax - onehot) */
 int swarm_cross_entropy(const float* logits, const int32_t* targets, size_t rows, size_t vocab, float grad_scale,
                         float* loss_sum, void* dlogits, swarm_stream_t stream);
+/* dlogits of dtype F32 | BF16 (F32: accurate expf, the fp32 mode) */
+int swarm_cross_entropy_ex(const float* logits, const int32_t* targets, size_t rows, size_t vocab, float grad_scale,
+                           float* loss_sum, void* dlogits, int dlogits_dtype, swarm_stream_t stream);
 /* fused AdamW over a flat fp32 arena; refreshes the bf16 shadow (p16, optional)
  * and zeroes the gradient when zero_grad != 0.  step >= 1 (bias correction). */
 int swarm_adamw_step(float* p32, void* p16, float* grad, float* m, float* v, size_t n, float lr, float beta1,
@@ -264,6 +283,10 @@ typedef struct {
                           maxout_k(LN(y)) (d/k wide), the receiver applies LN then W_d (d/k -> d) */
     float lr, beta1, beta2, eps, weight_decay, init_std;
     uint64_t seed;
+    int fp32;          /* 1: fp32 arithmetic mode — fp32 activations and wire tensors, fp32 GEMMs
+                          (swarm_gemm_f32) reading the fp32 master weights, unfused attention;
+                          0 (default): bf16 storage, tcgen05 bf16 GEMMs, fp32 accumulation.
+                          Delayed-update banks need the bf16 mode. */
 } swarm_stage_config;
 
 int swarm_stage_create(const swarm_stage_config* cfg, swarm_stage_t* out);
@@ -360,7 +383,10 @@ int swarm_stage_profile_read(swarm_stage_t st, double* gemm_ms, double* gemm_flo
 int swarm_gpu_spin(uint64_t ns, swarm_stream_t stream);
 void swarm_stage_profile_breakdown(swarm_stage_t st, double* ms /* [SWARM_PROF_CATEGORIES] */,
                                    uint64_t* launches /* [SWARM_PROF_CATEGORIES] */);
-/* saved activation of (slot, layer) by name ("x","a","qkv","P","o","h","c","u","g","xf","dxf"), for tests */
+/* saved activation of (slot, layer) by name ("x","a","qkv","P","o","h","c","u","g","xf","dxf"), for tests;
+ * also "wire_out" (the tensor the last forward of `slot` encoded), "wire_in" (the decoded input wire
+ * tensor) and "dx_last" (the input gradient the stage's last backward visit encoded).  Elements are
+ * bf16, or fp32 in the fp32 mode. */
 int swarm_stage_activation(swarm_stage_t st, int slot, int layer, const char* name, void** ptr, size_t* numel);
 
 /* ---- host control plane: stochastic wiring + rebalancing ------------------

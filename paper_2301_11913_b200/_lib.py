@@ -34,7 +34,7 @@ class StageConfigC(C.Structure):
                                        "shared_layers", "vocab", "is_first", "is_last", "causal", "max_slots", "wire",
                                        "block_size", "maxout_k")] + \
                [(n, C.c_float) for n in ("lr", "beta1", "beta2", "eps", "weight_decay", "init_std")] + \
-               [("seed", C.c_uint64)]
+               [("seed", C.c_uint64), ("fp32", C.c_int)]
 
 
 class EngineRecord(C.Structure):
@@ -62,6 +62,7 @@ SIGNATURES = {
     "swarm_layer_norm_backward": (I, [P, P, I, SZ, SZ, P, P, P, P, P, P, P, I, P, P]),
     "swarm_matvec_f64": (I, [P, SZ, P, SZ, P, P]),
     "swarm_gemm_bf16": (I, [C.POINTER(GemmArgs), P]),
+    "swarm_gemm_f32": (I, [C.POINTER(GemmArgs), P]),
     "swarm_gemm_workspace_bytes": (SZ, []),
     "swarm_gemm_pair_clusters": (I, []),
     "swarm_embedding_forward": (I, [P, SZ, P, SZ, SZ, P, P]),
@@ -69,6 +70,11 @@ SIGNATURES = {
     "swarm_attn_softmax_forward": (I, [P, SZ, SZ, I, P, P]),
     "swarm_attn_softmax_backward": (I, [P, P, SZ, SZ, F, P, P]),
     "swarm_cross_entropy": (I, [P, P, SZ, SZ, F, P, P, P]),
+    "swarm_cross_entropy_ex": (I, [P, P, SZ, SZ, F, P, P, I, P]),
+    "swarm_embedding_forward_ex": (I, [P, SZ, P, SZ, SZ, P, I, P]),
+    "swarm_embedding_backward_ex": (I, [P, SZ, P, SZ, SZ, P, I, P]),
+    "swarm_attn_softmax_forward_ex": (I, [P, SZ, SZ, I, P, I, P]),
+    "swarm_attn_softmax_backward_ex": (I, [P, P, SZ, SZ, F, P, I, P]),
     "swarm_attn_scores_softmax": (I, [P, P, I, I, I, I, I, I, F, I, P, P]),
     "swarm_attn_scores_softmax_backward": (I, [P, I, P, I, I, P, I, P, I, I, I, I, F, I, P, P]),
     "swarm_adamw_step": (I, [P, P, P, P, P, SZ, F, F, F, F, F, I, F, I, P]),

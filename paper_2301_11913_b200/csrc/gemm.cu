@@ -136,20 +136,19 @@ __device__ __forceinline__ void epilogue_chunk(const Params& p, float (&v)[32], 
             if (full) {
 #pragma unroll
                 for (int q = 0; q < 8; ++q) {
-                    float4 o = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
-                    if (p.epi == SWARM_EPI_ACCUM_F32) {
-                        const float4 c = reinterpret_cast<const float4*>(dst)[q];
-                        o.x += c.x;
-                        o.y += c.y;
-                        o.z += c.z;
-                        o.w += c.w;
-                    }
-                    reinterpret_cast<float4*>(dst)[q] = o;
+                    const float4 o = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+                    // accumulation is a vector atomic (red.global.add.v4.f32): two lanes of a stage
+                    // may accumulate into one gradient concurrently (swarm_stage_enable_lanes)
+                    if (p.epi == SWARM_EPI_ACCUM_F32) atomicAdd(reinterpret_cast<float4*>(dst) + q, o);
+                    else reinterpret_cast<float4*>(dst)[q] = o;
                 }
             } else {
 #pragma unroll
                 for (int j = 0; j < 32; ++j)
-                    if (j < ncols_valid) dst[j] = (p.epi == SWARM_EPI_ACCUM_F32) ? dst[j] + v[j] : v[j];
+                    if (j < ncols_valid) {
+                        if (p.epi == SWARM_EPI_ACCUM_F32) atomicAdd(dst + j, v[j]);
+                        else dst[j] = v[j];
+                    }
             }
             break;
         }

@@ -21,6 +21,19 @@ namespace {
 
 using bf16 = uint16_t;  // storage only; kernels interpret it
 
+// Element pointer into an activation buffer.  Its element is bf16 (2 B) or, in
+// the fp32 arithmetic mode (swarm_stage_config.fp32), fp32 (4 B); offsets are in
+// elements of the stage's dtype, so the visit code is the same in both modes.
+struct EP {
+    char* p = nullptr;
+    int es = 2;
+    EP() = default;
+    EP(std::nullptr_t) {}
+    EP(void* q, int e) : p(static_cast<char*>(q)), es(e) {}
+    EP operator+(size_t n) const { return p ? EP(p + n * es, es) : EP(); }
+    operator void*() const { return p; }
+};
+
 struct TensorInfo {
     std::string name;
     size_t off, rows, cols;
@@ -28,7 +41,7 @@ struct TensorInfo {
 
 // one layer's backward gradients that its weight gradients read (paired mode)
 struct Stash {
-    bf16 *dy = nullptr, *du = nullptr, *dhid = nullptr, *dqkv = nullptr;
+    EP dy, du, dhid, dqkv;
 };
 
 struct LayerW {
@@ -36,24 +49,24 @@ struct LayerW {
 };
 
 struct Act {
-    bf16 *x, *a, *qkv, *P, *o, *h, *c, *u, *g;
+    EP x, a, qkv, P, o, h, c, u, g;
     float *mu1, *rs1, *mu2, *rs2;
 };
 
 struct Slot {
     std::vector<Act> layer;  // n_layers entries; layer[l].x is the input of application l
-    bf16* out;               // output of the last application (input of the next stage / final LN)
-    bf16* xf;                // final LN output (last stage)
+    EP out;               // output of the last application (input of the next stage / final LN)
+    EP xf;                // final LN output (last stage)
     float *muf, *rsf;
-    bf16* dxf;               // d loss / d xf, produced by the fused LM-head backward
+    EP dxf;               // d loss / d xf, produced by the fused LM-head backward
     int32_t* tokens;         // first stage: the microbatch's token ids (embedding backward)
     // maxout bottleneck: sender keeps LN_c(out), its stats and the argmax;
     // receiver keeps the dequantized wire tensor, LN_d of it and its stats
-    bf16* z;
+    EP z;
     float *muc, *rsc;
-    bf16* mo;
+    EP mo;
     uint8_t* am;
-    bf16 *mi, *ni;
+    EP mi, ni;
     float *mud, *rsd;
 };
 
@@ -62,8 +75,7 @@ struct Slot {
 // so two visits of the stage can be in flight on two streams.
 struct Work {
     float *S = nullptr, *dP = nullptr, *logits = nullptr;
-    bf16 *dS = nullptr, *gy[2] = {nullptr, nullptr}, *dhid = nullptr, *dc = nullptr, *du = nullptr,
-         *dqkv = nullptr, *dO = nullptr, *da = nullptr, *dlogits = nullptr, *wtmp = nullptr;
+    EP dS, gy[2], dhid, dc, du, dqkv, dO, da, dlogits, wtmp;
     void* lnws = nullptr;
     cudaStream_t side = nullptr;
     void* skws[2] = {nullptr, nullptr};
@@ -80,6 +92,9 @@ struct swarm_stage {
     std::vector<TensorInfo> tensors;
     std::vector<LayerW> layers;
     size_t emb = 0, lnfg = 0, lnfb = 0, head = 0;
+    bool f32 = false;    // fp32 arithmetic mode (swarm_stage_config.fp32)
+    int es = 2;          // activation element size: 2 (bf16) or 4 (fp32)
+    int dt = SWARM_DTYPE_BF16;  // activation dtype passed to the kernels
     bool bneck = false;  // maxout bottleneck at the boundaries
     bool stacked = false;  // layer-shared: stacked weight-gradient inputs (one K = n_layers*T GEMM per weight)
     int wire_w = 0;      // features per token on the wire (d, or d / maxout_k)
@@ -105,8 +120,7 @@ struct swarm_stage {
     // workspaces (one visit at a time per stage)
     float *S = nullptr, *dP = nullptr, *logits = nullptr;
     void* wire_hdr = nullptr;  // device copy of this stage's swarm_wire_header
-    bf16 *dS = nullptr, *gy[2] = {nullptr, nullptr}, *dhid = nullptr, *dc = nullptr, *du = nullptr, *dqkv = nullptr,
-         *dO = nullptr, *da = nullptr, *dlogits = nullptr, *wtmp = nullptr;
+    EP dS, gy[2], dhid, dc, du, dqkv, dO, da, dlogits, wtmp;
     void* lnws = nullptr;
     std::vector<void*> allocations;
     int step = 0;
@@ -118,6 +132,7 @@ struct swarm_stage {
     cudaEvent_t ev_fork[7] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
     cudaEvent_t ev_join = nullptr;
     cudaEvent_t ev_dq = nullptr;  // dQ (side stream) complete
+    EP last_dx;                   // the input gradient the last backward visit encoded (tests: "dx_last")
     std::vector<Work> lanes;      // all workspace sets when lanes are enabled (lanes[lane] is stale while active)
     int lane = 0;
     // visit profiling (bench.py's live roofline and step breakdown): event pairs
@@ -170,6 +185,18 @@ int alloc(swarm_stage* s, T** p, size_t count) {
     *p = static_cast<T*>(q);
     return SWARM_OK;
 }
+
+// an activation buffer of `count` elements of the stage's dtype
+int alloc(swarm_stage* s, EP* p, size_t count) {
+    void* q = nullptr;
+    TRY(dmalloc(s, &q, count * s->es));
+    *p = EP(q, s->es);
+    return SWARM_OK;
+}
+
+// the weights the visit's GEMMs read: the bf16 shadow of the current bank, or the
+// fp32 master itself in the fp32 mode
+EP wts(const swarm_stage* s) { return s->f32 ? EP(s->p32, 4) : EP(s->p16, 2); }
 
 // fp32 LayerNorm parameter at arena offset `off` as the current visit must read it
 const float* ln_param(const swarm_stage* s, size_t off) {
@@ -253,10 +280,11 @@ int run_gemm(swarm_gemm_args g, cudaStream_t st) {
         g.workspace = t_cur->skws[st == t_cur->side ? 1 : 0];
         g.workspace_bytes = swarm_gemm_workspace_bytes();
     }
+    auto gemm = (t_cur && t_cur->f32) ? swarm_gemm_f32 : swarm_gemm_bf16;
     swarm_stage* s = t_prof;
-    if (!s) return swarm_gemm_bf16(&g, st);
+    if (!s) return gemm(&g, st);
     TRY(prof_begin(SWARM_PROF_GEMM, st));
-    const int rc = swarm_gemm_bf16(&g, st);
+    const int rc = gemm(&g, st);
     prof_end(st);
     s->prof_used -= 1;  // fill in the FLOPs of the pair just closed
     double kfrac = 1.0;  // executed share of K when a causal A lets the kernel skip zero k-blocks
@@ -397,10 +425,10 @@ int join_side(swarm_stage* s, cudaStream_t main) {
 }
 
 // ---------------------------------------------------------- block forward --
-int block_forward(swarm_stage* s, Act& A, bf16* y, const LayerW& W, cudaStream_t st) {
+int block_forward(swarm_stage* s, Act& A, EP y, const LayerW& W, cudaStream_t st) {
     const int T = s->T, d = s->d, H = s->H, dh = s->dh, F = s->F, L = s->L;
-    const bf16* p16 = s->p16;
-    PTRY(SWARM_PROF_LAYERNORM, st, swarm_layer_norm_forward(A.x, SWARM_DTYPE_BF16, T, d, ln_param(s, W.ln1g), ln_param(s, W.ln1b), 1e-5, A.a, A.mu1, A.rs1, st));
+    const EP p16 = wts(s);
+    PTRY(SWARM_PROF_LAYERNORM, st, swarm_layer_norm_forward(A.x, s->dt, T, d, ln_param(s, W.ln1g), ln_param(s, W.ln1b), 1e-5, A.a, A.mu1, A.rs1, st));
     TRY(mm(T, 3 * d, d, {A.a, d, T, d, false}, {p16 + W.wqkv, d, 3 * d, d, false}, A.qkv, 3 * d,
            SWARM_EPI_STORE_BF16, nullptr, 1.f, st));
     const float scale = 1.f / std::sqrt(static_cast<float>(dh));
@@ -412,14 +440,14 @@ int block_forward(swarm_stage* s, Act& A, bf16* y, const LayerW& W, cudaStream_t
         TRY(bmm(s, L, L, dh, {{A.qkv, 3 * d, T, d, false}, L, 0, 0, dh},
                 {{A.qkv + d, 3 * d, T, d, false}, L, 0, 0, dh}, s->S, L, H * L, L, 0, 0, SWARM_EPI_STORE_F32, scale,
                 st));
-        PTRY(SWARM_PROF_ATTENTION, st, swarm_attn_softmax_forward(s->S, static_cast<size_t>(s->B) * H * L, L, s->cfg.causal, A.P, st));
+        PTRY(SWARM_PROF_ATTENTION, st, swarm_attn_softmax_forward_ex(s->S, static_cast<size_t>(s->B) * H * L, L, s->cfg.causal, A.P, s->dt, st));
     }
     // O = P V  (V read MN-major straight from the qkv buffer)
     TRY(bmm(s, L, dh, L, {{A.P, L, s->B * H * L, L, false}, H * L, L, 0, 0},
             {{A.qkv + 2 * d, 3 * d, T, d, true}, L, 0, 0, dh}, A.o, d, L, 0, 0, dh, SWARM_EPI_STORE_BF16, 1.f, st, 1));
     // h = x + O Wo^T
     TRY(mm(T, d, d, {A.o, d, T, d, false}, {p16 + W.wo, d, d, d, false}, A.h, d, SWARM_EPI_RESIDUAL, A.x, 1.f, st));
-    PTRY(SWARM_PROF_LAYERNORM, st, swarm_layer_norm_forward(A.h, SWARM_DTYPE_BF16, T, d, ln_param(s, W.ln2g), ln_param(s, W.ln2b), 1e-5, A.c, A.mu2, A.rs2, st));
+    PTRY(SWARM_PROF_LAYERNORM, st, swarm_layer_norm_forward(A.h, s->dt, T, d, ln_param(s, W.ln2g), ln_param(s, W.ln2b), 1e-5, A.c, A.mu2, A.rs2, st));
     // u = c W1^T, g = gelu(u)
     TRY(mm(T, F, d, {A.c, d, T, d, false}, {p16 + W.w1, d, F, d, false}, A.g, F, SWARM_EPI_GELU, A.u, 1.f, st));
     // y = h + g W2^T
@@ -446,16 +474,37 @@ int wgrad(swarm_stage* s, const WgradPlan& wp, int M, int N, Op dy, Op x, Op dy_
     return mm2(M, N, 2 * T, dy_prev, x_prev, dy.p, x.p, out, ldo, sd);
 }
 
-int block_backward(swarm_stage* s, const Act& A, const bf16* dy, bf16* dx, const LayerW& W, cudaStream_t st,
+// LayerNorm backward of a block: dx = LN'(dy) + dres on the visit stream, the gain /
+// bias gradients (a second pass over dy and x, off the critical path) on the side
+// stream after fork `fork_i`.  The fp32 mode's generic kernel computes both in one
+// call on the visit stream.
+int ln_backward_split(swarm_stage* s, EP dy, EP x, const float* gain, const float* mu, const float* rs, EP dres,
+                      EP dx, float* dgain, float* dbias, cudaStream_t st, int fork_i) {
+    const int T = s->T, d = s->d;
+    if (s->f32) {
+        PTRY(SWARM_PROF_LAYERNORM, st, swarm_layer_norm_backward(dy, x, s->dt, T, d, gain, mu, rs, dres, dx, dgain, dbias,
+                                                                 1, s->lnws, st));
+        return SWARM_OK;
+    }
+    PTRY(SWARM_PROF_LAYERNORM, st, swarm_layer_norm_backward(dy, x, s->dt, T, d, gain, mu, rs, dres, dx, nullptr,
+                                                             nullptr, 1, s->lnws, st));
+    TRY(fork_side(s, st, fork_i));
+    cudaStream_t sd = side_of(s, st);
+    PTRY(SWARM_PROF_LAYERNORM, sd, swarm_layer_norm_backward(dy, x, s->dt, T, d, gain, mu, rs, nullptr, nullptr, dgain,
+                                                             dbias, 1, s->lnws, sd));
+    return SWARM_OK;
+}
+
+int block_backward(swarm_stage* s, const Act& A, EP dy, EP dx, const LayerW& W, cudaStream_t st,
                    const WgradPlan& wp = WgradPlan{}, const Stash* cs = nullptr) {
     const int T = s->T, d = s->d, H = s->H, dh = s->dh, F = s->F, L = s->L, BHL = s->B * s->H * s->L;
-    const bf16* p16 = s->p16;
+    const EP p16 = wts(s);
     float* G = s->grad;
     cudaStream_t sd = side_of(s, st);  // weight gradients
     // dY tensors the weight gradients read: per-visit workspaces, or this layer's stash
-    bf16* du = cs ? cs->du : s->du;
-    bf16* dhid = cs ? cs->dhid : s->dhid;
-    bf16* dqkv = cs ? cs->dqkv : s->dqkv;
+    EP du = cs ? cs->du : s->du;
+    EP dhid = cs ? cs->dhid : s->dhid;
+    EP dqkv = cs ? cs->dqkv : s->dqkv;
     const Act* PA = wp.prev;
     const Stash* ps = wp.ps;
     const bool pr = wp.mode == SWARM_WGRAD_PAIR;
@@ -471,11 +520,7 @@ int block_backward(swarm_stage* s, const Act& A, const bf16* dy, bf16* dx, const
            st));
     // dh = LN2'(dc) + dy on the visit stream; LN2's gain / bias gradients (a second pass
     // over dc and h, off the critical path) on the side stream
-    PTRY(SWARM_PROF_LAYERNORM, st, swarm_layer_norm_backward(s->dc, A.h, SWARM_DTYPE_BF16, T, d, ln_param(s, W.ln2g), A.mu2, A.rs2, dy, dhid,
-                                  nullptr, nullptr, 1, s->lnws, st));
-    TRY(fork_side(s, st, 5));
-    PTRY(SWARM_PROF_LAYERNORM, sd, swarm_layer_norm_backward(s->dc, A.h, SWARM_DTYPE_BF16, T, d, ln_param(s, W.ln2g), A.mu2, A.rs2, nullptr, nullptr,
-                                  G + W.ln2g, G + W.ln2b, 1, s->lnws, sd));
+    TRY(ln_backward_split(s, s->dc, A.h, ln_param(s, W.ln2g), A.mu2, A.rs2, dy, dhid, G + W.ln2g, G + W.ln2b, st, 5));
     // attention output projection
     TRY(fork_side(s, st, 2));
     TRY(wgrad(s, wp, d, d, {dhid, d, T, d, true}, {A.o, d, T, d, true}, {pr ? ps->dhid : nullptr, d, T, d, true},
@@ -491,7 +536,7 @@ int block_backward(swarm_stage* s, const Act& A, const bf16* dy, bf16* dx, const
         TRY(bmm(s, L, L, dh, {{s->dO, d, T, d, false}, L, 0, 0, dh},
                 {{A.qkv + 2 * d, 3 * d, T, d, false}, L, 0, 0, dh}, s->dP, L, H * L, L, 0, 0, SWARM_EPI_STORE_F32,
                 1.f, st));
-        PTRY(SWARM_PROF_ATTENTION, st, swarm_attn_softmax_backward(A.P, s->dP, BHL, L, scale, s->dS, st));
+        PTRY(SWARM_PROF_ATTENTION, st, swarm_attn_softmax_backward_ex(A.P, s->dP, BHL, L, scale, s->dS, s->dt, st));
     }
     // dQ = dS K ; dK = dS^T Q ; dV = P^T dO   (all read in place, written into dqkv); dQ runs on the
     // side stream beside dK, dV (three independent GEMMs of 1.7 waves each fill each other's tails)
@@ -511,11 +556,7 @@ int block_backward(swarm_stage* s, const Act& A, const bf16* dy, bf16* dx, const
     TRY(mm(T, d, 3 * d, {dqkv, 3 * d, T, 3 * d, false}, {p16 + W.wqkv, d, 3 * d, d, true}, s->da, d,
            SWARM_EPI_STORE_BF16, nullptr, 1.f, st));
     // dx = LN1'(da) + dh; LN1's gain / bias gradients on the side stream
-    PTRY(SWARM_PROF_LAYERNORM, st, swarm_layer_norm_backward(s->da, A.x, SWARM_DTYPE_BF16, T, d, ln_param(s, W.ln1g), A.mu1, A.rs1, dhid, dx,
-                                  nullptr, nullptr, 1, s->lnws, st));
-    TRY(fork_side(s, st, 6));
-    PTRY(SWARM_PROF_LAYERNORM, sd, swarm_layer_norm_backward(s->da, A.x, SWARM_DTYPE_BF16, T, d, ln_param(s, W.ln1g), A.mu1, A.rs1, nullptr, nullptr,
-                                  G + W.ln1g, G + W.ln1b, 1, s->lnws, sd));
+    TRY(ln_backward_split(s, s->da, A.x, ln_param(s, W.ln1g), A.mu1, A.rs1, dhid, dx, G + W.ln1g, G + W.ln1b, st, 6));
     // the next layer overwrites the workspaces the weight gradients read
     return join_side(s, st);
 }
@@ -528,24 +569,24 @@ size_t wire_payload_bytes(const swarm_stage* s) {
         const size_t bs = static_cast<size_t>(s->cfg.block_size);
         return ((n + 15) & ~size_t(15)) + (((n + bs - 1) / bs) * sizeof(float) + 15) / 16 * 16;
     }
-    return (n * 2 + 15) / 16 * 16;
+    return (n * s->es + 15) / 16 * 16;  // raw activations in the stage's dtype
 }
 
 size_t wire_bytes(const swarm_stage* s) { return wire_payload_bytes(s) + sizeof(swarm_wire_header); }
 
-int wire_decode(swarm_stage* s, const void* msg, bf16* out, cudaStream_t st) {
+int wire_decode(swarm_stage* s, const void* msg, EP out, cudaStream_t st) {
     const size_t n = static_cast<size_t>(s->T) * s->wire_w;
     if (s->cfg.wire == SWARM_WIRE_INT8) {
         const int8_t* codes = static_cast<const int8_t*>(msg);
         const void* scales = static_cast<const char*>(msg) + ((n + 15) & ~size_t(15));
-        return swarm_dequantize_blockwise(codes, scales, SWARM_DTYPE_F32, n, s->cfg.block_size, out, SWARM_DTYPE_BF16,
+        return swarm_dequantize_blockwise(codes, scales, SWARM_DTYPE_F32, n, s->cfg.block_size, out, s->dt,
                                           st);
     }
-    const cudaError_t e = cudaMemcpyAsync(out, msg, n * 2, cudaMemcpyDeviceToDevice, st);
+    const cudaError_t e = cudaMemcpyAsync(out, msg, n * s->es, cudaMemcpyDeviceToDevice, st);
     return e == cudaSuccess ? SWARM_OK : SWARM_E_CUDA;
 }
 
-int wire_encode(swarm_stage* s, const bf16* x, void* msg, cudaStream_t st) {
+int wire_encode(swarm_stage* s, EP x, void* msg, cudaStream_t st) {
     const size_t n = static_cast<size_t>(s->T) * s->wire_w;
     // header first (a 16-byte device-to-device copy of the stage's prebuilt header)
     if (cudaMemcpyAsync(static_cast<char*>(msg) + wire_payload_bytes(s), s->wire_hdr, sizeof(swarm_wire_header),
@@ -554,9 +595,9 @@ int wire_encode(swarm_stage* s, const bf16* x, void* msg, cudaStream_t st) {
     if (s->cfg.wire == SWARM_WIRE_INT8) {
         int8_t* codes = static_cast<int8_t*>(msg);
         void* scales = static_cast<char*>(msg) + ((n + 15) & ~size_t(15));
-        return swarm_quantize_blockwise(x, SWARM_DTYPE_BF16, n, s->cfg.block_size, codes, scales, nullptr, st);
+        return swarm_quantize_blockwise(x, s->dt, n, s->cfg.block_size, codes, scales, nullptr, st);
     }
-    const cudaError_t e = cudaMemcpyAsync(msg, x, n * 2, cudaMemcpyDeviceToDevice, st);
+    const cudaError_t e = cudaMemcpyAsync(msg, x, n * s->es, cudaMemcpyDeviceToDevice, st);
     return e == cudaSuccess ? SWARM_OK : SWARM_E_CUDA;
 }
 
@@ -572,7 +613,7 @@ int init_params(swarm_stage* s, cudaStream_t st) {
         const float stdv = (is_gain || is_bias) ? 0.f : s->cfg.init_std;
         TRY(swarm_fill_normal(s->p32 + t.off, n, mean, stdv, base + i, st));
     }
-    TRY(swarm_cast_f32_bf16(s->p32, s->p16, s->nparams, st));
+    if (!s->f32) TRY(swarm_cast_f32_bf16(s->p32, s->p16, s->nparams, st));
     if (cudaMemsetAsync(s->grad, 0, s->nparams * 4, st) != cudaSuccess ||
         cudaMemsetAsync(s->m, 0, s->nparams * 4, st) != cudaSuccess ||
         cudaMemsetAsync(s->v, 0, s->nparams * 4, st) != cudaSuccess)
@@ -582,6 +623,9 @@ int init_params(swarm_stage* s, cudaStream_t st) {
 
 int create(const swarm_stage_config* c, swarm_stage* s) {
     s->cfg = *c;
+    s->f32 = c->fp32 != 0;
+    s->es = s->f32 ? 4 : 2;
+    s->dt = s->f32 ? SWARM_DTYPE_F32 : SWARM_DTYPE_BF16;
     s->d = c->d_model;
     s->H = c->n_heads;
     s->F = c->d_ffn;
@@ -637,7 +681,7 @@ int create(const swarm_stage_config* c, swarm_stage* s) {
     TRY(alloc(s, &s->grad, s->nparams));
     TRY(alloc(s, &s->m, s->nparams));
     TRY(alloc(s, &s->v, s->nparams));
-    TRY(alloc(s, &s->p16, s->nparams));
+    if (!s->f32) TRY(alloc(s, &s->p16, s->nparams));
     // activation slots
     const size_t T = s->T, Td = T * d, TF = T * F, BHLL = static_cast<size_t>(s->B) * s->H * s->L * s->L;
     s->slots.resize(c->max_slots);
@@ -647,7 +691,7 @@ int create(const swarm_stage_config* c, swarm_stage* s) {
     const size_t nl = static_cast<size_t>(c->n_layers);
     for (auto& sl : s->slots) {
         sl.layer.resize(c->n_layers);
-        bf16 *sa = nullptr, *so = nullptr, *sc = nullptr, *sg = nullptr;
+        EP sa, so, sc, sg;
         if (s->stacked) {
             TRY(alloc(s, &sa, nl * Td));
             TRY(alloc(s, &so, nl * Td));
@@ -699,7 +743,7 @@ int create(const swarm_stage_config* c, swarm_stage* s) {
     // workspaces (fp32 scores only for the unfused attention path)
     {
         const char* e = getenv("SWARM_ATTN_FUSED");
-        s->fused_attn = !(e && e[0] == '0') && s->L % 128 == 0 && s->L <= 512 && s->dh % 64 == 0 && s->dh <= 128;
+        s->fused_attn = !s->f32 && !(e && e[0] == '0') && s->L % 128 == 0 && s->L <= 512 && s->dh % 64 == 0 && s->dh <= 128;
     }
     if (!s->fused_attn) {
         TRY(alloc(s, &s->S, BHLL));
@@ -884,6 +928,7 @@ float* swarm_stage_params(swarm_stage_t s) { return s->p32; }
 void* swarm_stage_params_bf16(swarm_stage_t s) { return s->p16; }
 
 int swarm_stage_sync_shadow(swarm_stage_t s, swarm_stream_t stream) {
+    if (s->f32) return SWARM_OK;  // the GEMMs read the fp32 master itself
     if (!s->banks) return swarm_cast_f32_bf16(s->p32, s->p16, s->nparams, stream);
     for (bf16* p : s->p16b) TRY(swarm_cast_f32_bf16(s->p32, p, s->nparams, stream));
     for (int b = 0; b < 2; ++b) TRY(refresh_ln(s, b, static_cast<cudaStream_t>(stream)));
@@ -892,6 +937,7 @@ int swarm_stage_sync_shadow(swarm_stage_t s, swarm_stream_t stream) {
 
 int swarm_stage_enable_banks(swarm_stage_t s, swarm_stream_t stream) {
     if (s->banks) return SWARM_OK;
+    if (s->f32) return fail("enable_banks: delayed-update banks need the bf16 mode");
     s->p16b[0] = s->p16;
     s->gradb[0] = s->grad;
     TRY(alloc(s, &s->p16b[1], s->nparams));
@@ -948,6 +994,9 @@ int swarm_stage_activation(swarm_stage_t s, int slot, int layer, const char* nam
     if (n == "out") return *ptr = sl.out, *numel = Td, SWARM_OK;
     if (n == "xf") return *ptr = sl.xf, *numel = sl.xf ? Td : 0, SWARM_OK;
     if (n == "dxf") return *ptr = sl.dxf, *numel = sl.dxf ? Td : 0, SWARM_OK;
+    if (n == "dx_last") return *ptr = s->last_dx, *numel = s->last_dx ? static_cast<size_t>(s->T) * s->wire_w : 0, SWARM_OK;
+    if (n == "wire_in") return *ptr = s->bneck ? sl.mi : sl.layer[0].x, *numel = static_cast<size_t>(s->T) * s->wire_w, SWARM_OK;
+    if (n == "wire_out") return *ptr = s->bneck ? sl.mo : sl.out, *numel = static_cast<size_t>(s->T) * s->wire_w, SWARM_OK;
     if (layer < 0 || layer >= static_cast<int>(sl.layer.size())) return fail("activation: bad layer");
     Act& A = sl.layer[layer];
     const size_t TF = static_cast<size_t>(s->T) * s->F;
@@ -974,20 +1023,20 @@ int swarm_stage_forward(swarm_stage_t s, int slot, const void* in, const int32_t
     if (s->cfg.is_first) {
         if (cudaMemcpyAsync(sl.tokens, in, T * sizeof(int32_t), cudaMemcpyDeviceToDevice, st) != cudaSuccess)
             return SWARM_E_CUDA;
-        PTRY(SWARM_PROF_OTHER, st, swarm_embedding_forward(sl.tokens, T, s->p16 + s->emb, s->V, d, sl.layer[0].x, st));
+        PTRY(SWARM_PROF_OTHER, st, swarm_embedding_forward_ex(sl.tokens, T, wts(s) + s->emb, s->V, d, sl.layer[0].x, s->dt, st));
     } else if (s->bneck) {
         // receiver: x0 = LN_d(dequant(wire)) W_d^T   (d/k -> d)
         const int w = s->wire_w;
         PTRY(SWARM_PROF_OTHER, st, wire_decode(s, in, sl.mi, st));
-        PTRY(SWARM_PROF_LAYERNORM, st, swarm_layer_norm_forward(sl.mi, SWARM_DTYPE_BF16, T, w, ln_param(s, s->bn_in_g), ln_param(s, s->bn_in_b), 1e-5,
+        PTRY(SWARM_PROF_LAYERNORM, st, swarm_layer_norm_forward(sl.mi, s->dt, T, w, ln_param(s, s->bn_in_g), ln_param(s, s->bn_in_b), 1e-5,
                                      sl.ni, sl.mud, sl.rsd, st));
-        TRY(mm(T, d, w, {sl.ni, w, T, w, false}, {s->p16 + s->bn_wd, w, d, w, false}, sl.layer[0].x, d,
+        TRY(mm(T, d, w, {sl.ni, w, T, w, false}, {wts(s) + s->bn_wd, w, d, w, false}, sl.layer[0].x, d,
                SWARM_EPI_STORE_BF16, nullptr, 1.f, st));
     } else {
         PTRY(SWARM_PROF_OTHER, st, wire_decode(s, in, sl.layer[0].x, st));
     }
     for (int l = 0; l < n; ++l) {
-        bf16* y = (l + 1 < n) ? sl.layer[l + 1].x : sl.out;
+        EP y = (l + 1 < n) ? sl.layer[l + 1].x : sl.out;
         TRY(block_forward(s, sl.layer[l], y, weights(s, l), st));
     }
     if (!s->cfg.is_last) {
@@ -997,24 +1046,24 @@ int swarm_stage_forward(swarm_stage_t s, int slot, const void* in, const int32_t
             return wire_encode(s, sl.out, out, st);
         }
         // sender: wire = int8(maxout_k(LN_c(out)))
-        PTRY(SWARM_PROF_LAYERNORM, st, swarm_layer_norm_forward(sl.out, SWARM_DTYPE_BF16, T, d, ln_param(s, s->bn_out_g), ln_param(s, s->bn_out_b), 1e-5,
+        PTRY(SWARM_PROF_LAYERNORM, st, swarm_layer_norm_forward(sl.out, s->dt, T, d, ln_param(s, s->bn_out_g), ln_param(s, s->bn_out_b), 1e-5,
                                      sl.z, sl.muc, sl.rsc, st));
-        PTRY(SWARM_PROF_OTHER, st, swarm_maxout_forward(sl.z, SWARM_DTYPE_BF16, static_cast<size_t>(T) * d, s->cfg.maxout_k, sl.mo, sl.am,
+        PTRY(SWARM_PROF_OTHER, st, swarm_maxout_forward(sl.z, s->dt, static_cast<size_t>(T) * d, s->cfg.maxout_k, sl.mo, sl.am,
                                  st));
         ProfOp po(SWARM_PROF_OTHER, st);
         return wire_encode(s, sl.mo, out, st);
     }
     if (!targets) return fail("forward: last stage needs targets");
     // final LN + LM head + cross-entropy, with the head's backward fused in
-    PTRY(SWARM_PROF_LAYERNORM, st, swarm_layer_norm_forward(sl.out, SWARM_DTYPE_BF16, T, d, ln_param(s, s->lnfg), ln_param(s, s->lnfb), 1e-5, sl.xf,
+    PTRY(SWARM_PROF_LAYERNORM, st, swarm_layer_norm_forward(sl.out, s->dt, T, d, ln_param(s, s->lnfg), ln_param(s, s->lnfb), 1e-5, sl.xf,
                                  sl.muf, sl.rsf, st));
-    TRY(mm(T, s->V, d, {sl.xf, d, T, d, false}, {s->p16 + s->head, d, s->V, d, false}, s->logits, s->V,
+    TRY(mm(T, s->V, d, {sl.xf, d, T, d, false}, {wts(s) + s->head, d, s->V, d, false}, s->logits, s->V,
            SWARM_EPI_STORE_F32, nullptr, 1.f, st));
-    PTRY(SWARM_PROF_OTHER, st, swarm_cross_entropy(s->logits, targets, T, s->V, loss_scale, loss_sum, s->dlogits, st));
+    PTRY(SWARM_PROF_OTHER, st, swarm_cross_entropy_ex(s->logits, targets, T, s->V, loss_scale, loss_sum, s->dlogits, s->dt, st));
     TRY(fork_side(s, st, 0));
     TRY(mm(s->V, d, T, {s->dlogits, s->V, T, s->V, true}, {sl.xf, d, T, d, true}, s->grad + s->head, d,
            SWARM_EPI_ACCUM_F32, nullptr, 1.f, side_of(s, st)));
-    TRY(mm(T, d, s->V, {s->dlogits, s->V, T, s->V, false}, {s->p16 + s->head, d, s->V, d, true}, sl.dxf, d,
+    TRY(mm(T, d, s->V, {s->dlogits, s->V, T, s->V, false}, {wts(s) + s->head, d, s->V, d, true}, sl.dxf, d,
            SWARM_EPI_STORE_BF16, nullptr, 1.f, st));
     return join_side(s, st);
 }
@@ -1023,9 +1072,24 @@ int swarm_stage_enable_lanes(swarm_stage_t s, int n) {
     if (!s || n < 1) return fail("enable_lanes: need at least one lane");
     if (!s->lanes.empty()) return static_cast<int>(s->lanes.size()) >= n ? SWARM_OK : fail("enable_lanes: already enabled");
     if (n == 1) return SWARM_OK;
-    s->lanes.resize(n);
-    work_save(s, s->lanes[0]);
-    for (int i = 1; i < n; ++i) TRY(work_alloc(s, s->lanes[i]));
+    // build every set first and commit only when all succeeded: a failed call leaves the
+    // stage without lanes (its device buffers stay owned by s->allocations)
+    std::vector<Work> sets(n);
+    work_save(s, sets[0]);
+    for (int i = 1; i < n; ++i) {
+        const int rc = work_alloc(s, sets[i]);
+        if (rc != SWARM_OK) {
+            for (int j = 1; j <= i; ++j) {
+                for (cudaEvent_t& e : sets[j].ev_fork)
+                    if (e) cudaEventDestroy(e);
+                if (sets[j].ev_join) cudaEventDestroy(sets[j].ev_join);
+                if (sets[j].ev_dq) cudaEventDestroy(sets[j].ev_dq);
+                if (sets[j].side) cudaStreamDestroy(sets[j].side);
+            }
+            return rc;
+        }
+    }
+    s->lanes = std::move(sets);
     s->lane = 0;
     return SWARM_OK;
 }
@@ -1057,7 +1121,7 @@ int swarm_stage_enable_wgrad_pairing_sets(swarm_stage_t s, int n_sets) {
     for (auto& set : s->stash) {
         set.resize(nl);
         if (s->stacked) {  // application order, contiguous: the stacked GEMMs read each as one K = n*T operand
-            bf16 *dy, *du, *dh, *dq;
+            EP dy, du, dh, dq;
             TRY(alloc(s, &dy, nl * T * d));
             TRY(alloc(s, &du, nl * T * F));
             TRY(alloc(s, &dh, nl * T * d));
@@ -1087,7 +1151,7 @@ int stacked_wgrad(swarm_stage* s, const Slot& cur, const std::vector<Stash>& cs,
     const int d = s->d, F = s->F, nT = s->cfg.n_layers * s->T;
     float* G = s->grad;
     const LayerW& W = weights(s, 0);
-    auto one = [&](int M, int N, int ldy, const bf16* dy, const bf16* pdy, int ldx, const bf16* x, const bf16* px,
+    auto one = [&](int M, int N, int ldy, EP dy, EP pdy, int ldx, EP x, EP px,
                    size_t off, int ldo) {
         if (!prev) return mm(M, N, nT, {dy, ldy, nT, ldy, true}, {x, ldx, nT, ldx, true}, G + off, ldo,
                              SWARM_EPI_ACCUM_F32, nullptr, 1.f, sd);
@@ -1145,19 +1209,19 @@ int swarm_stage_backward_ex(swarm_stage_t s, int slot, const void* grad_in, void
     const int T = s->T, d = s->d, n = s->cfg.n_layers;
     const bool stashed = wgrad_mode != SWARM_WGRAD_NOW;
     // the gradient entering the last layer: a workspace, or that layer's stash
-    bf16* g_in = stashed ? s->stash[set][n - 1].dy : s->gy[0];
+    EP g_in = stashed ? s->stash[set][n - 1].dy : s->gy[0];
     int cur = 0;
     if (s->cfg.is_last) {
-        PTRY(SWARM_PROF_LAYERNORM, st, swarm_layer_norm_backward(sl.dxf, sl.out, SWARM_DTYPE_BF16, T, d, ln_param(s, s->lnfg), sl.muf, sl.rsf, nullptr,
+        PTRY(SWARM_PROF_LAYERNORM, st, swarm_layer_norm_backward(sl.dxf, sl.out, s->dt, T, d, ln_param(s, s->lnfg), sl.muf, sl.rsf, nullptr,
                                       g_in, s->grad + s->lnfg, s->grad + s->lnfb, 1, s->lnws, st));
     } else {
         if (!grad_in) return fail("backward: null gradient message");
         if (s->bneck) {
             // d out = LN_c'(maxout'(dequant(grad)))
             PTRY(SWARM_PROF_OTHER, st, wire_decode(s, grad_in, s->wtmp, st));
-            PTRY(SWARM_PROF_OTHER, st, swarm_maxout_backward(s->wtmp, SWARM_DTYPE_BF16, sl.am, static_cast<size_t>(T) * s->wire_w,
+            PTRY(SWARM_PROF_OTHER, st, swarm_maxout_backward(s->wtmp, s->dt, sl.am, static_cast<size_t>(T) * s->wire_w,
                                       s->cfg.maxout_k, s->dc, st));
-            PTRY(SWARM_PROF_LAYERNORM, st, swarm_layer_norm_backward(s->dc, sl.out, SWARM_DTYPE_BF16, T, d, ln_param(s, s->bn_out_g), sl.muc, sl.rsc,
+            PTRY(SWARM_PROF_LAYERNORM, st, swarm_layer_norm_backward(s->dc, sl.out, s->dt, T, d, ln_param(s, s->bn_out_g), sl.muc, sl.rsc,
                                           nullptr, g_in, s->grad + s->bn_out_g, s->grad + s->bn_out_b, 1, s->lnws,
                                           st));
         } else {
@@ -1179,7 +1243,7 @@ int swarm_stage_backward_ex(swarm_stage_t s, int slot, const void* grad_in, void
                 wp.prev = &s->slots[prev_slot].layer[l];
                 wp.ps = &s->stash[prev_set][l];
             }
-            bf16* dx = l > 0 ? s->stash[set][l - 1].dy : s->gy[0];
+            EP dx = l > 0 ? s->stash[set][l - 1].dy : s->gy[0];
             TRY(block_backward(s, sl.layer[l], s->stash[set][l].dy, dx, weights(s, l), st, wp, &s->stash[set][l]));
         }
         if (s->stacked && wgrad_mode == SWARM_WGRAD_PAIR) {
@@ -1191,23 +1255,25 @@ int swarm_stage_backward_ex(swarm_stage_t s, int slot, const void* grad_in, void
     }
     if (s->cfg.is_first) {
         ProfOp po(SWARM_PROF_OTHER, st);
-        return swarm_embedding_backward(sl.tokens, T, s->gy[cur], s->V, d, s->grad + s->emb, st);
+        return swarm_embedding_backward_ex(sl.tokens, T, s->gy[cur], s->V, d, s->grad + s->emb, s->dt, st);
     }
     if (!grad_out) return fail("backward: null output gradient message");
     if (!s->bneck) {
         ProfOp po(SWARM_PROF_OTHER, st);
+        s->last_dx = s->gy[cur];
         return wire_encode(s, s->gy[cur], grad_out, st);
     }
     // receiver side of the bottleneck: dW_d += dx0^T ni ; dni = dx0 W_d ; dmi = LN_d'(dni)
     const int w = s->wire_w;
-    bf16* dx0 = s->gy[cur];
+    EP dx0 = s->gy[cur];
     TRY(mm(d, w, T, {dx0, d, T, d, true}, {sl.ni, w, T, w, true}, s->grad + s->bn_wd, w, SWARM_EPI_ACCUM_F32, nullptr,
            1.f, st));
-    TRY(mm(T, w, d, {dx0, d, T, d, false}, {s->p16 + s->bn_wd, w, d, w, true}, s->wtmp, w, SWARM_EPI_STORE_BF16,
+    TRY(mm(T, w, d, {dx0, d, T, d, false}, {wts(s) + s->bn_wd, w, d, w, true}, s->wtmp, w, SWARM_EPI_STORE_BF16,
            nullptr, 1.f, st));
-    PTRY(SWARM_PROF_LAYERNORM, st, swarm_layer_norm_backward(s->wtmp, sl.mi, SWARM_DTYPE_BF16, T, w, ln_param(s, s->bn_in_g), sl.mud, sl.rsd, nullptr,
+    PTRY(SWARM_PROF_LAYERNORM, st, swarm_layer_norm_backward(s->wtmp, sl.mi, s->dt, T, w, ln_param(s, s->bn_in_g), sl.mud, sl.rsd, nullptr,
                                   s->dqkv, s->grad + s->bn_in_g, s->grad + s->bn_in_b, 1, s->lnws, st));
     ProfOp po(SWARM_PROF_OTHER, st);
+    s->last_dx = s->dqkv;
     return wire_encode(s, s->dqkv, grad_out, st);
 }
 

@@ -40,7 +40,17 @@ __global__ void k_embed_fwd(const int32_t* __restrict__ tok, int n, const uint4*
     }
 }
 
-__global__ void k_embed_bwd(const int32_t* __restrict__ tok, int n, const __nv_bfloat16* __restrict__ dout,
+__device__ __forceinline__ float to_f(float v) { return v; }
+__device__ __forceinline__ float to_f(__nv_bfloat16 v) { return __bfloat162float(v); }
+template <typename T>
+__device__ __forceinline__ T from_f(float v);
+template <>
+__device__ __forceinline__ float from_f<float>(float v) { return v; }
+template <>
+__device__ __forceinline__ __nv_bfloat16 from_f<__nv_bfloat16>(float v) { return __float2bfloat16_rn(v); }
+
+template <typename T>
+__global__ void k_embed_bwd(const int32_t* __restrict__ tok, int n, const T* __restrict__ dout,
                             int vocab, int d, float* __restrict__ dtable) {
     const int warps = (gridDim.x * blockDim.x) >> 5;
     const int lane = threadIdx.x & 31;
@@ -48,15 +58,15 @@ __global__ void k_embed_bwd(const int32_t* __restrict__ tok, int n, const __nv_b
         const int id = tok[t];
         if (id < 0 || id >= vocab) continue;
         for (int c = lane; c < d; c += 32)
-            atomicAdd(dtable + static_cast<size_t>(id) * d + c, __bfloat162float(dout[static_cast<size_t>(t) * d + c]));
+            atomicAdd(dtable + static_cast<size_t>(id) * d + c, to_f(dout[static_cast<size_t>(t) * d + c]));
     }
 }
 
 // --------------------------------------------------------------- softmax --
 constexpr int kMaxLPerLane = 32;  // L <= 1024
 
-__global__ void k_softmax_fwd(const float* __restrict__ S, int rows, int L, int causal,
-                              __nv_bfloat16* __restrict__ P) {
+template <typename T>
+__global__ void k_softmax_fwd(const float* __restrict__ S, int rows, int L, int causal, T* __restrict__ P) {
     const int warps = (gridDim.x * blockDim.x) >> 5;
     const int lane = threadIdx.x & 31;
     const float log2e = 1.4426950408889634f;
@@ -80,22 +90,24 @@ __global__ void k_softmax_fwd(const float* __restrict__ S, int rows, int L, int 
         float sum = 0.f;
 #pragma unroll
         for (int k = 0; k < kMaxLPerLane; ++k) {
-            const float e = (v[k] == -INFINITY) ? 0.f : exp2f((v[k] - m) * log2e);
+            // fp32 output (the fp32 arithmetic mode): expf of the difference, as the oracle
+            const float e = (v[k] == -INFINITY) ? 0.f : (sizeof(T) == 4 ? expf(v[k] - m) : exp2f((v[k] - m) * log2e));
             v[k] = e;
             sum += e;
         }
         const float inv = 1.f / warp_sum(sum);
-        __nv_bfloat16* p = P + static_cast<size_t>(row) * L;
+        T* p = P + static_cast<size_t>(row) * L;
 #pragma unroll
         for (int k = 0; k < kMaxLPerLane; ++k) {
             const int j = k * 32 + lane;
-            if (j < L) p[j] = __float2bfloat16_rn(v[k] * inv);
+            if (j < L) p[j] = from_f<T>(v[k] * inv);
         }
     }
 }
 
-__global__ void k_softmax_bwd(const __nv_bfloat16* __restrict__ P, const float* __restrict__ dP, int rows, int L,
-                              float scale, __nv_bfloat16* __restrict__ dS) {
+template <typename T>
+__global__ void k_softmax_bwd(const T* __restrict__ P, const float* __restrict__ dP, int rows, int L, float scale,
+                              T* __restrict__ dS) {
     const int warps = (gridDim.x * blockDim.x) >> 5;
     const int lane = threadIdx.x & 31;
     for (int row = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; row < rows; row += warps) {
@@ -105,7 +117,7 @@ __global__ void k_softmax_bwd(const __nv_bfloat16* __restrict__ P, const float* 
 #pragma unroll
         for (int k = 0; k < kMaxLPerLane; ++k) {
             const int j = k * 32 + lane;
-            p[k] = j < L ? __bfloat162float(P[base + j]) : 0.f;
+            p[k] = j < L ? to_f(P[base + j]) : 0.f;
             g[k] = j < L ? dP[base + j] : 0.f;
             acc += p[k] * g[k];
         }
@@ -113,7 +125,7 @@ __global__ void k_softmax_bwd(const __nv_bfloat16* __restrict__ P, const float* 
 #pragma unroll
         for (int k = 0; k < kMaxLPerLane; ++k) {
             const int j = k * 32 + lane;
-            if (j < L) dS[base + j] = __float2bfloat16_rn(scale * p[k] * (g[k] - acc));
+            if (j < L) dS[base + j] = from_f<T>(scale * p[k] * (g[k] - acc));
         }
     }
 }
@@ -121,10 +133,16 @@ __global__ void k_softmax_bwd(const __nv_bfloat16* __restrict__ P, const float* 
 // ---------------------------------------------------------- cross-entropy --
 constexpr int kCeThreads = 512;
 
+template <typename T>
+__device__ __forceinline__ float ce_exp(float x) {
+    return sizeof(T) == 4 ? expf(x) : __expf(x);  // fp32 mode: the accurate exponential
+}
+
+template <typename T>
 __global__ void __launch_bounds__(kCeThreads) k_cross_entropy(const float* __restrict__ logits,
                                                               const int32_t* __restrict__ targets, int vocab,
                                                               float grad_scale, float* __restrict__ loss_sum,
-                                                              __nv_bfloat16* __restrict__ dlogits) {
+                                                              T* __restrict__ dlogits) {
     __shared__ float sm[kCeThreads / 32], ss[kCeThreads / 32];
     const int row = blockIdx.x;
     const float* x = logits + static_cast<size_t>(row) * vocab;
@@ -132,10 +150,10 @@ __global__ void __launch_bounds__(kCeThreads) k_cross_entropy(const float* __res
     for (int j = threadIdx.x; j < vocab; j += kCeThreads) {
         const float v = x[j];
         if (v > m) {
-            s = s * __expf(m - v) + 1.f;
+            s = s * ce_exp<T>(m - v) + 1.f;
             m = v;
         } else {
-            s += __expf(v - m);
+            s += ce_exp<T>(v - m);
         }
     }
     // combine (m, s) pairs: warp then block
@@ -143,7 +161,7 @@ __global__ void __launch_bounds__(kCeThreads) k_cross_entropy(const float* __res
     for (int o = 16; o > 0; o >>= 1) {
         const float m2 = __shfl_xor_sync(0xffffffffu, m, o), s2 = __shfl_xor_sync(0xffffffffu, s, o);
         const float mm = fmaxf(m, m2);
-        s = (mm == -INFINITY) ? 0.f : s * __expf(m - mm) + s2 * __expf(m2 - mm);
+        s = (mm == -INFINITY) ? 0.f : s * ce_exp<T>(m - mm) + s2 * ce_exp<T>(m2 - mm);
         m = mm;
     }
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -155,15 +173,15 @@ __global__ void __launch_bounds__(kCeThreads) k_cross_entropy(const float* __res
     float M = -INFINITY;
     for (int w = 0; w < kCeThreads / 32; ++w) M = fmaxf(M, sm[w]);
     float Ssum = 0.f;
-    for (int w = 0; w < kCeThreads / 32; ++w) Ssum += ss[w] * __expf(sm[w] - M);
+    for (int w = 0; w < kCeThreads / 32; ++w) Ssum += ss[w] * ce_exp<T>(sm[w] - M);
     const float lse = M + logf(Ssum);
     const int tgt = targets[row];
     if (threadIdx.x == 0 && loss_sum) atomicAdd(loss_sum, lse - x[tgt]);
     if (dlogits) {
-        __nv_bfloat16* d = dlogits + static_cast<size_t>(row) * vocab;
+        T* d = dlogits + static_cast<size_t>(row) * vocab;
         for (int j = threadIdx.x; j < vocab; j += kCeThreads) {
-            const float p = __expf(x[j] - lse);
-            d[j] = __float2bfloat16_rn(grad_scale * (p - (j == tgt ? 1.f : 0.f)));
+            const float p = ce_exp<T>(x[j] - lse);
+            d[j] = from_f<T>(grad_scale * (p - (j == tgt ? 1.f : 0.f)));
         }
     }
 }
@@ -315,51 +333,103 @@ using namespace swarm;
 
 extern "C" {
 
-int swarm_embedding_forward(const int32_t* tokens, size_t n, const void* table, size_t vocab, size_t d, void* out,
-                            swarm_stream_t stream) {
-    if (d % 8) return invalid("embedding: d must be a multiple of 8");
+int swarm_embedding_forward_ex(const int32_t* tokens, size_t n, const void* table, size_t vocab, size_t d, void* out,
+                               int dtype, swarm_stream_t stream) {
+    if (dtype != SWARM_DTYPE_BF16 && dtype != SWARM_DTYPE_F32) return invalid("embedding: dtype must be f32 or bf16");
+    const size_t row_bytes = d * (dtype == SWARM_DTYPE_F32 ? 4 : 2);
+    if (row_bytes % 16) return invalid("embedding: rows must be a multiple of 16 bytes");
     if (n == 0) return SWARM_OK;
     k_embed_fwd<<<grid_for(n * 32, 256), 256, 0, as_stream(stream)>>>(
         tokens, static_cast<int>(n), static_cast<const uint4*>(table), static_cast<int>(vocab),
-        static_cast<int>(d / 8), static_cast<uint4*>(out));
+        static_cast<int>(row_bytes / 16), static_cast<uint4*>(out));
     SWARM_LAUNCH_CHECK("k_embed_fwd");
+    return SWARM_OK;
+}
+
+int swarm_embedding_forward(const int32_t* tokens, size_t n, const void* table, size_t vocab, size_t d, void* out,
+                            swarm_stream_t stream) {
+    if (d % 8) return invalid("embedding: d must be a multiple of 8");
+    return swarm_embedding_forward_ex(tokens, n, table, vocab, d, out, SWARM_DTYPE_BF16, stream);
+}
+
+int swarm_embedding_backward_ex(const int32_t* tokens, size_t n, const void* dout, size_t vocab, size_t d,
+                                float* dtable, int dtype, swarm_stream_t stream) {
+    if (n == 0) return SWARM_OK;
+    const unsigned g = grid_for(n * 32, 256);
+    if (dtype == SWARM_DTYPE_F32)
+        k_embed_bwd<float><<<g, 256, 0, as_stream(stream)>>>(tokens, static_cast<int>(n),
+                                                             static_cast<const float*>(dout), static_cast<int>(vocab),
+                                                             static_cast<int>(d), dtable);
+    else if (dtype == SWARM_DTYPE_BF16)
+        k_embed_bwd<__nv_bfloat16><<<g, 256, 0, as_stream(stream)>>>(
+            tokens, static_cast<int>(n), static_cast<const __nv_bfloat16*>(dout), static_cast<int>(vocab),
+            static_cast<int>(d), dtable);
+    else
+        return invalid("embedding backward: dtype must be f32 or bf16");
+    SWARM_LAUNCH_CHECK("k_embed_bwd");
     return SWARM_OK;
 }
 
 int swarm_embedding_backward(const int32_t* tokens, size_t n, const void* dout, size_t vocab, size_t d, float* dtable,
                              swarm_stream_t stream) {
-    if (n == 0) return SWARM_OK;
-    k_embed_bwd<<<grid_for(n * 32, 256), 256, 0, as_stream(stream)>>>(
-        tokens, static_cast<int>(n), static_cast<const __nv_bfloat16*>(dout), static_cast<int>(vocab),
-        static_cast<int>(d), dtable);
-    SWARM_LAUNCH_CHECK("k_embed_bwd");
+    return swarm_embedding_backward_ex(tokens, n, dout, vocab, d, dtable, SWARM_DTYPE_BF16, stream);
+}
+
+int swarm_attn_softmax_forward_ex(const float* s, size_t rows, size_t L, int causal, void* p, int p_dtype,
+                                  swarm_stream_t stream) {
+    if (L == 0 || L > 32 * kMaxLPerLane) return invalid("attn softmax: L must be in [1, 1024]");
+    if (rows == 0) return SWARM_OK;
+    const unsigned g = grid_for(rows * 32, 256);
+    if (p_dtype == SWARM_DTYPE_F32)
+        k_softmax_fwd<float><<<g, 256, 0, as_stream(stream)>>>(s, static_cast<int>(rows), static_cast<int>(L), causal,
+                                                               static_cast<float*>(p));
+    else if (p_dtype == SWARM_DTYPE_BF16)
+        k_softmax_fwd<__nv_bfloat16><<<g, 256, 0, as_stream(stream)>>>(s, static_cast<int>(rows), static_cast<int>(L),
+                                                                       causal, static_cast<__nv_bfloat16*>(p));
+    else
+        return invalid("attn softmax: dtype must be f32 or bf16");
+    SWARM_LAUNCH_CHECK("k_softmax_fwd");
     return SWARM_OK;
 }
 
 int swarm_attn_softmax_forward(const float* s, size_t rows, size_t L, int causal, void* p, swarm_stream_t stream) {
-    if (L == 0 || L > 32 * kMaxLPerLane) return invalid("attn softmax: L must be in [1, 1024]");
+    return swarm_attn_softmax_forward_ex(s, rows, L, causal, p, SWARM_DTYPE_BF16, stream);
+}
+
+int swarm_attn_softmax_backward_ex(const void* p, const float* dp, size_t rows, size_t L, float scale, void* ds,
+                                   int dtype, swarm_stream_t stream) {
+    if (L == 0 || L > 32 * kMaxLPerLane) return invalid("attn softmax bwd: L must be in [1, 1024]");
     if (rows == 0) return SWARM_OK;
-    k_softmax_fwd<<<grid_for(rows * 32, 256), 256, 0, as_stream(stream)>>>(
-        s, static_cast<int>(rows), static_cast<int>(L), causal, static_cast<__nv_bfloat16*>(p));
-    SWARM_LAUNCH_CHECK("k_softmax_fwd");
+    const unsigned g = grid_for(rows * 32, 256);
+    if (dtype == SWARM_DTYPE_F32)
+        k_softmax_bwd<float><<<g, 256, 0, as_stream(stream)>>>(static_cast<const float*>(p), dp, static_cast<int>(rows),
+                                                               static_cast<int>(L), scale, static_cast<float*>(ds));
+    else if (dtype == SWARM_DTYPE_BF16)
+        k_softmax_bwd<__nv_bfloat16><<<g, 256, 0, as_stream(stream)>>>(
+            static_cast<const __nv_bfloat16*>(p), dp, static_cast<int>(rows), static_cast<int>(L), scale,
+            static_cast<__nv_bfloat16*>(ds));
+    else
+        return invalid("attn softmax bwd: dtype must be f32 or bf16");
+    SWARM_LAUNCH_CHECK("k_softmax_bwd");
     return SWARM_OK;
 }
 
 int swarm_attn_softmax_backward(const void* p, const float* dp, size_t rows, size_t L, float scale, void* ds,
                                 swarm_stream_t stream) {
-    if (L == 0 || L > 32 * kMaxLPerLane) return invalid("attn softmax bwd: L must be in [1, 1024]");
-    if (rows == 0) return SWARM_OK;
-    k_softmax_bwd<<<grid_for(rows * 32, 256), 256, 0, as_stream(stream)>>>(
-        static_cast<const __nv_bfloat16*>(p), dp, static_cast<int>(rows), static_cast<int>(L), scale,
-        static_cast<__nv_bfloat16*>(ds));
-    SWARM_LAUNCH_CHECK("k_softmax_bwd");
-    return SWARM_OK;
+    return swarm_attn_softmax_backward_ex(p, dp, rows, L, scale, ds, SWARM_DTYPE_BF16, stream);
 }
 
-int swarm_cross_entropy(const float* logits, const int32_t* targets, size_t rows, size_t vocab, float grad_scale,
-                        float* loss_sum, void* dlogits, swarm_stream_t stream) {
+int swarm_cross_entropy_ex(const float* logits, const int32_t* targets, size_t rows, size_t vocab, float grad_scale,
+                           float* loss_sum, void* dlogits, int dlogits_dtype, swarm_stream_t stream) {
     if (vocab == 0) return invalid("cross_entropy: empty vocab");
     if (rows == 0) return SWARM_OK;
+    if (dlogits_dtype == SWARM_DTYPE_F32) {
+        k_cross_entropy<float><<<static_cast<unsigned>(rows), kCeThreads, 0, as_stream(stream)>>>(
+            logits, targets, static_cast<int>(vocab), grad_scale, loss_sum, static_cast<float*>(dlogits));
+        SWARM_LAUNCH_CHECK("k_cross_entropy");
+        return SWARM_OK;
+    }
+    if (dlogits_dtype != SWARM_DTYPE_BF16) return invalid("cross_entropy: dlogits dtype must be f32 or bf16");
     if (vocab % 8 == 0 && !(reinterpret_cast<uintptr_t>(logits) & 15) && !(reinterpret_cast<uintptr_t>(dlogits) & 15)) {
         // at most 2 rows per SM in flight (the unused dynamic smem only caps occupancy): 296 rows x
         // 200 KB stay L2-resident between the two passes over a row, 4 per SM would not
@@ -374,10 +444,16 @@ int swarm_cross_entropy(const float* logits, const int32_t* targets, size_t rows
         SWARM_LAUNCH_CHECK("k_cross_entropy_v");
         return SWARM_OK;
     }
-    k_cross_entropy<<<static_cast<unsigned>(rows), kCeThreads, 0, as_stream(stream)>>>(
+    k_cross_entropy<__nv_bfloat16><<<static_cast<unsigned>(rows), kCeThreads, 0, as_stream(stream)>>>(
         logits, targets, static_cast<int>(vocab), grad_scale, loss_sum, static_cast<__nv_bfloat16*>(dlogits));
     SWARM_LAUNCH_CHECK("k_cross_entropy");
     return SWARM_OK;
+}
+
+int swarm_cross_entropy(const float* logits, const int32_t* targets, size_t rows, size_t vocab, float grad_scale,
+                        float* loss_sum, void* dlogits, swarm_stream_t stream) {
+    return swarm_cross_entropy_ex(logits, targets, rows, vocab, grad_scale, loss_sum, dlogits, SWARM_DTYPE_BF16,
+                                  stream);
 }
 
 int swarm_adamw_step(float* p32, void* p16, float* grad, float* m, float* v, size_t n, float lr, float beta1,

@@ -42,6 +42,7 @@ class StageConfig:
     weight_decay: float = 0.0
     init_std: float = 0.02
     seed: int = 0
+    fp32: int = 0  # 1: fp32 arithmetic mode (fp32 activations / wire / SIMT GEMMs on the fp32 master)
 
     def to_c(self) -> L.StageConfigC:
         c = L.StageConfigC()
@@ -169,7 +170,17 @@ class Stage:
         return device_view(self.lib.swarm_stage_params(self.h), self.n_params, torch.float32, self.device)
 
     def params_bf16(self) -> torch.Tensor:
+        if self.cfg.fp32:
+            raise ValueError("fp32 stage: the GEMMs read the fp32 master (params()); there is no bf16 shadow")
         return device_view(self.lib.swarm_stage_params_bf16(self.h), self.n_params, torch.bfloat16, self.device)
+
+    @property
+    def act_dtype(self) -> torch.dtype:
+        return torch.float32 if self.cfg.fp32 else torch.bfloat16
+
+    def weights(self) -> torch.Tensor:
+        """The weights the visit GEMMs read: the bf16 shadow, or the fp32 master in fp32 mode."""
+        return self.params() if self.cfg.fp32 else self.params_bf16()
 
     def optimizer_state(self):
         """(m, v, step): AdamW moments as fp32 device views and the step counter."""
@@ -193,7 +204,9 @@ class Stage:
         """A parameter (fp32 master), its bf16 shadow or its gradient, shaped [rows, cols]."""
         for n, off, r, c in self.param_info():
             if n == name:
-                src = {"param": self.params(), "bf16": self.params_bf16(), "grad": self.grads()}[which]
+                src = {"param": self.params(), "bf16": self.params_bf16, "weights": self.weights,
+                       "grad": self.grads()}[which]
+                src = src() if callable(src) else src
                 return src[off:off + r * c].view(r, c)
         raise KeyError(name)
 
@@ -222,4 +235,4 @@ class Stage:
         ptr, n = C.c_void_p(), C.c_size_t()
         L.check(self.lib.swarm_stage_activation(self.h, slot, layer, name.encode(), C.byref(ptr), C.byref(n)),
                 "stage_activation")
-        return device_view(ptr.value, n.value, torch.bfloat16, self.device)
+        return device_view(ptr.value, n.value, self.act_dtype, self.device)

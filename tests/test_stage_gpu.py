@@ -267,3 +267,70 @@ def test_paired_weight_gradients_match_per_microbatch(cuda, shape):
     scale = float(grads[0].abs().max())
     for other in grads[1:]:
         torch.testing.assert_close(other, grads[0], rtol=1e-4, atol=1e-5 * scale)
+
+
+def _wire_from(st, x):
+    """A wire message carrying the int8 codec of x (the stage's wire width), as a sender builds it."""
+    import torch
+    from paper_2301_11913_b200 import ops
+    n = x.numel()
+    off = (n + 15) // 16 * 16
+    nb = (n + st.cfg.block_size - 1) // st.cfg.block_size
+    msg = st.new_wire()
+    ops.quantize(x.reshape(-1), st.cfg.block_size, codes=msg[:n].view(torch.int8),
+                 scales=msg[off:off + nb * 4].view(torch.float32))
+    return msg
+
+
+def _decode_any(st, wire, width):
+    import torch
+    from paper_2301_11913_b200 import ops
+    n = st.cfg.tokens * width
+    off = (n + 15) // 16 * 16
+    nb = (n + st.cfg.block_size - 1) // st.cfg.block_size
+    return ops.dequantize(wire[:n].view(torch.int8), wire[off:off + nb * 4].view(torch.float32), st.cfg.block_size,
+                          torch.bfloat16).view(st.cfg.tokens, width)
+
+
+@pytest.mark.parametrize("shape", ["configs2", "configs3"])
+def test_one_block_at_baseline_shape(cuda, shape):
+    """One middle-stage visit (int8 wire in, int8 wire out, backward with an int8
+    gradient wire) at the BASELINE shapes, against the fp64 oracle fed the exact
+    bits the stage received, at the bf16 tolerances stated at the top of this file.
+      configs2: d 2048, 16 heads, d_ffn 8192, seq 512, microbatch 4, one block;
+      configs3: d 4096, 32 heads, d_ffn 16384, seq 512, microbatch 1, two applications
+                of one shared block, maxout k=2 bottleneck on both boundaries."""
+    import os
+
+    import torch
+    from oracle import block_oracle as BO
+    from paper_2301_11913_b200.stage import Stage
+    torch.set_num_threads(os.cpu_count() or 1)
+    if shape == "configs2":
+        cfg = tiny_cfg(d_model=2048, n_heads=16, d_ffn=8192, seq_len=512, micro_batch=4, n_layers=1, is_first=0,
+                       is_last=0, max_slots=1, init_std=0.02, seed=21)
+    else:
+        cfg = tiny_cfg(d_model=4096, n_heads=32, d_ffn=16384, seq_len=512, micro_batch=1, n_layers=2,
+                       shared_layers=1, maxout_k=2, is_first=0, is_last=0, max_slots=1, init_std=0.02, seed=22)
+    st = Stage(cfg)
+    width = cfg.d_model // max(cfg.maxout_k, 1)
+    g = torch.Generator(device="cuda").manual_seed(5)
+    x = torch.randn(cfg.tokens, width, device="cuda", generator=g)
+    dy = torch.randn(cfg.tokens, width, device="cuda", generator=g) * 1e-3
+    win, gin = _wire_from(st, x), _wire_from(st, dy)
+    wout, gout = st.new_wire(), st.new_wire()
+    st.forward(0, win, out=wout)
+    st.backward(0, grad_in=gin, grad_out=gout)
+    torch.cuda.synchronize()
+    x_in = _decode_any(st, win, width).double().cpu().requires_grad_()
+    P = oracle_params(st)
+    y_ref, _ = BO.stage(P, cfg, x_in)
+    assert rel(st.activation(0, 0, "wire_out").view(cfg.tokens, -1), y_ref.detach()) <= FWD_TOL
+    y_ref.backward(_decode_any(st, gin, width).double().cpu())
+    # the bottleneck's maxout re-routes a near-tied window's gradient on a bf16 rounding
+    # difference; everything upstream of it gets the wider tolerance (see the top of this file)
+    tol = GRAD_TOL_MAXOUT_UPSTREAM if cfg.maxout_k > 1 else GRAD_TOL
+    for name, off, r, c in st.param_info():
+        e = rel(grad_of(st, name, r), P[name].grad)
+        assert e <= tol, (name, e)
+    assert rel(st.activation(0, 0, "dx_last").view(cfg.tokens, -1), x_in.grad) <= tol
