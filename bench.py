@@ -266,11 +266,18 @@ def bench_codec(args, world, rank, local):
                       "quantize_gbs": bq / (qus * 1e-6) / 1e9, "dequantize_gbs": bq / (dqus * 1e-6) / 1e9})
     del flush
 
-    # parity guard: a fast wrong kernel is not a result
+    # parity guard (a fast wrong kernel is not a result): on every 997th block, the codes and
+    # scales equal the reference formula evaluated in fp64 by torch (compression.cpp:18-27:
+    # a = max|x|, code = round-half-away(127 x / a)), and the dequantized values equal
+    # fp32(code * a / 127) (compression.cpp:33-35)
     idx = torch.arange(0, CODEC_N // CODEC_BS, 997, device=dev)
-    err = (y.view(-1, CODEC_BS)[idx] - x.view(-1, CODEC_BS)[idx]).abs().amax(1)
-    ymax = y.view(-1, CODEC_BS)[idx].abs().amax(1)
-    ok = bool((err <= 0.5 * scales[idx] / 127 + ymax * 2.0 ** -24).all())
+    xb = x.view(-1, CODEC_BS)[idx].double()
+    a = xb.abs().amax(1, keepdim=True)
+    q = 127.0 * xb / a
+    want_codes = (torch.sign(q) * torch.floor(q.abs() + 0.5)).clamp(-127, 127).to(torch.int8)
+    ok = bool(torch.equal(codes.view(-1, CODEC_BS)[idx], want_codes)) and bool(
+        torch.equal(scales[idx].double(), a.view(-1)))
+    ok = ok and bool(torch.equal(y.view(-1, CODEC_BS)[idx], (want_codes.double() * a / 127.0).float()))
 
     # e2e: the reference-facing by-value path — HOST (pinned) buffers, the
     # C-ABI *_host entry points do H2D -> kernel -> D2H inside the timed region.
@@ -339,11 +346,13 @@ TRAIN_STAGES = 4
 TRAIN_MICROBATCHES = 32
 
 
-def cpu_block_reference_steps(m, steps: int, warmup: int, total_budget_s: float = 90.0):
-    """--impl reference, train: the CPU block oracle timed as K steps after W
-    warm-ups, each step a bounded sample (whole-microbatch fwd+bwd passes through
-    one block, as many as fit the per-step share of ~90 s), extrapolated per token
-    to the full model exactly like cpu_block_baseline."""
+def cpu_block_reference_steps(m, steps: int, warmup: int):
+    """--impl reference, train: the CPU block oracle (the reference has no training
+    path) timed as exactly K steps after W warm-ups.  Each step is
+    one bounded sample of the workload: fwd+bwd of one whole microbatch through ONE
+    of the model's blocks, i.e. 1/(stages*layers) of a microbatch's block work, so a
+    step "processes" tokens/(stages*layers) model tokens.  Returns (tokens/s, measured
+    seconds per step, threads, sample)."""
     import torch
 
     from oracle import block_oracle as BO
@@ -362,22 +371,18 @@ def cpu_block_reference_steps(m, steps: int, warmup: int, total_budget_s: float 
         y = BO.block(x, W, m.micro_batch, m.seq_len, m.n_heads, True)
         y.backward(torch.ones_like(y))
 
-    t_one = None
-    for _ in range(max(1, warmup)):
-        t0 = time.perf_counter()
+    for _ in range(warmup):
         one()
-        t_one = time.perf_counter() - t0
-    reps = max(1, int(total_budget_s / max(1, steps + warmup) / t_one))
     t0 = time.perf_counter()
-    for _ in range(steps * reps):
+    for _ in range(steps):
         one()
-    dt = (time.perf_counter() - t0) / (steps * reps)
+    step_s = (time.perf_counter() - t0) / steps
     layers = m.layers_per_stage * TRAIN_STAGES
-    tok_s = m.tokens / (dt * layers)
-    sample = (f"fp32 torch-CPU block oracle: {steps} step(s) x {reps} fwd+bwd pass(es) of a {m.tokens}-token "
-              f"microbatch through one d={d} block ({dt:.2f} s each) after {max(1, warmup)} warm-up pass(es), "
-              f"extrapolated to {layers} layers")
-    return tok_s, threads, sample
+    tok_s = m.tokens / layers / step_s
+    sample = (f"fp32 torch-CPU block oracle on {threads} threads: each of the {steps} timed step(s) (after {warmup} "
+              f"warm-up(s)) is fwd+bwd of one {m.tokens}-token microbatch through one d={d} block ({step_s:.3f} s), "
+              f"= {m.tokens}/{layers} model tokens of the {layers}-block model (embedding / LM head not sampled)")
+    return tok_s, step_s, threads, sample
 
 
 def cpu_block_baseline(m, budget_s: float = 20.0):
@@ -414,15 +419,58 @@ def cpu_block_baseline(m, budget_s: float = 20.0):
     return tok_s, threads, sample
 
 
+class Shape:
+    """A BASELINE model shape (mirrors paper_2301_11913_b200.swarm.PRESETS; tests/
+    test_bench_host.py keeps the two equal).  Kept here so that the --impl reference
+    arm never imports the product package."""
+
+    def __init__(self, d_model, n_heads, d_ffn, seq_len, micro_batch, layers_per_stage, vocab, shared_layers=0,
+                 maxout_k=0, block_size=4096):
+        self.d_model, self.n_heads, self.d_ffn, self.seq_len = d_model, n_heads, d_ffn, seq_len
+        self.micro_batch, self.layers_per_stage, self.vocab = micro_batch, layers_per_stage, vocab
+        self.shared_layers, self.maxout_k, self.block_size = shared_layers, maxout_k, block_size
+
+    @property
+    def tokens(self) -> int:
+        return self.micro_batch * self.seq_len
+
+    def params_per_layer(self) -> int:  # cost_model.cpp:31-35
+        return 4 * self.d_model * self.d_model + 2 * self.d_model * self.d_ffn
+
+    def flops_per_token(self, n_stages: int) -> float:
+        per_layer = 2 * self.params_per_layer() + 4 * self.seq_len * self.d_model
+        return 3.0 * per_layer * self.layers_per_stage * n_stages
+
+
+SHAPES = {
+    "tiny": Shape(256, 4, 1024, 128, 8, 2, 512),
+    "C": Shape(2048, 16, 8192, 512, 4, 8, 50304),
+    "D": Shape(4096, 32, 16384, 512, 1, 16, 50304, shared_layers=1, maxout_k=2),
+}
+
+
+def shape_of(args) -> Shape:
+    import copy
+    m = copy.copy(SHAPES[args.model])
+    mb = getattr(args, "micro_batch", None)
+    if mb:
+        m.micro_batch = mb
+    return m
+
+
 def model_config(args):
-    """The named preset, with the microbatch size overridden by --micro-batch
-    (configs[2] at B=4, swept over 1, 2, 4, 8)."""
+    """The product's preset (GPU arm only), with the microbatch size overridden by
+    --micro-batch (configs[2] at B=4, swept over 1, 2, 4, 8)."""
     import dataclasses
 
     from paper_2301_11913_b200.swarm import PRESETS
     m = PRESETS[args.model]
     mb = getattr(args, "micro_batch", None)
     return dataclasses.replace(m, micro_batch=mb) if mb else m
+
+
+def placement_str(world: int, S: int) -> str:
+    return f"{S} stages x {world // S} peer(s) per stage" if world >= S else f"{world} GPU(s) x {S // world} stage(s) each"
 
 
 def measure_link(world, rank, nbytes=4 << 20, reps=20):
@@ -526,9 +574,10 @@ def cost_model_report(mcfg, S, M, world, step_s, link):
                     "the driver's scaling run measures the same N"}
 
 
-def train_config(args) -> dict:
-    """The configs[2] workload description shared by both arms' JSON lines."""
-    m = model_config(args)
+def train_config(args, world: int) -> dict:
+    """The workload description, identical in both arms' JSON lines (the driver
+    compares them); per-run details go to the line's "run" object."""
+    m = shape_of(args)
     S, M = args.stages, args.microbatches
     which = {"C": "configs[2]", "D": "configs[3] (paper scale)", "tiny": "configs[0] (tiny)"}[args.model]
     layers = f"{m.layers_per_stage} {'shared ' if m.shared_layers else ''}layers/stage"
@@ -536,7 +585,9 @@ def train_config(args) -> dict:
     return {"workload": f"BASELINE {which}: {S} stages, {layers}, d_model {m.d_model}, {m.n_heads} heads, "
                         f"seq {m.seq_len}, {codec}, stochastic wiring + intra-stage all-reduce",
             "model": args.model, "global_batch": M * m.micro_batch, "micro_batch": m.micro_batch,
-            "microbatches_per_step": M, "seq_len": m.seq_len, "tokens_per_step": M * m.tokens, "vocab": m.vocab}
+            "microbatches_per_step": M, "seq_len": m.seq_len, "tokens_per_step": M * m.tokens, "vocab": m.vocab,
+            "parallelism": placement_str(world, S),
+            "l2": "per-step working set (weights + activations, GBs) far exceeds the 126 MB L2; no flush needed"}
 
 
 def bench_train(args, world, rank, local):
@@ -645,11 +696,11 @@ def bench_train(args, world, rank, local):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
         "data": "synthetic tokens uniform over the vocab, random-init weights",
-        "config": {**train_config(args), "parallelism": placement,
-                   "optimizer": "AdamW (fused, fp32 master)" + (", delayed parameter updates (1 step)" if args.dpu else ""),
-                   "l2": "per-step working set (weights + activations, GBs) far exceeds L2; no flush needed",
-                   "mean_loss": mean_loss, "model_tflops_per_s": model_tflops,
-                   "model_flops_per_token": mcfg.flops_per_token(S)},
+        "config": train_config(args, world),
+        "run": {"placement": placement,
+                "optimizer": "AdamW (fused, fp32 master)" + (", delayed parameter updates (1 step)" if args.dpu else ""),
+                "mean_loss": mean_loss, "model_tflops_per_s": model_tflops,
+                "model_flops_per_token": mcfg.flops_per_token(S)},
         "roofline": {"bound": "tensor", "kernel": "k_gemm (tcgen05 bf16, every block/attention/head GEMM)",
                      "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
                      "traffic": gemm_traffic.get("dram_bytes_per_launch"),
@@ -773,19 +824,17 @@ def bench_engine(args, world, rank, local):
         "unit": "tokens/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
         "dtype": "bf16", "data": "synthetic tokens uniform over the vocab (per-trainer pool), random-init weights",
-        "config": {**train_config(args), "parallelism": (f"{S} stages x {P_.P} peer(s) per stage" if world >= S else
-                                                         f"{world} GPU(s) x {S // world} stage(s) each"),
-                   "execution": "asynchronous SWARM: the reference DES engine's record order (csrc/engine.cpp, "
-                                "decision-identical to sim::run), one compute stream per peer, NCCL isend/irecv "
-                                "of int8 wire messages, stage all-reduce + AdamW at every AllReduceTick",
-                   "trainers": ex.T, "trainers_per_peer": args.trainers_per_peer, "lanes_per_peer": args.lanes,
-                   "schedule": "forward 1.0 / backward 2.0 virtual s, AllReduceTick every "
-                               f"{period:.4g} virtual s (= {M} completions at the schedule's own rate: one optimizer "
-                               f"step per stage per {M} microbatches); one step = {M} microbatch completions",
-                   "optimizer": "AdamW (fused, fp32 master), paired weight gradients",
-                   "mean_loss": float(loss.item()) / max(tokens, 1),
-                   "model_tflops_per_s": value * mcfg.flops_per_token(S) / 1e12,
-                   "l2": "per-step working set far exceeds L2; no flush needed"},
+        "config": train_config(args, world),
+        "run": {"execution": "asynchronous SWARM: the reference DES engine's record order (csrc/engine.cpp, "
+                             "decision-identical to sim::run), one compute stream per peer, NCCL send/recv "
+                             "of int8 wire messages, stage all-reduce + AdamW at every AllReduceTick",
+                "trainers": ex.T, "trainers_per_peer": args.trainers_per_peer, "lanes_per_peer": args.lanes,
+                "schedule": "forward 1.0 / backward 2.0 virtual s, AllReduceTick every "
+                            f"{period:.4g} virtual s (= {M} completions at the schedule's own rate: one optimizer "
+                            f"step per stage per {M} microbatches); one step = {M} microbatch completions",
+                "optimizer": "AdamW (fused, fp32 master), paired weight gradients",
+                "mean_loss": float(loss.item()) / max(tokens, 1),
+                "model_tflops_per_s": value * mcfg.flops_per_token(S) / 1e12},
         "engine": {"records": r1 - r0, "virtual_seconds": v1 - v0, "optimizer_steps_rank": t_1 - t_0,
                    "microbatches": done, "graph_captures_in_timed_region_rank0": c1 - c0},
         "e2e": {"value": e2e_done * mcfg.tokens / e2e_s, "unit": "tokens/s",
@@ -885,15 +934,16 @@ def run_reference(args, world, rank):
     has no training path); codec: the unmodified reference codec (oracle/_ref)."""
     if rank != 0:
         return None
-    if args.workload == "train":
-        from paper_2301_11913_b200.swarm import PRESETS
-        m = model_config(args)
-        tok_s, thr, sample = cpu_block_reference_steps(m, args.steps, args.warmup)
+    if args.workload in ("train", "engine"):
+        m = shape_of(args)
+        tok_s, step_s, thr, sample = cpu_block_reference_steps(m, args.steps, args.warmup)
         return {"impl": "reference", "metric": "training tokens/s (SWARM pipeline)", "value": tok_s,
                 "unit": "tokens/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-                "ms_per_step": TRAIN_MICROBATCHES * m.tokens / tok_s * 1e3, "higher_is_better": True,
+                "ms_per_step": step_s * 1e3, "higher_is_better": True,
                 "scaling": "strong", "vs_baseline": None, "dtype": "f32 (CPU)", "data": "synthetic",
-                "config": {**train_config(args), "parallelism": "CPU (rank 0 only)"},
+                "config": train_config(args, world),
+                "run": {"execution": "CPU block oracle on rank 0's host cores (the reference has no training path)",
+                        "tokens_per_step": m.tokens / (m.layers_per_stage * TRAIN_STAGES)},
                 "cpu_baseline": {"value": tok_s, "unit": "tokens/s", "cores": thr, "kind": "port", "sample": sample},
                 "e2e": {"value": tok_s, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     threads = os.cpu_count() or 1
@@ -944,7 +994,9 @@ def main():
     args.warmup = max(args.warmup, 3)
     world, rank, local = dist_setup(args)
     if args.lanes is None:
-        args.lanes = 2 if world >= 2 else 1
+        args.lanes = 2 if world >= 2 and not args.single_stream else 1
+    elif args.lanes > 1 and args.single_stream:
+        ap.error("--lanes > 1 needs a stream per peer (drop --single-stream)")
     if args.impl == "reference":
         line = run_reference(args, world, rank)
     elif args.workload == "codec":
@@ -985,9 +1037,10 @@ def main():
             gc.collect()
             torch.cuda.empty_cache()
         if not args.no_codec:
-            c = bench_codec(argparse.Namespace(steps=200, warmup=5, no_cpu_baseline=True, e2e_steps=0), world, rank,
-                            local)
-            line["codec"] = {k: c[k] for k in ("metric", "value", "unit", "roofline")}
+            c = bench_codec(argparse.Namespace(steps=200, warmup=5, no_cpu_baseline=args.no_cpu_baseline, e2e_steps=2),
+                            world, rank, local)
+            line["codec"] = {k: c[k] for k in ("metric", "value", "unit", "ms_per_step", "steps", "config", "roofline",
+                                               "e2e", "sweep", "parity_ok", "cpu_baseline", "gpu_launches") if k in c}
     if rank == 0 and line is not None:
         print(json.dumps(line), flush=True)
     if world > 1:

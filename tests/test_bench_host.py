@@ -40,3 +40,40 @@ def test_engine_tick_period_matches_completions():
             done = 0
     steady = per_tick[5:]
     assert steady and abs(sum(steady) / len(steady) - M) <= 2
+
+
+def test_bench_shapes_mirror_the_product_presets():
+    import bench
+    from paper_2301_11913_b200.swarm import PRESETS
+    for name, p in PRESETS.items():
+        s = bench.SHAPES[name]
+        for f in ("d_model", "n_heads", "d_ffn", "seq_len", "micro_batch", "layers_per_stage", "vocab",
+                  "shared_layers", "maxout_k", "block_size"):
+            assert getattr(s, f) == getattr(p, f), (name, f)
+        assert s.flops_per_token(4) == p.flops_per_token(4)
+
+
+def test_reference_arm_runs_without_the_product_package():
+    """--impl reference times the CPU path only: it must not load paper_2301_11913_b200 (nor its
+    .so files), its config must equal the GPU arm's, and K steps must take about K x ms_per_step."""
+    import json
+    import subprocess
+    import time
+    code = ("import sys, runpy; sys.argv = ['bench.py', '--impl', 'reference', '--model', 'tiny', '--steps', '3', "
+            "'--warmup', '3']; runpy.run_path('bench.py', run_name='__main__'); "
+            "bad = [m for m in sys.modules if m.startswith('paper_2301_11913_b200')]; "
+            "print('LOADED', bad)")
+    t0 = time.perf_counter()
+    out = subprocess.run([sys.executable, "-c", code], cwd=ROOT, capture_output=True, text=True, timeout=600)
+    wall = time.perf_counter() - t0
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = out.stdout.strip().splitlines()
+    assert lines[-1] == "LOADED []"
+    j = json.loads(lines[-2])
+    assert j["impl"] == "reference" and j["steps"] == 3
+    assert j["ms_per_step"] * (j["steps"] + j["warmup"]) / 1e3 <= wall
+    import argparse
+
+    import bench
+    ns = argparse.Namespace(model="tiny", stages=4, microbatches=32, micro_batch=None)
+    assert j["config"] == bench.train_config(ns, 1)
