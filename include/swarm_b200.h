@@ -449,6 +449,94 @@ int swarm_engine_next(swarm_engine_t e, swarm_engine_record* records, size_t cap
 int swarm_engine_summary(swarm_engine_t e, uint64_t* dispatched, uint64_t* completed, double* buckets,
                          size_t n_buckets, double* now);
 
+/* ---- NCCL transport: stage-to-stage hops and intra-stage all-reduce ------
+ * Raw NCCL (resolved at run time: the process's libnccl.so.2, SWARM_NCCL_LIB to
+ * override).  One process per GPU; the caller sets the CUDA device first.
+ * SWARM_E_UNSUPPORTED when no NCCL library is found. */
+typedef struct swarm_comm* swarm_comm_t;
+const char* swarm_comm_last_error(void);
+int swarm_comm_nccl_version(void);
+int swarm_comm_unique_id(void* id /* 128 bytes, ncclUniqueId */);
+int swarm_comm_create(const void* id, int nranks, int rank, swarm_comm_t* out); /* ncclCommInitRank */
+/* ncclCommSplit: collective over `parent`; color < 0 leaves this rank out (*out = NULL) */
+int swarm_comm_split(swarm_comm_t parent, int color, int key, swarm_comm_t* out);
+void swarm_comm_destroy(swarm_comm_t c);
+int swarm_comm_size(swarm_comm_t c, int* nranks, int* rank);
+int swarm_comm_group_start(void);
+int swarm_comm_group_end(void);
+/* The stage-to-stage hop (replaces Engine::dispatch_current's queue move,
+ * P/src/sim.cpp:405-436, and the link-time model of cost_model.cpp:55-59): one
+ * wire message [payload | swarm_wire_header] (swarm_stage_wire_bytes) as a single
+ * ncclSend / ncclRecv to / from `peer` (rank in `c`), stream-ordered. */
+int swarm_send_compressed(swarm_comm_t c, const void* msg, size_t bytes, int peer, swarm_stream_t stream);
+int swarm_recv_compressed(swarm_comm_t c, void* msg, size_t bytes, int peer, swarm_stream_t stream);
+/* in-place SUM all-reduce of `count` F32 | BF16 elements */
+int swarm_allreduce_sum(swarm_comm_t c, void* buf, size_t count, int dtype, swarm_stream_t stream);
+/* The intra-stage gradient averaging (replaces the AllReduceTick stall,
+ * P/src/sim.cpp:245-250, :352): SUM of the stage's fp32 gradient arena over the
+ * stage's peers (`stage_comm`; NULL or one member: no-op).  The optimizer step that
+ * follows divides by the microbatches the stage served (grad_scale). */
+int swarm_stage_allreduce(swarm_stage_t st, swarm_comm_t stage_comm, swarm_stream_t stream);
+
+/* ---- host driver: the engine-driven SWARM executor in C++ ------------------
+ * Walks engine records (START / HOP / ALLREDUCE / DONE, above) and issues the
+ * real work where the reference advances simulated time: visits at START
+ * (Engine::start_service, sim.cpp:395-403), transfers for cross-rank HOPs
+ * (dispatch_current, :405-436; both halves issued at the consumer's START),
+ * all-reduce + AdamW at ALLREDUCE (:245-250, :352).  Placement:
+ * world >= n_stages: peer id == rank, `layout[s]` peers on stage s (NULL: even);
+ * world < n_stages: each rank hosts n_stages / world consecutive stages.  Every
+ * rank runs the same engine on the same seed. */
+typedef struct {
+    swarm_stage_config model; /* every stage's shapes / wire / optimizer; is_first, is_last, max_slots
+                                 (= trainers) and seed (= seed * 1000 + stage) are set per peer */
+    int n_stages;
+    int world, rank;
+    const int* layout;
+    double forward_seconds, backward_multiplier, allreduce_period, allreduce_stall, duration_seconds;
+    int trainers_per_peer;
+    uint64_t seed;
+    int lanes;           /* visits a peer serves concurrently (swarm_stage_enable_lanes) */
+    int pair_wgrad;      /* paired weight gradients over a peer's consecutive backward visits */
+    int use_graphs;      /* CUDA-graph replay of every (peer, kind, trainer, pair, lane) visit */
+    int stream_per_peer; /* 0: every local peer shares one stream */
+    int n_pool;          /* synthetic token pool size (microbatch (t, k) uses entry (7 t + k) % n_pool) */
+    swarm_comm_t comm;   /* world communicator (NULL when world == 1) */
+} swarm_driver_config;
+typedef struct {
+    uint64_t records, visits, ticks, optimizer_steps, completed, captures, kernels;
+    uint32_t n_trainers;
+    size_t wire_bytes;
+    size_t visit_log_size;
+} swarm_driver_counters;
+typedef struct swarm_driver* swarm_driver_t;
+const char* swarm_driver_last_error(void);
+int swarm_driver_create(const swarm_driver_config* cfg, swarm_driver_t* out);
+void swarm_driver_destroy(swarm_driver_t d);
+/* process the driver's own engine records until n more microbatches completed */
+int swarm_driver_run(swarm_driver_t d, uint64_t n_microbatches, uint64_t* completed);
+/* the additive hook: one record from any engine that emits the same records in the same
+ * order (the driver's own, or the reference Engine patched as INTEGRATION.md §4 shows) */
+int swarm_driver_on_record(swarm_driver_t d, const swarm_engine_record* record);
+/* every peer stream waits for `stream` (start of a region) / `stream` waits for every peer
+ * stream and outstanding transfer (end of a region) */
+int swarm_driver_fork(swarm_driver_t d, swarm_stream_t stream);
+int swarm_driver_finish(swarm_driver_t d, swarm_stream_t stream);
+int swarm_driver_flush_wgrad(swarm_driver_t d);
+/* replace the token pool: device copy (host = 0), or pinned host buffers read by each
+ * consuming visit (host = 1: end-to-end mode; NULL pointers switch it off) */
+int swarm_driver_set_pool(swarm_driver_t d, const int32_t* tokens, const int32_t* targets, int n_pool, int host);
+int swarm_driver_pool(swarm_driver_t d, int32_t** tokens, int32_t** targets, int* n_pool, int* tokens_per_microbatch);
+float* swarm_driver_loss_sum(swarm_driver_t d); /* device float: token cross-entropy sum x loss scale */
+swarm_stage_t swarm_driver_stage(swarm_driver_t d, int peer); /* NULL when the peer is not on this rank */
+/* the peer's stream after joining its lanes (e.g. to read its loss) */
+swarm_stream_t swarm_driver_peer_stream(swarm_driver_t d, int peer);
+swarm_engine_t swarm_driver_engine(swarm_driver_t d);
+int swarm_driver_stats(swarm_driver_t d, swarm_driver_counters* stats);
+int swarm_driver_visit_log(swarm_driver_t d, size_t i, uint32_t* trainer, uint64_t* microbatch, uint32_t* stage,
+                           int* backward, int64_t* peer);
+int swarm_driver_peer_of_rank(swarm_driver_t d, int peer); /* the rank hosting `peer` */
+
 #ifdef __cplusplus
 }
 #endif

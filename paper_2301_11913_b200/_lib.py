@@ -45,6 +45,20 @@ class EngineRecord(C.Structure):
 
 ENG_START, ENG_HOP, ENG_DONE, ENG_ALLREDUCE = range(4)
 
+
+class DriverConfig(C.Structure):
+    _fields_ = [("model", StageConfigC), ("n_stages", C.c_int), ("world", C.c_int), ("rank", C.c_int),
+                ("layout", C.POINTER(C.c_int)), ("forward_seconds", C.c_double), ("backward_multiplier", C.c_double),
+                ("allreduce_period", C.c_double), ("allreduce_stall", C.c_double), ("duration_seconds", C.c_double),
+                ("trainers_per_peer", C.c_int), ("seed", C.c_uint64), ("lanes", C.c_int), ("pair_wgrad", C.c_int),
+                ("use_graphs", C.c_int), ("stream_per_peer", C.c_int), ("n_pool", C.c_int), ("comm", C.c_void_p)]
+
+
+class DriverCounters(C.Structure):
+    _fields_ = [(n, C.c_uint64) for n in ("records", "visits", "ticks", "optimizer_steps", "completed", "captures",
+                                          "kernels")] + [("n_trainers", C.c_uint32), ("wire_bytes", C.c_size_t),
+                                                         ("visit_log_size", C.c_size_t)]
+
 # (name, restype, argtypes) for every symbol include/swarm_b200.h declares
 P, SZ, I, U32P, U8P, F, D = C.c_void_p, C.c_size_t, C.c_int, C.c_void_p, C.c_void_p, C.c_float, C.c_double
 SIGNATURES = {
@@ -128,6 +142,37 @@ SIGNATURES = {
     "swarm_engine_n_trainers": (SZ, [P]),
     "swarm_engine_next": (I, [P, C.POINTER(EngineRecord), SZ, C.POINTER(SZ)]),
     "swarm_engine_summary": (I, [P, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64), P, SZ, C.POINTER(D)]),
+    "swarm_comm_last_error": (C.c_char_p, []),
+    "swarm_comm_nccl_version": (I, []),
+    "swarm_comm_unique_id": (I, [P]),
+    "swarm_comm_create": (I, [P, I, I, C.POINTER(P)]),
+    "swarm_comm_split": (I, [P, I, I, C.POINTER(P)]),
+    "swarm_comm_destroy": (None, [P]),
+    "swarm_comm_size": (I, [P, C.POINTER(I), C.POINTER(I)]),
+    "swarm_comm_group_start": (I, []),
+    "swarm_comm_group_end": (I, []),
+    "swarm_send_compressed": (I, [P, P, SZ, I, P]),
+    "swarm_recv_compressed": (I, [P, P, SZ, I, P]),
+    "swarm_allreduce_sum": (I, [P, P, SZ, I, P]),
+    "swarm_stage_allreduce": (I, [P, P, P]),
+    "swarm_driver_last_error": (C.c_char_p, []),
+    "swarm_driver_create": (I, [C.POINTER(DriverConfig), C.POINTER(P)]),
+    "swarm_driver_destroy": (None, [P]),
+    "swarm_driver_run": (I, [P, C.c_uint64, C.POINTER(C.c_uint64)]),
+    "swarm_driver_on_record": (I, [P, C.POINTER(EngineRecord)]),
+    "swarm_driver_fork": (I, [P, P]),
+    "swarm_driver_finish": (I, [P, P]),
+    "swarm_driver_flush_wgrad": (I, [P]),
+    "swarm_driver_set_pool": (I, [P, P, P, I, I]),
+    "swarm_driver_pool": (I, [P, C.POINTER(P), C.POINTER(P), C.POINTER(I), C.POINTER(I)]),
+    "swarm_driver_loss_sum": (P, [P]),
+    "swarm_driver_stage": (P, [P, I]),
+    "swarm_driver_peer_stream": (P, [P, I]),
+    "swarm_driver_engine": (P, [P]),
+    "swarm_driver_stats": (I, [P, C.POINTER(DriverCounters)]),
+    "swarm_driver_visit_log": (I, [P, SZ, C.POINTER(C.c_uint32), C.POINTER(C.c_uint64), C.POINTER(C.c_uint32),
+                                   C.POINTER(I), C.POINTER(C.c_int64)]),
+    "swarm_driver_peer_of_rank": (I, [P, I]),
 }
 
 _lib = None

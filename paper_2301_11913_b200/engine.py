@@ -67,9 +67,19 @@ class Engine:
         self.n_trainers = L.swarm_engine_n_trainers(h)
         self._buf = (_lib.EngineRecord * 1024)()
 
+    @classmethod
+    def borrow(cls, handle: int, cfg: EngineConfig) -> "Engine":
+        """A view of an engine owned by the C++ driver (never destroyed here)."""
+        e = cls.__new__(cls)
+        e.cfg, e.h, e._borrowed = cfg, C.c_void_p(handle), True
+        e.n_workers = len(cfg.worker_stages())
+        e.n_trainers = _lib.lib().swarm_engine_n_trainers(e.h)
+        e._buf = (_lib.EngineRecord * 1024)()
+        return e
+
     def __del__(self):
         try:
-            if getattr(self, "h", None):
+            if getattr(self, "h", None) and not getattr(self, "_borrowed", False):
                 _lib.lib().swarm_engine_destroy(self.h)
                 self.h = None
         except Exception:  # interpreter shutdown

@@ -70,7 +70,11 @@ def hop_action(pl: Placement, S: int, r, rank: int):
     return None
 
 
-class EngineExecutor:
+class PyEngineExecutor:
+    """The executor's record walk in Python over torch.distributed (round 1's data
+    plane), kept as an independent host implementation to cross-check the C++
+    driver (EngineExecutor below) against: same engine, same visits, same gradients."""
+
     def __init__(self, mcfg: ModelConfig, n_stages: int = 4, *, trainers_per_peer: int = 1, seed: int = 0,
                  lr: float = 1e-4, weight_decay: float = 0.0, forward_seconds: float = 1.0,
                  backward_multiplier: float = 2.0, allreduce_period: float = 0.0, allreduce_stall: float = 0.0,
@@ -448,7 +452,193 @@ class EngineExecutor:
         return L.lib().swarm_launch_count() - self.captured_kernels + self.replayed_kernels
 
 
-def sequential_reference_grads(ex: EngineExecutor) -> dict:
+class EngineExecutor:
+    """The engine-driven executor: a thin handle on the C++ host driver
+    (csrc/driver.cpp, include/swarm_b200.h swarm_driver_*), which walks the engine's
+    records and issues the visits, the NCCL transfers of the wire messages and the
+    stage all-reduces itself.  Python only supplies the NCCL unique id exchange
+    and torch views of driver-owned memory."""
+
+    def __init__(self, mcfg: ModelConfig, n_stages: int = 4, *, trainers_per_peer: int = 1, seed: int = 0,
+                 lr: float = 1e-4, weight_decay: float = 0.0, forward_seconds: float = 1.0,
+                 backward_multiplier: float = 2.0, allreduce_period: float = 0.0, allreduce_stall: float = 0.0,
+                 duration_seconds: float = 1e9, use_graphs: bool = True, n_pool: int = 16,
+                 tokens: torch.Tensor | None = None, targets: torch.Tensor | None = None, pair_wgrad: bool = True,
+                 stream_per_peer: bool = True, lanes: int = 1, fp32: bool = False):
+        import ctypes as C
+
+        from .stage import device_view
+        self.m = mcfg
+        self.S = n_stages
+        self.seed = seed
+        self.world = dist.get_world_size() if dist.is_initialized() else 1
+        self.rank = dist.get_rank() if dist.is_initialized() else 0
+        self.device = torch.device("cuda", torch.cuda.current_device())
+        self.pl = Placement(self.world, n_stages)
+        if lanes > 1 and not stream_per_peer:
+            raise ValueError("lanes need a stream per peer")
+        self.lib = L.lib()
+        self.comm = None
+        if self.world > 1:
+            uid = torch.zeros(128, dtype=torch.uint8)
+            if self.rank == 0:
+                L.check(self.lib.swarm_comm_unique_id(C.c_void_p(uid.data_ptr())), "comm_unique_id")
+            t = uid.to(self.device)
+            dist.broadcast(t, 0)
+            uid = t.cpu()
+            h = C.c_void_p()
+            rc = self.lib.swarm_comm_create(C.c_void_p(uid.data_ptr()), self.world, self.rank, C.byref(h))
+            if rc:
+                raise RuntimeError("comm_create: " + self.lib.swarm_comm_last_error().decode())
+            self.comm = h
+        self.stage_cfg = StageConfig(d_model=mcfg.d_model, n_heads=mcfg.n_heads, d_ffn=mcfg.d_ffn,
+                                     seq_len=mcfg.seq_len, micro_batch=mcfg.micro_batch,
+                                     n_layers=mcfg.layers_per_stage, shared_layers=mcfg.shared_layers,
+                                     vocab=mcfg.vocab, causal=mcfg.causal, wire=mcfg.wire,
+                                     block_size=mcfg.block_size, maxout_k=mcfg.maxout_k, lr=lr,
+                                     weight_decay=weight_decay, fp32=int(fp32))
+        c = L.DriverConfig()
+        c.model = self.stage_cfg.to_c()
+        c.n_stages, c.world, c.rank = n_stages, self.world, self.rank
+        c.forward_seconds, c.backward_multiplier = forward_seconds, backward_multiplier
+        c.allreduce_period, c.allreduce_stall, c.duration_seconds = allreduce_period, allreduce_stall, duration_seconds
+        c.trainers_per_peer, c.seed, c.lanes = trainers_per_peer, seed, lanes
+        c.pair_wgrad, c.use_graphs, c.stream_per_peer = int(pair_wgrad), int(use_graphs), int(stream_per_peer)
+        c.n_pool = n_pool if tokens is None else int(tokens.shape[0])
+        c.comm = self.comm
+        h = C.c_void_p()
+        rc = self.lib.swarm_driver_create(C.byref(c), C.byref(h))
+        if rc:
+            msg = self.lib.swarm_driver_last_error().decode()
+            if rc == L.SWARM_E_INVALID:
+                from ._swarmsim_b200 import ConfigError
+                raise ConfigError(msg)
+            raise RuntimeError(msg)
+        self.h = h
+        self.lanes = lanes
+        self.ecfg = EngineConfig(n_stages=n_stages, initial_peers=[[1.0] * self.pl.layout[s] for s in range(n_stages)],
+                                 forward_service_seconds=forward_seconds, backward_multiplier=backward_multiplier,
+                                 trainers_per_peer=trainers_per_peer, allreduce_period=allreduce_period,
+                                 allreduce_stall=allreduce_stall, duration_seconds=duration_seconds,
+                                 bucket_seconds=max(duration_seconds / 64, 1e-9))
+        self.engine = Engine.borrow(self.lib.swarm_driver_engine(h), self.ecfg)
+        self.T = self.engine.n_trainers
+        self.local = [pid for pid in range(len(self.pl.stage_of)) if self.pl.rank_of_peer(pid) == self.rank]
+        self.stages: dict[int, Stage] = {}
+        for pid in self.local:
+            s = self.pl.stage_of_peer(pid)
+            cfg = StageConfig(**{**self.stage_cfg.__dict__, "is_first": int(s == 0), "is_last": int(s == n_stages - 1),
+                                 "max_slots": self.T, "seed": seed * 1000 + s})
+            self.stages[pid] = Stage.borrow(self.lib.swarm_driver_stage(h, pid), cfg, self.device)
+        self.loss_sum = device_view(self.lib.swarm_driver_loss_sum(h), 1, torch.float32, self.device)
+        if tokens is not None:
+            tokens = tokens.to(self.device, torch.int32).contiguous()
+            targets = targets.to(self.device, torch.int32).contiguous()
+            L.check(self.lib.swarm_driver_set_pool(h, C.c_void_p(tokens.data_ptr()), C.c_void_p(targets.data_ptr()),
+                                                   int(tokens.shape[0]), 0), "driver_set_pool")
+        tp, gp, npool, ntok = C.c_void_p(), C.c_void_p(), C.c_int(), C.c_int()
+        self.lib.swarm_driver_pool(h, C.byref(tp), C.byref(gp), C.byref(npool), C.byref(ntok))
+        self.pool_tok = device_view(tp.value, npool.value * ntok.value, torch.int32, self.device).view(npool.value, -1)
+        self.pool_tgt = device_view(gp.value, npool.value * ntok.value, torch.int32, self.device).view(npool.value, -1)
+        self._host_pool = None
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.lib.swarm_driver_destroy(self.h)
+            self.h = None
+        if getattr(self, "comm", None):
+            self.lib.swarm_comm_destroy(self.comm)
+            self.comm = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def _check(self, rc: int, what: str) -> None:
+        if rc:
+            raise RuntimeError(f"{what}: {self.lib.swarm_driver_last_error().decode()}")
+
+    def _counters(self):
+        import ctypes as C
+        k = L.DriverCounters()
+        self._check(self.lib.swarm_driver_stats(self.h, C.byref(k)), "driver_stats")
+        return k
+
+    records = property(lambda self: self._counters().records)
+    optimizer_steps = property(lambda self: self._counters().optimizer_steps)
+    ticks = property(lambda self: self._counters().ticks)
+    captures = property(lambda self: self._counters().captures)
+    completed = property(lambda self: self._counters().completed)
+    visits_local = property(lambda self: self._counters().visits)
+
+    def _pool_index(self, t: int, k: int) -> int:
+        return (t * 7 + k) % self.pool_tok.shape[0]
+
+    @property
+    def visit_log(self) -> list:
+        """(trainer, microbatch, stage, backward, peer) of every visit, in record order."""
+        import ctypes as C
+        out = []
+        t, k, s, b, p = C.c_uint32(), C.c_uint64(), C.c_uint32(), C.c_int(), C.c_int64()
+        for i in range(self._counters().visit_log_size):
+            self.lib.swarm_driver_visit_log(self.h, i, C.byref(t), C.byref(k), C.byref(s), C.byref(b), C.byref(p))
+            out.append((t.value, k.value, s.value, bool(b.value), p.value))
+        return out
+
+    @property
+    def bwd_log(self) -> list:
+        logs = [[] for _ in range(self.S)]
+        for t, k, s, b, _ in self.visit_log:
+            if b:
+                logs[s].append((t, k))
+        return logs
+
+    def run(self, n_microbatches: int) -> int:
+        import ctypes as C
+        self.fork()  # peer streams start after whatever the caller queued (e.g. a loss reset)
+        done = C.c_uint64()
+        self._check(self.lib.swarm_driver_run(self.h, n_microbatches, C.byref(done)), "driver_run")
+        return done.value
+
+    def fork(self) -> None:
+        self._check(self.lib.swarm_driver_fork(self.h, torch.cuda.current_stream().cuda_stream), "driver_fork")
+
+    def finish(self) -> None:
+        self._check(self.lib.swarm_driver_finish(self.h, torch.cuda.current_stream().cuda_stream), "driver_finish")
+
+    def flush_wgrad(self) -> None:
+        self._check(self.lib.swarm_driver_flush_wgrad(self.h), "driver_flush_wgrad")
+
+    def use_host_pool(self, enable: bool = True) -> None:
+        """End-to-end mode: every microbatch's tokens / targets are copied from pinned
+        host memory by the visit that consumes them."""
+        import ctypes as C
+        if enable:
+            self._host_pool = (self.pool_tok.cpu().pin_memory(), self.pool_tgt.cpu().pin_memory())
+            ht, hg = self._host_pool
+            self._check(self.lib.swarm_driver_set_pool(self.h, C.c_void_p(ht.data_ptr()), C.c_void_p(hg.data_ptr()),
+                                                       ht.shape[0], 1), "driver_set_pool")
+        else:
+            self.finish()
+            torch.cuda.current_stream().synchronize()
+            self._check(self.lib.swarm_driver_set_pool(self.h, None, None, 1, 1), "driver_set_pool")
+            self._host_pool = None
+
+    def last_stage_stream(self):
+        """A stream ordered after every lane of this rank's last-stage peer (it owns
+        loss_sum), or None."""
+        for pid in self.local:
+            if self.pl.stage_of_peer(pid) == self.S - 1:
+                return torch.cuda.ExternalStream(self.lib.swarm_driver_peer_stream(self.h, pid), device=self.device)
+        return None
+
+    def kernels_launched(self) -> int:
+        return self._counters().kernels
+
+
+def sequential_reference_grads(ex) -> dict:
     """Verification helper: every peer's gradient over exactly the visits the
     schedule ran on it, recomputed sequentially on fresh replicas (same seeds,
     one slot, no optimizer step), one microbatch at a time along its route.

@@ -86,10 +86,21 @@ class Stage:
         self.n_params = int(self.lib.swarm_stage_num_params(h))
         self.wire_bytes = int(self.lib.swarm_stage_wire_bytes(h))
 
+    @classmethod
+    def borrow(cls, handle: int, cfg: StageConfig, device: torch.device) -> "Stage":
+        """A view of a stage owned by someone else (the C++ driver): never destroyed here."""
+        st = cls.__new__(cls)
+        st.cfg, st.device, st.lib = cfg, device, L.lib()
+        st.h = C.c_void_p(handle)
+        st._borrowed = True
+        st.n_params = int(st.lib.swarm_stage_num_params(st.h))
+        st.wire_bytes = int(st.lib.swarm_stage_wire_bytes(st.h))
+        return st
+
     def close(self):
-        if getattr(self, "h", None):
+        if getattr(self, "h", None) and not getattr(self, "_borrowed", False):
             self.lib.swarm_stage_destroy(self.h)
-            self.h = None
+        self.h = None
 
     def __del__(self):
         try:

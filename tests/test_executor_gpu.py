@@ -69,3 +69,50 @@ def test_executor_maxout_shared_layers_with_lanes(cuda, lanes):
     ref = sequential_reference_grads(ex)
     for pid, st in ex.stages.items():
         assert rel(st.grads(), ref[pid]) <= 1e-4, (pid, rel(st.grads(), ref[pid]))
+
+
+@pytest.mark.parametrize("lanes", [1, 2])
+@pytest.mark.parametrize("S,tpp", [(2, 2), (4, 1)])
+def test_native_driver_matches_python_orchestrator(cuda, S, tpp, lanes):
+    """Two independent host implementations of the data plane — the C++ driver
+    (csrc/driver.cpp) and the Python record walk (PyEngineExecutor) — run the same
+    engine schedule on the same pool: same visit log, same gradients (up to the
+    fp32 summation order of concurrent atomic accumulation)."""
+    import torch
+    from paper_2301_11913_b200.executor import EngineExecutor, PyEngineExecutor
+    from paper_2301_11913_b200.swarm import PRESETS
+    nat = EngineExecutor(PRESETS["tiny"], S, trainers_per_peer=tpp, seed=9, n_pool=4, lanes=lanes)
+    py = PyEngineExecutor(PRESETS["tiny"], S, trainers_per_peer=tpp, seed=9, lanes=lanes,
+                          tokens=nat.pool_tok.cpu(), targets=nat.pool_tgt.cpu())
+    assert nat.run(9) == 9 and py.run(9) == 9
+    nat.finish()
+    py.finish()
+    nat.flush_wgrad()
+    py.flush_wgrad()
+    torch.cuda.synchronize()
+    assert nat.visit_log == [(t, k, s, b, p) for t, k, s, b, p in py.visit_log]
+    assert abs(nat.loss_sum.item() - py.loss_sum.item()) <= 1e-5 * abs(py.loss_sum.item())
+    for pid in nat.stages:
+        g1, g2 = nat.stages[pid].grads(), py.stages[pid].grads()
+        assert rel(g1, g2) <= 1e-5, (pid, rel(g1, g2))
+
+
+def test_lanes_do_not_change_the_result_across_ticks(cuda):
+    """the lane join / fork around ALLREDUCE ticks.  The same schedule with
+    ticks at lanes = 1 and lanes = 2: after several ticks (all-reduce + AdamW) the
+    parameters agree within fp32 summation-order noise."""
+    import torch
+    from paper_2301_11913_b200.executor import EngineExecutor
+    from paper_2301_11913_b200.swarm import PRESETS
+    runs = []
+    for lanes in (1, 2):
+        ex = EngineExecutor(PRESETS["tiny"], 4, trainers_per_peer=2, seed=4, lr=1e-3, n_pool=3, lanes=lanes,
+                            allreduce_period=10.0, allreduce_stall=0.1)
+        ex.run(24)
+        ex.finish()
+        torch.cuda.synchronize()
+        assert ex.optimizer_steps >= 4
+        runs.append({pid: st.params().clone() for pid, st in ex.stages.items()})
+        runs[-1]["loss"] = ex.loss_sum.clone()
+    for pid in runs[0]:
+        assert rel(runs[1][pid], runs[0][pid]) <= 1e-5, pid
