@@ -1,6 +1,9 @@
 """torchrun check of the engine-driven executor on N GPUs (NCCL): each rank's
 stage gradients after K microbatches (no tick) equal a sequential recomputation
-of exactly the visits the schedule ran.  Prints one line per rank; exit 1 on mismatch."""
+of exactly the visits the schedule ran; with ticks (stage all-reduce + AdamW) the
+C++ driver (EngineExecutor, raw NCCL) and the Python orchestrator
+(PyEngineExecutor, torch.distributed) end with the same parameters.  Prints one
+line per rank; exit 1 on mismatch."""
 import os
 import sys
 
@@ -8,7 +11,7 @@ import torch
 import torch.distributed as dist
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-from paper_2301_11913_b200.executor import EngineExecutor, sequential_reference_grads  # noqa: E402
+from paper_2301_11913_b200.executor import EngineExecutor, PyEngineExecutor, sequential_reference_grads  # noqa: E402
 from paper_2301_11913_b200.swarm import PRESETS  # noqa: E402
 
 local = int(os.environ.get("LOCAL_RANK", "0"))
@@ -37,6 +40,16 @@ ex2.run(40)
 ex2.finish()
 torch.cuda.synchronize()
 print(f"rank {dist.get_rank()} ticks {ex2.ticks} steps {ex2.optimizer_steps} loss {ex2.loss_sum.item():.4f}", flush=True)
+py2 = PyEngineExecutor(PRESETS["tiny"], S, trainers_per_peer=tpp, seed=3, lr=3e-3, allreduce_period=12.0,
+                       allreduce_stall=0.1, lanes=lanes, tokens=ex2.pool_tok.cpu(), targets=ex2.pool_tgt.cpu())
+py2.run(40)
+py2.finish()
+torch.cuda.synchronize()
+for pid, st in ex2.stages.items():
+    r = float((st.params() - py2.stages[pid].params()).norm() / py2.stages[pid].params().norm())
+    ok &= r <= 1e-4
+    print(f"rank {dist.get_rank()} peer {pid}: C++ driver vs Python orchestrator params after "
+          f"{ex2.optimizer_steps} optimizer steps: rel {r:.3e}", flush=True)
 dist.barrier()
 dist.destroy_process_group()
 sys.exit(0 if ok else 1)
