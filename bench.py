@@ -729,29 +729,33 @@ def bench_train(args, world, rank, local):
 
 
 # ----------------------------------------------------------------- engine
-def bench_engine(args, world, rank, local):
+def run_engine(args, world, rank, local, model: str, S: int, steps: int, warmup: int, *, fp32: bool = False,
+               profile: bool = True, e2e_steps: int = 3) -> dict:
     """asynchronous SWARM training driven by the reference's event
-    engine (csrc/engine.cpp, decision-identical to sim::run): trainers keep one
-    microbatch each in flight, peers serve FIFO queues, stage peers all-reduce +
-    AdamW at every AllReduceTick.  A "step" = M microbatch completions (the same
-    65,536 tokens as the train workload); the tick period is sized so a stage serves
-    ~M microbatches between ticks."""
+    engine (csrc/engine.cpp, decision-identical to sim::run) and executed by the C++
+    host driver (csrc/driver.cpp): trainers keep one microbatch each in flight, peers
+    serve FIFO queues, wire messages move over raw NCCL, stage peers all-reduce +
+    AdamW at every AllReduceTick.  A "step" = M microbatch completions; the tick
+    period is sized so a stage serves ~M microbatches between ticks."""
+    import argparse as _ap
+    import dataclasses
+
     import torch
 
+    from paper_2301_11913_b200.engine import Engine, EngineConfig
     from paper_2301_11913_b200.executor import EngineExecutor
-    from paper_2301_11913_b200.swarm import Placement  # noqa: F811
+    from paper_2301_11913_b200.swarm import Placement
     dev = torch.device("cuda", local)
     torch.cuda.set_device(dev)
-    mcfg = model_config(args)
-    S, M = args.stages, args.microbatches
-    P = Placement(world, S).P
+    margs = _ap.Namespace(model=model, micro_batch=getattr(args, "micro_batch", None) if model == args.model else None)
+    mcfg = model_config(margs)
+    M = args.microbatches
+    pl = Placement(world, S)
+    P = pl.P
     bm = 2.0
     # tick period: M microbatch completions of the engine's own schedule (its virtual
     # completion rate for this layout, from a throwaway run without ticks), so every
-    # stage takes one optimizer step per M microbatches = 65,536 tokens, as the
-    # synchronous step does
-    from paper_2301_11913_b200.engine import Engine, EngineConfig
-    pl = Placement(world, S)
+    # stage takes one optimizer step per M microbatches
     horizon = 400.0 * M * (1.0 + bm) / P
     cal = Engine(EngineConfig(n_stages=S, initial_peers=[[1.0] * pl.layout[s] for s in range(S)],
                               forward_service_seconds=1.0, backward_multiplier=bm,
@@ -762,13 +766,12 @@ def bench_engine(args, world, rank, local):
     period = M * horizon / max(cal.summary()["completed"], 1)
     ex = EngineExecutor(mcfg, S, trainers_per_peer=args.trainers_per_peer, seed=1, lr=1e-4, forward_seconds=1.0,
                         backward_multiplier=bm, allreduce_period=period, allreduce_stall=0.05,
-                        stream_per_peer=not args.single_stream, lanes=args.lanes)
+                        stream_per_peer=not args.single_stream, lanes=args.lanes, fp32=fp32)
     stream = torch.cuda.current_stream()
-    # untimed warm-up: W steps plus two more (eight more with several peers per stage,
-    # whose routes mix trainer pairs more), so that the visit graphs of most (peer,
-    # trainer pair, lane) combinations are captured before the timed region (a capture
-    # inside it costs host time: 29 per rank measured -2.7% at 2 stages x 2 peers)
-    ex.run(M * (args.warmup + (8 if P > 1 else 2)))
+    # untimed warm-up: W steps plus two more (eight more with several peers per stage, whose
+    # routes mix trainer pairs more), so that the visit graphs of most (peer, trainer pair, lane)
+    # combinations are captured before the timed region
+    ex.run(M * (warmup + (8 if P > 1 else 2)))
     ex.finish()
     torch.cuda.synchronize()
     ex.loss_sum.zero_()
@@ -782,69 +785,138 @@ def bench_engine(args, world, rank, local):
     t0 = torch.cuda.Event(enable_timing=True)
     t1 = torch.cuda.Event(enable_timing=True)
     t0.record(stream)
-    ex.fork()
-    done = ex.run(M * args.steps)
+    done = ex.run(M * steps)
     v1, r1, t_1, c1 = ex.engine.summary()["now"], ex.records, ex.optimizer_steps, ex.captures
     ex.finish()
     t1.record(stream)
     torch.cuda.synchronize()
     barrier(world)
     clocks = clk.stop()
-    ms = max_over_ranks(t0.elapsed_time(t1), world)
+    launches = int(ex.kernels_launched() - n0)
+    ms_rank = t0.elapsed_time(t1)
+    ms = max_over_ranks(ms_rank, world)
     tokens = done * mcfg.tokens
     value = tokens / (ms / 1e3)
     loss = ex.loss_sum.clone()
     if world > 1:
         import torch.distributed as dist
         dist.all_reduce(loss)
-    # e2e: every microbatch's tokens / targets H2D from pinned host memory inside the
-    # visit that consumes them, the loss D2H after every step's M completions
-    e2e_steps = max(1, min(args.steps, 3))
-    ex.use_host_pool(True)
-    hloss = torch.empty(1, dtype=torch.float32).pin_memory()
-    lst = ex.last_stage_stream()
-    ex.run(M)  # untimed: warm the host-pool path
-    ex.finish()
-    barrier(world)
-    torch.cuda.synchronize()
-    w0 = time.perf_counter()
-    e2e_done = 0
-    for _ in range(e2e_steps):
-        e2e_done += ex.run(M)
-        if lst is not None:
-            with torch.cuda.stream(lst):
-                hloss.copy_(ex.loss_sum, non_blocking=True)
-    ex.finish()
-    torch.cuda.synchronize()
-    e2e_s = max_over_ranks(time.perf_counter() - w0, world)
-    ex.use_host_pool(False)
-    P_ = Placement(world, S)
-    line = {
-        "metric": "training tokens/s (SWARM pipeline)", "value": value,
-        "unit": "tokens/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
-        "dtype": "bf16", "data": "synthetic tokens uniform over the vocab (per-trainer pool), random-init weights",
-        "config": train_config(args, world),
-        "run": {"execution": "asynchronous SWARM: the reference DES engine's record order (csrc/engine.cpp, "
-                             "decision-identical to sim::run), one compute stream per peer, NCCL send/recv "
-                             "of int8 wire messages, stage all-reduce + AdamW at every AllReduceTick",
-                "trainers": ex.T, "trainers_per_peer": args.trainers_per_peer, "lanes_per_peer": args.lanes,
-                "schedule": "forward 1.0 / backward 2.0 virtual s, AllReduceTick every "
-                            f"{period:.4g} virtual s (= {M} completions at the schedule's own rate: one optimizer "
-                            f"step per stage per {M} microbatches); one step = {M} microbatch completions",
-                "optimizer": "AdamW (fused, fp32 master), paired weight gradients",
-                "mean_loss": float(loss.item()) / max(tokens, 1),
-                "model_tflops_per_s": value * mcfg.flops_per_token(S) / 1e12},
-        "engine": {"records": r1 - r0, "virtual_seconds": v1 - v0, "optimizer_steps_rank": t_1 - t_0,
-                   "microbatches": done, "graph_captures_in_timed_region_rank0": c1 - c0},
-        "e2e": {"value": e2e_done * mcfg.tokens / e2e_s, "unit": "tokens/s",
-                "h2d_bytes_per_step": int(M * mcfg.tokens * 4 * 2),
-                "d2h_bytes_per_step": 4, "path": "EngineExecutor.run with each microbatch's tokens / targets copied "
-                                                 "from pinned host memory by its consuming visit and the loss read "
-                                                 "back after every step (wall clock, max over ranks)"},
-        "gpu_launches": int(ex.kernels_launched() - n0), "clocks": clocks,
-    }
+    res = {"value": value, "ms_per_step": ms / steps, "steps": steps, "warmup": warmup, "clocks": clocks,
+           "gpu_launches": launches, "tokens_per_step": M * mcfg.tokens,
+           "run": {"execution": "asynchronous SWARM: the reference DES engine's record order (csrc/engine.cpp, "
+                                "decision-identical to sim::run) walked by the C++ host driver (csrc/driver.cpp), one "
+                                "compute stream per peer, raw-NCCL send/recv of int8 wire messages, stage all-reduce "
+                                "+ AdamW at every AllReduceTick",
+                   "arithmetic": "fp32 (SIMT fp32 GEMMs, fp32 activations)" if fp32 else
+                                 "bf16 storage, tcgen05 GEMMs with fp32 accumulation",
+                   "placement": placement_str(world, S), "trainers": ex.T,
+                   "trainers_per_peer": args.trainers_per_peer, "lanes_per_peer": args.lanes,
+                   "schedule": "forward 1.0 / backward 2.0 virtual s, AllReduceTick every "
+                               f"{period:.4g} virtual s (= {M} completions at the schedule's own rate: one optimizer "
+                               f"step per stage per {M} microbatches); one step = {M} microbatch completions",
+                   "optimizer": "AdamW (fused, fp32 master), paired weight gradients",
+                   "mean_loss": float(loss.item()) / max(tokens, 1),
+                   "model_tflops_per_s": value * mcfg.flops_per_token(S) / 1e12,
+                   "model_flops_per_token": mcfg.flops_per_token(S)},
+           "engine": {"records": r1 - r0, "virtual_seconds": v1 - v0, "optimizer_steps_rank": t_1 - t_0,
+                      "microbatches": done, "graph_captures_in_timed_region_rank0": c1 - c0}}
+    # e2e: every microbatch's tokens / targets H2D from pinned host memory inside the visit
+    # that consumes them, the loss D2H after every step's M completions
+    if e2e_steps > 0:
+        ex.use_host_pool(True)
+        hloss = torch.empty(1, dtype=torch.float32).pin_memory()
+        lst = ex.last_stage_stream()
+        ex.run(M)  # untimed: warm the host-pool path
+        ex.finish()
+        barrier(world)
+        torch.cuda.synchronize()
+        w0 = time.perf_counter()
+        e2e_done = 0
+        rd = torch.cuda.Stream()  # a torch-owned stream reads the loss (the driver's streams die with it)
+        for _ in range(e2e_steps):
+            e2e_done += ex.run(M)
+            if lst is not None:
+                rd.wait_stream(lst)
+                with torch.cuda.stream(rd):
+                    hloss.copy_(ex.loss_sum, non_blocking=True)
+        ex.finish()
+        torch.cuda.synchronize()
+        e2e_s = max_over_ranks(time.perf_counter() - w0, world)
+        ex.use_host_pool(False)
+        res["e2e"] = {"value": e2e_done * mcfg.tokens / e2e_s, "unit": "tokens/s",
+                      "h2d_bytes_per_step": int(M * mcfg.tokens * 4 * 2), "d2h_bytes_per_step": 4,
+                      "path": "EngineExecutor.run (C++ driver) with each microbatch's tokens / targets copied from "
+                              "pinned host memory by its consuming visit and the loss read back after every step "
+                              "(wall clock, max over ranks)"}
+    if profile:
+        # live roofline: one more step as a profiled region -- every visit eager on one stream behind
+        # a GPU spin, CUDA events around every kernel -- so each GEMM is timed alone
+        pr = ex.profile(M)
+        pk = peaks()
+        achieved = pr["gemm_flops"] / (pr["gemm_ms"] / 1e3) / 1e12 if pr["gemm_ms"] > 0 else 0.0
+        kern_ms = sum(v[0] for v in pr["categories"].values())
+        traffic = {}
+        prof = os.path.join(ROOT, "profiles", "ncu_gemm_qkv_traffic.json")
+        if os.path.exists(prof):
+            with open(prof) as f:
+                traffic = json.load(f)
+        res["roofline"] = {
+            "bound": "tensor", "kernel": "k_gemm / k_gemm2 (tcgen05 bf16: every block, attention and head GEMM)",
+            "achieved": achieved, "peak": pk["bf16_tflops"], "unit": "TFLOP/s", "frac": achieved / pk["bf16_tflops"],
+            "frac_of_sustained_peak": achieved / (pk["bf16_tflops_sustained"] or pk["bf16_tflops"]),
+            "traffic": traffic.get("dram_bytes_per_launch"), "traffic_note": traffic.get("note"),
+            "peak_source": pk["source"] + " bf16 burst (the kernels are timed alone)",
+            "gemm_ms_per_step": pr["gemm_ms"], "gemm_flops_per_step": pr["gemm_flops"],
+            "gemm_launches_per_step": pr["gemm_launches"],
+            "gemm_share_of_kernel_time": pr["gemm_ms"] / kern_ms if kern_ms else None,
+            "note": "one extra step of the same engine-driven run as a profiled region: every visit issued eagerly "
+                    "on one stream behind a GPU spin (swarm_driver_profile_begin), CUDA events around each kernel; "
+                    "achieved = executed GEMM FLOPs / summed GEMM event time of that step (this rank)"}
+        res["step_breakdown"] = {
+            "note": "isolated kernel time per category over one profiled step (this rank, kernels serialised); the "
+                    "headline step overlaps peers' kernels on several streams, so the sum can exceed ms_per_step",
+            **{c: {"ms_per_step": v[0], "launches": int(v[1])} for c, v in pr["categories"].items()}}
+    res["_ex"] = ex
+    return res
+
+
+def bench_engine(args, world, rank, local):
+    """The headline: BASELINE configs[2] (or --model) through the C++ driver (run_engine)."""
+    S = args.stages
+    r = run_engine(args, world, rank, local, args.model, S, args.steps, args.warmup)
+    r.pop("_ex")
+    mcfg = shape_of(args)
+    line = {"metric": "training tokens/s (SWARM pipeline)", "value": r["value"], "unit": "tokens/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": r["ms_per_step"],
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
+            "data": "synthetic tokens uniform over the vocab (per-trainer pool), random-init weights",
+            "config": train_config(args, world), **{k: r[k] for k in ("run", "engine", "e2e", "gpu_launches",
+                                                                      "clocks", "roofline", "step_breakdown")
+                                                   if k in r}}
+    line["cost_model"] = cost_model_report(model_config(args), S, args.microbatches, world,
+                                           (r["ms_per_step"] / 1e3), measure_link(world, rank))
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        tok_s, thr, sample = cpu_block_baseline(mcfg)
+        line["cpu_baseline"] = {"value": tok_s, "unit": "tokens/s", "cores": thr, "kind": "port", "sample": sample}
     return line
+
+
+def sub_config(args, world, model, S, which, steps, warmup, fp32=False) -> dict:
+    """A second BASELINE config measured in the same run (a sub-object of the line)."""
+    import gc
+
+    import torch
+    ns = argparse.Namespace(**{**vars(args), "model": model, "stages": S, "micro_batch": None})
+    r = run_engine(ns, world, int(os.environ.get("RANK", "0")), int(os.environ.get("LOCAL_RANK", "0")), model, S,
+                   steps, warmup, fp32=fp32, profile=not fp32, e2e_steps=1)
+    r.pop("_ex")
+    gc.collect()
+    torch.cuda.empty_cache()
+    out = {"metric": "training tokens/s (SWARM pipeline)", "value": r["value"], "unit": "tokens/s",
+           "ms_per_step": r["ms_per_step"], "steps": steps, "warmup": warmup, "dtype": "f32" if fp32 else "bf16",
+           "config": {**train_config(ns, world), "which": which},
+           **{k: r[k] for k in ("run", "e2e", "gpu_launches", "clocks", "roofline") if k in r}}
+    return out
 
 
 # ----------------------------------------------------------------- failure
@@ -968,7 +1040,9 @@ def main():
     ap.add_argument("--steps", type=int, default=None)
     ap.add_argument("--warmup", type=int, default=None)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="train", choices=["train", "codec", "failure", "engine"])
+    ap.add_argument("--workload", default="train", choices=["train", "codec", "failure", "engine"],
+                    help="train (default): the engine-driven headline + codec + configs[0] / configs[3] sub-lines; "
+                         "engine: the headline only")
     ap.add_argument("--trainers-per-peer", type=int, default=2, help="engine: trainers per peer (sim trainers_per_peer)")
     ap.add_argument("--single-stream", action="store_true", help="engine: one compute stream per GPU (not per peer)")
     ap.add_argument("--lanes", type=int, default=None,
@@ -983,6 +1057,7 @@ def main():
     ap.add_argument("--stages", type=int, default=TRAIN_STAGES, help="pipeline stages (default 4, SURVEY §8(d))")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-codec", action="store_true", help="train: skip the codec sub-measurement")
+    ap.add_argument("--no-extra", action="store_true", help="train: skip the configs[0] / configs[3] sub-lines")
     ap.add_argument("--sync", action="store_true",
                     help="train: headline = the synchronous GPipe step (default: the asynchronous engine-driven "
                          "pipeline, with the GPipe step reported beside it)")
@@ -1005,42 +1080,31 @@ def main():
         line = bench_failure(args, world, rank, local)
     elif args.workload == "engine":
         line = bench_engine(args, world, rank, local)
+    elif args.sync:
+        line = bench_train(args, world, rank, local)
     else:
-        g = bench_train(args, world, rank, local)
-        if args.sync:
-            line = g
-        else:
-            # headline: the asynchronous engine-driven pipeline; the synchronous
-            # GPipe step of the same model is measured first and reported beside it, and the GEMM
-            # roofline / kernel breakdown / cost model / CPU baseline come from its profiled steps
-            import gc
+        # headline: the asynchronous engine-driven pipeline through the C++ driver,
+        # with its live roofline, e2e, cost model and CPU baseline; then the other BASELINE configs
+        import gc
 
-            import torch
-            gc.collect()
-            torch.cuda.empty_cache()
-            try:
-                line = bench_engine(args, world, rank, local)
-            except Exception as e:  # keep the measured synchronous line rather than no line
-                line = dict(g)
-                line["engine_async_error"] = repr(e)[:400]
-                g = {}
-            for k in ("roofline", "step_breakdown", "cost_model", "step_phases_ms", "cpu_baseline"):
-                if k in g:
-                    line[k] = g[k]
-            if g:
-                line["roofline"]["note"] = ("measured on the synchronous step's profiled visits (same kernels, same "
-                                            "shapes): " + line["roofline"]["note"])
-                line["gpipe_sync"] = {k: g[k] for k in ("value", "ms_per_step", "steps", "e2e", "gpu_launches",
-                                                        "clocks")}
-                line["gpipe_sync"]["note"] = ("the same workload as one synchronous GPipe optimizer step over 32 "
-                                              "microbatches (bench.py --sync); paired weight gradients")
-            gc.collect()
-            torch.cuda.empty_cache()
+        import torch
+        line = bench_engine(args, world, rank, local)
+        gc.collect()
+        torch.cuda.empty_cache()
         if not args.no_codec:
             c = bench_codec(argparse.Namespace(steps=200, warmup=5, no_cpu_baseline=args.no_cpu_baseline, e2e_steps=2),
                             world, rank, local)
             line["codec"] = {k: c[k] for k in ("metric", "value", "unit", "ms_per_step", "steps", "config", "roofline",
                                                "e2e", "sweep", "parity_ok", "cpu_baseline", "gpu_launches") if k in c}
+            gc.collect()
+            torch.cuda.empty_cache()
+        if not args.no_extra and args.model == "C":
+            line["configs0_tiny_fp32"] = sub_config(
+                args, world, "tiny", 2, "BASELINE configs[0]: tiny 2-stage pipeline, 2 layers/stage, d 256, seq 128, "
+                "batch 8, fp32 arithmetic, int8 boundary codec (a parity config: launch-bound)", 6, 3, fp32=True)
+            line["configs3_paper_scale"] = sub_config(
+                args, world, "D", args.stages, "BASELINE configs[3]: d 4096, 32 heads, 16 shared layers/stage, "
+                "maxout k=2 + int8 boundary", 3, 3)
     if rank == 0 and line is not None:
         print(json.dumps(line), flush=True)
     if world > 1:

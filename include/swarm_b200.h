@@ -536,6 +536,14 @@ int swarm_driver_stats(swarm_driver_t d, swarm_driver_counters* stats);
 int swarm_driver_visit_log(swarm_driver_t d, size_t i, uint32_t* trainer, uint64_t* microbatch, uint32_t* stage,
                            int* backward, int64_t* peer);
 int swarm_driver_peer_of_rank(swarm_driver_t d, int peer); /* the rank hosting `peer` */
+/* Profiled region (bench.py's live roofline): until profile_end every visit runs eagerly on
+ * one stream behind a `spin_ns` GPU spin, with the stages' per-kernel CUDA events on
+ * (swarm_stage_profile), so each kernel is timed alone.  profile_end sums, over the local
+ * stages, the GEMM time (ms), executed GEMM FLOPs and launches, and the per-category
+ * time / launches (SWARM_PROF_*), and restores the normal streams. */
+int swarm_driver_profile_begin(swarm_driver_t d, uint64_t spin_ns);
+int swarm_driver_profile_end(swarm_driver_t d, double* gemm_ms, double* gemm_flops, uint64_t* gemm_launches,
+                             double* cat_ms /* [SWARM_PROF_CATEGORIES] */, uint64_t* cat_launches);
 
 #ifdef __cplusplus
 }

@@ -173,6 +173,8 @@ SIGNATURES = {
     "swarm_driver_visit_log": (I, [P, SZ, C.POINTER(C.c_uint32), C.POINTER(C.c_uint64), C.POINTER(C.c_uint32),
                                    C.POINTER(I), C.POINTER(C.c_int64)]),
     "swarm_driver_peer_of_rank": (I, [P, I]),
+    "swarm_driver_profile_begin": (I, [P, C.c_uint64]),
+    "swarm_driver_profile_end": (I, [P, C.POINTER(D), C.POINTER(D), C.POINTER(C.c_uint64), P, P]),
 }
 
 _lib = None

@@ -131,6 +131,12 @@ struct swarm_driver {
     uint64_t records = 0, visits = 0, ticks = 0, optimizer_steps = 0, completed = 0, captures = 0;
     uint64_t captured_kernels = 0, replayed_kernels = 0;
     cudaEvent_t ev_tmp = nullptr;
+    // profiled region: every visit eager (no graph) on one stream with the stages' kernel
+    // profiling on, so the events around each kernel time it alone (the live roofline)
+    bool prof = false;
+    cudaStream_t prof_stream = nullptr;
+
+    cudaStream_t lane_stream(const Peer& p) const { return prof ? prof_stream : p.lanes[p.cur]; }
 
     int rank_of_peer(int pid) const { return W >= S ? pid : stage_of[pid] / per_rank; }
 
@@ -156,9 +162,9 @@ struct swarm_driver {
     }
 
     int replay(uint64_t key, cudaStream_t st, const std::function<int()>& fn) {
-        if (!cfg.use_graphs || !warm.count(key)) {  // first use runs eagerly (lazy init, tensor-map caches)
+        if (!cfg.use_graphs || !warm.count(key) || prof) {  // first use runs eagerly (lazy init, tensor-map caches)
             TRY(fn());
-            warm.insert(key);
+            if (!prof) warm.insert(key);
             return SWARM_OK;
         }
         auto it = graphs.find(key);
@@ -190,11 +196,11 @@ struct swarm_driver {
 
     int after_slot(Peer& p, int t) {
         if (!p.has_slot[t]) return SWARM_OK;
-        return wait(p.lanes[p.cur], p.slot_ev[t]);
+        return wait(lane_stream(p), p.slot_ev[t]);
     }
     int mark_slot(Peer& p, int t) {
         p.has_slot[t] = 1;
-        return mark(p.slot_ev[t], p.lanes[p.cur]);
+        return mark(p.slot_ev[t], lane_stream(p));
     }
 
     int pool_index(int t, uint64_t k) const { return static_cast<int>((uint64_t(t) * 7 + k) % uint64_t(n_pool)); }
@@ -203,7 +209,7 @@ struct swarm_driver {
     int flush(Peer& p) {  // the peer's pending deferred weight gradients, alone, on its current lane
         const int t = p.pend;
         p.pend = -1;
-        cudaStream_t st = p.lanes[p.cur];
+        cudaStream_t st = lane_stream(p);
         if (cfg.lanes > 1) {
             TRY(swarm_stage_set_lane(p.st, p.cur));
             TRY(after_slot(p, t));
@@ -215,7 +221,7 @@ struct swarm_driver {
 
     int visit(Peer& p, const swarm_engine_record& r, int s, int t, bool bwd, int* paired) {
         *paired = -1;
-        cudaStream_t st = p.lanes[p.cur];
+        cudaStream_t st = lane_stream(p);
         Buf* in = buf_for(t, s, bwd);
         Buf* out = out_for(t, s, bwd);
         if (in && in->has_recvd) {  // the transfer into this buffer (pair stream)
@@ -351,6 +357,8 @@ struct swarm_driver {
     }
 
     int join_lanes(Peer& p) {  // lane 0 waits for every other lane
+        p.cur = 0;
+        if (prof) return SWARM_OK;  // one stream while profiling
         for (size_t i = 1; i < p.lanes.size(); ++i) {
             TRY(mark(p.lane_ev, p.lanes[i]));
             TRY(wait(p.lanes[0], p.lane_ev));
@@ -367,12 +375,13 @@ struct swarm_driver {
         for (Peer& p : peers) {
             const int n = served[p.stage];
             if (n == 0) continue;
-            cudaStream_t st = p.lanes[0];
+            cudaStream_t st = lane_stream(p);
             TRY(swarm_stage_allreduce(p.st, p.stage_comm, st));
             TRY(swarm_stage_optimizer_step(p.st, 1.0f / static_cast<float>(n), st));  // mean over the stage's microbatches
             optimizer_steps += 1;
         }
         for (Peer& p : peers) {  // every lane's next visit sees the updated weights
+            if (prof) break;
             TRY(mark(p.lane_ev, p.lanes[0]));
             for (size_t i = 1; i < p.lanes.size(); ++i) TRY(wait(p.lanes[i], p.lane_ev));
         }
@@ -407,6 +416,7 @@ struct swarm_driver {
             if (s) cudaStreamDestroy(s);
         for (swarm_comm_t c : owned_comms) swarm_comm_destroy(c);
         if (ev_tmp) cudaEventDestroy(ev_tmp);
+        if (prof_stream) cudaStreamDestroy(prof_stream);
         for (void* p : allocs) cudaFree(p);
         if (engine) swarm_engine_destroy(engine);
     }
@@ -712,6 +722,60 @@ int swarm_driver_visit_log(swarm_driver_t d, size_t i, uint32_t* trainer, uint64
     if (stage) *stage = v.stage;
     if (backward) *backward = v.backward;
     if (peer) *peer = v.peer;
+    return SWARM_OK;
+}
+
+int swarm_driver_profile_begin(swarm_driver_t d, uint64_t spin_ns) {
+    if (!d) return fail("driver: null handle");
+    if (d->prof) return fail("driver: profiling already on");
+    if (!d->prof_stream) CU(cudaStreamCreateWithFlags(&d->prof_stream, cudaStreamNonBlocking));
+    for (Peer& p : d->peers)  // the profile stream starts after every lane
+        for (cudaStream_t s : p.lanes) {
+            CU(cudaEventRecord(d->ev_tmp, s));
+            CU(cudaStreamWaitEvent(d->prof_stream, d->ev_tmp, 0));
+        }
+    // queue the profiled kernels behind a GPU spin so host launch gaps fall outside their events
+    if (spin_ns) TRY(swarm_gpu_spin(spin_ns, d->prof_stream));
+    for (Peer& p : d->peers) {
+        swarm_stage_profile(p.st, 1);
+        swarm_stage_profile_weight(p.st, 1.0);
+    }
+    d->prof = true;
+    return SWARM_OK;
+}
+
+int swarm_driver_profile_end(swarm_driver_t d, double* gemm_ms, double* gemm_flops, uint64_t* gemm_launches,
+                             double* cat_ms, uint64_t* cat_launches) {
+    if (!d || !d->prof) return fail("driver: profiling is off");
+    d->prof = false;
+    for (Peer& p : d->peers) {  // every lane continues after the profiled region
+        swarm_stage_profile(p.st, 0);
+        CU(cudaEventRecord(d->ev_tmp, d->prof_stream));
+        for (cudaStream_t s : p.lanes) CU(cudaStreamWaitEvent(s, d->ev_tmp, 0));
+    }
+    double ms = 0, fl = 0;
+    uint64_t n = 0;
+    double cm[SWARM_PROF_CATEGORIES] = {};
+    uint64_t cn[SWARM_PROF_CATEGORIES] = {};
+    for (Peer& p : d->peers) {
+        double a = 0, b = 0;
+        uint64_t c = 0;
+        TRY(swarm_stage_profile_read(p.st, &a, &b, &c));
+        ms += a;
+        fl += b;
+        n += c;
+        double pm[SWARM_PROF_CATEGORIES];
+        uint64_t pn[SWARM_PROF_CATEGORIES];
+        swarm_stage_profile_breakdown(p.st, pm, pn);
+        for (int k = 0; k < SWARM_PROF_CATEGORIES; ++k) cm[k] += pm[k], cn[k] += pn[k];
+    }
+    if (gemm_ms) *gemm_ms = ms;
+    if (gemm_flops) *gemm_flops = fl;
+    if (gemm_launches) *gemm_launches = n;
+    for (int k = 0; k < SWARM_PROF_CATEGORIES; ++k) {
+        if (cat_ms) cat_ms[k] = cm[k];
+        if (cat_launches) cat_launches[k] = cn[k];
+    }
     return SWARM_OK;
 }
 

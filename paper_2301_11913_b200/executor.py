@@ -637,6 +637,26 @@ class EngineExecutor:
     def kernels_launched(self) -> int:
         return self._counters().kernels
 
+    PROF_CATEGORIES = ("gemm", "attention", "layernorm", "other")
+
+    def profile(self, n_microbatches: int, spin_ns: int = 200_000_000) -> dict:
+        """Run `n_microbatches` more completions as a profiled region (every visit eager on
+        one stream, per-kernel CUDA events, swarm_driver_profile_begin/end) and return
+        {"gemm_ms", "gemm_flops", "gemm_launches", "categories": {name: (ms, launches)},
+        "region_ms"} summed over this rank's stages."""
+        import ctypes as C
+        self.fork()
+        self._check(self.lib.swarm_driver_profile_begin(self.h, spin_ns), "driver_profile_begin")
+        done = C.c_uint64()
+        self._check(self.lib.swarm_driver_run(self.h, n_microbatches, C.byref(done)), "driver_run")
+        ms, fl, n = C.c_double(), C.c_double(), C.c_uint64()
+        cm, cn = (C.c_double * 4)(), (C.c_uint64 * 4)()
+        self._check(self.lib.swarm_driver_profile_end(self.h, C.byref(ms), C.byref(fl), C.byref(n), cm, cn),
+                    "driver_profile_end")
+        self.finish()
+        return {"gemm_ms": ms.value, "gemm_flops": fl.value, "gemm_launches": n.value, "microbatches": done.value,
+                "categories": {c: (cm[i], cn[i]) for i, c in enumerate(self.PROF_CATEGORIES)}}
+
 
 def sequential_reference_grads(ex) -> dict:
     """Verification helper: every peer's gradient over exactly the visits the
