@@ -421,6 +421,15 @@ int swarm_rebalance_decide(size_t n_stages, const size_t* offsets, const uint64_
 #define SWARM_ENG_HOP 1        /* trainer's input dispatched to `worker`'s queue; from_worker produced it (-1: new microbatch) */
 #define SWARM_ENG_DONE 2       /* trainer's microbatch finished (backward at stage 0 on `worker`) */
 #define SWARM_ENG_ALLREDUCE 3  /* stage-wide all-reduce tick; starts stall until end_time */
+/* membership records (churn and rebalancing, P/src/sim.cpp:527-719) */
+#define SWARM_ENG_LEAVE 4      /* `worker` died (kill_worker; backward = 1: it was migrating); its queued jobs
+                                  follow as HOP records to other peers (requeue) */
+#define SWARM_ENG_JOIN 5       /* new `worker` joined `stage` (on_peer_join); its trainers start */
+#define SWARM_ENG_MIGRATE 6    /* `worker` leaves stage `from_worker` for `stage` (begin_migration); it downloads
+                                  the destination's state until end_time */
+#define SWARM_ENG_MIGRATED 7   /* `worker` serves `stage` again (on_migration_complete) */
+#define SWARM_ENG_REBALANCE 8  /* Alg. 2 decision: from stage `from_worker` to `stage`, mover `worker` (-1: none;
+                                  backward = 1: skipped on a stale table) */
 typedef struct {
     double time;
     double end_time;
@@ -434,6 +443,30 @@ typedef struct {
 } swarm_engine_record;
 typedef struct swarm_engine* swarm_engine_t;
 const char* swarm_engine_last_error(void);
+/* The reference SimConfig (P/include/swarmsim/sim.hpp:21-54) with an explicit initial population
+ * and churn trace (trace::Trace of (t, delta), trace.hpp:10-16): */
+typedef struct {
+    size_t n_stages;
+    size_t n_workers;            /* initial_peers flattened stage by stage */
+    const size_t* worker_stage;
+    const double* worker_speed;  /* NULL = 1.0 */
+    size_t n_churn;              /* churn trace: delta > 0 joins, < 0 leaves, at time t */
+    const double* churn_t;
+    const int64_t* churn_delta;
+    double forward_seconds, backward_multiplier;
+    size_t trainers_per_peer;
+    double allreduce_period, allreduce_stall;
+    int rebalance_periodic;      /* RebalanceMode::Periodic (else None) */
+    double rebalance_period, straggler_timeout, propagation_delay, announce_ttl;
+    uint64_t state_transfer_bytes;
+    double download_bps;         /* DeviceProfile::download_bps: migration downtime = bytes * 8 / bps */
+    double duration_seconds, bucket_seconds;
+} swarm_sim_config;
+swarm_sim_config swarm_sim_config_default(void); /* the reference's defaults */
+int swarm_engine_create_ex(const swarm_sim_config* cfg, uint64_t seed, swarm_engine_t* out);
+/* SimResult::requeued / abandoned, workers ever created and alive now */
+int swarm_engine_counts(swarm_engine_t e, uint64_t* requeued, uint64_t* abandoned, size_t* n_workers, int64_t* alive);
+int swarm_engine_worker(swarm_engine_t e, size_t worker, size_t* stage, int* alive, int* migrating);
 /* SimConfig fields: n_stages, initial_peers (worker_stage/worker_speed, speed may be NULL = 1.0),
  * forward_service_seconds, backward_multiplier, trainers_per_peer, allreduce_period/_stall,
  * duration_seconds, bucket_seconds; seed = sim::run's seed.  Errors: SWARM_E_INVALID (ConfigError). */

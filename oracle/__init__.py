@@ -96,6 +96,8 @@ def _load_ref():
     lib.ref_stage_cost.restype = C.c_int
     lib.ref_sim_run.argtypes = [C.c_char_p, C.c_uint64, P, P, P, sz, P]
     lib.ref_sim_run.restype = C.c_int
+    lib.ref_sim_run_churn.argtypes = [C.c_char_p, P, P, sz, C.c_uint64, P, P, sz, P, C.c_char_p, sz]
+    lib.ref_sim_run_churn.restype = C.c_int
     return lib
 
 

@@ -8,6 +8,11 @@
 #include "swarmsim/errors.hpp"
 #include "swarmsim/rebalancer.hpp"
 #include "swarmsim/wiring.hpp"
+#include "swarmsim/sim.hpp"
+#include "swarmsim/trace.hpp"
+#include <algorithm>
+#include <cstring>
+#include <string>
 
 using namespace swarmsim;
 
@@ -152,6 +157,36 @@ extern "C" int ref_sim_run(const char* json, uint64_t seed, uint64_t* dispatched
         *completed = r.completed;
         *n_buckets_out = r.throughput.completed.size();
         for (size_t i = 0; i < n_buckets && i < r.throughput.completed.size(); ++i) buckets[i] = r.throughput.completed[i];
+        return 0;
+    } catch (const swarmsim::ConfigError&) {
+        return 1;
+    } catch (const std::exception&) {
+        return 3;
+    }
+}
+
+// sim::run with a churn trace (SimConfig::from_json has no trace; the CLI loads it separately,
+// P/tools/swarmsim_main.cpp) returning the counters and the event log (JSON lines, '\n'-joined).
+extern "C" int ref_sim_run_churn(const char* json, const double* churn_t, const int64_t* churn_delta, size_t n_churn,
+                                 uint64_t seed, uint64_t* counts /* dispatched, completed, requeued, abandoned */,
+                                 double* buckets, size_t n_buckets, size_t* n_buckets_out, char* log, size_t log_cap) {
+    try {
+        auto cfg = swarmsim::sim::SimConfig::from_json(std::string(json));
+        for (size_t i = 0; i < n_churn; ++i) cfg.churn.push_back(swarmsim::trace::TraceEvent{churn_t[i], churn_delta[i]});
+        const auto r = swarmsim::sim::run(cfg, seed);
+        counts[0] = r.dispatched;
+        counts[1] = r.completed;
+        counts[2] = r.requeued;
+        counts[3] = r.abandoned;
+        *n_buckets_out = r.throughput.completed.size();
+        for (size_t i = 0; i < n_buckets && i < r.throughput.completed.size(); ++i) buckets[i] = r.throughput.completed[i];
+        std::string all;
+        for (const auto& line : r.event_log) all += line + "\n";
+        if (log && log_cap) {
+            const size_t n = std::min(all.size(), log_cap - 1);
+            std::memcpy(log, all.data(), n);
+            log[n] = 0;
+        }
         return 0;
     } catch (const swarmsim::ConfigError&) {
         return 1;

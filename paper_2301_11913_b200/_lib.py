@@ -43,7 +43,19 @@ class EngineRecord(C.Structure):
                 ("microbatch", C.c_uint64)]
 
 
-ENG_START, ENG_HOP, ENG_DONE, ENG_ALLREDUCE = range(4)
+ENG_START, ENG_HOP, ENG_DONE, ENG_ALLREDUCE, ENG_LEAVE, ENG_JOIN, ENG_MIGRATE, ENG_MIGRATED, ENG_REBALANCE = range(9)
+
+
+class SimConfigC(C.Structure):
+    _fields_ = [("n_stages", C.c_size_t), ("n_workers", C.c_size_t), ("worker_stage", C.POINTER(C.c_size_t)),
+                ("worker_speed", C.POINTER(C.c_double)), ("n_churn", C.c_size_t), ("churn_t", C.POINTER(C.c_double)),
+                ("churn_delta", C.POINTER(C.c_int64)), ("forward_seconds", C.c_double),
+                ("backward_multiplier", C.c_double), ("trainers_per_peer", C.c_size_t),
+                ("allreduce_period", C.c_double), ("allreduce_stall", C.c_double), ("rebalance_periodic", C.c_int),
+                ("rebalance_period", C.c_double), ("straggler_timeout", C.c_double),
+                ("propagation_delay", C.c_double), ("announce_ttl", C.c_double),
+                ("state_transfer_bytes", C.c_uint64), ("download_bps", C.c_double),
+                ("duration_seconds", C.c_double), ("bucket_seconds", C.c_double)]
 
 
 class DriverConfig(C.Structure):
@@ -142,6 +154,10 @@ SIGNATURES = {
     "swarm_engine_n_trainers": (SZ, [P]),
     "swarm_engine_next": (I, [P, C.POINTER(EngineRecord), SZ, C.POINTER(SZ)]),
     "swarm_engine_summary": (I, [P, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64), P, SZ, C.POINTER(D)]),
+    "swarm_sim_config_default": (SimConfigC, []),
+    "swarm_engine_create_ex": (I, [C.POINTER(SimConfigC), C.c_uint64, C.POINTER(P)]),
+    "swarm_engine_counts": (I, [P, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64), C.POINTER(SZ), C.POINTER(C.c_int64)]),
+    "swarm_engine_worker": (I, [P, SZ, C.POINTER(SZ), C.POINTER(I), C.POINTER(I)]),
     "swarm_comm_last_error": (C.c_char_p, []),
     "swarm_comm_nccl_version": (I, []),
     "swarm_comm_unique_id": (I, [P]),

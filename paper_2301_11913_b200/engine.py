@@ -13,6 +13,8 @@ from dataclasses import dataclass, field
 from . import _lib
 
 START, HOP, DONE, ALLREDUCE = _lib.ENG_START, _lib.ENG_HOP, _lib.ENG_DONE, _lib.ENG_ALLREDUCE
+LEAVE, JOIN, MIGRATE, MIGRATED, REBALANCE = (_lib.ENG_LEAVE, _lib.ENG_JOIN, _lib.ENG_MIGRATE, _lib.ENG_MIGRATED,
+                                             _lib.ENG_REBALANCE)
 
 
 @dataclass
@@ -27,6 +29,13 @@ class EngineConfig:
     allreduce_stall: float = 0.0
     duration_seconds: float = 3600.0
     bucket_seconds: float = 60.0
+    churn: list = field(default_factory=list)  # trace::Trace: [(t, delta), ...] (trace.hpp:10-16)
+    rebalance_period: float = 0.0              # > 0: RebalanceMode::Periodic with this period
+    straggler_timeout: float = 5.0
+    propagation_delay: float = 1.0
+    announce_ttl: float = 300.0
+    state_transfer_bytes: int = 0
+    download_bps: float = 500e6
 
     def worker_stages(self) -> list[int]:
         return [s for s, peers in enumerate(self.initial_peers) for _ in peers]
@@ -44,22 +53,46 @@ class EngineConfig:
             "allreduce_stall": self.allreduce_stall,
             "duration_seconds": self.duration_seconds,
             "bucket_seconds": self.bucket_seconds,
+            "rebalance": ({"mode": "periodic", "period": self.rebalance_period} if self.rebalance_period > 0
+                          else {"mode": "none"}),
+            "straggler_timeout": self.straggler_timeout,
+            "propagation_delay": self.propagation_delay,
+            "announce_ttl": self.announce_ttl,
+            "state_transfer_bytes": int(self.state_transfer_bytes),
+            "device": {"download_bps": self.download_bps},
         })
+
+    def to_c(self):
+        """The swarm_sim_config struct (keeps its arrays alive on the returned object)."""
+        c = _lib.lib().swarm_sim_config_default()
+        stages = self.worker_stages()
+        speeds = [float(v) for peers in self.initial_peers for v in peers]
+        c._keep = [(C.c_size_t * len(stages))(*stages), (C.c_double * len(speeds))(*speeds),
+                   (C.c_double * max(len(self.churn), 1))(*[float(t) for t, _ in self.churn]),
+                   (C.c_int64 * max(len(self.churn), 1))(*[int(d) for _, d in self.churn])]
+        c.n_stages, c.n_workers = self.n_stages, len(stages)
+        c.worker_stage, c.worker_speed = c._keep[0], c._keep[1]
+        c.n_churn, c.churn_t, c.churn_delta = len(self.churn), c._keep[2], c._keep[3]
+        c.forward_seconds, c.backward_multiplier = self.forward_service_seconds, self.backward_multiplier
+        c.trainers_per_peer = self.trainers_per_peer
+        c.allreduce_period, c.allreduce_stall = self.allreduce_period, self.allreduce_stall
+        c.rebalance_periodic = int(self.rebalance_period > 0)
+        c.rebalance_period = self.rebalance_period if self.rebalance_period > 0 else 300.0
+        c.straggler_timeout, c.propagation_delay = self.straggler_timeout, self.propagation_delay
+        c.announce_ttl, c.state_transfer_bytes = self.announce_ttl, int(self.state_transfer_bytes)
+        c.download_bps = self.download_bps
+        c.duration_seconds, c.bucket_seconds = self.duration_seconds, self.bucket_seconds
+        return c
 
 
 class Engine:
     def __init__(self, cfg: EngineConfig, seed: int):
         L = _lib.lib()
         self.cfg = cfg
-        stages = cfg.worker_stages()
-        speeds = [float(v) for peers in cfg.initial_peers for v in peers]
-        self.n_workers = len(stages)
-        st = (C.c_size_t * len(stages))(*stages)
-        sp = (C.c_double * len(speeds))(*speeds)
+        self.n_workers = len(cfg.worker_stages())
+        c = cfg.to_c()
         h = C.c_void_p()
-        rc = L.swarm_engine_create(cfg.n_stages, len(stages), st, sp, cfg.forward_service_seconds,
-                                   cfg.backward_multiplier, cfg.trainers_per_peer, cfg.allreduce_period,
-                                   cfg.allreduce_stall, cfg.duration_seconds, cfg.bucket_seconds, seed, C.byref(h))
+        rc = L.swarm_engine_create_ex(C.byref(c), seed, C.byref(h))
         if rc != _lib.SWARM_OK:
             from ._swarmsim_b200 import ConfigError
             raise ConfigError(L.swarm_engine_last_error().decode())
@@ -104,4 +137,7 @@ class Engine:
         d, c, now = C.c_uint64(), C.c_uint64(), C.c_double()
         buckets = (C.c_double * max(nb, 1))()
         _lib.lib().swarm_engine_summary(self.h, C.byref(d), C.byref(c), buckets, nb, C.byref(now))
-        return {"dispatched": d.value, "completed": c.value, "buckets": list(buckets)[:nb], "now": now.value}
+        rq, ab, nw, alive = C.c_uint64(), C.c_uint64(), C.c_size_t(), C.c_int64()
+        _lib.lib().swarm_engine_counts(self.h, C.byref(rq), C.byref(ab), C.byref(nw), C.byref(alive))
+        return {"dispatched": d.value, "completed": c.value, "buckets": list(buckets)[:nb], "now": now.value,
+                "requeued": rq.value, "abandoned": ab.value, "workers": nw.value, "alive": alive.value}
