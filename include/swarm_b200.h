@@ -236,6 +236,8 @@ int swarm_adamw_step(float* p32, void* p16, float* grad, float* m, float* v, siz
 /* p[i] = mean + std * N(0,1) from a counter-based hash of (seed, i) */
 int swarm_fill_normal(float* p, size_t n, float mean, float std, uint64_t seed, swarm_stream_t stream);
 int swarm_cast_f32_bf16(const float* in, void* out, size_t n, swarm_stream_t stream);
+/* dst[i] += src[i] (fp32): sums the gradient arenas of a stage's peers that share a GPU */
+int swarm_add_f32(float* dst, const float* src, size_t n, swarm_stream_t stream);
 
 /* ---- stage executor -------------------------------------------------------
  * One SWARM pipeline stage on one GPU: a contiguous range of pre-LN
@@ -535,12 +537,21 @@ typedef struct {
     int stream_per_peer; /* 0: every local peer shares one stream */
     int n_pool;          /* synthetic token pool size (microbatch (t, k) uses entry (7 t + k) % n_pool) */
     swarm_comm_t comm;   /* world communicator (NULL when world == 1) */
+    /* optional full SimConfig (churn trace, rebalancing, peer speeds): when set, it replaces the
+       engine fields above and its initial_peers give the layout.  Peer pid lives on rank
+       pid * world / n_initial (joiners: pid % world), so any layout runs on any world size
+       (peers sharing a GPU sum their gradients locally before the NCCL all-reduce). */
+    const swarm_sim_config* sim;
 } swarm_driver_config;
 typedef struct {
     uint64_t records, visits, ticks, optimizer_steps, completed, captures, kernels;
     uint32_t n_trainers;
     size_t wire_bytes;
     size_t visit_log_size;
+    uint64_t recomputes;   /* backward visits that first recomputed the stage forward (peer changed) */
+    uint64_t migrations;   /* MIGRATE records */
+    uint64_t state_bytes;  /* params + AdamW state moved to migrating / joining peers */
+    size_t n_peers;        /* peers ever created */
 } swarm_driver_counters;
 typedef struct swarm_driver* swarm_driver_t;
 const char* swarm_driver_last_error(void);
@@ -548,6 +559,10 @@ int swarm_driver_create(const swarm_driver_config* cfg, swarm_driver_t* out);
 void swarm_driver_destroy(swarm_driver_t d);
 /* process the driver's own engine records until n more microbatches completed */
 int swarm_driver_run(swarm_driver_t d, uint64_t n_microbatches, uint64_t* completed);
+/* the same, stopping early right after a record of kind `stop_kind` (>= 0), e.g. SWARM_ENG_LEAVE */
+int swarm_driver_run_until(swarm_driver_t d, uint64_t n_microbatches, int stop_kind, uint64_t* completed);
+/* membership as the records left it: the peer's stage, liveness, migration state and rank */
+int swarm_driver_peer_info(swarm_driver_t d, int peer, int* stage, int* alive, int* migrating, int* rank);
 /* the additive hook: one record from any engine that emits the same records in the same
  * order (the driver's own, or the reference Engine patched as INTEGRATION.md §4 shows) */
 int swarm_driver_on_record(swarm_driver_t d, const swarm_engine_record* record);

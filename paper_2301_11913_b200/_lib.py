@@ -63,13 +63,16 @@ class DriverConfig(C.Structure):
                 ("layout", C.POINTER(C.c_int)), ("forward_seconds", C.c_double), ("backward_multiplier", C.c_double),
                 ("allreduce_period", C.c_double), ("allreduce_stall", C.c_double), ("duration_seconds", C.c_double),
                 ("trainers_per_peer", C.c_int), ("seed", C.c_uint64), ("lanes", C.c_int), ("pair_wgrad", C.c_int),
-                ("use_graphs", C.c_int), ("stream_per_peer", C.c_int), ("n_pool", C.c_int), ("comm", C.c_void_p)]
+                ("use_graphs", C.c_int), ("stream_per_peer", C.c_int), ("n_pool", C.c_int), ("comm", C.c_void_p),
+                ("sim", C.c_void_p)]
 
 
 class DriverCounters(C.Structure):
     _fields_ = [(n, C.c_uint64) for n in ("records", "visits", "ticks", "optimizer_steps", "completed", "captures",
                                           "kernels")] + [("n_trainers", C.c_uint32), ("wire_bytes", C.c_size_t),
-                                                         ("visit_log_size", C.c_size_t)]
+                                                         ("visit_log_size", C.c_size_t), ("recomputes", C.c_uint64),
+                                                         ("migrations", C.c_uint64), ("state_bytes", C.c_uint64),
+                                                         ("n_peers", C.c_size_t)]
 
 # (name, restype, argtypes) for every symbol include/swarm_b200.h declares
 P, SZ, I, U32P, U8P, F, D = C.c_void_p, C.c_size_t, C.c_int, C.c_void_p, C.c_void_p, C.c_float, C.c_double
@@ -106,6 +109,7 @@ SIGNATURES = {
     "swarm_adamw_step": (I, [P, P, P, P, P, SZ, F, F, F, F, F, I, F, I, P]),
     "swarm_fill_normal": (I, [P, SZ, F, F, C.c_uint64, P]),
     "swarm_cast_f32_bf16": (I, [P, P, SZ, P]),
+    "swarm_add_f32": (I, [P, P, SZ, P]),
     "swarm_stage_create": (I, [C.POINTER(StageConfigC), C.POINTER(C.c_void_p)]),
     "swarm_stage_destroy": (None, [P]),
     "swarm_stage_wire_bytes": (SZ, [P]),
@@ -189,6 +193,8 @@ SIGNATURES = {
     "swarm_driver_visit_log": (I, [P, SZ, C.POINTER(C.c_uint32), C.POINTER(C.c_uint64), C.POINTER(C.c_uint32),
                                    C.POINTER(I), C.POINTER(C.c_int64)]),
     "swarm_driver_peer_of_rank": (I, [P, I]),
+    "swarm_driver_run_until": (I, [P, C.c_uint64, I, C.POINTER(C.c_uint64)]),
+    "swarm_driver_peer_info": (I, [P, I, C.POINTER(I), C.POINTER(I), C.POINTER(I), C.POINTER(I)]),
     "swarm_driver_profile_begin": (I, [P, C.c_uint64]),
     "swarm_driver_profile_end": (I, [P, C.POINTER(D), C.POINTER(D), C.POINTER(C.c_uint64), P, P]),
 }

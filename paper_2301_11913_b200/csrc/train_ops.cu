@@ -320,6 +320,19 @@ __global__ void k_fill_normal(float* __restrict__ p, size_t n, float mean, float
     }
 }
 
+__global__ void k_add4(float4* __restrict__ dst, const float4* __restrict__ src, size_t n4) {
+    for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n4;
+         i += static_cast<size_t>(gridDim.x) * blockDim.x) {
+        const float4 a = dst[i], b = src[i];
+        dst[i] = make_float4(a.x + b.x, a.y + b.y, a.z + b.z, a.w + b.w);
+    }
+}
+__global__ void k_add(float* __restrict__ dst, const float* __restrict__ src, size_t n) {
+    for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<size_t>(gridDim.x) * blockDim.x)
+        dst[i] += src[i];
+}
+
 __global__ void k_cast(const float* __restrict__ in, __nv_bfloat16* __restrict__ out, size_t n) {
     for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n;
          i += static_cast<size_t>(gridDim.x) * blockDim.x)
@@ -486,6 +499,19 @@ int swarm_fill_normal(float* p, size_t n, float mean, float stdv, uint64_t seed,
     if (n == 0) return SWARM_OK;
     k_fill_normal<<<grid_for(n, 256), 256, 0, as_stream(stream)>>>(p, n, mean, stdv, seed);
     SWARM_LAUNCH_CHECK("k_fill_normal");
+    return SWARM_OK;
+}
+
+int swarm_add_f32(float* dst, const float* src, size_t n, swarm_stream_t stream) {
+    if (n == 0) return SWARM_OK;
+    if (n % 4 == 0 && !((reinterpret_cast<uintptr_t>(dst) | reinterpret_cast<uintptr_t>(src)) & 15)) {
+        k_add4<<<grid_for(n / 4, 256, 148u * 16u), 256, 0, as_stream(stream)>>>(
+            reinterpret_cast<float4*>(dst), reinterpret_cast<const float4*>(src), n / 4);
+        SWARM_LAUNCH_CHECK("k_add4");
+        return SWARM_OK;
+    }
+    k_add<<<grid_for(n, 256, 148u * 16u), 256, 0, as_stream(stream)>>>(dst, src, n);
+    SWARM_LAUNCH_CHECK("k_add");
     return SWARM_OK;
 }
 

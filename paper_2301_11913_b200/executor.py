@@ -464,7 +464,9 @@ class EngineExecutor:
                  backward_multiplier: float = 2.0, allreduce_period: float = 0.0, allreduce_stall: float = 0.0,
                  duration_seconds: float = 1e9, use_graphs: bool = True, n_pool: int = 16,
                  tokens: torch.Tensor | None = None, targets: torch.Tensor | None = None, pair_wgrad: bool = True,
-                 stream_per_peer: bool = True, lanes: int = 1, fp32: bool = False):
+                 stream_per_peer: bool = True, lanes: int = 1, fp32: bool = False, sim: EngineConfig | None = None):
+        """sim: a full SimConfig (initial_peers with speeds, churn trace, rebalancing); it replaces
+        the engine arguments and gives the layout (any layout on any world size)."""
         import ctypes as C
 
         from .stage import device_view
@@ -474,7 +476,7 @@ class EngineExecutor:
         self.world = dist.get_world_size() if dist.is_initialized() else 1
         self.rank = dist.get_rank() if dist.is_initialized() else 0
         self.device = torch.device("cuda", torch.cuda.current_device())
-        self.pl = Placement(self.world, n_stages)
+        self.pl = Placement(self.world, n_stages) if sim is None else None
         if lanes > 1 and not stream_per_peer:
             raise ValueError("lanes need a stream per peer")
         self.lib = L.lib()
@@ -506,6 +508,9 @@ class EngineExecutor:
         c.pair_wgrad, c.use_graphs, c.stream_per_peer = int(pair_wgrad), int(use_graphs), int(stream_per_peer)
         c.n_pool = n_pool if tokens is None else int(tokens.shape[0])
         c.comm = self.comm
+        if sim is not None:
+            self._sim_c = sim.to_c()
+            c.sim = C.cast(C.pointer(self._sim_c), C.c_void_p)
         h = C.c_void_p()
         rc = self.lib.swarm_driver_create(C.byref(c), C.byref(h))
         if rc:
@@ -516,20 +521,13 @@ class EngineExecutor:
             raise RuntimeError(msg)
         self.h = h
         self.lanes = lanes
-        self.ecfg = EngineConfig(n_stages=n_stages, initial_peers=[[1.0] * self.pl.layout[s] for s in range(n_stages)],
-                                 forward_service_seconds=forward_seconds, backward_multiplier=backward_multiplier,
-                                 trainers_per_peer=trainers_per_peer, allreduce_period=allreduce_period,
-                                 allreduce_stall=allreduce_stall, duration_seconds=duration_seconds,
-                                 bucket_seconds=max(duration_seconds / 64, 1e-9))
+        self.ecfg = sim or EngineConfig(
+            n_stages=n_stages, initial_peers=[[1.0] * self.pl.layout[s] for s in range(n_stages)],
+            forward_service_seconds=forward_seconds, backward_multiplier=backward_multiplier,
+            trainers_per_peer=trainers_per_peer, allreduce_period=allreduce_period, allreduce_stall=allreduce_stall,
+            duration_seconds=duration_seconds, bucket_seconds=max(duration_seconds / 64, 1e-9))
         self.engine = Engine.borrow(self.lib.swarm_driver_engine(h), self.ecfg)
         self.T = self.engine.n_trainers
-        self.local = [pid for pid in range(len(self.pl.stage_of)) if self.pl.rank_of_peer(pid) == self.rank]
-        self.stages: dict[int, Stage] = {}
-        for pid in self.local:
-            s = self.pl.stage_of_peer(pid)
-            cfg = StageConfig(**{**self.stage_cfg.__dict__, "is_first": int(s == 0), "is_last": int(s == n_stages - 1),
-                                 "max_slots": self.T, "seed": seed * 1000 + s})
-            self.stages[pid] = Stage.borrow(self.lib.swarm_driver_stage(h, pid), cfg, self.device)
         self.loss_sum = device_view(self.lib.swarm_driver_loss_sum(h), 1, torch.float32, self.device)
         if tokens is not None:
             tokens = tokens.to(self.device, torch.int32).contiguous()
@@ -565,6 +563,52 @@ class EngineExecutor:
         k = L.DriverCounters()
         self._check(self.lib.swarm_driver_stats(self.h, C.byref(k)), "driver_stats")
         return k
+
+    def peer_info(self, pid: int) -> dict:
+        """The peer's stage / liveness / migration state / rank, as the records left them."""
+        import ctypes as C
+        st, al, mg, rk = C.c_int(), C.c_int(), C.c_int(), C.c_int()
+        self._check(self.lib.swarm_driver_peer_info(self.h, pid, C.byref(st), C.byref(al), C.byref(mg), C.byref(rk)),
+                    "driver_peer_info")
+        return {"stage": st.value, "alive": bool(al.value), "migrating": bool(mg.value), "rank": rk.value}
+
+    @property
+    def n_peers(self) -> int:
+        return self._counters().n_peers
+
+    @property
+    def local(self) -> list:
+        return [pid for pid in range(self.n_peers) if self.peer_info(pid)["rank"] == self.rank]
+
+    def stage_of_peer(self, pid: int) -> int:
+        return self.peer_info(pid)["stage"]
+
+    @property
+    def stages(self) -> dict:
+        """Views of this rank's live, serving peers' stages (re-read: migration replaces a stage)."""
+        out = {}
+        for pid in self.local:
+            info = self.peer_info(pid)
+            if not info["alive"] or info["migrating"]:
+                continue
+            s = info["stage"]
+            cfg = StageConfig(**{**self.stage_cfg.__dict__, "is_first": int(s == 0), "is_last": int(s == self.S - 1),
+                                 "max_slots": self.T, "seed": self.seed * 1000 + s})
+            out[pid] = Stage.borrow(self.lib.swarm_driver_stage(self.h, pid), cfg, self.device)
+        return out
+
+    def counters(self) -> dict:
+        k = self._counters()
+        return {f: getattr(k, f) for f, _ in L.DriverCounters._fields_}
+
+    def run_until(self, n_microbatches: int, stop_kind: int) -> int:
+        """run(), stopping right after the first record of kind `stop_kind` (engine.LEAVE, ...)."""
+        import ctypes as C
+        self.fork()
+        done = C.c_uint64()
+        self._check(self.lib.swarm_driver_run_until(self.h, n_microbatches, stop_kind, C.byref(done)),
+                    "driver_run_until")
+        return done.value
 
     records = property(lambda self: self._counters().records)
     optimizer_steps = property(lambda self: self._counters().optimizer_steps)
@@ -630,7 +674,8 @@ class EngineExecutor:
         """A stream ordered after every lane of this rank's last-stage peer (it owns
         loss_sum), or None."""
         for pid in self.local:
-            if self.pl.stage_of_peer(pid) == self.S - 1:
+            info = self.peer_info(pid)
+            if info["stage"] == self.S - 1 and info["alive"] and not info["migrating"]:
                 return torch.cuda.ExternalStream(self.lib.swarm_driver_peer_stream(self.h, pid), device=self.device)
         return None
 
@@ -668,8 +713,10 @@ def sequential_reference_grads(ex) -> dict:
     ALLREDUCE tick changed the weights."""
     S, m = ex.S, ex.m
     ref = {}
-    for pid in range(len(ex.pl.stage_of)):
-        s = ex.pl.stage_of_peer(pid)
+    n_peers = ex.n_peers if hasattr(ex, "n_peers") else len(ex.pl.stage_of)
+    stage_of = ex.stage_of_peer if hasattr(ex, "stage_of_peer") else ex.pl.stage_of_peer
+    for pid in range(n_peers):
+        s = stage_of(pid)
         cfg = StageConfig(d_model=m.d_model, n_heads=m.n_heads, d_ffn=m.d_ffn, seq_len=m.seq_len,
                           micro_batch=m.micro_batch, n_layers=m.layers_per_stage, shared_layers=m.shared_layers,
                           vocab=m.vocab, is_first=int(s == 0), is_last=int(s == S - 1), causal=m.causal,

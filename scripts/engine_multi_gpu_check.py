@@ -29,7 +29,7 @@ ex.flush_wgrad()
 ref = sequential_reference_grads(ex)
 ok = True
 for pid, st in ex.stages.items():
-    s = ex.pl.stage_of_peer(pid)
+    s = ex.stage_of_peer(pid)
     r = float((st.grads() - ref[pid]).norm() / ref[pid].norm().clamp_min(1e-30))
     ok &= r <= 1e-4
     print(f"rank {dist.get_rank()} peer {pid} stage {s}: rel {r:.3e} visits {ex.visits_local}", flush=True)
