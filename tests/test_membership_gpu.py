@@ -39,11 +39,20 @@ def make(cfg, **kw):
     return EngineExecutor(PRESETS["tiny"], cfg.n_stages, seed=3, n_pool=5, sim=cfg, **kw)
 
 
-def replay_reference(ex):
-    """Per live peer: the gradient the visits it ran must have accumulated, from a sequential
-    replay of every microbatch on fresh replicas (weights fixed: no tick ran)."""
+def replay_reference(ex, cfg, seed=3):
+    """Per live peer: the gradient the visits it ran on its current stage object (since its last
+    migration) must have accumulated, from a sequential replay of every microbatch on fresh
+    replicas (weights fixed: no tick ran)."""
     import torch
+    from paper_2301_11913_b200.engine import MIGRATED, START, Engine
     from paper_2301_11913_b200.stage import Stage, StageConfig
+    # the visit-log position where each peer's current stage object started (its last MIGRATED)
+    since, n_start = {}, 0
+    for r in Engine(cfg, seed).records():
+        if r.kind == START:
+            n_start += 1
+        elif r.kind == MIGRATED:
+            since[r.worker] = n_start
     m, S = ex.m, ex.S
     reps = {}
     for s in range(S):
@@ -76,9 +85,9 @@ def replay_reference(ex):
     torch.cuda.synchronize()
     want = {}
     last_fwd = {}  # (t, k, s) -> peer of the latest forward START
-    for t, k, s, b, p in log:
+    for i, (t, k, s, b, p) in enumerate(log):
         info = ex.peer_info(p)
-        counts = info["alive"] and not info["migrating"] and info["stage"] == s
+        counts = info["alive"] and not info["migrating"] and info["stage"] == s and i >= since.get(p, 0)
         if not b:
             last_fwd[(t, k, s)] = p
             if counts:
@@ -93,7 +102,8 @@ def replay_reference(ex):
 def test_peer_death_and_migration_gradients_match_replay(cuda):
     import torch
     from paper_2301_11913_b200.engine import LEAVE, MIGRATED
-    ex = make(config_e(ticks=False))
+    cfg = config_e(ticks=False)
+    ex = make(cfg)
     ex.run(10 ** 6)  # the whole schedule (duration_seconds)
     ex.finish()
     ex.flush_wgrad()
@@ -103,7 +113,7 @@ def test_peer_death_and_migration_gradients_match_replay(cuda):
     assert c["recomputes"] >= 1, c  # some backward re-routed away from its forward peer
     alive = [p for p in range(ex.n_peers) if ex.peer_info(p)["alive"]]
     assert len(alive) == 3
-    want = replay_reference(ex)
+    want = replay_reference(ex, cfg)
     for pid, st in ex.stages.items():
         assert pid in want
         e = rel(st.grads(), want[pid])
