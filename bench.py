@@ -921,83 +921,115 @@ def sub_config(args, world, model, S, which, steps, warmup, fp32=False) -> dict:
 
 # ----------------------------------------------------------------- failure
 def bench_failure(args, world, rank, local):
-    """BASELINE configs[4]: peer failure + adaptive
-    rebalancing on a real multi-GPU pipeline.  Start imbalanced (one stage short
-    a peer, e.g. 3,1,2,2 on 8 GPUs or 3,1 on 4), rebalance (Alg. 2 moves a peer,
-    which downloads weights + AdamW state from a stage-mate), then remove a peer
-    mid-training and rebalance again.  Each phase's tokens/s is measured; the
-    CPU reference is the reference's own oracle_throughput (P/src/sim.cpp:88-116,
-    compiled in oracle/_ref) fed the measured per-peer stage rate."""
+    """BASELINE configs[4]: peer failure + adaptive rebalancing,
+    asynchronously through the engine and the C++ driver.  The reference Engine's own
+    schedule (csrc/engine.cpp, decision-identical to sim::run incl. churn and Alg. 2 on
+    the queue-length time-integral average_load, sim.cpp:378-393) starts one stage short
+    of peers, rebalances periodically, and loses a peer mid-run (a churn-trace leave);
+    the driver executes it: requeued jobs, backward recompute where the forward peer is
+    gone, migration as a real NCCL download of params + AdamW state.  Each segment
+    between membership changes is timed on the device; the CPU reference is the
+    unmodified sim::run (oracle/_ref) on the same SimConfig and seed."""
     import ctypes as C
 
     import torch
-    import torch.distributed as dist
 
-    from paper_2301_11913_b200.swarm import PRESETS, SwarmPipeline, synthetic_batch
+    from paper_2301_11913_b200.engine import EngineConfig
+    from paper_2301_11913_b200.executor import EngineExecutor
     dev = torch.device("cuda", local)
     torch.cuda.set_device(dev)
-    S = args.stages if args.stages != TRAIN_STAGES or world >= 8 else max(2, world // 2)
-    if world < 2 * S:
-        raise SystemExit("failure workload needs >= 2 peers per stage on average (world >= 2*stages)")
-    per = world // S
-    layout = [per + 1, per - 1] + [per] * (S - 2)  # stage 1 short one peer
     mcfg = model_config(args)
-    M = args.microbatches
-    pipe = SwarmPipeline(mcfg, S, n_microbatches=M, seed=1, lr=1e-4, layout=layout, max_slots=M)
-    tok, tgt = synthetic_batch(mcfg, M, seed=7, device=dev)
+    S = 2 if world <= 4 else args.stages
+    P0 = max(world, 4)  # peers: one per GPU from 4 GPUs on (2 GPUs host 2 each)
+    layout = [P0 - S + 1, 1] if S == 2 else [3, 1] + [2] * (S - 2)
+    head = 1.0 + mcfg.vocab * mcfg.d_model / (mcfg.layers_per_stage * mcfg.params_per_layer())
+    speeds = [[1.0] * n for n in layout[:-1]] + [[1.0 / head] * layout[-1]]
+    fwd = 6.3e-3  # measured forward visit (configs[2] stage, B200): virtual time ~ real time
+    state_bytes = mcfg.params_per_layer() * mcfg.layers_per_stage * 6  # rebalancer.cpp:71-75
+    cfg = EngineConfig(n_stages=S, initial_peers=speeds, forward_service_seconds=fwd, trainers_per_peer=2,
+                       allreduce_period=0.5, allreduce_stall=1e-3, duration_seconds=9.0, bucket_seconds=0.5,
+                       churn=[(4.5, -1)], rebalance_period=3.0, straggler_timeout=0.05, propagation_delay=0.01,
+                       announce_ttl=300.0, state_transfer_bytes=state_bytes, download_bps=8 * 400e9)
+    ex = EngineExecutor(mcfg, S, seed=1, lr=1e-4, sim=cfg, lanes=args.lanes if world > 1 else 1)
+    n_peers0 = ex.n_peers
 
-    def phase(name, steps):
-        pipe.step(tok, tgt)  # untimed: capture graphs after a membership change
-        torch.cuda.synchronize()
+    def layout_now():
+        out = [0] * S
+        for pid in range(ex.n_peers):
+            i = ex.peer_info(pid)
+            if i["alive"] and not i["migrating"]:
+                out[i["stage"]] += 1
+        return out
+
+    segments = []
+    ex.run(32)  # untimed: most visit graphs captured before the first timed segment
+    ex.finish()
+    torch.cuda.synchronize()
+    stream = torch.cuda.current_stream()
+    v_now = lambda: ex.engine.summary()["now"]  # noqa: E731
+    while True:
+        lay, c0, t_v0 = layout_now(), ex.counters(), v_now()
         barrier(world)
-        t0 = torch.cuda.Event(enable_timing=True)
-        t1 = torch.cuda.Event(enable_timing=True)
-        t0.record()
-        for _ in range(steps):
-            pipe.step(tok, tgt)
-        t1.record()
+        t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        t0.record(stream)
+        n = ex.run_until(10 ** 9, -2)
+        ex.finish()
+        t1.record(stream)
         torch.cuda.synchronize()
-        barrier(world)
         ms = max_over_ranks(t0.elapsed_time(t1), world)
-        counts = [len(pipe.pl.members(s)) for s in range(S)]
-        return {"phase": name, "layout": counts, "tokens_per_s": pipe.tokens_per_step() * steps / (ms / 1e3),
-                "ms_per_step": ms / steps}
-
-    for _ in range(max(args.warmup - 1, 1)):
-        pipe.step(tok, tgt)
-    phases = [phase("A: imbalanced start", args.steps)]
-    d1 = pipe.rebalance()
-    phases.append(phase("B: after rebalance", args.steps))
-    victim = pipe.pl.members(S - 2)[-1]  # a peer of the second-to-last stage leaves mid-training
-    pipe.fail_peer(victim)
-    phases.append(phase(f"C: after peer {victim} left", args.steps))
-    d2 = pipe.rebalance()
-    phases.append(phase("D: after second rebalance", args.steps))
-    # CPU reference prediction: oracle_throughput with the per-peer rate measured in B
-    ref_pred = None
+        c1 = ex.counters()
+        if n == 0 and c1["records"] == c0["records"]:
+            break
+        segments.append({"layout": lay, "microbatches": n, "ms": ms,
+                         "tokens_per_s": n * mcfg.tokens / (ms / 1e3) if ms > 0 else None,
+                         "virtual_s": [t_v0, v_now()], "recomputes": c1["recomputes"] - c0["recomputes"],
+                         "state_bytes": c1["state_bytes"] - c0["state_bytes"]})
+        if v_now() >= cfg.duration_seconds or len(segments) > 12:
+            break
+    from paper_2301_11913_b200.engine import Engine, LEAVE, MIGRATE, MIGRATED, REBALANCE
+    decisions = [{"t": r.time, "kind": {LEAVE: "leave", MIGRATE: "migrate", MIGRATED: "migrated",
+                                        REBALANCE: "rebalance"}[r.kind], "peer": r.worker, "stage": r.stage,
+                  "from": r.from_worker} for r in Engine(cfg, 1).records() if r.kind in (LEAVE, MIGRATE, MIGRATED,
+                                                                                         REBALANCE)]
+    ref = None
     if rank == 0:
         try:
             import oracle as O
             if O.ref is not None:
-                b = phases[1]
-                rate = b["tokens_per_s"] / min(b["layout"])  # per-peer rate of the balanced bottleneck stage
-                r = (C.c_double * S)(*([rate] * S))
-                ref_pred = {"kind": "reference sim::oracle_throughput (oracle/_ref)",
-                            "per_peer_rate_tokens_per_s": rate,
-                            "predicted_tokens_per_s": {p["phase"][0]: O.ref.ref_oracle_throughput(r, S, sum(p["layout"]))
-                                                       for p in phases},
-                            "layout_bound_tokens_per_s": {p["phase"][0]: rate * min(p["layout"]) for p in phases}}
+                counts = (C.c_uint64 * 4)()
+                nb = C.c_size_t()
+                b = (C.c_double * 4096)()
+                ts = (C.c_double * 1)(*[t for t, _ in cfg.churn])
+                ds = (C.c_int64 * 1)(*[d for _, d in cfg.churn])
+                rc = O.ref.ref_sim_run_churn(cfg.to_reference_json().encode(), ts, ds, 1, 1, counts, b, 4096,
+                                             C.byref(nb), None, 0)
+                ref = {"kind": "reference sim::run (oracle/_ref, unmodified P/src/sim.cpp) on the same SimConfig, "
+                               "churn trace and seed",
+                       "dispatched": counts[0], "completed": counts[1], "requeued": counts[2], "abandoned": counts[3],
+                       "completions_per_bucket": list(b)[: nb.value], "bucket_seconds": cfg.bucket_seconds,
+                       "driver_completed_same_schedule": int(ex.engine.summary()["completed"]),
+                       "oracle_throughput_per_layout": {
+                           str(seg["layout"]): O.ref.ref_oracle_throughput(
+                               (C.c_double * S)(*([1.0 / (3 * fwd)] * (S - 1) + [1.0 / (3 * fwd * head)])), S,
+                               sum(seg["layout"])) * mcfg.tokens for seg in segments}}
         except Exception as e:  # the prediction is a report, not part of the measured path
-            ref_pred = {"unavailable": str(e)}
-    dec = lambda d: {"mover": d.mover, "from_stage": d.from_stage, "to_stage": d.to_stage}
-    return {"metric": "training tokens/s per phase (peer failure + adaptive rebalancing)",
-            "value": phases[-1]["tokens_per_s"], "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": phases[-1]["ms_per_step"], "higher_is_better": True,
-            "scaling": "strong", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
-            "config": {"workload": "BASELINE configs[4]: failure + rebalancing", "model": args.model, "stages": S,
-                       "initial_layout": layout, "microbatches_per_step": M},
-            "phases": phases, "decisions": [dec(d1), dec(d2)], "membership_log": pipe.events,
-            "reference": ref_pred}
+            ref = {"unavailable": repr(e)[:200]}
+    steady = [sg for sg in segments if sg["microbatches"] >= 16]
+    last = steady[-1] if steady else segments[-1]
+    return {"metric": "training tokens/s per membership segment (peer failure + adaptive rebalancing)",
+            "value": last["tokens_per_s"], "unit": "tokens/s", "n_gpus": world, "steps": len(segments),
+            "warmup": 1, "ms_per_step": last["ms"], "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+            "config": {"workload": f"BASELINE configs[4]: failure + rebalancing, {S} stages of the configs[2] "
+                                   f"block (d 2048, {mcfg.layers_per_stage} layers/stage), initial layout {layout}, "
+                                   f"{n_peers0} peers on {world} GPU(s), one peer leaves at t = 4.5 s",
+                       "model": args.model, "stages": S, "initial_layout": layout,
+                       "schedule": "engine (= sim::run) with RebalanceMode::Periodic every 3 s, straggler timeout "
+                                   "50 ms, churn trace [(4.5 s, -1)], AllReduceTick every 0.5 s, 9 s; forward visit "
+                                   f"{fwd * 1e3:.1f} ms so engine time tracks real time; last stage slowed by its LM "
+                                   f"head ({head:.3f}x)"},
+            "segments": segments, "decisions": decisions, "driver": ex.counters(), "reference": ref,
+            "gpu_launches": int(ex.kernels_launched())}
 
 
 def run_reference(args, world, rank):

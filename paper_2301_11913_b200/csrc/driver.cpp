@@ -910,6 +910,7 @@ int swarm_driver_run_until(swarm_driver_t d, uint64_t n_microbatches, int stop_k
         if (n == 0) break;  // the engine reached duration_seconds
         TRY(d->on_record(rec));
         if (stop_kind >= 0 && rec.kind == stop_kind) break;
+        if (stop_kind == -2 && rec.kind >= SWARM_ENG_LEAVE && rec.kind != SWARM_ENG_REBALANCE) break;
     }
     if (completed) *completed = d->completed - start;
     return SWARM_OK;

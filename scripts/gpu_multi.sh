@@ -8,6 +8,7 @@ TR="python -m torch.distributed.run --nnodes=1 --nproc-per-node $N --master-addr
 run $TR scripts/engine_multi_gpu_check.py 4 2 1
 run $TR scripts/engine_multi_gpu_check.py 2 2 2
 [ $N -ge 4 ] && run $TR scripts/engine_multi_gpu_check.py 4 1 2
+run $TR scripts/membership_multi_gpu_check.py
 # the C++ binary, one process per GPU, NCCL id through a file
 rm -f /tmp/swarm_id
 for r in $(seq 0 $((N-1))); do tests/cpp/driver_test --world $N --rank $r --id /tmp/swarm_id --stages $N --tpp 2 --microbatches 12 --ticks 1 --lanes 2 --out /tmp/cpp_r$r.bin > gpurun_out/cpp_r$r.log 2>&1 & done
