@@ -420,7 +420,8 @@ int swarm_rebalance_decide(size_t n_stages, const size_t* offsets, const uint64_
  * Workers are SimConfig::initial_peers flattened stage by stage (PeerId ==
  * index, as Engine::add_worker assigns them). */
 #define SWARM_ENG_START 0      /* worker begins the visit (trainer, stage, backward); time..end_time modeled */
-#define SWARM_ENG_HOP 1        /* trainer's input dispatched to `worker`'s queue; from_worker produced it (-1: new microbatch) */
+#define SWARM_ENG_HOP 1        /* trainer's input dispatched to `worker`'s queue; from_worker produced it (-1: new
+                                  microbatch; -2: not given -- the driver derives it from the START records) */
 #define SWARM_ENG_DONE 2       /* trainer's microbatch finished (backward at stage 0 on `worker`) */
 #define SWARM_ENG_ALLREDUCE 3  /* stage-wide all-reduce tick; starts stall until end_time */
 /* membership records (churn and rebalancing, P/src/sim.cpp:527-719) */

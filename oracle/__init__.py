@@ -22,6 +22,7 @@ import numpy as np
 HERE = os.path.dirname(os.path.abspath(__file__))
 ORC_PATH = os.path.join(HERE, "liborc.so")
 REF_PATH = os.path.join(HERE, "_ref", "libswarmsim_ref.so")
+HOOKED_PATH = os.path.join(HERE, "_ref", "libswarmsim_hooked.so")
 
 OK, E_INVALID, E_NONFINITE = 0, 1, 2
 
@@ -215,3 +216,17 @@ def f32_to_bf16_bits(x: np.ndarray) -> np.ndarray:
     u = np.ascontiguousarray(x, np.float32).view(np.uint32).astype(np.uint64)
     r = (u + 0x7FFF + ((u >> 16) & 1)) >> 16
     return r.astype(np.uint16)
+
+
+def _load_hooked():
+    """The reference engine with the additive record hook (oracle/hook_patch.py), or None."""
+    if not os.path.exists(HOOKED_PATH):
+        return None
+    lib = C.CDLL(HOOKED_PATH)
+    lib.hooked_sim_run.argtypes = [C.c_char_p, C.c_void_p, C.c_void_p, C.c_size_t, C.c_uint64, C.c_void_p,
+                                   C.c_void_p, C.c_void_p, C.c_void_p]
+    lib.hooked_sim_run.restype = C.c_int
+    return lib
+
+
+hooked = _load_hooked()

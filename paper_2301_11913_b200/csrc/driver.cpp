@@ -142,6 +142,12 @@ struct swarm_driver {
     std::vector<void*> allocs;
     // forward peer of each (trainer, stage) visit of the current microbatch (and its epoch)
     std::vector<int> fwd_peer, fwd_epoch;
+    // per trainer, derived from the records alone (so any engine emitting START / HOP / DONE
+    // drives the executor, e.g. the reference Engine through the hook of INTEGRATION.md §4):
+    // its current job (stage, direction), the peer of that job's latest START and the peer that
+    // ran the job before it (the producer of a requeued job's input), and its microbatch count
+    std::vector<int> job_key, job_peer, prev_peer;
+    std::vector<uint64_t> mb_count;
     // NCCL: one communicator + stream per rank pair, one per stage whose live peers span ranks
     std::vector<swarm_comm_t> pair_comm;
     std::vector<cudaStream_t> pair_stream;
@@ -355,7 +361,7 @@ struct swarm_driver {
             // activations from the trainer's stage input (activation checkpointing);
             // the output and the loss go to scratch (the pipeline already used them), the last
             // stage's LM-head gradient is accumulated here as the backward needs
-            TRY(load_tokens(t, r.microbatch, s, st));
+            TRY(load_tokens(t, mb_count[t], s, st));
             const void* inp = s == 0 ? static_cast<const void*>(tok[t]) : fin->p;
             const int32_t* tg = s == S - 1 ? tgt[t] : nullptr;
             TRY(swarm_stage_forward(p.st, t, inp, tg, s == S - 1 ? nullptr : scratch_wire, scratch_loss, scale, st));
@@ -366,7 +372,7 @@ struct swarm_driver {
             }
         }
         if (!bwd) {
-            TRY(load_tokens(t, r.microbatch, s, st));
+            TRY(load_tokens(t, mb_count[t], s, st));
             const void* inp = s == 0 ? static_cast<const void*>(tok[t]) : in->p;
             void* o = out ? out->p : nullptr;
             const int32_t* tg = s == S - 1 ? tgt[t] : nullptr;
@@ -436,7 +442,13 @@ struct swarm_driver {
         const bool bwd = r.backward != 0;
         if (t >= Tmax) return fail("driver: trainer beyond the driver's capacity");
         if (bwd) served[s] += 1;
-        log.push_back(VisitLog{r.trainer, r.stage, r.microbatch, r.backward, r.worker});
+        const int key = 2 * s + (bwd ? 1 : 0);
+        if (job_key[t] != key) {
+            prev_peer[t] = job_peer[t];
+            job_key[t] = key;
+        }
+        job_peer[t] = pid;
+        log.push_back(VisitLog{r.trainer, r.stage, mb_count[t], r.backward, r.worker});
         Buf* in = buf_for(t, s, bwd);
         if (in && in->xfer_op >= 0) {  // both ranks of a cross-rank hop, at the same record
             const int op = in->xfer_op;
@@ -485,8 +497,14 @@ struct swarm_driver {
         // (an event orders two peers' streams on one GPU).  A cross-rank transfer is noted here and
         // issued by both ranks at the consuming visit's START: a receive posted at dispatch time
         // would spin an NCCL kernel on the SMs through the whole producing visit.
-        const int64_t src = r.from_worker, dst = r.worker;
-        Buf* b = buf_for(static_cast<int>(r.trainer), static_cast<int>(r.stage), r.backward != 0);
+        const int t = static_cast<int>(r.trainer);
+        if (t >= Tmax) return fail("driver: trainer beyond the driver's capacity");
+        // the producer of the job's input: the peer that ran the trainer's previous job (a requeued
+        // job's predecessor); engines that know it (csrc/engine.cpp) give the same value
+        const int key = 2 * static_cast<int>(r.stage) + (r.backward ? 1 : 0);
+        const int64_t src = r.from_worker >= -1 ? r.from_worker : (job_key[t] == key ? prev_peer[t] : job_peer[t]);
+        const int64_t dst = r.worker;
+        Buf* b = buf_for(t, static_cast<int>(r.stage), r.backward != 0);
         if (!b) return SWARM_OK;
         if (b->xfer_op >= 0 && b->xfer_peer != dst) b->xfer_op = -1;  // a requeue replaces an older route
         if (src < 0 || src == dst) return SWARM_OK;
@@ -702,7 +720,13 @@ struct swarm_driver {
             case SWARM_ENG_START: return on_start(r);
             case SWARM_ENG_HOP: return on_hop(r);
             case SWARM_ENG_ALLREDUCE: return on_allreduce();
-            case SWARM_ENG_DONE: completed += 1; return SWARM_OK;
+            case SWARM_ENG_DONE:
+                completed += 1;
+                if (r.trainer < mb_count.size()) {
+                    mb_count[r.trainer] += 1;
+                    job_key[r.trainer] = -1;  // the next microbatch starts from the tokens
+                }
+                return SWARM_OK;
             case SWARM_ENG_LEAVE: return on_leave(r);
             case SWARM_ENG_JOIN: return on_join(r);
             case SWARM_ENG_MIGRATE: return on_migrate(r);
@@ -796,6 +820,10 @@ struct swarm_driver {
         }
         fwd_peer.assign(size_t(Tmax) * S, -1);
         fwd_epoch.assign(size_t(Tmax) * S, 0);
+        job_key.assign(Tmax, -1);
+        job_peer.assign(Tmax, -1);
+        prev_peer.assign(Tmax, -1);
+        mb_count.assign(Tmax, 0);
         const swarm_stage_config& m = c.model;
         tokens = m.seq_len * m.micro_batch;
         for (int pid = 0; pid < n0; ++pid)
