@@ -766,7 +766,8 @@ def run_engine(args, world, rank, local, model: str, S: int, steps: int, warmup:
     period = M * horizon / max(cal.summary()["completed"], 1)
     ex = EngineExecutor(mcfg, S, trainers_per_peer=args.trainers_per_peer, seed=1, lr=1e-4, forward_seconds=1.0,
                         backward_multiplier=bm, allreduce_period=period, allreduce_stall=0.05,
-                        stream_per_peer=not args.single_stream, lanes=args.lanes, fp32=fp32)
+                        stream_per_peer=not args.single_stream, lanes=args.lanes, fp32=fp32,
+                        dpu=bool(getattr(args, "dpu", False)))
     stream = torch.cuda.current_stream()
     # untimed warm-up: W steps plus two more (eight more with several peers per stage, whose
     # routes mix trainer pairs more), so that the visit graphs of most (peer, trainer pair, lane)
@@ -814,7 +815,9 @@ def run_engine(args, world, rank, local, model: str, S: int, steps: int, warmup:
                    "schedule": "forward 1.0 / backward 2.0 virtual s, AllReduceTick every "
                                f"{period:.4g} virtual s (= {M} completions at the schedule's own rate: one optimizer "
                                f"step per stage per {M} microbatches); one step = {M} microbatch completions",
-                   "optimizer": "AdamW (fused, fp32 master), paired weight gradients",
+                   "optimizer": "AdamW (fused, fp32 master), paired weight gradients" + (
+                       ", delayed parameter updates (tick all-reduce + AdamW overlapped with the next interval)"
+                       if getattr(args, "dpu", False) else ""),
                    "mean_loss": float(loss.item()) / max(tokens, 1),
                    "model_tflops_per_s": value * mcfg.flops_per_token(S) / 1e12,
                    "model_flops_per_token": mcfg.flops_per_token(S)},

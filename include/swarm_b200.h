@@ -357,6 +357,7 @@ int swarm_stage_sync_shadow(swarm_stage_t st, swarm_stream_t stream);
 int swarm_stage_enable_banks(swarm_stage_t st, swarm_stream_t stream);
 int swarm_stage_set_bank(swarm_stage_t st, int bank);
 float* swarm_stage_grads_bank(swarm_stage_t st, int bank);
+void* swarm_stage_params_bf16_bank(swarm_stage_t st, int bank); /* bank b's bf16 weight shadow */
 int swarm_stage_optimizer_step_bank(swarm_stage_t st, int bank, float grad_scale, swarm_stream_t stream);
 /* enumerate parameter tensors: index -> name, offset (elements), rows, cols */
 int swarm_stage_param_info(swarm_stage_t st, int index, const char** name, size_t* offset, size_t* rows,
@@ -543,6 +544,10 @@ typedef struct {
        pid * world / n_initial (joiners: pid % world), so any layout runs on any world size
        (peers sharing a GPU sum their gradients locally before the NCCL all-reduce). */
     const swarm_sim_config* sim;
+    /* delayed parameter updates: 1 = each tick's all-reduce + AdamW run on an
+       update stream, overlapped with the next interval, whose visits use the other weight / gradient bank
+       (swarm_stage_enable_banks): one optimizer step of delay */
+    int dpu;
 } swarm_driver_config;
 typedef struct {
     uint64_t records, visits, ticks, optimizer_steps, completed, captures, kernels;

@@ -64,7 +64,7 @@ class DriverConfig(C.Structure):
                 ("allreduce_period", C.c_double), ("allreduce_stall", C.c_double), ("duration_seconds", C.c_double),
                 ("trainers_per_peer", C.c_int), ("seed", C.c_uint64), ("lanes", C.c_int), ("pair_wgrad", C.c_int),
                 ("use_graphs", C.c_int), ("stream_per_peer", C.c_int), ("n_pool", C.c_int), ("comm", C.c_void_p),
-                ("sim", C.c_void_p)]
+                ("sim", C.c_void_p), ("dpu", C.c_int)]
 
 
 class DriverCounters(C.Structure):
@@ -130,6 +130,7 @@ SIGNATURES = {
     "swarm_stage_flush_wgrad": (I, [P, I, I, P]),
     "swarm_stage_set_bank": (I, [P, I]),
     "swarm_stage_grads_bank": (P, [P, I]),
+    "swarm_stage_params_bf16_bank": (P, [P, I]),
     "swarm_stage_optimizer_step_bank": (I, [P, I, F, P]),
     "swarm_stage_param_info": (I, [P, I, C.POINTER(C.c_char_p), C.POINTER(SZ), C.POINTER(SZ), C.POINTER(SZ)]),
     "swarm_stage_activation": (I, [P, I, I, C.c_char_p, C.POINTER(P), C.POINTER(SZ)]),

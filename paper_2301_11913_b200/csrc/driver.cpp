@@ -96,6 +96,11 @@ struct Peer {
     std::vector<cudaEvent_t> slot_ev;
     std::vector<char> has_slot;
     cudaEvent_t lane_ev = nullptr;
+    // delayed parameter updates: the all-reduce + AdamW of bank b run on `upd` while the visits
+    // continue on the other bank; upd_ev[b] marks that update's end
+    cudaStream_t upd = nullptr;
+    cudaEvent_t upd_ev[2] = {nullptr, nullptr};
+    bool upd_pending[2] = {false, false};
 };
 
 struct Graph {
@@ -164,6 +169,7 @@ struct swarm_driver {
     // profiling on, so the events around each kernel time it alone (the live roofline)
     bool prof = false;
     cudaStream_t prof_stream = nullptr;
+    int bank = 0;  // DPU: the bank (weights shadow + gradient arena) the current interval's visits use
 
     cudaStream_t lane_stream(const Peer& p) const { return prof ? prof_stream : p.lanes[p.cur]; }
 
@@ -188,9 +194,9 @@ struct swarm_driver {
     }
 
     // ------------------------------------------------------------- graphs
-    static uint64_t gkey(int pid, int kind, int t, int p, int lane) {
+    uint64_t gkey(int pid, int kind, int t, int p, int lane) const {  // + the DPU bank: graphs bake its pointers
         return (uint64_t(pid) << 48) | (uint64_t(kind) << 44) | (uint64_t(t & 0xFFFF) << 28) |
-               (uint64_t((p + 1) & 0xFFFF) << 12) | uint64_t(lane & 0xFFF);
+               (uint64_t((p + 1) & 0xFFFF) << 12) | (uint64_t(bank & 1) << 11) | uint64_t(lane & 0x7FF);
     }
 
     int replay(uint64_t key, cudaStream_t st, const std::function<int()>& fn) {
@@ -274,6 +280,11 @@ struct swarm_driver {
             return fail(std::string("driver: ") + swarm_last_error());
         if (cfg.lanes > 1 && swarm_stage_enable_lanes(p.st, cfg.lanes) != SWARM_OK)
             return fail(std::string("driver: ") + swarm_last_error());
+        if (cfg.dpu) {
+            if (swarm_stage_enable_banks(p.st, nullptr) != SWARM_OK || swarm_stage_set_bank(p.st, bank) != SWARM_OK)
+                return fail(std::string("driver: ") + swarm_last_error());
+            CU(cudaDeviceSynchronize());
+        }
         std::fill(p.has_slot.begin(), p.has_slot.end(), 0);
         p.pend = -1;
         p.rr = p.cur = 0;
@@ -300,6 +311,10 @@ struct swarm_driver {
         p->has_slot.assign(Tmax, 0);
         for (auto& e : p->slot_ev) CU(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
         CU(cudaEventCreateWithFlags(&p->lane_ev, cudaEventDisableTiming));
+        if (cfg.dpu) {
+            CU(cudaStreamCreateWithFlags(&p->upd, cudaStreamNonBlocking));
+            for (auto& e : p->upd_ev) CU(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        }
         local[pid] = p.get();
         peers.push_back(std::move(p));
         return SWARM_OK;
@@ -482,6 +497,7 @@ struct swarm_driver {
             TRY(swarm_stage_set_lane(p.st, p.cur));
             TRY(after_slot(p, t));  // this slot's previous visit (e.g. the last stage's forward)
         }
+        if (p.upd_pending[bank]) TRY(wait(lane_stream(p), p.upd_ev[bank]));  // DPU: this bank's weights are ready
         int paired = -1;
         TRY(visit(p, r, s, t, bwd, recompute, &paired));
         if (cfg.lanes > 1) {
@@ -528,7 +544,57 @@ struct swarm_driver {
 
     bool serving(const Peer& p) const { return !p.dead && !p.migrating; }
 
+    // DPU tick: the interval's gradients (bank b) are all-reduced and applied by AdamW on each
+    // stage lead's update stream, overlapped with the next interval, which computes on bank 1 - b (the
+    // weights of the previous update: one step of delay) after that bank's own update has finished
+    int on_allreduce_dpu() {
+        ticks += 1;
+        for (auto& p : peers) TRY(join_lanes(*p));
+        for (auto& p : peers)
+            if (p->pend >= 0 && serving(*p)) TRY(flush(*p));
+        const int b = bank;
+        for (int s = 0; s < S; ++s) {
+            const int n = served[s];
+            std::vector<Peer*> mine;
+            for (auto& p : peers)
+                if (serving(*p) && p->stage == s) mine.push_back(p.get());
+            if (mine.empty() || n == 0) continue;
+            Peer& lead = *mine[0];
+            cudaStream_t u = lead.upd;
+            for (Peer* q : mine) TRY(after_peer(u, *q));
+            if (prof) {  // the profiled region's visits ran on the profile stream
+                TRY(mark(ev_tmp, prof_stream));
+                TRY(wait(u, ev_tmp));
+            }
+            const size_t np = swarm_stage_num_params(lead.st);
+            float* lg = swarm_stage_grads_bank(lead.st, b);
+            for (size_t i = 1; i < mine.size(); ++i) TRY(swarm_add_f32(lg, swarm_stage_grads_bank(mine[i]->st, b), np, u));
+            if (stage_comm[s]) TRY(swarm_allreduce_sum(stage_comm[s], lg, np, SWARM_DTYPE_F32, u));
+            for (size_t i = 1; i < mine.size(); ++i)
+                CU(cudaMemcpyAsync(swarm_stage_grads_bank(mine[i]->st, b), lg, np * sizeof(float),
+                                   cudaMemcpyDeviceToDevice, u));
+            for (Peer* q : mine) TRY(swarm_stage_optimizer_step_bank(q->st, b, 1.0f / static_cast<float>(n), u));
+            for (Peer* q : mine) {
+                TRY(mark(q->upd_ev[b], u));
+                q->upd_pending[b] = true;
+            }
+            optimizer_steps += mine.size();
+        }
+        for (int pid = 0; pid < static_cast<int>(peer_stage.size()); ++pid)
+            if (peer_alive[pid] && !peer_migrating[pid] && served[peer_stage[pid]] > 0) peer_steps[pid] += 1;
+        bank ^= 1;
+        for (auto& p : peers)
+            if (p->st) TRY(swarm_stage_set_bank(p->st, bank));
+        for (auto& p : peers) {  // every lane of the peer continues after the join
+            TRY(mark(p->lane_ev, p->lanes[0]));
+            for (size_t i = 1; i < p->lanes.size(); ++i) TRY(wait(p->lanes[i], p->lane_ev));
+        }
+        std::fill(served.begin(), served.end(), 0);
+        return SWARM_OK;
+    }
+
     int on_allreduce() {
+        if (cfg.dpu) return on_allreduce_dpu();
         ticks += 1;
         for (auto& p : peers) TRY(join_lanes(*p));  // the tick follows every visit on every lane
         for (auto& p : peers)
@@ -621,6 +687,10 @@ struct swarm_driver {
             swarm_stage_optimizer_state(pd->st, &dm, &dv, nullptr);
         }
         state_bytes += np * 12;
+        if (ps && ps->upd) {  // DPU: the source's update in flight lands first
+            TRY(mark(ev_tmp, ps->upd));
+            for (cudaStream_t s : ps->lanes) TRY(wait(s, ev_tmp));
+        }
         if (rs == rd) {  // both on this GPU
             cudaStream_t st = pd->lanes[0];
             TRY(after_peer(st, *ps));
@@ -742,6 +812,9 @@ struct swarm_driver {
         for (auto& p : peers) {
             for (cudaEvent_t e : p->slot_ev) cudaEventDestroy(e);
             if (p->lane_ev) cudaEventDestroy(p->lane_ev);
+            for (cudaEvent_t e : p->upd_ev)
+                if (e) cudaEventDestroy(e);
+            if (p->upd) cudaStreamDestroy(p->upd);
             if (p->st) swarm_stage_destroy(p->st);
         }
         for (cudaStream_t s : streams) cudaStreamDestroy(s);
@@ -971,6 +1044,11 @@ int swarm_driver_finish(swarm_driver_t d, swarm_stream_t stream) {
             b.has_recvd = false;
         }
     }
+    for (auto& p : d->peers)  // delayed parameter updates in flight
+        if (p->upd) {
+            CU(cudaEventRecord(d->ev_tmp, p->upd));
+            CU(cudaStreamWaitEvent(cur, d->ev_tmp, 0));
+        }
     for (cudaStream_t s : d->pair_stream)  // state downloads
         if (s) {
             CU(cudaEventRecord(d->ev_tmp, s));

@@ -961,6 +961,11 @@ int swarm_stage_set_bank(swarm_stage_t s, int bank) {
     return SWARM_OK;
 }
 
+void* swarm_stage_params_bf16_bank(swarm_stage_t s, int bank) {
+    if (!s->banks) return bank == 0 ? s->p16 : nullptr;
+    return (bank == 0 || bank == 1) ? s->p16b[bank] : nullptr;
+}
+
 float* swarm_stage_grads_bank(swarm_stage_t s, int bank) {
     if (!s->banks) return bank == 0 ? s->grad : nullptr;
     return (bank == 0 || bank == 1) ? s->gradb[bank] : nullptr;

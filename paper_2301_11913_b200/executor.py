@@ -464,7 +464,8 @@ class EngineExecutor:
                  backward_multiplier: float = 2.0, allreduce_period: float = 0.0, allreduce_stall: float = 0.0,
                  duration_seconds: float = 1e9, use_graphs: bool = True, n_pool: int = 16,
                  tokens: torch.Tensor | None = None, targets: torch.Tensor | None = None, pair_wgrad: bool = True,
-                 stream_per_peer: bool = True, lanes: int = 1, fp32: bool = False, sim: EngineConfig | None = None):
+                 stream_per_peer: bool = True, lanes: int = 1, fp32: bool = False, sim: EngineConfig | None = None,
+                 dpu: bool = False):
         """sim: a full SimConfig (initial_peers with speeds, churn trace, rebalancing); it replaces
         the engine arguments and gives the layout (any layout on any world size)."""
         import ctypes as C
@@ -508,6 +509,7 @@ class EngineExecutor:
         c.pair_wgrad, c.use_graphs, c.stream_per_peer = int(pair_wgrad), int(use_graphs), int(stream_per_peer)
         c.n_pool = n_pool if tokens is None else int(tokens.shape[0])
         c.comm = self.comm
+        c.dpu = int(dpu)
         if sim is not None:
             self._sim_c = sim.to_c()
             c.sim = C.cast(C.pointer(self._sim_c), C.c_void_p)

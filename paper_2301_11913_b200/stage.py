@@ -169,6 +169,12 @@ class Stage:
             raise ValueError(f"no gradient bank {bank}")
         return device_view(ptr, self.n_params, torch.float32, self.device)
 
+    def params_bf16_bank(self, bank: int) -> torch.Tensor:
+        ptr = self.lib.swarm_stage_params_bf16_bank(self.h, bank)
+        if not ptr:
+            raise ValueError(f"no weight bank {bank}")
+        return device_view(ptr, self.n_params, torch.bfloat16, self.device)
+
     def optimizer_step_bank(self, bank: int, grad_scale: float = 1.0, stream=None) -> None:
         L.check(self.lib.swarm_stage_optimizer_step_bank(self.h, bank, grad_scale, _stream(stream)),
                 "stage_optimizer_step_bank")
