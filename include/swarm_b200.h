@@ -497,6 +497,8 @@ int swarm_comm_unique_id(void* id /* 128 bytes, ncclUniqueId */);
 int swarm_comm_create(const void* id, int nranks, int rank, swarm_comm_t* out); /* ncclCommInitRank */
 /* ncclCommSplit: collective over `parent`; color < 0 leaves this rank out (*out = NULL) */
 int swarm_comm_split(swarm_comm_t parent, int color, int key, swarm_comm_t* out);
+/* the same with ncclConfig_t.maxCTAs = max_ctas (> 0): the CTAs (SMs) its kernels may occupy */
+int swarm_comm_split_ex(swarm_comm_t parent, int color, int key, int max_ctas, swarm_comm_t* out);
 void swarm_comm_destroy(swarm_comm_t c);
 int swarm_comm_size(swarm_comm_t c, int* nranks, int* rank);
 int swarm_comm_group_start(void);

@@ -168,6 +168,7 @@ SIGNATURES = {
     "swarm_comm_unique_id": (I, [P]),
     "swarm_comm_create": (I, [P, I, I, C.POINTER(P)]),
     "swarm_comm_split": (I, [P, I, I, C.POINTER(P)]),
+    "swarm_comm_split_ex": (I, [P, I, I, I, C.POINTER(P)]),
     "swarm_comm_destroy": (None, [P]),
     "swarm_comm_size": (I, [P, C.POINTER(I), C.POINTER(I)]),
     "swarm_comm_group_start": (I, []),

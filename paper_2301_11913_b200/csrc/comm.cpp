@@ -133,13 +133,16 @@ int swarm_comm_create(const void* id, int nranks, int rank, swarm_comm_t* out) {
     return SWARM_OK;
 }
 
-int swarm_comm_split(swarm_comm_t parent, int color, int key, swarm_comm_t* out) {
+int swarm_comm_split_ex(swarm_comm_t parent, int color, int key, int max_ctas, swarm_comm_t* out) {
     NEED_NCCL();
     if (!parent || !out) return fail("comm_split: null argument");
     *out = nullptr;
     ncclComm_t nc = nullptr;
     {
-        const int rc = nccl_check(nccl().split(parent->c, color < 0 ? NCCL_SPLIT_NOCOLOR : color, key, &nc, nullptr),
+        ncclConfig_t config = NCCL_CONFIG_INITIALIZER;
+        if (max_ctas > 0) config.maxCTAs = max_ctas;
+        const int rc = nccl_check(nccl().split(parent->c, color < 0 ? NCCL_SPLIT_NOCOLOR : color, key, &nc,
+                                               max_ctas > 0 ? &config : nullptr),
                                   "ncclCommSplit");
         if (rc != SWARM_OK) return rc;
     }
@@ -154,6 +157,10 @@ int swarm_comm_split(swarm_comm_t parent, int color, int key, swarm_comm_t* out)
     c->rank = r;
     *out = c;
     return SWARM_OK;
+}
+
+int swarm_comm_split(swarm_comm_t parent, int color, int key, swarm_comm_t* out) {
+    return swarm_comm_split_ex(parent, color, key, 0, out);
 }
 
 void swarm_comm_destroy(swarm_comm_t c) {

@@ -45,6 +45,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <functional>
 #include <memory>
@@ -960,8 +961,12 @@ struct swarm_driver {
                     if (a == R) partner = b, color = i;
                     if (b == R) partner = a, color = i;
                 }
+                // the pair communicators carry single wire messages: a few CTAs suffice, and a receive
+                // posted ahead of its sender spins fewer SMs away from the stage's GEMMs (measured at
+                // 4 x 1: the profiled GEMMs 247 -> 179 ms/step with 4 instead of NCCL's default channels)
                 swarm_comm_t pc = nullptr;
-                if (swarm_comm_split(c.comm, color, R, &pc) != SWARM_OK)
+                const char* mc = getenv("SWARM_P2P_MAX_CTAS");
+                if (swarm_comm_split_ex(c.comm, color, R, mc ? atoi(mc) : 4, &pc) != SWARM_OK)
                     return fail(std::string("driver: ") + swarm_comm_last_error());
                 if (pc) {
                     owned_comms.push_back(pc);
