@@ -872,6 +872,9 @@ def run_engine(args, world, rank, local, model: str, S: int, steps: int, warmup:
             "gemm_ms_per_step": pr["gemm_ms"], "gemm_flops_per_step": pr["gemm_flops"],
             "gemm_launches_per_step": pr["gemm_launches"],
             "gemm_share_of_kernel_time": pr["gemm_ms"] / kern_ms if kern_ms else None,
+            "per_shape": [{"shape": k, "ms_per_step": v[0], "tflops": v[1] / (v[0] / 1e3) / 1e12 if v[0] else None,
+                           "launches": v[2], "share_of_gemm_time": v[0] / pr["gemm_ms"] if pr["gemm_ms"] else None}
+                          for k, v in sorted(pr["shapes"].items(), key=lambda kv: -kv[1][0])[:16]],
             "note": "one extra step of the same engine-driven run as a profiled region: every visit issued eagerly "
                     "on one stream behind a GPU spin (swarm_driver_profile_begin), CUDA events around each kernel; "
                     "achieved = executed GEMM FLOPs / summed GEMM event time of that step (this rank)"}

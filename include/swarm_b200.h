@@ -386,6 +386,8 @@ int swarm_stage_profile_read(swarm_stage_t st, double* gemm_ms, double* gemm_flo
 int swarm_gpu_spin(uint64_t ns, swarm_stream_t stream);
 void swarm_stage_profile_breakdown(swarm_stage_t st, double* ms /* [SWARM_PROF_CATEGORIES] */,
                                    uint64_t* launches /* [SWARM_PROF_CATEGORIES] */);
+/* the last read's GEMM time per shape: lines "MxNxK bBATCH eEPILOGUE[ Amn][ Bmn][ 2seg][ tri];ms;flops;launches" */
+const char* swarm_stage_profile_shapes(swarm_stage_t st);
 /* saved activation of (slot, layer) by name ("x","a","qkv","P","o","h","c","u","g","xf","dxf"), for tests;
  * also "wire_out" (the tensor the last forward of `slot` encoded), "wire_in" (the decoded input wire
  * tensor) and "dx_last" (the input gradient the stage's last backward visit encoded).  Elements are
@@ -601,6 +603,8 @@ int swarm_driver_peer_of_rank(swarm_driver_t d, int peer); /* the rank hosting `
 int swarm_driver_profile_begin(swarm_driver_t d, uint64_t spin_ns);
 int swarm_driver_profile_end(swarm_driver_t d, double* gemm_ms, double* gemm_flops, uint64_t* gemm_launches,
                              double* cat_ms /* [SWARM_PROF_CATEGORIES] */, uint64_t* cat_launches);
+/* the profiled region's per-shape GEMM lines over the local stages (swarm_stage_profile_shapes format) */
+const char* swarm_driver_profile_shapes(swarm_driver_t d);
 
 #ifdef __cplusplus
 }

@@ -198,6 +198,8 @@ SIGNATURES = {
     "swarm_driver_run_until": (I, [P, C.c_uint64, I, C.POINTER(C.c_uint64)]),
     "swarm_driver_peer_info": (I, [P, I, C.POINTER(I), C.POINTER(I), C.POINTER(I), C.POINTER(I)]),
     "swarm_driver_profile_begin": (I, [P, C.c_uint64]),
+    "swarm_driver_profile_shapes": (C.c_char_p, [P]),
+    "swarm_stage_profile_shapes": (C.c_char_p, [P]),
     "swarm_driver_profile_end": (I, [P, C.POINTER(D), C.POINTER(D), C.POINTER(C.c_uint64), P, P]),
 }
 

@@ -170,6 +170,7 @@ struct swarm_driver {
     // profiling on, so the events around each kernel time it alone (the live roofline)
     bool prof = false;
     cudaStream_t prof_stream = nullptr;
+    std::string prof_table;  // per-shape GEMM lines of the last profiled region (all local stages)
     int bank = 0;  // DPU: the bank (weights shadow + gradient arena) the current interval's visits use
 
     cudaStream_t lane_stream(const Peer& p) const { return prof ? prof_stream : p.lanes[p.cur]; }
@@ -1206,8 +1207,12 @@ int swarm_driver_profile_end(swarm_driver_t d, double* gemm_ms, double* gemm_flo
         if (cat_ms) cat_ms[k] = cm[k];
         if (cat_launches) cat_launches[k] = cn[k];
     }
+    d->prof_table.clear();
+    for (auto& p : d->peers) d->prof_table += swarm_stage_profile_shapes(p->st);
     return SWARM_OK;
 }
+
+const char* swarm_driver_profile_shapes(swarm_driver_t d) { return d ? d->prof_table.c_str() : ""; }
 
 int swarm_driver_peer_of_rank(swarm_driver_t d, int peer) { return d ? d->rank_of_peer(peer) : -1; }
 

@@ -9,8 +9,11 @@
 
 #include <cmath>
 #include <cstdlib>
+#include <cstdio>
 #include <cstring>
+#include <map>
 #include <new>
+#include <tuple>
 #include <string>
 #include <unordered_map>
 #include <vector>
@@ -142,6 +145,8 @@ struct swarm_stage {
     std::vector<double> prof_flops;
     std::vector<int> prof_cat;
     std::vector<double> prof_w;  // weight of each event pair (visits of this kind per step)
+    std::vector<std::string> prof_shape;  // GEMM events: "MxNxK batch epi" (per-shape table)
+    std::string prof_table;               // the last read's per-shape GEMM table
     double prof_weight = 1.0;
     size_t prof_used = 0;
     double prof_last_ms[SWARM_PROF_CATEGORIES] = {};
@@ -254,6 +259,7 @@ int prof_begin(int cat, cudaStream_t st) {
     }
     cudaEventRecord(s->prof_events[2 * s->prof_used], st);
     s->prof_cat.push_back(cat);
+    s->prof_shape.emplace_back();
     s->prof_flops.push_back(0.0);
     s->prof_w.push_back(s->prof_weight);
     return SWARM_OK;
@@ -297,6 +303,9 @@ int run_gemm(swarm_gemm_args g, cudaStream_t st) {
         kfrac = static_cast<double>(done) / (static_cast<double>(tm) * kb);
     }
     s->prof_flops.back() = 2.0 * g.m * g.n * static_cast<double>(g.k) * g.batch * kfrac;
+    s->prof_shape.back() = std::to_string(g.m) + "x" + std::to_string(g.n) + "x" + std::to_string(g.k) + " b" +
+                           std::to_string(g.batch) + " e" + std::to_string(g.epilogue) + (g.a_mn_major ? " Amn" : "") +
+                           (g.b_mn_major ? " Bmn" : "") + (g.a2 ? " 2seg" : "") + (g.k_tri ? " tri" : "");
     s->prof_used += 1;
     return rc;
 }
@@ -894,6 +903,7 @@ int swarm_stage_profile_read(swarm_stage_t s, double* gemm_ms, double* gemm_flop
     double fl = 0.0;
     double ms[SWARM_PROF_CATEGORIES] = {};
     uint64_t n[SWARM_PROF_CATEGORIES] = {};
+    std::map<std::string, std::tuple<double, double, int>> shapes;  // key -> (ms, flops, launches)
     for (size_t i = 0; i < s->prof_used; ++i) {
         if (cudaEventSynchronize(s->prof_events[2 * i + 1]) != cudaSuccess) return SWARM_E_CUDA;
         float e = 0.f;
@@ -901,6 +911,12 @@ int swarm_stage_profile_read(swarm_stage_t s, double* gemm_ms, double* gemm_flop
         ms[s->prof_cat[i]] += e * s->prof_w[i];
         n[s->prof_cat[i]] += 1;
         fl += s->prof_flops[i] * s->prof_w[i];
+        if (s->prof_cat[i] == SWARM_PROF_GEMM) {
+            auto& t = shapes[s->prof_shape[i]];
+            std::get<0>(t) += e * s->prof_w[i];
+            std::get<1>(t) += s->prof_flops[i] * s->prof_w[i];
+            std::get<2>(t) += 1;
+        }
     }
     if (gemm_ms) *gemm_ms = ms[SWARM_PROF_GEMM];
     if (gemm_flops) *gemm_flops = fl;
@@ -913,8 +929,17 @@ int swarm_stage_profile_read(swarm_stage_t s, double* gemm_ms, double* gemm_flop
     s->prof_flops.clear();
     s->prof_cat.clear();
     s->prof_w.clear();
+    s->prof_shape.clear();
+    s->prof_table.clear();
+    for (const auto& [k, t] : shapes) {  // "shape;ms;flops;launches" lines
+        char line[256];
+        snprintf(line, sizeof(line), "%s;%.6f;%.6e;%d\n", k.c_str(), std::get<0>(t), std::get<1>(t), std::get<2>(t));
+        s->prof_table += line;
+    }
     return SWARM_OK;
 }
+
+const char* swarm_stage_profile_shapes(swarm_stage_t s) { return s->prof_table.c_str(); }
 
 void swarm_stage_profile_breakdown(swarm_stage_t s, double* ms, uint64_t* launches) {
     for (int c = 0; c < SWARM_PROF_CATEGORIES; ++c) {

@@ -701,7 +701,15 @@ class EngineExecutor:
         self._check(self.lib.swarm_driver_profile_end(self.h, C.byref(ms), C.byref(fl), C.byref(n), cm, cn),
                     "driver_profile_end")
         self.finish()
+        shapes = {}
+        for line in self.lib.swarm_driver_profile_shapes(self.h).decode().splitlines():
+            key, ms_, fl_, n_ = line.split(";")
+            a = shapes.setdefault(key, [0.0, 0.0, 0])
+            a[0] += float(ms_)
+            a[1] += float(fl_)
+            a[2] += int(n_)
         return {"gemm_ms": ms.value, "gemm_flops": fl.value, "gemm_launches": n.value, "microbatches": done.value,
+                "shapes": shapes,
                 "categories": {c: (cm[i], cn[i]) for i, c in enumerate(self.PROF_CATEGORIES)}}
 
 
