@@ -134,6 +134,8 @@ int swarm_matvec_f64(const double* x, size_t rows, const double* w, size_t cols,
 #define SWARM_EPI_RESIDUAL 3    /* D = bf16(alpha*acc + R)                     */
 #define SWARM_EPI_GELU 4        /* U = bf16(acc); D = bf16(gelu(acc))          */
 #define SWARM_EPI_DGELU 5       /* D = bf16(acc * gelu'(U))                    */
+#define SWARM_EPI_GELU_DERIV 6  /* U = bf16(gelu'(acc)); D = bf16(gelu(acc))   (one tanh for both) */
+#define SWARM_EPI_MUL 7         /* D = bf16(acc * U)   (the MLP backward with U = gelu' saved) */
 typedef struct {
     int m, n, k, batch, bh;
     /* operand storage: a_rows x a_cols row-major with row stride lda (0,0 =

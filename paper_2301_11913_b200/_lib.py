@@ -15,7 +15,7 @@ LIB_PATH = os.path.join(HERE, "libswarm_b200.so")
 SWARM_OK, SWARM_E_INVALID, SWARM_E_NONFINITE, SWARM_E_CUDA, SWARM_E_UNSUPPORTED, SWARM_E_NO_PEER = 0, 1, 2, 3, 4, 5
 DT_F32, DT_BF16, DT_F64 = 0, 1, 2
 FLAG_NONFINITE = 1
-EPI_STORE_BF16, EPI_STORE_F32, EPI_ACCUM_F32, EPI_RESIDUAL, EPI_GELU, EPI_DGELU = range(6)
+EPI_STORE_BF16, EPI_STORE_F32, EPI_ACCUM_F32, EPI_RESIDUAL, EPI_GELU, EPI_DGELU, EPI_GELU_DERIV, EPI_MUL = range(8)
 
 
 class GemmArgs(C.Structure):

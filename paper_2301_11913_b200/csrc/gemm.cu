@@ -74,14 +74,32 @@ struct Cfg {
     static_assert(2 * STAGES * 8 + 4 * 8 + 4 <= 256, "barrier area overflow");
 };
 
+// tanh on the SFU (MUFU.TANH, max relative error ~2^-11): the GeLU epilogues round to bf16
+// (2^-8), so the accurate tanhf -- ~20 FMA-pipe instructions per element -- only cost issue
+// slots (the live per-shape table showed the DGELU GEMM at 689 TFLOP/s against ~1100 for the
+// same shape with a plain epilogue).  The fp32 mode's GEMM (gemm_f32.cu) keeps tanhf.
+__device__ __forceinline__ float tanh_approx(float x) {
+    float y;
+    asm("tanh.approx.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
 __device__ __forceinline__ float gelu_f(float x) {
     const float k0 = 0.7978845608028654f, k1 = 0.044715f;
-    return 0.5f * x * (1.f + tanhf(k0 * (x + k1 * x * x * x)));
+    const float hx = 0.5f * x;
+    return fmaf(hx, tanh_approx(k0 * fmaf(k1 * x, x * x, x)), hx);
+}
+// gelu(x) and gelu'(x) from one tanh (SWARM_EPI_GELU_DERIV)
+__device__ __forceinline__ void gelu_both(float x, float& g, float& dg) {
+    const float k0 = 0.7978845608028654f, k1 = 0.044715f;
+    const float t = tanh_approx(k0 * fmaf(k1 * x, x * x, x));
+    const float hx = 0.5f * x;
+    g = fmaf(hx, t, hx);
+    dg = fmaf(0.5f, 1.f + t, hx * fmaf(-t, t, 1.f) * k0 * fmaf(3.f * k1, x * x, 1.f));
 }
 __device__ __forceinline__ float dgelu_f(float x) {
     const float k0 = 0.7978845608028654f, k1 = 0.044715f;
-    const float t = tanhf(k0 * (x + k1 * x * x * x));
-    return 0.5f * (1.f + t) + 0.5f * x * (1.f - t * t) * k0 * (1.f + 3.f * k1 * x * x);
+    const float t = tanh_approx(k0 * fmaf(k1 * x, x * x, x));
+    return fmaf(0.5f, 1.f + t, 0.5f * x * fmaf(-t, t, 1.f) * k0 * fmaf(3.f * k1, x * x, 1.f));
 }
 
 __device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
@@ -205,6 +223,24 @@ __device__ __forceinline__ void epilogue_chunk(const Params& p, float (&v)[32], 
             }
             break;
         }
+        case SWARM_EPI_GELU_DERIV:
+        case SWARM_EPI_MUL: {
+            __nv_bfloat16* dst = static_cast<__nv_bfloat16*>(p.d) + off;
+            __nv_bfloat16* u = const_cast<__nv_bfloat16*>(static_cast<const __nv_bfloat16*>(p.aux)) + off;
+#pragma unroll
+            for (int j = 0; j < 32; ++j) {
+                if (j >= ncols_valid) continue;
+                if (p.epi == SWARM_EPI_MUL) {
+                    dst[j] = __float2bfloat16_rn(v[j] * __bfloat162float(u[j]));
+                } else {
+                    float g, dg;
+                    gelu_both(v[j], g, dg);
+                    u[j] = __float2bfloat16_rn(dg);
+                    dst[j] = __float2bfloat16_rn(g);
+                }
+            }
+            break;
+        }
         default: break;
     }
 }
@@ -322,6 +358,30 @@ __device__ __forceinline__ void drain_tile(const Params& p, const CUtensorMap* m
                 }
                 stage_bf16(slot, lane, v);
                 break;
+            case SWARM_EPI_GELU_DERIV: {  // U = gelu'(pre-activation), D = gelu(pre-activation)
+                float dg[32];
+#pragma unroll
+                for (int j = 0; j < 32; ++j) gelu_both(v[j], v[j], dg[j]);
+                stage_bf16(slot + 2048, lane, dg);
+                stage_bf16(slot, lane, v);
+                break;
+            }
+            case SWARM_EPI_MUL:  // D = acc * U (U = gelu' saved by the forward)
+                if (row_ok) {
+                    const uint4* u4 = reinterpret_cast<const uint4*>(static_cast<const __nv_bfloat16*>(p.aux) + off);
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        const uint4 w = u4[q];
+                        const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+                        for (int j = 0; j < 4; ++j) {
+                            v[q * 8 + 2 * j] *= bf_lo(ws[j]);
+                            v[q * 8 + 2 * j + 1] *= bf_hi(ws[j]);
+                        }
+                    }
+                }
+                stage_bf16(slot, lane, v);
+                break;
             default:
                 stage_bf16(slot, lane, v);
                 break;
@@ -331,7 +391,7 @@ __device__ __forceinline__ void drain_tile(const Params& p, const CUtensorMap* m
         if (lane == 0 && row_base < p.m && !(p.dbg & 1)) {
             if (p.epi == SWARM_EPI_ACCUM_F32) tma_reduce_add_2d(md, slot, gc, gr);
             else tma_store_2d(md, slot, gc, gr);
-            if (p.epi == SWARM_EPI_GELU) tma_store_2d(mu, slot + 2048, gc, gr);
+            if (p.epi == SWARM_EPI_GELU || p.epi == SWARM_EPI_GELU_DERIV) tma_store_2d(mu, slot + 2048, gc, gr);
             bulk_commit();
         }
     }
@@ -1114,10 +1174,11 @@ extern "C" int swarm_gemm_bf16(const swarm_gemm_args* a, swarm_stream_t stream) 
     if (!a) return invalid("gemm: null args");
     if (a->m <= 0 || a->n <= 0 || a->k <= 0 || a->batch <= 0 || a->bh <= 0) return invalid("gemm: bad shape");
     if (!a->a || !a->b || !a->d) return invalid("gemm: null operand");
-    if ((a->epilogue == SWARM_EPI_RESIDUAL || a->epilogue == SWARM_EPI_GELU || a->epilogue == SWARM_EPI_DGELU) &&
+    if ((a->epilogue == SWARM_EPI_RESIDUAL || a->epilogue == SWARM_EPI_GELU || a->epilogue == SWARM_EPI_DGELU ||
+         a->epilogue == SWARM_EPI_GELU_DERIV || a->epilogue == SWARM_EPI_MUL) &&
         !a->aux)
         return invalid("gemm: epilogue needs aux");
-    if (a->epilogue < 0 || a->epilogue > SWARM_EPI_DGELU) return invalid("gemm: bad epilogue");
+    if (a->epilogue < 0 || a->epilogue > SWARM_EPI_MUL) return invalid("gemm: bad epilogue");
     if (a->k_tri < 0 || a->k_tri > 2 || (a->k_tri && a->m != a->k)) return invalid("gemm: k_tri needs M == K");
     if (a->lda % 8 || a->ldb % 8 || (reinterpret_cast<uintptr_t>(a->a) & 15) || (reinterpret_cast<uintptr_t>(a->b) & 15))
         return invalid("gemm: A/B rows must be 16-byte aligned");
@@ -1261,7 +1322,8 @@ extern "C" int swarm_gemm_bf16(const swarm_gemm_args* a, swarm_stream_t stream) 
     if (p.tma_epi) {
         const bool f32 = esz == 4;
         rc = encode_2d_out(&td, a->d, d_rows, d_cols, a->ldd, f32);
-        if (rc == SWARM_OK && a->epilogue == SWARM_EPI_GELU) rc = encode_2d_out(&tu, a->aux, d_rows, d_cols, a->ldd, false);
+        if (rc == SWARM_OK && (a->epilogue == SWARM_EPI_GELU || a->epilogue == SWARM_EPI_GELU_DERIV))
+            rc = encode_2d_out(&tu, a->aux, d_rows, d_cols, a->ldd, false);
         if (rc != SWARM_OK) p.tma_epi = 0;  // fall back to direct stores
     }
     p.dp_tiles = p.total_tiles;

@@ -111,6 +111,11 @@ __global__ void __launch_bounds__(kThreads) k_gemm_f32(const swarm_gemm_args g) 
                     D[o] = gelu32(v);
                     break;
                 case SWARM_EPI_DGELU: D[o] = v * dgelu32(U[o]); break;
+                case SWARM_EPI_GELU_DERIV:
+                    U[o] = dgelu32(v);
+                    D[o] = gelu32(v);
+                    break;
+                case SWARM_EPI_MUL: D[o] = v * U[o]; break;
                 default: D[o] = v; break;  // STORE_BF16 (an fp32 activation here) / STORE_F32
             }
         }
@@ -126,8 +131,9 @@ extern "C" int swarm_gemm_f32(const swarm_gemm_args* a, swarm_stream_t stream) {
     if (!a) return invalid("gemm_f32: null args");
     if (a->m <= 0 || a->n <= 0 || a->k <= 0 || a->batch <= 0 || a->bh <= 0) return invalid("gemm_f32: bad shape");
     if (!a->a || !a->b || !a->d) return invalid("gemm_f32: null operand");
-    if (a->epilogue < 0 || a->epilogue > SWARM_EPI_DGELU) return invalid("gemm_f32: bad epilogue");
-    if ((a->epilogue == SWARM_EPI_RESIDUAL || a->epilogue == SWARM_EPI_GELU || a->epilogue == SWARM_EPI_DGELU) &&
+    if (a->epilogue < 0 || a->epilogue > SWARM_EPI_MUL) return invalid("gemm_f32: bad epilogue");
+    if ((a->epilogue == SWARM_EPI_RESIDUAL || a->epilogue == SWARM_EPI_GELU || a->epilogue == SWARM_EPI_DGELU ||
+         a->epilogue == SWARM_EPI_GELU_DERIV || a->epilogue == SWARM_EPI_MUL) &&
         !a->aux)
         return invalid("gemm_f32: epilogue needs aux");
     if ((a->a2 || a->b2) && (!a->a2 || !a->b2 || a->batch != 1 || a->k % 2))

@@ -278,3 +278,24 @@ def test_gemm_two_k_segments(cuda, m, n, t, a_t, b_t):
     ops.gemm_raw(g)
     ref = ref_mm(A, B, a_t, b_t) + 1
     torch.testing.assert_close(acc, ref, rtol=1e-4, atol=1e-4 * math.sqrt(k))
+
+
+@pytest.mark.parametrize("m,n,k", [(512, 1024, 256), (2048, 8192, 512), (200, 136, 64)])
+def test_gemm_gelu_deriv_and_mul_epilogues(cuda, m, n, k):
+    """The MLP's forward / backward epilogue pair: GELU_DERIV writes gelu(acc) and keeps
+    gelu'(acc) in U (one SFU tanh for both); MUL multiplies the backward product by U."""
+    import torch
+    from paper_2301_11913_b200 import _lib as L, ops
+    torch.manual_seed(1)
+    a = torch.randn(m, k, device="cuda").bfloat16() * 0.25
+    b = torch.randn(n, k, device="cuda").bfloat16() * 0.25
+    ref = a.float() @ b.float().t()
+    u = torch.empty(m, n, device="cuda", dtype=torch.bfloat16)
+    g = ops.gemm(a, b, epilogue=L.EPI_GELU_DERIV, aux=u)
+    x = ref.clone().requires_grad_()
+    y = torch.nn.functional.gelu(x, approximate="tanh")
+    y.backward(torch.ones_like(y))
+    torch.testing.assert_close(g.float(), y.detach(), rtol=1e-2, atol=2e-2)
+    torch.testing.assert_close(u.float(), x.grad, rtol=1e-2, atol=2e-2)
+    out = ops.gemm(a, b, epilogue=L.EPI_MUL, aux=u)
+    torch.testing.assert_close(out.float(), ref * u.float(), rtol=1e-2, atol=5e-2)
