@@ -433,6 +433,14 @@ int join_side(swarm_stage* s, cudaStream_t main) {
     return cudaStreamWaitEvent(main, s->ev_join, 0) == cudaSuccess ? SWARM_OK : SWARM_E_CUDA;
 }
 
+bool gelu_deriv() {
+    static const bool on = [] {
+        const char* e = getenv("SWARM_GELU_DERIV");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
+
 // ---------------------------------------------------------- block forward --
 int block_forward(swarm_stage* s, Act& A, EP y, const LayerW& W, cudaStream_t st) {
     const int T = s->T, d = s->d, H = s->H, dh = s->dh, F = s->F, L = s->L;
@@ -458,8 +466,10 @@ int block_forward(swarm_stage* s, Act& A, EP y, const LayerW& W, cudaStream_t st
     TRY(mm(T, d, d, {A.o, d, T, d, false}, {p16 + W.wo, d, d, d, false}, A.h, d, SWARM_EPI_RESIDUAL, A.x, 1.f, st));
     PTRY(SWARM_PROF_LAYERNORM, st, swarm_layer_norm_forward(A.h, s->dt, T, d, ln_param(s, W.ln2g), ln_param(s, W.ln2b), 1e-5, A.c, A.mu2, A.rs2, st));
     // u = c W1^T, g = gelu(u)
-    // g = gelu(c W1^T); u keeps gelu'(c W1^T) for the backward (one tanh for both)
-    TRY(mm(T, F, d, {A.c, d, T, d, false}, {p16 + W.w1, d, F, d, false}, A.g, F, SWARM_EPI_GELU_DERIV, A.u, 1.f, st));
+    // g = gelu(c W1^T); u keeps gelu'(c W1^T) for the backward (one tanh for both;
+    // SWARM_GELU_DERIV=0: u keeps the pre-activation and the backward recomputes gelu')
+    TRY(mm(T, F, d, {A.c, d, T, d, false}, {p16 + W.w1, d, F, d, false}, A.g, F,
+           gelu_deriv() ? SWARM_EPI_GELU_DERIV : SWARM_EPI_GELU, A.u, 1.f, st));
     // y = h + g W2^T
     TRY(mm(T, d, F, {A.g, F, T, F, false}, {p16 + W.w2, F, d, F, false}, y, d, SWARM_EPI_RESIDUAL, A.h, 1.f, st));
     return SWARM_OK;
@@ -522,7 +532,8 @@ int block_backward(swarm_stage* s, const Act& A, EP dy, EP dx, const LayerW& W, 
     TRY(fork_side(s, st, 0));
     TRY(wgrad(s, wp, d, F, {dy, d, T, d, true}, {A.g, F, T, F, true}, {pr ? ps->dy : nullptr, d, T, d, true},
               {pr ? PA->g : nullptr, F, T, F, true}, G + W.w2, F, sd));
-    TRY(mm(T, F, d, {dy, d, T, d, false}, {p16 + W.w2, F, d, F, true}, du, F, SWARM_EPI_MUL, A.u, 1.f, st));
+    TRY(mm(T, F, d, {dy, d, T, d, false}, {p16 + W.w2, F, d, F, true}, du, F,
+           gelu_deriv() ? SWARM_EPI_MUL : SWARM_EPI_DGELU, A.u, 1.f, st));
     TRY(fork_side(s, st, 1));
     TRY(wgrad(s, wp, F, d, {du, F, T, F, true}, {A.c, d, T, d, true}, {pr ? ps->du : nullptr, F, T, F, true},
               {pr ? PA->c : nullptr, d, T, d, true}, G + W.w1, d, sd));
