@@ -8,6 +8,7 @@
 //             (fp64 for the f64 API path).  Backward is the standard LN gradient with
 //             deterministic two-stage column reductions for dgain/dbias.
 #include <algorithm>
+#include <cstdlib>
 
 #include "common.cuh"
 
@@ -534,6 +535,7 @@ __global__ void __launch_bounds__(256) k_ln_bwd_dgb(const uint4* __restrict__ dy
     const int r0 = blockIdx.y * rows_per_split, r1 = min(rows, r0 + rows_per_split);
     float ag[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f}, ab[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
     if (c8 < cols8) {
+#pragma unroll 4
         for (int r = r0 + rl; r < r1; r += 32) {
             float xv[8], dv[8];
             unpack8(x[static_cast<size_t>(r) * cols8 + c8], xv);
@@ -668,7 +670,14 @@ int ln_bwd_launch(const T* dy, const T* x, int rows, int cols, const float* g, c
             })) {
             if (dx) SWARM_LAUNCH_CHECK("k_ln_bwd_dx_w");
             if (dg || db) {
-                const int splits = std::max(1, std::min(ln_bwd_parts(rows), (rows + 63) / 64));
+                // row splits of SWARM_LN_DGB_ROWS (128) rows: fatter CTAs than the 64-row split, whose
+                // per-CTA reduction + arrival counter cost dominated (ncu 12.3 us for 16 MB of reads);
+                // measured dx + dgain/dbias at 2048 x 2048: 13.6 (64) / 12.05 (128) / 12.9 (256) / 15.5 (512) us
+                static const int rows_per = [] {
+                    const char* e = getenv("SWARM_LN_DGB_ROWS");
+                    return e ? std::max(32, atoi(e)) : 128;
+                }();
+                const int splits = std::max(1, std::min(ln_bwd_parts(rows), (rows + rows_per - 1) / rows_per));
                 const int rps = (rows + splits - 1) / splits;
                 int* strips = reinterpret_cast<int*>(ws);  // fixed counter area, see swarm_layer_norm_backward_workspace
                 float* pg = ws + kLnCounterBytes / sizeof(float);
