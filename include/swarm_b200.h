@@ -214,6 +214,12 @@ int swarm_attn_softmax_backward_ex(const void* p, const float* dp, size_t rows, 
  * query block's causal extent ((i/128 + 1) * 128) are not written. */
 int swarm_attn_scores_softmax(const void* q, const void* k, int ld, int n_cols, int B, int H, int L, int d_head,
                               float scale, int causal, void* P, swarm_stream_t stream);
+/* The same probabilities P plus the attention output O = P V in one kernel (d_head 128): each key
+ * chunk's P is written over its K chunk in shared memory once the score MMA has read it, stored to
+ * P from there, and multiplied by the V chunk (tcgen05, O accumulated in TMEM); O[b*L + i, h*d_head
+ * .. +d_head] (row stride ld_o) in bf16.  v has q's storage geometry (ld, n_cols). */
+int swarm_attn_forward_pv(const void* q, const void* k, const void* v, int ld, int n_cols, int B, int H, int L,
+                          int d_head, float scale, int causal, void* P, void* O, int ld_o, swarm_stream_t stream);
 /* dS = scale * P * (dP - rowsum(P * dP)) with dP = dO_z V_z^T computed in TMEM (bf16 out); the
  * row statistic is taken as dO . O (O = P V, the forward's attention output, [B*L, ld_o] with
  * head h at column h*d_head), which equals rowsum(P * dP) and saves a second pass.

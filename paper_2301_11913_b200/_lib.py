@@ -105,6 +105,7 @@ SIGNATURES = {
     "swarm_attn_softmax_forward_ex": (I, [P, SZ, SZ, I, P, I, P]),
     "swarm_attn_softmax_backward_ex": (I, [P, P, SZ, SZ, F, P, I, P]),
     "swarm_attn_scores_softmax": (I, [P, P, I, I, I, I, I, I, F, I, P, P]),
+    "swarm_attn_forward_pv": (I, [P, P, P, I, I, I, I, I, I, F, I, P, P, I, P]),
     "swarm_attn_scores_softmax_backward": (I, [P, I, P, I, I, P, I, P, I, I, I, I, F, I, P, P]),
     "swarm_adamw_step": (I, [P, P, P, P, P, SZ, F, F, F, F, F, I, F, I, P]),
     "swarm_fill_normal": (I, [P, SZ, F, F, C.c_uint64, P]),

@@ -55,12 +55,16 @@ constexpr int kChunkBytes = (kMaxDh / 64) * BKV * 128;  // 16 KB: K / V chunk
 constexpr int kPChunkBytes = BQ * BKV * 2;              // 16 KB: P chunk (backward), dS written in place
 // forward: 3-stage K ring + 4 row warps x 2 staging slots; backward: 2-stage
 // (V chunk, P chunk) ring, dS staged in place of the P chunk it replaces
-template <bool BWD>
+// PV (forward with O = P V fused, d_head = 128): 2-stage (K chunk, V chunk) ring; each chunk's P is
+// written over its stage's K chunk once the score MMA has read it, stored from there, and read
+// there by the P V MMA (A operand); the O accumulator takes TMEM columns 128-255
+template <bool BWD, bool PV = false>
 struct Lay {
-    static constexpr int kStages = BWD ? 2 : 3;
-    static constexpr int kStageBytes = kChunkBytes + (BWD ? kPChunkBytes : 0);
-    static constexpr int kStgBytes = BWD ? 0 : 4 * 2 * kSlot;
+    static constexpr int kStages = BWD || PV ? 2 : 3;
+    static constexpr int kStageBytes = kChunkBytes + (BWD ? kPChunkBytes : (PV ? kChunkBytes : 0));
+    static constexpr int kStgBytes = BWD || PV ? 0 : 4 * 2 * kSlot;
     static constexpr int kSmem = kABytes + kStages * kStageBytes + kStgBytes + 1024 + 256;
+    static constexpr int kTmemCols = PV ? 4 * BKV : 2 * BKV;
     static_assert(2 * (kSmem + 1024) <= 233472, "two attention CTAs must fit one SM");
 };
 
@@ -143,11 +147,12 @@ __device__ __forceinline__ void trace(const Params& p, int slot) {
     if (p.trace && blockIdx.x < kTraceCtas) g_attn_trace[blockIdx.x][slot] = gtimer();
 }
 
-template <bool BWD>
+template <bool BWD, bool PV = false>
 __global__ void __launch_bounds__(kThreads, 2)
     k_attn_chunks(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUtensorMap tma_b,
                   const __grid_constant__ CUtensorMap tma_p, const __grid_constant__ CUtensorMap tma_out,
                   const Params p) {
+    // PV: tma_p maps V (the forward reads no P), O goes to p.o_out
     // forward: pass 0 row max / sum, pass 1 probabilities; backward: one pass, the
     // row statistic rowsum(P * dP) = dO . O comes from the forward output
     constexpr int kPasses = BWD ? 1 : 2;
@@ -163,7 +168,7 @@ __global__ void __launch_bounds__(kThreads, 2)
     extern __shared__ uint8_t smem_raw[];
     const uint32_t raw = smem_u32(smem_raw);
     uint8_t* smem = smem_raw + ((1024 - (raw & 1023)) & 1023);
-    using Y = Lay<BWD>;
+    using Y = Lay<BWD, PV>;
     constexpr int kStages = Y::kStages;
     uint8_t* sa = smem;
     uint8_t* sb = sa + kABytes;  // stage s: K / V chunk, then (backward) the P chunk
@@ -174,7 +179,9 @@ __global__ void __launch_bounds__(kThreads, 2)
     uint64_t* empty = full + kStages;
     uint64_t* sfull = empty + kStages;
     uint64_t* sempty = sfull + 2;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sempty + 2);
+    uint64_t* pfull = sempty + 2;  // PV: the 4 row warps wrote a chunk's P (over its K chunk)
+    uint64_t* ofull = pfull + 1;   // PV: the last P V MMA committed
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(ofull + 1);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int nqb = p.L / BQ, nz = p.B * p.H;
@@ -189,16 +196,20 @@ __global__ void __launch_bounds__(kThreads, 2)
         mbar_init(qfull, 1);
         for (int s = 0; s < kStages; ++s) {
             mbar_init(&full[s], 1);
-            mbar_init(&empty[s], BWD ? 5 : 1);  // bwd: the MMA and the 4 row warps (P read, dS stored)
+            // bwd: the MMA and the 4 row warps (P read, dS stored); PV: the MMA (scores, or P V) and
+            // the 4 row warps (S read in pass 0, P stored from the stage in pass 1)
+            mbar_init(&empty[s], BWD || PV ? 5 : 1);
         }
         for (int b = 0; b < 2; ++b) {
             mbar_init(&sfull[b], 1);
             mbar_init(&sempty[b], 4);
         }
+        mbar_init(pfull, 4);
+        mbar_init(ofull, 1);
         fence_barrier_init();
     }
     if (warp == 2) {
-        tmem_alloc(tmem_slot, 2 * BKV);
+        tmem_alloc(tmem_slot, Y::kTmemCols);
         tmem_relinquish();
     }
     tc_fence_before();
@@ -219,9 +230,14 @@ __global__ void __launch_bounds__(kThreads, 2)
             for (int j = 0; j < nch; ++j) {
                 mbar_wait(&empty[stage], phase ^ 1);
                 uint8_t* sst = sb + stage * Y::kStageBytes;
-                mbar_arrive_expect_tx(&full[stage], kboxes * BKV * 128 + (BWD ? kPChunkBytes : 0));
+                const bool load_v = PV && pass == 1;
+                mbar_arrive_expect_tx(&full[stage], kboxes * BKV * 128 * (load_v ? 2 : 1) + (BWD ? kPChunkBytes : 0));
                 for (int kb = 0; kb < kboxes; ++kb)
                     tma_load_2d(sst + kb * BKV * 128, &tma_b, &full[stage], bcol + kb * 64, brow + j * BKV);
+                if (load_v)  // V chunk (MN-major B of the P V MMA): [64 keys x 64 d_head] boxes after the K chunk
+                    for (int kb = 0; kb < kboxes; ++kb)
+                        tma_load_2d(sst + kChunkBytes + kb * BKV * 128, &tma_p, &full[stage], bcol + kb * 64,
+                                    brow + j * BKV);
                 if constexpr (BWD)  // P[z, mt*128 .. +128, j*64 .. +64]
                     tma_load_2d(sst + kChunkBytes, &tma_p, &full[stage], j * BKV, z * p.L + mt * BQ);
                 if (++stage == kStages) {
@@ -236,6 +252,23 @@ __global__ void __launch_bounds__(kThreads, 2)
         int stage = 0, buf = 0;
         uint32_t phase = 0, bphase = 0;
         const int ksteps = p.dh / 16;
+        // PV: O += P_j V_j (M 128, N d_head, K 64 keys): A = P_j over the K chunk, B = V_j MN-major
+        constexpr uint32_t idesc_pv = make_idesc_bf16(BQ, kMaxDh, false, true);
+        uint32_t pphase = 0;
+        auto issue_pv = [&](int st_pv, int jj) {
+            mbar_wait(pfull, pphase);
+            pphase ^= 1;
+            tc_fence_after();
+            const uint32_t p_base = smem_u32(sb + st_pv * Y::kStageBytes);
+            const uint32_t v_base = p_base + kChunkBytes;
+            for (int kk = 0; kk < BKV / 16; ++kk) {
+                const uint64_t ad = make_sdesc(p_base + kk * 32, 16, 1024);
+                const uint64_t bd = make_sdesc(v_base + kk * 2048, BKV * 128, 1024);
+                mma_bf16(tmem + 2 * BKV, ad, bd, idesc_pv, (jj != 0 || kk != 0) ? 1u : 0u);
+            }
+            mma_commit(&empty[st_pv]);
+        };
+        int prev_stage = -1;
         for (int pass = 0; pass < kPasses; ++pass)
             for (int j = 0; j < nch; ++j) {
                 mbar_wait(&full[stage], phase);
@@ -247,8 +280,13 @@ __global__ void __launch_bounds__(kThreads, 2)
                     const uint64_t bd = make_sdesc(b_base + (kk >> 2) * (BKV * 128) + (kk & 3) * 32, 16, 1024);
                     mma_bf16(tmem + buf * BKV, ad, bd, idesc, kk != 0 ? 1u : 0u);
                 }
-                mma_commit(&empty[stage]);
+                const bool pv_pass = PV && pass == kPasses - 1;
+                if (!pv_pass) mma_commit(&empty[stage]);  // (PV pass: the stage is released after P V)
                 mma_commit(&sfull[buf]);
+                if (pv_pass) {  // the previous chunk's P V overlaps this chunk's softmax
+                    if (j > 0) issue_pv(prev_stage, j - 1);
+                    prev_stage = stage;
+                }
                 if (++stage == kStages) {
                     stage = 0;
                     phase ^= 1;
@@ -258,6 +296,10 @@ __global__ void __launch_bounds__(kThreads, 2)
                     bphase ^= 1;
                 }
             }
+        if constexpr (PV) {
+            issue_pv(prev_stage, nch - 1);
+            mma_commit(ofull);
+        }
     } else if (warp >= 4) {
         // ------------------------------------------------------------ one query row per thread
         const int q = warp - 4;
@@ -274,6 +316,8 @@ __global__ void __launch_bounds__(kThreads, 2)
         const float cs = p.scale * 1.4426950408889634f;
         if (r == 0) trace(p, 1);
         float bias = 0.f;  // fwd pass 1: max(u) + log2(sum), so p = 2^(u - bias); bwd: dO . O
+        int stage = 0;
+        uint32_t sphase = 0;
         if constexpr (!BWD) {
             // ---------------- pass 0: online row max / sum
             float mu = -INFINITY, l = 0.f;
@@ -286,7 +330,14 @@ __global__ void __launch_bounds__(kThreads, 2)
                 tmem_ld_wait();
                 tc_fence_before();
                 __syncwarp();
-                if (lane == 0) mbar_arrive(&sempty[buf]);
+                if (lane == 0) {
+                    mbar_arrive(&sempty[buf]);
+                    if (PV) mbar_arrive(&empty[stage]);  // (PV: a stage is freed by the MMA and the 4 row warps)
+                }
+                if (++stage == kStages) {
+                    stage = 0;
+                    sphase ^= 1;
+                }
                 if (++buf == 2) {
                     buf = 0;
                     bphase ^= 1;
@@ -350,8 +401,6 @@ __global__ void __launch_bounds__(kThreads, 2)
         }
         if (r == 0) trace(p, 2);
         // ---------------- probabilities (fwd pass 1) / score gradients (bwd)
-        int stage = 0;
-        uint32_t sphase = 0;
         for (int j = 0; j < nch; ++j) {
             const int c0 = j * BKV;
             uint32_t ra[32], rb[32];
@@ -377,6 +426,32 @@ __global__ void __launch_bounds__(kThreads, 2)
                         v[jj] = (c0 + jj < valid) ? fast_exp2(fmaf(__uint_as_float(ra[jj]), cs, -bias)) : 0.f;
                         v[32 + jj] = (c0 + 32 + jj < valid) ? fast_exp2(fmaf(__uint_as_float(rb[jj]), cs, -bias)) : 0.f;
                     }
+                }
+                if constexpr (PV) {
+                    // P_j over this stage's K chunk (the score MMA has read it: sfull), in the
+                    // SWIZZLE_128B K-major layout the P V MMA reads as its A operand (128-B rows, 16-B
+                    // piece k of row r at k ^ (r & 7)); stored to global from there too
+                    uint8_t* pt = sb + stage * Y::kStageBytes;
+                    const uint32_t prow = smem_u32(pt) + r * 128;
+#pragma unroll
+                    for (int k = 0; k < 8; ++k)
+                        st_shared_v4(prow + ((k ^ (r & 7)) << 4), pack_bf16(v[8 * k], v[8 * k + 1]),
+                                     pack_bf16(v[8 * k + 2], v[8 * k + 3]), pack_bf16(v[8 * k + 4], v[8 * k + 5]),
+                                     pack_bf16(v[8 * k + 6], v[8 * k + 7]));
+                    fence_async_smem();
+                    __syncwarp();
+                    if (lane == 0) {
+                        tma_store_2d(&tma_out, pt + q * 32 * 128, c0, out_row);
+                        bulk_commit();
+                        mbar_arrive(pfull);
+                        bulk_wait_read<0>();  // the box has left smem: the stage may be refilled
+                        mbar_arrive(&empty[stage]);
+                    }
+                    if (++stage == kStages) {
+                        stage = 0;
+                        sphase ^= 1;
+                    }
+                    continue;
                 }
 #pragma unroll
                 for (int h = 0; h < 2; ++h) {
@@ -431,6 +506,27 @@ __global__ void __launch_bounds__(kThreads, 2)
                 }
             }
         }
+        if constexpr (PV) {
+            // O row (d_head = 128 fp32 accumulators, TMEM columns 128-255) -> bf16 at O[b*L + qi, h*dh]
+            mbar_wait(ofull, 0);
+            tc_fence_after();
+            __nv_bfloat16* orow = const_cast<__nv_bfloat16*>(p.o) + (static_cast<size_t>(zb) * p.L + qi) * p.ld_o +
+                                  zh * p.dh;
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+                uint32_t ro[32];
+                tmem_ld_32x32b_x32(trow + 2 * BKV + 32 * c, ro);
+                tmem_ld_wait();
+                uint4* dst = reinterpret_cast<uint4*>(orow + 32 * c);
+#pragma unroll
+                for (int w = 0; w < 4; ++w)
+                    dst[w] = make_uint4(pack_bf16(__uint_as_float(ro[8 * w]), __uint_as_float(ro[8 * w + 1])),
+                                        pack_bf16(__uint_as_float(ro[8 * w + 2]), __uint_as_float(ro[8 * w + 3])),
+                                        pack_bf16(__uint_as_float(ro[8 * w + 4]), __uint_as_float(ro[8 * w + 5])),
+                                        pack_bf16(__uint_as_float(ro[8 * w + 6]), __uint_as_float(ro[8 * w + 7])));
+            }
+            tc_fence_before();
+        }
         // keys past the causal block are never written (nothing on the hot path
         // reads them; the stage executor zeroes P / dS once at creation)
         if (lane == 0) bulk_wait_all();
@@ -441,7 +537,7 @@ __global__ void __launch_bounds__(kThreads, 2)
     __syncthreads();
     if (warp == 2) {
         tc_fence_after();
-        tmem_dealloc(tmem, 2 * BKV);
+        tmem_dealloc(tmem, Y::kTmemCols);
     }
     if (threadIdx.x == 128) trace(p, 4);
 }
@@ -525,10 +621,11 @@ bool trace_enabled() {
     return on;
 }
 
-template <bool BWD>
+template <bool BWD, bool PV = false>
 int launch(const void* a, int lda, int a_cols, int a_col0, const void* b, int ldb, int b_cols, int b_col0,
            const void* pin, const void* o, int ld_o, void* out, int B, int H, int L, int dh, float scale, int causal,
            cudaStream_t st) {
+    // PV: pin = V (same storage geometry as K), o = the O output [B*L, ld_o]
     if (L % BQ || L > kMaxL || dh % 64 || dh > kMaxDh || B <= 0 || H <= 0)
         return invalid("attention: need L % 128 == 0, L <= 1024, dh % 64 == 0, dh <= 128");
     if (BWD && (!pin || (reinterpret_cast<uintptr_t>(pin) & 15)))
@@ -540,15 +637,19 @@ int launch(const void* a, int lda, int a_cols, int a_col0, const void* b, int ld
     CUtensorMap ta, tb, tp{}, to;
     // forward P: 32 x 32 boxes (SWIZZLE_64B staging); backward dS: 32 rows x 64 keys, in place of
     // the P chunk loaded with 128 x 64 boxes (SWIZZLE_128B)
+    if (PV && (dh != kMaxDh || !pin || !o || (reinterpret_cast<uintptr_t>(o) & 15) || ld_o % 8))
+        return invalid("attention P V: needs d_head 128, V, and a 16-byte aligned O");
     if (map_bf16(&ta, a, T, a_cols, lda, 64, BQ, CU_TENSOR_MAP_SWIZZLE_128B) ||
         map_bf16(&tb, b, T, b_cols, ldb, 64, BKV, CU_TENSOR_MAP_SWIZZLE_128B) ||
-        (BWD ? map_bf16(&to, out, rows_out, L, L, 64, 32, CU_TENSOR_MAP_SWIZZLE_128B)
-             : map_bf16(&to, out, rows_out, L, L, 32, 32, CU_TENSOR_MAP_SWIZZLE_64B)))
+        (BWD || PV ? map_bf16(&to, out, rows_out, L, L, 64, 32, CU_TENSOR_MAP_SWIZZLE_128B)
+                   : map_bf16(&to, out, rows_out, L, L, 32, 32, CU_TENSOR_MAP_SWIZZLE_64B)))
         return invalid("attention: tensor map encoding failed");
     if (BWD && map_bf16(&tp, pin, rows_out, L, L, 64, BQ, CU_TENSOR_MAP_SWIZZLE_128B))
         return invalid("attention: tensor map encoding failed (P)");
-    auto kern = k_attn_chunks<BWD>;
-    constexpr int kSmem = Lay<BWD>::kSmem;
+    if (PV && map_bf16(&tp, pin, T, b_cols, ldb, 64, BKV, CU_TENSOR_MAP_SWIZZLE_128B))
+        return invalid("attention: tensor map encoding failed (V)");
+    auto kern = k_attn_chunks<BWD, PV>;
+    constexpr int kSmem = Lay<BWD, PV>::kSmem;
     static bool attr = false;
     if (!attr) {
         SWARM_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem));
@@ -574,6 +675,12 @@ int swarm_attn_scores_softmax(const void* q, const void* k, int ld, int n_cols, 
                               float scale, int causal, void* P, swarm_stream_t stream) {
     return swarm::attn::launch<false>(q, ld, n_cols, 0, k, ld, n_cols, 0, nullptr, nullptr, 0, P, B, H, L, dh, scale,
                                       causal, swarm::as_stream(stream));
+}
+
+int swarm_attn_forward_pv(const void* q, const void* k, const void* v, int ld, int n_cols, int B, int H, int L,
+                          int dh, float scale, int causal, void* P, void* O, int ld_o, swarm_stream_t stream) {
+    return swarm::attn::launch<false, true>(q, ld, n_cols, 0, k, ld, n_cols, 0, v, O, ld_o, P, B, H, L, dh, scale,
+                                            causal, swarm::as_stream(stream));
 }
 
 int swarm_attn_scores_softmax_backward(const void* dO, int ld_do, const void* v, int ld_v, int v_cols, const void* o,

@@ -433,6 +433,15 @@ int join_side(swarm_stage* s, cudaStream_t main) {
     return cudaStreamWaitEvent(main, s->ev_join, 0) == cudaSuccess ? SWARM_OK : SWARM_E_CUDA;
 }
 
+// the forward's P V inside the attention kernel (d_head 128; SWARM_ATTN_PV=0 keeps the separate GEMM)
+bool attn_pv(const swarm_stage* s) {
+    static const bool on = [] {
+        const char* e = getenv("SWARM_ATTN_PV");
+        return !(e && e[0] == '0');
+    }();
+    return on && s->dh == 128;
+}
+
 bool gelu_deriv() {
     static const bool on = [] {
         const char* e = getenv("SWARM_GELU_DERIV");
@@ -449,7 +458,11 @@ int block_forward(swarm_stage* s, Act& A, EP y, const LayerW& W, cudaStream_t st
     TRY(mm(T, 3 * d, d, {A.a, d, T, d, false}, {p16 + W.wqkv, d, 3 * d, d, false}, A.qkv, 3 * d,
            SWARM_EPI_STORE_BF16, nullptr, 1.f, st));
     const float scale = 1.f / std::sqrt(static_cast<float>(dh));
-    if (s->fused_attn) {
+    if (s->fused_attn && attn_pv(s)) {
+        // P = softmax(scale * Q K^T) and O = P V in one kernel (scores and O in TMEM)
+        PTRY(SWARM_PROF_ATTENTION, st, swarm_attn_forward_pv(A.qkv, A.qkv + d, A.qkv + 2 * d, 3 * d, d, s->B, H, L, dh,
+                                                             scale, s->cfg.causal, A.P, A.o, d, st));
+    } else if (s->fused_attn) {
         // P = softmax(scale * Q K^T) per (b, h), scores kept in TMEM
         PTRY(SWARM_PROF_ATTENTION, st, swarm_attn_scores_softmax(A.qkv, A.qkv + d, 3 * d, d, s->B, H, L, dh, scale, s->cfg.causal, A.P, st));
     } else {
@@ -459,9 +472,11 @@ int block_forward(swarm_stage* s, Act& A, EP y, const LayerW& W, cudaStream_t st
                 st));
         PTRY(SWARM_PROF_ATTENTION, st, swarm_attn_softmax_forward_ex(s->S, static_cast<size_t>(s->B) * H * L, L, s->cfg.causal, A.P, s->dt, st));
     }
-    // O = P V  (V read MN-major straight from the qkv buffer)
-    TRY(bmm(s, L, dh, L, {{A.P, L, s->B * H * L, L, false}, H * L, L, 0, 0},
-            {{A.qkv + 2 * d, 3 * d, T, d, true}, L, 0, 0, dh}, A.o, d, L, 0, 0, dh, SWARM_EPI_STORE_BF16, 1.f, st, 1));
+    // O = P V  (V read MN-major straight from the qkv buffer), unless the attention kernel did it
+    if (!(s->fused_attn && attn_pv(s)))
+        TRY(bmm(s, L, dh, L, {{A.P, L, s->B * H * L, L, false}, H * L, L, 0, 0},
+                {{A.qkv + 2 * d, 3 * d, T, d, true}, L, 0, 0, dh}, A.o, d, L, 0, 0, dh, SWARM_EPI_STORE_BF16, 1.f, st,
+                1));
     // h = x + O Wo^T
     TRY(mm(T, d, d, {A.o, d, T, d, false}, {p16 + W.wo, d, d, d, false}, A.h, d, SWARM_EPI_RESIDUAL, A.x, 1.f, st));
     PTRY(SWARM_PROF_LAYERNORM, st, swarm_layer_norm_forward(A.h, s->dt, T, d, ln_param(s, W.ln2g), ln_param(s, W.ln2b), 1e-5, A.c, A.mu2, A.rs2, st));

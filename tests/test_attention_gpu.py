@@ -83,3 +83,34 @@ def test_fused_matches_unfused_path(cuda):
     P2 = torch.empty_like(P1)
     _lib.lib().swarm_attn_softmax_forward(C.c_void_p(S.data_ptr()), B * H * L, L, 1, C.c_void_p(P2.data_ptr()), st)
     torch.testing.assert_close(P1.float(), P2.float(), rtol=0, atol=4e-3)
+
+
+@pytest.mark.parametrize("B,H,L,dh,causal", [(2, 4, 512, 128, 1), (2, 4, 512, 128, 0), (1, 3, 256, 128, 1),
+                                             (4, 16, 512, 128, 1), (1, 2, 1024, 128, 1)])
+def test_fused_attention_forward_pv(cuda, B, H, L, dh, causal):
+    """swarm_attn_forward_pv: the same P as swarm_attn_scores_softmax (bit for bit) and O = P V
+    (P rounded to bf16, fp32 accumulation) within bf16 output rounding."""
+    import torch
+    from paper_2301_11913_b200 import _lib
+    torch.manual_seed(3 * L + dh + causal)
+    d = H * dh
+    qkv = (torch.randn(B * L, 3 * d, device="cuda") * 2).bfloat16()
+    P0 = torch.zeros(B * H * L, L, device="cuda", dtype=torch.bfloat16)
+    P1 = torch.zeros_like(P0)
+    O = torch.zeros(B * L, d, device="cuda", dtype=torch.bfloat16)
+    scale = 1 / math.sqrt(dh)
+    st = torch.cuda.current_stream().cuda_stream
+    L_ = _lib.lib()
+    ptr = lambda t: C.c_void_p(t.data_ptr())  # noqa: E731
+    assert L_.swarm_attn_scores_softmax(ptr(qkv), ptr(qkv[:, d:]), 3 * d, d, B, H, L, dh, scale, causal, ptr(P0), st) == 0
+    rc = L_.swarm_attn_forward_pv(ptr(qkv), ptr(qkv[:, d:]), ptr(qkv[:, 2 * d:]), 3 * d, d, B, H, L, dh, scale, causal,
+                                  ptr(P1), ptr(O), d, st)
+    assert rc == 0, _lib.last_error()
+    torch.cuda.synchronize()
+    assert torch.equal(P0, P1)
+    v = qkv[:, 2 * d:].float().view(B, L, H, dh).transpose(1, 2)
+    ref = (P1.float().view(B, H, L, L) @ v).transpose(1, 2).reshape(B * L, d)
+    torch.testing.assert_close(O.float(), ref, rtol=1e-2, atol=1e-2 * float(ref.abs().max()))
+    # and both match the fp32 reference attention within the bf16 P rounding
+    full = (ref_P(qkv, B, H, L, dh, causal).view(B, H, L, L) @ v).transpose(1, 2).reshape(B * L, d)
+    assert float((O.float() - full).norm() / full.norm()) < 1e-2
