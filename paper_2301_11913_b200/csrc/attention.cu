@@ -179,8 +179,11 @@ __global__ void __launch_bounds__(kThreads, 2)
     uint64_t* empty = full + kStages;
     uint64_t* sfull = empty + kStages;
     uint64_t* sempty = sfull + 2;
-    uint64_t* pfull = sempty + 2;  // PV: the 4 row warps wrote a chunk's P (over its K chunk)
-    uint64_t* ofull = pfull + 1;   // PV: the last P V MMA committed
+    // PV: per stage, the 4 row warps wrote that stage's chunk P (over its K chunk).  One barrier per
+    // stage, not one overall: the row warps may finish two chunks' P before the MMA thread polls, and a
+    // single barrier would then have moved two phases past the waiter's parity
+    uint64_t* pfull = sempty + 2;
+    uint64_t* ofull = pfull + 2;  // PV: the last P V MMA committed
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(ofull + 1);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -204,7 +207,8 @@ __global__ void __launch_bounds__(kThreads, 2)
             mbar_init(&sfull[b], 1);
             mbar_init(&sempty[b], 4);
         }
-        mbar_init(pfull, 4);
+        mbar_init(&pfull[0], 4);
+        mbar_init(&pfull[1], 4);
         mbar_init(ofull, 1);
         fence_barrier_init();
     }
@@ -254,10 +258,10 @@ __global__ void __launch_bounds__(kThreads, 2)
         const int ksteps = p.dh / 16;
         // PV: O += P_j V_j (M 128, N d_head, K 64 keys): A = P_j over the K chunk, B = V_j MN-major
         constexpr uint32_t idesc_pv = make_idesc_bf16(BQ, kMaxDh, false, true);
-        uint32_t pphase = 0;
+        uint32_t pphase[2] = {0, 0};
         auto issue_pv = [&](int st_pv, int jj) {
-            mbar_wait(pfull, pphase);
-            pphase ^= 1;
+            mbar_wait(&pfull[st_pv], pphase[st_pv]);
+            pphase[st_pv] ^= 1;
             tc_fence_after();
             const uint32_t p_base = smem_u32(sb + st_pv * Y::kStageBytes);
             const uint32_t v_base = p_base + kChunkBytes;
@@ -443,7 +447,7 @@ __global__ void __launch_bounds__(kThreads, 2)
                     if (lane == 0) {
                         tma_store_2d(&tma_out, pt + q * 32 * 128, c0, out_row);
                         bulk_commit();
-                        mbar_arrive(pfull);
+                        mbar_arrive(&pfull[stage]);
                         bulk_wait_read<0>();  // the box has left smem: the stage may be refilled
                         mbar_arrive(&empty[stage]);
                     }
