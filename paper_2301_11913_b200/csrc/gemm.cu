@@ -63,11 +63,14 @@ struct Params {
                   // 8 stream-K units store directly (no fixup), 16 fixup without waiting for partials
 };
 
-template <int BN>
+// MINB = 2: a short-K variant with two CTAs per SM (2 stages), for many small tiles (the batched
+// attention GEMMs: 256 tiles of 128 x 128 x <= 512): one CTA's prologue / epilogue overlaps the
+// other's MMAs instead of each tile paying its pipeline fill alone
+template <int BN, int MINB = 1>
 struct Cfg {
     static constexpr int A_BYTES = BM * BK * 2;
     static constexpr int B_BYTES = BN * BK * 2;
-    static constexpr int STAGES = BN == 256 ? 4 : 6;
+    static constexpr int STAGES = MINB == 2 ? 2 : (BN == 256 ? 4 : 6);
     static constexpr int TMEM_COLS = 2 * BN;
     static constexpr int SMEM = STAGES * (A_BYTES + B_BYTES) + kEpiSmem + 1024 + 256;
     static_assert(SMEM <= 232448, "GEMM exceeds the 227 KB dynamic smem limit");
@@ -405,11 +408,11 @@ __device__ __forceinline__ void k_range(const Params& p, int mt, int& kb0, int& 
     else if (p.k_tri == 2) kb0 = (mt * BM) / BK;
 }
 
-template <int BN, bool A_MN, bool B_MN>
-__global__ void __launch_bounds__(kThreads, 1)
+template <int BN, bool A_MN, bool B_MN, int MINB = 1>
+__global__ void __launch_bounds__(kThreads, MINB)
     k_gemm(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUtensorMap tma_b,
            const __grid_constant__ CUtensorMap tma_d, const __grid_constant__ CUtensorMap tma_u, const Params p) {
-    using C = Cfg<BN>;
+    using C = Cfg<BN, MINB>;
     pdl_trigger();
     extern __shared__ uint8_t smem_raw[];
     const uint32_t raw = smem_u32(smem_raw);
@@ -1034,17 +1037,17 @@ int num_sms() {
     return n;
 }
 
-template <int BN, bool A_MN, bool B_MN>
+template <int BN, bool A_MN, bool B_MN, int MINB = 1>
 int launch(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& td, const CUtensorMap& tu, const Params& p,
            cudaStream_t st) {
-    auto kern = k_gemm<BN, A_MN, B_MN>;
+    auto kern = k_gemm<BN, A_MN, B_MN, MINB>;
     static bool attr = false;
     if (!attr) {
-        SWARM_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg<BN>::SMEM));
+        SWARM_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg<BN, MINB>::SMEM));
         attr = true;
     }
-    const int grid = std::min(p.total_tiles, num_sms());
-    SWARM_CUDA_TRY(launch_pdl(kern, dim3(grid), dim3(kThreads), Cfg<BN>::SMEM, st, ta, tb, td, tu, p));
+    const int grid = std::min(p.total_tiles, num_sms() * MINB);
+    SWARM_CUDA_TRY(launch_pdl(kern, dim3(grid), dim3(kThreads), Cfg<BN, MINB>::SMEM, st, ta, tb, td, tu, p));
     SWARM_LAUNCH_CHECK("k_gemm");
     return SWARM_OK;
 }
@@ -1150,6 +1153,18 @@ bool pair_enabled() {
 template <int BN>
 int dispatch(bool amn, bool bmn, const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& td,
              const CUtensorMap& tu, const Params& p, cudaStream_t st) {
+    if constexpr (BN == 128) {
+        static const bool two = [] {
+            const char* e = getenv("SWARM_GEMM_TWO_CTA");
+            return !(e && e[0] == '0');
+        }();
+        if (two && p.k_blocks <= 16 && p.total_tiles > num_sms()) {  // many short tiles
+            if (!amn && !bmn) return launch<BN, false, false, 2>(ta, tb, td, tu, p, st);
+            if (!amn && bmn) return launch<BN, false, true, 2>(ta, tb, td, tu, p, st);
+            if (amn && !bmn) return launch<BN, true, false, 2>(ta, tb, td, tu, p, st);
+            return launch<BN, true, true, 2>(ta, tb, td, tu, p, st);
+        }
+    }
     if (!amn && !bmn) return launch<BN, false, false>(ta, tb, td, tu, p, st);
     if (!amn && bmn) return launch<BN, false, true>(ta, tb, td, tu, p, st);
     if (amn && !bmn) return launch<BN, true, false>(ta, tb, td, tu, p, st);
