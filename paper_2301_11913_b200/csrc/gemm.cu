@@ -59,6 +59,7 @@ struct Params {
     int* sk_ready;  // [cluster][first|last][half][warp] partial-ready flags (self-resetting)
     int k_tri;    // swarm_gemm_args.k_tri (1-CTA kernel): skip all-zero k-blocks of a triangular A
     int kb_half;  // two-segment K (pair kernel): k-blocks >= kb_half come from tma_a2 / tma_b2 (0 = one segment)
+    int aux_prefetch;  // epilogue: request R / U before the TMEM drain (SWARM_GEMM_AUX_PREFETCH=0: after)
     int dbg;      // SWARM_GEMM_DBG (experiments only): 1 skip output stores, 2 skip MMAs, 4 skip TMA loads,
                   // 8 stream-K units store directly (no fixup), 16 fixup without waiting for partials
 };
@@ -284,13 +285,34 @@ __device__ __forceinline__ void drain_tile(const Params& p, const CUtensorMap* m
                                            long long cd, int col_tile0, int lane, uint64_t fix_slots = 0,
                                            int nfix = 0, size_t fix_row = 0) {
     const int row = row_base + lane;
+    // epilogues that read a bf16 operand (R, U): this chunk's 64 B of it are requested before the
+    // TMEM load, and the next chunk's are pulled into L2, so the global latency overlaps the
+    // accumulator drain instead of serialising once per 32-column chunk
+    const bool reads_aux = p.tma_epi && p.aux &&
+                           (p.epi == SWARM_EPI_RESIDUAL || p.epi == SWARM_EPI_DGELU || p.epi == SWARM_EPI_MUL);
+    const bool pre = reads_aux && p.aux_prefetch;
 #pragma unroll 1
     for (int c = 0; c < BN_TILE / 32; ++c) {
+        const int col0 = col_tile0 + c * 32;
+        uint4 a4[4];
+        if (pre && row < p.m && col0 < p.n) {
+            const uint4* src =
+                reinterpret_cast<const uint4*>(static_cast<const __nv_bfloat16*>(p.aux) + (rd + row) * p.ldd + cd + col0);
+#pragma unroll
+            for (int q = 0; q < 4; ++q) a4[q] = src[q];
+            if (c + 1 < BN_TILE / 32 && col0 + 32 < p.n)
+                asm volatile("prefetch.global.L2 [%0];" ::"l"(src + 4));
+        }
         uint32_t rr[32];
         tmem_ld_32x32b_x32(taddr + static_cast<uint32_t>(c * 32), rr);
         tmem_ld_wait();
-        const int col0 = col_tile0 + c * 32;
         if (col0 >= p.n) continue;  // warp-uniform
+        if (reads_aux && !pre && row < p.m) {  // SWARM_GEMM_AUX_PREFETCH=0: load after the drain
+            const uint4* src =
+                reinterpret_cast<const uint4*>(static_cast<const __nv_bfloat16*>(p.aux) + (rd + row) * p.ldd + cd + col0);
+#pragma unroll
+            for (int q = 0; q < 4; ++q) a4[q] = src[q];
+        }
         float v[32];
 #pragma unroll
         for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(rr[j]);
@@ -325,10 +347,9 @@ __device__ __forceinline__ void drain_tile(const Params& p, const CUtensorMap* m
                 break;
             case SWARM_EPI_RESIDUAL:
                 if (row_ok) {
-                    const uint4* r4 = reinterpret_cast<const uint4*>(static_cast<const __nv_bfloat16*>(p.aux) + off);
 #pragma unroll
                     for (int q = 0; q < 4; ++q) {
-                        const uint4 w = r4[q];
+                        const uint4 w = a4[q];
                         const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
 #pragma unroll
                         for (int j = 0; j < 4; ++j) {
@@ -347,10 +368,9 @@ __device__ __forceinline__ void drain_tile(const Params& p, const CUtensorMap* m
                 break;
             case SWARM_EPI_DGELU:
                 if (row_ok) {
-                    const uint4* u4 = reinterpret_cast<const uint4*>(static_cast<const __nv_bfloat16*>(p.aux) + off);
 #pragma unroll
                     for (int q = 0; q < 4; ++q) {
-                        const uint4 w = u4[q];
+                        const uint4 w = a4[q];
                         const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
 #pragma unroll
                         for (int j = 0; j < 4; ++j) {
@@ -371,10 +391,9 @@ __device__ __forceinline__ void drain_tile(const Params& p, const CUtensorMap* m
             }
             case SWARM_EPI_MUL:  // D = acc * U (U = gelu' saved by the forward)
                 if (row_ok) {
-                    const uint4* u4 = reinterpret_cast<const uint4*>(static_cast<const __nv_bfloat16*>(p.aux) + off);
 #pragma unroll
                     for (int q = 0; q < 4; ++q) {
-                        const uint4 w = u4[q];
+                        const uint4 w = a4[q];
                         const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
 #pragma unroll
                         for (int j = 0; j < 4; ++j) {
@@ -1329,6 +1348,11 @@ extern "C" int swarm_gemm_bf16(const swarm_gemm_args* a, swarm_stream_t stream) 
             return e ? atoi(e) : 0;
         }();
         p.dbg = dbg;
+        static const int pf = [] {
+            const char* e = getenv("SWARM_GEMM_AUX_PREFETCH");
+            return e && e[0] == '0' ? 0 : 1;
+        }();
+        p.aux_prefetch = pf;
     }
     p.tma_epi = tma_epi_enabled() && (a->batch == 1 || exact) && d_cols <= a->ldd &&
                 ((reinterpret_cast<uintptr_t>(a->d) & 15) == 0) && ((a->ldd * esz) % 16 == 0) &&
