@@ -973,8 +973,24 @@ def bench_failure(args, world, rank, local):
     torch.cuda.synchronize()
     stream = torch.cuda.current_stream()
     v_now = lambda: ex.engine.summary()["now"]  # noqa: E731
+    warm = 24  # per segment: the first microbatches after a membership change run untimed (a migrated
+    # peer's new stage captures its visit graphs there; requeued work drains)
     while True:
         lay, c0, t_v0 = layout_now(), ex.counters(), v_now()
+        nw = ex.run_until(warm, -2)
+        ex.finish()
+        torch.cuda.synchronize()
+        if layout_now() != lay or nw < warm:  # the segment ended inside its warm-up: a transition
+            c1 = ex.counters()
+            if nw == 0 and c1["records"] == c0["records"]:
+                break
+            segments.append({"layout": lay, "microbatches": nw, "ms": None, "tokens_per_s": None,
+                             "virtual_s": [t_v0, v_now()], "recomputes": c1["recomputes"] - c0["recomputes"],
+                             "state_bytes": c1["state_bytes"] - c0["state_bytes"],
+                             "note": "transition (shorter than the untimed warm-up)"})
+            if v_now() >= cfg.duration_seconds or len(segments) > 12:
+                break
+            continue
         barrier(world)
         t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         t0.record(stream)
@@ -984,10 +1000,8 @@ def bench_failure(args, world, rank, local):
         torch.cuda.synchronize()
         ms = max_over_ranks(t0.elapsed_time(t1), world)
         c1 = ex.counters()
-        if n == 0 and c1["records"] == c0["records"]:
-            break
-        segments.append({"layout": lay, "microbatches": n, "ms": ms,
-                         "tokens_per_s": n * mcfg.tokens / (ms / 1e3) if ms > 0 else None,
+        segments.append({"layout": lay, "microbatches": n, "untimed_warmup_microbatches": nw, "ms": ms,
+                         "tokens_per_s": n * mcfg.tokens / (ms / 1e3) if ms > 0 and n > 0 else None,
                          "virtual_s": [t_v0, v_now()], "recomputes": c1["recomputes"] - c0["recomputes"],
                          "state_bytes": c1["state_bytes"] - c0["state_bytes"]})
         if v_now() >= cfg.duration_seconds or len(segments) > 12:
@@ -1014,13 +1028,13 @@ def bench_failure(args, world, rank, local):
                        "dispatched": counts[0], "completed": counts[1], "requeued": counts[2], "abandoned": counts[3],
                        "completions_per_bucket": list(b)[: nb.value], "bucket_seconds": cfg.bucket_seconds,
                        "driver_completed_same_schedule": int(ex.engine.summary()["completed"]),
-                       "oracle_throughput_per_layout": {
-                           str(seg["layout"]): O.ref.ref_oracle_throughput(
+                       "oracle_throughput_for_n_peers": {
+                           str(sum(seg["layout"])): O.ref.ref_oracle_throughput(
                                (C.c_double * S)(*([1.0 / (3 * fwd)] * (S - 1) + [1.0 / (3 * fwd * head)])), S,
                                sum(seg["layout"])) * mcfg.tokens for seg in segments}}
         except Exception as e:  # the prediction is a report, not part of the measured path
             ref = {"unavailable": repr(e)[:200]}
-    steady = [sg for sg in segments if sg["microbatches"] >= 16]
+    steady = [sg for sg in segments if sg["tokens_per_s"]]
     last = steady[-1] if steady else segments[-1]
     return {"metric": "training tokens/s per membership segment (peer failure + adaptive rebalancing)",
             "value": last["tokens_per_s"], "unit": "tokens/s", "n_gpus": world, "steps": len(segments),
