@@ -956,7 +956,8 @@ def bench_failure(args, world, rank, local):
                        allreduce_period=0.5, allreduce_stall=1e-3, duration_seconds=9.0, bucket_seconds=0.5,
                        churn=[(4.5, -1)], rebalance_period=3.0, straggler_timeout=0.05, propagation_delay=0.01,
                        announce_ttl=300.0, state_transfer_bytes=state_bytes, download_bps=8 * 400e9)
-    ex = EngineExecutor(mcfg, S, seed=1, lr=1e-4, sim=cfg, lanes=args.lanes if world > 1 else 1)
+    ex = EngineExecutor(mcfg, S, seed=1, lr=1e-4, sim=cfg, lanes=args.lanes if world > 1 else 1,
+                        use_graphs=not args.no_graphs)
     n_peers0 = ex.n_peers
 
     def layout_now():
@@ -976,11 +977,14 @@ def bench_failure(args, world, rank, local):
     warm = 24  # per segment: the first microbatches after a membership change run untimed (a migrated
     # peer's new stage captures its visit graphs there; requeued work drains)
     while True:
-        lay, c0, t_v0 = layout_now(), ex.counters(), v_now()
+        c0, t_v0 = ex.counters(), v_now()
+        # the membership record the previous segment stopped in front of is processed first (stage
+        # re-created, communicators re-split, state downloaded: untimed), then the warm-up
         nw = ex.run_until(warm, -2)
         ex.finish()
         torch.cuda.synchronize()
-        if layout_now() != lay or nw < warm:  # the segment ended inside its warm-up: a transition
+        lay = layout_now()
+        if nw < warm:  # the next membership change came inside the warm-up: a transition
             c1 = ex.counters()
             if nw == 0 and c1["records"] == c0["records"]:
                 break
@@ -1110,6 +1114,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-codec", action="store_true", help="train: skip the codec sub-measurement")
     ap.add_argument("--no-extra", action="store_true", help="train: skip the configs[0] / configs[3] sub-lines")
+    ap.add_argument("--no-graphs", action="store_true", help="failure: eager visits (no CUDA-graph capture / replay)")
     ap.add_argument("--sync", action="store_true",
                     help="train: headline = the synchronous GPipe step (default: the asynchronous engine-driven "
                          "pipeline, with the GPipe step reported beside it)")

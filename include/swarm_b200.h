@@ -577,8 +577,9 @@ int swarm_driver_create(const swarm_driver_config* cfg, swarm_driver_t* out);
 void swarm_driver_destroy(swarm_driver_t d);
 /* process the driver's own engine records until n more microbatches completed */
 int swarm_driver_run(swarm_driver_t d, uint64_t n_microbatches, uint64_t* completed);
-/* the same, stopping early right after a record of kind `stop_kind` (>= 0), e.g. SWARM_ENG_LEAVE, or
- * after any membership change (LEAVE / JOIN / MIGRATE / MIGRATED) for stop_kind = -2 */
+/* the same, stopping early right after a record of kind `stop_kind` (>= 0), e.g. SWARM_ENG_LEAVE, or,
+ * for stop_kind = -2, right *before* a membership record (LEAVE / JOIN / MIGRATE / MIGRATED) once at
+ * least one microbatch completed (the record is processed first by the next call) */
 int swarm_driver_run_until(swarm_driver_t d, uint64_t n_microbatches, int stop_kind, uint64_t* completed);
 /* membership as the records left it: the peer's stage, liveness, migration state and rank */
 int swarm_driver_peer_info(swarm_driver_t d, int peer, int* stage, int* alive, int* migrating, int* rank);

@@ -171,6 +171,8 @@ struct swarm_driver {
     bool prof = false;
     cudaStream_t prof_stream = nullptr;
     std::string prof_table;  // per-shape GEMM lines of the last profiled region (all local stages)
+    swarm_engine_record pending{};  // run_until(-2): the membership record it stopped in front of
+    bool has_pending = false;
     int bank = 0;  // DPU: the bank (weights shadow + gradient arena) the current interval's visits use
 
     cudaStream_t lane_stream(const Peer& p) const { return prof ? prof_stream : p.lanes[p.cur]; }
@@ -1012,12 +1014,23 @@ int swarm_driver_run_until(swarm_driver_t d, uint64_t n_microbatches, int stop_k
     swarm_engine_record rec;
     while (d->completed < target) {
         size_t n = 0;
-        if (swarm_engine_next(d->engine, &rec, 1, &n) != SWARM_OK)
+        if (d->has_pending) {  // a membership record held back by the previous call
+            rec = d->pending;
+            d->has_pending = false;
+            n = 1;
+        } else if (swarm_engine_next(d->engine, &rec, 1, &n) != SWARM_OK) {
             return fail(std::string("driver: ") + swarm_engine_last_error());
+        }
         if (n == 0) break;  // the engine reached duration_seconds
+        const bool membership = rec.kind >= SWARM_ENG_LEAVE && rec.kind != SWARM_ENG_REBALANCE;
+        if (stop_kind == -2 && membership && d->completed > start) {
+            // stop *before* it: its work (a stage re-created, communicators re-split) belongs to the next region
+            d->pending = rec;
+            d->has_pending = true;
+            break;
+        }
         TRY(d->on_record(rec));
         if (stop_kind >= 0 && rec.kind == stop_kind) break;
-        if (stop_kind == -2 && rec.kind >= SWARM_ENG_LEAVE && rec.kind != SWARM_ENG_REBALANCE) break;
     }
     if (completed) *completed = d->completed - start;
     return SWARM_OK;
