@@ -953,8 +953,8 @@ def bench_failure(args, world, rank, local):
     fwd = 6.3e-3  # measured forward visit (configs[2] stage, B200): virtual time ~ real time
     state_bytes = mcfg.params_per_layer() * mcfg.layers_per_stage * 6  # rebalancer.cpp:71-75
     cfg = EngineConfig(n_stages=S, initial_peers=speeds, forward_service_seconds=fwd, trainers_per_peer=2,
-                       allreduce_period=0.5, allreduce_stall=1e-3, duration_seconds=9.0, bucket_seconds=0.5,
-                       churn=[(4.5, -1)], rebalance_period=3.0, straggler_timeout=0.05, propagation_delay=0.01,
+                       allreduce_period=0.5, allreduce_stall=1e-3, duration_seconds=17.9, bucket_seconds=0.5,
+                       churn=[(9.0, -1)], rebalance_period=6.0, straggler_timeout=0.05, propagation_delay=0.01,
                        announce_ttl=300.0, state_transfer_bytes=state_bytes, download_bps=8 * 400e9)
     ex = EngineExecutor(mcfg, S, seed=1, lr=1e-4, sim=cfg, lanes=args.lanes if world > 1 else 1,
                         use_graphs=not args.no_graphs)
@@ -974,7 +974,7 @@ def bench_failure(args, world, rank, local):
     torch.cuda.synchronize()
     stream = torch.cuda.current_stream()
     v_now = lambda: ex.engine.summary()["now"]  # noqa: E731
-    warm = 24  # per segment: the first microbatches after a membership change run untimed (a migrated
+    warm = 48  # per segment: the first microbatches after a membership change run untimed (a migrated
     # peer's new stage captures its visit graphs there; requeued work drains)
     while True:
         c0, t_v0 = ex.counters(), v_now()
@@ -1046,10 +1046,10 @@ def bench_failure(args, world, rank, local):
             "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
             "config": {"workload": f"BASELINE configs[4]: failure + rebalancing, {S} stages of the configs[2] "
                                    f"block (d 2048, {mcfg.layers_per_stage} layers/stage), initial layout {layout}, "
-                                   f"{n_peers0} peers on {world} GPU(s), one peer leaves at t = 4.5 s",
+                                   f"{n_peers0} peers on {world} GPU(s), one peer leaves at t = 9 s",
                        "model": args.model, "stages": S, "initial_layout": layout,
-                       "schedule": "engine (= sim::run) with RebalanceMode::Periodic every 3 s, straggler timeout "
-                                   "50 ms, churn trace [(4.5 s, -1)], AllReduceTick every 0.5 s, 9 s; forward visit "
+                       "schedule": "engine (= sim::run) with RebalanceMode::Periodic every 6 s, straggler timeout "
+                                   "50 ms, churn trace [(9 s, -1)], AllReduceTick every 0.5 s, 17.9 s; forward visit "
                                    f"{fwd * 1e3:.1f} ms so engine time tracks real time; last stage slowed by its LM "
                                    f"head ({head:.3f}x)"},
             "segments": segments, "decisions": decisions, "driver": ex.counters(), "reference": ref,
