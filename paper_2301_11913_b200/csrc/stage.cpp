@@ -80,6 +80,7 @@ struct Work {
     float *S = nullptr, *dP = nullptr, *logits = nullptr;
     EP dS, gy[2], dhid, dc, du, dqkv, dO, da, dlogits, wtmp;
     void* lnws = nullptr;
+    void* abws = nullptr;
     cudaStream_t side = nullptr;
     void* skws[2] = {nullptr, nullptr};
     cudaEvent_t ev_fork[7] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
@@ -128,6 +129,8 @@ struct swarm_stage {
     std::vector<void*> allocations;
     int step = 0;
     bool fused_attn = false;  // scores+softmax in one tcgen05 kernel (csrc/attention.cu)
+    bool fused_bwd = false;   // the attention backward in one kernel (csrc/attn_bwd.cu)
+    void* abws = nullptr;     // its dQ accumulator + arrival counters (zeroed once; kernels leave it zeroed)
     // weight-gradient GEMMs run on a side stream forked/joined per layer, so they
     // fill the SMs the data-gradient chain leaves idle (GEMM wave tails)
     cudaStream_t side = nullptr;
@@ -181,6 +184,11 @@ int dmalloc(swarm_stage* s, void** p, size_t bytes) {
     }
     s->allocations.push_back(*p);
     return SWARM_OK;
+}
+
+// the fused attention backward's workspace (zero-filled; the kernel leaves it zeroed)
+int attn_ws_alloc(swarm_stage* s, void** p) {
+    return dmalloc(s, p, swarm_attn_backward_workspace(s->B, s->H, s->L, s->dh));
 }
 
 template <typename T>
@@ -530,9 +538,35 @@ int ln_backward_split(swarm_stage* s, EP dy, EP x, const float* gain, const floa
     return SWARM_OK;
 }
 
+// The unfused attention backward: score gradients (fused softmax-backward kernel, or a GEMM
+// + row kernel), then dQ, dK, dV as batched GEMMs over dS / P (SWARM_ATTN_BWD_FUSED=0, d_head != 128)
+int attn_backward_unfused(swarm_stage* s, const Act& A, EP dqkv, float scale, cudaStream_t st) {
+    const int T = s->T, d = s->d, H = s->H, dh = s->dh, L = s->L, BHL = s->B * s->H * s->L;
+    if (s->fused_attn) {
+        PTRY(SWARM_PROF_ATTENTION, st, swarm_attn_scores_softmax_backward(s->dO, d, A.qkv + 2 * d, 3 * d, d, A.o, d, A.P, s->B, H, L, dh, scale,
+                                               s->cfg.causal, s->dS, st));
+    } else {
+        TRY(bmm(s, L, L, dh, {{s->dO, d, T, d, false}, L, 0, 0, dh},
+                {{A.qkv + 2 * d, 3 * d, T, d, false}, L, 0, 0, dh}, s->dP, L, H * L, L, 0, 0, SWARM_EPI_STORE_F32,
+                1.f, st));
+        PTRY(SWARM_PROF_ATTENTION, st, swarm_attn_softmax_backward_ex(A.P, s->dP, BHL, L, scale, s->dS, s->dt, st));
+    }
+    // dQ = dS K ; dK = dS^T Q ; dV = P^T dO   (all read in place, written into dqkv); dQ runs on the
+    // side stream beside dK, dV (three independent GEMMs of 1.7 waves each fill each other's tails)
+    TRY(fork_side(s, st, 4));
+    TRY(bmm(s, L, dh, L, {{s->dS, L, BHL, L, false}, H * L, L, 0, 0}, {{A.qkv + d, 3 * d, T, d, true}, L, 0, 0, dh},
+            dqkv, 3 * d, L, 0, 0, dh, SWARM_EPI_STORE_BF16, 1.f, side_of(s, st), 1));
+    TRY(bmm(s, L, dh, L, {{s->dS, L, BHL, L, true}, H * L, L, 0, 0}, {{A.qkv, 3 * d, T, d, true}, L, 0, 0, dh},
+            dqkv + d, 3 * d, L, 0, 0, dh, SWARM_EPI_STORE_BF16, 1.f, st, 2));
+    TRY(bmm(s, L, dh, L, {{A.P, L, BHL, L, true}, H * L, L, 0, 0}, {{s->dO, d, T, d, true}, L, 0, 0, dh},
+            dqkv + 2 * d, 3 * d, L, 0, 0, dh, SWARM_EPI_STORE_BF16, 1.f, st, 2));
+    TRY(wait_side(s, st, s->ev_dq));  // dqkv complete on main (the dWqkv fork below then carries it to the side)
+    return SWARM_OK;
+}
+
 int block_backward(swarm_stage* s, const Act& A, EP dy, EP dx, const LayerW& W, cudaStream_t st,
                    const WgradPlan& wp = WgradPlan{}, const Stash* cs = nullptr) {
-    const int T = s->T, d = s->d, H = s->H, dh = s->dh, F = s->F, L = s->L, BHL = s->B * s->H * s->L;
+    const int T = s->T, d = s->d, H = s->H, dh = s->dh, F = s->F, L = s->L;
     const EP p16 = wts(s);
     float* G = s->grad;
     cudaStream_t sd = side_of(s, st);  // weight gradients
@@ -565,25 +599,14 @@ int block_backward(swarm_stage* s, const Act& A, EP dy, EP dx, const LayerW& W, 
            st));
     // dP = dO V^T ; dS = scale * P (dP - rowsum(P dP))
     const float scale = 1.f / std::sqrt(static_cast<float>(dh));
-    if (s->fused_attn) {
-        PTRY(SWARM_PROF_ATTENTION, st, swarm_attn_scores_softmax_backward(s->dO, d, A.qkv + 2 * d, 3 * d, d, A.o, d, A.P, s->B, H, L, dh, scale,
-                                               s->cfg.causal, s->dS, st));
+    if (s->fused_bwd) {
+        // the whole attention backward in one kernel: dP, dS on chip, dQ | dK | dV into dqkv
+        PTRY(SWARM_PROF_ATTENTION, st, swarm_attn_backward(s->dO, d, A.qkv, 3 * d, 3 * d, d, 2 * d, A.o, d, A.P, s->B, H, L,
+                                                           dh, scale, s->cfg.causal, dqkv, 3 * d, d, 2 * d, s->abws,
+                                                           st));
     } else {
-        TRY(bmm(s, L, L, dh, {{s->dO, d, T, d, false}, L, 0, 0, dh},
-                {{A.qkv + 2 * d, 3 * d, T, d, false}, L, 0, 0, dh}, s->dP, L, H * L, L, 0, 0, SWARM_EPI_STORE_F32,
-                1.f, st));
-        PTRY(SWARM_PROF_ATTENTION, st, swarm_attn_softmax_backward_ex(A.P, s->dP, BHL, L, scale, s->dS, s->dt, st));
+        TRY(attn_backward_unfused(s, A, dqkv, scale, st));
     }
-    // dQ = dS K ; dK = dS^T Q ; dV = P^T dO   (all read in place, written into dqkv); dQ runs on the
-    // side stream beside dK, dV (three independent GEMMs of 1.7 waves each fill each other's tails)
-    TRY(fork_side(s, st, 4));
-    TRY(bmm(s, L, dh, L, {{s->dS, L, BHL, L, false}, H * L, L, 0, 0}, {{A.qkv + d, 3 * d, T, d, true}, L, 0, 0, dh},
-            dqkv, 3 * d, L, 0, 0, dh, SWARM_EPI_STORE_BF16, 1.f, side_of(s, st), 1));
-    TRY(bmm(s, L, dh, L, {{s->dS, L, BHL, L, true}, H * L, L, 0, 0}, {{A.qkv, 3 * d, T, d, true}, L, 0, 0, dh},
-            dqkv + d, 3 * d, L, 0, 0, dh, SWARM_EPI_STORE_BF16, 1.f, st, 2));
-    TRY(bmm(s, L, dh, L, {{A.P, L, BHL, L, true}, H * L, L, 0, 0}, {{s->dO, d, T, d, true}, L, 0, 0, dh},
-            dqkv + 2 * d, 3 * d, L, 0, 0, dh, SWARM_EPI_STORE_BF16, 1.f, st, 2));
-    TRY(wait_side(s, st, s->ev_dq));  // dqkv complete on main (the dWqkv fork below then carries it to the side)
     // da = dqkv Wqkv ; dWqkv += dqkv^T a
     TRY(fork_side(s, st, 3));
     TRY(wgrad(s, wp, 3 * d, d, {dqkv, 3 * d, T, 3 * d, true}, {A.a, d, T, d, true},
@@ -781,11 +804,16 @@ int create(const swarm_stage_config* c, swarm_stage* s) {
         const char* e = getenv("SWARM_ATTN_FUSED");
         s->fused_attn = !s->f32 && !(e && e[0] == '0') && s->L % 128 == 0 && s->L <= 512 && s->dh % 64 == 0 && s->dh <= 128;
     }
+    {
+        const char* e = getenv("SWARM_ATTN_BWD_FUSED");
+        s->fused_bwd = s->fused_attn && s->dh == 128 && !(e && e[0] == '0');
+    }
     if (!s->fused_attn) {
         TRY(alloc(s, &s->S, BHLL));
         TRY(alloc(s, &s->dP, BHLL));
     }
-    TRY(alloc(s, &s->dS, BHLL));
+    if (s->fused_bwd) TRY(attn_ws_alloc(s, &s->abws));
+    else TRY(alloc(s, &s->dS, BHLL));
     TRY(alloc(s, &s->gy[0], Td));
     TRY(alloc(s, &s->gy[1], Td));
     TRY(alloc(s, &s->dhid, Td));
@@ -829,7 +857,7 @@ int create(const swarm_stage_config* c, swarm_stage* s) {
 
 namespace {
 #define SWARM_WORK_FIELDS(X) X(S) X(dP) X(logits) X(dS) X(dhid) X(dc) X(du) X(dqkv) X(dO) X(da) X(dlogits) X(wtmp) \
-    X(lnws) X(side) X(ev_join) X(ev_dq)
+    X(lnws) X(abws) X(side) X(ev_join) X(ev_dq)
 void work_save(const swarm_stage* s, Work& w) {
 #define X(f) w.f = s->f;
     SWARM_WORK_FIELDS(X)
@@ -851,7 +879,8 @@ int work_alloc(swarm_stage* s, Work& w) {
         TRY(alloc(s, &w.S, BHLL));
         TRY(alloc(s, &w.dP, BHLL));
     }
-    TRY(alloc(s, &w.dS, BHLL));
+    if (s->fused_bwd) TRY(attn_ws_alloc(s, &w.abws));
+    else TRY(alloc(s, &w.dS, BHLL));
     TRY(alloc(s, &w.gy[0], Td));
     TRY(alloc(s, &w.gy[1], Td));
     TRY(alloc(s, &w.dhid, Td));

@@ -114,3 +114,85 @@ def test_fused_attention_forward_pv(cuda, B, H, L, dh, causal):
     # and both match the fp32 reference attention within the bf16 P rounding
     full = (ref_P(qkv, B, H, L, dh, causal).view(B, H, L, L) @ v).transpose(1, 2).reshape(B * L, d)
     assert float((O.float() - full).norm() / full.norm()) < 1e-2
+
+
+def attn_backward_ref(qkv, dO, O, P, B, H, L, dh):
+    """torch fp32 of the same op on the same bf16 inputs: dS = scale * P * (dO V^T - dO.O) rounded to
+    bf16 (the kernel keeps dS in bf16 shared memory as the MMA operand), dV = P^T dO, dK = dS^T Q, dQ = dS K."""
+    d = H * dh
+    split = lambda t: t.float().view(B, L, H, dh).transpose(1, 2)  # noqa: E731
+    q, k, v = split(qkv[:, :d]), split(qkv[:, d:2 * d]), split(qkv[:, 2 * d:])
+    do, o = split(dO), split(O)
+    Pf = P.float().view(B, H, L, L)
+    D = (do * o).sum(-1, keepdim=True)
+    dS = ((Pf * (do @ v.transpose(-1, -2) - D)) / math.sqrt(dh)).bfloat16().float()
+    join = lambda t: t.transpose(1, 2).reshape(B * L, d)  # noqa: E731
+    return join(dS @ k), join(dS.transpose(-1, -2) @ q), join(Pf.transpose(-1, -2) @ do)
+
+
+@pytest.mark.parametrize("B,H,L,dh,causal", [(2, 4, 512, 128, 1), (2, 4, 512, 128, 0), (1, 3, 256, 128, 1),
+                                             (1, 2, 384, 128, 1), (4, 16, 512, 128, 1), (1, 2, 1024, 128, 1),
+                                             (1, 1, 128, 128, 1)])
+def test_fused_attention_backward(cuda, B, H, L, dh, causal):
+    """swarm_attn_backward (dP, dS on chip; dQ | dK | dV into one dqkv) vs torch fp32 of the same op,
+    run twice on one workspace (the kernel must leave its dQ accumulator and counters zeroed)."""
+    import torch
+    from paper_2301_11913_b200 import _lib
+    torch.manual_seed(5 * L + causal + H)
+    d = H * dh
+    qkv = (torch.randn(B * L, 3 * d, device="cuda") * 2).bfloat16()
+    P = torch.zeros(B * H * L, L, device="cuda", dtype=torch.bfloat16)
+    O = torch.zeros(B * L, d, device="cuda", dtype=torch.bfloat16)
+    scale = 1 / math.sqrt(dh)
+    st = torch.cuda.current_stream().cuda_stream
+    L_ = _lib.lib()
+    ptr = lambda t: C.c_void_p(t.data_ptr())  # noqa: E731
+    assert L_.swarm_attn_forward_pv(ptr(qkv), ptr(qkv[:, d:]), ptr(qkv[:, 2 * d:]), 3 * d, d, B, H, L, dh, scale,
+                                    causal, ptr(P), ptr(O), d, st) == 0
+    ws = torch.zeros(L_.swarm_attn_backward_workspace(B, H, L, dh), device="cuda", dtype=torch.uint8)
+    for it in range(2):
+        dO = torch.randn(B * L, d, device="cuda").bfloat16()
+        dqkv = torch.full((B * L, 3 * d), float("nan"), device="cuda", dtype=torch.bfloat16)
+        rc = L_.swarm_attn_backward(ptr(dO), d, ptr(qkv), 3 * d, 3 * d, d, 2 * d, ptr(O), d, ptr(P), B, H, L, dh,
+                                    scale, causal, ptr(dqkv), 3 * d, d, 2 * d, ptr(ws), st)
+        assert rc == 0, _lib.last_error()
+        torch.cuda.synchronize()
+        assert int(ws.count_nonzero()) == 0, "workspace not left zeroed"
+        want = attn_backward_ref(qkv, dO, O, P, B, H, L, dh)
+        for name, got, ref in zip("QKV", dqkv.float().split(d, 1), want):
+            err = float((got - ref).norm() / ref.norm())
+            assert err < 1e-2, (it, name, err)
+            torch.testing.assert_close(got, ref, rtol=2e-2, atol=2e-2 * float(ref.abs().max()), msg=f"d{name}")
+
+
+def test_fused_attention_backward_matches_unfused(cuda):
+    """The one-kernel backward against the unfused kernels the executor used before (score-gradient
+    kernel, then dQ / dK / dV as GEMMs over the materialised dS): same op, same bf16 dS."""
+    import torch
+    from paper_2301_11913_b200 import _lib
+    B, H, L, dh, causal = 2, 4, 512, 128, 1
+    d = H * dh
+    torch.manual_seed(11)
+    qkv = torch.randn(B * L, 3 * d, device="cuda").bfloat16()
+    P = torch.zeros(B * H * L, L, device="cuda", dtype=torch.bfloat16)
+    O = torch.zeros(B * L, d, device="cuda", dtype=torch.bfloat16)
+    dO = torch.randn(B * L, d, device="cuda").bfloat16()
+    scale = 1 / math.sqrt(dh)
+    st = torch.cuda.current_stream().cuda_stream
+    L_ = _lib.lib()
+    ptr = lambda t: C.c_void_p(t.data_ptr())  # noqa: E731
+    assert L_.swarm_attn_forward_pv(ptr(qkv), ptr(qkv[:, d:]), ptr(qkv[:, 2 * d:]), 3 * d, d, B, H, L, dh, scale,
+                                    causal, ptr(P), ptr(O), d, st) == 0
+    dS = torch.zeros_like(P)
+    assert L_.swarm_attn_scores_softmax_backward(ptr(dO), d, ptr(qkv[:, 2 * d:]), 3 * d, d, ptr(O), d, ptr(P), B, H, L,
+                                                 dh, scale, causal, ptr(dS), st) == 0
+    ws = torch.zeros(L_.swarm_attn_backward_workspace(B, H, L, dh), device="cuda", dtype=torch.uint8)
+    dqkv = torch.empty(B * L, 3 * d, device="cuda", dtype=torch.bfloat16)
+    assert L_.swarm_attn_backward(ptr(dO), d, ptr(qkv), 3 * d, 3 * d, d, 2 * d, ptr(O), d, ptr(P), B, H, L, dh, scale,
+                                  causal, ptr(dqkv), 3 * d, d, 2 * d, ptr(ws), st) == 0
+    split = lambda t: t.float().view(B, L, H, dh).transpose(1, 2)  # noqa: E731
+    join = lambda t: t.transpose(1, 2).reshape(B * L, d)  # noqa: E731
+    dSf = dS.float().view(B, H, L, L)
+    q, k = split(qkv[:, :d]), split(qkv[:, d:2 * d])
+    for got, ref in zip(dqkv.float().split(d, 1)[:2], (join(dSf @ k), join(dSf.transpose(-1, -2) @ q))):
+        assert float((got - ref).norm() / ref.norm()) < 5e-3
