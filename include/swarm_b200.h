@@ -229,16 +229,16 @@ int swarm_attn_forward_pv(const void* q, const void* k, const void* v, int ld, i
 int swarm_attn_scores_softmax_backward(const void* dO, int ld_do, const void* v, int ld_v, int v_cols, const void* o,
                                        int ld_o, const void* P, int B, int H, int L, int d_head, float scale,
                                        int causal, void* dS, swarm_stream_t stream);
-/* The whole attention backward in one kernel (tcgen05, d_head 128, L % 128 == 0): with dO
+/* The attention backward with dP and dS on chip (tcgen05, d_head 128, L % 128 == 0): with dO
  * [B*L, ld_do] (head h at column h*128), the forward's qkv storage (Q at column 0, K at k_col0,
  * V at v_col0, row stride ld_qkv, qkv_cols valid columns), O [B*L, ld_o] and the forward's P
  * (bf16 [B*H*L, L]), writes dQ | dK | dV (bf16) into dqkv at columns 0 | dk_col0 | dv_col0
  * (+ h*128, row stride ld_dqkv):
  *   dV = P^T dO,  dS = scale * P * (dO V^T - dO.O),  dK = dS^T Q,  dQ = dS K
- * with dP and dS kept on chip.  workspace: swarm_attn_backward_workspace(B, H, L, 128) bytes,
- * zeroed by the caller once (every launch leaves it zeroed); one launch in flight per workspace.
- * dQ's fp32 sum over key blocks uses atomics (summation order not fixed).  Replaces
- * swarm_attn_scores_softmax_backward + the three dS / P GEMMs. */
+ * workspace: swarm_attn_backward_workspace(B, H, L, 128) bytes, zeroed by the caller once (every
+ * call leaves its fp32 dQ accumulator, the head B*L*H*128*4 bytes, zeroed); one call in flight per
+ * workspace.  dQ's fp32 sum over key blocks uses reduce-add (summation order not fixed).
+ * Replaces swarm_attn_scores_softmax_backward + the three dS / P GEMMs (csrc/attn_bwd.cu). */
 size_t swarm_attn_backward_workspace(int B, int H, int L, int d_head);
 int swarm_attn_backward(const void* dO, int ld_do, const void* qkv, int ld_qkv, int qkv_cols, int k_col0, int v_col0,
                         const void* O, int ld_o, const void* P, int B, int H, int L, int d_head, float scale,

@@ -1,39 +1,38 @@
 // Fused attention backward (sm_100a, tcgen05 + TMEM + TMA), d_head 128:
 //
-//   dP = dO V^T,  dS = scale * P * (dP - dO.O),  dV = P^T dO,  dK = dS^T Q,  dQ = dS K
+//   dP = dO V^T,  dS = scale * P * (dP - D),  dV = P^T dO,  dK = dS^T Q,  dQ = dS K
 //
-// for z = b*H + h, with P the forward's bf16 probabilities.  It replaces the
-// score-gradient kernel + three batched GEMMs of the unfused backward: dS never
-// leaves shared memory, and dV / dK / dQ come out of this one kernel.
+// for z = b*H + h, with P the forward's bf16 probabilities and D = rowsum(dO * O) (=
+// rowsum(P * dP)).  It replaces the score-gradient kernel + three batched GEMMs of the
+// unfused backward: dP and dS never leave the SM.  Three launches:
+//   k_attn_rowdot  D per (z, query)                          (reads dO, O once: 16 MB at configs[2])
+//   k_attn_bwd     dK, dV (bf16, into dqkv) and dQ partials  (TMA reduce-add into an fp32 accumulator)
+//   k_attn_dq_out  the accumulator -> bf16 dQ into dqkv, and back to zero
 //
-// One CTA owns key blocks of 128 keys of one (b, h) and streams the query blocks
-// that see them (causal: query blocks >= the key block).  Per query block j:
-//   TMA      dO_j, Q_j, P_j (three [128 x 128] bf16 tiles, SWIZZLE_128B 64-column boxes)
-//   MMA      dP = dO_j V_i^T            (TMEM columns   0-127, M = queries)
-//            dV += P_j^T dO_j           (TMEM columns 384-511, M = keys; P_j read MN-major)
-//   rows     dS_j = scale * P_j * (dP - D_j), written over P_j in shared memory
-//            (one query row per thread; D_j = dO_j . O_j per row from warp 3)
-//   MMA      dK += dS_j^T Q_j           (TMEM columns 256-383; dS read MN-major)
-//            dQ_j = dS_j K_i            (TMEM columns 128-255; dS read K-major)
-//   rows     dQ_j -> red.global.add into an fp32 accumulator; the last key block to
-//            add to query block j (an arrival counter) converts it to bf16 into dqkv
-//            and re-zeroes the accumulator and the counter
-// and once per key block the dK / dV accumulators go to dqkv in bf16.  The same
-// shared-memory tile serves as K-major and MN-major operand (SWIZZLE_128B atoms are
-// 8 rows x 128 B either way; only the descriptor's reading of them differs).
+// k_attn_bwd: one CTA owns key blocks of 128 keys of one (b, h) and streams the query
+// blocks that see them (causal: query blocks >= the key block).  Per query block j:
+//   TMA    dO_j, Q_j, P_j ([128 x 128] bf16 tiles as two SWIZZLE_128B 64-column boxes; P
+//          double-buffered, dO reloaded as soon as its MMAs are issued, Q after dK's)
+//   MMA    dP = dO_j V_i^T        (TMEM columns   0-127, M = queries)
+//          dV += P_j^T dO_j       (TMEM columns 384-511, M = keys; P_j read MN-major)
+//   rows   dS_j = scale * P_j * (dP - D_j) over P_j in shared memory (warps 4-7, one query
+//          row per thread)
+//   MMA    dK += dS_j^T Q_j       (TMEM columns 256-383; dS read MN-major)
+//          dQ_j = dS_j K_i        (TMEM columns 128-255; dS read K-major)
+//   rows   dQ_j -> shared staging -> TMA reduce-add (warps 8-11, off the dS critical path)
+// and per key block dK, dV: TMEM -> bf16 over K_i / V_i in shared memory -> TMA stores.
+// One shared-memory tile serves as K-major and MN-major operand: SWIZZLE_128B atoms are
+// 8 rows x 128 B either way; only the descriptor's reading of them differs.
 //
-// Causal work is paired: a CTA takes key blocks t and nkb-1-t, so every CTA streams
-// nkb + 1 query blocks (configs[2]: L = 512 -> 2 CTAs per (b, h), 128 CTAs, one wave).
-// TMEM: all 512 columns, so one CTA per SM.
+// Causal work is paired: a CTA takes key blocks t and nkb-1-t, so every CTA streams nkb + 1
+// query blocks (configs[2]: L 512 -> 2 CTAs per (b, h), 128 CTAs, one wave).  Everything a
+// CTA reads after its first block is prefetched to L2 at entry.  TMEM: all 512 columns
+// (one CTA per SM).  Warps: 0 TMA, 1 MMA issuer, 2 TMEM allocator, 4-7 dS rows, 8-11 dQ rows.
 //
-// Warp roles: warp 0 TMA, warp 1 MMA issuer, warps 2-3 dQ conversion (warp 2 also allocates
-// TMEM), warps 4-7 dS rows and warps 8-11 dQ rows, one row per thread (TMEM lane quarter =
-// warp % 4).
-//
-// dQ's fp32 sum over key blocks is taken with atomics, so its order (<= L/128 terms)
-// is not fixed; SWARM_ATTN_BWD_FUSED=0 selects the unfused path (csrc/attention.cu +
-// batched GEMMs), whose results are order-deterministic.  Parity: tests/test_attention_gpu.py
-// (torch fp32 reference of the same op) and the stage tests against the fp64 oracle.
+// dQ's fp32 sum over key blocks uses reduce-add, so its order (<= L/128 terms) is not
+// fixed; SWARM_ATTN_BWD_FUSED=0 selects the unfused, order-deterministic path
+// (csrc/attention.cu + batched GEMMs).  Parity: tests/test_attention_gpu.py (torch fp32 of
+// the same op; the unfused kernels) and the stage tests against the fp64 oracle.
 #include <cudaTypedefs.h>
 
 #include <cstdlib>
@@ -61,10 +60,9 @@ constexpr int kBlk = 128;         // keys per key block = queries per query bloc
 constexpr int kDh = 128;          // d_head
 constexpr int kBox = kBlk * 128;  // one [128 rows x 64 columns] bf16 SWIZZLE_128B box: 16 KB
 constexpr int kTile = 2 * kBox;   // [128 x 128] bf16: 32 KB
-constexpr int kBars = 12;
-constexpr int kMaxBlocks = 24;  // query blocks one CTA streams (causal pair: nkb + 1 <= 9; else nkb <= 8)
+constexpr int kBars = 20;
 constexpr int kStg = kBlk * 128;  // dQ staging: [128 rows x 32] fp32, SWIZZLE_128B (16 KB)
-constexpr int kSmem = 6 * kTile + 2 * kStg + kBars * 8 + 16 + 4 * kMaxBlocks + 1024;
+constexpr int kSmem = 6 * kTile + 2 * kStg + kBars * 8 + 16 + 1024;
 constexpr uint32_t kColDP = 0, kColDQ = 128, kColDK = 256, kColDV = 384;
 static_assert(kSmem <= 232448, "attention backward: shared memory");
 
@@ -72,23 +70,17 @@ struct Params {
     int B, H, L, causal;
     float scale;
     int q_col0, k_col0, v_col0;  // head-0 columns of Q, K, V in the qkv storage
-    const __nv_bfloat16* o;      // forward output O [B*L, ld_o], head h at column h*128
-    int ld_o;
-    float* dq_acc;  // fp32 dQ accumulator [B*L, ld_acc] (zero on entry, left zero)
+    const float* D;              // rowsum(dO * O) per (z, query) [B*H*L] (k_attn_rowdot)
+    float* dq_acc;               // fp32 dQ accumulator [B*L, ld_acc] (zero on entry, left zero)
     int ld_acc;
-    int* counters;  // [B*H*(L/128)] key-block arrivals per query block (zero on entry, left zero)
     __nv_bfloat16* dqkv;
     int ld_dqkv, dq_col0, dk_col0, dv_col0;
-    int dbg;  // experiments (SWARM_ATTN_BWD_DBG): 1 skips the dQ reductions, 2 the dQ write-out
+    int dbg;  // experiments (SWARM_ATTN_BWD_DBG): 1 skips the dQ reductions, 2 the dQ write-out, 4 traces
 };
 
 __device__ __forceinline__ uint32_t pack2(float a, float b) {
     const __nv_bfloat162 p = __floats2bfloat162_rn(a, b);
     return *reinterpret_cast<const uint32_t*>(&p);
-}
-__device__ __forceinline__ void red_add_v4(float* p, float a, float b, float c, float d) {
-    asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p), "f"(a), "f"(b), "f"(c), "f"(d)
-                 : "memory");
 }
 __device__ __forceinline__ void tma_prefetch_l2(const CUtensorMap* m, int c0, int c1) {
     asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global [%0, {%1, %2}];" ::"l"(reinterpret_cast<uint64_t>(m)),
@@ -98,23 +90,6 @@ __device__ __forceinline__ void tma_prefetch_l2(const CUtensorMap* m, int c0, in
 __device__ __forceinline__ void dq_bar() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
 __device__ __forceinline__ float lo(uint32_t w) { return __uint_as_float(w << 16); }
 __device__ __forceinline__ float hi(uint32_t w) { return __uint_as_float(w & 0xffff0000u); }
-
-// 128 fp32 TMEM columns of this thread's lane -> 128 bf16 at dst (16-B aligned)
-__device__ __forceinline__ void tmem_row_to_bf16(uint32_t taddr, __nv_bfloat16* dst) {
-    uint4* d4 = reinterpret_cast<uint4*>(dst);
-#pragma unroll
-    for (int c = 0; c < 4; ++c) {
-        uint32_t r[32];
-        tmem_ld_32x32b_x32(taddr + 32 * c, r);
-        tmem_ld_wait();
-#pragma unroll
-        for (int w = 0; w < 4; ++w)
-            d4[4 * c + w] = make_uint4(pack2(__uint_as_float(r[8 * w]), __uint_as_float(r[8 * w + 1])),
-                                       pack2(__uint_as_float(r[8 * w + 2]), __uint_as_float(r[8 * w + 3])),
-                                       pack2(__uint_as_float(r[8 * w + 4]), __uint_as_float(r[8 * w + 5])),
-                                       pack2(__uint_as_float(r[8 * w + 6]), __uint_as_float(r[8 * w + 7])));
-    }
-}
 
 // the key blocks CTA `t` of a (b, h) owns: causal pairs (t, nkb-1-t), else one
 __device__ __forceinline__ int key_blocks(const Params& p, int t, int (&kb)[2]) {
@@ -127,8 +102,7 @@ __device__ __forceinline__ int key_blocks(const Params& p, int t, int (&kb)[2]) 
     return 1;
 }
 
-// per-CTA timeline for experiments (SWARM_ATTN_BWD_DBG & 4): globaltimer at fixed points of
-// thread 128 (row 0)
+// per-CTA timeline for experiments (SWARM_ATTN_BWD_DBG & 4): globaltimer at fixed points
 constexpr int kTr = 96;
 __device__ unsigned long long g_abwd_trace[256][kTr];
 __device__ __forceinline__ unsigned long long gtime() {
@@ -136,25 +110,60 @@ __device__ __forceinline__ unsigned long long gtime() {
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
     return t;
 }
-#define TR(i)                                                                            \
-    do {                                                                                 \
-        if ((p.dbg & 4) && r == 0 && blockIdx.x < 256 && (i) < kTr) g_abwd_trace[blockIdx.x][(i)] = gtime(); \
+#define TR(cond, i)                                                                                              \
+    do {                                                                                                         \
+        if ((p.dbg & 4) && (cond) && blockIdx.x < 256 && (i) < kTr) g_abwd_trace[blockIdx.x][(i)] = gtime();    \
     } while (0)
-#define TRL(i)                                                                                   \
-    do {                                                                                         \
-        if ((p.dbg & 4) && lane == 0 && blockIdx.x < 256 && (i) < kTr) g_abwd_trace[blockIdx.x][(i)] = gtime(); \
-    } while (0)
-#define TR0(i)                                                                                        \
-    do {                                                                                              \
-        if ((p.dbg & 4) && threadIdx.x == 128 && blockIdx.x < 256) g_abwd_trace[blockIdx.x][(i)] = gtime(); \
-    } while (0)
+
+// D[z*L + q] = dO[b*L + q, h*128 ..] . O[b*L + q, h*128 ..]: 16 threads per (row, head)
+__global__ void __launch_bounds__(256) k_attn_rowdot(const __nv_bfloat16* __restrict__ dO, int ld_do,
+                                                     const __nv_bfloat16* __restrict__ O, int ld_o, int B, int H,
+                                                     int L, float* __restrict__ D) {
+    pdl_trigger();
+    pdl_wait();
+    const int gid = blockIdx.x * blockDim.x + threadIdx.x;
+    const int item = gid >> 4, part = gid & 15;
+    const int rows = B * L;
+    const bool ok = item < rows * H;
+    const int row = ok ? item / H : 0, h = ok ? item - (item / H) * H : 0;
+    float acc = 0.f;
+    if (ok) {
+        const uint4 a = __ldg(reinterpret_cast<const uint4*>(dO + static_cast<size_t>(row) * ld_do + h * kDh) + part);
+        const uint4 o = __ldg(reinterpret_cast<const uint4*>(O + static_cast<size_t>(row) * ld_o + h * kDh) + part);
+        const uint32_t wa[4] = {a.x, a.y, a.z, a.w}, wo[4] = {o.x, o.y, o.z, o.w};
+#pragma unroll
+        for (int k = 0; k < 4; ++k) acc += lo(wa[k]) * lo(wo[k]) + hi(wa[k]) * hi(wo[k]);
+    }
+#pragma unroll
+    for (int off = 8; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+    if (ok && part == 0) {
+        const int b = row / L, q = row - b * L;
+        D[(static_cast<size_t>(b) * H + h) * L + q] = acc;
+    }
+}
+
+// dQ: the fp32 accumulator -> bf16 into dqkv, and back to zero for the next launch (8 columns per thread)
+__global__ void __launch_bounds__(256) k_attn_dq_out(float* __restrict__ acc, int rows, int cols,
+                                                     __nv_bfloat16* __restrict__ dqkv, int ld_dqkv) {
+    pdl_trigger();
+    pdl_wait();
+    const long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+    const int c8 = cols / 8;
+    if (i >= static_cast<long long>(rows) * c8) return;
+    const long long row = i / c8, c = (i - row * c8) * 8;
+    float4* a = reinterpret_cast<float4*>(acc + row * cols + c);
+    const float4 x = __ldcg(a), y = __ldcg(a + 1);
+    *reinterpret_cast<uint4*>(dqkv + row * ld_dqkv + c) = make_uint4(pack2(x.x, x.y), pack2(x.z, x.w), pack2(y.x, y.y), pack2(y.z, y.w));
+    __stcg(a, make_float4(0.f, 0.f, 0.f, 0.f));
+    __stcg(a + 1, make_float4(0.f, 0.f, 0.f, 0.f));
+}
 
 __global__ void __launch_bounds__(kThreads, 1)
     k_attn_bwd(const __grid_constant__ CUtensorMap tm_qkv, const __grid_constant__ CUtensorMap tm_do,
-               const __grid_constant__ CUtensorMap tm_p, const __grid_constant__ CUtensorMap tm_o,
-               const __grid_constant__ CUtensorMap tm_acc, const Params p) {
+               const __grid_constant__ CUtensorMap tm_p, const __grid_constant__ CUtensorMap tm_acc,
+               const __grid_constant__ CUtensorMap tm_out, const Params p) {
     pdl_trigger();
-    TR0(0);
+    TR(threadIdx.x == 128, 0);
     extern __shared__ uint8_t smem_raw[];
     const uint32_t raw = smem_u32(smem_raw);
     uint8_t* smem = smem_raw + ((1024 - (raw & 1023)) & 1023);
@@ -162,25 +171,24 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint8_t* sV = sK + kTile;
     uint8_t* sDO = sV + kTile;
     uint8_t* sQ = sDO + kTile;
-    uint8_t* sP = sQ + kTile;  // P_j, then dS_j in place
-    uint8_t* sO = sP + kTile;
-    uint8_t* sStg = sO + kTile;  // two dQ staging buffers
+    uint8_t* sP = sQ + kTile;    // two buffers: P_j, then dS_j in place
+    uint8_t* sStg = sP + 2 * kTile;  // two dQ staging buffers
     uint64_t* bars = reinterpret_cast<uint64_t*>(sStg + 2 * kStg);
-    uint64_t* kv_full = bars + 0;      // TMA: K_i, V_i landed
-    uint64_t* kv_free = bars + 1;      // MMA: done with K_i, V_i
-    uint64_t* ld_full = bars + 2;      // TMA: dO_j, Q_j, P_j, O_j landed
-    uint64_t* ld_free = bars + 3;      // MMA (after the rows' dS): done with dO_j, Q_j, dS_j, O_j
-    uint64_t* mma12 = bars + 4;        // dP, dV updated
-    uint64_t* ds_ready = bars + 5;     // dS rows: dS_j written (4 warps)
-    uint64_t* mma34 = bars + 6;        // dK updated, dQ_j ready
-    uint64_t* dq_free = bars + 7;      // dQ rows: dQ_j read out of TMEM (4 warps)
-    uint64_t* acc_full = bars + 8;     // dK, dV of the key block complete
-    uint64_t* acc_free = bars + 9;     // dK (dS rows) and dV (dQ rows) read out (8 warps)
+    uint64_t* kv_full = bars + 0;   // TMA: K_i, V_i landed
+    uint64_t* kv_free = bars + 1;   // dS rows: dK, dV staged through sK / sV and stored (TMA read them)
+    uint64_t* do_full = bars + 2;   // TMA: dO_j landed
+    uint64_t* do_free = bars + 3;   // MMA: done with dO_j (dP, dV issued)
+    uint64_t* q_full = bars + 4;    // TMA: Q_j landed
+    uint64_t* q_free = bars + 5;    // MMA: done with Q_j (dK issued)
+    uint64_t* p_full = bars + 6;    // [2] TMA: P_j landed in buffer j % 2
+    uint64_t* p_free = bars + 8;    // [2] MMA: done with dS_j in buffer j % 2
+    uint64_t* mma12 = bars + 10;    // dP, dV updated
+    uint64_t* ds_ready = bars + 11; // dS rows: dS_j written (4 warps)
+    uint64_t* mma34 = bars + 12;    // dK updated, dQ_j ready
+    uint64_t* dq_free = bars + 13;  // dQ rows: dQ_j read out of TMEM (4 warps)
+    uint64_t* acc_full = bars + 14; // dK, dV of the key block complete
+    uint64_t* acc_free = bars + 15; // dS rows: dK, dV read out (4 warps)
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + kBars);
-    int* last_flag = reinterpret_cast<int*>(tmem_slot + 1);
-    // dQ rows -> converter: per block, whether this CTA was the last to add to its query block
-    volatile int* conv_posted = reinterpret_cast<volatile int*>(tmem_slot + 2);
-    int* conv_flag = reinterpret_cast<int*>(tmem_slot + 4);  // [kMaxBlocks]
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int nz = p.B * p.H, nqb = p.L / kBlk;
@@ -188,19 +196,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int zb = z / p.H, zh = z - zb * p.H;
     int kbs[2] = {0, 0};
     const int nk = key_blocks(p, t, kbs);
+    auto j0 = [&](int ti) { return p.causal ? kbs[ti] : 0; };
 
     if (warp == 0 && lane == 0) {
-        mbar_init(kv_full, 1);
-        mbar_init(kv_free, 1);
-        mbar_init(ld_full, 1);
-        mbar_init(ld_free, 1);
-        mbar_init(mma12, 1);
-        mbar_init(ds_ready, 4);
-        mbar_init(mma34, 1);
-        mbar_init(dq_free, 4);
-        mbar_init(acc_full, 1);
-        mbar_init(acc_free, 8);
-        *conv_posted = 0;
+        for (int i = 0; i < 16; ++i) mbar_init(bars + i, (i == 11 || i == 13 || i == 15) ? 4 : 1);
         fence_barrier_init();
     }
     if (warp == 2) {
@@ -211,48 +210,53 @@ __global__ void __launch_bounds__(kThreads, 1)
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
-                TR0(1);
+    TR(threadIdx.x == 128, 1);
     pdl_wait();
 
     if (warp == 0) {
         if (lane == 0) {
             // ------------------------------------------------------------ TMA
+            const int qcol = p.q_col0 + zh * kDh;
+            auto qrow = [&](int j) { return zb * p.L + j * kBlk; };
+            // everything this CTA reads after its first block, to L2 now (in order of use)
+            if (nk == 2)
+                for (int b = 0; b < 2; ++b) {
+                    tma_prefetch_l2(&tm_qkv, p.k_col0 + zh * kDh + 64 * b, qrow(kbs[1]));
+                    tma_prefetch_l2(&tm_qkv, p.v_col0 + zh * kDh + 64 * b, qrow(kbs[1]));
+                }
+            for (int ti = 0; ti < nk; ++ti)
+                for (int j = j0(ti) + (ti == 0); j < nqb; ++j)
+                    for (int b = 0; b < 2; ++b) {
+                        tma_prefetch_l2(&tm_p, kbs[ti] * kBlk + 64 * b, z * p.L + j * kBlk);
+                        if (ti == 0) {
+                            tma_prefetch_l2(&tm_do, zh * kDh + 64 * b, qrow(j));
+                            tma_prefetch_l2(&tm_qkv, qcol + 64 * b, qrow(j));
+                        }
+                    }
             int n = 0;
             for (int ti = 0; ti < nk; ++ti) {
                 const int kb = kbs[ti];
                 if (ti > 0) mbar_wait(kv_free, (ti - 1) & 1);
-                if (ti > 0) TRL(90);
                 mbar_arrive_expect_tx(kv_full, 2 * kTile);
-                const int krow = zb * p.L + kb * kBlk;
                 for (int b = 0; b < 2; ++b) {
-                    tma_load_2d(sK + b * kBox, &tm_qkv, kv_full, p.k_col0 + zh * kDh + 64 * b, krow);
-                    tma_load_2d(sV + b * kBox, &tm_qkv, kv_full, p.v_col0 + zh * kDh + 64 * b, krow);
+                    tma_load_2d(sK + b * kBox, &tm_qkv, kv_full, p.k_col0 + zh * kDh + 64 * b, qrow(kb));
+                    tma_load_2d(sV + b * kBox, &tm_qkv, kv_full, p.v_col0 + zh * kDh + 64 * b, qrow(kb));
                 }
-                if (ti == 0 && nk == 2)  // the second key block's K, V: to L2 now, to smem at the switch
-                    for (int b = 0; b < 2; ++b) {
-                        const int krow2 = zb * p.L + kbs[1] * kBlk;
-                        tma_prefetch_l2(&tm_qkv, p.k_col0 + zh * kDh + 64 * b, krow2);
-                        tma_prefetch_l2(&tm_qkv, p.v_col0 + zh * kDh + 64 * b, krow2);
-                    }
-                for (int j = p.causal ? kb : 0; j < nqb; ++j, ++n) {
-                    if (j + 1 < nqb)  // the next query block's tiles to L2 while this one computes
-                        for (int b = 0; b < 2; ++b) {
-                            const int qrow2 = zb * p.L + (j + 1) * kBlk;
-                            tma_prefetch_l2(&tm_do, zh * kDh + 64 * b, qrow2);
-                            tma_prefetch_l2(&tm_qkv, p.q_col0 + zh * kDh + 64 * b, qrow2);
-                            tma_prefetch_l2(&tm_p, kb * kBlk + 64 * b, z * p.L + (j + 1) * kBlk);
-                            tma_prefetch_l2(&tm_o, zh * kDh + 64 * b, qrow2);
-                        }
-                    if (n > 0) mbar_wait(ld_free, (n - 1) & 1);
-                    if (ti > 0) TRL(91);
-                    mbar_arrive_expect_tx(ld_full, 4 * kTile);
-                    const int qrow = zb * p.L + j * kBlk;
-                    for (int b = 0; b < 2; ++b) {
-                        tma_load_2d(sDO + b * kBox, &tm_do, ld_full, zh * kDh + 64 * b, qrow);
-                        tma_load_2d(sQ + b * kBox, &tm_qkv, ld_full, p.q_col0 + zh * kDh + 64 * b, qrow);
-                        tma_load_2d(sP + b * kBox, &tm_p, ld_full, kb * kBlk + 64 * b, z * p.L + j * kBlk);
-                        tma_load_2d(sO + b * kBox, &tm_o, ld_full, zh * kDh + 64 * b, qrow);
-                    }
+                for (int j = j0(ti); j < nqb; ++j, ++n) {
+                    // dO_j once dP, dV of the previous block are issued; P_j into the buffer block n-2
+                    // used; Q_j once the previous dK is issued (needed only after this block's dS)
+                    if (n > 0) mbar_wait(do_free, (n - 1) & 1);
+                    mbar_arrive_expect_tx(do_full, kTile);
+                    for (int b = 0; b < 2; ++b) tma_load_2d(sDO + b * kBox, &tm_do, do_full, zh * kDh + 64 * b, qrow(j));
+                    const int pb = n & 1;
+                    if (n > 1) mbar_wait(&p_free[pb], ((n >> 1) - 1) & 1);
+                    mbar_arrive_expect_tx(&p_full[pb], kTile);
+                    for (int b = 0; b < 2; ++b)
+                        tma_load_2d(sP + pb * kTile + b * kBox, &tm_p, &p_full[pb], kb * kBlk + 64 * b,
+                                    z * p.L + j * kBlk);
+                    if (n > 0) mbar_wait(q_free, (n - 1) & 1);
+                    mbar_arrive_expect_tx(q_full, kTile);
+                    for (int b = 0; b < 2; ++b) tma_load_2d(sQ + b * kBox, &tm_qkv, q_full, qcol + 64 * b, qrow(j));
                 }
             }
         }
@@ -262,37 +266,34 @@ __global__ void __launch_bounds__(kThreads, 1)
             constexpr uint32_t id_kk = make_idesc_bf16(kBlk, kDh, false, false);
             constexpr uint32_t id_mm = make_idesc_bf16(kBlk, kDh, true, true);
             constexpr uint32_t id_km = make_idesc_bf16(kBlk, kDh, false, true);
-            const uint32_t aK = smem_u32(sK), aV = smem_u32(sV), aDO = smem_u32(sDO), aQ = smem_u32(sQ),
-                           aP = smem_u32(sP);
+            const uint32_t aK = smem_u32(sK), aV = smem_u32(sV), aDO = smem_u32(sDO), aQ = smem_u32(sQ);
             // K-major operand: k-step kk (16 columns) sits in box kk/4 at +32 B per step; MN-major
             // operand: k-step kk is rows 16kk.. (+2048 B), the two 64-wide MN chunks one box apart
             auto kmaj = [](uint32_t base, int kk) { return make_sdesc(base + (kk >> 2) * kBox + (kk & 3) * 32, 16, 1024); };
             auto mnmaj = [](uint32_t base, int kk) { return make_sdesc(base + kk * 2048, kBox, 1024); };
             int n = 0;
             for (int ti = 0; ti < nk; ++ti) {
-                const int kb = kbs[ti];
                 mbar_wait(kv_full, ti & 1);
-                if (ti > 0) TRL(92);
                 if (ti > 0) mbar_wait(acc_free, (ti - 1) & 1);  // the previous key block's dK, dV were read out
-                if (ti > 0) TRL(93);
                 tc_fence_after();
-                for (int j = p.causal ? kb : 0, jj = 0; j < nqb; ++j, ++jj, ++n) {
-                    mbar_wait(ld_full, n & 1);
-                    TRL(8 + 9 * n + 5);
+                for (int j = j0(ti), jj = 0; j < nqb; ++j, ++jj, ++n) {
+                    const int pb = n & 1;
+                    const uint32_t aP = smem_u32(sP + pb * kTile);
+                    mbar_wait(do_full, n & 1);
+                    mbar_wait(&p_full[pb], (n >> 1) & 1);
                     tc_fence_after();
                     for (int kk = 0; kk < kDh / 16; ++kk)  // dP = dO_j V_i^T (K = d_head)
                         mma_bf16(tmem + kColDP, kmaj(aDO, kk), kmaj(aV, kk), id_kk, kk != 0 ? 1u : 0u);
                     for (int kk = 0; kk < kBlk / 16; ++kk)  // dV += P_j^T dO_j (K = queries)
                         mma_bf16(tmem + kColDV, mnmaj(aP, kk), mnmaj(aDO, kk), id_mm, (jj | kk) != 0 ? 1u : 0u);
                     mma_commit(mma12);
-                    if (p.dbg & 4) {
-                        mbar_wait(mma12, n & 1);
-                        TRL(8 + 9 * n + 7);
-                    }
+                    mma_commit(do_free);
                     mbar_wait(ds_ready, n & 1);
+                    mbar_wait(q_full, n & 1);
                     tc_fence_after();
                     for (int kk = 0; kk < kBlk / 16; ++kk)  // dK += dS_j^T Q_j (K = queries)
                         mma_bf16(tmem + kColDK, mnmaj(aP, kk), mnmaj(aQ, kk), id_mm, (jj | kk) != 0 ? 1u : 0u);
+                    mma_commit(q_free);
                     if (n > 0) {
                         mbar_wait(dq_free, (n - 1) & 1);
                         tc_fence_after();
@@ -300,45 +301,12 @@ __global__ void __launch_bounds__(kThreads, 1)
                     for (int kk = 0; kk < kBlk / 16; ++kk)  // dQ_j = dS_j K_i (K = keys)
                         mma_bf16(tmem + kColDQ, kmaj(aP, kk), mnmaj(aK, kk), id_km, kk != 0 ? 1u : 0u);
                     mma_commit(mma34);
-                    mma_commit(ld_free);
-                    if (p.dbg & 4) {
-                        mbar_wait(mma34, n & 1);
-                        TRL(8 + 9 * n + 8);
-                    }
+                    mma_commit(&p_free[pb]);
+                    TR(true, 8 + 9 * n + 5);
                 }
-                mma_commit(acc_full);
-                mma_commit(kv_free);
+                mma_commit(acc_full);  // (every MMA reading K_i, V_i is complete too)
             }
         }
-    } else if (warp == 2 || warp == 3) {
-        // ------------------------------------------------ converter: dQ_j fp32 -> bf16 (+ re-zero)
-        // for the query blocks this CTA completed last; coalesced, warp w rows 64(w-2).., lane l
-        // columns 4l..4l+3
-        int n = 0;
-        for (int ti = 0; ti < nk; ++ti)
-            for (int j = p.causal ? kbs[ti] : 0; j < nqb; ++j, ++n) {
-                while (*conv_posted <= n) __nanosleep(64);
-                __threadfence_block();
-                if (!conv_flag[n] || (p.dbg & 2)) continue;
-                const size_t row0 = static_cast<size_t>(zb) * p.L + j * kBlk + 64 * (warp - 2);
-                float* a0 = p.dq_acc + row0 * p.ld_acc + zh * kDh + 4 * lane;
-                __nv_bfloat16* o0 = p.dqkv + row0 * p.ld_dqkv + p.dq_col0 + zh * kDh + 4 * lane;
-#pragma unroll 1
-                for (int hh = 0; hh < 4; ++hh) {
-                    float4 x[16];
-#pragma unroll
-                    for (int i = 0; i < 16; ++i)
-                        x[i] = __ldcg(reinterpret_cast<const float4*>(a0 + static_cast<size_t>(16 * hh + i) * p.ld_acc));
-#pragma unroll
-                    for (int i = 0; i < 16; ++i) {
-                        const size_t rr = 16 * hh + i;
-                        *reinterpret_cast<uint2*>(o0 + rr * p.ld_dqkv) = make_uint2(pack2(x[i].x, x[i].y), pack2(x[i].z, x[i].w));
-                        __stcg(reinterpret_cast<float4*>(a0 + rr * p.ld_acc), make_float4(0.f, 0.f, 0.f, 0.f));
-                    }
-                }
-                asm volatile("bar.sync 2, 64;" ::: "memory");
-                if (warp == 2 && lane == 0) p.counters[z * nqb + j] = 0;
-            }
     } else if (warp >= 4 && warp < 8) {
         // ------------------------------------------------ dS rows: one query row per thread
         const int r = (warp - 4) * 32 + lane;
@@ -346,38 +314,21 @@ __global__ void __launch_bounds__(kThreads, 1)
         int n = 0;
         for (int ti = 0; ti < nk; ++ti) {
             const int kb = kbs[ti];
-            for (int j = p.causal ? kb : 0; j < nqb; ++j, ++n) {
-                // D = dO_j[r] . O_j[r] (both rows from shared memory) while the MMAs run
-                mbar_wait(ld_full, n & 1);
-                float D = 0.f;
-#pragma unroll
-                for (int b = 0; b < 2; ++b) {
-                    const uint32_t ra = smem_u32(sDO + b * kBox) + r * 128, rb = smem_u32(sO + b * kBox) + r * 128;
-#pragma unroll
-                    for (int c = 0; c < 8; ++c) {
-                        uint32_t a[4], o[4];
-                        const uint32_t off = (c ^ (r & 7)) << 4;
-                        asm volatile("ld.shared.v4.b32 {%0,%1,%2,%3}, [%4];"
-                                     : "=r"(a[0]), "=r"(a[1]), "=r"(a[2]), "=r"(a[3])
-                                     : "r"(ra + off));
-                        asm volatile("ld.shared.v4.b32 {%0,%1,%2,%3}, [%4];"
-                                     : "=r"(o[0]), "=r"(o[1]), "=r"(o[2]), "=r"(o[3])
-                                     : "r"(rb + off));
-#pragma unroll
-                        for (int k = 0; k < 4; ++k) D += lo(a[k]) * lo(o[k]) + hi(a[k]) * hi(o[k]);
-                    }
-                }
-                // dS_j row r = scale * P * (dP - D) over P in place
+            for (int j = j0(ti); j < nqb; ++j, ++n) {
+                const int pb = n & 1;
+                const float D = __ldg(p.D + static_cast<size_t>(z) * p.L + j * kBlk + r);
+                mbar_wait(&p_full[pb], (n >> 1) & 1);  // (TMA writes visible to these threads)
                 mbar_wait(mma12, n & 1);
-                TR(8 + 9 * n + 0);
+                TR(r == 0, 8 + 9 * n + 0);
                 tc_fence_after();
+                // dS_j row r = scale * P * (dP - D) over P in place
 #pragma unroll
                 for (int h = 0; h < 2; ++h) {
                     uint32_t ra[32], rb[32];
                     tmem_ld_32x32b_x32(trow + kColDP + 64 * h, ra);
                     tmem_ld_32x32b_x32(trow + kColDP + 64 * h + 32, rb);
                     tmem_ld_wait();
-                    const uint32_t prow = smem_u32(sP + h * kBox) + r * 128;
+                    const uint32_t prow = smem_u32(sP + pb * kTile + h * kBox) + r * 128;
 #pragma unroll
                     for (int k = 0; k < 8; ++k) {
                         const uint32_t addr = prow + ((k ^ (r & 7)) << 4);
@@ -403,29 +354,59 @@ __global__ void __launch_bounds__(kThreads, 1)
                 tc_fence_before();
                 __syncwarp();
                 if (lane == 0) mbar_arrive(ds_ready);
-                TR(8 + 9 * n + 1);
+                TR(r == 0, 8 + 9 * n + 1);
             }
-            // dK rows of key block kb
+            // dK, dV of key block kb: TMEM -> bf16 rows over K_i / V_i in shared memory (the key
+            // block's MMAs are complete) -> TMA stores; then the next K, V may load there
             mbar_wait(acc_full, ti & 1);
-            TR(2 + 2 * ti);
+            TR(r == 0, 2 + 2 * ti);
             tc_fence_after();
-            const size_t krow = static_cast<size_t>(zb) * p.L + kb * kBlk + r;
-            tmem_row_to_bf16(trow + kColDK, p.dqkv + krow * p.ld_dqkv + p.dk_col0 + zh * kDh);
+#pragma unroll
+            for (int g = 0; g < 2; ++g) {
+                uint32_t v[4][32];
+#pragma unroll
+                for (int c = 0; c < 4; ++c) tmem_ld_32x32b_x32(trow + (g ? kColDV : kColDK) + 32 * c, v[c]);
+                tmem_ld_wait();
+                uint8_t* dst = g ? sV : sK;
+#pragma unroll
+                for (int c = 0; c < 4; ++c)
+#pragma unroll
+                    for (int w = 0; w < 4; ++w) {
+                        const int k16 = 4 * c + w;  // 16-B piece of the 256-B row: box k16 / 8, piece k16 % 8
+                        const uint32_t addr = smem_u32(dst + (k16 >> 3) * kBox) + r * 128 + (((k16 & 7) ^ (r & 7)) << 4);
+                        st_shared_v4(addr, pack2(__uint_as_float(v[c][8 * w]), __uint_as_float(v[c][8 * w + 1])),
+                                     pack2(__uint_as_float(v[c][8 * w + 2]), __uint_as_float(v[c][8 * w + 3])),
+                                     pack2(__uint_as_float(v[c][8 * w + 4]), __uint_as_float(v[c][8 * w + 5])),
+                                     pack2(__uint_as_float(v[c][8 * w + 6]), __uint_as_float(v[c][8 * w + 7])));
+                    }
+            }
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(acc_free);
-            TR(3 + 2 * ti);
+            fence_async_smem();
+            asm volatile("bar.sync 3, 128;" ::: "memory");
+            if (r == 0) {
+                const int krow = zb * p.L + kb * kBlk;
+                for (int b = 0; b < 2; ++b) {
+                    tma_store_2d(&tm_out, sK + b * kBox, p.dk_col0 + zh * kDh + 64 * b, krow);
+                    tma_store_2d(&tm_out, sV + b * kBox, p.dv_col0 + zh * kDh + 64 * b, krow);
+                }
+                bulk_commit();
+                bulk_wait_read<0>();
+                mbar_arrive(kv_free);
+                if (ti == nk - 1) bulk_wait_all();
+            }
+            TR(r == 0, 3 + 2 * ti);
         }
     } else if (warp >= 8) {
         // ------------------------------------------------ dQ rows (off the dS critical path)
         const int r = (warp - 8) * 32 + lane;
         const uint32_t trow = tmem + (static_cast<uint32_t>((warp & 3) * 32) << 16);
         int n = 0;
-        for (int ti = 0; ti < nk; ++ti) {
-            const int kb = kbs[ti];
-            for (int j = p.causal ? kb : 0; j < nqb; ++j, ++n) {
+        for (int ti = 0; ti < nk; ++ti)
+            for (int j = j0(ti); j < nqb; ++j, ++n) {
                 mbar_wait(mma34, n & 1);
-                TR(8 + 9 * n + 2);
+                TR(r == 0, 8 + 9 * n + 2);
                 tc_fence_after();
                 uint32_t v[4][32];
 #pragma unroll
@@ -436,62 +417,33 @@ __global__ void __launch_bounds__(kThreads, 1)
                 if (lane == 0) mbar_arrive(dq_free);  // the next dQ MMA may overwrite TMEM now
                 // dQ_j -> the fp32 accumulator by TMA reduce-add, 32 columns at a time through two
                 // SWIZZLE_128B staging buffers (16-B piece k of row r at k ^ (r & 7))
-                if (!(p.dbg & 1)) {
 #pragma unroll
-                    for (int c = 0; c < 4; ++c) {
-                        uint8_t* stg = sStg + (c & 1) * kStg;
-                        if (c >= 2) {
-                            if (r == 0) bulk_wait_read<1>();  // the reduce issued from this buffer has read it
-                            dq_bar();
-                        } else if (c == 0 && n > 0) {
-                            dq_bar();  // row 0 has waited for the previous block's reduces (bulk wait below)
-                        }
-                        const uint32_t row = smem_u32(stg) + r * 128;
-#pragma unroll
-                        for (int k = 0; k < 8; ++k)
-                            st_shared_v4(row + ((k ^ (r & 7)) << 4), v[c][4 * k], v[c][4 * k + 1], v[c][4 * k + 2],
-                                         v[c][4 * k + 3]);
-                        fence_async_smem();
+                for (int c = 0; c < 4; ++c) {
+                    uint8_t* stg = sStg + (c & 1) * kStg;
+                    if (n > 0 || c >= 2) {
+                        if (r == 0) bulk_wait_read<1>();  // the reduce issued from this buffer has read it
                         dq_bar();
-                        if (r == 0) {
-                            tma_reduce_add_2d(&tm_acc, stg, zh * kDh + 32 * c, zb * p.L + j * kBlk);
-                            bulk_commit();
-                        }
+                    }
+                    const uint32_t row = smem_u32(stg) + r * 128;
+#pragma unroll
+                    for (int k = 0; k < 8; ++k)
+                        st_shared_v4(row + ((k ^ (r & 7)) << 4), v[c][4 * k], v[c][4 * k + 1], v[c][4 * k + 2],
+                                     v[c][4 * k + 3]);
+                    fence_async_smem();
+                    dq_bar();
+                    if (r == 0) {
+                        if (!(p.dbg & 1)) tma_reduce_add_2d(&tm_acc, stg, zh * kDh + 32 * c, zb * p.L + j * kBlk);
+                        bulk_commit();
                     }
                 }
-                TR(8 + 9 * n + 3);
-                // the last key block to add to query block j converts dQ_j to bf16 and re-zeroes it:
-                // the reduces complete (bulk wait), one gpu-scope fence, the arrival
-                int* cnt = p.counters + z * nqb + j;
-                if (r == 0) {
-                    bulk_wait_all();
-                    const int need = p.causal ? j + 1 : nqb;
-                    __threadfence();
-                    const int last = atomicAdd(cnt, 1) == need - 1;
-                    if (last) __threadfence();
-                    *last_flag = last;
-                }
-                TR(8 + 9 * n + 4);
-                if (r == 0) {
-                    conv_flag[n] = *last_flag;
-                    __threadfence_block();
-                    *conv_posted = n + 1;
-                }
+                TR(r == 0, 8 + 9 * n + 3);
             }
-            // dV rows of key block kb
-            mbar_wait(acc_full, ti & 1);
-            tc_fence_after();
-            const size_t krow = static_cast<size_t>(zb) * p.L + kb * kBlk + r;
-            tmem_row_to_bf16(trow + kColDV, p.dqkv + krow * p.ld_dqkv + p.dv_col0 + zh * kDh);
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) mbar_arrive(acc_free);
-        }
+        if (r == 0) bulk_wait_all();  // the reduces complete before the CTA retires
     }
-    TR0(6);
+    TR(threadIdx.x == 128, 6);
     tc_fence_before();
     __syncthreads();
-    TR0(7);
+    TR(threadIdx.x == 128, 7);
     if (warp == 2) {
         tc_fence_after();
         tmem_dealloc(tmem, 512);
@@ -525,16 +477,15 @@ int map_f32(CUtensorMap* m, const void* ptr, long long rows, long long cols) {
     return SWARM_OK;
 }
 
-int launch(const Params& p, const void* qkv, int ld_qkv, int qkv_cols, const void* dO, int ld_do, const void* P,
-           cudaStream_t st) {
-    // (O's tensor map is built from p.o / p.ld_o)
+int launch(const Params& p, const void* qkv, int ld_qkv, int qkv_cols, const void* dO, int ld_do, const void* O,
+           int ld_o, const void* P, cudaStream_t st) {
     using swarm::attn::map_bf16;
     const long long T = static_cast<long long>(p.B) * p.L, rows_p = static_cast<long long>(p.B) * p.H * p.L;
-    CUtensorMap tq, td, tp, to, ta;
+    CUtensorMap tq, td, tp, ta, tout;
     if (map_bf16(&tq, qkv, T, qkv_cols, ld_qkv, 64, kBlk, CU_TENSOR_MAP_SWIZZLE_128B) ||
         map_bf16(&td, dO, T, static_cast<long long>(p.H) * kDh, ld_do, 64, kBlk, CU_TENSOR_MAP_SWIZZLE_128B) ||
         map_bf16(&tp, P, rows_p, p.L, p.L, 64, kBlk, CU_TENSOR_MAP_SWIZZLE_128B) ||
-        map_bf16(&to, p.o, T, static_cast<long long>(p.H) * kDh, p.ld_o, 64, kBlk, CU_TENSOR_MAP_SWIZZLE_128B))
+        map_bf16(&tout, p.dqkv, T, p.ld_dqkv, p.ld_dqkv, 64, kBlk, CU_TENSOR_MAP_SWIZZLE_128B))
         return invalid("attention backward: tensor map encoding failed");
     if (map_f32(&ta, p.dq_acc, T, p.ld_acc))
         return invalid("attention backward: tensor map encoding failed (dQ accumulator)");
@@ -543,10 +494,21 @@ int launch(const Params& p, const void* qkv, int ld_qkv, int qkv_cols, const voi
         SWARM_CUDA_TRY(cudaFuncSetAttribute(k_attn_bwd, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem));
         attr = true;
     }
+    const long long items = T * p.H * 16;
+    launch_pdl(k_attn_rowdot, dim3(static_cast<unsigned>((items + 255) / 256)), dim3(256), 0, st,
+               static_cast<const __nv_bfloat16*>(dO), ld_do, static_cast<const __nv_bfloat16*>(O), ld_o, p.B, p.H,
+               p.L, const_cast<float*>(p.D));
+    SWARM_LAUNCH_CHECK("k_attn_rowdot");
     const int nkb = p.L / kBlk;
     const int per_z = p.causal ? (nkb + 1) / 2 : nkb;
-    k_attn_bwd<<<p.B * p.H * per_z, kThreads, kSmem, st>>>(tq, td, tp, to, ta, p);
+    k_attn_bwd<<<p.B * p.H * per_z, kThreads, kSmem, st>>>(tq, td, tp, ta, tout, p);
     SWARM_LAUNCH_CHECK("k_attn_bwd");
+    if (!(p.dbg & 2)) {
+        const long long n8 = T * p.ld_acc / 8;
+        launch_pdl(k_attn_dq_out, dim3(static_cast<unsigned>((n8 + 255) / 256)), dim3(256), 0, st, p.dq_acc,
+                   static_cast<int>(T), p.ld_acc, p.dqkv + p.dq_col0, p.ld_dqkv);
+        SWARM_LAUNCH_CHECK("k_attn_dq_out");
+    }
     return SWARM_OK;
 }
 
@@ -569,8 +531,7 @@ int swarm_debug_abwd_trace(uint64_t* host, int n_ctas) {
 size_t swarm_attn_backward_workspace(int B, int H, int L, int d_head) {
     if (B <= 0 || H <= 0 || L <= 0 || d_head <= 0) return 0;
     const size_t acc = static_cast<size_t>(B) * L * H * d_head * sizeof(float);
-    const size_t cnt = static_cast<size_t>(B) * H * ((L + 127) / 128) * sizeof(int);
-    return acc + ((cnt + 255) / 256) * 256;
+    return acc + static_cast<size_t>(B) * H * L * sizeof(float);  // + D
 }
 
 int swarm_attn_backward(const void* dO, int ld_do, const void* qkv, int ld_qkv, int qkv_cols, int k_col0, int v_col0,
@@ -597,12 +558,9 @@ int swarm_attn_backward(const void* dO, int ld_do, const void* qkv, int ld_qkv, 
     p.q_col0 = 0;
     p.k_col0 = k_col0;
     p.v_col0 = v_col0;
-    p.o = static_cast<const __nv_bfloat16*>(O);
-    p.ld_o = ld_o;
     p.dq_acc = static_cast<float*>(workspace);
     p.ld_acc = H * kDh;
-    p.counters = reinterpret_cast<int*>(static_cast<char*>(workspace) +
-                                        static_cast<size_t>(B) * L * H * kDh * sizeof(float));
+    p.D = reinterpret_cast<const float*>(static_cast<char*>(workspace) + static_cast<size_t>(B) * L * H * kDh * sizeof(float));
     p.dqkv = static_cast<__nv_bfloat16*>(dqkv);
     p.ld_dqkv = ld_dqkv;
     p.dq_col0 = 0;
@@ -613,7 +571,7 @@ int swarm_attn_backward(const void* dO, int ld_do, const void* qkv, int ld_qkv, 
         return e ? atoi(e) : 0;
     }();
     p.dbg = dbg;
-    return launch(p, qkv, ld_qkv, qkv_cols, dO, ld_do, P, swarm::as_stream(stream));
+    return launch(p, qkv, ld_qkv, qkv_cols, dO, ld_do, O, ld_o, P, swarm::as_stream(stream));
 }
 
 }  // extern "C"

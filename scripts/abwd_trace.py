@@ -33,6 +33,5 @@ for c in (0, 1, 64, 127):
     print(f"CTA {c}: setup {rel[c,1]:.1f}")
     for blk in range(5):
         v = rel[c, 8 + 9 * blk:17 + 9 * blk]
-        print(f"   blk {blk}: ld_full {v[5]:.1f} D {v[6]:.1f} | mma12 {v[7]:.1f}/{v[0]:.1f} ds {v[1]:.1f} mma34 {v[8]:.1f}/{v[2]:.1f} dq_out {v[3]:.1f} cnt {v[4]:.1f}")
-    print(f"   switch: producer kv_free {rel[c,90]:.1f} ld_free {rel[c,91]:.1f} | mma kv_full {rel[c,92]:.1f} acc_free {rel[c,93]:.1f}")
-    print(f"   kb0 acc {rel[c,2]:.1f} out {rel[c,3]:.1f}  kb1 acc {rel[c,4]:.1f} out {rel[c,5]:.1f}  end {rel[c,6]:.1f}")
+        print(f"   blk {blk}: dS-rows mma12 {v[0]:.1f} ds {v[1]:.1f} | mma34 issued {v[5]:.1f} | dQ-rows mma34 {v[2]:.1f} reduces {v[3]:.1f} counter {v[4]:.1f}")
+    print(f"   kb0 acc {rel[c,2]:.1f} out {rel[c,3]:.1f}  kb1 acc {rel[c,4]:.1f} out {rel[c,5]:.1f}  end {rel[c,6]:.1f} exit {rel[c,7]:.1f}")
