@@ -730,7 +730,7 @@ def bench_train(args, world, rank, local):
 
 # ----------------------------------------------------------------- engine
 def run_engine(args, world, rank, local, model: str, S: int, steps: int, warmup: int, *, fp32: bool = False,
-               profile: bool = True, e2e_steps: int = 3) -> dict:
+               profile: bool = True, e2e_steps: int = 5) -> dict:
     """asynchronous SWARM training driven by the reference's event
     engine (csrc/engine.cpp, decision-identical to sim::run) and executed by the C++
     host driver (csrc/driver.cpp): trainers keep one microbatch each in flight, peers
@@ -835,6 +835,7 @@ def run_engine(args, world, rank, local, model: str, S: int, steps: int, warmup:
         torch.cuda.synchronize()
         w0 = time.perf_counter()
         e2e_done = 0
+        cap0 = ex.counters()["captures"]
         rd = torch.cuda.Stream()  # a torch-owned stream reads the loss (the driver's streams die with it)
         for _ in range(e2e_steps):
             e2e_done += ex.run(M)
@@ -848,6 +849,7 @@ def run_engine(args, world, rank, local, model: str, S: int, steps: int, warmup:
         ex.use_host_pool(False)
         res["e2e"] = {"value": e2e_done * mcfg.tokens / e2e_s, "unit": "tokens/s",
                       "h2d_bytes_per_step": int(M * mcfg.tokens * 4 * 2), "d2h_bytes_per_step": 4,
+                      "steps": e2e_steps, "graph_captures_in_timed_region": ex.counters()["captures"] - cap0,
                       "path": "EngineExecutor.run (C++ driver) with each microbatch's tokens / targets copied from "
                               "pinned host memory by its consuming visit and the loss read back after every step "
                               "(wall clock, max over ranks)"}

@@ -34,3 +34,12 @@ for name, fn, nbytes in (("fwd", fwd, 4 * rows * cols), ("bwd", bwd, 8 * rows * 
     e0.record(); graph.replay(); e1.record(); torch.cuda.synchronize()
     us = e0.elapsed_time(e1) / 20 * 1e3
     print(f"ln {name}: {us:.2f} us/call, {nbytes / us / 1e3:.0f} GB/s algorithmic", flush=True)
+    # cold: every call behind a 256 MB L2 flush (the in-step case: x comes from DRAM)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    tot = 0.0
+    for _ in range(20):
+        flush.zero_()
+        e0, e1 = torch.cuda.Event(True), torch.cuda.Event(True)
+        e0.record(); fn(torch.cuda.current_stream().cuda_stream); e1.record(); torch.cuda.synchronize()
+        tot += e0.elapsed_time(e1)
+    print(f"ln {name} (L2 flushed): {tot / 20 * 1e3:.2f} us/call", flush=True)
