@@ -783,6 +783,7 @@ def run_engine(args, world, rank, local, model: str, S: int, steps: int, warmup:
     torch.cuda.synchronize()
     n0 = ex.kernels_launched()
     v0, r0, t_0, c0 = ex.engine.summary()["now"], ex.records, ex.optimizer_steps, ex.captures
+    tick0 = ex.tick_time()
     t0 = torch.cuda.Event(enable_timing=True)
     t1 = torch.cuda.Event(enable_timing=True)
     t0.record(stream)
@@ -794,6 +795,8 @@ def run_engine(args, world, rank, local, model: str, S: int, steps: int, warmup:
     barrier(world)
     clocks = clk.stop()
     launches = int(ex.kernels_launched() - n0)
+    tick1 = ex.tick_time()
+    local_peers = sum(1 for pid in range(ex.n_peers) if ex.peer_info(pid)["alive"] and ex.peer_info(pid)["rank"] == rank)
     ms_rank = t0.elapsed_time(t1)
     ms = max_over_ranks(ms_rank, world)
     tokens = done * mcfg.tokens
@@ -818,6 +821,12 @@ def run_engine(args, world, rank, local, model: str, S: int, steps: int, warmup:
                    "optimizer": "AdamW (fused, fp32 master), paired weight gradients" + (
                        ", delayed parameter updates (tick all-reduce + AdamW overlapped with the next interval)"
                        if getattr(args, "dpu", False) else ""),
+                   "tick_cost": {"ms_per_step_per_peer_stream": (tick1[0] - tick0[0]) / steps / max(local_peers, 1),
+                                 "share_of_step": (tick1[0] - tick0[0]) / steps / max(local_peers, 1) / (ms_rank / steps),
+                                 "stretches": tick1[1] - tick0[1], "local_peer_streams": local_peers,
+                                 "what": "GPU time a peer's compute stream spends in a tick (gradient sum, NCCL "
+                                         "all-reduce, AdamW) or, with DPU, blocked at the first visit after one "
+                                         "(rank 0)"},
                    "mean_loss": float(loss.item()) / max(tokens, 1),
                    "model_tflops_per_s": value * mcfg.flops_per_token(S) / 1e12,
                    "model_flops_per_token": mcfg.flops_per_token(S)},

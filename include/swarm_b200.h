@@ -616,6 +616,11 @@ swarm_stage_t swarm_driver_stage(swarm_driver_t d, int peer); /* NULL when the p
 swarm_stream_t swarm_driver_peer_stream(swarm_driver_t d, int peer);
 swarm_engine_t swarm_driver_engine(swarm_driver_t d);
 int swarm_driver_stats(swarm_driver_t d, swarm_driver_counters* stats);
+/* Tick cost on this rank's compute streams, cumulative: the GPU time (ms) the peers' streams spent
+ * in a tick (the stage gradient sum + all-reduce + AdamW on the lead's stream, the stage-mates
+ * waiting for it) or, with dpu, blocked at the first visit after a tick on that bank's update;
+ * `spans` = the number of such stretches.  Waits for the GPU to reach the last one. */
+int swarm_driver_tick_time(swarm_driver_t d, double* ms, uint64_t* spans);
 int swarm_driver_visit_log(swarm_driver_t d, size_t i, uint32_t* trainer, uint64_t* microbatch, uint32_t* stage,
                            int* backward, int64_t* peer);
 int swarm_driver_peer_of_rank(swarm_driver_t d, int peer); /* the rank hosting `peer` */

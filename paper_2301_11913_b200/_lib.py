@@ -194,6 +194,7 @@ SIGNATURES = {
     "swarm_driver_stage": (P, [P, I]),
     "swarm_driver_peer_stream": (P, [P, I]),
     "swarm_driver_engine": (P, [P]),
+    "swarm_driver_tick_time": (I, [P, C.POINTER(C.c_double), C.POINTER(C.c_uint64)]),
     "swarm_driver_stats": (I, [P, C.POINTER(DriverCounters)]),
     "swarm_driver_visit_log": (I, [P, SZ, C.POINTER(C.c_uint32), C.POINTER(C.c_uint64), C.POINTER(C.c_uint32),
                                    C.POINTER(I), C.POINTER(C.c_int64)]),

@@ -102,6 +102,7 @@ struct Peer {
     cudaStream_t upd = nullptr;
     cudaEvent_t upd_ev[2] = {nullptr, nullptr};
     bool upd_pending[2] = {false, false};
+    bool upd_fresh[2] = {false, false};  // the bank's update was issued at the last tick and not yet waited for
 };
 
 struct Graph {
@@ -166,6 +167,13 @@ struct swarm_driver {
     uint64_t records = 0, visits = 0, ticks = 0, optimizer_steps = 0, completed = 0, captures = 0;
     uint64_t captured_kernels = 0, replayed_kernels = 0, recomputes = 0, migrations = 0, state_bytes = 0;
     cudaEvent_t ev_tmp = nullptr;
+    // tick cost on the compute streams: a (pre, post) timing-event pair around every stretch a
+    // peer's stream spends in, or blocked on, a tick (the stage all-reduce + AdamW; with DPU the
+    // first visit after a tick waiting for its bank's update); resolved into tick_ms
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> tick_open;
+    std::vector<cudaEvent_t> tick_pool;
+    double tick_ms = 0.0;
+    uint64_t tick_spans = 0;
     // profiled region: every visit eager (no graph) on one stream with the stages' kernel
     // profiling on, so the events around each kernel time it alone (the live roofline)
     bool prof = false;
@@ -246,6 +254,47 @@ struct swarm_driver {
 
     // ------------------------------------------------------------- helpers
     int wait(cudaStream_t st, cudaEvent_t ev) { return cuda(cudaStreamWaitEvent(st, ev, 0), "cudaStreamWaitEvent"); }
+    int timing_event(cudaEvent_t* e) {
+        if (!tick_pool.empty()) {
+            *e = tick_pool.back();
+            tick_pool.pop_back();
+            return SWARM_OK;
+        }
+        return cuda(cudaEventCreate(e), "cudaEventCreate");
+    }
+    int tick_begin(cudaStream_t st, cudaEvent_t* pre) {
+        *pre = nullptr;
+        if (prof) return SWARM_OK;
+        TRY(timing_event(pre));
+        return mark(*pre, st);
+    }
+    int tick_end(cudaStream_t st, cudaEvent_t pre) {
+        if (!pre) return SWARM_OK;
+        cudaEvent_t post = nullptr;
+        TRY(timing_event(&post));
+        TRY(mark(post, st));
+        tick_open.emplace_back(pre, post);
+        tick_spans += 1;
+        if (tick_open.size() > 256) tick_resolve(false);
+        return SWARM_OK;
+    }
+    // fold the completed pairs into tick_ms (block: wait for every open pair)
+    void tick_resolve(bool block) {
+        std::vector<std::pair<cudaEvent_t, cudaEvent_t>> keep;
+        for (auto& [a, b] : tick_open) {
+            if (block) cudaEventSynchronize(b);
+            float ms = 0.f;
+            if (cudaEventElapsedTime(&ms, a, b) == cudaSuccess) {
+                tick_ms += ms;
+                tick_pool.push_back(a);
+                tick_pool.push_back(b);
+            } else {
+                cudaGetLastError();  // not ready yet
+                keep.emplace_back(a, b);
+            }
+        }
+        tick_open.swap(keep);
+    }
     int mark(cudaEvent_t ev, cudaStream_t st) { return cuda(cudaEventRecord(ev, st), "cudaEventRecord"); }
     // `st` waits for everything issued so far on every lane of `p`
     int after_peer(cudaStream_t st, Peer& p) {
@@ -501,7 +550,14 @@ struct swarm_driver {
             TRY(swarm_stage_set_lane(p.st, p.cur));
             TRY(after_slot(p, t));  // this slot's previous visit (e.g. the last stage's forward)
         }
-        if (p.upd_pending[bank]) TRY(wait(lane_stream(p), p.upd_ev[bank]));  // DPU: this bank's weights are ready
+        if (p.upd_pending[bank]) {  // DPU: this bank's weights are ready
+            cudaEvent_t pre = nullptr;
+            const bool first = p.upd_fresh[bank];  // (the first visit after the tick is the one that can stall)
+            if (first) TRY(tick_begin(lane_stream(p), &pre));
+            TRY(wait(lane_stream(p), p.upd_ev[bank]));
+            if (first) TRY(tick_end(lane_stream(p), pre));
+            p.upd_fresh[bank] = false;
+        }
         int paired = -1;
         TRY(visit(p, r, s, t, bwd, recompute, &paired));
         if (cfg.lanes > 1) {
@@ -581,6 +637,7 @@ struct swarm_driver {
             for (Peer* q : mine) {
                 TRY(mark(q->upd_ev[b], u));
                 q->upd_pending[b] = true;
+                q->upd_fresh[b] = true;
             }
             optimizer_steps += mine.size();
         }
@@ -613,6 +670,8 @@ struct swarm_driver {
             Peer& lead = *mine[0];
             cudaStream_t st = lane_stream(lead);
             const size_t np = swarm_stage_num_params(lead.st);
+            cudaEvent_t pre = nullptr;
+            TRY(tick_begin(st, &pre));
             // the stage's gradient sum: peers sharing this GPU first, then across GPUs
             for (size_t i = 1; i < mine.size(); ++i) {
                 TRY(after_peer(st, *mine[i]));
@@ -624,9 +683,15 @@ struct swarm_driver {
                                    cudaMemcpyDeviceToDevice, st));
             for (Peer* q : mine)  // mean over the stage's microbatches since the last tick
                 TRY(swarm_stage_optimizer_step(q->st, 1.0f / static_cast<float>(n), st));
+            TRY(tick_end(st, pre));
             if (mine.size() > 1 && !prof) {
                 TRY(mark(ev_tmp, st));
-                for (size_t i = 1; i < mine.size(); ++i) TRY(wait(mine[i]->lanes[0], ev_tmp));
+                for (size_t i = 1; i < mine.size(); ++i) {
+                    cudaEvent_t q0 = nullptr;
+                    TRY(tick_begin(mine[i]->lanes[0], &q0));
+                    TRY(wait(mine[i]->lanes[0], ev_tmp));
+                    TRY(tick_end(mine[i]->lanes[0], q0));
+                }
             }
             optimizer_steps += mine.size();
         }
@@ -812,6 +877,11 @@ struct swarm_driver {
 
     ~swarm_driver() {
         cudaDeviceSynchronize();
+        for (auto& [a, b] : tick_open) {
+            cudaEventDestroy(a);
+            cudaEventDestroy(b);
+        }
+        for (cudaEvent_t e : tick_pool) cudaEventDestroy(e);
         for (auto& kv : graphs) cudaGraphExecDestroy(kv.second.exec);
         for (auto& p : peers) {
             for (cudaEvent_t e : p->slot_ev) cudaEventDestroy(e);
@@ -1149,6 +1219,14 @@ int swarm_driver_stats(swarm_driver_t d, swarm_driver_counters* s) {
     s->migrations = d->migrations;
     s->state_bytes = d->state_bytes;
     s->n_peers = d->peer_stage.size();
+    return SWARM_OK;
+}
+
+int swarm_driver_tick_time(swarm_driver_t d, double* ms, uint64_t* spans) {
+    if (!d) return fail("driver: null argument");
+    d->tick_resolve(true);
+    if (ms) *ms = d->tick_ms;
+    if (spans) *spans = d->tick_spans;
     return SWARM_OK;
 }
 

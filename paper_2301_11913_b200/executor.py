@@ -599,6 +599,14 @@ class EngineExecutor:
             out[pid] = Stage.borrow(self.lib.swarm_driver_stage(self.h, pid), cfg, self.device)
         return out
 
+    def tick_time(self) -> tuple:
+        """(ms, spans): cumulative GPU time this rank's peer streams spent in or blocked on ticks
+        (swarm_driver_tick_time; waits for the GPU to reach the last one)."""
+        import ctypes as C
+        ms, n = C.c_double(), C.c_uint64()
+        self._check(self.lib.swarm_driver_tick_time(self.h, C.byref(ms), C.byref(n)), "driver_tick_time")
+        return ms.value, n.value
+
     def counters(self) -> dict:
         k = self._counters()
         return {f: getattr(k, f) for f, _ in L.DriverCounters._fields_}

@@ -48,6 +48,8 @@ def test_executor_trains_with_allreduce_ticks(cuda, lanes):
     assert ex.optimizer_steps > 0 and ex.ticks > 0
     assert all(c == c for c in curve)
     assert curve[-1] < curve[0] - 0.3, curve
+    ms, spans = ex.tick_time()  # the ticks' GPU time on the peer streams was measured
+    assert spans >= ex.ticks and ms > 0.0, (ms, spans)
 
 
 @pytest.mark.parametrize("lanes", [1, 2])
