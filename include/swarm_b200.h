@@ -220,6 +220,12 @@ int swarm_attn_scores_softmax(const void* q, const void* k, int ld, int n_cols, 
  * .. +d_head] (row stride ld_o) in bf16.  v has q's storage geometry (ld, n_cols). */
 int swarm_attn_forward_pv(const void* q, const void* k, const void* v, int ld, int n_cols, int B, int H, int L,
                           int d_head, float scale, int causal, void* P, void* O, int ld_o, swarm_stream_t stream);
+/* The same forward storing no P: lse[z*L + i] (float, [B*H*L]) = log2 sum_j 2^(scale * q_z[i] . k_z[j] *
+ * log2(e)) over the unmasked keys -- the row's log-sum-exp in base 2 -- and O as above (bit-identical
+ * to swarm_attn_forward_pv's O).  The backward recomputes P from it (swarm_attn_backward_lse), so
+ * no [B*H*L, L] buffer exists on this path. */
+int swarm_attn_forward_lse(const void* q, const void* k, const void* v, int ld, int n_cols, int B, int H, int L,
+                           int d_head, float scale, int causal, float* lse, void* O, int ld_o, swarm_stream_t stream);
 /* dS = scale * P * (dP - rowsum(P * dP)) with dP = dO_z V_z^T computed in TMEM (bf16 out); the
  * row statistic is taken as dO . O (O = P V, the forward's attention output, [B*L, ld_o] with
  * head h at column h*d_head), which equals rowsum(P * dP) and saves a second pass.
@@ -240,6 +246,13 @@ int swarm_attn_scores_softmax_backward(const void* dO, int ld_do, const void* v,
  * workspace.  dQ's fp32 sum over key blocks uses reduce-add (summation order not fixed).
  * Replaces swarm_attn_scores_softmax_backward + the three dS / P GEMMs (csrc/attn_bwd.cu). */
 size_t swarm_attn_backward_workspace(int B, int H, int L, int d_head);
+/* The same with P recomputed on chip from the forward's log2-sum-exp (swarm_attn_forward_lse):
+ * S = Q K^T per (query, key) block in TMEM, P = 2^(S * scale * log2(e) - lse) in bf16 (causal
+ * mask on the diagonal blocks), then as above.  Same workspace. */
+int swarm_attn_backward_lse(const void* dO, int ld_do, const void* qkv, int ld_qkv, int qkv_cols, int k_col0,
+                            int v_col0, const void* O, int ld_o, const float* lse, int B, int H, int L, int d_head,
+                            float scale, int causal, void* dqkv, int ld_dqkv, int dk_col0, int dv_col0,
+                            void* workspace, swarm_stream_t stream);
 int swarm_attn_backward(const void* dO, int ld_do, const void* qkv, int ld_qkv, int qkv_cols, int k_col0, int v_col0,
                         const void* O, int ld_o, const void* P, int B, int H, int L, int d_head, float scale,
                         int causal, void* dqkv, int ld_dqkv, int dk_col0, int dv_col0, void* workspace,

@@ -109,6 +109,8 @@ SIGNATURES = {
     "swarm_attn_scores_softmax_backward": (I, [P, I, P, I, I, P, I, P, I, I, I, I, F, I, P, P]),
     "swarm_attn_backward_workspace": (SZ, [I, I, I, I]),
     "swarm_attn_backward": (I, [P, I, P, I, I, I, I, P, I, P, I, I, I, I, F, I, P, I, I, I, P, P]),
+    "swarm_attn_backward_lse": (I, [P, I, P, I, I, I, I, P, I, P, I, I, I, I, F, I, P, I, I, I, P, P]),
+    "swarm_attn_forward_lse": (I, [P, P, P, I, I, I, I, I, I, F, I, P, P, I, P]),
     "swarm_adamw_step": (I, [P, P, P, P, P, SZ, F, F, F, F, F, I, F, I, P]),
     "swarm_fill_normal": (I, [P, SZ, F, F, C.c_uint64, P]),
     "swarm_cast_f32_bf16": (I, [P, P, SZ, P]),

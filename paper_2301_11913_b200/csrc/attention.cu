@@ -48,6 +48,7 @@ struct Params {
     const __nv_bfloat16* o;  // backward: O = P V [B*L, ld_o] (head h at column h*dh)
     int ld_o;
     int trace;  // record the per-CTA timeline (experiments)
+    float* lse;  // PV forward: when set, P is not stored; lse[z*L + i] = the row's log2-sum-exp of scale * q.k * log2(e)
 };
 
 constexpr int kABytes = (kMaxDh / 64) * BQ * 128;       // 32 KB: Q / dO block
@@ -445,10 +446,12 @@ __global__ void __launch_bounds__(kThreads, 2)
                     fence_async_smem();
                     __syncwarp();
                     if (lane == 0) {
-                        tma_store_2d(&tma_out, pt + q * 32 * 128, c0, out_row);
-                        bulk_commit();
+                        if (!p.lse) {
+                            tma_store_2d(&tma_out, pt + q * 32 * 128, c0, out_row);
+                            bulk_commit();
+                        }
                         mbar_arrive(&pfull[stage]);
-                        bulk_wait_read<0>();  // the box has left smem: the stage may be refilled
+                        if (!p.lse) bulk_wait_read<0>();  // the box has left smem: the stage may be refilled
                         mbar_arrive(&empty[stage]);
                     }
                     if (++stage == kStages) {
@@ -511,6 +514,7 @@ __global__ void __launch_bounds__(kThreads, 2)
             }
         }
         if constexpr (PV) {
+            if (p.lse) p.lse[static_cast<size_t>(z) * p.L + qi] = bias;
             // O row (d_head = 128 fp32 accumulators, TMEM columns 128-255) -> bf16 at O[b*L + qi, h*dh]
             mbar_wait(ofull, 0);
             tc_fence_after();
@@ -628,7 +632,7 @@ bool trace_enabled() {
 template <bool BWD, bool PV = false>
 int launch(const void* a, int lda, int a_cols, int a_col0, const void* b, int ldb, int b_cols, int b_col0,
            const void* pin, const void* o, int ld_o, void* out, int B, int H, int L, int dh, float scale, int causal,
-           cudaStream_t st) {
+           cudaStream_t st, float* lse = nullptr) {
     // PV: pin = V (same storage geometry as K), o = the O output [B*L, ld_o]
     if (L % BQ || L > kMaxL || dh % 64 || dh > kMaxDh || B <= 0 || H <= 0)
         return invalid("attention: need L % 128 == 0, L <= 1024, dh % 64 == 0, dh <= 128");
@@ -643,11 +647,13 @@ int launch(const void* a, int lda, int a_cols, int a_col0, const void* b, int ld
     // the P chunk loaded with 128 x 64 boxes (SWIZZLE_128B)
     if (PV && (dh != kMaxDh || !pin || !o || (reinterpret_cast<uintptr_t>(o) & 15) || ld_o % 8))
         return invalid("attention P V: needs d_head 128, V, and a 16-byte aligned O");
+    if (!out && !(PV && lse)) return invalid("attention: null output");
     if (map_bf16(&ta, a, T, a_cols, lda, 64, BQ, CU_TENSOR_MAP_SWIZZLE_128B) ||
         map_bf16(&tb, b, T, b_cols, ldb, 64, BKV, CU_TENSOR_MAP_SWIZZLE_128B) ||
-        (BWD || PV ? map_bf16(&to, out, rows_out, L, L, 64, 32, CU_TENSOR_MAP_SWIZZLE_128B)
-                   : map_bf16(&to, out, rows_out, L, L, 32, 32, CU_TENSOR_MAP_SWIZZLE_64B)))
+        (out && (BWD || PV ? map_bf16(&to, out, rows_out, L, L, 64, 32, CU_TENSOR_MAP_SWIZZLE_128B)
+                           : map_bf16(&to, out, rows_out, L, L, 32, 32, CU_TENSOR_MAP_SWIZZLE_64B))))
         return invalid("attention: tensor map encoding failed");
+    if (!out) to = ta;  // (unused: the LSE forward stores no P)
     if (BWD && map_bf16(&tp, pin, rows_out, L, L, 64, BQ, CU_TENSOR_MAP_SWIZZLE_128B))
         return invalid("attention: tensor map encoding failed (P)");
     if (PV && map_bf16(&tp, pin, T, b_cols, ldb, 64, BKV, CU_TENSOR_MAP_SWIZZLE_128B))
@@ -661,7 +667,7 @@ int launch(const void* a, int lda, int a_cols, int a_col0, const void* b, int ld
         attr = true;
     }
     Params p{B, H, L, dh, causal, a_col0, b_col0, scale, static_cast<const __nv_bfloat16*>(o), ld_o,
-             trace_enabled() ? 1 : 0};
+             trace_enabled() ? 1 : 0, lse};
     // launched without programmatic serialization: letting the next-but-one grid's
     // CTAs claim the free slots early measured ~1 us slower per launch here
     // (scripts/launch_overhead.py); the kernel still triggers its own dependents
@@ -685,6 +691,13 @@ int swarm_attn_forward_pv(const void* q, const void* k, const void* v, int ld, i
                           int dh, float scale, int causal, void* P, void* O, int ld_o, swarm_stream_t stream) {
     return swarm::attn::launch<false, true>(q, ld, n_cols, 0, k, ld, n_cols, 0, v, O, ld_o, P, B, H, L, dh, scale,
                                             causal, swarm::as_stream(stream));
+}
+
+int swarm_attn_forward_lse(const void* q, const void* k, const void* v, int ld, int n_cols, int B, int H, int L,
+                           int dh, float scale, int causal, float* lse, void* O, int ld_o, swarm_stream_t stream) {
+    if (!lse) return swarm::invalid("attention: null lse");
+    return swarm::attn::launch<false, true>(q, ld, n_cols, 0, k, ld, n_cols, 0, v, O, ld_o, nullptr, B, H, L, dh, scale,
+                                            causal, swarm::as_stream(stream), lse);
 }
 
 int swarm_attn_scores_softmax_backward(const void* dO, int ld_do, const void* v, int ld_v, int v_cols, const void* o,

@@ -60,7 +60,7 @@ constexpr int kBlk = 128;         // keys per key block = queries per query bloc
 constexpr int kDh = 128;          // d_head
 constexpr int kBox = kBlk * 128;  // one [128 rows x 64 columns] bf16 SWIZZLE_128B box: 16 KB
 constexpr int kTile = 2 * kBox;   // [128 x 128] bf16: 32 KB
-constexpr int kBars = 20;
+constexpr int kBars = 20;  // (+ the TMEM slot after them)
 constexpr int kStg = kBlk * 128;  // dQ staging: [128 rows x 32] fp32, SWIZZLE_128B (16 KB)
 constexpr int kSmem = 6 * kTile + 2 * kStg + kBars * 8 + 16 + 1024;
 constexpr uint32_t kColDP = 0, kColDQ = 128, kColDK = 256, kColDV = 384;
@@ -71,6 +71,7 @@ struct Params {
     float scale;
     int q_col0, k_col0, v_col0;  // head-0 columns of Q, K, V in the qkv storage
     const float* D;              // rowsum(dO * O) per (z, query) [B*H*L] (k_attn_rowdot)
+    const float* lse;            // RECOMP: the forward's log2-sum-exp per (z, query) [B*H*L]
     float* dq_acc;               // fp32 dQ accumulator [B*L, ld_acc] (zero on entry, left zero)
     int ld_acc;
     __nv_bfloat16* dqkv;
@@ -158,6 +159,19 @@ __global__ void __launch_bounds__(256) k_attn_dq_out(float* __restrict__ acc, in
     __stcg(a + 1, make_float4(0.f, 0.f, 0.f, 0.f));
 }
 
+// 2^x on the SFU (ex2.approx.ftz: 2 ulp; P is rounded to bf16)
+__device__ __forceinline__ float fast_exp2(float x) {
+    float y;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+
+// RECOMP = false: P_j is the forward's stored probabilities, TMA-loaded (double-buffered).
+// RECOMP = true:  the forward stored only each row's log2-sum-exp (swarm_attn_forward_lse);
+//                 S_j = Q_j K_i^T is recomputed into the dP columns and the dS rows write
+//                 P_j = 2^(S_j * scale * log2 e - lse) into the (single) P buffer; Q is
+//                 double-buffered instead, since S needs it at the start of the block.
+template <bool RECOMP>
 __global__ void __launch_bounds__(kThreads, 1)
     k_attn_bwd(const __grid_constant__ CUtensorMap tm_qkv, const __grid_constant__ CUtensorMap tm_do,
                const __grid_constant__ CUtensorMap tm_p, const __grid_constant__ CUtensorMap tm_acc,
@@ -170,25 +184,29 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint8_t* sK = smem;
     uint8_t* sV = sK + kTile;
     uint8_t* sDO = sV + kTile;
-    uint8_t* sQ = sDO + kTile;
-    uint8_t* sP = sQ + kTile;    // two buffers: P_j, then dS_j in place
-    uint8_t* sStg = sP + 2 * kTile;  // two dQ staging buffers
+    uint8_t* sX = sDO + kTile;  // 3 tiles: Q + P[2], or (RECOMP) Q[2] + P
+    auto sQb = [&](int n) { return RECOMP ? sX + (n & 1) * kTile : sX; };
+    auto sPb = [&](int n) { return RECOMP ? sX + 2 * kTile : sX + kTile + (n & 1) * kTile; };
+    uint8_t* sStg = sX + 3 * kTile;  // two dQ staging buffers
     uint64_t* bars = reinterpret_cast<uint64_t*>(sStg + 2 * kStg);
     uint64_t* kv_full = bars + 0;   // TMA: K_i, V_i landed
     uint64_t* kv_free = bars + 1;   // dS rows: dK, dV staged through sK / sV and stored (TMA read them)
     uint64_t* do_full = bars + 2;   // TMA: dO_j landed
     uint64_t* do_free = bars + 3;   // MMA: done with dO_j (dP, dV issued)
-    uint64_t* q_full = bars + 4;    // TMA: Q_j landed
-    uint64_t* q_free = bars + 5;    // MMA: done with Q_j (dK issued)
-    uint64_t* p_full = bars + 6;    // [2] TMA: P_j landed in buffer j % 2
-    uint64_t* p_free = bars + 8;    // [2] MMA: done with dS_j in buffer j % 2
-    uint64_t* mma12 = bars + 10;    // dP, dV updated
-    uint64_t* ds_ready = bars + 11; // dS rows: dS_j written (4 warps)
-    uint64_t* mma34 = bars + 12;    // dK updated, dQ_j ready
-    uint64_t* dq_free = bars + 13;  // dQ rows: dQ_j read out of TMEM (4 warps)
-    uint64_t* acc_full = bars + 14; // dK, dV of the key block complete
-    uint64_t* acc_free = bars + 15; // dS rows: dK, dV read out (4 warps)
+    uint64_t* q_full = bars + 4;    // [2] TMA: Q_j landed (buffer n % 2; one buffer unless RECOMP)
+    uint64_t* q_free = bars + 6;    // [2] MMA: done with Q_j
+    uint64_t* p_full = bars + 8;    // [2] TMA: P_j landed in buffer n % 2 (not RECOMP)
+    uint64_t* p_free = bars + 10;   // [2] MMA: done with dS_j in its buffer
+    uint64_t* mma12 = bars + 12;    // dP, dV updated
+    uint64_t* ds_ready = bars + 13; // dS rows: dS_j written (4 warps)
+    uint64_t* mma34 = bars + 14;    // dK updated, dQ_j ready
+    uint64_t* dq_free = bars + 15;  // dQ rows: dQ_j read out of TMEM (4 warps)
+    uint64_t* acc_full = bars + 16; // dK, dV of the key block complete
+    uint64_t* acc_free = bars + 17; // dS rows: dK, dV read out (4 warps)
+    uint64_t* s_full = bars + 18;   // RECOMP: S_j = Q_j K_i^T in TMEM
+    uint64_t* p_ready = bars + 19;  // RECOMP: dS rows: P_j written (4 warps)
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + kBars);
+    const int qbuf = RECOMP ? 2 : 1;  // Q buffers
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int nz = p.B * p.H, nqb = p.L / kBlk;
@@ -199,7 +217,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     auto j0 = [&](int ti) { return p.causal ? kbs[ti] : 0; };
 
     if (warp == 0 && lane == 0) {
-        for (int i = 0; i < 16; ++i) mbar_init(bars + i, (i == 11 || i == 13 || i == 15) ? 4 : 1);
+        for (int i = 0; i < kBars; ++i) mbar_init(bars + i, (i == 13 || i == 15 || i == 17 || i == 19) ? 4 : 1);
         fence_barrier_init();
     }
     if (warp == 2) {
@@ -227,7 +245,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             for (int ti = 0; ti < nk; ++ti)
                 for (int j = j0(ti) + (ti == 0); j < nqb; ++j)
                     for (int b = 0; b < 2; ++b) {
-                        tma_prefetch_l2(&tm_p, kbs[ti] * kBlk + 64 * b, z * p.L + j * kBlk);
+                        if (!RECOMP) tma_prefetch_l2(&tm_p, kbs[ti] * kBlk + 64 * b, z * p.L + j * kBlk);
                         if (ti == 0) {
                             tma_prefetch_l2(&tm_do, zh * kDh + 64 * b, qrow(j));
                             tma_prefetch_l2(&tm_qkv, qcol + 64 * b, qrow(j));
@@ -243,20 +261,30 @@ __global__ void __launch_bounds__(kThreads, 1)
                     tma_load_2d(sV + b * kBox, &tm_qkv, kv_full, p.v_col0 + zh * kDh + 64 * b, qrow(kb));
                 }
                 for (int j = j0(ti); j < nqb; ++j, ++n) {
-                    // dO_j once dP, dV of the previous block are issued; P_j into the buffer block n-2
-                    // used; Q_j once the previous dK is issued (needed only after this block's dS)
+                    // RECOMP: Q_j first (the score MMA needs it at the block's start), into the
+                    // buffer block n-2 used; dO_j once dP, dV of the previous block are issued.
+                    // Else: dO_j, then P_j into the buffer block n-2 used, then Q_j once the
+                    // previous dK is issued (needed only after this block's dS)
+                    const int qb = RECOMP ? (n & 1) : 0;
+                    auto load_q = [&]() {
+                        if (RECOMP ? n > 1 : n > 0)
+                            mbar_wait(&q_free[qb], RECOMP ? (((n >> 1) - 1) & 1) : ((n - 1) & 1));
+                        mbar_arrive_expect_tx(&q_full[qb], kTile);
+                        for (int b = 0; b < 2; ++b)
+                            tma_load_2d(sQb(n) + b * kBox, &tm_qkv, &q_full[qb], qcol + 64 * b, qrow(j));
+                    };
+                    if (RECOMP) load_q();
                     if (n > 0) mbar_wait(do_free, (n - 1) & 1);
                     mbar_arrive_expect_tx(do_full, kTile);
                     for (int b = 0; b < 2; ++b) tma_load_2d(sDO + b * kBox, &tm_do, do_full, zh * kDh + 64 * b, qrow(j));
-                    const int pb = n & 1;
-                    if (n > 1) mbar_wait(&p_free[pb], ((n >> 1) - 1) & 1);
-                    mbar_arrive_expect_tx(&p_full[pb], kTile);
-                    for (int b = 0; b < 2; ++b)
-                        tma_load_2d(sP + pb * kTile + b * kBox, &tm_p, &p_full[pb], kb * kBlk + 64 * b,
-                                    z * p.L + j * kBlk);
-                    if (n > 0) mbar_wait(q_free, (n - 1) & 1);
-                    mbar_arrive_expect_tx(q_full, kTile);
-                    for (int b = 0; b < 2; ++b) tma_load_2d(sQ + b * kBox, &tm_qkv, q_full, qcol + 64 * b, qrow(j));
+                    if (!RECOMP) {
+                        const int pb = n & 1;
+                        if (n > 1) mbar_wait(&p_free[pb], ((n >> 1) - 1) & 1);
+                        mbar_arrive_expect_tx(&p_full[pb], kTile);
+                        for (int b = 0; b < 2; ++b)
+                            tma_load_2d(sPb(n) + b * kBox, &tm_p, &p_full[pb], kb * kBlk + 64 * b, z * p.L + j * kBlk);
+                        load_q();
+                    }
                 }
             }
         }
@@ -266,7 +294,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             constexpr uint32_t id_kk = make_idesc_bf16(kBlk, kDh, false, false);
             constexpr uint32_t id_mm = make_idesc_bf16(kBlk, kDh, true, true);
             constexpr uint32_t id_km = make_idesc_bf16(kBlk, kDh, false, true);
-            const uint32_t aK = smem_u32(sK), aV = smem_u32(sV), aDO = smem_u32(sDO), aQ = smem_u32(sQ);
+            const uint32_t aK = smem_u32(sK), aV = smem_u32(sV), aDO = smem_u32(sDO);
             // K-major operand: k-step kk (16 columns) sits in box kk/4 at +32 B per step; MN-major
             // operand: k-step kk is rows 16kk.. (+2048 B), the two 64-wide MN chunks one box apart
             auto kmaj = [](uint32_t base, int kk) { return make_sdesc(base + (kk >> 2) * kBox + (kk & 3) * 32, 16, 1024); };
@@ -277,10 +305,21 @@ __global__ void __launch_bounds__(kThreads, 1)
                 if (ti > 0) mbar_wait(acc_free, (ti - 1) & 1);  // the previous key block's dK, dV were read out
                 tc_fence_after();
                 for (int j = j0(ti), jj = 0; j < nqb; ++j, ++jj, ++n) {
-                    const int pb = n & 1;
-                    const uint32_t aP = smem_u32(sP + pb * kTile);
+                    const int qb = RECOMP ? (n & 1) : 0, pb = RECOMP ? 0 : (n & 1);
+                    const uint32_t aP = smem_u32(sPb(n)), aQ = smem_u32(sQb(n));
+                    const uint32_t q_par = RECOMP ? ((n >> 1) & 1) : (n & 1);
+                    if constexpr (RECOMP) {
+                        // S_j = Q_j K_i^T into the dP columns (the rows read dP_{j-1} before ds_ready)
+                        mbar_wait(&q_full[qb], q_par);
+                        tc_fence_after();
+                        for (int kk = 0; kk < kDh / 16; ++kk)
+                            mma_bf16(tmem + kColDP, kmaj(aQ, kk), kmaj(aK, kk), id_kk, kk != 0 ? 1u : 0u);
+                        mma_commit(s_full);
+                        mbar_wait(p_ready, n & 1);  // P_j written (and S_j read) by the rows
+                    } else {
+                        mbar_wait(&p_full[pb], (n >> 1) & 1);
+                    }
                     mbar_wait(do_full, n & 1);
-                    mbar_wait(&p_full[pb], (n >> 1) & 1);
                     tc_fence_after();
                     for (int kk = 0; kk < kDh / 16; ++kk)  // dP = dO_j V_i^T (K = d_head)
                         mma_bf16(tmem + kColDP, kmaj(aDO, kk), kmaj(aV, kk), id_kk, kk != 0 ? 1u : 0u);
@@ -289,11 +328,11 @@ __global__ void __launch_bounds__(kThreads, 1)
                     mma_commit(mma12);
                     mma_commit(do_free);
                     mbar_wait(ds_ready, n & 1);
-                    mbar_wait(q_full, n & 1);
+                    if (!RECOMP) mbar_wait(&q_full[0], q_par);
                     tc_fence_after();
                     for (int kk = 0; kk < kBlk / 16; ++kk)  // dK += dS_j^T Q_j (K = queries)
                         mma_bf16(tmem + kColDK, mnmaj(aP, kk), mnmaj(aQ, kk), id_mm, (jj | kk) != 0 ? 1u : 0u);
-                    mma_commit(q_free);
+                    mma_commit(&q_free[qb]);
                     if (n > 0) {
                         mbar_wait(dq_free, (n - 1) & 1);
                         tc_fence_after();
@@ -311,13 +350,49 @@ __global__ void __launch_bounds__(kThreads, 1)
         // ------------------------------------------------ dS rows: one query row per thread
         const int r = (warp - 4) * 32 + lane;
         const uint32_t trow = tmem + (static_cast<uint32_t>((warp & 3) * 32) << 16);
+        const float cs = p.scale * 1.4426950408889634f;
         int n = 0;
         for (int ti = 0; ti < nk; ++ti) {
             const int kb = kbs[ti];
             for (int j = j0(ti); j < nqb; ++j, ++n) {
-                const int pb = n & 1;
-                const float D = __ldg(p.D + static_cast<size_t>(z) * p.L + j * kBlk + r);
-                mbar_wait(&p_full[pb], (n >> 1) & 1);  // (TMA writes visible to these threads)
+                const int pb = RECOMP ? 0 : (n & 1);
+                uint8_t* sPn = sPb(n);
+                const size_t qz = static_cast<size_t>(z) * p.L + j * kBlk + r;
+                const float D = __ldg(p.D + qz);
+                if constexpr (RECOMP) {
+                    // P_j row r = 2^(S * cs - lse), keys past the query masked (causal diagonal block)
+                    const float lse = __ldg(p.lse + qz);
+                    const int valid = (p.causal && kb == j) ? r + 1 : kBlk;  // columns < valid are unmasked
+                    if (n > 0) mbar_wait(&p_free[0], (n - 1) & 1);  // dS_{j-1} consumed by dK, dQ
+                    mbar_wait(s_full, n & 1);
+                    tc_fence_after();
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) {
+                        uint32_t ra[32], rb[32];
+                        tmem_ld_32x32b_x32(trow + kColDP + 64 * h, ra);
+                        tmem_ld_32x32b_x32(trow + kColDP + 64 * h + 32, rb);
+                        tmem_ld_wait();
+                        const uint32_t prow = smem_u32(sPn + h * kBox) + r * 128;
+#pragma unroll
+                        for (int k = 0; k < 8; ++k) {
+                            float o[8];
+#pragma unroll
+                            for (int e = 0; e < 8; ++e) {
+                                const int c = k * 8 + e;  // column inside the half
+                                const float sv = __uint_as_float(c < 32 ? ra[c] : rb[c - 32]);
+                                o[e] = (64 * h + c < valid) ? fast_exp2(fmaf(sv, cs, -lse)) : 0.f;
+                            }
+                            st_shared_v4(prow + ((k ^ (r & 7)) << 4), pack2(o[0], o[1]), pack2(o[2], o[3]),
+                                         pack2(o[4], o[5]), pack2(o[6], o[7]));
+                        }
+                    }
+                    fence_async_smem();  // P (generic-proxy writes) -> the dV MMA's operand reads
+                    tc_fence_before();
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(p_ready);
+                } else {
+                    mbar_wait(&p_full[pb], (n >> 1) & 1);  // (TMA writes visible to these threads)
+                }
                 mbar_wait(mma12, n & 1);
                 TR(r == 0, 8 + 9 * n + 0);
                 tc_fence_after();
@@ -328,7 +403,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     tmem_ld_32x32b_x32(trow + kColDP + 64 * h, ra);
                     tmem_ld_32x32b_x32(trow + kColDP + 64 * h + 32, rb);
                     tmem_ld_wait();
-                    const uint32_t prow = smem_u32(sP + pb * kTile + h * kBox) + r * 128;
+                    const uint32_t prow = smem_u32(sPn + h * kBox) + r * 128;
 #pragma unroll
                     for (int k = 0; k < 8; ++k) {
                         const uint32_t addr = prow + ((k ^ (r & 7)) << 4);
@@ -484,14 +559,16 @@ int launch(const Params& p, const void* qkv, int ld_qkv, int qkv_cols, const voi
     CUtensorMap tq, td, tp, ta, tout;
     if (map_bf16(&tq, qkv, T, qkv_cols, ld_qkv, 64, kBlk, CU_TENSOR_MAP_SWIZZLE_128B) ||
         map_bf16(&td, dO, T, static_cast<long long>(p.H) * kDh, ld_do, 64, kBlk, CU_TENSOR_MAP_SWIZZLE_128B) ||
-        map_bf16(&tp, P, rows_p, p.L, p.L, 64, kBlk, CU_TENSOR_MAP_SWIZZLE_128B) ||
+        (P ? map_bf16(&tp, P, rows_p, p.L, p.L, 64, kBlk, CU_TENSOR_MAP_SWIZZLE_128B) : 0) ||
         map_bf16(&tout, p.dqkv, T, p.ld_dqkv, p.ld_dqkv, 64, kBlk, CU_TENSOR_MAP_SWIZZLE_128B))
         return invalid("attention backward: tensor map encoding failed");
     if (map_f32(&ta, p.dq_acc, T, p.ld_acc))
         return invalid("attention backward: tensor map encoding failed (dQ accumulator)");
+    if (!P) tp = td;  // (unused: P is recomputed from the log2-sum-exp)
     static bool attr = false;
     if (!attr) {
-        SWARM_CUDA_TRY(cudaFuncSetAttribute(k_attn_bwd, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem));
+        SWARM_CUDA_TRY(cudaFuncSetAttribute(k_attn_bwd<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem));
+        SWARM_CUDA_TRY(cudaFuncSetAttribute(k_attn_bwd<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem));
         attr = true;
     }
     const long long items = T * p.H * 16;
@@ -501,7 +578,8 @@ int launch(const Params& p, const void* qkv, int ld_qkv, int qkv_cols, const voi
     SWARM_LAUNCH_CHECK("k_attn_rowdot");
     const int nkb = p.L / kBlk;
     const int per_z = p.causal ? (nkb + 1) / 2 : nkb;
-    k_attn_bwd<<<p.B * p.H * per_z, kThreads, kSmem, st>>>(tq, td, tp, ta, tout, p);
+    if (p.lse) k_attn_bwd<true><<<p.B * p.H * per_z, kThreads, kSmem, st>>>(tq, td, tp, ta, tout, p);
+    else k_attn_bwd<false><<<p.B * p.H * per_z, kThreads, kSmem, st>>>(tq, td, tp, ta, tout, p);
     SWARM_LAUNCH_CHECK("k_attn_bwd");
     if (!(p.dbg & 2)) {
         const long long n8 = T * p.ld_acc / 8;
@@ -534,16 +612,16 @@ size_t swarm_attn_backward_workspace(int B, int H, int L, int d_head) {
     return acc + static_cast<size_t>(B) * H * L * sizeof(float);  // + D
 }
 
-int swarm_attn_backward(const void* dO, int ld_do, const void* qkv, int ld_qkv, int qkv_cols, int k_col0, int v_col0,
-                        const void* O, int ld_o, const void* P, int B, int H, int L, int d_head, float scale,
-                        int causal, void* dqkv, int ld_dqkv, int dk_col0, int dv_col0, void* workspace,
-                        swarm_stream_t stream) {
+static int attn_backward(const void* dO, int ld_do, const void* qkv, int ld_qkv, int qkv_cols, int k_col0,
+                         int v_col0, const void* O, int ld_o, const void* P, const float* lse, int B, int H, int L,
+                         int d_head, float scale, int causal, void* dqkv, int ld_dqkv, int dk_col0, int dv_col0,
+                         void* workspace, swarm_stream_t stream) {
     using namespace swarm::attn_bwd;
     if (d_head != kDh || L % kBlk || L <= 0 || B <= 0 || H <= 0)
         return swarm::invalid("attention backward: need d_head 128 and L % 128 == 0");
-    if (!dO || !qkv || !O || !P || !dqkv || !workspace)
+    if (!dO || !qkv || !O || !(P || lse) || !dqkv || !workspace)
         return swarm::invalid("attention backward: null operand or workspace");
-    if (!al16(dO) || !al16(qkv) || !al16(O) || !al16(P) || !al16(dqkv) || !al16(workspace) || ld_do % 8 ||
+    if (!al16(dO) || !al16(qkv) || !al16(O) || (P && !al16(P)) || !al16(dqkv) || !al16(workspace) || ld_do % 8 ||
         ld_qkv % 8 || ld_o % 8 || ld_dqkv % 8 || k_col0 % 8 || v_col0 % 8 || dk_col0 % 8 || dv_col0 % 8)
         return swarm::invalid("attention backward: operands must be 16-byte aligned bf16 rows");
     if (qkv_cols < v_col0 + H * kDh || qkv_cols < k_col0 + H * kDh || ld_qkv < qkv_cols || ld_do < H * kDh ||
@@ -558,6 +636,7 @@ int swarm_attn_backward(const void* dO, int ld_do, const void* qkv, int ld_qkv, 
     p.q_col0 = 0;
     p.k_col0 = k_col0;
     p.v_col0 = v_col0;
+    p.lse = lse;
     p.dq_acc = static_cast<float*>(workspace);
     p.ld_acc = H * kDh;
     p.D = reinterpret_cast<const float*>(static_cast<char*>(workspace) + static_cast<size_t>(B) * L * H * kDh * sizeof(float));
@@ -572,6 +651,24 @@ int swarm_attn_backward(const void* dO, int ld_do, const void* qkv, int ld_qkv, 
     }();
     p.dbg = dbg;
     return launch(p, qkv, ld_qkv, qkv_cols, dO, ld_do, O, ld_o, P, swarm::as_stream(stream));
+}
+
+int swarm_attn_backward(const void* dO, int ld_do, const void* qkv, int ld_qkv, int qkv_cols, int k_col0, int v_col0,
+                        const void* O, int ld_o, const void* P, int B, int H, int L, int d_head, float scale,
+                        int causal, void* dqkv, int ld_dqkv, int dk_col0, int dv_col0, void* workspace,
+                        swarm_stream_t stream) {
+    if (!P) return swarm::invalid("attention backward: null P");
+    return attn_backward(dO, ld_do, qkv, ld_qkv, qkv_cols, k_col0, v_col0, O, ld_o, P, nullptr, B, H, L, d_head, scale,
+                         causal, dqkv, ld_dqkv, dk_col0, dv_col0, workspace, stream);
+}
+
+int swarm_attn_backward_lse(const void* dO, int ld_do, const void* qkv, int ld_qkv, int qkv_cols, int k_col0,
+                            int v_col0, const void* O, int ld_o, const float* lse, int B, int H, int L, int d_head,
+                            float scale, int causal, void* dqkv, int ld_dqkv, int dk_col0, int dv_col0,
+                            void* workspace, swarm_stream_t stream) {
+    if (!lse) return swarm::invalid("attention backward: null lse");
+    return attn_backward(dO, ld_do, qkv, ld_qkv, qkv_cols, k_col0, v_col0, O, ld_o, nullptr, lse, B, H, L, d_head,
+                         scale, causal, dqkv, ld_dqkv, dk_col0, dv_col0, workspace, stream);
 }
 
 }  // extern "C"

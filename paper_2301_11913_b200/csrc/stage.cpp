@@ -52,8 +52,9 @@ struct LayerW {
 };
 
 struct Act {
-    EP x, a, qkv, P, o, h, c, u, g;
+    EP x, a, qkv, P, o, h, c, u, g;  // P: the forward's probabilities (not on the log2-sum-exp path)
     float *mu1, *rs1, *mu2, *rs2;
+    float* lse = nullptr;  // the attention rows' log2-sum-exp [B*H*L] (the backward recomputes P from it)
 };
 
 struct Slot {
@@ -130,6 +131,7 @@ struct swarm_stage {
     int step = 0;
     bool fused_attn = false;  // scores+softmax in one tcgen05 kernel (csrc/attention.cu)
     bool fused_bwd = false;   // the attention backward in one kernel (csrc/attn_bwd.cu)
+    bool attn_lse = false;    // forward stores log2-sum-exp, not P; the backward recomputes P
     void* abws = nullptr;     // its dQ accumulator + arrival counters (zeroed once; kernels leave it zeroed)
     // weight-gradient GEMMs run on a side stream forked/joined per layer, so they
     // fill the SMs the data-gradient chain leaves idle (GEMM wave tails)
@@ -466,7 +468,12 @@ int block_forward(swarm_stage* s, Act& A, EP y, const LayerW& W, cudaStream_t st
     TRY(mm(T, 3 * d, d, {A.a, d, T, d, false}, {p16 + W.wqkv, d, 3 * d, d, false}, A.qkv, 3 * d,
            SWARM_EPI_STORE_BF16, nullptr, 1.f, st));
     const float scale = 1.f / std::sqrt(static_cast<float>(dh));
-    if (s->fused_attn && attn_pv(s)) {
+    if (s->attn_lse) {
+        // O = softmax(scale * Q K^T) V in one kernel (scores and O in TMEM); only each row's log2-sum-exp
+        // is kept for the backward
+        PTRY(SWARM_PROF_ATTENTION, st, swarm_attn_forward_lse(A.qkv, A.qkv + d, A.qkv + 2 * d, 3 * d, d, s->B, H, L, dh,
+                                                              scale, s->cfg.causal, A.lse, A.o, d, st));
+    } else if (s->fused_attn && attn_pv(s)) {
         // P = softmax(scale * Q K^T) and O = P V in one kernel (scores and O in TMEM)
         PTRY(SWARM_PROF_ATTENTION, st, swarm_attn_forward_pv(A.qkv, A.qkv + d, A.qkv + 2 * d, 3 * d, d, s->B, H, L, dh,
                                                              scale, s->cfg.causal, A.P, A.o, d, st));
@@ -599,7 +606,12 @@ int block_backward(swarm_stage* s, const Act& A, EP dy, EP dx, const LayerW& W, 
            st));
     // dP = dO V^T ; dS = scale * P (dP - rowsum(P dP))
     const float scale = 1.f / std::sqrt(static_cast<float>(dh));
-    if (s->fused_bwd) {
+    if (s->attn_lse) {
+        // the attention backward with P recomputed on chip from the forward's log2-sum-exp
+        PTRY(SWARM_PROF_ATTENTION, st, swarm_attn_backward_lse(s->dO, d, A.qkv, 3 * d, 3 * d, d, 2 * d, A.o, d, A.lse,
+                                                               s->B, H, L, dh, scale, s->cfg.causal, dqkv, 3 * d, d,
+                                                               2 * d, s->abws, st));
+    } else if (s->fused_bwd) {
         // the whole attention backward in one kernel: dP, dS on chip, dQ | dK | dV into dqkv
         PTRY(SWARM_PROF_ATTENTION, st, swarm_attn_backward(s->dO, d, A.qkv, 3 * d, 3 * d, d, 2 * d, A.o, d, A.P, s->B, H, L,
                                                            dh, scale, s->cfg.causal, dqkv, 3 * d, d, 2 * d, s->abws,
@@ -743,6 +755,21 @@ int create(const swarm_stage_config* c, swarm_stage* s) {
     if (!s->f32) TRY(alloc(s, &s->p16, s->nparams));
     // activation slots
     const size_t T = s->T, Td = T * d, TF = T * F, BHLL = static_cast<size_t>(s->B) * s->H * s->L * s->L;
+    // attention path: fused score kernels; the one-kernel backward (d_head 128); with it, the
+    // forward stores each row's log2-sum-exp instead of P and the backward recomputes P on chip
+    // (SWARM_ATTN_FUSED / SWARM_ATTN_BWD_FUSED / SWARM_ATTN_LSE = 0 turn each off)
+    {
+        const char* e = getenv("SWARM_ATTN_FUSED");
+        s->fused_attn = !s->f32 && !(e && e[0] == '0') && s->L % 128 == 0 && s->L <= 512 && s->dh % 64 == 0 && s->dh <= 128;
+    }
+    {
+        const char* e = getenv("SWARM_ATTN_BWD_FUSED");
+        s->fused_bwd = s->fused_attn && s->dh == 128 && !(e && e[0] == '0');
+    }
+    {
+        const char* e = getenv("SWARM_ATTN_LSE");
+        s->attn_lse = s->fused_bwd && attn_pv(s) && !(e && e[0] == '0');
+    }
     s->slots.resize(c->max_slots);
     // layer-shared stages keep the weight-gradient inputs (a, o, c, g) of all
     // applications stacked in application order, so one GEMM with K = n_layers * T
@@ -763,7 +790,8 @@ int create(const swarm_stage_config* c, swarm_stage* s) {
             if (s->stacked) A.a = sa + l * Td;
             else TRY(alloc(s, &A.a, Td));
             TRY(alloc(s, &A.qkv, 3 * Td));
-            TRY(alloc(s, &A.P, BHLL));
+            if (s->attn_lse) TRY(alloc(s, &A.lse, static_cast<size_t>(s->B) * s->H * s->L));
+            else TRY(alloc(s, &A.P, BHLL));
             if (s->stacked) A.o = so + l * Td;
             else TRY(alloc(s, &A.o, Td));
             TRY(alloc(s, &A.h, Td));
@@ -800,14 +828,6 @@ int create(const swarm_stage_config* c, swarm_stage* s) {
         }
     }
     // workspaces (fp32 scores only for the unfused attention path)
-    {
-        const char* e = getenv("SWARM_ATTN_FUSED");
-        s->fused_attn = !s->f32 && !(e && e[0] == '0') && s->L % 128 == 0 && s->L <= 512 && s->dh % 64 == 0 && s->dh <= 128;
-    }
-    {
-        const char* e = getenv("SWARM_ATTN_BWD_FUSED");
-        s->fused_bwd = s->fused_attn && s->dh == 128 && !(e && e[0] == '0');
-    }
     if (!s->fused_attn) {
         TRY(alloc(s, &s->S, BHLL));
         TRY(alloc(s, &s->dP, BHLL));
@@ -1091,7 +1111,8 @@ int swarm_stage_activation(swarm_stage_t s, int slot, int layer, const char* nam
         void* p;
         size_t n;
     } table[] = {{"x", A.x, Td}, {"a", A.a, Td}, {"qkv", A.qkv, 3 * Td},
-                 {"P", A.P, static_cast<size_t>(s->B) * s->H * s->L * s->L},
+                 {"P", A.P, A.P ? static_cast<size_t>(s->B) * s->H * s->L * s->L : 0},
+                 {"lse", A.lse, A.lse ? static_cast<size_t>(s->B) * s->H * s->L : 0},
                  {"o", A.o, Td}, {"h", A.h, Td}, {"c", A.c, Td}, {"u", A.u, TF}, {"g", A.g, TF}};
     for (auto& e : table)
         if (n == e.k) return *ptr = e.p, *numel = e.n, SWARM_OK;

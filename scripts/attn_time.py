@@ -22,8 +22,14 @@ sgrad = lambda: lib.swarm_attn_scores_softmax_backward(ptr(dO), d, ptr(qkv[:, 2 
                                                        H, L, dh, sc, 1, ptr(dS), st)
 bwd = lambda: lib.swarm_attn_backward(ptr(dO), d, ptr(qkv), 3 * d, 3 * d, d, 2 * d, ptr(O), d, ptr(P), B, H, L, dh, sc,
                                       1, ptr(dqkv), 3 * d, d, 2 * d, ptr(ws), st)
+lse = torch.zeros(B * H * L, device="cuda")
+fwd_lse = lambda: lib.swarm_attn_forward_lse(ptr(qkv), ptr(qkv[:, d:]), ptr(qkv[:, 2 * d:]), 3 * d, d, B, H, L, dh, sc,
+                                             1, ptr(lse), ptr(O), d, st)
+bwd_lse = lambda: lib.swarm_attn_backward_lse(ptr(dO), d, ptr(qkv), 3 * d, 3 * d, d, 2 * d, ptr(O), d, ptr(lse), B, H,
+                                              L, dh, sc, 1, ptr(dqkv), 3 * d, d, 2 * d, ptr(ws), st)
 flush = torch.empty(256 << 20, device="cuda", dtype=torch.uint8)
-for name, fn in (("forward_pv", fwd), ("score_grad (unfused bwd, 1 of 4 launches)", sgrad), ("backward_fused", bwd)):
+for name, fn in (("forward_pv", fwd), ("score_grad (unfused bwd, 1 of 4 launches)", sgrad), ("backward_fused", bwd),
+                 ("forward_lse (no P stored)", fwd_lse), ("backward_lse (P recomputed)", bwd_lse)):
     for _ in range(3):
         assert fn() == 0, _lib.last_error()
     torch.cuda.synchronize()

@@ -198,3 +198,59 @@ def test_fused_attention_backward_matches_unfused(cuda):
     q, k = split(qkv[:, :d]), split(qkv[:, d:2 * d])
     for got, ref in zip(dqkv.float().split(d, 1)[:2], (join(dSf @ k), join(dSf.transpose(-1, -2) @ q))):
         assert float((got - ref).norm() / ref.norm()) < 5e-3
+
+
+@pytest.mark.parametrize("B,H,L,causal", [(2, 4, 512, 1), (2, 4, 512, 0), (1, 3, 256, 1), (1, 2, 384, 1),
+                                          (4, 16, 512, 1), (1, 2, 1024, 1), (1, 1, 128, 1)])
+def test_attention_lse_forward_and_recompute_backward(cuda, B, H, L, causal):
+    """swarm_attn_forward_lse: O bit-identical to the P-storing forward's, lse = the row's base-2
+    log-sum-exp (torch fp32); swarm_attn_backward_lse (P recomputed on chip from lse) vs torch fp32
+    of the same op with exact softmax probabilities, and against the P-reading backward."""
+    import torch
+    from paper_2301_11913_b200 import _lib
+    dh = 128
+    torch.manual_seed(7 * L + causal + H)
+    d = H * dh
+    qkv = (torch.randn(B * L, 3 * d, device="cuda") * 2).bfloat16()
+    P = torch.zeros(B * H * L, L, device="cuda", dtype=torch.bfloat16)
+    O = torch.zeros(B * L, d, device="cuda", dtype=torch.bfloat16)
+    O2 = torch.zeros_like(O)
+    lse = torch.full((B * H * L,), float("nan"), device="cuda")
+    scale = 1 / math.sqrt(dh)
+    st = torch.cuda.current_stream().cuda_stream
+    L_ = _lib.lib()
+    ptr = lambda t: C.c_void_p(t.data_ptr())  # noqa: E731
+    assert L_.swarm_attn_forward_pv(ptr(qkv), ptr(qkv[:, d:]), ptr(qkv[:, 2 * d:]), 3 * d, d, B, H, L, dh, scale,
+                                    causal, ptr(P), ptr(O), d, st) == 0
+    rc = L_.swarm_attn_forward_lse(ptr(qkv), ptr(qkv[:, d:]), ptr(qkv[:, 2 * d:]), 3 * d, d, B, H, L, dh, scale,
+                                   causal, ptr(lse), ptr(O2), d, st)
+    assert rc == 0, _lib.last_error()
+    torch.cuda.synchronize()
+    assert torch.equal(O, O2)
+    split = lambda t: t.float().view(B, L, H, dh).transpose(1, 2)  # noqa: E731
+    q, k = split(qkv[:, :d]), split(qkv[:, d:2 * d])
+    s = (q @ k.transpose(-1, -2)) * scale
+    if causal:
+        s = s.masked_fill(torch.triu(torch.ones(L, L, dtype=torch.bool, device="cuda"), 1), float("-inf"))
+    ref_lse = (torch.logsumexp(s, -1) / math.log(2)).reshape(-1)
+    torch.testing.assert_close(lse, ref_lse, rtol=0, atol=2e-3)
+    # backward: recomputed P vs the exact softmax (rounded to bf16 like the kernel's operand)
+    Pex = torch.softmax(s, -1).bfloat16()
+    ws = torch.zeros(L_.swarm_attn_backward_workspace(B, H, L, dh), device="cuda", dtype=torch.uint8)
+    dO = torch.randn(B * L, d, device="cuda").bfloat16()
+    dqkv = torch.full((B * L, 3 * d), float("nan"), device="cuda", dtype=torch.bfloat16)
+    rc = L_.swarm_attn_backward_lse(ptr(dO), d, ptr(qkv), 3 * d, 3 * d, d, 2 * d, ptr(O), d, ptr(lse), B, H, L, dh,
+                                    scale, causal, ptr(dqkv), 3 * d, d, 2 * d, ptr(ws), st)
+    assert rc == 0, _lib.last_error()
+    torch.cuda.synchronize()
+    assert int(ws[:B * L * H * dh * 4].count_nonzero()) == 0
+    want = attn_backward_ref(qkv, dO, O, Pex.view(B * H * L, L), B, H, L, dh)
+    for name, got, ref in zip("QKV", dqkv.float().split(d, 1), want):
+        err = float((got - ref).norm() / ref.norm())
+        assert err < 1.5e-2, (name, err)
+    dqkv_p = torch.empty_like(dqkv)
+    assert L_.swarm_attn_backward(ptr(dO), d, ptr(qkv), 3 * d, 3 * d, d, 2 * d, ptr(O), d, ptr(P), B, H, L, dh, scale,
+                                  causal, ptr(dqkv_p), 3 * d, d, 2 * d, ptr(ws), st) == 0
+    torch.cuda.synchronize()
+    for got, ref in zip(dqkv.float().split(d, 1), dqkv_p.float().split(d, 1)):
+        assert float((got - ref).norm() / ref.norm()) < 1e-2
