@@ -148,7 +148,7 @@ __device__ __forceinline__ void trace(const Params& p, int slot) {
     if (p.trace && blockIdx.x < kTraceCtas) g_attn_trace[blockIdx.x][slot] = gtimer();
 }
 
-template <bool BWD, bool PV = false>
+template <bool BWD, bool PV = false, bool ONE = false>
 __global__ void __launch_bounds__(kThreads, 2)
     k_attn_chunks(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUtensorMap tma_b,
                   const __grid_constant__ CUtensorMap tma_p, const __grid_constant__ CUtensorMap tma_out,
@@ -156,7 +156,10 @@ __global__ void __launch_bounds__(kThreads, 2)
     // PV: tma_p maps V (the forward reads no P), O goes to p.o_out
     // forward: pass 0 row max / sum, pass 1 probabilities; backward: one pass, the
     // row statistic rowsum(P * dP) = dO . O comes from the forward output
-    constexpr int kPasses = BWD ? 1 : 2;
+    // PV with an lse output: one pass with an online row max (O rescaled in TMEM when the max
+    // grows by more than 2^8; the final O divided by the row sum), no statistics pass
+    constexpr bool one = PV && ONE;
+    constexpr int kPasses = (BWD || one) ? 1 : 2;
     pdl_trigger();
     if (threadIdx.x == 128) {
         trace(p, 0);
@@ -185,7 +188,8 @@ __global__ void __launch_bounds__(kThreads, 2)
     // single barrier would then have moved two phases past the waiter's parity
     uint64_t* pfull = sempty + 2;
     uint64_t* ofull = pfull + 2;  // PV: the last P V MMA committed
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(ofull + 1);
+    uint64_t* pvdone = ofull + 1;  // one pass: each P V MMA committed (the rows rescale O after it)
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(pvdone + 1);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int nqb = p.L / BQ, nz = p.B * p.H;
@@ -211,6 +215,7 @@ __global__ void __launch_bounds__(kThreads, 2)
         mbar_init(&pfull[0], 4);
         mbar_init(&pfull[1], 4);
         mbar_init(ofull, 1);
+        mbar_init(pvdone, 1);
         fence_barrier_init();
     }
     if (warp == 2) {
@@ -235,7 +240,7 @@ __global__ void __launch_bounds__(kThreads, 2)
             for (int j = 0; j < nch; ++j) {
                 mbar_wait(&empty[stage], phase ^ 1);
                 uint8_t* sst = sb + stage * Y::kStageBytes;
-                const bool load_v = PV && pass == 1;
+                const bool load_v = PV && pass == kPasses - 1;
                 mbar_arrive_expect_tx(&full[stage], kboxes * BKV * 128 * (load_v ? 2 : 1) + (BWD ? kPChunkBytes : 0));
                 for (int kb = 0; kb < kboxes; ++kb)
                     tma_load_2d(sst + kb * BKV * 128, &tma_b, &full[stage], bcol + kb * 64, brow + j * BKV);
@@ -272,6 +277,7 @@ __global__ void __launch_bounds__(kThreads, 2)
                 mma_bf16(tmem + 2 * BKV, ad, bd, idesc_pv, (jj != 0 || kk != 0) ? 1u : 0u);
             }
             mma_commit(&empty[st_pv]);
+            if constexpr (one) mma_commit(pvdone);
         };
         int prev_stage = -1;
         for (int pass = 0; pass < kPasses; ++pass)
@@ -323,7 +329,9 @@ __global__ void __launch_bounds__(kThreads, 2)
         float bias = 0.f;  // fwd pass 1: max(u) + log2(sum), so p = 2^(u - bias); bwd: dO . O
         int stage = 0;
         uint32_t sphase = 0;
-        if constexpr (!BWD) {
+        float m_used = -INFINITY, l_run = 0.f;  // one pass: the exponent offset in use, the running sum
+        float resc = 1.f;                         // one pass: this chunk's O rescale factor
+        if constexpr (!BWD && !one) {
             // ---------------- pass 0: online row max / sum
             float mu = -INFINITY, l = 0.f;
             for (int j = 0; j < nch; ++j) {
@@ -377,7 +385,7 @@ __global__ void __launch_bounds__(kThreads, 2)
                 mu = nmu;
             }
             bias = mu + __log2f(l);
-        } else {
+        } else if (BWD) {
             // D = dO[row] . O[row] over this head's d_head columns (= rowsum(P * dP))
             const size_t grow = static_cast<size_t>(zb) * p.L + qi;
             // dO[row] from the A tile (2 x 128-B SWIZZLE_128B boxes), O[row] from global in 2 batches
@@ -423,6 +431,36 @@ __global__ void __launch_bounds__(kThreads, 2)
             }
             if constexpr (!BWD) {
                 float v[64];
+                if constexpr (one) {
+                    // online max: a chunk whose max exceeds the offset in use by more than 2^8 moves it,
+                    // rescaling the running sum and this row's O accumulator (after the P V MMAs issued so
+                    // far completed: by the in-order tensor pipe, all but P V of the previous chunk)
+                    float f = 1.f;
+                    if (c0 < valid) {
+                        float cm = -INFINITY;
+                        if (c0 + BKV <= valid) {
+#pragma unroll
+                            for (int jj = 0; jj < 32; ++jj)
+                                cm = fmaxf(cm, fmaxf(__uint_as_float(ra[jj]), __uint_as_float(rb[jj])));
+                        } else {
+#pragma unroll
+                            for (int jj = 0; jj < 32; ++jj) {
+                                if (c0 + jj < valid) cm = fmaxf(cm, __uint_as_float(ra[jj]));
+                                if (c0 + 32 + jj < valid) cm = fmaxf(cm, __uint_as_float(rb[jj]));
+                            }
+                        }
+                        const float cmu = cm * cs;
+                        if (m_used == -INFINITY) {
+                            m_used = cmu;
+                        } else if (cmu > m_used + 8.f) {
+                            f = fast_exp2(m_used - cmu);
+                            l_run *= f;
+                            m_used = cmu;
+                        }
+                    }
+                    resc = f;  // (O itself is rescaled after P_j is written, before P V_j may start)
+                    bias = m_used;
+                }
                 if (c0 + BKV <= valid) {
                     exp2_64(ra, rb, cs, -bias, v);
                 } else {
@@ -431,6 +469,12 @@ __global__ void __launch_bounds__(kThreads, 2)
                         v[jj] = (c0 + jj < valid) ? fast_exp2(fmaf(__uint_as_float(ra[jj]), cs, -bias)) : 0.f;
                         v[32 + jj] = (c0 + 32 + jj < valid) ? fast_exp2(fmaf(__uint_as_float(rb[jj]), cs, -bias)) : 0.f;
                     }
+                }
+                if constexpr (one) {
+                    float add = 0.f;
+#pragma unroll
+                    for (int jj = 0; jj < 64; ++jj) add += v[jj];
+                    l_run += add;
                 }
                 if constexpr (PV) {
                     // P_j over this stage's K chunk (the score MMA has read it: sfull), in the
@@ -443,6 +487,26 @@ __global__ void __launch_bounds__(kThreads, 2)
                         st_shared_v4(prow + ((k ^ (r & 7)) << 4), pack_bf16(v[8 * k], v[8 * k + 1]),
                                      pack_bf16(v[8 * k + 2], v[8 * k + 3]), pack_bf16(v[8 * k + 4], v[8 * k + 5]),
                                      pack_bf16(v[8 * k + 6], v[8 * k + 7]));
+                    if constexpr (one) {
+                        // the offset moved for some row of the warp: rescale the warp's O rows once every
+                        // P V MMA issued so far completed (by the in-order tensor pipe, all but the previous
+                        // chunk's are: the score MMA of this chunk followed them)
+                        if (__any_sync(0xffffffffu, resc != 1.f)) {
+                            if (j > 0) mbar_wait(pvdone, (j - 1) & 1);
+                            tc_fence_after();
+#pragma unroll
+                            for (int c = 0; c < 4; ++c) {
+                                uint32_t ro[32];
+                                tmem_ld_32x32b_x32(trow + 2 * BKV + 32 * c, ro);
+                                tmem_ld_wait();
+#pragma unroll
+                                for (int w = 0; w < 32; ++w) ro[w] = __float_as_uint(__uint_as_float(ro[w]) * resc);
+                                tmem_st_32x32b_x32(trow + 2 * BKV + 32 * c, ro);
+                            }
+                            tmem_st_wait();
+                            tc_fence_before();
+                        }
+                    }
                     fence_async_smem();
                     __syncwarp();
                     if (lane == 0) {
@@ -514,7 +578,8 @@ __global__ void __launch_bounds__(kThreads, 2)
             }
         }
         if constexpr (PV) {
-            if (p.lse) p.lse[static_cast<size_t>(z) * p.L + qi] = bias;
+            const float inv_l = one ? 1.f / l_run : 1.f;
+            if (one) p.lse[static_cast<size_t>(z) * p.L + qi] = m_used + __log2f(l_run);
             // O row (d_head = 128 fp32 accumulators, TMEM columns 128-255) -> bf16 at O[b*L + qi, h*dh]
             mbar_wait(ofull, 0);
             tc_fence_after();
@@ -528,10 +593,10 @@ __global__ void __launch_bounds__(kThreads, 2)
                 uint4* dst = reinterpret_cast<uint4*>(orow + 32 * c);
 #pragma unroll
                 for (int w = 0; w < 4; ++w)
-                    dst[w] = make_uint4(pack_bf16(__uint_as_float(ro[8 * w]), __uint_as_float(ro[8 * w + 1])),
-                                        pack_bf16(__uint_as_float(ro[8 * w + 2]), __uint_as_float(ro[8 * w + 3])),
-                                        pack_bf16(__uint_as_float(ro[8 * w + 4]), __uint_as_float(ro[8 * w + 5])),
-                                        pack_bf16(__uint_as_float(ro[8 * w + 6]), __uint_as_float(ro[8 * w + 7])));
+                    dst[w] = make_uint4(pack_bf16(__uint_as_float(ro[8 * w]) * inv_l, __uint_as_float(ro[8 * w + 1]) * inv_l),
+                                        pack_bf16(__uint_as_float(ro[8 * w + 2]) * inv_l, __uint_as_float(ro[8 * w + 3]) * inv_l),
+                                        pack_bf16(__uint_as_float(ro[8 * w + 4]) * inv_l, __uint_as_float(ro[8 * w + 5]) * inv_l),
+                                        pack_bf16(__uint_as_float(ro[8 * w + 6]) * inv_l, __uint_as_float(ro[8 * w + 7]) * inv_l));
             }
             tc_fence_before();
         }
@@ -658,12 +723,14 @@ int launch(const void* a, int lda, int a_cols, int a_col0, const void* b, int ld
         return invalid("attention: tensor map encoding failed (P)");
     if (PV && map_bf16(&tp, pin, T, b_cols, ldb, 64, BKV, CU_TENSOR_MAP_SWIZZLE_128B))
         return invalid("attention: tensor map encoding failed (V)");
-    auto kern = k_attn_chunks<BWD, PV>;
+    auto kern = (PV && lse) ? k_attn_chunks<BWD, PV, true> : k_attn_chunks<BWD, PV, false>;
     constexpr int kSmem = Lay<BWD, PV>::kSmem;
     static bool attr = false;
     if (!attr) {
-        SWARM_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem));
-        SWARM_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+        for (auto kf : {k_attn_chunks<BWD, PV, false>, k_attn_chunks<BWD, PV, true>}) {
+            SWARM_CUDA_TRY(cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem));
+            SWARM_CUDA_TRY(cudaFuncSetAttribute(kf, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+        }
         attr = true;
     }
     Params p{B, H, L, dh, causal, a_col0, b_col0, scale, static_cast<const __nv_bfloat16*>(o), ld_o,

@@ -19,9 +19,14 @@ f = lambda: lib.swarm_attn_scores_softmax(C.c_void_p(qkv.data_ptr()), C.c_void_p
 g = lambda: lib.swarm_attn_scores_softmax_backward(C.c_void_p(dO.data_ptr()), d, C.c_void_p(qkv[:, 2 * d:].data_ptr()), 3 * d, d,
                                                    C.c_void_p(O.data_ptr()), d, C.c_void_p(P.data_ptr()), B, H, L, dh,
                                                    C.c_float(1 / math.sqrt(dh)), 1, C.c_void_p(dS.data_ptr()), st)
+lse = torch.zeros(B * H * L, device="cuda")
+h = lambda: lib.swarm_attn_forward_lse(C.c_void_p(qkv.data_ptr()), C.c_void_p(qkv[:, d:].data_ptr()),
+                                       C.c_void_p(qkv[:, 2 * d:].data_ptr()), 3 * d, d, B, H, L, dh,
+                                       C.c_float(1 / math.sqrt(dh)), 1, C.c_void_p(lse.data_ptr()),
+                                       C.c_void_p(O.data_ptr()), d, st)
 nz, nqb = B * H, L // 128
 n = nz * nqb
-for name, fn in (("fwd", f), ("bwd", g)):
+for name, fn in (("fwd", f), ("bwd", g), ("fwd_lse (P V fused)", h)):
     for _ in range(3):
         fn()
     torch.cuda.synchronize()

@@ -203,9 +203,10 @@ def test_fused_attention_backward_matches_unfused(cuda):
 @pytest.mark.parametrize("B,H,L,causal", [(2, 4, 512, 1), (2, 4, 512, 0), (1, 3, 256, 1), (1, 2, 384, 1),
                                           (4, 16, 512, 1), (1, 2, 1024, 1), (1, 1, 128, 1)])
 def test_attention_lse_forward_and_recompute_backward(cuda, B, H, L, causal):
-    """swarm_attn_forward_lse: O bit-identical to the P-storing forward's, lse = the row's base-2
-    log-sum-exp (torch fp32); swarm_attn_backward_lse (P recomputed on chip from lse) vs torch fp32
-    of the same op with exact softmax probabilities, and against the P-reading backward."""
+    """swarm_attn_forward_lse (one pass, online row max): O vs the P-storing two-pass forward's and vs
+    torch fp32 attention within bf16 rounding, lse = the row's base-2 log-sum-exp (torch fp32);
+    swarm_attn_backward_lse (P recomputed on chip from lse) vs torch fp32 of the same op with exact
+    softmax probabilities, and against the P-reading backward."""
     import torch
     from paper_2301_11913_b200 import _lib
     dh = 128
@@ -226,9 +227,11 @@ def test_attention_lse_forward_and_recompute_backward(cuda, B, H, L, causal):
                                    causal, ptr(lse), ptr(O2), d, st)
     assert rc == 0, _lib.last_error()
     torch.cuda.synchronize()
-    assert torch.equal(O, O2)
+    assert float((O2.float() - O.float()).norm() / O.float().norm()) < 5e-3
     split = lambda t: t.float().view(B, L, H, dh).transpose(1, 2)  # noqa: E731
     q, k = split(qkv[:, :d]), split(qkv[:, d:2 * d])
+    full = (ref_P(qkv, B, H, L, dh, causal).view(B, H, L, L) @ split(qkv[:, 2 * d:])).transpose(1, 2).reshape(B * L, d)
+    assert float((O2.float() - full).norm() / full.norm()) < 1e-2
     s = (q @ k.transpose(-1, -2)) * scale
     if causal:
         s = s.masked_fill(torch.triu(torch.ones(L, L, dtype=torch.bool, device="cuda"), 1), float("-inf"))
