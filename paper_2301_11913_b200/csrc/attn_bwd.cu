@@ -299,46 +299,60 @@ __global__ void __launch_bounds__(kThreads, 1)
             // operand: k-step kk is rows 16kk.. (+2048 B), the two 64-wide MN chunks one box apart
             auto kmaj = [](uint32_t base, int kk) { return make_sdesc(base + (kk >> 2) * kBox + (kk & 3) * 32, 16, 1024); };
             auto mnmaj = [](uint32_t base, int kk) { return make_sdesc(base + kk * 2048, kBox, 1024); };
+            // RECOMP: block n's S, dP and dQ share TMEM region rg(n) (columns 0 or 128, alternating), so
+            // the next block's S = Q K^T can be issued into the other region right after this block's
+            // dP / dV -- while the rows compute dS -- and the rows' next exponentials overlap dK / dQ
+            auto rg = [&](int m) -> uint32_t { return RECOMP ? ((m & 1) ? kColDQ : kColDP) : kColDP; };
+            auto rq = [&](int m) -> uint32_t { return RECOMP ? rg(m) : kColDQ; };
+            auto issue_s = [&](int m, uint32_t aQm) {  // S_m = Q_m K_i^T (K = d_head)
+                mbar_wait(&q_full[m & 1], (m >> 1) & 1);
+                tc_fence_after();
+                for (int kk = 0; kk < kDh / 16; ++kk)
+                    mma_bf16(tmem + rg(m), kmaj(aQm, kk), kmaj(aK, kk), id_kk, kk != 0 ? 1u : 0u);
+                mma_commit(s_full);
+            };
             int n = 0;
             for (int ti = 0; ti < nk; ++ti) {
                 mbar_wait(kv_full, ti & 1);
                 if (ti > 0) mbar_wait(acc_free, (ti - 1) & 1);  // the previous key block's dK, dV were read out
                 tc_fence_after();
+                const int jn = nqb - j0(ti);  // blocks of this key block
                 for (int j = j0(ti), jj = 0; j < nqb; ++j, ++jj, ++n) {
                     const int qb = RECOMP ? (n & 1) : 0, pb = RECOMP ? 0 : (n & 1);
                     const uint32_t aP = smem_u32(sPb(n)), aQ = smem_u32(sQb(n));
                     const uint32_t q_par = RECOMP ? ((n >> 1) & 1) : (n & 1);
                     if constexpr (RECOMP) {
-                        // S_j = Q_j K_i^T into the dP columns (the rows read dP_{j-1} before ds_ready)
-                        mbar_wait(&q_full[qb], q_par);
-                        tc_fence_after();
-                        for (int kk = 0; kk < kDh / 16; ++kk)
-                            mma_bf16(tmem + kColDP, kmaj(aQ, kk), kmaj(aK, kk), id_kk, kk != 0 ? 1u : 0u);
-                        mma_commit(s_full);
+                        // (the first block of a key block: S was not issued ahead -- K changed; its region
+                        // last held dQ_{n-2}, whose read-out was awaited before dQ_{n-1}'s MMA)
+                        if (jj == 0) issue_s(n, aQ);
                         mbar_wait(p_ready, n & 1);  // P_j written (and S_j read) by the rows
+                        TR(true, 8 + 9 * n + 7);
                     } else {
                         mbar_wait(&p_full[pb], (n >> 1) & 1);
                     }
                     mbar_wait(do_full, n & 1);
                     tc_fence_after();
-                    for (int kk = 0; kk < kDh / 16; ++kk)  // dP = dO_j V_i^T (K = d_head)
-                        mma_bf16(tmem + kColDP, kmaj(aDO, kk), kmaj(aV, kk), id_kk, kk != 0 ? 1u : 0u);
+                    for (int kk = 0; kk < kDh / 16; ++kk)  // dP = dO_j V_i^T (K = d_head), over S_j
+                        mma_bf16(tmem + rg(n), kmaj(aDO, kk), kmaj(aV, kk), id_kk, kk != 0 ? 1u : 0u);
                     for (int kk = 0; kk < kBlk / 16; ++kk)  // dV += P_j^T dO_j (K = queries)
                         mma_bf16(tmem + kColDV, mnmaj(aP, kk), mnmaj(aDO, kk), id_mm, (jj | kk) != 0 ? 1u : 0u);
                     mma_commit(mma12);
                     mma_commit(do_free);
+                    // dQ_{n-1} read out of its region (also the region S_{n+1} goes to): observed before
+                    // every dQ MMA, so the dQ rows are never two phases ahead of this wait
+                    if (n > 0) {
+                        mbar_wait(dq_free, (n - 1) & 1);
+                        tc_fence_after();
+                    }
+                    if (RECOMP && jj + 1 < jn) issue_s(n + 1, smem_u32(sQb(n + 1)));
                     mbar_wait(ds_ready, n & 1);
                     if (!RECOMP) mbar_wait(&q_full[0], q_par);
                     tc_fence_after();
                     for (int kk = 0; kk < kBlk / 16; ++kk)  // dK += dS_j^T Q_j (K = queries)
                         mma_bf16(tmem + kColDK, mnmaj(aP, kk), mnmaj(aQ, kk), id_mm, (jj | kk) != 0 ? 1u : 0u);
                     mma_commit(&q_free[qb]);
-                    if (n > 0) {
-                        mbar_wait(dq_free, (n - 1) & 1);
-                        tc_fence_after();
-                    }
-                    for (int kk = 0; kk < kBlk / 16; ++kk)  // dQ_j = dS_j K_i (K = keys)
-                        mma_bf16(tmem + kColDQ, kmaj(aP, kk), mnmaj(aK, kk), id_km, kk != 0 ? 1u : 0u);
+                    for (int kk = 0; kk < kBlk / 16; ++kk)  // dQ_j = dS_j K_i (K = keys), over dP_j (RECOMP)
+                        mma_bf16(tmem + rq(n), kmaj(aP, kk), mnmaj(aK, kk), id_km, kk != 0 ? 1u : 0u);
                     mma_commit(mma34);
                     mma_commit(&p_free[pb]);
                     TR(true, 8 + 9 * n + 5);
@@ -360,36 +374,46 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const size_t qz = static_cast<size_t>(z) * p.L + j * kBlk + r;
                 const float D = __ldg(p.D + qz);
                 if constexpr (RECOMP) {
-                    // P_j row r = 2^(S * cs - lse), keys past the query masked (causal diagonal block)
+                    // P_j row r = 2^(S * cs - lse), keys past the query masked (causal diagonal block); the
+                    // exponentials are taken while dK / dQ of the previous block may still read its dS
+                    // out of the P buffer, and written once that buffer is free
                     const float lse = __ldg(p.lse + qz);
                     const int valid = (p.causal && kb == j) ? r + 1 : kBlk;  // columns < valid are unmasked
-                    if (n > 0) mbar_wait(&p_free[0], (n - 1) & 1);  // dS_{j-1} consumed by dK, dQ
+                    const uint32_t rgn = (n & 1) ? kColDQ : kColDP;
                     mbar_wait(s_full, n & 1);
+                    TR(r == 0, 8 + 9 * n + 6);
                     tc_fence_after();
+                    uint32_t pk[64];  // P_j row, packed bf16 pairs
 #pragma unroll
                     for (int h = 0; h < 2; ++h) {
                         uint32_t ra[32], rb[32];
-                        tmem_ld_32x32b_x32(trow + kColDP + 64 * h, ra);
-                        tmem_ld_32x32b_x32(trow + kColDP + 64 * h + 32, rb);
+                        tmem_ld_32x32b_x32(trow + rgn + 64 * h, ra);
+                        tmem_ld_32x32b_x32(trow + rgn + 64 * h + 32, rb);
                         tmem_ld_wait();
-                        const uint32_t prow = smem_u32(sPn + h * kBox) + r * 128;
 #pragma unroll
-                        for (int k = 0; k < 8; ++k) {
-                            float o[8];
-#pragma unroll
-                            for (int e = 0; e < 8; ++e) {
-                                const int c = k * 8 + e;  // column inside the half
-                                const float sv = __uint_as_float(c < 32 ? ra[c] : rb[c - 32]);
-                                o[e] = (64 * h + c < valid) ? fast_exp2(fmaf(sv, cs, -lse)) : 0.f;
-                            }
-                            st_shared_v4(prow + ((k ^ (r & 7)) << 4), pack2(o[0], o[1]), pack2(o[2], o[3]),
-                                         pack2(o[4], o[5]), pack2(o[6], o[7]));
+                        for (int e = 0; e < 32; ++e) {
+                            const int c = 2 * e;  // column inside the half
+                            const float s0 = __uint_as_float(c < 32 ? ra[c] : rb[c - 32]);
+                            const float s1 = __uint_as_float(c + 1 < 32 ? ra[c + 1] : rb[c - 31]);
+                            const float p0 = (64 * h + c < valid) ? fast_exp2(fmaf(s0, cs, -lse)) : 0.f;
+                            const float p1 = (64 * h + c + 1 < valid) ? fast_exp2(fmaf(s1, cs, -lse)) : 0.f;
+                            pk[32 * h + e] = pack2(p0, p1);
                         }
                     }
-                    fence_async_smem();  // P (generic-proxy writes) -> the dV MMA's operand reads
                     tc_fence_before();
+                    if (n > 0) mbar_wait(&p_free[0], (n - 1) & 1);  // dS_{j-1} consumed by dK, dQ
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) {
+                        const uint32_t prow = smem_u32(sPn + h * kBox) + r * 128;
+#pragma unroll
+                        for (int k = 0; k < 8; ++k)
+                            st_shared_v4(prow + ((k ^ (r & 7)) << 4), pk[32 * h + 4 * k], pk[32 * h + 4 * k + 1],
+                                         pk[32 * h + 4 * k + 2], pk[32 * h + 4 * k + 3]);
+                    }
+                    fence_async_smem();  // P (generic-proxy writes) -> the dV MMA's operand reads
                     __syncwarp();
                     if (lane == 0) mbar_arrive(p_ready);
+                    TR(r == 0, 8 + 9 * n + 4);
                 } else {
                     mbar_wait(&p_full[pb], (n >> 1) & 1);  // (TMA writes visible to these threads)
                 }
@@ -400,8 +424,9 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
                 for (int h = 0; h < 2; ++h) {
                     uint32_t ra[32], rb[32];
-                    tmem_ld_32x32b_x32(trow + kColDP + 64 * h, ra);
-                    tmem_ld_32x32b_x32(trow + kColDP + 64 * h + 32, rb);
+                    const uint32_t rgd = (RECOMP && (n & 1)) ? kColDQ : kColDP;
+                    tmem_ld_32x32b_x32(trow + rgd + 64 * h, ra);
+                    tmem_ld_32x32b_x32(trow + rgd + 64 * h + 32, rb);
                     tmem_ld_wait();
                     const uint32_t prow = smem_u32(sPn + h * kBox) + r * 128;
 #pragma unroll
@@ -485,11 +510,12 @@ __global__ void __launch_bounds__(kThreads, 1)
                 tc_fence_after();
                 uint32_t v[4][32];
 #pragma unroll
-                for (int c = 0; c < 4; ++c) tmem_ld_32x32b_x32(trow + kColDQ + 32 * c, v[c]);
+                const uint32_t rgq = (RECOMP && !(n & 1)) ? kColDP : kColDQ;  // RECOMP: dQ_j sits in block j's region
+                for (int c = 0; c < 4; ++c) tmem_ld_32x32b_x32(trow + rgq + 32 * c, v[c]);
                 tmem_ld_wait();
                 tc_fence_before();
                 __syncwarp();
-                if (lane == 0) mbar_arrive(dq_free);  // the next dQ MMA may overwrite TMEM now
+                if (lane == 0) mbar_arrive(dq_free);  // the region may be overwritten now
                 // dQ_j -> the fp32 accumulator by TMA reduce-add, 32 columns at a time through two
                 // SWIZZLE_128B staging buffers (16-B piece k of row r at k ^ (r & 7))
 #pragma unroll

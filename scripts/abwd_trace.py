@@ -16,10 +16,19 @@ dqkv = torch.empty_like(qkv)
 ws = torch.zeros(lib.swarm_attn_backward_workspace(B, H, L, dh), device="cuda", dtype=torch.uint8)
 st = torch.cuda.current_stream().cuda_stream
 sc = 1 / math.sqrt(dh)
-lib.swarm_attn_forward_pv(ptr(qkv), ptr(qkv[:, d:]), ptr(qkv[:, 2 * d:]), 3 * d, d, B, H, L, dh, sc, 1, ptr(P), ptr(O), d, st)
+lse = torch.zeros(B * H * L, device="cuda")
+RECOMP = os.environ.get("ABWD_LSE", "1") == "1"
+if RECOMP:
+    lib.swarm_attn_forward_lse(ptr(qkv), ptr(qkv[:, d:]), ptr(qkv[:, 2 * d:]), 3 * d, d, B, H, L, dh, sc, 1, ptr(lse), ptr(O), d, st)
+else:
+    lib.swarm_attn_forward_pv(ptr(qkv), ptr(qkv[:, d:]), ptr(qkv[:, 2 * d:]), 3 * d, d, B, H, L, dh, sc, 1, ptr(P), ptr(O), d, st)
 for _ in range(3):
-    assert lib.swarm_attn_backward(ptr(dO), d, ptr(qkv), 3 * d, 3 * d, d, 2 * d, ptr(O), d, ptr(P), B, H, L, dh, sc, 1,
-                                   ptr(dqkv), 3 * d, d, 2 * d, ptr(ws), st) == 0
+    if RECOMP:
+        assert lib.swarm_attn_backward_lse(ptr(dO), d, ptr(qkv), 3 * d, 3 * d, d, 2 * d, ptr(O), d, ptr(lse), B, H, L, dh, sc, 1,
+                                           ptr(dqkv), 3 * d, d, 2 * d, ptr(ws), st) == 0
+    else:
+        assert lib.swarm_attn_backward(ptr(dO), d, ptr(qkv), 3 * d, 3 * d, d, 2 * d, ptr(O), d, ptr(P), B, H, L, dh, sc, 1,
+                                       ptr(dqkv), 3 * d, d, 2 * d, ptr(ws), st) == 0
 torch.cuda.synchronize()
 tr = np.zeros((256, 96), dtype=np.uint64)
 lib.swarm_debug_abwd_trace.argtypes = [C.c_void_p, C.c_int]
@@ -33,5 +42,5 @@ for c in (0, 1, 64, 127):
     print(f"CTA {c}: setup {rel[c,1]:.1f}")
     for blk in range(5):
         v = rel[c, 8 + 9 * blk:17 + 9 * blk]
-        print(f"   blk {blk}: dS-rows mma12 {v[0]:.1f} ds {v[1]:.1f} | mma34 issued {v[5]:.1f} | dQ-rows mma34 {v[2]:.1f} reduces {v[3]:.1f} counter {v[4]:.1f}")
+        print(f"   blk {blk}: rows s_full {v[6]:.1f} p_ready {v[4]:.1f} | mma p_seen {v[7]:.1f} | rows mma12 {v[0]:.1f} ds {v[1]:.1f} | mma34 issued {v[5]:.1f} | dQ-rows mma34 {v[2]:.1f} reduced {v[3]:.1f}")
     print(f"   kb0 acc {rel[c,2]:.1f} out {rel[c,3]:.1f}  kb1 acc {rel[c,4]:.1f} out {rel[c,5]:.1f}  end {rel[c,6]:.1f} exit {rel[c,7]:.1f}")
