@@ -52,7 +52,7 @@ constexpr int kNumSMs = 148;
 // allocation, descriptor prefetch) on SMs the previous kernel's tail leaves
 // idle — before that kernel finishes.  Every such kernel calls pdl_trigger()
 // first and pdl_wait() before its first global-memory access; both are no-ops
-// for a kernel launched without the attribute.  SWARM_PDL=0 disables it.
+// for a kernel launched without the attribute.  Off unless SWARM_PDL=1 (csrc/lib.cu).
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 bool pdl_enabled();

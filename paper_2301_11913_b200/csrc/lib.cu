@@ -14,10 +14,14 @@ std::atomic<uint64_t> g_launches{0};
 
 void set_error(const std::string& msg) { g_last_error = msg; }
 
+// Off by default since round 2c: with several peers' streams sharing a GPU, dependents launched
+// early hold SM slots other streams' kernels could use -- the engine headline measured +0.7% at
+// 1 GPU and +1% at 4 GPUs without it (scripts/gpu_ab_multi.sh, gpu_scale_env_ab.sh).  SWARM_PDL=1
+// turns it on (a single-stream caller may prefer it).
 bool pdl_enabled() {
     static const bool on = [] {
         const char* e = getenv("SWARM_PDL");
-        return !(e && e[0] == '0');
+        return e && e[0] == '1';
     }();
     return on;
 }

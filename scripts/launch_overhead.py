@@ -1,6 +1,6 @@
 """Kernel-boundary cost on this GPU: 200 back-to-back launches captured in a CUDA
 graph of (a) a 1-thread spin(0) kernel (no PDL attribute) and (b) a 1-row
-LayerNorm (PDL attribute unless SWARM_PDL=0), and of (c) the attention forward
+LayerNorm (PDL attribute when SWARM_PDL=1), and of (c) the attention forward
 kernel; us per launch."""
 import ctypes as C, math, os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
@@ -29,4 +29,4 @@ for name, fn in cases.items():
     torch.cuda.synchronize(); g.replay(); torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(True), torch.cuda.Event(True)
     e0.record(); g.replay(); e1.record(); torch.cuda.synchronize()
-    print(f"PDL={os.environ.get('SWARM_PDL', '1')} {name}: {e0.elapsed_time(e1) / n * 1e3:.2f} us/launch", flush=True)
+    print(f"PDL={os.environ.get('SWARM_PDL', '0')} {name}: {e0.elapsed_time(e1) / n * 1e3:.2f} us/launch", flush=True)
