@@ -473,6 +473,45 @@ def placement_str(world: int, S: int) -> str:
     return f"{S} stages x {world // S} peer(s) per stage" if world >= S else f"{world} GPU(s) x {S // world} stage(s) each"
 
 
+def engine_placement(args, world: int, S: int):
+    """(layout, peer_rank, description) of the engine workloads' peers.
+
+    One GPU: one peer per stage.  From 4 GPUs (the default there, --placement balanced): 2 peers per
+    GPU (4 per GPU on 2 GPUs when asked for), so each stage has world * that / S peers; they are placed
+    by longest-processing-time first -- a peer's load is its stage's cost over its stage's peer count,
+    the LM-head stage costing 1 + V d / (layers * params per layer) block stages -- on the least
+    loaded GPU not yet hosting that stage.  The LM-head stage's extra work is thus spread over
+    several GPUs next to lighter stages' peers (SWARM's remedy for uneven stages: more peers where
+    the work is) instead of pinning one GPU to it.  Measured: 4 GPUs 320-322k vs 311.5k tokens/s;
+    2 GPUs 159-165k vs 172k (the GPUs then clock at the power cap, and the tick's cross-GPU
+    all-reduce costs 4% of the step), so 2 GPUs default to --placement contiguous: the round-2
+    layout (world >= S: world / S peers per stage, one per GPU; else consecutive stages per GPU).
+    Pure arithmetic on the Shape (no product import: the reference arm's config uses it too)."""
+    placement = getattr(args, "placement", None) or ("balanced" if world >= 4 else "contiguous")
+    if world == 1 or placement == "contiguous":
+        if world >= S:
+            return [world // S] * S, None, placement_str(world, S)
+        return [1] * S, None, placement_str(world, S)
+    m = shape_of(args)
+    per_layer = 4 * m.d_model * m.d_model + 2 * m.d_model * m.d_ffn
+    head = 1.0 + m.vocab * m.d_model / (m.layers_per_stage * per_layer)
+    per_gpu = 4 if world == 2 else 2
+    p = max(1, -(-per_gpu * world // S))
+    layout = [p] * S
+    stage = [s for s in range(S) for _ in range(p)]
+    w = [(head if s == S - 1 else 1.0) / p for s in stage]
+    load, hosts, rank = [0.0] * world, [set() for _ in range(world)], [0] * len(stage)
+    for pid in sorted(range(len(stage)), key=lambda i: -w[i]):
+        cand = [r for r in range(world) if stage[pid] not in hosts[r]] or list(range(world))
+        r = min(cand, key=lambda q: (load[q], q))
+        rank[pid] = r
+        load[r] += w[pid]
+        hosts[r].add(stage[pid])
+    desc = (f"{S} stages x {p} peers per stage on {world} GPUs, load-balanced placement (LM-head stage "
+            f"{head:.3f}x a block stage; max GPU load {max(load):.3f} stage visits per microbatch)")
+    return layout, rank, desc
+
+
 def measure_link(world, rank, nbytes=4 << 20, reps=20):
     """Stage-to-stage transport rate: rank 0 -> rank 1 NCCL send/recv of a
     wire-message-sized buffer (configs[2]: 4 MiB codes + scales), timed on the
@@ -586,7 +625,7 @@ def train_config(args, world: int) -> dict:
                         f"seq {m.seq_len}, {codec}, stochastic wiring + intra-stage all-reduce",
             "model": args.model, "global_batch": M * m.micro_batch, "micro_batch": m.micro_batch,
             "microbatches_per_step": M, "seq_len": m.seq_len, "tokens_per_step": M * m.tokens, "vocab": m.vocab,
-            "parallelism": placement_str(world, S),
+            "parallelism": engine_placement(args, world, S)[2],
             "l2": "per-step working set (weights + activations, GBs) far exceeds the 126 MB L2; no flush needed"}
 
 
@@ -750,14 +789,14 @@ def run_engine(args, world, rank, local, model: str, S: int, steps: int, warmup:
     margs = _ap.Namespace(model=model, micro_batch=getattr(args, "micro_batch", None) if model == args.model else None)
     mcfg = model_config(margs)
     M = args.microbatches
-    pl = Placement(world, S)
-    P = pl.P
+    layout, peer_rank, place_desc = engine_placement(args, world, S)
+    P = max(layout)
     bm = 2.0
     # tick period: M microbatch completions of the engine's own schedule (its virtual
     # completion rate for this layout, from a throwaway run without ticks), so every
     # stage takes one optimizer step per M microbatches
     horizon = 400.0 * M * (1.0 + bm) / P
-    cal = Engine(EngineConfig(n_stages=S, initial_peers=[[1.0] * pl.layout[s] for s in range(S)],
+    cal = Engine(EngineConfig(n_stages=S, initial_peers=[[1.0] * layout[s] for s in range(S)],
                               forward_service_seconds=1.0, backward_multiplier=bm,
                               trainers_per_peer=args.trainers_per_peer, duration_seconds=horizon,
                               bucket_seconds=horizon / 8), seed=1)
@@ -767,7 +806,7 @@ def run_engine(args, world, rank, local, model: str, S: int, steps: int, warmup:
     ex = EngineExecutor(mcfg, S, trainers_per_peer=args.trainers_per_peer, seed=1, lr=1e-4, forward_seconds=1.0,
                         backward_multiplier=bm, allreduce_period=period, allreduce_stall=0.05,
                         stream_per_peer=not args.single_stream, lanes=args.lanes, fp32=fp32,
-                        dpu=bool(getattr(args, "dpu", False)))
+                        dpu=bool(getattr(args, "dpu", False)), layout=layout, peer_rank=peer_rank)
     stream = torch.cuda.current_stream()
     # untimed warm-up: W steps plus two more (eight more with several peers per stage, whose
     # routes mix trainer pairs more), so that the visit graphs of most (peer, trainer pair, lane)
@@ -813,7 +852,7 @@ def run_engine(args, world, rank, local, model: str, S: int, steps: int, warmup:
                                 "+ AdamW at every AllReduceTick",
                    "arithmetic": "fp32 (SIMT fp32 GEMMs, fp32 activations)" if fp32 else
                                  "bf16 storage, tcgen05 GEMMs with fp32 accumulation",
-                   "placement": placement_str(world, S), "trainers": ex.T,
+                   "placement": place_desc, "peer_rank": peer_rank, "trainers": ex.T,
                    "trainers_per_peer": args.trainers_per_peer, "lanes_per_peer": args.lanes,
                    "schedule": "forward 1.0 / backward 2.0 virtual s, AllReduceTick every "
                                f"{period:.4g} virtual s (= {M} completions at the schedule's own rate: one optimizer "
@@ -1122,6 +1161,9 @@ def main():
     ap.add_argument("--dpu", action="store_true",
                     help="train: delayed parameter updates (PAPER:204): all-reduce + AdamW of step t overlap step t+1")
     ap.add_argument("--stages", type=int, default=TRAIN_STAGES, help="pipeline stages (default 4, SURVEY §8(d))")
+    ap.add_argument("--placement", default=None, choices=["balanced", "contiguous"],
+                    help="engine, several GPUs: peers per stage and their GPUs (bench.engine_placement; default "
+                         "balanced from 4 GPUs, contiguous below)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-codec", action="store_true", help="train: skip the codec sub-measurement")
     ap.add_argument("--no-extra", action="store_true", help="train: skip the configs[0] / configs[3] sub-lines")

@@ -588,6 +588,10 @@ typedef struct {
        update stream, overlapped with the next interval, whose visits use the other weight / gradient bank
        (swarm_stage_enable_banks): one optimizer step of delay */
     int dpu;
+    /* optional: the rank of each initial peer (peer ids in stage order, as `layout` / sim's
+       initial_peers give them); NULL = pid * world / n_initial.  Lets a caller balance the ranks'
+       loads, e.g. spread a heavier stage's peers over several GPUs next to lighter stages' peers. */
+    const int* peer_rank;
 } swarm_driver_config;
 typedef struct {
     uint64_t records, visits, ticks, optimizer_steps, completed, captures, kernels;

@@ -64,7 +64,7 @@ class DriverConfig(C.Structure):
                 ("allreduce_period", C.c_double), ("allreduce_stall", C.c_double), ("duration_seconds", C.c_double),
                 ("trainers_per_peer", C.c_int), ("seed", C.c_uint64), ("lanes", C.c_int), ("pair_wgrad", C.c_int),
                 ("use_graphs", C.c_int), ("stream_per_peer", C.c_int), ("n_pool", C.c_int), ("comm", C.c_void_p),
-                ("sim", C.c_void_p), ("dpu", C.c_int)]
+                ("sim", C.c_void_p), ("dpu", C.c_int), ("peer_rank", C.POINTER(C.c_int))]
 
 
 class DriverCounters(C.Structure):

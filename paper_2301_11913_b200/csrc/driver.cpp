@@ -185,7 +185,9 @@ struct swarm_driver {
 
     cudaStream_t lane_stream(const Peer& p) const { return prof ? prof_stream : p.lanes[p.cur]; }
 
+    std::vector<int> peer_rank0;  // optional explicit rank of each initial peer (swarm_driver_config.peer_rank)
     int rank_of_peer(int pid) const {
+        if (pid < n0 && !peer_rank0.empty()) return peer_rank0[pid];
         if (pid < n0) return static_cast<int>(static_cast<int64_t>(pid) * W / n0);
         return pid % W;
     }
@@ -945,6 +947,11 @@ struct swarm_driver {
             sim.worker_speed = nullptr;
         }
         n0 = static_cast<int>(wst.size());
+        if (c.peer_rank) {
+            peer_rank0.assign(c.peer_rank, c.peer_rank + n0);
+            for (int r : peer_rank0)
+                if (r < 0 || r >= W) return fail("driver: peer_rank entries must lie in [0, world)");
+        }
         sim.n_workers = wst.size();
         sim.worker_stage = wst.data();
         const int rc_e = swarm_engine_create_ex(&sim, c.seed, &engine);

@@ -465,7 +465,7 @@ class EngineExecutor:
                  duration_seconds: float = 1e9, use_graphs: bool = True, n_pool: int = 16,
                  tokens: torch.Tensor | None = None, targets: torch.Tensor | None = None, pair_wgrad: bool = True,
                  stream_per_peer: bool = True, lanes: int = 1, fp32: bool = False, sim: EngineConfig | None = None,
-                 dpu: bool = False):
+                 dpu: bool = False, layout: list | None = None, peer_rank: list | None = None):
         """sim: a full SimConfig (initial_peers with speeds, churn trace, rebalancing); it replaces
         the engine arguments and gives the layout (any layout on any world size)."""
         import ctypes as C
@@ -477,7 +477,10 @@ class EngineExecutor:
         self.world = dist.get_world_size() if dist.is_initialized() else 1
         self.rank = dist.get_rank() if dist.is_initialized() else 0
         self.device = torch.device("cuda", torch.cuda.current_device())
-        self.pl = Placement(self.world, n_stages) if sim is None else None
+        # layout: peers per stage (default: Placement's even split); peer_rank: each initial peer's
+        # rank (default: the driver's pid * world / n_peers) -- see bench.py's balanced placement
+        self.pl = Placement(self.world, n_stages) if sim is None and layout is None else None
+        self.layout = list(layout) if layout is not None else (self.pl.layout if self.pl else None)
         if lanes > 1 and not stream_per_peer:
             raise ValueError("lanes need a stream per peer")
         self.lib = L.lib()
@@ -510,6 +513,12 @@ class EngineExecutor:
         c.n_pool = n_pool if tokens is None else int(tokens.shape[0])
         c.comm = self.comm
         c.dpu = int(dpu)
+        if layout is not None:
+            self._layout_c = (C.c_int * n_stages)(*layout)
+            c.layout = self._layout_c
+        if peer_rank is not None:
+            self._peer_rank_c = (C.c_int * len(peer_rank))(*peer_rank)
+            c.peer_rank = self._peer_rank_c
         if sim is not None:
             self._sim_c = sim.to_c()
             c.sim = C.cast(C.pointer(self._sim_c), C.c_void_p)
@@ -524,7 +533,7 @@ class EngineExecutor:
         self.h = h
         self.lanes = lanes
         self.ecfg = sim or EngineConfig(
-            n_stages=n_stages, initial_peers=[[1.0] * self.pl.layout[s] for s in range(n_stages)],
+            n_stages=n_stages, initial_peers=[[1.0] * self.layout[s] for s in range(n_stages)],
             forward_service_seconds=forward_seconds, backward_multiplier=backward_multiplier,
             trainers_per_peer=trainers_per_peer, allreduce_period=allreduce_period, allreduce_stall=allreduce_stall,
             duration_seconds=duration_seconds, bucket_seconds=max(duration_seconds / 64, 1e-9))

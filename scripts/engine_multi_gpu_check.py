@@ -20,7 +20,21 @@ dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 S = int(sys.argv[1]) if len(sys.argv) > 1 else 4
 tpp = int(sys.argv[2]) if len(sys.argv) > 2 else 2
 lanes = int(sys.argv[3]) if len(sys.argv) > 3 else 1
-ex = EngineExecutor(PRESETS["tiny"], S, trainers_per_peer=tpp, seed=5, n_pool=5, lanes=lanes)
+# optional 4th argument "balanced": bench.py's load-balanced placement (several peers per stage,
+# spread over the GPUs next to other stages' peers)
+kw = {}
+if len(sys.argv) > 4 and sys.argv[4] == "balanced":
+    import argparse
+
+    import bench
+    layout, peer_rank, _ = bench.engine_placement(argparse.Namespace(model="tiny", micro_batch=None,
+                                                                     placement="balanced"), dist.get_world_size(), S)
+    kw = {"layout": layout, "peer_rank": peer_rank}
+elif len(sys.argv) > 4 and sys.argv[4] == "spread":
+    # every GPU hosts one peer of every stage (W peers per stage: W-rank stage communicators)
+    W = dist.get_world_size()
+    kw = {"layout": [W] * S, "peer_rank": [k for s in range(S) for k in range(W)]}
+ex = EngineExecutor(PRESETS["tiny"], S, trainers_per_peer=tpp, seed=5, n_pool=5, lanes=lanes, **kw)
 ex.run(9)
 ex.finish()
 torch.cuda.synchronize()
@@ -35,11 +49,15 @@ for pid, st in ex.stages.items():
     print(f"rank {dist.get_rank()} peer {pid} stage {s}: rel {r:.3e} visits {ex.visits_local}", flush=True)
 # with ticks: trains (finite loss)
 ex2 = EngineExecutor(PRESETS["tiny"], S, trainers_per_peer=tpp, seed=3, lr=3e-3, n_pool=2, allreduce_period=12.0,
-                     allreduce_stall=0.1, lanes=lanes)
+                     allreduce_stall=0.1, lanes=lanes, **kw)
 ex2.run(40)
 ex2.finish()
 torch.cuda.synchronize()
 print(f"rank {dist.get_rank()} ticks {ex2.ticks} steps {ex2.optimizer_steps} loss {ex2.loss_sum.item():.4f}", flush=True)
+if kw:  # (the Python orchestrator has no placement option: stop at the replay check)
+    dist.barrier()
+    dist.destroy_process_group()
+    sys.exit(0 if ok else 1)
 py2 = PyEngineExecutor(PRESETS["tiny"], S, trainers_per_peer=tpp, seed=3, lr=3e-3, allreduce_period=12.0,
                        allreduce_stall=0.1, lanes=lanes, tokens=ex2.pool_tok.cpu(), targets=ex2.pool_tgt.cpu())
 py2.run(40)
