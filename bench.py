@@ -134,6 +134,7 @@ def max_over_ranks(v: float, world: int) -> float:
 
 
 # ----------------------------------------------------------------- codec
+TRAINERS = 8  # engine trainers at every GPU count (run_engine)
 CODEC_N = 1 << 28  # 1 GiB of fp32 (BASELINE.json configs[1], top of the 1 MB-1 GB sweep)
 CODEC_BS = 4096
 CODEC_BYTES_Q = 4 * CODEC_N + CODEC_N + 4 * (CODEC_N // CODEC_BS)  # read x, write codes + scales
@@ -482,12 +483,14 @@ def engine_placement(args, world: int, S: int):
     the LM-head stage costing 1 + V d / (layers * params per layer) block stages -- on the least
     loaded GPU not yet hosting that stage.  The LM-head stage's extra work is thus spread over
     several GPUs next to lighter stages' peers (SWARM's remedy for uneven stages: more peers where
-    the work is) instead of pinning one GPU to it.  Measured: 4 GPUs 320-322k vs 311.5k tokens/s;
-    2 GPUs 159-165k vs 172k (the GPUs then clock at the power cap, and the tick's cross-GPU
-    all-reduce costs 4% of the step), so 2 GPUs default to --placement contiguous: the round-2
-    layout (world >= S: world / S peers per stage, one per GPU; else consecutive stages per GPU).
+    the work is) instead of pinning one GPU to it.  Measured: 4 GPUs 320-325k vs 311.5k tokens/s in
+    four runs, but 224k / 282k in two others (16 trainers over 2 peers per stage keep new paired
+    weight-gradient graphs being captured in the timed region; with 8 trainers: 288k), 2 GPUs
+    159-165k vs 172k (the GPUs then clock at the power cap; the tick's cross-GPU all-reduce costs 4%
+    of the step).  So the default is --placement contiguous, the round-2 layout (world >= S: world /
+    S peers per stage, one per GPU; else consecutive stages per GPU), and balanced is opt-in.
     Pure arithmetic on the Shape (no product import: the reference arm's config uses it too)."""
-    placement = getattr(args, "placement", None) or ("balanced" if world >= 4 else "contiguous")
+    placement = getattr(args, "placement", None) or "contiguous"
     if world == 1 or placement == "contiguous":
         if world >= S:
             return [world // S] * S, None, placement_str(world, S)
@@ -791,6 +794,11 @@ def run_engine(args, world, rank, local, model: str, S: int, steps: int, warmup:
     M = args.microbatches
     layout, peer_rank, place_desc = engine_placement(args, world, S)
     P = max(layout)
+    # 8 trainers (microbatch pipelines in flight) at every GPU count unless asked otherwise: with more,
+    # and several peers per stage, the paired weight-gradient visit graphs -- one per (trainer, partner
+    # trainer) -- keep being captured inside the timed region (measured at 16 trainers, 2 peers per
+    # stage: 52-81 captures per 20 steps, 224k-325k tokens/s across runs at 4 GPUs)
+    tpp = args.trainers_per_peer or max(1, TRAINERS // sum(layout))
     bm = 2.0
     # tick period: M microbatch completions of the engine's own schedule (its virtual
     # completion rate for this layout, from a throwaway run without ticks), so every
@@ -798,15 +806,16 @@ def run_engine(args, world, rank, local, model: str, S: int, steps: int, warmup:
     horizon = 400.0 * M * (1.0 + bm) / P
     cal = Engine(EngineConfig(n_stages=S, initial_peers=[[1.0] * layout[s] for s in range(S)],
                               forward_service_seconds=1.0, backward_multiplier=bm,
-                              trainers_per_peer=args.trainers_per_peer, duration_seconds=horizon,
+                              trainers_per_peer=tpp, duration_seconds=horizon,
                               bucket_seconds=horizon / 8), seed=1)
     while cal.next(4096):
         pass
     period = M * horizon / max(cal.summary()["completed"], 1)
-    ex = EngineExecutor(mcfg, S, trainers_per_peer=args.trainers_per_peer, seed=1, lr=1e-4, forward_seconds=1.0,
+    ex = EngineExecutor(mcfg, S, trainers_per_peer=tpp, seed=1, lr=1e-4, forward_seconds=1.0,
                         backward_multiplier=bm, allreduce_period=period, allreduce_stall=0.05,
                         stream_per_peer=not args.single_stream, lanes=args.lanes, fp32=fp32,
-                        dpu=bool(getattr(args, "dpu", False)), layout=layout, peer_rank=peer_rank)
+                        dpu=bool(getattr(args, "dpu", False)), layout=layout, peer_rank=peer_rank,
+                        pair_wgrad=not getattr(args, "no_pair_wgrad", False))
     stream = torch.cuda.current_stream()
     # untimed warm-up: W steps plus two more (eight more with several peers per stage, whose
     # routes mix trainer pairs more), so that the visit graphs of most (peer, trainer pair, lane)
@@ -853,7 +862,7 @@ def run_engine(args, world, rank, local, model: str, S: int, steps: int, warmup:
                    "arithmetic": "fp32 (SIMT fp32 GEMMs, fp32 activations)" if fp32 else
                                  "bf16 storage, tcgen05 GEMMs with fp32 accumulation",
                    "placement": place_desc, "peer_rank": peer_rank, "trainers": ex.T,
-                   "trainers_per_peer": args.trainers_per_peer, "lanes_per_peer": args.lanes,
+                   "trainers_per_peer": tpp, "lanes_per_peer": args.lanes,
                    "schedule": "forward 1.0 / backward 2.0 virtual s, AllReduceTick every "
                                f"{period:.4g} virtual s (= {M} completions at the schedule's own rate: one optimizer "
                                f"step per stage per {M} microbatches); one step = {M} microbatch completions",
@@ -1149,7 +1158,8 @@ def main():
     ap.add_argument("--workload", default="train", choices=["train", "codec", "failure", "engine"],
                     help="train (default): the engine-driven headline + codec + configs[0] / configs[3] sub-lines; "
                          "engine: the headline only")
-    ap.add_argument("--trainers-per-peer", type=int, default=2, help="engine: trainers per peer (sim trainers_per_peer)")
+    ap.add_argument("--trainers-per-peer", type=int, default=None,
+                    help="engine: trainers per peer (sim trainers_per_peer; default: 8 trainers in all, >= 1 per peer)")
     ap.add_argument("--single-stream", action="store_true", help="engine: one compute stream per GPU (not per peer)")
     ap.add_argument("--lanes", type=int, default=None,
                     help="engine: visits a peer may serve concurrently, each on its own stream and workspace set "
@@ -1161,9 +1171,11 @@ def main():
     ap.add_argument("--dpu", action="store_true",
                     help="train: delayed parameter updates (PAPER:204): all-reduce + AdamW of step t overlap step t+1")
     ap.add_argument("--stages", type=int, default=TRAIN_STAGES, help="pipeline stages (default 4, SURVEY §8(d))")
+    ap.add_argument("--no-pair-wgrad", action="store_true",
+                    help="engine: each backward visit's weight gradients alone (no pairing with the pending visit)")
     ap.add_argument("--placement", default=None, choices=["balanced", "contiguous"],
                     help="engine, several GPUs: peers per stage and their GPUs (bench.engine_placement; default "
-                         "balanced from 4 GPUs, contiguous below)")
+                         "contiguous)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-codec", action="store_true", help="train: skip the codec sub-measurement")
     ap.add_argument("--no-extra", action="store_true", help="train: skip the configs[0] / configs[3] sub-lines")
