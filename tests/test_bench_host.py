@@ -77,3 +77,48 @@ def test_reference_arm_runs_without_the_product_package():
     import bench
     ns = argparse.Namespace(model="tiny", stages=4, microbatches=32, micro_batch=None)
     assert j["config"] == bench.train_config(ns, 1)
+
+
+def test_engine_placement_layouts_and_trainers():
+    """bench.engine_placement: the contiguous default at every GPU count (8 trainers in all, >= 1 per
+    peer), and the opt-in balanced placement -- no GPU hosts two peers of one stage, the LM-head
+    stage's peers sit beside lighter stages' peers, and the max GPU load drops below contiguous."""
+    import argparse
+
+    import bench
+    C = argparse.Namespace(model="C", micro_batch=None, placement=None)
+    for w, lay in ((1, [1, 1, 1, 1]), (2, [1, 1, 1, 1]), (4, [1, 1, 1, 1]), (8, [2, 2, 2, 2])):
+        layout, peer_rank, desc = bench.engine_placement(C, w, 4)
+        assert layout == lay and peer_rank is None
+        assert sum(layout) * max(1, bench.TRAINERS // sum(layout)) == 8
+    B = argparse.Namespace(model="C", micro_batch=None, placement="balanced")
+    head = 1 + 50304 * 2048 / (8 * (4 * 2048 * 2048 + 2 * 2048 * 8192))
+    for w in (2, 4, 8):
+        layout, peer_rank, desc = bench.engine_placement(B, w, 4)
+        assert len(peer_rank) == sum(layout) and set(peer_rank) == set(range(w))
+        stage = [s for s in range(4) for _ in range(layout[s])]
+        hosted = {}
+        load = [0.0] * w
+        for pid, r in enumerate(peer_rank):
+            assert stage[pid] not in hosted.setdefault(r, set()), (w, pid, r)
+            hosted[r].add(stage[pid])
+            load[r] += (head if stage[pid] == 3 else 1.0) / layout[stage[pid]]
+        contiguous_max = head if w >= 4 else (1.0 + head) * (4 // w) / 2
+        assert max(load) < contiguous_max - 1e-9, (w, load)
+        assert "load-balanced" in desc
+
+
+def test_reference_arm_config_matches_the_gpu_arm():
+    """train_config (shared by both arms' JSON lines) depends on the placement description only through
+    bench.engine_placement, which is pure arithmetic on the Shape (no product import)."""
+    import argparse
+    import subprocess
+    import bench
+    for w in (1, 2, 4, 8):
+        a = argparse.Namespace(model="C", micro_batch=None, placement=None, stages=4, microbatches=32)
+        assert bench.train_config(a, w)["parallelism"] == bench.engine_placement(a, w, 4)[2]
+    r = subprocess.run([sys.executable, "-c", "import sys; sys.path.insert(0, %r); import bench, argparse; "
+                        "bench.engine_placement(argparse.Namespace(model='C', micro_batch=None, placement='balanced'),"
+                        " 8, 4); print('paper_2301_11913_b200' in sys.modules)" % ROOT],
+                       capture_output=True, text=True, timeout=120)
+    assert r.stdout.strip() == "False", r.stdout + r.stderr
