@@ -152,3 +152,25 @@ def test_engine_dpu_semantics(cuda):
         ex.finish()
         curve.append(ex.loss_sum.item() / max(n, 1) / ex.m.tokens)
     assert ex.optimizer_steps >= 4 and curve[-1] < curve[0] - 0.2, curve
+
+
+@pytest.mark.parametrize("layout", [[2, 1, 1, 2], [1, 3]])
+def test_executor_explicit_layout_and_peer_rank(cuda, layout):
+    """An explicit layout (several peers per stage on one GPU, whose gradients are summed locally) and
+    an explicit peer_rank (swarm_driver_config.peer_rank, all 0 on one GPU) drive the same engine: every
+    peer's gradient equals the sequential replay of the visits it ran."""
+    import torch
+    from paper_2301_11913_b200.executor import EngineExecutor, sequential_reference_grads
+    from paper_2301_11913_b200.swarm import PRESETS
+    S = len(layout)
+    ex = EngineExecutor(PRESETS["tiny"], S, trainers_per_peer=1, seed=7, n_pool=5, layout=layout,
+                        peer_rank=[0] * sum(layout))
+    assert ex.n_peers == sum(layout)
+    assert [ex.peer_info(p)["stage"] for p in range(ex.n_peers)] == [s for s in range(S) for _ in range(layout[s])]
+    assert ex.run(6) == 6
+    ex.finish()
+    torch.cuda.synchronize()
+    ex.flush_wgrad()
+    ref = sequential_reference_grads(ex)
+    for pid, st in ex.stages.items():
+        assert rel(st.grads(), ref[pid]) <= 1e-4, (pid, rel(st.grads(), ref[pid]))
