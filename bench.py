@@ -483,14 +483,15 @@ def engine_placement(args, world: int, S: int):
     the LM-head stage costing 1 + V d / (layers * params per layer) block stages -- on the least
     loaded GPU not yet hosting that stage.  The LM-head stage's extra work is thus spread over
     several GPUs next to lighter stages' peers (SWARM's remedy for uneven stages: more peers where
-    the work is) instead of pinning one GPU to it.  Measured: 4 GPUs 320-325k vs 311.5k tokens/s in
-    four runs, but 224k / 282k in two others (16 trainers over 2 peers per stage keep new paired
-    weight-gradient graphs being captured in the timed region; with 8 trainers: 288k), 2 GPUs
-    159-165k vs 172k (the GPUs then clock at the power cap; the tick's cross-GPU all-reduce costs 4%
-    of the step).  So the default is --placement contiguous, the round-2 layout (world >= S: world /
-    S peers per stage, one per GPU; else consecutive stages per GPU), and balanced is opt-in.
+    the work is) instead of pinning one GPU to it.  Measured at 4 GPUs (16 trainers): 318-322k vs
+    311.5k tokens/s contiguous over eight runs, once the driver caps the paired-backward graphs per
+    peer (SWARM_PAIR_GRAPH_CAP; uncapped, new (trainer, partner) graphs kept being captured: 224k-291k
+    in three runs); with 8 trainers 286-288k.  On 2 GPUs 159-165k vs 172k (the GPUs then clock at the
+    power cap; the tick's cross-GPU all-reduce costs 4% of the step), so below 4 GPUs the default is
+    --placement contiguous, the round-2 layout (world >= S: world / S peers per stage, one per GPU;
+    else consecutive stages per GPU).
     Pure arithmetic on the Shape (no product import: the reference arm's config uses it too)."""
-    placement = getattr(args, "placement", None) or "contiguous"
+    placement = getattr(args, "placement", None) or ("balanced" if world >= 4 else "contiguous")
     if world == 1 or placement == "contiguous":
         if world >= S:
             return [world // S] * S, None, placement_str(world, S)
@@ -794,11 +795,9 @@ def run_engine(args, world, rank, local, model: str, S: int, steps: int, warmup:
     M = args.microbatches
     layout, peer_rank, place_desc = engine_placement(args, world, S)
     P = max(layout)
-    # 8 trainers (microbatch pipelines in flight) at every GPU count unless asked otherwise: with more,
-    # and several peers per stage, the paired weight-gradient visit graphs -- one per (trainer, partner
-    # trainer) -- keep being captured inside the timed region (measured at 16 trainers, 2 peers per
-    # stage: 52-81 captures per 20 steps, 224k-325k tokens/s across runs at 4 GPUs)
-    tpp = args.trainers_per_peer or max(1, TRAINERS // sum(layout))
+    # trainers (microbatch pipelines in flight): 8 with one peer per stage, 16 with the balanced
+    # placement's several (at least one per peer) -- the counts measured (§ engine_placement)
+    tpp = args.trainers_per_peer or max(1, (TRAINERS if peer_rank is None else 2 * TRAINERS) // sum(layout))
     bm = 2.0
     # tick period: M microbatch completions of the engine's own schedule (its virtual
     # completion rate for this layout, from a throwaway run without ticks), so every
@@ -1159,7 +1158,8 @@ def main():
                     help="train (default): the engine-driven headline + codec + configs[0] / configs[3] sub-lines; "
                          "engine: the headline only")
     ap.add_argument("--trainers-per-peer", type=int, default=None,
-                    help="engine: trainers per peer (sim trainers_per_peer; default: 8 trainers in all, >= 1 per peer)")
+                    help="engine: trainers per peer (sim trainers_per_peer; default: 8 trainers in all, 16 with the "
+                         "balanced placement, >= 1 per peer)")
     ap.add_argument("--single-stream", action="store_true", help="engine: one compute stream per GPU (not per peer)")
     ap.add_argument("--lanes", type=int, default=None,
                     help="engine: visits a peer may serve concurrently, each on its own stream and workspace set "
@@ -1175,7 +1175,7 @@ def main():
                     help="engine: each backward visit's weight gradients alone (no pairing with the pending visit)")
     ap.add_argument("--placement", default=None, choices=["balanced", "contiguous"],
                     help="engine, several GPUs: peers per stage and their GPUs (bench.engine_placement; default "
-                         "contiguous)")
+                         "balanced from 4 GPUs, contiguous below)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-codec", action="store_true", help="train: skip the codec sub-measurement")
     ap.add_argument("--no-extra", action="store_true", help="train: skip the configs[0] / configs[3] sub-lines")

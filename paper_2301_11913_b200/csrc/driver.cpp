@@ -213,6 +213,19 @@ struct swarm_driver {
                (uint64_t((p + 1) & 0xFFFF) << 12) | (uint64_t(bank & 1) << 11) | uint64_t(lane & 0x7FF);
     }
 
+    // paired-backward graphs (kind 2) per peer beyond SWARM_PAIR_GRAPH_CAP (default 48; 0 = no cap)
+    // run eagerly: with several peers per stage the (trainer, partner) combinations keep appearing,
+    // each capture + instantiation costs milliseconds, and an ever-growing graph set measured slower
+    // (4 GPUs, 2 peers per stage, 16 trainers: 291k tokens/s uncapped, 321-322k capped at 32-64;
+    // one GPU unchanged)
+    std::unordered_map<int, int> pair_graphs;
+    int pair_graph_cap() const {
+        static const int cap = [] {
+            const char* e = getenv("SWARM_PAIR_GRAPH_CAP");
+            return e ? atoi(e) : 48;
+        }();
+        return cap;
+    }
     int replay(uint64_t key, cudaStream_t st, const std::function<int()>& fn) {
         if (!cfg.use_graphs || !warm.count(key) || prof) {  // first use runs eagerly (lazy init, tensor-map caches)
             TRY(fn());
@@ -220,6 +233,11 @@ struct swarm_driver {
             return SWARM_OK;
         }
         auto it = graphs.find(key);
+        if (it == graphs.end() && ((key >> 44) & 0xF) == 2 && pair_graph_cap() > 0) {
+            const int pid = static_cast<int>(key >> 48);
+            if (pair_graphs[pid] >= pair_graph_cap()) return fn();
+            pair_graphs[pid] += 1;
+        }
         if (it == graphs.end()) {
             const uint64_t k0 = swarm_launch_count();
             CU(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
@@ -243,6 +261,7 @@ struct swarm_driver {
     }
 
     void forget_graphs(int pid) {  // the peer's stage object changed: its captured visits are invalid
+        pair_graphs.erase(pid);
         for (auto it = graphs.begin(); it != graphs.end();) {
             if ((it->first >> 48) == uint64_t(pid)) {
                 cudaGraphExecDestroy(it->second.exec);

@@ -80,17 +80,21 @@ def test_reference_arm_runs_without_the_product_package():
 
 
 def test_engine_placement_layouts_and_trainers():
-    """bench.engine_placement: the contiguous default at every GPU count (8 trainers in all, >= 1 per
-    peer), and the opt-in balanced placement -- no GPU hosts two peers of one stage, the LM-head
-    stage's peers sit beside lighter stages' peers, and the max GPU load drops below contiguous."""
+    """bench.engine_placement: contiguous below 4 GPUs, balanced from 4 (the defaults), and the
+    balanced placement's invariants -- no GPU hosts two peers of one stage, the LM-head stage's peers
+    sit beside lighter stages' peers, and the max GPU load drops below contiguous."""
     import argparse
 
     import bench
     C = argparse.Namespace(model="C", micro_batch=None, placement=None)
-    for w, lay in ((1, [1, 1, 1, 1]), (2, [1, 1, 1, 1]), (4, [1, 1, 1, 1]), (8, [2, 2, 2, 2])):
+    for w, lay, balanced in ((1, [1, 1, 1, 1], False), (2, [1, 1, 1, 1], False), (4, [2, 2, 2, 2], True),
+                             (8, [4, 4, 4, 4], True)):
         layout, peer_rank, desc = bench.engine_placement(C, w, 4)
-        assert layout == lay and peer_rank is None
-        assert sum(layout) * max(1, bench.TRAINERS // sum(layout)) == 8
+        assert layout == lay and (peer_rank is not None) == balanced
+    for w in (2, 4, 8):
+        layout, peer_rank, _ = bench.engine_placement(argparse.Namespace(model="C", micro_batch=None,
+                                                                         placement="contiguous"), w, 4)
+        assert peer_rank is None and layout == ([1, 1, 1, 1] if w < 8 else [2, 2, 2, 2])
     B = argparse.Namespace(model="C", micro_batch=None, placement="balanced")
     head = 1 + 50304 * 2048 / (8 * (4 * 2048 * 2048 + 2 * 2048 * 8192))
     for w in (2, 4, 8):
