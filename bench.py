@@ -123,6 +123,20 @@ def barrier(world):
         dist.barrier()
 
 
+def warm_until_no_captures(ex, M: int, world: int, max_steps: int = 24) -> int:
+    """Untimed steps until a whole step captured no new visit graph on any rank (with several peers
+    per stage a paired backward's graph depends on its partner trainer, so a fixed warm-up can leave
+    captures -- milliseconds each -- inside the timed region; the driver's per-peer cap on those
+    graphs, SWARM_PAIR_GRAPH_CAP, bounds how many there can be).  Returns the steps run."""
+    for k in range(max_steps):
+        c0 = ex.captures
+        ex.run(M)
+        ex.finish()
+        if max_over_ranks(float(ex.captures - c0), world) == 0.0:
+            return k + 1
+    return max_steps
+
+
 def max_over_ranks(v: float, world: int) -> float:
     if world == 1:
         return v
@@ -821,6 +835,7 @@ def run_engine(args, world, rank, local, model: str, S: int, steps: int, warmup:
     # combinations are captured before the timed region
     ex.run(M * (warmup + (8 if P > 1 else 2)))
     ex.finish()
+    warm_until_no_captures(ex, M, world)
     torch.cuda.synchronize()
     ex.loss_sum.zero_()
     clk = ClockSampler(local)
@@ -887,6 +902,7 @@ def run_engine(args, world, rank, local, model: str, S: int, steps: int, warmup:
         lst = ex.last_stage_stream()
         ex.run(M)  # untimed: warm the host-pool path
         ex.finish()
+        warm_until_no_captures(ex, M, world)
         barrier(world)
         torch.cuda.synchronize()
         w0 = time.perf_counter()
