@@ -286,7 +286,8 @@ template <int BN_TILE>
 __device__ __forceinline__ void drain_tile(const Params& p, const CUtensorMap* md, const CUtensorMap* mu,
                                            uint8_t* stg, int& slot_idx, uint32_t taddr, int row_base, long long rd,
                                            long long cd, int col_tile0, int lane, uint64_t fix_slots = 0,
-                                           int nfix = 0, size_t fix_row = 0) {
+                                           int nfix = 0, size_t fix_row = 0, int c_begin = 0,
+                                           int c_end = BN_TILE / 32, int nslots = 2) {
     const int row = row_base + lane;
     // epilogues that read a bf16 operand (R, U): this chunk's 64 B of it are requested before the
     // TMEM load, and the next chunk's are pulled into L2, so the global latency overlaps the
@@ -295,7 +296,7 @@ __device__ __forceinline__ void drain_tile(const Params& p, const CUtensorMap* m
                            (p.epi == SWARM_EPI_RESIDUAL || p.epi == SWARM_EPI_DGELU || p.epi == SWARM_EPI_MUL);
     const bool pre = reads_aux && p.aux_prefetch;
 #pragma unroll 1
-    for (int c = 0; c < BN_TILE / 32; ++c) {
+    for (int c = c_begin; c < c_end; ++c) {
         const int col0 = col_tile0 + c * 32;
         uint4 a4[4];
         if (pre && row < p.m && col0 < p.n) {
@@ -337,9 +338,12 @@ __device__ __forceinline__ void drain_tile(const Params& p, const CUtensorMap* m
             if (row < p.m) epilogue_chunk(p, v, off, min(32, p.n - col0));
             continue;
         }
-        uint8_t* slot = stg + slot_idx * kEpiSlot;
+        uint8_t* slot = stg + (nslots == 2 ? slot_idx : 0) * kEpiSlot;
         slot_idx ^= 1;
-        if (lane == 0) bulk_wait_read<1>();  // the store issued from this slot two chunks ago has read it
+        if (lane == 0) {  // the store issued from this slot (two chunks ago; one with a single slot) has read it
+            if (nslots == 2) bulk_wait_read<1>();
+            else bulk_wait_read<0>();
+        }
         __syncwarp();
         const bool row_ok = row < p.m;
         const int gc = static_cast<int>(cd) + col0, gr = static_cast<int>(rd) + row_base;
@@ -650,8 +654,10 @@ struct Cfg2 {
     static_assert(2 * STAGES * 8 + 4 * 8 + 4 <= 256, "barrier area overflow");
 };
 
-template <bool A_MN, bool B_MN, int NPAIR>
-__global__ void __launch_bounds__(kThreads, 1)
+// EPI8: eight epilogue warps (2-9, two per TMEM lane quarter, each group half of a tile's columns,
+// one staging slot each) instead of four (4-7): the fused epilogues' arithmetic is halved per warp
+template <bool A_MN, bool B_MN, int NPAIR, bool EPI8 = false>
+__global__ void __launch_bounds__(EPI8 ? 320 : kThreads, 1)
     k_gemm2(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUtensorMap tma_b,
             const __grid_constant__ CUtensorMap tma_d, const __grid_constant__ CUtensorMap tma_u,
             const __grid_constant__ CUtensorMap tma_a2, const __grid_constant__ CUtensorMap tma_b2, const Params p) {
@@ -694,7 +700,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         for (int s = 0; s < 2; ++s) {
             mbar_init(&tfull[s], 1);
-            mbar_init(&tempty[s], 8);  // 4 epilogue warps x 2 CTAs (only the leader's is used)
+            mbar_init(&tempty[s], EPI8 ? 16 : 8);  // epilogue warps x 2 CTAs (only the leader's is used)
         }
         fence_barrier_init();
     }
@@ -815,11 +821,12 @@ __global__ void __launch_bounds__(kThreads, 1)
                 if (acc == 0) acc_phase ^= 1;
             }
         }
-    } else if (warp >= 4) {
+    } else if (EPI8 ? warp >= 2 : warp >= 4) {
         // ------------------------------------------------ epilogue (both CTAs, own 128 rows)
-        const int q = warp - 4;
+        const int q = warp & 3;
+        const int grp = EPI8 ? (warp - 2) >> 2 : 0;  // EPI8: column half of the tile
         const uint32_t tempty_leader[2] = {map_to_cta(&tempty[0], rank & ~1u), map_to_cta(&tempty[1], rank & ~1u)};
-        uint8_t* stg = stg_all + q * 2 * kEpiSlot;
+        uint8_t* stg = stg_all + (EPI8 ? (warp - 2) : 2 * q) * kEpiSlot;
         int slot_idx = 0;
         int acc = 0;
         uint32_t acc_phase = 0;
@@ -839,7 +846,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             int nfix = 0;
             const size_t fix_row = static_cast<size_t>(half * 128 + q * 32) * PAIR_BN;
             bool drain = true;
-            if (u.sk >= 0 && (u.kb0 != 0 || u.kb1 != p.k_blocks) && !(p.dbg & 8)) {
+            if (!EPI8 && u.sk >= 0 && (u.kb0 != 0 || u.kb1 != p.k_blocks) && !(p.dbg & 8)) {
                 // stream-K partial tile: the last of its clusters to arrive (per warp
                 // quarter) sums everyone's partials and runs the epilogue; the others
                 // park their fp32 partial in the workspace.  Nobody waits on a
@@ -888,7 +895,9 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
             if (drain)
                 drain_tile<PAIR_BN>(p, &tma_d, &tma_u, stg, slot_idx, taddr, mt * 256 + half * 128 + q * 32, rd, cd,
-                                    (nt * NPAIR + pair) * PAIR_BN, lane, fix_slots, nfix, fix_row);
+                                    (nt * NPAIR + pair) * PAIR_BN, lane, fix_slots, nfix, fix_row,
+                                    EPI8 ? grp * (PAIR_BN / 64) : 0, EPI8 ? (grp + 1) * (PAIR_BN / 64) : PAIR_BN / 32,
+                                    EPI8 ? 1 : 2);
             __syncwarp();
             if (lane == 0)
                 for (int f = 0; f < nfix; ++f)
@@ -1074,10 +1083,31 @@ int launch(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& td, 
     return SWARM_OK;
 }
 
+bool epi8_enabled() {
+    static const bool on = [] {
+        const char* e = getenv("SWARM_GEMM_EPI8");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
+
+template <bool A_MN, bool B_MN, int NPAIR, bool EPI8>
+int launch_pair_k(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& td, const CUtensorMap& tu,
+                  const CUtensorMap& ta2, const CUtensorMap& tb2, const Params& p, int clusters, cudaStream_t st);
+
 template <bool A_MN, bool B_MN, int NPAIR>
 int launch_pair(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& td, const CUtensorMap& tu,
                 const CUtensorMap& ta2, const CUtensorMap& tb2, const Params& p, int clusters, cudaStream_t st) {
-    auto kern = k_gemm2<A_MN, B_MN, NPAIR>;
+    // eight epilogue warps unless stream-K partial tiles are in play (their fix-up is per warp quarter)
+    if (epi8_enabled() && p.sk_tiles == 0)
+        return launch_pair_k<A_MN, B_MN, NPAIR, true>(ta, tb, td, tu, ta2, tb2, p, clusters, st);
+    return launch_pair_k<A_MN, B_MN, NPAIR, false>(ta, tb, td, tu, ta2, tb2, p, clusters, st);
+}
+
+template <bool A_MN, bool B_MN, int NPAIR, bool EPI8>
+int launch_pair_k(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& td, const CUtensorMap& tu,
+                  const CUtensorMap& ta2, const CUtensorMap& tb2, const Params& p, int clusters, cudaStream_t st) {
+    auto kern = k_gemm2<A_MN, B_MN, NPAIR, EPI8>;
     static bool attr = false;
     if (!attr) {
         SWARM_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg2::SMEM));
@@ -1085,7 +1115,7 @@ int launch_pair(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap&
     }
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(2 * NPAIR * clusters);
-    cfg.blockDim = dim3(kThreads);
+    cfg.blockDim = dim3(EPI8 ? 320 : kThreads);
     cfg.dynamicSmemBytes = Cfg2::SMEM;
     cfg.stream = st;
     cudaLaunchAttribute attrs[2];
