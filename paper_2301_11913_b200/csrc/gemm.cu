@@ -1083,12 +1083,21 @@ int launch(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& td, 
     return SWARM_OK;
 }
 
-bool epi8_enabled() {
-    static const bool on = [] {
+// SWARM_GEMM_EPI8: 0 = four epilogue warps, 1 = eight, 2 (default) = eight for bf16 outputs only
+// (an fp32 chunk fills a warp's whole staging slot, so with eight warps and one slot each
+// the reduce-add / store of chunk c must finish reading before chunk c+1 is staged:
+// fp32 outputs measured 2.5-3.5% faster with four double-buffered warps, scripts/ffn_epi_probe.py)
+int epi8_mode() {
+    static const int m = [] {
         const char* e = getenv("SWARM_GEMM_EPI8");
-        return !(e && e[0] == '0');
+        return e ? atoi(e) : 2;
     }();
-    return on;
+    return m;
+}
+bool epi8_for(int epi) {
+    const int m = epi8_mode();
+    if (m == 0) return false;
+    return m != 2 || (epi != SWARM_EPI_STORE_F32 && epi != SWARM_EPI_ACCUM_F32);
 }
 
 template <bool A_MN, bool B_MN, int NPAIR, bool EPI8>
@@ -1099,7 +1108,7 @@ template <bool A_MN, bool B_MN, int NPAIR>
 int launch_pair(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& td, const CUtensorMap& tu,
                 const CUtensorMap& ta2, const CUtensorMap& tb2, const Params& p, int clusters, cudaStream_t st) {
     // eight epilogue warps unless stream-K partial tiles are in play (their fix-up is per warp quarter)
-    if (epi8_enabled() && p.sk_tiles == 0)
+    if (epi8_for(p.epi) && p.sk_tiles == 0)
         return launch_pair_k<A_MN, B_MN, NPAIR, true>(ta, tb, td, tu, ta2, tb2, p, clusters, st);
     return launch_pair_k<A_MN, B_MN, NPAIR, false>(ta, tb, td, tu, ta2, tb2, p, clusters, st);
 }

@@ -231,11 +231,11 @@ print("ok")
 
 @pytest.mark.parametrize("env", [{"SWARM_GEMM_MCAST": "0"}, {"SWARM_GEMM_PAIR": "0"},
                                  {"SWARM_GEMM_TMA_EPI": "0"}, {"SWARM_PDL": "1"}, {"SWARM_GEMM_STREAMK": "1"},
-                                 {"SWARM_GEMM_STREAMK": "0"}, {"SWARM_GEMM_EPI8": "0"}])
+                                 {"SWARM_GEMM_STREAMK": "0"}, {"SWARM_GEMM_EPI8": "0"}, {"SWARM_GEMM_EPI8": "1"}])
 def test_gemm_kernel_variants(cuda, env):
     """The non-default kernel variants (2-CTA pairs without multicast, 1-CTA
     tiles, direct-store epilogue, programmatic dependent launch on, stream-K
-    forced on / off, the four-warp pair epilogue) stay correct; the selection is read once per process,
+    forced on / off, the four-warp pair epilogue, eight warps for fp32 outputs too) stay correct; the selection is read once per process,
     hence a subprocess per variant."""
     import os
     import subprocess
