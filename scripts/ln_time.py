@@ -17,10 +17,13 @@ ws = torch.zeros(L.lib().swarm_layer_norm_backward_workspace(rows, cols), dtype=
 lib = L.lib()
 def fwd(st):
     lib.swarm_layer_norm_forward(_ptr(x), _DT[x.dtype], rows, cols, _ptr(g), _ptr(b), 1e-5, _ptr(y), _ptr(mu), _ptr(rs), st)
+def fwd_nogb(st):  # gain / bias omitted (1, 0): no per-row parameter loads
+    lib.swarm_layer_norm_forward(_ptr(x), _DT[x.dtype], rows, cols, None, None, 1e-5, _ptr(y), _ptr(mu), _ptr(rs), st)
 def bwd(st):
     lib.swarm_layer_norm_backward(_ptr(dy), _ptr(x), _DT[x.dtype], rows, cols, _ptr(g), _ptr(mu), _ptr(rs), _ptr(dres),
                                   _ptr(dx), _ptr(dg), _ptr(db), 1, _ptr(ws), st)
-for name, fn, nbytes in (("fwd", fwd, 4 * rows * cols), ("bwd", bwd, 8 * rows * cols)):
+for name, fn, nbytes in (("fwd", fwd, 4 * rows * cols), ("fwd no gain/bias", fwd_nogb, 4 * rows * cols),
+                         ("bwd", bwd, 8 * rows * cols)):
     s = torch.cuda.Stream()
     with torch.cuda.stream(s):
         fn(s.cuda_stream)
