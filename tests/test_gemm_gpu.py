@@ -299,3 +299,36 @@ def test_gemm_gelu_deriv_and_mul_epilogues(cuda, m, n, k):
     torch.testing.assert_close(u.float(), x.grad, rtol=1e-2, atol=2e-2)
     out = ops.gemm(a, b, epilogue=L.EPI_MUL, aux=u)
     torch.testing.assert_close(out.float(), ref * u.float(), rtol=1e-2, atol=5e-2)
+
+
+@pytest.mark.parametrize("m,n,k,b_t", [(2048, 2048, 2048, False), (2048, 2000, 1024, False), (1024, 3072, 512, True)])
+def test_gemm_bf16_epilogues_pair_shapes(cuda, m, n, k, b_t):
+    """Every bf16-output epilogue at shapes the 2-CTA pair kernel takes (its eight-warp
+    epilogue: two warps per TMEM lane quarter, each draining half of a tile's columns),
+    including the o-projection's 2048^3 (one tile per cluster), a ragged N whose last
+    tile ends inside a 32-column chunk of the second warp group, and an MN-major B."""
+    import torch
+    from paper_2301_11913_b200 import _lib as L, ops
+    torch.manual_seed(m + n + k)
+    a = torch.randn(m, k, device="cuda").bfloat16() * 0.25
+    b = (torch.randn(k, n, device="cuda") if b_t else torch.randn(n, k, device="cuda")).bfloat16() * 0.25
+    ref = a.float() @ (b.float() if b_t else b.float().t())
+    tol = dict(rtol=1e-2, atol=3e-2)
+    out = ops.gemm(a, b, b_t=b_t)
+    torch.testing.assert_close(out.float(), ref, **tol)
+    r = torch.randn(m, n, device="cuda").bfloat16()
+    out = ops.gemm(a, b, b_t=b_t, epilogue=L.EPI_RESIDUAL, aux=r)
+    torch.testing.assert_close(out.float(), ref + r.float(), **tol)
+    u = torch.empty(m, n, device="cuda", dtype=torch.bfloat16)
+    out = ops.gemm(a, b, b_t=b_t, epilogue=L.EPI_GELU, aux=u)
+    torch.testing.assert_close(u.float(), ref, **tol)
+    torch.testing.assert_close(out.float(), torch.nn.functional.gelu(ref, approximate="tanh"), **tol)
+    x = ref.clone().requires_grad_()
+    torch.nn.functional.gelu(x, approximate="tanh").backward(torch.ones_like(x))
+    out = ops.gemm(a, b, b_t=b_t, epilogue=L.EPI_DGELU, aux=u)
+    torch.testing.assert_close(out.float(), ref * x.grad, rtol=2e-2, atol=5e-2)
+    g = ops.gemm(a, b, b_t=b_t, epilogue=L.EPI_GELU_DERIV, aux=u)
+    torch.testing.assert_close(g.float(), torch.nn.functional.gelu(ref, approximate="tanh"), **tol)
+    torch.testing.assert_close(u.float(), x.grad, **tol)
+    out = ops.gemm(a, b, b_t=b_t, epilogue=L.EPI_MUL, aux=u)
+    torch.testing.assert_close(out.float(), ref * u.float(), rtol=1e-2, atol=5e-2)
