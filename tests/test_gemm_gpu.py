@@ -332,3 +332,34 @@ def test_gemm_bf16_epilogues_pair_shapes(cuda, m, n, k, b_t):
     torch.testing.assert_close(u.float(), x.grad, **tol)
     out = ops.gemm(a, b, b_t=b_t, epilogue=L.EPI_MUL, aux=u)
     torch.testing.assert_close(out.float(), ref * u.float(), rtol=1e-2, atol=5e-2)
+
+
+@pytest.mark.parametrize("m,n,k", [(2048, 2048, 2048), (2048, 2000, 512)])
+def test_gemm_pair_epilogues_repeatable(cuda, m, n, k):
+    """Race check of the pair kernel's epilogues (staging slots reused under TMA stores /
+    reduce-adds, eight bf16 warps, four fp32 warps): each epilogue's output is a fixed
+    function of the inputs, so 200 launches (pairs back to back) must agree bit for bit."""
+    import torch
+    from paper_2301_11913_b200 import _lib as L, ops
+    torch.manual_seed(m + n)
+    a = torch.randn(m, k, device="cuda").bfloat16()
+    b = torch.randn(n, k, device="cuda").bfloat16()
+    r = torch.randn(m, n, device="cuda").bfloat16()
+    for epi in (L.EPI_STORE_BF16, L.EPI_RESIDUAL, L.EPI_GELU_DERIV, L.EPI_STORE_F32, L.EPI_ACCUM_F32):
+        f32 = epi in (L.EPI_STORE_F32, L.EPI_ACCUM_F32)
+        outs = [torch.zeros(m, n, device="cuda", dtype=torch.float32 if f32 else torch.bfloat16) for _ in range(2)]
+        auxs = [torch.empty(m, n, device="cuda", dtype=torch.bfloat16) for _ in range(2)]
+        aux_of = lambda u: r if epi == L.EPI_RESIDUAL else (u if epi == L.EPI_GELU_DERIV else None)
+        ops.gemm(a, b, epilogue=epi, aux=aux_of(auxs[0]), out=outs[0])
+        torch.cuda.synchronize()
+        first = (outs[0].clone(), auxs[0].clone())
+        for it in range(100):  # two launches back to back per check
+            for o, u in zip(outs, auxs):
+                if epi == L.EPI_ACCUM_F32:
+                    o.zero_()
+                ops.gemm(a, b, epilogue=epi, aux=aux_of(u), out=o)
+            torch.cuda.synchronize()
+            for o, u in zip(outs, auxs):
+                assert torch.equal(o, first[0]), (epi, it)
+                if epi == L.EPI_GELU_DERIV:
+                    assert torch.equal(u, first[1]), (epi, it)
