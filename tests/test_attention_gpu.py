@@ -257,3 +257,43 @@ def test_attention_lse_forward_and_recompute_backward(cuda, B, H, L, causal):
     torch.cuda.synchronize()
     for got, ref in zip(dqkv.float().split(d, 1), dqkv_p.float().split(d, 1)):
         assert float((got - ref).norm() / ref.norm()) < 1e-2
+
+
+def test_attention_lse_paths_repeatable(cuda):
+    """Race check of the default attention kernels at the configs[2] shape (B 4, H 16, L 512):
+    the one-pass forward's O and lse, and the recomputing backward's dK / dV (each owned by one
+    CTA), must be bit-identical over 50 back-to-back launch pairs; dQ (fp32 reduce-add over key
+    blocks, order not fixed) must stay within fp32 reordering of the first result."""
+    import torch
+    from paper_2301_11913_b200 import _lib
+    B, H, L, dh, causal = 4, 16, 512, 128, 1
+    torch.manual_seed(3)
+    d = H * dh
+    qkv = (torch.randn(B * L, 3 * d, device="cuda") * 2).bfloat16()
+    dO = torch.randn(B * L, d, device="cuda").bfloat16()
+    scale = 1 / math.sqrt(dh)
+    st = torch.cuda.current_stream().cuda_stream
+    L_ = _lib.lib()
+    ptr = lambda t: C.c_void_p(t.data_ptr())  # noqa: E731
+    ws = torch.zeros(L_.swarm_attn_backward_workspace(B, H, L, dh), device="cuda", dtype=torch.uint8)
+
+    def run():
+        O = torch.empty(B * L, d, device="cuda", dtype=torch.bfloat16)
+        lse = torch.empty(B * H * L, device="cuda")
+        dqkv = torch.empty(B * L, 3 * d, device="cuda", dtype=torch.bfloat16)
+        assert L_.swarm_attn_forward_lse(ptr(qkv), ptr(qkv[:, d:]), ptr(qkv[:, 2 * d:]), 3 * d, d, B, H, L, dh, scale,
+                                         causal, ptr(lse), ptr(O), d, st) == 0
+        assert L_.swarm_attn_backward_lse(ptr(dO), d, ptr(qkv), 3 * d, 3 * d, d, 2 * d, ptr(O), d, ptr(lse), B, H, L,
+                                          dh, scale, causal, ptr(dqkv), 3 * d, d, 2 * d, ptr(ws), st) == 0
+        return O, lse, dqkv
+
+    O0, lse0, dqkv0 = run()
+    torch.cuda.synchronize()
+    for it in range(50):
+        outs = [run(), run()]
+        torch.cuda.synchronize()
+        for O, lse, dqkv in outs:
+            assert torch.equal(O, O0) and torch.equal(lse, lse0), it
+            assert torch.equal(dqkv[:, d:], dqkv0[:, d:]), it  # dK, dV
+            dq, dq0 = dqkv[:, :d].float(), dqkv0[:, :d].float()
+            assert float((dq - dq0).norm() / dq0.norm()) < 1e-2, it
