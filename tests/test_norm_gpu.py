@@ -120,3 +120,37 @@ def test_layer_norm_backward_split_parts(cuda):
     assert torch.equal(dx, dx_full)
     torch.testing.assert_close(dg, dg_full + 1, rtol=0, atol=1e-5 * float(dg_full.abs().max()))
     torch.testing.assert_close(db, db_full + 1, rtol=0, atol=1e-5 * float(db_full.abs().max()))
+
+
+def test_layer_norm_backward_repeatable_with_reused_workspace(cuda):
+    """The dgain / dbias pass's per-strip arrival counters reset themselves for the next launch:
+    100 back-to-back launches on ONE workspace (as the executor runs them) give bit-identical
+    dx, dgain and dbias (the last CTA of a strip sums the split partials in a fixed order)."""
+    import torch
+    from paper_2301_11913_b200 import _lib as L, ops
+    from paper_2301_11913_b200.ops import _ptr, _DT
+    rows, cols = 2048, 2048
+    torch.manual_seed(5)
+    x = torch.randn(rows, cols, device="cuda").bfloat16()
+    g = torch.rand(cols, device="cuda") + 0.5
+    _, mean, rstd = ops.layer_norm(x, g, torch.zeros(cols, device="cuda"))
+    dy = torch.randn(rows, cols, device="cuda").bfloat16()
+    lib = L.lib()
+    ws = torch.zeros(lib.swarm_layer_norm_backward_workspace(rows, cols), dtype=torch.uint8, device="cuda")
+    st = torch.cuda.current_stream().cuda_stream
+
+    def run():
+        dx = torch.empty_like(x)
+        dg = torch.empty(cols, device="cuda")
+        db = torch.empty(cols, device="cuda")
+        assert lib.swarm_layer_norm_backward(_ptr(dy), _ptr(x), _DT[x.dtype], rows, cols, _ptr(g), _ptr(mean),
+                                             _ptr(rstd), None, _ptr(dx), _ptr(dg), _ptr(db), 0, _ptr(ws), st) == 0
+        return dx, dg, db
+
+    first = run()
+    torch.cuda.synchronize()
+    for it in range(50):
+        outs = [run(), run()]
+        torch.cuda.synchronize()
+        for o in outs:
+            assert all(torch.equal(a, b) for a, b in zip(o, first)), it
